@@ -1,0 +1,355 @@
+"""Sparse symmetric matrices, BASELINE problem generators and Matrix Market I/O.
+
+``SparseSymMatrix`` keeps the reference's constructor and invariants
+(`/root/reference/pkg/src/spdkit/sparse.py:24-90`: CSR with both triangles,
+strictly increasing columns, exact value symmetry, positive diagonal).  The
+host arrays are the *input format*; every product of the matrix with a vector
+(``matvec``/``@``) runs on the B200 through the C-ABI SpMV kernel
+(``spand_csr_spmv``), with a device copy (int32 indices) uploaded lazily and
+cached.  There is no host SpMV.
+
+Generators:
+- ``laplacian_2d`` reproduces the reference generator bit for bit
+  (`sparse.py:181-196`; pinned by ``tests/golden``);
+- ``laplacian_3d``, ``diffusion_fv`` and ``log_uniform_block_field`` build the
+  BASELINE.json configs C2-C4 that the reference has no generator for
+  (SURVEY.md §0, §8d): 7-point/5-point finite volumes, harmonic-mean face
+  coefficients, Dirichlet boundary faces adding the cell's own coefficient
+  (the reference's convention, `sparse.py:278-282`), so a constant field
+  reduces exactly to the Laplacian.
+- ``baseline_problem(name)`` returns (A, b, levels) for C1-C4 with the seeding
+  convention "field first, then b = rng.standard_normal(n)".
+"""
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from .errors import (
+    AsymmetricValues,
+    DimensionMismatch,
+    NonpositiveDiagonal,
+    NotSymmetricReal,
+    ParseError,
+)
+
+
+@dataclass(frozen=True)
+class SparseSymMatrix:
+    """Symmetric CSR matrix, both triangles stored (reference `sparse.py:24`)."""
+
+    n: int
+    row_ptr: np.ndarray
+    col_idx: np.ndarray
+    values: np.ndarray
+    _dev: dict = field(repr=False, compare=False, default=None)
+
+    def __post_init__(self):
+        n = int(self.n)
+        rp = np.asarray(self.row_ptr, dtype=np.int64)
+        ci = np.asarray(self.col_idx, dtype=np.int64)
+        va = np.asarray(self.values, dtype=np.float64)
+        if rp.shape != (n + 1,):
+            raise DimensionMismatch("row_ptr must have length n+1")
+        counts = np.diff(rp)
+        if np.any(counts < 1):
+            raise NonpositiveDiagonal("every row needs its diagonal entry")
+        if rp[0] != 0 or rp[-1] != ci.size or ci.size != va.size:
+            raise DimensionMismatch("row_ptr, col_idx and values disagree")
+        if ci.size and (ci.min() < 0 or ci.max() >= n):
+            raise ParseError("column index out of range")
+        rows = np.repeat(np.arange(n, dtype=np.int64), counts)
+        same_row = rows[1:] == rows[:-1]
+        if np.any(np.diff(ci)[same_row] <= 0):
+            raise ParseError("column indices must be strictly increasing per row")
+        # exact symmetry of pattern and values: sort the transpose's
+        # triplets into row-major order and compare elementwise
+        key_t = ci * n + rows
+        order = np.argsort(key_t, kind="stable")
+        if not (np.array_equal(ci[order], rows) and
+                np.array_equal(rows[order], ci) and
+                np.array_equal(va[order], va)):
+            raise AsymmetricValues("stored pattern or values are not symmetric")
+        diag_pos = np.flatnonzero(rows == ci)
+        if diag_pos.size != n or np.any(va[diag_pos] <= 0.0):
+            raise NonpositiveDiagonal("diagonal entries must be strictly positive")
+        object.__setattr__(self, "n", n)
+        object.__setattr__(self, "row_ptr", rp)
+        object.__setattr__(self, "col_idx", ci)
+        object.__setattr__(self, "values", va)
+        object.__setattr__(self, "_dev", {})
+
+    @property
+    def nnz(self):
+        return int(self.values.size)
+
+    def diagonal(self):
+        rows = np.repeat(np.arange(self.n), np.diff(self.row_ptr))
+        d = np.zeros(self.n)
+        m = rows == self.col_idx
+        d[rows[m]] = self.values[m]
+        return d
+
+    def toarray(self):
+        rows = np.repeat(np.arange(self.n), np.diff(self.row_ptr))
+        out = np.zeros((self.n, self.n))
+        out[rows, self.col_idx] = self.values
+        return out
+
+    def to_scipy(self):
+        import scipy.sparse as sp
+        return sp.csr_matrix((self.values, self.col_idx, self.row_ptr),
+                             shape=(self.n, self.n))
+
+    # -- device side -----------------------------------------------------
+    def device(self, perm=None):
+        """Device CSR (int32 indices, fp64 values), optionally symmetrically
+        permuted so that new index ``i`` is old index ``perm[i]``."""
+        from .device import DeviceCSR
+        key = None if perm is None else id(perm)
+        cached = self._dev.get(key)
+        if cached is not None and (perm is None or cached[0] is perm):
+            return cached[1]
+        dev = DeviceCSR.from_host(self, perm)
+        self._dev[key] = (perm, dev)
+        return dev
+
+    def matvec(self, x):
+        """y = A x on the B200 (numpy in -> numpy out, torch in -> torch out)."""
+        from .device import as_device_vector, like_input
+        xd, kind = as_device_vector(x, self.n)
+        y = self.device().spmv(xd)
+        return like_input(y, kind)
+
+    def __matmul__(self, x):
+        return self.matvec(x)
+
+
+def from_coo(n, rows, cols, vals):
+    """SparseSymMatrix from COO triplets covering both triangles."""
+    rows = np.asarray(rows, dtype=np.int64)
+    cols = np.asarray(cols, dtype=np.int64)
+    vals = np.asarray(vals, dtype=np.float64)
+    order = np.lexsort((cols, rows))
+    rows, cols, vals = rows[order], cols[order], vals[order]
+    row_ptr = np.zeros(n + 1, dtype=np.int64)
+    np.cumsum(np.bincount(rows, minlength=n), out=row_ptr[1:])
+    return SparseSymMatrix(n, row_ptr, cols, vals)
+
+
+# ---------------------------------------------------------------------------
+# Matrix Market (input side, reference `sparse.py:98-173`)
+
+
+def read_matrix_market(path):
+    """Read a `matrix coordinate real symmetric` file (one triangle stored)."""
+    with open(path, "r") as fh:
+        header = fh.readline().strip()
+        tok = header.split()
+        if len(tok) != 5 or tok[0] != "%%MatrixMarket":
+            raise ParseError(f"bad Matrix Market header: {header!r}")
+        if tok[1].lower() != "matrix" or tok[2].lower() != "coordinate":
+            raise ParseError(f"unsupported object/format: {header!r}")
+        if tok[3].lower() != "real" or tok[4].lower() != "symmetric":
+            raise NotSymmetricReal(
+                f"only real symmetric matrices are supported, got "
+                f"{tok[3]} {tok[4]}")
+        line = fh.readline()
+        while line and (line.startswith("%") or not line.strip()):
+            line = fh.readline()
+        try:
+            m, n, nnz = (int(t) for t in line.split())
+        except ValueError:
+            raise ParseError(f"bad size line: {line.strip()!r}") from None
+        if m != n:
+            raise NotSymmetricReal("matrix must be square")
+        entries = {}
+        for _ in range(nnz):
+            line = fh.readline()
+            if not line:
+                raise ParseError("file ends before declared entry count")
+            parts = line.split()
+            if len(parts) != 3:
+                raise ParseError(f"bad entry line: {line.strip()!r}")
+            try:
+                i, j, v = int(parts[0]) - 1, int(parts[1]) - 1, float(parts[2])
+            except ValueError:
+                raise ParseError(f"bad entry line: {line.strip()!r}") from None
+            if not (0 <= i < n and 0 <= j < n):
+                raise ParseError(f"index out of range: ({i + 1}, {j + 1})")
+            if (i, j) in entries:
+                raise ParseError(f"duplicate entry ({i + 1}, {j + 1})")
+            if i != j and (j, i) in entries and entries[(j, i)] != v:
+                raise AsymmetricValues(
+                    f"entries ({j + 1}, {i + 1}) and ({i + 1}, {j + 1}) "
+                    f"disagree: {entries[(j, i)]} vs {v}")
+            entries[(i, j)] = v
+    rows, cols, vals = [], [], []
+    for (i, j), v in entries.items():
+        rows.append(i)
+        cols.append(j)
+        vals.append(v)
+        if i != j and (j, i) not in entries:
+            rows.append(j)
+            cols.append(i)
+            vals.append(v)
+    return from_coo(n, rows, cols, vals)
+
+
+def write_matrix_market(path, a):
+    """Write the lower triangle in coordinate format, column-major order."""
+    rows = np.repeat(np.arange(a.n), np.diff(a.row_ptr))
+    low = rows >= a.col_idx
+    r, c, v = rows[low], a.col_idx[low], a.values[low]
+    order = np.lexsort((r, c))
+    with open(path, "w") as fh:
+        fh.write("%%MatrixMarket matrix coordinate real symmetric\n")
+        fh.write(f"{a.n} {a.n} {r.size}\n")
+        for k in order:
+            fh.write(f"{r[k] + 1} {c[k] + 1} {v[k]:.17g}\n")
+
+
+def jacobi_prescale(a, b):
+    """A' = D^-1/2 A D^-1/2, b' = D^-1/2 b (reference `sparse.py:290-308`).
+
+    Input-side preprocessing (one pass over nnz(A)); the scale of entry
+    (i, j) is the product s_i * s_j grouped the same way for (i, j) and
+    (j, i) so the result stays exactly symmetric.
+    """
+    diag = a.diagonal()
+    if np.any(diag <= 0.0):
+        raise NonpositiveDiagonal("jacobi_prescale needs a positive diagonal")
+    s = 1.0 / np.sqrt(diag)
+    rows = np.repeat(np.arange(a.n), np.diff(a.row_ptr))
+    vals = a.values * (s[rows] * s[a.col_idx])
+    return (SparseSymMatrix(a.n, a.row_ptr, a.col_idx, vals),
+            np.asarray(b, dtype=np.float64) * s, diag)
+
+
+# ---------------------------------------------------------------------------
+# generators
+
+
+def laplacian_2d(d):
+    """5-point Laplacian on a d x d grid, Dirichlet, diagonal 4.
+
+    Same matrix (index i*d+j, values 4/-1, sorted CSR) as the reference
+    `sparse.py:181-196`.
+    """
+    if d < 2:
+        raise DimensionMismatch("grid side must be at least 2")
+    a = diffusion_fv(np.ones((d, d)))
+    if d > 5:
+        return a
+    # For d <= 5 the reference's scipy kron takes its block-sparse path and
+    # stores the d x d blocks of the block-tridiagonal pattern densely,
+    # explicit zeros included; those zeros are graph edges for the
+    # partitioner and count in nnz(A), so reproduce them.
+    blk = np.arange(d * d) // d
+    dense = a.toarray()
+    rows, cols = np.nonzero(np.abs(blk[:, None] - blk[None, :]) <= 1)
+    return from_coo(d * d, rows, cols, dense[rows, cols])
+
+
+def laplacian_3d(d):
+    """7-point Laplacian on a d^3 grid, Dirichlet, diagonal 6 (config C2)."""
+    if d < 2:
+        raise DimensionMismatch("grid side must be at least 2")
+    return diffusion_fv(np.ones((d, d, d)))
+
+
+def harmonic_face(a1, a2):
+    """Harmonic mean 2 a1 a2 / (a1 + a2); exactly 1 for a1 = a2 = 1."""
+    return 2.0 * a1 * a2 / (a1 + a2)
+
+
+def diffusion_fv(coef):
+    """Finite-volume -div(a grad u) on a 2D/3D cell grid, Dirichlet boundary.
+
+    ``coef`` has one positive value per cell (shape (d0, d1) or (d0, d1, d2));
+    cell index = C-order ravel.  Interior faces carry the harmonic mean of
+    the two cells; a boundary face adds the cell's own coefficient to the
+    diagonal.  Rows are emitted in CSR with sorted columns.
+    """
+    coef = np.asarray(coef, dtype=np.float64)
+    if coef.ndim not in (2, 3) or min(coef.shape) < 2:
+        raise DimensionMismatch("need a 2D or 3D grid with sides >= 2")
+    if np.any(coef <= 0.0):
+        raise NonpositiveDiagonal("coefficients must be positive")
+    shape = coef.shape
+    n = coef.size
+    strides = [int(np.prod(shape[ax + 1:])) for ax in range(coef.ndim)]
+    idx = np.arange(n).reshape(shape)
+    diag = np.zeros(shape)
+    # (offset, row-index, col-index, weight) per face orientation; lower
+    # neighbours (negative offsets) first so columns come out sorted
+    lower, upper = [], []
+    for ax in range(coef.ndim):
+        lo = [slice(None)] * coef.ndim
+        hi = [slice(None)] * coef.ndim
+        lo[ax] = slice(0, shape[ax] - 1)
+        hi[ax] = slice(1, shape[ax])
+        w = harmonic_face(coef[tuple(lo)], coef[tuple(hi)])
+        diag[tuple(lo)] += w
+        diag[tuple(hi)] += w
+        upper.append((strides[ax], idx[tuple(lo)].ravel(), -w.ravel()))
+        lower.append((-strides[ax], idx[tuple(hi)].ravel(), -w.ravel()))
+        first = [slice(None)] * coef.ndim
+        last = [slice(None)] * coef.ndim
+        first[ax] = slice(0, 1)
+        last[ax] = slice(shape[ax] - 1, shape[ax])
+        diag[tuple(first)] += coef[tuple(first)]
+        diag[tuple(last)] += coef[tuple(last)]
+    rows, cols, vals = [], [], []
+    for off, r, w in lower + upper:
+        rows.append(r)
+        cols.append(r + off)
+        vals.append(w)
+    rows.append(np.arange(n))
+    cols.append(np.arange(n))
+    vals.append(diag.ravel())
+    return from_coo(n, np.concatenate(rows), np.concatenate(cols),
+                    np.concatenate(vals))
+
+
+def log_uniform_block_field(shape, block, decades, rng):
+    """Piecewise-constant field: one value 10**U(-decades, decades) per
+    block of ``block`` cells per axis (C3: 16x16 blocks of 32^2 cells,
+    C4: 8^3 blocks of 8^3 cells)."""
+    nb = tuple(s // block for s in shape)
+    if any(b * block != s for b, s in zip(nb, shape)):
+        raise DimensionMismatch("grid must be a multiple of the block size")
+    logs = rng.uniform(-decades, decades, size=nb)
+    a = 10.0 ** logs
+    for ax in range(len(shape)):
+        a = np.repeat(a, block, axis=ax)
+    return a
+
+
+BASELINE_CONFIGS = {
+    # name: (grid, block, decades, seed, levels)
+    "C1": ((128, 128), None, 0.0, 0, 7),
+    "C2": ((32, 32, 32), None, 0.0, 1, 10),
+    "C3": ((512, 512), 32, 3.0, 2, 12),
+    "C4": ((64, 64, 64), 8, 3.0, 3, 15),
+}
+
+
+def baseline_problem(name, grid=None):
+    """(A, b, levels) for BASELINE.json config ``name`` (C1-C4).
+
+    ``grid`` overrides the grid side (same construction, smaller size) for
+    tests; the field is drawn first, then ``b = rng.standard_normal(n)``.
+    """
+    shape, block, decades, seed, levels = BASELINE_CONFIGS[name]
+    if grid is not None:
+        shape = tuple([grid] * len(shape))
+    rng = np.random.default_rng(seed)
+    if block is None:
+        a = diffusion_fv(np.ones(shape))
+    else:
+        if grid is not None:
+            block = max(1, min(block, grid // 8 if grid >= 8 else 1))
+        a = diffusion_fv(log_uniform_block_field(shape, block, decades, rng))
+    b = rng.standard_normal(a.n)
+    return a, b, levels
