@@ -1,0 +1,159 @@
+/*
+ * spand_b200 — C-ABI of the B200-native spaND hot path (sm_100a).
+ *
+ * Boundary contract (mirrors the reference's Python operators; the host
+ * package paper_2007_00789_b200 binds these with ctypes):
+ *   - every entry point takes caller-owned DEVICE pointers, plain sizes and a
+ *     cudaStream_t passed as void*; nothing here allocates device memory;
+ *   - return value: 0 on success, a cudaError_t (>0) if the launch failed,
+ *     -1 on a bad argument.  Numerical failures (non-SPD pivots) are reported
+ *     through device `info` arrays (LAPACK convention: info = pivot + 1).
+ *   - descriptors of batched work are device arrays of int64 rows (layouts
+ *     documented per function), so no C struct crosses the boundary.
+ *
+ * Geometry convention shared by all factorization kernels: every dense
+ * matrix is stored column-major at its cluster pair's ORIGINAL size
+ * (m0[rc] x m0[cc], ld = m0[rc]); the live part is rows [off[rc], m0[rc]) x
+ * cols [off[cc], m0[cc]), where `off` (device int32) grows as sparsification
+ * drops fine slots (the reference keeps `dofs[n_fine:]`,
+ * /root/reference/pkg/src/spdkit/factorize.py:187-190).  An OPERAND row is 7
+ * int64: {ptr, rc, cc, rskip, cskip, rcount, ccount}: the operand starts
+ * rskip/cskip past the live start, and is clamped to rcount/ccount when >= 0.
+ */
+#ifndef SPAND_B200_H
+#define SPAND_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+int spand_version(void);
+int spand_device_sm_count(void);
+
+/* ---- PCG building blocks (replace scipy csr_matvec sparse.py:64-68 and the
+ *      NumPy vector algebra of krylov.py:93-131) ---------------------------- */
+
+/* y = A x for CSR A (int32 indices).  If pdot != NULL also writes the
+ * per-block partials of x.y into pdot (nblocks = spand_spmv_blocks(n)). */
+int spand_spmv_blocks(int n);
+int spand_csr_spmv(int n, const int32_t* row_ptr, const int32_t* col_idx,
+                   const double* vals, const double* x, double* y,
+                   double* pdot, void* stream);
+
+/* deterministic two-stage dot: partials[nb] then out[0] = sum (fixed order) */
+int spand_dot_blocks(int n);
+int spand_dot(int n, const double* x, const double* y, double* partials,
+              double* out, void* stream);
+/* sum of nparts partials into out[0] (fixed order) */
+int spand_reduce_sum(int nparts, const double* partials, double* out,
+                     void* stream);
+
+/* scal[0] = rz, scal[1] = pap -> alpha = rz / pap;  x += alpha p;
+ * r -= alpha ap; partials of r.r (spand_dot_blocks(n) entries) */
+int spand_pcg_xr(int n, const double* scal, double* x, double* r,
+                 const double* p, const double* ap, double* partials,
+                 void* stream);
+/* beta = scal[2] / scal[0] (rz_new / rz); p = z + beta p */
+int spand_pcg_p(int n, const double* scal, const double* z, double* p,
+                void* stream);
+/* y = x[perm] (gather) and y[perm] = x (scatter) */
+int spand_gather(int n, const int32_t* perm, const double* x, double* y,
+                 void* stream);
+int spand_scatter_perm(int n, const int32_t* perm, const double* x, double* y,
+                       void* stream);
+
+/* ---- preconditioner apply (replaces Elimination/Scaling/Orthogonal/
+ *      ErrorCorrection.apply_inv/apply_inv_t, schemes.py:102-112,136-140,
+ *      162-166,188-192, and Factorization.apply_* factorize.py:269-282) ------
+ *
+ * A pass is a sequence of phases; a phase is one spand_gemv_tiles launch
+ * (products of stored dense payloads with gathered vector pieces, written to
+ * scratch) followed by one spand_apply_scatter launch (overwrite or
+ * deterministic ordered subtract-accumulate into x).
+ *
+ * GEMV task row (8 x int64): {M, ld, rows, cols, trans, rot, in_kind, in_ptr}
+ *   op = M (trans 0: outputs index rows, the inner index k runs over
+ *   columns) or M^T (trans 1: outputs index columns, k runs over rows); M is
+ *   column-major; logical column j of M is physical column (j + rot) % cols
+ *   (the fine-first column order of the Orthogonal op, schemes.py:291).
+ *   Input element k: in_kind 0: x[idx[k]] with idx = (int32*)in_ptr;
+ *   in_kind 1: ((double*)in_ptr)[k] (a contiguous piece of x).
+ * tile row (8 x int64): {task, ob, oc, kb, kc, out_off, 0, 0}
+ *   scratch[out_off + i] = sum_{k in [kb, kb+kc)} op(M)[ob+i, k] * in[k], i < oc <= 64,
+ *   kc <= 2048 (larger inner dimensions are split into several tiles whose
+ *   partial sums the scatter step adds in a fixed order).
+ * nvec right-hand sides: x is (n x nvec) with leading dim ldx and scratch
+ * (len x nvec) with leading dim ldscr.
+ */
+int spand_gemv_tiles(int ntiles, const int64_t* tiles, const int64_t* tasks,
+                     const double* x, int64_t ldx, double* scratch,
+                     int64_t ldscr, int nvec, void* stream);
+/* for e in [0, nout): s = sum_{t in [ptr[e], ptr[e+1])} scratch[src[t]]
+ * (summed in the stored order: deterministic); mode[e] == 0: x[dst[e]] = s,
+ * mode[e] == 1: x[dst[e]] -= s. */
+int spand_apply_scatter(int nout, const int32_t* dst, const int8_t* mode,
+                        const int64_t* ptr, const int64_t* src, double* x,
+                        int64_t ldx, const double* scratch, int64_t ldscr,
+                        int nvec, void* stream);
+
+/* ---- factorization kernels (replace dense.py:45-183 and the BLAS calls of
+ *      schemes.py:199-236, factorize.py:131-220) ---------------------------- */
+
+/* Batched in-place Cholesky (lower) of square operands (7 int64 each).
+ * info[t] = 0 or failing pivot + 1 (dense.py:53-55). */
+int spand_potrf_batched(int ntask, const int64_t* ops, const int32_t* m0,
+                        const int32_t* off, int32_t* info, void* stream);
+/* Batched lower-triangular inverse: task row = {L operand(7), Linv operand(7)}.
+ * Upper triangle of Linv is written with zeros (dense.py:85-93). */
+int spand_trtri_batched(int ntask, const int64_t* ops, const int32_t* m0,
+                        const int32_t* off, void* stream);
+/* Batched copy: task row = {src operand(7), dst operand(7), mode}; mode 0:
+ * copy the full live rectangle, 1: copy lower triangle + zero upper, 2:
+ * write the identity (src ignored). */
+int spand_copy_batched(int ntask, const int64_t* ops, const int32_t* m0,
+                       const int32_t* off, void* stream);
+
+/* Grouped FP64 GEMM on DMMA tensor cores (mma.sync m8n8k4 f64):
+ *   C = beta * C + alpha * sum_{s in segs(target)} A_s * op(B_s)
+ * target row (8 int64): {C operand(7), seg_begin}; seg_end = next target's
+ * seg_begin (targets array has ntarget+1 rows' worth of seg_begin: the row
+ * after the last carries only seg_begin at column 7).
+ * segment row (14 int64): {A operand(7), B operand(7)}; A is M x K; B is N x K
+ * (bT = 1: op(B) = B^T, "NT") or K x N (bT = 0, "NN").
+ * tile row (3 int64): {target, m0_tile, n0_tile}; tile 64 x 64.
+ * lower_only: skip tiles strictly above the diagonal (SYRK use). */
+int spand_gemm_grouped(int ntile, const int64_t* tiles, const int64_t* targets,
+                       const int64_t* segs, const int32_t* m0,
+                       const int32_t* off, double alpha, double beta, int bT,
+                       int lower_only, void* stream);
+
+/* Batched early-stopping column-pivoted Householder QR of interface panels
+ * (restates dense.py:117-222, schemes.py:272-318, factorize.py:175-196).
+ * See rrqr.cu for the task/neighbour row layouts. */
+int spand_rrqr_wave(int npanel, const int64_t* panels, const int64_t* nbrs,
+                    int32_t* m0, int32_t* off, double eps, int scheme,
+                    int64_t* events, double* work, void* stream);
+int spand_rrqr_cta_count(void);
+
+/* Final dense block (factorize.py:198-220): assemble the live parts of the
+ * remaining clusters into one square operand. */
+int spand_assemble_final(int ncl, const int64_t* cl, int64_t nblk,
+                         const int64_t* blocks, const int32_t* m0,
+                         int32_t* off, int32_t final_id, double* dst,
+                         void* stream);
+
+/* ---- host-side integer structure (partition.py:118-268) ------------------ */
+
+/* Nested-dissection hierarchy of the graph of a CSR matrix (host memory).
+ * dofs_out[n]: cluster dofs concatenated in id order; cptr_out[n+1]: cluster
+ * boundaries; depth_out[n]: cluster depths; ncl_out[0]: cluster count. */
+int spand_nd_partition(int64_t n, const int64_t* row_ptr, const int64_t* col_idx,
+                       int levels, int64_t* dofs_out, int64_t* cptr_out,
+                       int32_t* depth_out, int64_t* ncl_out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,145 @@
+// Preconditioner apply: batched dense GEMV tiles + ordered scatter.
+// Replaces the per-operator NumPy GEMVs and fancy-index gathers/scatters of
+// schemes.py:102-112,136-140,162-166,188-192 (apply_inv / apply_inv_t).
+// HBM-bound: every payload entry is read once per pass, coalesced along the
+// column-major storage; vectors are staged in shared memory.
+#include "common.cuh"
+#include "../../include/spand_b200.h"
+
+namespace {
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+constexpr int kTileOut = 64;
+constexpr int kTileK = 2048;
+
+struct Task {
+  const double* M;
+  int64_t ld;
+  int rows, cols, trans, rot, in_kind;
+  const void* in;
+};
+
+__device__ __forceinline__ Task load_task(const int64_t* t) {
+  Task k;
+  k.M = reinterpret_cast<const double*>(t[0]);
+  k.ld = t[1];
+  k.rows = (int)t[2];
+  k.cols = (int)t[3];
+  k.trans = (int)t[4];
+  k.rot = (int)t[5];
+  k.in_kind = (int)t[6];
+  k.in = reinterpret_cast<const void*>(t[7]);
+  return k;
+}
+
+__device__ __forceinline__ int phys_col(int j, int rot, int cols) {
+  int c = j + rot;
+  return c >= cols ? c - cols : c;
+}
+
+__global__ void __launch_bounds__(kThreads)
+gemv_tiles_kernel(const int64_t* __restrict__ tiles, const int64_t* __restrict__ tasks,
+                  const double* __restrict__ x, int64_t ldx, double* __restrict__ scratch,
+                  int64_t ldscr, int nvec) {
+  __shared__ double vin[kTileK];
+  __shared__ double part[kWarps][kTileOut];
+  const int64_t* tr = tiles + 8 * (int64_t)blockIdx.x;
+  const Task T = load_task(tasks + 8 * tr[0]);
+  const int ob = (int)tr[1], oc = (int)tr[2], kb = (int)tr[3], kc = (int)tr[4];
+  double* out = scratch + tr[5];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int v = 0; v < nvec; ++v) {
+    const double* xv = x + v * ldx;
+    __syncthreads();
+    for (int k = threadIdx.x; k < kc; k += kThreads) {
+      const int kk = kb + k;
+      vin[k] = T.in_kind == 0 ? xv[reinterpret_cast<const int32_t*>(T.in)[kk]]
+                              : reinterpret_cast<const double*>(T.in)[kk + v * ldx];
+    }
+    __syncthreads();
+    if (T.trans == 0) {
+      // y[r] = sum_c M[r, c] in[c]; warp w takes columns w, w+8, ...;
+      // lane takes rows ob+lane and ob+lane+32 (coalesced down a column)
+      double a0 = 0.0, a1 = 0.0;
+      const int r0 = ob + lane, r1 = ob + lane + 32;
+      const bool ok0 = lane < oc, ok1 = lane + 32 < oc;
+      for (int c = w; c < kc; c += kWarps) {
+        const double* col = T.M + (int64_t)phys_col(kb + c, T.rot, T.cols) * T.ld;
+        const double xi = vin[c];
+        if (ok0) a0 += __ldg(col + r0) * xi;
+        if (ok1) a1 += __ldg(col + r1) * xi;
+      }
+      part[w][lane] = a0;
+      part[w][lane + 32] = a1;
+    } else {
+      // y[j] = sum_r M[r, j] in[r]; warp w takes output columns w*8..w*8+7
+      for (int jj = 0; jj < kTileOut / kWarps; ++jj) {
+        const int j = w * (kTileOut / kWarps) + jj;
+        double a = 0.0;
+        if (j < oc) {
+          const double* col = T.M + (int64_t)phys_col(ob + j, T.rot, T.cols) * T.ld + kb;
+          for (int r = lane; r < kc; r += 32) a += __ldg(col + r) * vin[r];
+        }
+        a = warp_sum(a);
+        if (lane == 0) part[0][j] = a;
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x < oc) {
+      double s;
+      if (T.trans == 0) {
+        s = 0.0;
+#pragma unroll
+        for (int i = 0; i < kWarps; ++i) s += part[i][threadIdx.x];
+      } else {
+        s = part[0][threadIdx.x];
+      }
+      out[threadIdx.x + v * ldscr] = s;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kThreads)
+scatter_kernel(int nout, const int32_t* __restrict__ dst, const int8_t* __restrict__ mode,
+               const int64_t* __restrict__ ptr, const int64_t* __restrict__ src,
+               double* __restrict__ x, int64_t ldx, const double* __restrict__ scratch,
+               int64_t ldscr, int nvec) {
+  const int e = blockIdx.x * kThreads + threadIdx.x;
+  if (e >= nout) return;
+  const int64_t b = ptr[e], f = ptr[e + 1];
+  const int d = dst[e];
+  const int md = mode[e];
+  for (int v = 0; v < nvec; ++v) {
+    double s = 0.0;
+    for (int64_t t = b; t < f; ++t) s += scratch[src[t] + v * ldscr];
+    double* xd = x + d + v * ldx;
+    if (md == 0) *xd = s;
+    else *xd -= s;
+  }
+}
+}  // namespace
+
+extern "C" {
+
+int spand_gemv_tiles(int ntiles, const int64_t* tiles, const int64_t* tasks, const double* x,
+                     int64_t ldx, double* scratch, int64_t ldscr, int nvec, void* stream) {
+  if (ntiles < 0 || nvec < 1) return -1;
+  if (ntiles == 0) return 0;
+  gemv_tiles_kernel<<<ntiles, kThreads, 0, as_stream(stream)>>>(tiles, tasks, x, ldx, scratch,
+                                                                ldscr, nvec);
+  SPAND_CHECK_LAUNCH();
+  return 0;
+}
+
+int spand_apply_scatter(int nout, const int32_t* dst, const int8_t* mode, const int64_t* ptr,
+                        const int64_t* src, double* x, int64_t ldx, const double* scratch,
+                        int64_t ldscr, int nvec, void* stream) {
+  if (nout < 0 || nvec < 1) return -1;
+  if (nout == 0) return 0;
+  scatter_kernel<<<(nout + kThreads - 1) / kThreads, kThreads, 0, as_stream(stream)>>>(
+      nout, dst, mode, ptr, src, x, ldx, scratch, ldscr, nvec);
+  SPAND_CHECK_LAUNCH();
+  return 0;
+}
+
+}  // extern "C"

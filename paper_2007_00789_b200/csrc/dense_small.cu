@@ -1,0 +1,191 @@
+// Batched FP64 Cholesky, triangular inverse and copies on live windows
+// (replace LAPACK dpotrf / dtrtri calls of dense.py:45-93 as used by
+// schemes.py:199-236 and factorize.py:131-220).  One CTA per matrix; sizes
+// are read from the device geometry so a whole level is one launch with no
+// host round trip.  The diagonal 32x32 tiles are factored in shared memory
+// with warp-level reductions; the rest is blocked left-looking updates.
+#include "common.cuh"
+#include "../../include/spand_b200.h"
+
+namespace {
+constexpr int kT = 256;
+constexpr int NB = 32;
+
+// Left-looking blocked Cholesky of one live window (in place, lower).
+__global__ void __launch_bounds__(kT)
+potrf_kernel(const int64_t* __restrict__ ops, const int32_t* __restrict__ m0,
+             const int32_t* __restrict__ off, int32_t* __restrict__ info) {
+  __shared__ double Bk[NB][65];     // rows jb..jb+NB of columns kb..kb+64
+  __shared__ double D[NB][NB + 1];  // diagonal tile
+  __shared__ int bad;
+  const Opnd A = load_opnd(ops + 7 * (int64_t)blockIdx.x, m0, off);
+  const int n = A.rows < A.cols ? A.rows : A.cols;
+  const int ld = A.ld;
+  double* a = A.p;
+  if (threadIdx.x == 0) bad = 0;
+  __syncthreads();
+  for (int jb = 0; jb < n; jb += NB) {
+    const int nbk = min(NB, n - jb);
+    // ---- panel update A[jb:, jb:jb+nbk] -= A[jb:, :jb] * A[jb:jb+nbk, :jb]^T
+    // each thread owns rows i = jb + tid + kT*r, 32 accumulators per row
+    for (int rb = jb; rb < n; rb += kT) {
+      const int i = rb + threadIdx.x;
+      double acc[NB];
+#pragma unroll
+      for (int j = 0; j < NB; ++j) acc[j] = 0.0;
+      for (int kb = 0; kb < jb; kb += 64) {
+        const int kc = min(64, jb - kb);
+        __syncthreads();
+        for (int e = threadIdx.x; e < NB * 64; e += kT) {
+          const int j = e / 64, k = e % 64;
+          Bk[j][k] = (j < nbk && k < kc) ? a[(jb + j) + (int64_t)(kb + k) * ld] : 0.0;
+        }
+        __syncthreads();
+        if (i < n) {
+          for (int k = 0; k < kc; ++k) {
+            const double aik = a[i + (int64_t)(kb + k) * ld];
+#pragma unroll
+            for (int j = 0; j < NB; ++j) acc[j] += aik * Bk[j][k];
+          }
+        }
+      }
+      if (i < n) {
+#pragma unroll
+        for (int j = 0; j < NB; ++j)
+          if (j < nbk) a[i + (int64_t)(jb + j) * ld] -= acc[j];
+      }
+    }
+    __syncthreads();
+    // ---- factor the diagonal tile in shared memory
+    for (int e = threadIdx.x; e < NB * NB; e += kT) {
+      const int r = e / NB, c = e % NB;
+      D[r][c] = (r < nbk && c < nbk && c <= r) ? a[(jb + r) + (int64_t)(jb + c) * ld] : 0.0;
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      const int l = threadIdx.x;
+      for (int j = 0; j < nbk; ++j) {
+        double d = D[j][j];
+        if (!(d > 0.0)) {  // also catches NaN
+          if (l == 0 && bad == 0) bad = jb + j + 1;
+          break;
+        }
+        d = sqrt(d);
+        __syncwarp();
+        if (l == 0) D[j][j] = d;
+        if (l > j && l < nbk) D[l][j] /= d;
+        __syncwarp();
+        // rank-1 update of the trailing tile (lower part), lane = row
+        if (l > j && l < nbk)
+          for (int c = j + 1; c <= l; ++c) D[l][c] -= D[l][j] * D[c][j];
+        __syncwarp();
+      }
+    }
+    __syncthreads();
+    if (bad) break;
+    for (int e = threadIdx.x; e < NB * NB; e += kT) {
+      const int r = e / NB, c = e % NB;
+      if (r < nbk && c < nbk && c <= r) a[(jb + r) + (int64_t)(jb + c) * ld] = D[r][c];
+    }
+    // ---- rows below: x = row * L_d^{-T}  (forward substitution per row)
+    for (int i = jb + nbk + threadIdx.x; i < n; i += kT) {
+      double x[NB];
+#pragma unroll
+      for (int j = 0; j < NB; ++j) x[j] = (j < nbk) ? a[i + (int64_t)(jb + j) * ld] : 0.0;
+#pragma unroll
+      for (int j = 0; j < NB; ++j) {
+        if (j < nbk) {
+          double s = x[j];
+#pragma unroll
+          for (int k = 0; k < j; ++k) s -= x[k] * D[j][k];
+          x[j] = s / D[j][j];
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < NB; ++j)
+        if (j < nbk) a[i + (int64_t)(jb + j) * ld] = x[j];
+    }
+    __syncthreads();
+  }
+  // zero the strict upper triangle (LAPACK dpotrf with clean=1, dense.py:53)
+  if (!bad) {
+    for (int64_t e = threadIdx.x; e < (int64_t)n * n; e += kT) {
+      const int r = (int)(e % n), c = (int)(e / n);
+      if (r < c) a[r + (int64_t)c * ld] = 0.0;
+    }
+  }
+  if (threadIdx.x == 0) info[blockIdx.x] = bad;
+}
+
+// Lower-triangular inverse, one thread per column (forward substitution),
+// x kept in the output column (L1 resident).
+__global__ void __launch_bounds__(kT)
+trtri_kernel(const int64_t* __restrict__ ops, const int32_t* __restrict__ m0,
+             const int32_t* __restrict__ off) {
+  const Opnd L = load_opnd(ops + 14 * (int64_t)blockIdx.x, m0, off);
+  const Opnd X = load_opnd(ops + 14 * (int64_t)blockIdx.x + 7, m0, off);
+  const int n = L.rows;
+  for (int j = threadIdx.x; j < n; j += kT) {
+    double* x = X.p + (int64_t)j * X.ld;
+    for (int i = 0; i < j; ++i) x[i] = 0.0;
+    x[j] = 1.0 / L.p[j + (int64_t)j * L.ld];
+    for (int i = j + 1; i < n; ++i) {
+      double s = 0.0;
+      for (int k = j; k < i; ++k) s += L.p[i + (int64_t)k * L.ld] * x[k];
+      x[i] = -s / L.p[i + (int64_t)i * L.ld];
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kT)
+copy_kernel(const int64_t* __restrict__ ops, const int32_t* __restrict__ m0,
+            const int32_t* __restrict__ off) {
+  const int64_t* d = ops + 15 * (int64_t)blockIdx.x;
+  const int mode = (int)d[14];
+  const Opnd D = load_opnd(d + 7, m0, off);
+  Opnd S = D;
+  if (mode != 2) S = load_opnd(d, m0, off);
+  const int rows = D.rows, cols = D.cols;
+  const int64_t total = (int64_t)rows * cols;
+  for (int64_t e = (int64_t)blockIdx.y * kT + threadIdx.x; e < total; e += (int64_t)gridDim.y * kT) {
+    const int r = (int)(e % rows), c = (int)(e / rows);
+    double v;
+    if (mode == 2) v = (r == c) ? 1.0 : 0.0;
+    else if (mode == 1 && r < c) v = 0.0;
+    else v = (r < S.rows && c < S.cols) ? S.p[r + (int64_t)c * S.ld] : 0.0;
+    D.p[r + (int64_t)c * D.ld] = v;
+  }
+}
+}  // namespace
+
+extern "C" {
+
+int spand_potrf_batched(int ntask, const int64_t* ops, const int32_t* m0, const int32_t* off,
+                        int32_t* info, void* stream) {
+  if (ntask < 0) return -1;
+  if (ntask == 0) return 0;
+  potrf_kernel<<<ntask, kT, 0, as_stream(stream)>>>(ops, m0, off, info);
+  SPAND_CHECK_LAUNCH();
+  return 0;
+}
+
+int spand_trtri_batched(int ntask, const int64_t* ops, const int32_t* m0, const int32_t* off,
+                        void* stream) {
+  if (ntask < 0) return -1;
+  if (ntask == 0) return 0;
+  trtri_kernel<<<ntask, kT, 0, as_stream(stream)>>>(ops, m0, off);
+  SPAND_CHECK_LAUNCH();
+  return 0;
+}
+
+int spand_copy_batched(int ntask, const int64_t* ops, const int32_t* m0, const int32_t* off,
+                       void* stream) {
+  if (ntask < 0) return -1;
+  if (ntask == 0) return 0;
+  dim3 grid(ntask, 16);
+  copy_kernel<<<grid, kT, 0, as_stream(stream)>>>(ops, m0, off);
+  SPAND_CHECK_LAUNCH();
+  return 0;
+}
+
+}  // extern "C"

@@ -1,0 +1,187 @@
+// Grouped FP64 GEMM on the DMMA tensor pipe (mma.sync.m8n8k4 f64 ->
+// SASS DMMA.8x8x4 on sm_100a).  Serves the Schur-complement / fill-in update
+// A_ww -= A_ws A_ss^-1 A_sw (schemes.py:220 + factorize.py:150-161, fused
+// over every same-level interior that touches a target block: K-concatenated
+// segments, one read-modify-write of C), the TRSMs of schemes.py:217,235
+// (as products with explicit triangular inverses) and the trailing updates
+// of the blocked factorizations.
+//
+// CTA tile 64x64, 4 warps (2x2) of 32x32, K staged 16 at a time through a
+// 2-deep cp.async shared-memory pipeline; live sizes come from the device
+// geometry so tiles past a block's live extent exit at once.
+#include "common.cuh"
+#include "../../include/spand_b200.h"
+
+namespace {
+constexpr int BM = 64, BN = 64, BK = 16, LDS = 68;  // LDS padding: conflict-free frags
+constexpr int kThreads = 128;
+
+__device__ __forceinline__ void cp_async8(double* smem, const double* gmem, bool pred) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  const int sz = pred ? 8 : 0;
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(sz));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::); }
+
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+struct SegIter {
+  int seg, seg_end, k0;
+};
+
+__global__ void __launch_bounds__(kThreads)
+gemm_grouped_kernel(const int64_t* __restrict__ tiles, const int64_t* __restrict__ targets,
+                    const int64_t* __restrict__ segs, const int32_t* __restrict__ m0,
+                    const int32_t* __restrict__ off, double alpha, double beta, int bT,
+                    int lower_only) {
+  __shared__ __align__(16) double As[2][BK][LDS];
+  __shared__ __align__(16) double Bs[2][BK][LDS];
+  const int64_t* tr = tiles + 3 * (int64_t)blockIdx.x;
+  const int64_t t = tr[0];
+  const int i0 = (int)tr[1], j0 = (int)tr[2];
+  if (lower_only && j0 > i0) return;
+  const int64_t* trow = targets + 8 * t;
+  const Opnd C = load_opnd(trow, m0, off);
+  if (i0 >= C.rows || j0 >= C.cols) return;
+  const int sb = (int)trow[7], se = (int)targets[8 * (t + 1) + 7];
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp >> 1, wn = warp & 1;
+  double acc[4][4][2];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+
+  // chunk iterator over (segment, k0)
+  int seg = sb, k0 = 0;
+  Opnd A, B;
+  int K = 0;
+  auto open_seg = [&](int s) {
+    A = load_opnd(segs + 14 * (int64_t)s, m0, off);
+    B = load_opnd(segs + 14 * (int64_t)s + 7, m0, off);
+    K = A.cols;
+    const int kb = bT ? B.cols : B.rows;
+    if (kb < K) K = kb;
+  };
+  // skip empty segments
+  while (seg < se) {
+    open_seg(seg);
+    if (K > 0) break;
+    ++seg;
+  }
+  auto load_stage = [&](int st, const Opnd& a, const Opnd& b, int kbase, int kmax) {
+#pragma unroll
+    for (int r = 0; r < (BM * BK) / kThreads; ++r) {
+      const int e = tid + r * kThreads;
+      const int m = e % BM, k = e / BM;
+      const int gm = i0 + m, gk = kbase + k;
+      const bool ok = gm < a.rows && gk < kmax;
+      cp_async8(&As[st][k][m], ok ? a.p + gm + (int64_t)gk * a.ld : a.p, ok);
+    }
+    if (bT) {
+#pragma unroll
+      for (int r = 0; r < (BN * BK) / kThreads; ++r) {
+        const int e = tid + r * kThreads;
+        const int nn = e % BN, k = e / BN;
+        const int gn = j0 + nn, gk = kbase + k;
+        const bool ok = gn < b.rows && gk < kmax;
+        cp_async8(&Bs[st][k][nn], ok ? b.p + gn + (int64_t)gk * b.ld : b.p, ok);
+      }
+    } else {
+#pragma unroll
+      for (int r = 0; r < (BN * BK) / kThreads; ++r) {
+        const int e = tid + r * kThreads;
+        const int k = e % BK, nn = e / BK;
+        const int gn = j0 + nn, gk = kbase + k;
+        const bool ok = gn < b.cols && gk < kmax;
+        cp_async8(&Bs[st][k][nn], ok ? b.p + gk + (int64_t)gn * b.ld : b.p, ok);
+      }
+    }
+    cp_commit();
+  };
+
+  if (seg < se) {
+    int st = 0;
+    load_stage(0, A, B, 0, K);
+    while (true) {
+      // advance iterator to the next chunk and prefetch it
+      Opnd An = A, Bn = B;
+      int Kn = K, segn = seg, kn = k0 + BK;
+      bool have_next = true;
+      if (kn >= Kn) {
+        kn = 0;
+        ++segn;
+        while (segn < se) {
+          An = load_opnd(segs + 14 * (int64_t)segn, m0, off);
+          Bn = load_opnd(segs + 14 * (int64_t)segn + 7, m0, off);
+          Kn = An.cols;
+          const int kb = bT ? Bn.cols : Bn.rows;
+          if (kb < Kn) Kn = kb;
+          if (Kn > 0) break;
+          ++segn;
+        }
+        have_next = segn < se;
+      }
+      cp_wait_all();
+      __syncthreads();
+      if (have_next) load_stage(st ^ 1, An, Bn, kn, Kn);
+#pragma unroll
+      for (int kk = 0; kk < BK / 4; ++kk) {
+        double af[4], bf[4];
+        const int kr = kk * 4 + (lane & 3);
+#pragma unroll
+        for (int mi = 0; mi < 4; ++mi) af[mi] = As[st][kr][wm * 32 + mi * 8 + (lane >> 2)];
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni) bf[ni] = Bs[st][kr][wn * 32 + ni * 8 + (lane >> 2)];
+#pragma unroll
+        for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+          for (int ni = 0; ni < 4; ++ni) dmma(acc[mi][ni][0], acc[mi][ni][1], af[mi], bf[ni]);
+      }
+      __syncthreads();
+      if (!have_next) break;
+      st ^= 1;
+      A = An;
+      B = Bn;
+      K = Kn;
+      seg = segn;
+      k0 = kn;
+    }
+  }
+  // epilogue: C = beta C + alpha acc
+#pragma unroll
+  for (int mi = 0; mi < 4; ++mi) {
+    const int r = i0 + wm * 32 + mi * 8 + (lane >> 2);
+    if (r >= C.rows) continue;
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int c = j0 + wn * 32 + ni * 8 + (lane & 3) * 2 + h;
+        if (c >= C.cols) continue;
+        double* pc = C.p + r + (int64_t)c * C.ld;
+        const double v = alpha * acc[mi][ni][h];
+        *pc = (beta == 0.0) ? v : beta * (*pc) + v;
+      }
+    }
+  }
+}
+}  // namespace
+
+extern "C" int spand_gemm_grouped(int ntile, const int64_t* tiles, const int64_t* targets,
+                                  const int64_t* segs, const int32_t* m0, const int32_t* off,
+                                  double alpha, double beta, int bT, int lower_only,
+                                  void* stream) {
+  if (ntile < 0) return -1;
+  if (ntile == 0) return 0;
+  gemm_grouped_kernel<<<ntile, kThreads, 0, as_stream(stream)>>>(tiles, targets, segs, m0, off,
+                                                                 alpha, beta, bT, lower_only);
+  SPAND_CHECK_LAUNCH();
+  return 0;
+}

@@ -1,0 +1,262 @@
+// Host-side nested-dissection hierarchy (integer structure, bit-exact with
+// the reference partition.py:135-268).  Native C++ replacement of the
+// reference's NumPy/scipy.csgraph recursion; C4 (n = 262144) runs in tens
+// of milliseconds instead of seconds.
+//
+// Semantics restated (cited lines of /root/reference/pkg/src/spdkit/partition.py):
+//  - graph = off-diagonal stored pattern of A (explicit zeros included), :237-242
+//  - recurse(verts, depth): leaf if depth == levels or |verts| < 6, :249-253
+//  - bisect: disconnected regions are split by whole components, largest
+//    first (ties: smaller label = smaller first vertex), each to the lighter
+//    side, :172-185; otherwise BFS from local vertex 0, seed = smallest
+//    farthest vertex, level sets from the seed, :188-194; cut at the level
+//    boundary minimising |side1 - estimated side2|, :200-203; partial fill of
+//    the next level (smallest ids first), :206-210; separator = part-2
+//    neighbours of part 1, :211-217; separator vertices with no part-2
+//    neighbour rejoin part 1, :218-224
+//  - unsplittable (no separator and an empty side) -> leaf, :255-259
+//  - cluster ids in DFS preorder, separator before its two halves, :260-263
+#include <algorithm>
+#include <cstdint>
+#include <vector>
+
+namespace {
+
+struct Graph {
+  std::vector<int64_t> ptr, idx;  // off-diagonal adjacency, sorted rows
+};
+
+struct Splitter {
+  const Graph& g;
+  std::vector<int64_t> local;  // global -> local id, -1 outside
+  explicit Splitter(const Graph& gr, int64_t n) : g(gr), local(n, -1) {}
+
+  // induced subgraph of sorted `verts`, local numbering
+  void extract(const std::vector<int64_t>& verts, std::vector<int64_t>& lp,
+               std::vector<int64_t>& li) {
+    const int64_t nv = (int64_t)verts.size();
+    for (int64_t i = 0; i < nv; ++i) local[verts[i]] = i;
+    lp.assign(nv + 1, 0);
+    li.clear();
+    for (int64_t i = 0; i < nv; ++i) {
+      const int64_t v = verts[i];
+      for (int64_t e = g.ptr[v]; e < g.ptr[v + 1]; ++e) {
+        const int64_t c = local[g.idx[e]];
+        if (c >= 0) li.push_back(c);
+      }
+      lp[i + 1] = (int64_t)li.size();
+    }
+    for (int64_t i = 0; i < nv; ++i) local[verts[i]] = -1;
+  }
+
+  static void bfs(const std::vector<int64_t>& lp, const std::vector<int64_t>& li,
+                  int64_t src, std::vector<int64_t>& dist) {
+    const int64_t nv = (int64_t)lp.size() - 1;
+    dist.assign(nv, -1);
+    std::vector<int64_t> q;
+    q.reserve(nv);
+    q.push_back(src);
+    dist[src] = 0;
+    for (size_t h = 0; h < q.size(); ++h) {
+      const int64_t u = q[h];
+      for (int64_t e = lp[u]; e < lp[u + 1]; ++e) {
+        const int64_t w = li[e];
+        if (dist[w] < 0) {
+          dist[w] = dist[u] + 1;
+          q.push_back(w);
+        }
+      }
+    }
+  }
+
+  // returns (p1, p2, sep), all sorted
+  void bisect(const std::vector<int64_t>& verts, std::vector<int64_t>& p1,
+              std::vector<int64_t>& p2, std::vector<int64_t>& sep) {
+    p1.clear();
+    p2.clear();
+    sep.clear();
+    const int64_t nv = (int64_t)verts.size();
+    if (nv < 2) {
+      p1 = verts;
+      return;
+    }
+    std::vector<int64_t> lp, li;
+    extract(verts, lp, li);
+    // connected components, labels in order of smallest member
+    std::vector<int64_t> label(nv, -1);
+    int64_t ncomp = 0;
+    {
+      std::vector<int64_t> st;
+      for (int64_t s = 0; s < nv; ++s) {
+        if (label[s] >= 0) continue;
+        label[s] = ncomp;
+        st.push_back(s);
+        while (!st.empty()) {
+          const int64_t u = st.back();
+          st.pop_back();
+          for (int64_t e = lp[u]; e < lp[u + 1]; ++e)
+            if (label[li[e]] < 0) {
+              label[li[e]] = ncomp;
+              st.push_back(li[e]);
+            }
+        }
+        ++ncomp;
+      }
+    }
+    if (ncomp > 1) {
+      std::vector<int64_t> size(ncomp, 0), order(ncomp);
+      for (int64_t i = 0; i < nv; ++i) ++size[label[i]];
+      for (int64_t c = 0; c < ncomp; ++c) order[c] = c;
+      std::stable_sort(order.begin(), order.end(),
+                       [&](int64_t a, int64_t b) { return size[a] > size[b]; });
+      std::vector<int8_t> side(ncomp, 0);
+      int64_t n1 = 0, n2 = 0;
+      for (int64_t c : order) {
+        if (n1 <= n2) {
+          side[c] = 1;
+          n1 += size[c];
+        } else {
+          side[c] = 2;
+          n2 += size[c];
+        }
+      }
+      for (int64_t i = 0; i < nv; ++i) (side[label[i]] == 1 ? p1 : p2).push_back(verts[i]);
+      return;
+    }
+    std::vector<int64_t> d0, dist;
+    bfs(lp, li, 0, d0);
+    const int64_t far = *std::max_element(d0.begin(), d0.end());
+    int64_t seed = 0;
+    while (d0[seed] != far) ++seed;
+    bfs(lp, li, seed, dist);
+    const int64_t nlev = *std::max_element(dist.begin(), dist.end()) + 1;
+    if (nlev == 1) {
+      sep = verts;
+      return;
+    }
+    std::vector<int64_t> width(nlev, 0);
+    for (int64_t i = 0; i < nv; ++i) ++width[dist[i]];
+    // order = vertices sorted by (dist, index): counting sort keeps index order
+    std::vector<int64_t> start(nlev + 1, 0), order(nv);
+    for (int64_t l = 0; l < nlev; ++l) start[l + 1] = start[l] + width[l];
+    {
+      std::vector<int64_t> fill(start.begin(), start.end() - 1);
+      for (int64_t i = 0; i < nv; ++i) order[fill[dist[i]]++] = i;
+    }
+    // bounds[j] = start[j+1]; estimated part 2 = nv - bounds[j] - width[j+1]
+    int64_t jbest = 0, best = -1;
+    for (int64_t j = 0; j + 1 < nlev; ++j) {
+      const int64_t b = start[j + 1];
+      const int64_t est = nv - b - width[j + 1];
+      const int64_t gap = b > est ? b - est : est - b;
+      if (best < 0 || gap < best) {
+        best = gap;
+        jbest = j;
+      }
+    }
+    const int64_t cut = start[jbest + 1];
+    std::vector<int8_t> part(nv, 0);  // 0 = part 2, 1 = part 1, 3 = separator
+    for (int64_t i = 0; i < cut; ++i) part[order[i]] = 1;
+    const int64_t w = width[jbest + 1];
+    const int64_t deficit = (nv - w) / 2 - cut;
+    if (deficit > 0 && w > 1) {
+      // level jbest+1 is already in index order inside `order`
+      const int64_t take = std::min(deficit, w - 1);
+      for (int64_t i = 0; i < take; ++i) part[order[cut + i]] = 1;
+    }
+    for (int64_t u = 0; u < nv; ++u) {
+      if (part[u] != 1) continue;
+      for (int64_t e = lp[u]; e < lp[u + 1]; ++e)
+        if (part[li[e]] == 0) part[li[e]] = 3;
+    }
+    bool any2 = false, anysep = false;
+    for (int64_t u = 0; u < nv; ++u) {
+      any2 |= part[u] == 0;
+      anysep |= part[u] == 3;
+    }
+    if (any2 && anysep) {
+      std::vector<int64_t> back;
+      for (int64_t u = 0; u < nv; ++u) {
+        if (part[u] != 3) continue;
+        bool hit = false;
+        for (int64_t e = lp[u]; e < lp[u + 1] && !hit; ++e) hit = part[li[e]] == 0;
+        if (!hit) back.push_back(u);
+      }
+      for (int64_t u : back) part[u] = 1;
+    }
+    for (int64_t u = 0; u < nv; ++u) {
+      if (part[u] == 1) p1.push_back(verts[u]);
+      else if (part[u] == 0) p2.push_back(verts[u]);
+      else sep.push_back(verts[u]);
+    }
+  }
+};
+
+struct Builder {
+  Splitter sp;
+  int levels;
+  std::vector<int64_t> dofs;
+  std::vector<int64_t> cptr{0};
+  std::vector<int32_t> depth;
+  Builder(const Graph& g, int64_t n, int lv) : sp(g, n), levels(lv) {}
+
+  void emit(const std::vector<int64_t>& v, int d) {
+    dofs.insert(dofs.end(), v.begin(), v.end());
+    cptr.push_back((int64_t)dofs.size());
+    depth.push_back(d);
+  }
+
+  void recurse(const std::vector<int64_t>& verts, int d) {
+    if (verts.empty()) return;
+    if (d == levels || verts.size() < 6) {
+      emit(verts, levels);
+      return;
+    }
+    std::vector<int64_t> p1, p2, sep;
+    sp.bisect(verts, p1, p2, sep);
+    if (sep.empty() && (p1.empty() || p2.empty())) {
+      emit(verts, levels);
+      return;
+    }
+    if (!sep.empty()) emit(sep, d);
+    recurse(p1, d + 1);
+    recurse(p2, d + 1);
+  }
+};
+
+}  // namespace
+
+extern "C" {
+
+// Nested-dissection hierarchy of the graph of a CSR matrix (both triangles).
+// Outputs: dofs_out[n] = cluster dofs concatenated in id order,
+// cptr_out[n+1] = cluster boundaries, depth_out[n] = cluster depths,
+// ncl_out[0] = number of clusters.  Returns 0 (or -1 on bad input).
+int spand_nd_partition(int64_t n, const int64_t* row_ptr, const int64_t* col_idx,
+                       int levels, int64_t* dofs_out, int64_t* cptr_out,
+                       int32_t* depth_out, int64_t* ncl_out) {
+  if (n < 0 || levels < 0) return -1;
+  Graph g;
+  g.ptr.assign(n + 1, 0);
+  for (int64_t r = 0; r < n; ++r) {
+    int64_t c = 0;
+    for (int64_t e = row_ptr[r]; e < row_ptr[r + 1]; ++e) c += col_idx[e] != r;
+    g.ptr[r + 1] = g.ptr[r] + c;
+  }
+  g.idx.resize(g.ptr[n]);
+  for (int64_t r = 0, k = 0; r < n; ++r)
+    for (int64_t e = row_ptr[r]; e < row_ptr[r + 1]; ++e)
+      if (col_idx[e] != r) g.idx[k++] = col_idx[e];
+  Builder b(g, n, levels);
+  std::vector<int64_t> all(n);
+  for (int64_t i = 0; i < n; ++i) all[i] = i;
+  b.recurse(all, 0);
+  const int64_t ncl = (int64_t)b.depth.size();
+  for (int64_t i = 0; i < n; ++i) dofs_out[i] = b.dofs[i];
+  for (int64_t i = 0; i <= ncl; ++i) cptr_out[i] = b.cptr[i];
+  for (int64_t i = 0; i < ncl; ++i) depth_out[i] = b.depth[i];
+  ncl_out[0] = ncl;
+  return 0;
+}
+
+}  // extern "C"

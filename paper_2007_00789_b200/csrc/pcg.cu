@@ -1,0 +1,173 @@
+// CSR SpMV and the fused PCG vector kernels (replace scipy csr_matvec,
+// sparse.py:64-68, and the NumPy algebra of krylov.py:93-131).
+// All reductions are two-stage with a fixed order: results are bitwise
+// reproducible run to run.
+#include "common.cuh"
+#include "../../include/spand_b200.h"
+
+namespace {
+constexpr int kVecThreads = 256;
+constexpr int kVecBlocksMax = 1184;  // 8 x 148 SMs
+
+int vec_blocks(int n) {
+  int b = (n + kVecThreads - 1) / kVecThreads;
+  return b < 1 ? 1 : (b > kVecBlocksMax ? kVecBlocksMax : b);
+}
+
+// one warp per row; lanes stride the row's nonzeros (rows have 5-81 entries)
+constexpr int kSpmvThreads = 256;
+constexpr int kRowsPerBlock = kSpmvThreads / 32;
+
+__global__ void __launch_bounds__(kSpmvThreads)
+spmv_kernel(int n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
+            const double* __restrict__ va, const double* __restrict__ x,
+            double* __restrict__ y, double* __restrict__ pdot) {
+  __shared__ double sh[kRowsPerBlock];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int row = blockIdx.x * kRowsPerBlock + w;
+  double dotc = 0.0;
+  if (row < n) {
+    const int b = __ldg(rp + row), e = __ldg(rp + row + 1);
+    double s = 0.0;
+    for (int k = b + lane; k < e; k += 32) s += __ldg(va + k) * __ldg(x + __ldg(ci + k));
+    s = warp_sum(s);
+    if (lane == 0) {
+      y[row] = s;
+      dotc = s * __ldg(x + row);
+    }
+  }
+  if (pdot) {
+    if (lane == 0) sh[w] = dotc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = 0.0;
+      for (int i = 0; i < kRowsPerBlock; ++i) t += sh[i];
+      pdot[blockIdx.x] = t;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kVecThreads)
+dot_kernel(int n, const double* __restrict__ x, const double* __restrict__ y,
+           double* __restrict__ part) {
+  __shared__ double sh[32];
+  double s = 0.0;
+  for (int i = blockIdx.x * kVecThreads + threadIdx.x; i < n; i += gridDim.x * kVecThreads)
+    s += x[i] * y[i];
+  s = block_sum<kVecThreads>(s, sh);
+  if (threadIdx.x == 0) part[blockIdx.x] = s;
+}
+
+__global__ void __launch_bounds__(1024) reduce_kernel(int np, const double* __restrict__ part,
+                                                      double* __restrict__ out) {
+  __shared__ double sh[32];
+  double s = 0.0;
+  for (int i = threadIdx.x; i < np; i += 1024) s += part[i];
+  s = block_sum<1024>(s, sh);
+  if (threadIdx.x == 0) out[0] = s;
+}
+
+__global__ void __launch_bounds__(kVecThreads)
+pcg_xr_kernel(int n, const double* __restrict__ scal, double* __restrict__ x,
+              double* __restrict__ r, const double* __restrict__ p,
+              const double* __restrict__ ap, double* __restrict__ part) {
+  __shared__ double sh[32];
+  const double alpha = scal[0] / scal[1];
+  double s = 0.0;
+  for (int i = blockIdx.x * kVecThreads + threadIdx.x; i < n; i += gridDim.x * kVecThreads) {
+    x[i] += alpha * p[i];
+    const double ri = r[i] - alpha * ap[i];
+    r[i] = ri;
+    s += ri * ri;
+  }
+  s = block_sum<kVecThreads>(s, sh);
+  if (threadIdx.x == 0) part[blockIdx.x] = s;
+}
+
+__global__ void __launch_bounds__(kVecThreads)
+pcg_p_kernel(int n, const double* __restrict__ scal, const double* __restrict__ z,
+             double* __restrict__ p) {
+  const double beta = scal[2] / scal[0];
+  for (int i = blockIdx.x * kVecThreads + threadIdx.x; i < n; i += gridDim.x * kVecThreads)
+    p[i] = z[i] + beta * p[i];
+}
+
+__global__ void gather_kernel(int n, const int32_t* __restrict__ perm,
+                              const double* __restrict__ x, double* __restrict__ y) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    y[i] = x[perm[i]];
+}
+__global__ void scatter_kernel(int n, const int32_t* __restrict__ perm,
+                               const double* __restrict__ x, double* __restrict__ y) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    y[perm[i]] = x[i];
+}
+}  // namespace
+
+extern "C" {
+
+int spand_version(void) { return 1; }
+
+int spand_device_sm_count(void) {
+  int dev = 0, sms = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return -1;
+  if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return -1;
+  return sms;
+}
+
+int spand_spmv_blocks(int n) { return (n + kRowsPerBlock - 1) / kRowsPerBlock; }
+
+int spand_csr_spmv(int n, const int32_t* rp, const int32_t* ci, const double* va,
+                   const double* x, double* y, double* pdot, void* stream) {
+  if (n < 0) return -1;
+  if (n == 0) return 0;
+  spmv_kernel<<<spand_spmv_blocks(n), kSpmvThreads, 0, as_stream(stream)>>>(n, rp, ci, va, x, y, pdot);
+  SPAND_CHECK_LAUNCH();
+  return 0;
+}
+
+int spand_dot_blocks(int n) { return vec_blocks(n); }
+
+int spand_dot(int n, const double* x, const double* y, double* part, double* out, void* stream) {
+  if (n < 0) return -1;
+  const int nb = vec_blocks(n);
+  dot_kernel<<<nb, kVecThreads, 0, as_stream(stream)>>>(n, x, y, part);
+  reduce_kernel<<<1, 1024, 0, as_stream(stream)>>>(nb, part, out);
+  SPAND_CHECK_LAUNCH();
+  return 0;
+}
+
+int spand_reduce_sum(int np, const double* part, double* out, void* stream) {
+  reduce_kernel<<<1, 1024, 0, as_stream(stream)>>>(np, part, out);
+  SPAND_CHECK_LAUNCH();
+  return 0;
+}
+
+int spand_pcg_xr(int n, const double* scal, double* x, double* r, const double* p,
+                 const double* ap, double* part, void* stream) {
+  pcg_xr_kernel<<<vec_blocks(n), kVecThreads, 0, as_stream(stream)>>>(n, scal, x, r, p, ap, part);
+  SPAND_CHECK_LAUNCH();
+  return 0;
+}
+
+int spand_pcg_p(int n, const double* scal, const double* z, double* p, void* stream) {
+  pcg_p_kernel<<<vec_blocks(n), kVecThreads, 0, as_stream(stream)>>>(n, scal, z, p);
+  SPAND_CHECK_LAUNCH();
+  return 0;
+}
+
+int spand_gather(int n, const int32_t* perm, const double* x, double* y, void* stream) {
+  if (n <= 0) return n < 0 ? -1 : 0;
+  gather_kernel<<<vec_blocks(n), kVecThreads, 0, as_stream(stream)>>>(n, perm, x, y);
+  SPAND_CHECK_LAUNCH();
+  return 0;
+}
+
+int spand_scatter_perm(int n, const int32_t* perm, const double* x, double* y, void* stream) {
+  if (n <= 0) return n < 0 ? -1 : 0;
+  scatter_kernel<<<vec_blocks(n), kVecThreads, 0, as_stream(stream)>>>(n, perm, x, y);
+  SPAND_CHECK_LAUNCH();
+  return 0;
+}
+
+}  // extern "C"

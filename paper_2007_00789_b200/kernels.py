@@ -1,0 +1,163 @@
+"""Thin Python wrappers over the batched C-ABI kernels.
+
+``Geometry`` holds the device ``m0``/``off`` arrays that every batched
+factorization kernel reads (see include/spand_b200.h): real clusters plus
+"virtual" clusters for workspaces and one-off matrices.  ``*_one`` helpers
+run a single task (the reference's per-block dense API in ``dense.py``).
+"""
+
+import numpy as np
+
+from . import _lib
+from .device import dev, ptr, require_cuda, stream, to_dev
+
+
+def opnd(p, rc, cc, rskip=0, cskip=0, rcount=-1, ccount=-1):
+    """Operand row (7 int64): see include/spand_b200.h."""
+    return [int(p), int(rc), int(cc), int(rskip), int(cskip), int(rcount),
+            int(ccount)]
+
+
+class Geometry:
+    """Device geometry table (int32 m0 and off)."""
+
+    def __init__(self, m0, off=None):
+        t = require_cuda()
+        m0 = np.asarray(m0, dtype=np.int32)
+        self.m0_host = m0.copy()
+        self.m0 = to_dev(m0, np.int32)
+        self.off = (to_dev(np.asarray(off, np.int32), np.int32) if off is not None
+                    else t.zeros(m0.size, dtype=t.int32, device=dev()))
+
+    @classmethod
+    def virtual(cls, sizes):
+        return cls(np.asarray(sizes, dtype=np.int32))
+
+
+def _rows(rows, width):
+    return to_dev(np.asarray(rows, dtype=np.int64).reshape(-1, width))
+
+
+def potrf_batched(geo, ops, info):
+    n = len(ops)
+    if n == 0:
+        return
+    d = _rows(ops, 7)
+    _lib.call("spand_potrf_batched", n, ptr(d), ptr(geo.m0), ptr(geo.off),
+              ptr(info), stream())
+
+
+def trtri_batched(geo, pairs):
+    n = len(pairs)
+    if n == 0:
+        return
+    d = _rows([a + b for a, b in pairs], 14)
+    _lib.call("spand_trtri_batched", n, ptr(d), ptr(geo.m0), ptr(geo.off),
+              stream())
+
+
+def copy_batched(geo, tasks):
+    """tasks: [(src operand, dst operand, mode)]"""
+    n = len(tasks)
+    if n == 0:
+        return
+    d = _rows([a + b + [m] for a, b, m in tasks], 15)
+    _lib.call("spand_copy_batched", n, ptr(d), ptr(geo.m0), ptr(geo.off),
+              stream())
+
+
+TILE = 64
+
+
+def gemm_grouped(geo, targets, alpha, beta, bT, lower_only=False,
+                 max_rows=None, max_cols=None):
+    """targets: [(C operand, [(A operand, B operand), ...], (max_m, max_n))].
+
+    Tiles are laid out for the maximal (m0-geometry) sizes; tiles beyond a
+    target's live size exit immediately on the device."""
+    if not targets:
+        return
+    trow, srow, tiles = [], [], []
+    for t, (c, segs, (mm, nn)) in enumerate(targets):
+        trow.append(c + [len(srow)])
+        for a, b in segs:
+            srow.append(a + b)
+        for i in range(0, max(mm, 0), TILE):
+            for j in range(0, max(nn, 0), TILE):
+                if lower_only and j > i:
+                    continue
+                tiles.append([t, i, j])
+    trow.append([0] * 7 + [len(srow)])
+    if not tiles:
+        return
+    if not srow:
+        srow.append([0] * 14)
+    td, sd, tl = _rows(trow, 8), _rows(srow, 14), _rows(tiles, 3)
+    _lib.call("spand_gemm_grouped", len(tiles), ptr(tl), ptr(td), ptr(sd),
+              ptr(geo.m0), ptr(geo.off), float(alpha), float(beta), int(bT),
+              int(bool(lower_only)), stream())
+
+
+# ---------------------------------------------------------------------------
+# single-task helpers for the reference's dense API
+
+
+def _colmajor_upload(a):
+    return to_dev(np.ascontiguousarray(np.asarray(a, dtype=np.float64).T).ravel())
+
+
+def _download(buf, rows, cols):
+    return buf[:rows * cols].cpu().numpy().reshape(cols, rows).T.copy()
+
+
+def potrf_one(a):
+    t = require_cuda()
+    n = a.shape[0]
+    geo = Geometry.virtual([n])
+    buf = _colmajor_upload(a)
+    info = t.zeros(1, dtype=t.int32, device=dev())
+    potrf_batched(geo, [opnd(buf.data_ptr(), 0, 0)], info)
+    return _download(buf, n, n), int(info.item())
+
+
+def trtri_one(l):
+    t = require_cuda()
+    n = l.shape[0]
+    geo = Geometry.virtual([n])
+    src = _colmajor_upload(l)
+    dst = t.zeros(n * n, dtype=t.float64, device=dev())
+    trtri_batched(geo, [(opnd(src.data_ptr(), 0, 0), opnd(dst.data_ptr(), 0, 0))])
+    return _download(dst, n, n)
+
+
+def gemm_one(a, b, trans_a=False, trans_b=False):
+    """C = op(A) op(B) on the DMMA GEMM (A, B host arrays)."""
+    t = require_cuda()
+    a = np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    if trans_a:
+        a = a.T
+    m, k = a.shape
+    k2, nn = (b.shape[1], b.shape[0]) if trans_b else b.shape
+    if k != k2:
+        raise ValueError("inner dimensions differ")
+    geo = Geometry.virtual([m, k, nn])
+    ad = _colmajor_upload(a)                     # m x k
+    if trans_b:
+        bd = _colmajor_upload(b)                 # n x k  ("NT")
+        bop = opnd(bd.data_ptr(), 2, 1)
+        bT = 1
+    else:
+        bd = _colmajor_upload(b)                 # k x n  ("NN")
+        bop = opnd(bd.data_ptr(), 1, 2)
+        bT = 0
+    cd = t.zeros(max(m * nn, 1), dtype=t.float64, device=dev())
+    gemm_grouped(geo, [(opnd(cd.data_ptr(), 0, 2),
+                        [(opnd(ad.data_ptr(), 0, 1), bop)], (m, nn))],
+                 1.0, 0.0, bT)
+    return _download(cd, m, nn)
+
+
+def rrqr_one(a, eps, scheme):
+    from .rrqr import rrqr_single
+    return rrqr_single(a, eps, scheme)
