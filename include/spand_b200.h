@@ -129,20 +129,34 @@ int spand_gemm_grouped(int ntile, const int64_t* tiles, const int64_t* targets,
                        const int32_t* off, double alpha, double beta, int bT,
                        int lower_only, void* stream);
 
-/* Batched early-stopping column-pivoted Householder QR of interface panels
- * (restates dense.py:117-222, schemes.py:272-318, factorize.py:175-196).
- * See rrqr.cu for the task/neighbour row layouts. */
-int spand_rrqr_wave(int npanel, const int64_t* panels, const int64_t* nbrs,
-                    int32_t* m0, int32_t* off, double eps, int scheme,
-                    int64_t* events, double* work, void* stream);
+/* One wave of the batched early-stopping column-pivoted Householder QR of
+ * interface panels (restates dense.py:117-222, schemes.py:272-318,
+ * factorize.py:175-196): gathers each panel from its blocks, factors it with
+ * a co-resident group of CTAs (cooperative launch of `grid` CTAs), writes
+ * R's coarse rows (and the kept correction rows) back into the blocks, Q
+ * into its buffer, advances off[p] by the fine count and records an event.
+ * scheme: 0 first, 1 second-full, 2 second-superfine.  vmax: largest live
+ * panel height in the wave (<= 6144).  Row layouts: see rrqr.cu. */
+int spand_rrqr_wave(int npanel, int grid, int vmax, const int64_t* panels,
+                    const int64_t* nbrs, int32_t* m0, int32_t* off, double eps,
+                    int scheme, int64_t* events, void* stream);
 int spand_rrqr_cta_count(void);
 
 /* Final dense block (factorize.py:198-220): assemble the live parts of the
- * remaining clusters into one square operand. */
+ * remaining clusters (cl[ncl] cluster ids, ascending) into the virtual
+ * cluster final_id's m0^2 buffer `dst` (zeroed by the caller), packed at the
+ * bottom-right; sets off[final_id].  block rows (4 int64): {index of ci in
+ * cl, index of cj in cl, block ptr, 0} for stored blocks (ci <= cj). */
 int spand_assemble_final(int ncl, const int64_t* cl, int64_t nblk,
                          const int64_t* blocks, const int32_t* m0,
                          int32_t* off, int32_t final_id, double* dst,
                          void* stream);
+
+/* Nonzero counts of stored payload windows: view rows {ptr, ld, rows, cols};
+ * out[i] += count (zeroed by the caller).  (count_nonzero of the reference's
+ * nnz properties, schemes.py:114-117,142-144,168-170,194-196.) */
+int spand_count_nonzero(int nview, const int64_t* views, unsigned long long* out,
+                        void* stream);
 
 /* ---- host-side integer structure (partition.py:118-268) ------------------ */
 

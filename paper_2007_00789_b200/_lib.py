@@ -36,9 +36,10 @@ SIGNATURES = {
     "spand_copy_batched": [_c_int, _P, _P, _P, _P],
     "spand_gemm_grouped": [_c_int, _P, _P, _P, _P, _P, _c_dbl, _c_dbl, _c_int,
                            _c_int, _P],
-    "spand_rrqr_wave": [_c_int, _P, _P, _P, _P, _c_dbl, _c_int, _P, _P, _P],
+    "spand_rrqr_wave": [_c_int, _c_int, _c_int, _P, _P, _P, _P, _c_dbl, _c_int, _P, _P],
     "spand_rrqr_cta_count": [],
     "spand_assemble_final": [_c_int, _P, _c_i64, _P, _P, _P, _c_int, _P, _P],
+    "spand_count_nonzero": [_c_int, _P, _P, _P],
     "spand_nd_partition": [_c_i64, _P, _P, _c_int, _P, _P, _P, _P],
 }
 

@@ -189,3 +189,89 @@ int spand_copy_batched(int ntask, const int64_t* ops, const int32_t* m0, const i
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Final dense block (factorize.py:198-220) and payload nonzero counts
+// (schemes.py:114-117,142-144,168-170,194-196).
+namespace {
+// cl rows: {cluster id}; block rows (4 int64): {ci index in cl, cj index in cl, ptr, 0}
+__global__ void __launch_bounds__(kT)
+assemble_kernel(int ncl, const int64_t* __restrict__ cl, const int64_t* __restrict__ blocks,
+                const int32_t* __restrict__ m0, const int32_t* __restrict__ off, int fid,
+                double* __restrict__ dst) {
+  const int cap = m0[fid];
+  const int64_t* br = blocks + 4 * (int64_t)blockIdx.x;
+  const int a = (int)br[0], b = (int)br[1];
+  const double* src = reinterpret_cast<const double*>(br[2]);
+  int total = 0, pa = 0, pb = 0;
+  for (int t = 0; t < ncl; ++t) {
+    const int c = (int)cl[t];
+    if (t == a) pa = total;
+    if (t == b) pb = total;
+    total += m0[c] - off[c];
+  }
+  const int base = cap - total;
+  const int ca = (int)cl[a], cb = (int)cl[b];
+  const int ra = m0[ca] - off[ca], rb = m0[cb] - off[cb];
+  const int lda = m0[ca];
+  for (int64_t e = threadIdx.x; e < (int64_t)ra * rb; e += kT) {
+    const int r = (int)(e % ra), c = (int)(e / ra);
+    const double v = src[(int64_t)(off[ca] + r) + (int64_t)(off[cb] + c) * lda];
+    dst[(int64_t)(base + pa + r) + (int64_t)(base + pb + c) * cap] = v;
+    if (a != b) dst[(int64_t)(base + pb + c) + (int64_t)(base + pa + r) * cap] = v;
+  }
+}
+
+__global__ void set_off_kernel(int ncl, const int64_t* __restrict__ cl, const int32_t* __restrict__ m0,
+                               int32_t* __restrict__ off, int fid) {
+  int total = 0;
+  for (int t = 0; t < ncl; ++t) {
+    const int c = (int)cl[t];
+    total += m0[c] - off[c];
+  }
+  off[fid] = m0[fid] - total;
+}
+
+// view rows (4 int64): {ptr, ld, rows, cols}; out[i] = nonzero count
+__global__ void __launch_bounds__(kT)
+count_kernel(const int64_t* __restrict__ views, unsigned long long* __restrict__ out) {
+  const int64_t* v = views + 4 * (int64_t)blockIdx.x;
+  const double* p = reinterpret_cast<const double*>(v[0]);
+  const int64_t ld = v[1], rows = v[2], cols = v[3];
+  unsigned long long c = 0;
+  for (int64_t e = (int64_t)blockIdx.y * kT + threadIdx.x; e < rows * cols; e += (int64_t)gridDim.y * kT) {
+    const int64_t r = e % rows, q = e / rows;
+    c += p[r + q * ld] != 0.0;
+  }
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(out + blockIdx.x, c);
+}
+}  // namespace
+
+extern "C" {
+
+int spand_assemble_final(int ncl, const int64_t* cl, int64_t nblk, const int64_t* blocks,
+                         const int32_t* m0, int32_t* off, int32_t final_id, double* dst,
+                         void* stream) {
+  if (ncl < 0 || nblk < 0) return -1;
+  if (ncl == 0) return 0;
+  // off[final_id] = m0[final_id] - (sum of live sizes): the live parts are
+  // packed at the bottom-right of the m0[final_id]^2 buffer
+  set_off_kernel<<<1, 1, 0, as_stream(stream)>>>(ncl, cl, m0, off, final_id);
+  if (nblk > 0)
+    assemble_kernel<<<(unsigned)nblk, kT, 0, as_stream(stream)>>>(ncl, cl, blocks, m0, off,
+                                                                  final_id, dst);
+  SPAND_CHECK_LAUNCH();
+  return 0;
+}
+
+int spand_count_nonzero(int nview, const int64_t* views, unsigned long long* out, void* stream) {
+  if (nview < 0) return -1;
+  if (nview == 0) return 0;
+  dim3 grid(nview, 4);
+  count_kernel<<<grid, kT, 0, as_stream(stream)>>>(views, out);
+  SPAND_CHECK_LAUNCH();
+  return 0;
+}
+
+}  // extern "C"

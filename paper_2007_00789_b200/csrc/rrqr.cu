@@ -1,0 +1,473 @@
+// Batched early-stopping column-pivoted Householder QR of interface panels:
+// the sparsification step.  Restates, per panel,
+//   _rrqr_core      /root/reference/pkg/src/spdkit/dense.py:117-183
+//   rrqr_sparsify   dense.py:186-222
+//   make_sparsification + EliminationState.sparsify
+//                   schemes.py:272-318, factorize.py:175-196
+//
+// One launch processes one WAVE of interfaces (no two of them are
+// neighbours, so they are independent).  Every panel gets a GROUP of CTAs
+// that together run the pivoted QR with one group barrier per elimination
+// step; the launch is cooperative so all groups are co-resident.  The
+// panel's columns are split in contiguous ranges over the group's CTAs and
+// never move: pivoting is bookkeeping (perm / pos arrays), exactly the
+// reference's swap order, so ties resolve to the smallest CURRENT position
+// like np.argmax on the swapped norms.  Per step, a CTA updates its own
+// columns with the Householder reflector (one warp per column: dot, rank-1
+// update, row-k entry, exact tail norm), downdates the running norms with
+// the reference's 0.01 refresh rule, and proposes its local argmax; the
+// reflector is rebuilt redundantly in every CTA from the winning column,
+// and Q (= H_0 H_1 ...) is updated row-parallel.
+//
+// Deciding values (eta, r11, stop test, coarse test) follow the reference
+// formulas; only summation order differs, so ranks match except within
+// ~1e-15 relative of a threshold (the events record the margins).
+#include <cooperative_groups.h>
+
+#include "common.cuh"
+#include "../../include/spand_b200.h"
+
+namespace {
+constexpr int kT = 256;
+constexpr int kWarps = kT / 32;
+constexpr int kMaxM = 6144;  // v in shared memory
+
+// panel row (16 int64):
+//  0 p        1 nbr_begin  2 nbr_end   3 W (double*, temp, >= m*n)
+//  4 Q (double*, m*m, compact ld = m)  5 aux (double*)  6 iaux (int32*)
+//  7 group_begin  8 group_size  9 counter (uint32*)  10 event slot
+//  11 ncap (column capacity of aux arrays)  12 mcap  13-15 unused
+// nbr row (4 int64): {w, block ptr, orientation, 0}
+//  orientation 0: block (p, w) stored with rows of p (ld = m0[p])
+//  orientation 1: block (w, p) stored with rows of w (ld = m0[w])
+// event row (12 int64): {p, m, n, k_stop, k_c, rank_f2, n_fine,
+//  bits(eta_stop), bits(r11), 0, 0, 0}
+
+struct Sh {
+  double red[kWarps];
+  double bval[kWarps];
+  int64_t bpos[kWarps];
+  int bcol[kWarps];
+  int nb_start[65];  // column start of each neighbour (first 64)
+};
+
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void group_barrier(unsigned* ctr, int G, unsigned& gen) {
+  __syncthreads();
+  if (G > 1) {
+    if (threadIdx.x == 0) {
+      __threadfence();
+      ++gen;
+      atomicAdd(ctr, 1u);
+      const unsigned target = gen * (unsigned)G;
+      while (ld_acquire(ctr) < target) {
+      }
+      __threadfence();
+    }
+    __syncthreads();
+  }
+}
+
+// better(a, b): larger value wins, ties -> smaller position
+__device__ __forceinline__ bool better(double va, int64_t pa, double vb, int64_t pb) {
+  return va > vb || (va == vb && pa < pb);
+}
+
+__global__ void __launch_bounds__(kT)
+rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* __restrict__ nbrs,
+                 int32_t* __restrict__ m0, int32_t* __restrict__ off, double eps, int scheme,
+                 int64_t* __restrict__ events) {
+  extern __shared__ double vsh[];
+  __shared__ Sh sh;
+  __shared__ double tile[kWarps][16][33];
+  // ---- locate my panel and rank in its group
+  int lo = 0, hi = npanel - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (panels[16 * (int64_t)mid + 7] <= blockIdx.x) lo = mid;
+    else hi = mid - 1;
+  }
+  const int64_t* P = panels + 16 * (int64_t)lo;
+  const int G = (int)P[8];
+  const int rank = (int)blockIdx.x - (int)P[7];
+  if (rank >= G) return;
+  const int p = (int)P[0];
+  const int nb0 = (int)P[1], nb1 = (int)P[2];
+  double* W = reinterpret_cast<double*>(P[3]);
+  double* Q = reinterpret_cast<double*>(P[4]);
+  double* aux = reinterpret_cast<double*>(P[5]);
+  int32_t* iaux = reinterpret_cast<int32_t*>(P[6]);
+  unsigned* ctr = reinterpret_cast<unsigned*>(P[9]);
+  const int64_t slot = P[10];
+  const int64_t ncap = P[11], mcap = P[12];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  unsigned gen = 0;
+
+  const int offp = off[p];
+  const int ldp = m0[p];
+  const int m = ldp - offp;
+  // column layout over neighbours (live columns at kernel start)
+  int n = 0;
+  const int nnb = nb1 - nb0;
+  for (int j = 0; j < nnb; ++j) {
+    const int w = (int)nbrs[4 * (int64_t)(nb0 + j)];
+    if (j < 64 && tid == 0) sh.nb_start[j] = n;
+    n += m0[w] - off[w];
+  }
+  if (tid == 0 && nnb <= 64) sh.nb_start[nnb] = n;
+  __syncthreads();
+
+  double* cur = aux;
+  double* ref = aux + ncap;
+  double* piv = aux + 2 * ncap;
+  // candidates, double-buffered by step parity: value, position, column
+  double* cand_v = aux + 2 * ncap + mcap;                      // 2G values
+  int64_t* cand_p = reinterpret_cast<int64_t*>(cand_v + 2 * G);  // 2G (pos << 32 | col)
+  double* betas = reinterpret_cast<double*>(cand_p + 2 * G);   // mcap
+  int32_t* perm = iaux;
+  int32_t* pos = iaux + ncap;
+  int32_t* done = iaux + 2 * ncap;
+
+  const int c0 = (int)(((int64_t)n * rank) / G), c1 = (int)(((int64_t)n * (rank + 1)) / G);
+  const int r0 = (int)(((int64_t)m * rank) / G), r1 = (int)(((int64_t)m * (rank + 1)) / G);
+  const int kmax = m < n ? m : n;
+
+  // neighbour of column c (linear scan; <= a few dozen neighbours)
+  auto nbr_of = [&](int c, int& j, int& cc) {
+    int jj = 0, start = 0;
+    if (nnb <= 64) {
+      while (jj + 1 < nnb && sh.nb_start[jj + 1] <= c) ++jj;
+      start = sh.nb_start[jj];
+    } else {
+      int s = 0;
+      for (jj = 0; jj < nnb; ++jj) {
+        const int w = (int)nbrs[4 * (int64_t)(nb0 + jj)];
+        const int len = m0[w] - off[w];
+        if (c < s + len) break;
+        s += len;
+      }
+      start = s;
+    }
+    j = jj;
+    cc = c - start;
+  };
+
+  // ---- gather my columns of the panel into W (ld = m), 32x32 tiles per warp
+  {
+    const int ntc = (c1 - c0 + 15) / 16, ntr = (m + 31) / 32;
+    for (int tix = warp; tix < ntc * ntr; tix += kWarps) {
+      const int tc = c0 + (tix / ntr) * 16, tr = (tix % ntr) * 32;
+      for (int q = 0; q < 16; ++q) {
+        const int c = tc + q;
+        double val = 0.0;
+        if (c < c1) {
+          int j, cc;
+          nbr_of(c, j, cc);
+          const int64_t* nr = nbrs + 4 * (int64_t)(nb0 + j);
+          const int w = (int)nr[0];
+          const double* blk = reinterpret_cast<const double*>(nr[1]);
+          const int i = tr + lane;
+          if (i < m) {
+            if (nr[2] == 0) val = blk[(int64_t)(offp + i) + (int64_t)(off[w] + cc) * ldp];
+            else val = blk[(int64_t)(off[w] + cc) + (int64_t)(offp + i) * m0[w]];
+          }
+        }
+        tile[warp][q][lane] = val;
+      }
+      __syncwarp();
+      for (int q = 0; q < 16; ++q) {
+        const int c = tc + q, i = tr + lane;
+        if (c < c1 && i < m) W[(int64_t)i + (int64_t)c * m] = tile[warp][q][lane];
+      }
+      __syncwarp();
+    }
+  }
+  __syncthreads();
+  // ---- initial norms, positions, local argmax
+  double bv = -1.0;
+  int64_t bp = 0x7fffffffffffLL;
+  int bc = -1;
+  for (int c = c0 + warp; c < c1; c += kWarps) {
+    const double* col = W + (int64_t)c * m;
+    double s = 0.0;
+    for (int i = lane; i < m; i += 32) s += col[i] * col[i];
+    s = warp_sum(s);
+    if (lane == 0) {
+      cur[c] = s;
+      ref[c] = s;
+      pos[c] = c;
+      done[c] = 0;
+      if (better(s, c, bv, bp)) {
+        bv = s;
+        bp = c;
+        bc = c;
+      }
+    }
+  }
+  // Q = I on my rows
+  for (int64_t e = tid; e < (int64_t)(r1 - r0) * m; e += kT) {
+    const int i = r0 + (int)(e % (r1 - r0)), c = (int)(e / (r1 - r0));
+    Q[(int64_t)i + (int64_t)c * m] = (i == c) ? 1.0 : 0.0;
+  }
+  auto publish = [&](double v, int64_t ps, int c, int parity) {
+    if (lane == 0) {
+      sh.bval[warp] = v;
+      sh.bpos[warp] = ps;
+      sh.bcol[warp] = c;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      double vv = sh.bval[0];
+      int64_t pp = sh.bpos[0];
+      int cc = sh.bcol[0];
+      for (int q = 1; q < kWarps; ++q)
+        if (better(sh.bval[q], sh.bpos[q], vv, pp)) {
+          vv = sh.bval[q];
+          pp = sh.bpos[q];
+          cc = sh.bcol[q];
+        }
+      cand_v[parity * G + rank] = vv;
+      cand_p[parity * G + rank] = (pp << 32) | (int64_t)(uint32_t)cc;
+    }
+  };
+  publish(bv, bp, bc, 0);
+  group_barrier(ctr, G, gen);
+
+  const double stop_tol = (scheme == 2) ? eps * eps : eps;
+  double r11 = 0.0, eta_last = 0.0;
+  int k = 0;
+  while (k < kmax) {
+    // ---- winning column: max value, smallest current position
+    double wv = -1.0;
+    int64_t wp = 0x7fffffffffffLL, wpc = 0;
+    const int par = k & 1;
+    for (int q = 0; q < G; ++q) {
+      const double v = __ldcg(cand_v + par * G + q);
+      const int64_t pc = __ldcg(reinterpret_cast<const long long*>(cand_p) + par * G + q);
+      const int64_t ps = pc >> 32;
+      if (better(v, ps, wv, wp)) {
+        wv = v;
+        wp = ps;
+        wpc = pc;
+      }
+    }
+    const int jpos = (int)wp;
+    const int j = (int)(uint32_t)(wpc & 0xffffffffLL);
+    const double* colj = W + (int64_t)j * m;
+    double s = 0.0;
+    for (int i = k + tid; i < m; i += kT) {
+      const double x = __ldcg(colj + i);
+      s += x * x;
+    }
+    const double eta = sqrt(block_sum<kT>(s, sh.red));
+    eta_last = eta;
+    if (k == 0) {
+      r11 = eta;
+      if (r11 == 0.0) break;
+    }
+    if (eta < stop_tol * r11) break;
+    // ---- swap bookkeeping (reference: r[:, [k, j]], perm[[k, j]] ...):
+    // the column at position k moves to j's old position; owners update
+    // their own columns' positions (no shared permutation array)
+    const bool own_j = j >= c0 && j < c1;
+    if (tid == 0) {
+      if (own_j) {
+        pos[j] = k;
+        done[j] = 1;
+      }
+      if (rank == 0) piv[k] = eta;
+    }
+    __syncthreads();
+    for (int c = c0 + tid; c < c1; c += kT)
+      if (c != j && !done[c] && pos[c] == k) pos[c] = jpos;
+    __syncthreads();
+    bv = -1.0;
+    bp = 0x7fffffffffffLL;
+    bc = -1;
+    if (eta > 0.0) {
+      // ---- reflector v = x - beta e1, beta = -sign(x0) eta (dense.py:155-159)
+      const double x0 = __ldcg(colj + k);
+      const double beta = x0 >= 0.0 ? -eta : eta;
+      const int len = m - k;
+      double vv = 0.0;
+      for (int i = tid; i < len; i += kT) {
+        double x = __ldcg(colj + k + i);
+        if (i == 0) x -= beta;
+        vsh[i] = x;
+        vv += x * x;
+      }
+      const double tau = 2.0 / block_sum<kT>(vv, sh.red);
+      if (rank == 0 && tid == 0) betas[k] = beta;
+      __syncthreads();
+      // ---- my columns: apply H_k, row-k entry, norm downdate / refresh
+      for (int c = c0 + warp; c < c1; c += kWarps) {
+        if (c == j) continue;
+        if (done[c]) continue;
+        double* col = W + (int64_t)c * m;
+        double d = 0.0;
+        for (int i = lane; i < len; i += 32) d += vsh[i] * col[k + i];
+        d = warp_sum(d) * tau;
+        double rk = 0.0, tail = 0.0;
+        for (int i = lane; i < len; i += 32) {
+          const double nv = col[k + i] - d * vsh[i];
+          col[k + i] = nv;
+          if (i == 0) rk = nv;
+          else tail += nv * nv;
+        }
+        tail = warp_sum(tail);
+        rk = __shfl_sync(0xffffffffu, rk, 0);
+        if (lane == 0) {
+          double cn = cur[c] - rk * rk;
+          if (cn < 0.0) cn = 0.0;
+          if (cn < 0.01 * ref[c]) {
+            cn = tail;
+            ref[c] = tail;
+          }
+          cur[c] = cn;
+          const int64_t ps = pos[c];
+          if (better(cn, ps, bv, bp)) {
+            bv = cn;
+            bp = ps;
+            bc = c;
+          }
+        }
+      }
+      // ---- Q[:, k:] -= (Q[:, k:] v) v^T tau on my rows
+      for (int i = r0 + tid; i < r1; i += kT) {
+        double t = 0.0;
+        for (int c = 0; c < len; ++c) t += Q[(int64_t)i + (int64_t)(k + c) * m] * vsh[c];
+        t *= tau;
+        for (int c = 0; c < len; ++c) Q[(int64_t)i + (int64_t)(k + c) * m] -= t * vsh[c];
+      }
+    } else {
+      // zero pivot (only when stop_tol * r11 == 0): no reflector
+      if (rank == 0 && tid == 0) betas[k] = 0.0;
+      for (int c = c0 + warp; c < c1; c += kWarps) {
+        if (lane == 0 && c != j && !done[c]) {
+          const int64_t ps = pos[c];
+          if (better(cur[c], ps, bv, bp)) {
+            bv = cur[c];
+            bp = ps;
+            bc = c;
+          }
+        }
+      }
+    }
+    __syncthreads();
+    publish(bv, bp, bc, (k + 1) & 1);
+    ++k;
+    group_barrier(ctr, G, gen);
+  }
+  const int k_stop = k;
+  // all CTAs are done reading pivot columns: finish the pivoted columns of
+  // R (row t = beta_t, zeros below; dense.py:163-164) and the permutation
+  group_barrier(ctr, G, gen);
+  for (int c = c0 + warp; c < c1; c += kWarps) {
+    const int t = pos[c];
+    if (done[c]) {
+      const double bt = __ldcg(betas + t);
+      double* col = W + (int64_t)c * m;
+      if (bt != 0.0)
+        for (int i = t + lane; i < m; i += 32) col[i] = (i == t) ? bt : 0.0;
+    }
+    if (lane == 0) perm[t] = c;
+  }
+  __syncthreads();
+  // k_c: first pivot below eps * r11 (dense.py:181-182)
+  int k_c = k_stop;
+  for (int t = 0; t < k_stop; ++t)
+    if (__ldcg(piv + t) < eps * r11) {
+      k_c = t;
+      break;
+    }
+  const int n_fine = m - k_c;
+  int n_corr = 0;  // rows of e_tilde kept in the dead slots
+  if (scheme == 1) n_corr = n_fine;
+  else if (scheme == 2) n_corr = k_stop - k_c;
+  // ---- write back: new slot s < n_fine <- R row k_c + s (only s < n_corr
+  //      are read later); slot n_fine + t <- R row t (t < k_c)
+  {
+    const int ntc = (c1 - c0 + 15) / 16, ntr = (m + 31) / 32;
+    for (int tix = warp; tix < ntc * ntr; tix += kWarps) {
+      const int tc = c0 + (tix / ntr) * 16, tr = (tix % ntr) * 32;
+      for (int q = 0; q < 16; ++q) {
+        const int c = tc + q, sl = tr + lane;
+        double val = 0.0;
+        if (c < c1 && sl < m) {
+          const int row = sl < n_fine ? k_c + sl : sl - n_fine;
+          val = W[(int64_t)row + (int64_t)c * m];
+        }
+        tile[warp][q][lane] = val;
+      }
+      __syncwarp();
+      for (int q = 0; q < 16; ++q) {
+        const int c = tc + q;
+        if (c >= c1) continue;
+        int j, cc;
+        nbr_of(c, j, cc);
+        const int64_t* nr = nbrs + 4 * (int64_t)(nb0 + j);
+        const int w = (int)nr[0];
+        double* blk = reinterpret_cast<double*>(nr[1]);
+        const int sl = tr + lane;
+        if (sl < m && (sl >= n_fine || sl < n_corr)) {
+          if (nr[2] == 0) blk[(int64_t)(offp + sl) + (int64_t)(off[w] + cc) * ldp] = tile[warp][q][lane];
+          else blk[(int64_t)(off[w] + cc) + (int64_t)(offp + sl) * m0[w]] = tile[warp][q][lane];
+        }
+      }
+      __syncwarp();
+    }
+  }
+  if (rank == 0 && tid == 0) {
+    int64_t* ev = events + 12 * slot;
+    ev[0] = p;
+    ev[1] = m;
+    ev[2] = n;
+    ev[3] = k_stop;
+    ev[4] = k_c;
+    ev[5] = (scheme == 2) ? k_stop - k_c : 0;
+    ev[6] = n_fine;
+    ev[7] = __double_as_longlong(eta_last);
+    ev[8] = __double_as_longlong(r11);
+  }
+  // every CTA of the group must finish reading off[p] before it moves
+  group_barrier(ctr, G, gen);
+  if (rank == 0 && tid == 0) off[p] = offp + n_fine;
+}
+}  // namespace
+
+extern "C" {
+
+int spand_rrqr_cta_count(void) {
+  int dev = 0, sms = 0, per = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return -1;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const size_t smem = kMaxM * sizeof(double);
+  cudaFuncSetAttribute(rrqr_wave_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, rrqr_wave_kernel, kT, smem) != cudaSuccess)
+    return -1;
+  return per * sms;
+}
+
+int spand_rrqr_wave(int npanel, int grid, int vmax, const int64_t* panels, const int64_t* nbrs,
+                    int32_t* m0, int32_t* off, double eps, int scheme, int64_t* events,
+                    void* stream) {
+  if (npanel < 0 || grid < 0 || vmax < 0 || vmax > kMaxM) return -1;
+  if (npanel == 0 || grid == 0) return 0;
+  const size_t smem = (size_t)(vmax > 0 ? vmax : 1) * sizeof(double);
+  cudaError_t e = cudaFuncSetAttribute(rrqr_wave_kernel,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)(kMaxM * sizeof(double)));
+  if (e != cudaSuccess) return (int)e;
+  void* args[] = {&npanel, &panels, &nbrs, &m0, &off, &eps, &scheme, &events};
+  e = cudaLaunchCooperativeKernel((void*)rrqr_wave_kernel, dim3(grid), dim3(kT), args, smem,
+                                  (cudaStream_t)stream);
+  if (e != cudaSuccess) return (int)e;
+  return 0;
+}
+
+}  // extern "C"

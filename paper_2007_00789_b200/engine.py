@@ -1,0 +1,600 @@
+"""Device factorization engine: host level scheduler + batched sm_100a kernels.
+
+Restates the reference driver (`/root/reference/pkg/src/spdkit/factorize.py`
+`EliminationState` :51-239 and `factorize` :285-366) as three stages:
+
+1. SYMBOLIC (host, once).  The block structure of the trailing matrix does
+   not depend on the ranks the sparsification finds (ranks only shrink the
+   live part of a cluster, `dofs[n_fine:]`, factorize.py:187-190), so the
+   whole schedule is computed up front: per level the interior batch, the
+   fill pattern and the grouped Schur targets (every same-level interior
+   adjacent to a target block contributes one K-segment), the rescale batch
+   and the sparsify WAVES (an interface waits for every adjacent interface
+   with a smaller id, factorize.py:323; same-wave interfaces are
+   independent).  Clusters that the reference drops (rank 0) simply have
+   zero live size here; their later operators are filtered at collection.
+
+2. NUMERIC (device, no host round trip).  Every dense matrix lives at its
+   cluster pair's original size in one pool, column-major; the live window
+   is read from the device ``off`` array that the RRQR kernel advances.  Per
+   level: batched potrf -> trtri -> TRSM as DMMA GEMM with the explicit
+   inverse -> one grouped DMMA GEMM for all Schur/fill updates; then (outside
+   the skip window) batched rescale potrf/trtri + two GEMM passes
+   (Z_i^-1 B Z_j^-T); then one cooperative RRQR launch per wave.  Finally
+   the leftover clusters are assembled into one dense block and factored.
+
+3. COLLECT (one sync).  Events (ranks, fine counts) and potrf infos come
+   back; the host replays the offsets to build the operator list in the
+   reference's order with device views of the payloads, the permutation,
+   diagnostics and nnz_factor (counted on the device).
+"""
+
+import hashlib
+import time
+
+import numpy as np
+
+from . import _lib
+from .dense import SCHEME_CODE, SchemeKind
+from .device import dev, ptr, require_cuda, stream, to_dev
+from .errors import NotSPD
+from .kernels import Geometry, TILE, opnd
+from .schemes import (Elimination, ErrorCorrection, MatView, Orthogonal,
+                      Scaling)
+
+RRQR_ROW = 16
+EVENT_ROW = 12
+MAX_PANEL_ROWS = 6144
+
+
+class Symbolic:
+    """Rank-independent schedule of the factorization (host)."""
+
+    def __init__(self, a, h, skip_levels):
+        t0 = time.perf_counter()
+        self.levels = h.levels
+        self.ncl = ncl = len(h.clusters)
+        self.m0 = np.array([c.dofs.size for c in h.clusters], dtype=np.int64)
+        self.depth = np.array([c.depth for c in h.clusters], dtype=np.int64)
+        self.dofs = [np.asarray(c.dofs, dtype=np.int64) for c in h.clusters]
+        self.cluster_of = h.cluster_of
+        n = a.n
+        rows = np.repeat(np.arange(n, dtype=np.int64), np.diff(a.row_ptr))
+        ci, cj = h.cluster_of[rows], h.cluster_of[a.col_idx]
+        up = ci <= cj
+        keys = np.unique(ci[up] * ncl + cj[up])
+        self.bkeys = []
+        self.bid = {}
+        adj = [set() for _ in range(ncl)]
+        cblocks = [set() for _ in range(ncl)]
+        for key in keys.tolist():
+            i, j = divmod(key, ncl)
+            self._new_block(i, j, cblocks)
+            if i != j:
+                adj[i].add(j)
+                adj[j].add(i)
+        for c in range(ncl):                 # every cluster owns a diagonal block
+            if (c, c) not in self.bid:
+                self._new_block(c, c, cblocks)
+        alive = set(range(ncl))
+        self.level_recs = []
+        L = h.levels
+        for level in range(L, 0, -1):
+            interiors = sorted(c for c in alive if self.depth[c] == level)
+            elim = []
+            schur = {}
+            for s in interiors:
+                nbrs = sorted(adj[s])
+                elim.append((s, tuple(nbrs)))
+                for ii, wa in enumerate(nbrs):
+                    for wb in nbrs[ii:]:
+                        key = (wa, wb)
+                        if key not in self.bid:
+                            self._new_block(wa, wb, cblocks)
+                            if wa != wb:
+                                adj[wa].add(wb)
+                                adj[wb].add(wa)
+                        schur.setdefault(key, []).append(s)
+                for w in nbrs:
+                    adj[w].discard(s)
+                for key in cblocks[s]:
+                    other = key[0] if key[1] == s else key[1]
+                    if other != s:
+                        cblocks[other].discard(key)
+                cblocks[s] = set()
+                adj[s] = set()
+                alive.discard(s)
+            skipped = (L - level) < skip_levels
+            rec = {"level": level, "elim": elim, "schur": schur,
+                   "skipped": skipped}
+            if not skipped:
+                active = sorted(alive)
+                rec["active"] = active
+                rec["rescale_blocks"] = sorted(
+                    {key for c in active for key in cblocks[c] if key[0] != key[1]})
+                wave = {}
+                spars = []
+                for p in active:
+                    nb = sorted(adj[p])
+                    wv = 0
+                    for q in nb:
+                        if q < p:
+                            wv = max(wv, wave[q] + 1)
+                    wave[p] = wv
+                    spars.append((p, tuple(nb), wv))
+                rec["spars"] = spars
+                rec["nwaves"] = (max(wave.values()) + 1) if wave else 0
+            self.level_recs.append(rec)
+        self.final = sorted(alive)
+        self.final_blocks = sorted({key for c in self.final for key in cblocks[c]})
+        self.seconds = time.perf_counter() - t0
+
+    def _new_block(self, i, j, cblocks):
+        b = len(self.bkeys)
+        self.bkeys.append((i, j))
+        self.bid[(i, j)] = b
+        cblocks[i].add((i, j))
+        cblocks[j].add((i, j))
+        return b
+
+
+class _Alloc:
+    """Bump allocator of fp64 element offsets within one device pool."""
+
+    def __init__(self):
+        self.size = 0
+
+    def take(self, count):
+        at = self.size
+        self.size += int(count)
+        return at
+
+
+def _groups(works, capacity):
+    """CTA group sizes proportional to work, at least 1, sum <= capacity."""
+    total = float(sum(works))
+    sizes = []
+    for w in works:
+        g = int(capacity * w / total) if total > 0 else 1
+        sizes.append(max(1, g))
+    while sum(sizes) > capacity:
+        k = int(np.argmax(sizes))
+        if sizes[k] == 1:
+            break
+        sizes[k] -= 1
+    return sizes
+
+
+class Engine:
+    def __init__(self, a, h, eps, scheme, skip_levels):
+        self.t = require_cuda()
+        self.a, self.h = a, h
+        self.eps, self.scheme, self.skip = eps, scheme, skip_levels
+        self.sym = Symbolic(a, h, skip_levels)
+        self.timings = {"symbolic_s": self.sym.seconds}
+
+    # ------------------------------------------------------------------ plan
+    def plan(self):
+        sym = self.sym
+        m0 = sym.m0
+        ncl = sym.ncl
+        pool = _Alloc()
+        self.boff = np.array([pool.take(m0[i] * m0[j]) for i, j in sym.bkeys],
+                             dtype=np.int64)
+        fac = _Alloc()
+        self.linv_off = {}           # eliminated s -> Linv offset
+        self.resc_off = {}           # (level, p) -> (L offset, Linv offset)
+        self.q_off = {}              # (level, p) -> Q offset
+        temp_need = 0
+        for rec in sym.level_recs:
+            for s, nbrs in rec["elim"]:
+                self.linv_off[s] = fac.take(m0[s] * m0[s])
+            trsm = sum(m0[w] * m0[s] for s, nbrs in rec["elim"] for w in nbrs)
+            temp_need = max(temp_need, trsm)
+            if not rec["skipped"]:
+                for p in rec["active"]:
+                    self.resc_off[(rec["level"], p)] = (fac.take(m0[p] ** 2),
+                                                        fac.take(m0[p] ** 2))
+                    self.q_off[(rec["level"], p)] = fac.take(m0[p] ** 2)
+                resc = sum(m0[i] * m0[j] for i, j in rec["rescale_blocks"])
+                temp_need = max(temp_need, resc)
+        self.fcap = int(sum(m0[c] for c in sym.final))
+        self.f_off = fac.take(self.fcap ** 2)
+        self.flinv_off = fac.take(self.fcap ** 2)
+        self.pool_size, self.fac_size = pool.size, fac.size
+        self.temp_need = temp_need
+        self.cta_cap = max(1, _lib.load().spand_rrqr_cta_count())
+
+    # -------------------------------------------------------------- numeric
+    def run(self):
+        t = self.t
+        sym = self.sym
+        m0 = sym.m0
+        ncl = sym.ncl
+        tstart = time.perf_counter()
+        self.plan()
+        self.timings["plan_s"] = time.perf_counter() - tstart
+        # geometry: clusters + final block (virtual cluster F = ncl)
+        self.F = ncl
+        geo_m0 = np.concatenate([m0, [self.fcap]]).astype(np.int32)
+        self.geo = geo = Geometry(geo_m0)
+        d = dev()
+        self.pool = pool = t.zeros(max(self.pool_size, 1), dtype=t.float64, device=d)
+        self.facbuf = fac = t.zeros(max(self.fac_size, 1), dtype=t.float64, device=d)
+        self._scatter_a()
+        pb, fb = pool.data_ptr(), fac.data_ptr()
+        self.pb, self.fb = pb, fb
+
+        def blk(i, j):
+            return pb + 8 * int(self.boff[sym.bid[(i, j)]])
+
+        self.blk = blk
+        infos = []          # (kind, key, device int32 tensor)
+        rrqr_waves = []
+        n_events = sum(len(r.get("spars", [])) for r in sym.level_recs)
+        self.events = t.zeros(max(n_events, 1) * EVENT_ROW, dtype=t.int64, device=d)
+        self.event_slot = {}
+        temp = None
+        ev = 0
+        for rec in sym.level_recs:
+            lvl = rec["level"]
+            elim = rec["elim"]
+            # ---------------- interior eliminations
+            if elim:
+                info = t.zeros(len(elim), dtype=t.int32, device=d)
+                from .kernels import potrf_batched, trtri_batched, gemm_grouped, copy_batched
+                potrf_batched(geo, [opnd(blk(s, s), s, s) for s, _ in elim], info)
+                infos.append(("G", lvl, [s for s, _ in elim], info))
+                trtri_batched(geo, [(opnd(blk(s, s), s, s),
+                                     opnd(fb + 8 * self.linv_off[s], s, s))
+                                    for s, _ in elim])
+                pairs = [(s, w) for s, nbrs in elim for w in nbrs]
+                if pairs:
+                    need = sum(m0[w] * m0[s] for s, w in pairs)
+                    temp = self._temp(temp, need)
+                    tb = temp.data_ptr()
+                    toff, acc = {}, 0
+                    for s, w in pairs:
+                        toff[(s, w)] = acc
+                        acc += m0[w] * m0[s]
+                    targets = [(opnd(tb + 8 * toff[(s, w)], w, s),
+                                [(opnd(blk(w, s), w, s),
+                                  opnd(fb + 8 * self.linv_off[s], s, s))],
+                                (m0[w], m0[s])) for s, w in pairs]
+                    gemm_grouped(geo, targets, 1.0, 0.0, bT=1)
+                    copy_batched(geo, [(opnd(tb + 8 * toff[(s, w)], w, s),
+                                        opnd(blk(w, s), w, s), 0) for s, w in pairs])
+                # grouped Schur / fill update
+                targets = []
+                for (wa, wb), slist in rec["schur"].items():
+                    segs = [(opnd(blk(wa, s), wa, s), opnd(blk(wb, s), wb, s))
+                            for s in slist]
+                    targets.append((opnd(blk(wa, wb), wa, wb), segs,
+                                    (m0[wa], m0[wb])))
+                self._schur(targets)
+            if rec["skipped"]:
+                continue
+            from .kernels import potrf_batched, trtri_batched, gemm_grouped, copy_batched
+            active = rec["active"]
+            # ---------------- rescale every active interface
+            lo = {p: self.resc_off[(lvl, p)] for p in active}
+            copy_batched(geo, [(opnd(blk(p, p), p, p), opnd(fb + 8 * lo[p][0], p, p), 1)
+                               for p in active])
+            info = t.zeros(len(active), dtype=t.int32, device=d)
+            potrf_batched(geo, [opnd(fb + 8 * lo[p][0], p, p) for p in active], info)
+            infos.append(("D", lvl, list(active), info))
+            trtri_batched(geo, [(opnd(fb + 8 * lo[p][0], p, p),
+                                 opnd(fb + 8 * lo[p][1], p, p)) for p in active])
+            copy_batched(geo, [(opnd(blk(p, p), p, p), opnd(blk(p, p), p, p), 2)
+                               for p in active])
+            rb = rec["rescale_blocks"]
+            if rb:
+                need = sum(m0[i] * m0[j] for i, j in rb)
+                temp = self._temp(temp, need)
+                tb = temp.data_ptr()
+                toff, acc = {}, 0
+                for i, j in rb:
+                    toff[(i, j)] = acc
+                    acc += m0[i] * m0[j]
+                # T = Z_i^-1 B  (NN), then B = T Z_j^-T (NT)
+                gemm_grouped(geo, [(opnd(tb + 8 * toff[(i, j)], i, j),
+                                    [(opnd(fb + 8 * lo[i][1], i, i), opnd(blk(i, j), i, j))],
+                                    (m0[i], m0[j])) for i, j in rb], 1.0, 0.0, bT=0)
+                gemm_grouped(geo, [(opnd(blk(i, j), i, j),
+                                    [(opnd(tb + 8 * toff[(i, j)], i, j),
+                                      opnd(fb + 8 * lo[j][1], j, j))],
+                                    (m0[i], m0[j])) for i, j in rb], 1.0, 0.0, bT=1)
+            # ---------------- sparsify, wave by wave
+            by_wave = [[] for _ in range(rec["nwaves"])]
+            for p, nbrs, wv in rec["spars"]:
+                self.event_slot[(lvl, p)] = ev
+                by_wave[wv].append((p, nbrs, ev))
+                ev += 1
+            for panels in by_wave:
+                temp = self._rrqr_wave(panels, lvl, temp)
+        # ---------------- final dense block
+        from .kernels import potrf_batched, trtri_batched
+        F = self.F
+        fin = sym.final
+        if fin:
+            index = {c: k for k, c in enumerate(fin)}
+            cl = to_dev(np.asarray(fin, dtype=np.int64))
+            rows = [[index[i], index[j], blk(i, j), 0] for i, j in sym.final_blocks]
+            brows = to_dev(np.asarray(rows, dtype=np.int64).reshape(-1, 4))
+            _lib.call("spand_assemble_final", len(fin), ptr(cl), len(rows),
+                      ptr(brows), ptr(geo.m0), ptr(geo.off), F,
+                      ctypes_ptr(fb + 8 * self.f_off), stream())
+            info = t.zeros(1, dtype=t.int32, device=d)
+            potrf_batched(geo, [opnd(fb + 8 * self.f_off, F, F)], info)
+            infos.append(("F", 0, [F], info))
+            trtri_batched(geo, [(opnd(fb + 8 * self.f_off, F, F),
+                                 opnd(fb + 8 * self.flinv_off, F, F))])
+        self.infos = infos
+        self._temp_keep = temp
+        t.cuda.synchronize()
+        self.timings["device_s"] = time.perf_counter() - tstart
+
+    def _temp(self, temp, need):
+        t = self.t
+        need = max(int(need), 1)
+        if temp is None or temp.numel() < need:
+            temp = t.empty(need, dtype=t.float64, device=dev())
+        return temp
+
+    def _schur(self, targets):
+        from .kernels import gemm_grouped
+        if not targets:
+            return
+        # diagonal targets: lower tiles only (potrf reads the lower triangle)
+        diag = [tg for tg in targets if tg[0][1] == tg[0][2]]
+        off = [tg for tg in targets if tg[0][1] != tg[0][2]]
+        if off:
+            gemm_grouped(self.geo, off, -1.0, 1.0, bT=1)
+        if diag:
+            gemm_grouped(self.geo, diag, -1.0, 1.0, bT=1, lower_only=True)
+
+    def _rrqr_wave(self, panels, lvl, temp):
+        t = self.t
+        sym = self.sym
+        m0 = sym.m0
+        cap = self.cta_cap
+        code = SCHEME_CODE[self.scheme]
+        # split a wave into launches of at most `cap` panels
+        for c0 in range(0, len(panels), cap):
+            chunk = panels[c0:c0 + cap]
+            works = []
+            for p, nbrs, _ in chunk:
+                ncap = int(sum(m0[w] for w in nbrs))
+                works.append(max(1, int(m0[p]) * max(ncap, 1)))
+            gs = _groups(works, cap)
+            # workspace layout per panel (doubles)
+            need = 0
+            lay = []
+            for (p, nbrs, evs), g in zip(chunk, gs):
+                ncap = int(sum(m0[w] for w in nbrs))
+                mc = int(m0[p])
+                wsz = mc * max(ncap, 1)
+                asz = 2 * ncap + 2 * mc + 4 * g + 4
+                isz = (3 * ncap + 1) // 2 + 1
+                lay.append((need, wsz, asz, isz, ncap, mc))
+                need += wsz + asz + isz + 1
+            temp = self._temp(temp, need)
+            tb = temp.data_ptr()
+            ctr = t.zeros(len(chunk), dtype=t.int32, device=dev())
+            prow, nrow = [], []
+            gbeg = 0
+            vmax = 1
+            for k, ((p, nbrs, evs), g, (at, wsz, asz, isz, ncap, mc)) in enumerate(
+                    zip(chunk, gs, lay)):
+                nb0 = len(nrow)
+                for w in nbrs:
+                    if w > p:
+                        nrow.append([w, self.blk(p, w), 0, 0])
+                    else:
+                        nrow.append([w, self.blk(w, p), 1, 0])
+                qoff = self.fb + 8 * self.q_off[(lvl, p)]
+                prow.append([p, nb0, len(nrow), tb + 8 * at, qoff,
+                             tb + 8 * (at + wsz), tb + 8 * (at + wsz + asz),
+                             gbeg, g, ctr.data_ptr() + 4 * k, evs, ncap, mc, 0, 0, 0])
+                gbeg += g
+                vmax = max(vmax, mc)
+            if vmax > MAX_PANEL_ROWS:
+                raise NotImplementedError(
+                    f"interface of {vmax} dofs exceeds the RRQR kernel limit")
+            pd = to_dev(np.asarray(prow, dtype=np.int64).reshape(-1, RRQR_ROW))
+            nd = to_dev(np.asarray(nrow if nrow else [[0, 0, 0, 0]],
+                                   dtype=np.int64).reshape(-1, 4))
+            _lib.call("spand_rrqr_wave", len(chunk), gbeg, vmax, ptr(pd), ptr(nd),
+                      ptr(self.geo.m0), ptr(self.geo.off), float(self.eps), code,
+                      ptr(self.events), stream())
+        return temp
+
+    def _scatter_a(self):
+        """Initial blocks from the entries of A (factorize.py:61-96)."""
+        sym, a = self.sym, self.a
+        n = a.n
+        rows = np.repeat(np.arange(n, dtype=np.int64), np.diff(a.row_ptr))
+        cols = a.col_idx
+        cl = sym.cluster_of
+        slot = np.empty(n, dtype=np.int64)
+        for c, d in enumerate(sym.dofs):
+            slot[d] = np.arange(d.size)
+        ci, cj = cl[rows], cl[cols]
+        up = ci <= cj
+        ci, cj, r, c = ci[up], cj[up], rows[up], cols[up]
+        keys = ci * sym.ncl + cj
+        bid_arr = np.empty(len(sym.bkeys), dtype=np.int64)
+        kk = np.array([i * sym.ncl + j for i, j in sym.bkeys], dtype=np.int64)
+        order = np.argsort(kk)
+        pos = order[np.searchsorted(kk[order], keys)]
+        del bid_arr
+        where = self.boff[pos] + slot[r] + slot[c] * sym.m0[ci]
+        vals = a.values[up]
+        t = self.t
+        self.pool[to_dev(where, np.int64)] = to_dev(vals, np.float64)
+
+    # --------------------------------------------------------------- collect
+    def collect(self):
+        t = self.t
+        sym = self.sym
+        m0 = sym.m0
+        t0 = time.perf_counter()
+        ev = self.events.cpu().numpy().reshape(-1, EVENT_ROW)
+        # first non-SPD pivot in operator order
+        for kind, lvl, ids, info in self.infos:
+            iv = info.cpu().numpy()
+            bad = np.flatnonzero(iv)
+            if bad.size:
+                raise NotSPD(int(iv[bad[0]]) - 1)
+        off = np.zeros(sym.ncl, dtype=np.int64)
+        pool, fac = self.pool, self.facbuf
+        ops, perm_parts, diags = [], [], []
+        views = []          # for the nonzero count: (MatView, op index)
+        dofs = sym.dofs
+
+        def live(c):
+            return dofs[c][off[c]:]
+
+        def bview(i, j, r0, c0, rows, cols, trans=False):
+            b = int(self.boff[sym.bid[(i, j)]])
+            return MatView(pool, b + r0 + c0 * m0[i], m0[i], rows, cols, trans)
+
+        def fview(at, c, size):
+            return MatView(fac, at + off[c] + off[c] * m0[c], m0[c], size, size)
+
+        scheme = self.scheme
+        for rec in sym.level_recs:
+            lvl = rec["level"]
+            nint, ndofs = 0, 0
+            for s, nbrs in rec["elim"]:
+                ns = m0[s] - off[s]
+                if ns == 0:
+                    continue
+                nint += 1
+                ndofs += ns
+                wl = [w for w in nbrs if m0[w] - off[w] > 0]
+                w_dofs = (np.concatenate([live(w) for w in wl]) if wl
+                          else np.empty(0, np.int64))
+                pv, r0 = [], 0
+                for w in wl:
+                    nw = m0[w] - off[w]
+                    pv.append((bview(w, s, off[w], off[s], nw, ns), r0))
+                    r0 += nw
+                low = bview(s, s, off[s], off[s], ns, ns)
+                linv = fview(self.linv_off[s], s, ns)
+                op = Elimination(live(s), w_dofs, low, pv, linv=linv)
+                ops.append(op)
+                perm_parts.append(live(s))
+            faces = []
+            if not rec["skipped"]:
+                act = [p for p in rec["active"] if m0[p] - off[p] > 0]
+                for p in act:
+                    lo = self.resc_off[(lvl, p)]
+                    mp = m0[p] - off[p]
+                    ops.append(Scaling(live(p), fview(lo[0], p, mp),
+                                       linv=fview(lo[1], p, mp)))
+                nbr_of = {p: nb for p, nb, _ in rec["spars"]}
+                for p in act:
+                    e = ev[self.event_slot[(lvl, p)]]
+                    mp, k_stop, k_c, rf2, n_fine = (int(e[1]), int(e[3]), int(e[4]),
+                                                    int(e[5]), int(e[6]))
+                    assert mp == m0[p] - off[p], "event / host offset mismatch"
+                    old = live(p)
+                    q = MatView(fac, self.q_off[(lvl, p)], max(mp, 1), mp, mp,
+                                rot=k_c if mp else 0)
+                    ops.append(Orthogonal(old, q))
+                    if scheme is SchemeKind.SECOND_ORDER_FULL:
+                        ncorr = n_fine
+                    elif scheme is SchemeKind.SECOND_ORDER_SUPERFINE:
+                        ncorr = k_stop - k_c
+                    else:
+                        ncorr = 0
+                    wl = [w for w in nbr_of[p] if m0[w] - off[w] > 0]
+                    ntot = int(sum(m0[w] - off[w] for w in wl))
+                    if ncorr and ntot:
+                        evs, c0 = [], 0
+                        for w in wl:
+                            nw = m0[w] - off[w]
+                            if w > p:
+                                v = bview(p, w, off[p], off[w], ncorr, nw)
+                            else:
+                                v = bview(w, p, off[w], off[p], nw, ncorr, trans=True)
+                            evs.append((v, c0))
+                            c0 += nw
+                        w_dofs = np.concatenate([live(w) for w in wl])
+                        ops.append(ErrorCorrection(old[:ncorr], w_dofs, evs))
+                    if n_fine:
+                        perm_parts.append(old[:n_fine])
+                    faces.append({"cluster": int(p), "size_before": int(mp),
+                                  "size_after": int(k_c), "rank_f2": int(rf2),
+                                  "eta_stop": float(np.int64(e[7]).view(np.float64)),
+                                  "r11": float(np.int64(e[8]).view(np.float64)),
+                                  "k_stop": int(k_stop)})
+                    off[p] += n_fine
+            digest = hashlib.sha256(repr([(f["cluster"], f["size_before"],
+                                           f["size_after"], f["rank_f2"])
+                                          for f in faces]).encode()).hexdigest()
+            diags.append({"level": int(lvl), "interior_clusters": nint,
+                          "interior_dofs": int(ndofs), "skipped": bool(rec["skipped"]),
+                          "interfaces": [{k: f[k] for k in ("cluster", "size_before",
+                                                            "size_after", "rank_f2")}
+                                         for f in faces],
+                          "margins": faces,
+                          "digest": digest})
+        fin = [c for c in sym.final if m0[c] - off[c] > 0]
+        total = int(sum(m0[c] - off[c] for c in fin))
+        if total:
+            F = self.F
+            foff = self.fcap - total
+            low = MatView(fac, self.f_off + foff + foff * self.fcap, self.fcap, total, total)
+            linv = MatView(fac, self.flinv_off + foff + foff * self.fcap, self.fcap,
+                           total, total)
+            fd = np.concatenate([live(c) for c in fin])
+            ops.append(Elimination(fd, np.empty(0, np.int64), low, [], linv=linv))
+            perm_parts.append(fd)
+        perm = (np.concatenate(perm_parts) if perm_parts else np.empty(0, np.int64))
+        nnz = self._count(ops)
+        self.timings["collect_s"] = time.perf_counter() - t0
+        return ops, perm, {"levels": diags, "final_block": total}, nnz
+
+    def _count(self, ops):
+        t = self.t
+        rows = []
+        for op in ops:
+            vs = []
+            if isinstance(op, Elimination):
+                vs = [op._lower] + [v for v, _ in op.panel_views]
+            elif isinstance(op, Scaling):
+                vs = [op._lower]
+            elif isinstance(op, Orthogonal):
+                vs = [op.q_view]
+            else:
+                vs = [v for v, _ in op.e_views]
+            for v in vs:
+                if v.rows and v.cols:
+                    rows.append([v.addr, v.ld, v.rows, v.cols])
+        if not rows:
+            return 0
+        vd = to_dev(np.asarray(rows, dtype=np.int64))
+        out = t.zeros(len(rows), dtype=t.int64, device=dev())
+        _lib.call("spand_count_nonzero", len(rows), ptr(vd), ptr(out), stream())
+        return int(out.sum().item())
+
+
+def ctypes_ptr(addr):
+    import ctypes
+    return ctypes.c_void_p(int(addr))
+
+
+def run_factorization(a, h, eps, scheme, skip_levels, collect_local_errors=False):
+    from .factorize import Factorization
+    t0 = time.perf_counter()
+    eng = Engine(a, h, eps, scheme, skip_levels)
+    eng.run()
+    ops, perm, diag, nnz = eng.collect()
+    eng.timings["total_s"] = time.perf_counter() - t0
+    f = Factorization(ops=ops, perm=perm, n=a.n, eps=float(eps), scheme=scheme,
+                      skip_levels=int(skip_levels), nnz_factor=int(nnz),
+                      diagnostics=diag,
+                      _keep=(eng.pool, eng.facbuf, eng.geo), timings=eng.timings)
+    return f

@@ -1,0 +1,69 @@
+"""GPU factorization parity against the reference (golden fixtures) and the
+oracle (payloads).  Integer structure bit-exact: hierarchy, perm, operator
+kinds, interface ranks (size_after) and rank_f2; payloads within 1e-8
+relative Frobenius per block; n_cg within +-1 (observed exact)."""
+
+import hashlib
+
+import numpy as np
+import pytest
+
+from tests.golden_cases import load, matrix_for, small_tags
+
+pytestmark = pytest.mark.gpu
+
+
+def sha(arr):
+    arr = np.ascontiguousarray(arr)
+    h = hashlib.sha256()
+    h.update(str(arr.dtype).encode())
+    h.update(str(arr.shape).encode())
+    h.update(arr.tobytes())
+    return h.hexdigest()
+
+
+def rel(a, b):
+    nb = np.linalg.norm(b)
+    return np.linalg.norm(a - b) / (nb if nb > 0 else 1.0)
+
+
+@pytest.mark.parametrize("tag", small_tags())
+def test_factorize_matches_reference(tag):
+    import paper_2007_00789_b200 as sp
+    from oracle import spand_oracle as orc
+    rec, arr = load(tag)
+    a = matrix_for(tag)
+    h = sp.build_hierarchy(a, rec["levels"])
+    f = sp.factorize(a, h, rec["eps"], rec["scheme"], skip_levels=rec["skip_levels"])
+    got = [[[e["cluster"], e["size_before"], e["size_after"], e["rank_f2"]]
+            for e in lv["interfaces"]] for lv in f.diagnostics["levels"]]
+    want = [lv["interfaces"] for lv in rec["diagnostics"]]
+    assert got == want
+    assert [lv["interior_clusters"] for lv in f.diagnostics["levels"]] == \
+        [lv["interior_clusters"] for lv in rec["diagnostics"]]
+    assert f.diagnostics["final_block"] == rec["final_block"]
+    assert sha(np.asarray(f.perm, np.int64)) == rec["perm_sha"]
+    kinds = "".join("GDQE"[["elimination", "scaling", "orthogonal",
+                            "error-correction"].index(op.kind.value)] for op in f.ops)
+    assert kinds == rec["op_kinds"]
+    assert abs(f.nnz_factor - rec["nnz_factor"]) <= 1e-3 * rec["nnz_factor"]
+    # payloads vs the oracle factor, per block
+    cl = [(c.id, c.dofs, c.depth) for c in h.clusters]
+    of = orc.factorize(a.n, a.row_ptr, a.col_idx, a.values, cl, rec["levels"],
+                       rec["eps"], rec["scheme"], rec["skip_levels"])
+    for x, y in zip(f.ops, of.ops):
+        assert np.array_equal(x.dofs, y.dofs)
+        if x.kind.value in ("elimination", "error-correction"):
+            assert np.array_equal(x.w_dofs, y.w_dofs)
+        for mine, theirs in (("lower", "lower"), ("panel", "panel"), ("q", "q"),
+                             ("e_tilde", "e_tilde")):
+            if getattr(y, theirs, None) is not None and hasattr(x, mine):
+                got_m, want_m = getattr(x, mine), getattr(y, theirs)
+                assert got_m.shape == want_m.shape, (x.kind, mine)
+                assert rel(got_m, want_m) <= 1e-8, (x.kind, mine, rel(got_m, want_m))
+    z = f.apply_m(arr["b"])
+    if "apply_m_b" in arr:
+        assert rel(z, arr["apply_m_b"]) <= 1e-9
+    x, rep = sp.pcg(a, arr["b"], m=f.apply_m, tol=rec["tol"])
+    assert abs(rep.n_cg - rec["n_cg"]) <= 1
+    assert rep.converged == rec["converged"]
