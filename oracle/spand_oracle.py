@@ -475,6 +475,8 @@ class _Trailing:
         m = old.size
         n_fine = m - res["rank_c"]
         ops = [Op("Q", old, q=np.hstack([res["q_f"], res["q_c"]]))]
+        ops[0].pivots = res["pivots"][:res["k_stop"]]   # test-side metadata
+        ops[0].k_c = res["rank_c"]
         ncorr = res["e_tilde"].shape[0]
         if ncorr and res["e_tilde"].size:
             ops.append(Op("E", old[:ncorr], w_dofs, e_tilde=res["e_tilde"]))
