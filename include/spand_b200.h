@@ -109,6 +109,12 @@ int spand_potrf_batched(int ntask, const int64_t* ops, const int32_t* m0,
  * Upper triangle of Linv is written with zeros (dense.py:85-93). */
 int spand_trtri_batched(int ntask, const int64_t* ops, const int32_t* m0,
                         const int32_t* off, void* stream);
+/* Inverse of <= 64x64 lower-triangular tiles (task row = {L operand, X
+ * operand}, each clamped to 64x64 with rcount/ccount); X's tile is written
+ * in full (zeros above the diagonal).  Used with spand_gemm_grouped for the
+ * recursive-doubling trtri of whole levels. */
+int spand_trtri_tiles(int ntask, const int64_t* ops, const int32_t* m0,
+                      const int32_t* off, void* stream);
 /* Batched copy: task row = {src operand(7), dst operand(7), mode}; mode 0:
  * copy the full live rectangle, 1: copy lower triangle + zero upper, 2:
  * write the identity (src ignored). */

@@ -33,6 +33,7 @@ SIGNATURES = {
                             _c_int, _P],
     "spand_potrf_batched": [_c_int, _P, _P, _P, _P, _P],
     "spand_trtri_batched": [_c_int, _P, _P, _P, _P],
+    "spand_trtri_tiles": [_c_int, _P, _P, _P, _P],
     "spand_copy_batched": [_c_int, _P, _P, _P, _P],
     "spand_gemm_grouped": [_c_int, _P, _P, _P, _P, _P, _c_dbl, _c_dbl, _c_int,
                            _c_int, _P],
@@ -66,9 +67,60 @@ def load(path=LIB_PATH):
     return lib
 
 
+# launches issued through call(), per entry point (bench.py's gpu_launches)
+COUNTS = {}
+# optional per-entry-point CUDA-event timing (profile() context manager)
+_PROFILE = None
+
+# host-only entry points (no kernel launch)
+_HOST_ONLY = {"spand_nd_partition", "spand_version", "spand_device_sm_count",
+              "spand_rrqr_cta_count", "spand_spmv_blocks", "spand_dot_blocks"}
+
+
 def call(name, *args):
     """Invoke an entry point; nonzero status raises RuntimeError."""
-    st = getattr(load(), name)(*args)
+    fn = getattr(load(), name)
+    if _PROFILE is not None and name not in _HOST_ONLY:
+        import torch
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        st = fn(*args)
+        e1.record()
+        _PROFILE.append((name, e0, e1))
+    else:
+        st = fn(*args)
     if st != 0:
         raise RuntimeError(f"{name} failed with status {st}")
+    if name not in _HOST_ONLY:
+        COUNTS[name] = COUNTS.get(name, 0) + 1
     return st
+
+
+def launches():
+    return sum(COUNTS.values())
+
+
+class profile:
+    """Context manager: per-entry-point device time (ms) on the current
+    stream, measured with CUDA events around every call()."""
+
+    def __enter__(self):
+        global _PROFILE
+        _PROFILE = []
+        self.result = {}
+        return self
+
+    def __exit__(self, *exc):
+        global _PROFILE
+        import torch
+        torch.cuda.synchronize()
+        out = {}
+        for name, e0, e1 in _PROFILE:
+            ms = e0.elapsed_time(e1)
+            tot, cnt = out.get(name, (0.0, 0))
+            out[name] = (tot + ms, cnt + 1)
+        _PROFILE = None
+        self.result = {k: {"ms": round(v[0], 3), "calls": v[1]} for k, v in
+                       sorted(out.items(), key=lambda kv: -kv[1][0])}
+        return False

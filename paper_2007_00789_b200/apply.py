@@ -189,18 +189,12 @@ class _Pass:
                                 dst.size))
 
     def run(self, x, scratch, ldx, ldscr, nvec):
-        lib = _lib.load()
         st = stream()
         for tiles, ntile, dst, mode, ptrs, src, nout in self.phases:
-            r = lib.spand_gemv_tiles(ntile, ptr(tiles), ptr(self.tasks), ptr(x),
-                                     ldx, ptr(scratch), ldscr, nvec, st)
-            if r:
-                raise RuntimeError(f"spand_gemv_tiles failed ({r})")
-            r = lib.spand_apply_scatter(nout, ptr(dst), ptr(mode), ptr(ptrs),
-                                        ptr(src), ptr(x), ldx, ptr(scratch),
-                                        ldscr, nvec, st)
-            if r:
-                raise RuntimeError(f"spand_apply_scatter failed ({r})")
+            _lib.call("spand_gemv_tiles", ntile, ptr(tiles), ptr(self.tasks),
+                      ptr(x), ldx, ptr(scratch), ldscr, nvec, st)
+            _lib.call("spand_apply_scatter", nout, ptr(dst), ptr(mode), ptr(ptrs),
+                      ptr(src), ptr(x), ldx, ptr(scratch), ldscr, nvec, st)
 
     @property
     def launches(self):

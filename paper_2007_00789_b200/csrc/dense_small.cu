@@ -275,3 +275,55 @@ int spand_count_nonzero(int nview, const int64_t* views, unsigned long long* out
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Inverse of <= 64 x 64 lower-triangular diagonal tiles in shared memory; the
+// off-diagonal blocks of L^-1 are then assembled by recursive doubling with
+// the DMMA GEMM ([A 0; B C]^-1 = [A^-1 0; -C^-1 B A^-1, C^-1]), so a whole
+// level's triangular inverses (dense.py:85-93) are O(log n) batched launches.
+namespace {
+__global__ void __launch_bounds__(kT)
+trtri_tile_kernel(const int64_t* __restrict__ ops, const int32_t* __restrict__ m0,
+                  const int32_t* __restrict__ off) {
+  extern __shared__ double tri_sm[];
+  double (*Ls)[65] = reinterpret_cast<double (*)[65]>(tri_sm);
+  double (*Xs)[65] = reinterpret_cast<double (*)[65]>(tri_sm + 64 * 65);
+  const Opnd L = load_opnd(ops + 14 * (int64_t)blockIdx.x, m0, off);
+  const Opnd X = load_opnd(ops + 14 * (int64_t)blockIdx.x + 7, m0, off);
+  const int n = min(L.rows, L.cols);
+  if (n <= 0) return;
+  for (int e = threadIdx.x; e < 64 * 64; e += kT) {
+    const int r = e % 64, c = e / 64;
+    Ls[r][c] = (r < n && c <= r) ? L.p[r + (int64_t)c * L.ld] : 0.0;
+    Xs[r][c] = 0.0;
+  }
+  __syncthreads();
+  // column j of X solves L x = e_j; one thread per column, forward order
+  if (threadIdx.x < n) {
+    const int j = threadIdx.x;
+    Xs[j][j] = 1.0 / Ls[j][j];
+    for (int i = j + 1; i < n; ++i) {
+      double s = 0.0;
+      for (int k = j; k < i; ++k) s += Ls[i][k] * Xs[k][j];
+      Xs[i][j] = -s / Ls[i][i];
+    }
+  }
+  __syncthreads();
+  const int nr = min(X.rows, 64), nc = min(X.cols, 64);
+  for (int e = threadIdx.x; e < nr * nc; e += kT) {
+    const int r = e % nr, c = e / nr;
+    X.p[r + (int64_t)c * X.ld] = (r < n && c < n) ? Xs[r][c] : 0.0;
+  }
+}
+}  // namespace
+
+extern "C" int spand_trtri_tiles(int ntask, const int64_t* ops, const int32_t* m0,
+                                 const int32_t* off, void* stream) {
+  if (ntask < 0) return -1;
+  if (ntask == 0) return 0;
+  const int smem = 2 * 64 * 65 * (int)sizeof(double);
+  cudaFuncSetAttribute(trtri_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  trtri_tile_kernel<<<ntask, kT, smem, as_stream(stream)>>>(ops, m0, off);
+  SPAND_CHECK_LAUNCH();
+  return 0;
+}

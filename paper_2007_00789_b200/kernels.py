@@ -47,13 +47,63 @@ def potrf_batched(geo, ops, info):
               ptr(info), stream())
 
 
-def trtri_batched(geo, pairs):
+def trtri_batched(geo, pairs, sizes=None):
+    """Lower-triangular inverses X = L^-1 for [(L operand, X operand)].
+
+    ``sizes`` (max live size per pair, default the m0 of the row cluster)
+    drive the recursive doubling: 64x64 diagonal tiles are inverted in
+    shared memory, then level r combines 2^r-tile blocks with two grouped
+    DMMA GEMMs, T = B A^-1 and X_21 = -C^-1 T."""
     n = len(pairs)
     if n == 0:
         return
-    d = _rows([a + b for a, b in pairs], 14)
-    _lib.call("spand_trtri_batched", n, ptr(d), ptr(geo.m0), ptr(geo.off),
-              stream())
+    if sizes is None:
+        sizes = [int(geo.m0_host[l[1]]) for l, _ in pairs]
+    t = require_cuda()
+    tiles = []
+    for (l, x), nm in zip(pairs, sizes):
+        for o in range(0, nm, TILE):
+            tiles.append(_sub(l, o, o, TILE, TILE) + _sub(x, o, o, TILE, TILE))
+    if tiles:
+        d = _rows(tiles, 14)
+        _lib.call("spand_trtri_tiles", len(tiles), ptr(d), ptr(geo.m0),
+                  ptr(geo.off), stream())
+    nmax = max(sizes) if sizes else 0
+    if nmax <= TILE:
+        return
+    # temp with the same geometry as each X (m0^2 of the row cluster)
+    toff, acc = [], 0
+    for l, _ in pairs:
+        toff.append(acc)
+        acc += int(geo.m0_host[l[1]]) ** 2
+    temp = t.empty(max(acc, 1), dtype=t.float64, device=dev())
+    tb = temp.data_ptr()
+    s = TILE
+    while s < nmax:
+        g1, g2 = [], []
+        for (l, x), nm, to in zip(pairs, sizes, toff):
+            tmp = [tb + 8 * to] + x[1:]
+            for o in range(0, nm - s, 2 * s):
+                # T = B A^-1 with B = L[o+s:o+2s, o:o+s], A^-1 = X[o:o+s, o:o+s]
+                g1.append((_sub(tmp, o + s, o, s, s),
+                           [(_sub(l, o + s, o, s, s), _sub(x, o, o, s, s))],
+                           (s, s)))
+                # X[o+s:o+2s, o:o+s] = -C^-1 T
+                g2.append((_sub(x, o + s, o, s, s),
+                           [(_sub(x, o + s, o + s, s, s), _sub(tmp, o + s, o, s, s))],
+                           (s, s)))
+        gemm_grouped(geo, g1, 1.0, 0.0, bT=0)
+        gemm_grouped(geo, g2, -1.0, 0.0, bT=0)
+        s *= 2
+    # `temp` may be released now: the caching allocator hands the block to
+    # later allocations on this stream only, i.e. after these GEMMs
+
+
+def _sub(o, rskip, cskip, rcount, ccount):
+    """Sub-operand of an operand row (skips are relative to its start)."""
+    return [o[0], o[1], o[2], o[3] + rskip, o[4] + cskip,
+            rcount if o[5] < 0 else min(rcount, max(o[5] - rskip, 0)),
+            ccount if o[6] < 0 else min(ccount, max(o[6] - cskip, 0))]
 
 
 def copy_batched(geo, tasks):
