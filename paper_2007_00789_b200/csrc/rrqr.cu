@@ -129,12 +129,14 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
   double* cand_v = aux + 2 * ncap + mcap;                      // 2G values
   int64_t* cand_p = reinterpret_cast<int64_t*>(cand_v + 2 * G);  // 2G (pos << 32 | col)
   double* betas = reinterpret_cast<double*>(cand_p + 2 * G);   // mcap
+  double* taus = betas + mcap;                                 // mcap
+  double* V = W + (int64_t)mcap * ncap;                        // m x kmax reflectors
   int32_t* perm = iaux;
   int32_t* pos = iaux + ncap;
   int32_t* done = iaux + 2 * ncap;
 
   const int c0 = (int)(((int64_t)n * rank) / G), c1 = (int)(((int64_t)n * (rank + 1)) / G);
-  const int r0 = (int)(((int64_t)m * rank) / G), r1 = (int)(((int64_t)m * (rank + 1)) / G);
+  const int q0 = (int)(((int64_t)m * rank) / G), q1 = (int)(((int64_t)m * (rank + 1)) / G);
   const int kmax = m < n ? m : n;
 
   // neighbour of column c (linear scan; <= a few dozen neighbours)
@@ -208,11 +210,6 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
         bc = c;
       }
     }
-  }
-  // Q = I on my rows
-  for (int64_t e = tid; e < (int64_t)(r1 - r0) * m; e += kT) {
-    const int i = r0 + (int)(e % (r1 - r0)), c = (int)(e / (r1 - r0));
-    Q[(int64_t)i + (int64_t)c * m] = (i == c) ? 1.0 : 0.0;
   }
   auto publish = [&](double v, int64_t ps, int c, int parity) {
     if (lane == 0) {
@@ -304,20 +301,50 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
       const double tau = 2.0 / block_sum<kT>(vv, sh.red);
       if (rank == 0 && tid == 0) betas[k] = beta;
       __syncthreads();
-      // ---- my columns: apply H_k, row-k entry, norm downdate / refresh
+      if (rank == 0) {
+        for (int i = tid; i < len; i += kT) V[(int64_t)k + i + (int64_t)k * m] = vsh[i];
+        if (tid == 0) taus[k] = tau;
+      }
+      // ---- my columns: apply H_k, row-k entry, norm downdate / refresh.
+      // One warp per column; rows are streamed 8 per lane per round so each
+      // lane keeps 8 independent loads in flight (the pass is bandwidth-bound).
       for (int c = c0 + warp; c < c1; c += kWarps) {
         if (c == j) continue;
         if (done[c]) continue;
-        double* col = W + (int64_t)c * m;
+        double* col = W + (int64_t)c * m + k;
         double d = 0.0;
-        for (int i = lane; i < len; i += 32) d += vsh[i] * col[k + i];
+        for (int base = 0; base < len; base += 256) {
+          double x[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int i = base + lane + 32 * u;
+            x[u] = i < len ? col[i] : 0.0;
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int i = base + lane + 32 * u;
+            if (i < len) d += vsh[i] * x[u];
+          }
+        }
         d = warp_sum(d) * tau;
         double rk = 0.0, tail = 0.0;
-        for (int i = lane; i < len; i += 32) {
-          const double nv = col[k + i] - d * vsh[i];
-          col[k + i] = nv;
-          if (i == 0) rk = nv;
-          else tail += nv * nv;
+        for (int base = 0; base < len; base += 256) {
+          double x[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int i = base + lane + 32 * u;
+            x[u] = i < len ? col[i] : 0.0;
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int i = base + lane + 32 * u;
+            if (i < len) {
+              const double nv = x[u] - d * vsh[i];
+              col[i] = nv;
+              if (i == 0) rk = nv;
+              else tail += nv * nv;
+            }
+          }
         }
         tail = warp_sum(tail);
         rk = __shfl_sync(0xffffffffu, rk, 0);
@@ -337,16 +364,12 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
           }
         }
       }
-      // ---- Q[:, k:] -= (Q[:, k:] v) v^T tau on my rows
-      for (int i = r0 + tid; i < r1; i += kT) {
-        double t = 0.0;
-        for (int c = 0; c < len; ++c) t += Q[(int64_t)i + (int64_t)(k + c) * m] * vsh[c];
-        t *= tau;
-        for (int c = 0; c < len; ++c) Q[(int64_t)i + (int64_t)(k + c) * m] -= t * vsh[c];
-      }
     } else {
       // zero pivot (only when stop_tol * r11 == 0): no reflector
-      if (rank == 0 && tid == 0) betas[k] = 0.0;
+      if (rank == 0 && tid == 0) {
+        betas[k] = 0.0;
+        taus[k] = 0.0;
+      }
       for (int c = c0 + warp; c < c1; c += kWarps) {
         if (lane == 0 && c != j && !done[c]) {
           const int64_t ps = pos[c];
@@ -376,6 +399,30 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
         for (int i = t + lane; i < m; i += 32) col[i] = (i == t) ? bt : 0.0;
     }
     if (lane == 0) perm[t] = c;
+  }
+  __syncthreads();
+  // ---- Q = H_0 H_1 ... H_{k_stop-1}, accumulated backwards (dorg2r order)
+  // on my column range: H_t only touches rows/columns >= t, columns are
+  // independent, so no group synchronisation is needed.
+  for (int64_t e = tid; e < (int64_t)(q1 - q0) * m; e += kT) {
+    const int i = (int)(e % m), c = q0 + (int)(e / m);
+    Q[(int64_t)i + (int64_t)c * m] = (i == c) ? 1.0 : 0.0;
+  }
+  for (int t = k_stop - 1; t >= 0; --t) {
+    const double tt = __ldcg(taus + t);
+    if (tt == 0.0) continue;
+    if (q1 <= t) continue;
+    const int len = m - t;
+    __syncthreads();
+    for (int i = tid; i < len; i += kT) vsh[i] = __ldcg(V + (int64_t)t + i + (int64_t)t * m);
+    __syncthreads();
+    for (int c = max(q0, t) + warp; c < q1; c += kWarps) {
+      double* col = Q + (int64_t)c * m + t;
+      double d = 0.0;
+      for (int i = lane; i < len; i += 32) d += vsh[i] * col[i];
+      d = warp_sum(d) * tt;
+      for (int i = lane; i < len; i += 32) col[i] -= d * vsh[i];
+    }
   }
   __syncthreads();
   // k_c: first pivot below eps * r11 (dense.py:181-182)

@@ -43,6 +43,7 @@ from .schemes import (Elimination, ErrorCorrection, MatView, Orthogonal,
                       Scaling)
 
 RRQR_ROW = 16
+WAVE_LOG = None      # set to [] to record per-wave CUDA events (profiling)
 EVENT_ROW = 12
 MAX_PANEL_ROWS = 6144
 
@@ -373,8 +374,8 @@ class Engine:
             for (p, nbrs, evs), g in zip(chunk, gs):
                 ncap = int(sum(m0[w] for w in nbrs))
                 mc = int(m0[p])
-                wsz = mc * max(ncap, 1)
-                asz = 2 * ncap + 2 * mc + 4 * g + 4
+                wsz = mc * max(ncap, 1) + mc * mc
+                asz = 2 * ncap + 3 * mc + 4 * g + 4
                 isz = (3 * ncap + 1) // 2 + 1
                 lay.append((need, wsz, asz, isz, ncap, mc))
                 need += wsz + asz + isz + 1
@@ -404,9 +405,18 @@ class Engine:
             pd = to_dev(np.asarray(prow, dtype=np.int64).reshape(-1, RRQR_ROW))
             nd = to_dev(np.asarray(nrow if nrow else [[0, 0, 0, 0]],
                                    dtype=np.int64).reshape(-1, 4))
+            if WAVE_LOG is not None:
+                e0 = t.cuda.Event(enable_timing=True)
+                e1 = t.cuda.Event(enable_timing=True)
+                e0.record()
             _lib.call("spand_rrqr_wave", len(chunk), gbeg, vmax, ptr(pd), ptr(nd),
                       ptr(self.geo.m0), ptr(self.geo.off), float(self.eps), code,
                       ptr(self.events), stream())
+            if WAVE_LOG is not None:
+                e1.record()
+                WAVE_LOG.append((lvl, len(chunk), gbeg, vmax,
+                                 [(int(m0[p]), int(sum(m0[w] for w in nb)), g)
+                                  for (p, nb, _), g in zip(chunk, gs)], e0, e1))
         return temp
 
     def _scatter_a(self):

@@ -26,8 +26,8 @@ def rrqr_single(a, eps, scheme, group=None):
     cap = max(1, _lib.load().spand_rrqr_cta_count())
     g = group or max(1, min(cap, n // 64, (m * n) // 65536 + 1))
     ncap, mcap = max(n, 1), max(m, 1)
-    wsz = mcap * ncap
-    asz = 2 * ncap + 2 * mcap + 4 * g + 4
+    wsz = mcap * ncap + mcap * mcap
+    asz = 2 * ncap + 3 * mcap + 4 * g + 4
     isz = (3 * ncap + 1) // 2 + 1
     work = t.zeros(wsz + asz + isz + 1, dtype=t.float64, device=dev())
     q = t.zeros(mcap * mcap, dtype=t.float64, device=dev())
