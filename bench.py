@@ -1,0 +1,383 @@
+"""Benchmark: spaND factorize + PCG solve on BASELINE config C4 (headline).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config C4] [--levels 15] [--no-cpu-baseline]
+
+Workload (BASELINE.json configs[3]): 3D 64^3 high-contrast diffusion,
+7-point finite volumes with harmonic faces, a piecewise constant on 8^3
+blocks with log10 a ~ U(-3, 3) (seed 3), n = 262144, nested dissection to
+15 levels, eps = 1e-2, second-order "second-full" scheme, skip_levels = 4,
+b ~ N(0, 1) from the same generator, PCG to relative residual 1e-12.
+Synthetic input built in-process (no dataset involved).
+
+A STEP is one full pass of the hot path: factorize(A, hierarchy) on the
+B200 followed by pcg(A, b, M) to 1e-12 (the hierarchy is the factorize
+input, as in the reference API; it is built once, on the host, and timed
+separately).  metric = algorithmic FP64 work of the step (F_elim +
+F_scale + F_rrqr + 4 nnz_factor per apply + 2 nnz(A) per SpMV, formulas in
+paper_2007_00789_b200/metrics.py) / step time, in GFLOP/s
+(higher is better); the same formula prices the CPU oracle's step, so the
+ratio is work-normalised even though the CPU runs a smaller sample.
+  value : inputs resident in HBM (A's device CSR and block-scatter arrays
+          cached on the device, b a device tensor, x left on the device);
+  e2e   : the public API from host buffers (a fresh SparseSymMatrix and a
+          NumPy b every step, x returned to the host): host->device copies
+          of A and b and the device->host copy of x inside the timed region.
+Timing: barrier + cuda.synchronize on both sides of the K timed steps,
+CUDA events on the launching stream, max over ranks; L2 flushed (256 MiB
+write) between steps; the factor (> 2 GB) exceeds L2 anyway.
+N > 1: replicas only (the path does not shard): every rank
+factors and solves its own copy; value = N * n / max-rank step time.
+
+--impl reference: the CPU oracle port (oracle/spand_oracle.py, a bitwise
+restatement of the reference spdkit, see tests/test_oracle_golden.py) on a
+bounded sample of the same workload family, all host threads, rank 0 only.
+"""
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, HERE)
+
+METRIC = ("spaND factorize+PCG-solve FP64 throughput (algorithmic GFLOP/s: "
+          "F_elim+F_scale+F_rrqr+apply+SpMV per step / step time)")
+FP64_PEAK_TFLOPS = 36.5   # measured DFMA loop on this pool's B200, profiles/fp64_peak_r01.jsonl
+SAMPLE = {"grid": 24, "block": 8, "levels": 11, "seed": 3}
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=3)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--config", default="C4")
+    p.add_argument("--levels", type=int, default=None)
+    p.add_argument("--eps", type=float, default=1e-2)
+    p.add_argument("--scheme", default="second-full")
+    p.add_argument("--tol", type=float, default=1e-12)
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    return p.parse_args()
+
+
+def dist_init(args):
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def peaks():
+    try:
+        with open(os.path.join(HERE, "MEASURED_PEAKS.json")) as fh:
+            return json.load(fh), "measured"
+    except OSError:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback"
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (clocks + throttle reasons)."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(
+                    ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                     "--format=csv,noheader,nounits"],
+                    capture_output=True, text=True, timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=6)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for s in self.samples:
+            for nm, v in zip(names, s[3:7]):
+                if v.strip().lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.samples)}
+
+
+def problem(args):
+    import paper_2007_00789_b200 as sp
+    a, b, lv = sp.baseline_problem(args.config)
+    return a, b, (args.levels or lv)
+
+
+def sample_problem():
+    """Bounded CPU sample of the C4 family: same generator and seeding
+    convention on a 24^3 grid (3x3x3 blocks of 8^3 cells), levels 11."""
+    import paper_2007_00789_b200.sparse as S
+    rng = np.random.default_rng(SAMPLE["seed"])
+    g = SAMPLE["grid"]
+    a = S.diffusion_fv(S.log_uniform_block_field((g, g, g), SAMPLE["block"], 3.0, rng))
+    b = rng.standard_normal(a.n)
+    return a, b, SAMPLE["levels"]
+
+
+def cpu_run(a, b, levels, eps, scheme, tol, threads):
+    """One factorize + PCG of the CPU oracle (timed, hierarchy excluded).
+    Returns (seconds, n_cg, algorithmic flops of the step)."""
+    from threadpoolctl import threadpool_limits
+    from oracle import spand_oracle as orc
+    from paper_2007_00789_b200.metrics import factor_flops, solve_flops
+    cl = orc.nd_hierarchy(a.n, a.row_ptr, a.col_idx, levels)
+    with threadpool_limits(limits=threads, user_api="blas"):
+        t0 = time.perf_counter()
+        f = orc.factorize(a.n, a.row_ptr, a.col_idx, a.values, cl, levels, eps,
+                          scheme, 4)
+        mv = orc.csr_matvec(a.n, a.row_ptr, a.col_idx, a.values)
+        _, its, _, _, _, _ = orc.pcg(mv, b, f.apply_m, tol)
+        dt = time.perf_counter() - t0
+    panels = [(op.dofs.size, op.n_cols, len(op.pivots)) for op in f.ops if op.kind == "Q"]
+    fl = factor_flops(f.ops, panels)["F_factor"] + solve_flops(f.nnz_factor, a.nnz,
+                                                                its + 1, its + 1)
+    return dt, its, fl
+
+
+def run_reference(args, rank):
+    if rank != 0:
+        return
+    a, b, lv = sample_problem()
+    threads = os.cpu_count() or 1
+    for _ in range(args.warmup):
+        cpu_run(a, b, lv, args.eps, args.scheme, args.tol, threads)
+    times = []
+    its = 0
+    fl = 0.0
+    for _ in range(args.steps):
+        dt, its, fl = cpu_run(a, b, lv, args.eps, args.scheme, args.tol, threads)
+        times.append(dt)
+    t = float(np.mean(times))
+    val = fl / t / 1e9
+    sample = (f"C4-family sample: 3D {SAMPLE['grid']}^3 high-contrast (n={a.n}), "
+              f"levels {lv}, eps {args.eps}, {args.scheme}, factorize+PCG(1e-12), "
+              f"n_cg {its}, mean of {args.steps} runs")
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC,
+        "value": val, "unit": "GFLOP/s", "higher_is_better": True,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1000 * t, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic",
+        "config": {"workload": sample, "parallelism": "cpu"},
+        "cpu_baseline": {"value": val, "unit": "GFLOP/s", "cores": threads,
+                         "kind": "port", "sample": sample},
+        "e2e": {"value": val, "unit": "GFLOP/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+def algorithmic_counts(f, a):
+    """Algorithmic work of one factorize/apply."""
+    diag = f.diagnostics
+    f_rrqr = 0.0
+    b_rrqr = 0.0
+    for lv in diag["levels"]:
+        for e in lv.get("margins", []):
+            m, k = e["size_before"], e["k_stop"]
+            n = e.get("n_cols", 0)
+            ks = np.arange(k, dtype=np.float64)
+            f_rrqr += float(np.sum(4 * (m - ks) * np.maximum(n - ks, 0) + 4 * m * (m - ks)))
+            b_rrqr += float(np.sum(16.0 * (m - ks) * np.maximum(n - ks, 0)))
+    b_apply = 16.0 * f.nnz_factor + 32.0 * a.n
+    b_spmv = 12.0 * a.nnz + 4.0 * (a.n + 1) + 16.0 * a.n
+    return {"F_rrqr": f_rrqr, "B_rrqr_step_traffic": b_rrqr, "B_apply": b_apply,
+            "B_spmv": b_spmv}
+
+
+def main():
+    args = parse()
+    rank, world, local = dist_init(args)
+    if args.impl == "reference":
+        run_reference(args, rank)
+        return
+    import torch
+    import paper_2007_00789_b200 as sp
+    from paper_2007_00789_b200 import _lib
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    a, b, levels = problem(args)
+    t0 = time.perf_counter()
+    h = sp.build_hierarchy(a, levels)
+    t_hier = time.perf_counter() - t0
+    bd = torch.from_numpy(b).cuda()
+    flush = torch.empty(256 * 2 ** 20 // 8, dtype=torch.float64, device="cuda")
+
+    def step_resident():
+        f = sp.factorize(a, h, args.eps, args.scheme)
+        x, rep = sp.pcg(a, bd, m=f.apply_m, tol=args.tol)
+        return f, rep
+
+    def step_e2e():
+        a2 = sp.SparseSymMatrix(a.n, a.row_ptr.copy(), a.col_idx.copy(), a.values.copy())
+        f = sp.factorize(a2, h, args.eps, args.scheme)
+        x, rep = sp.pcg(a2, b, m=f.apply_m, tol=args.tol)
+        return f, rep, x
+
+    def barrier():
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(v):
+        if dist is None:
+            return v
+        tv = torch.tensor([v], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tv, op=dist.ReduceOp.MAX)
+        return float(tv.item())
+
+    for _ in range(args.warmup):
+        step_resident()
+    # ---- timed region: K steps, inputs resident
+    barrier()
+    st = torch.cuda.current_stream()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    launches0 = _lib.launches()
+    step_ms = []
+    with Clocks(local) as clk, _lib.profile() as prof:
+        ev0.record(st)
+        for _ in range(args.steps):
+            flush.zero_()
+            s0 = torch.cuda.Event(enable_timing=True)
+            s1 = torch.cuda.Event(enable_timing=True)
+            s0.record(st)
+            f, rep = step_resident()
+            s1.record(st)
+            torch.cuda.synchronize()
+            step_ms.append(s0.elapsed_time(s1))
+        ev1.record(st)
+        barrier()
+    launches = _lib.launches() - launches0
+    total_ms = max_over_ranks(float(np.sum(step_ms)))
+    ms_step = total_ms / args.steps
+    # ---- e2e: public API from host buffers
+    e2e_ms = []
+    for _ in range(max(1, min(args.steps, 2))):
+        barrier()
+        t0 = time.perf_counter()
+        f2, rep2, x2 = step_e2e()
+        torch.cuda.synchronize()
+        e2e_ms.append(1000 * (time.perf_counter() - t0))
+    e2e_step = max_over_ranks(float(np.mean(e2e_ms)))
+    csr_bytes = 4 * (a.n + 1) + 12 * a.nnz
+    h2d = csr_bytes + 16 * a.nnz + 8 * a.n      # CSR + block-scatter (index, value) + b
+    d2h = 8 * a.n
+    # ---- roofline of the dominant kernel, from the timed-region events
+    kern = prof.result
+    dom = max(kern.items(), key=lambda kv: kv[1]["ms"])
+    counts = algorithmic_counts(f, a)
+    pk, pk_kind = peaks()
+    t_f = f.timings.get("total_s", 0.0)
+    if dom[0] == "spand_rrqr_wave":
+        per_launch_ms = dom[1]["ms"] / dom[1]["calls"]
+        bytes_step = counts["B_rrqr_step_traffic"]
+        achieved = bytes_step / (dom[1]["ms"] / args.steps / 1000.0) / 1e9
+        roof = {"kernel": dom[0], "bound": "hbm", "achieved": achieved,
+                "peak": pk["hbm_gbs"], "unit": "GB/s", "frac": achieved / pk["hbm_gbs"],
+                "peak_kind": pk_kind, "traffic": None,
+                "ms_per_step": dom[1]["ms"] / args.steps, "launches_per_step": dom[1]["calls"] / args.steps,
+                "basis": "16 B x (m-k)(n-k) per elimination step of every panel (1 read + 1 write of the trailing panel), summed over the step's panels"}
+    elif dom[0] == "spand_gemv_tiles":
+        achieved = counts["B_apply"] * (rep.n_cg + 1) / (dom[1]["ms"] / args.steps / 1000.0) / 1e9
+        roof = {"kernel": dom[0], "bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"],
+                "unit": "GB/s", "frac": achieved / pk["hbm_gbs"], "peak_kind": pk_kind,
+                "traffic": None, "basis": "B_apply = 16 nnz_factor + 32 n per apply_m"}
+    else:
+        roof = {"kernel": dom[0], "bound": "tensor", "achieved": None, "peak": FP64_PEAK_TFLOPS,
+                "unit": "TFLOP/s", "frac": None, "traffic": None}
+    prof_path = os.path.join(HERE, "profiles", "ncu_r01_summary.json")
+    if os.path.exists(prof_path):
+        try:
+            with open(prof_path) as fh:
+                roof["traffic"] = json.load(fh).get("traffic_per_launch")
+        except Exception:
+            pass
+    from paper_2007_00789_b200.metrics import (device_panels, factor_flops,
+                                               solve_flops)
+    ff = factor_flops(f.ops, device_panels(f))
+    f_step = ff["F_factor"] + solve_flops(f.nnz_factor, a.nnz, rep.n_cg + 1, rep.n_cg + 1)
+    # apply GB/s over the whole solve
+    apply_ms = kern.get("spand_gemv_tiles", {}).get("ms", 0.0) + kern.get("spand_apply_scatter", {}).get("ms", 0.0)
+    n_apply = (rep.n_cg + 1) * args.steps
+    apply_gbs = counts["B_apply"] * n_apply / (apply_ms / 1000.0) / 1e9 if apply_ms else None
+    line = {
+        "metric": METRIC, "value": world * f_step / (ms_step / 1000.0) / 1e9,
+        "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{args.config}: 3D 64^3 high-contrast harmonic FV, n={a.n}, "
+                               f"ND levels {levels}, eps {args.eps}, {args.scheme}, skip 4, "
+                               f"PCG tol {args.tol}, b~N(0,1) seed 3",
+                   "parallelism": "replicas" if world > 1 else "single",
+                   "l2": "flushed between steps (256 MiB write); factor > L2"},
+        "factorize_s": t_f, "solve_s": rep.solve_seconds, "n_cg": rep.n_cg,
+        "true_residual": rep.true_residual, "hierarchy_s": t_hier,
+        "nnz_factor": f.nnz_factor, "mu": f.nnz_factor / a.nnz,
+        "apply_gbs": apply_gbs,
+        "kernels_ms_per_step": {k: round(v["ms"] / args.steps, 3) for k, v in kern.items()},
+        "flops_per_step": ff | {"F_step": f_step},
+        "dof_per_s": world * a.n / (ms_step / 1000.0),
+        "e2e": {"value": world * f_step / (e2e_step / 1000.0) / 1e9, "unit": "GFLOP/s",
+                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+                "ms_per_step": e2e_step},
+        "roofline": roof, "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        sa, sb, slv = sample_problem()
+        dt, its, sfl = cpu_run(sa, sb, slv, args.eps, args.scheme, args.tol, 1)
+        line["cpu_baseline"] = {
+            "value": sfl / dt / 1e9, "unit": "GFLOP/s", "cores": 1, "kind": "port",
+            "sample": f"oracle port (bitwise restatement of spdkit) on a C4-family "
+                      f"24^3 sample (n={sa.n}, levels {slv}), factorize+PCG {dt:.2f} s, "
+                      f"n_cg {its}, OpenBLAS 1 thread"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

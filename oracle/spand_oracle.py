@@ -477,6 +477,7 @@ class _Trailing:
         ops = [Op("Q", old, q=np.hstack([res["q_f"], res["q_c"]]))]
         ops[0].pivots = res["pivots"][:res["k_stop"]]   # test-side metadata
         ops[0].k_c = res["rank_c"]
+        ops[0].n_cols = panel.shape[1]
         ncorr = res["e_tilde"].shape[0]
         if ncorr and res["e_tilde"].size:
             ops.append(Op("E", old[:ncorr], w_dofs, e_tilde=res["e_tilde"]))

@@ -420,8 +420,17 @@ class Engine:
         return temp
 
     def _scatter_a(self):
-        """Initial blocks from the entries of A (factorize.py:61-96)."""
+        """Initial blocks from the entries of A (factorize.py:61-96).
+
+        The (pool offset, value) pairs are cached on the matrix's device
+        cache per hierarchy, so refactorizing resident inputs does no
+        host->device traffic."""
         sym, a = self.sym, self.a
+        key = ("scatter", id(self.h), self.pool_size)
+        cached = a._dev.get(key) if a._dev is not None else None
+        if cached is not None and cached[0] is self.h:
+            self.pool[cached[1]] = cached[2]
+            return
         n = a.n
         rows = np.repeat(np.arange(n, dtype=np.int64), np.diff(a.row_ptr))
         cols = a.col_idx
@@ -440,8 +449,10 @@ class Engine:
         del bid_arr
         where = self.boff[pos] + slot[r] + slot[c] * sym.m0[ci]
         vals = a.values[up]
-        t = self.t
-        self.pool[to_dev(where, np.int64)] = to_dev(vals, np.float64)
+        wd, vd = to_dev(where, np.int64), to_dev(vals, np.float64)
+        self.pool[wd] = vd
+        if a._dev is not None:
+            a._dev[key] = (self.h, wd, vd)
 
     # --------------------------------------------------------------- collect
     def collect(self):
@@ -539,7 +550,7 @@ class Engine:
                                   "size_after": int(k_c), "rank_f2": int(rf2),
                                   "eta_stop": float(np.int64(e[7]).view(np.float64)),
                                   "r11": float(np.int64(e[8]).view(np.float64)),
-                                  "k_stop": int(k_stop)})
+                                  "k_stop": int(k_stop), "n_cols": int(e[2])})
                     off[p] += n_fine
             digest = hashlib.sha256(repr([(f["cluster"], f["size_before"],
                                            f["size_after"], f["rank_f2"])
