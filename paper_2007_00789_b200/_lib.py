@@ -80,7 +80,7 @@ _HOST_ONLY = {"spand_nd_partition", "spand_version", "spand_device_sm_count",
 def call(name, *args):
     """Invoke an entry point; nonzero status raises RuntimeError."""
     fn = getattr(load(), name)
-    if _PROFILE is not None and name not in _HOST_ONLY:
+    if _PROFILE is not None and name not in _HOST_ONLY and not _capturing():
         import torch
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
@@ -95,6 +95,11 @@ def call(name, *args):
     if name not in _HOST_ONLY:
         COUNTS[name] = COUNTS.get(name, 0) + 1
     return st
+
+
+def _capturing():
+    import torch
+    return torch.cuda.is_current_stream_capturing()
 
 
 def launches():

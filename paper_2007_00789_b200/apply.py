@@ -21,7 +21,7 @@ scatter (spand_apply_scatter).  The result is deterministic run to run.
 import numpy as np
 
 from . import _lib
-from .device import dev, ptr, require_cuda, stream, to_dev
+from .device import dev, ptr, require_cuda, stream, to_dev, to_dev_async
 from .schemes import MatView, OpKind
 
 TILE_OUT = 64
@@ -29,12 +29,13 @@ TILE_K = 2048
 
 
 class _Micro:
-    __slots__ = ("reads", "writes", "accs", "tasks", "mode")
+    __slots__ = ("reads", "writes", "accs", "tasks", "mode", "phase")
 
     def __init__(self, reads, writes, accs, tasks, mode):
         self.reads, self.writes, self.accs = reads, writes, accs
         self.tasks = tasks        # [(MatView, optrans, in_dofs, out_dofs)]
         self.mode = mode          # 0 overwrite-with-sum, 1 subtract-sum
+        self.phase = None         # structural phase (engine factors) or None
 
 
 def _views(op):
@@ -90,6 +91,13 @@ def _micro_ops(op, backward):
                 out.append(_Micro(w, None, s, tasks, 1))
             else:
                 out.append(_Micro(s, None, w, tasks, 1))
+    # structural phases supplied by the engine: "T" (transform) and "A"
+    # (accumulate) micro-ops of this operator in this direction
+    ph = getattr(op, "_phases", None)
+    if ph is not None:
+        key = 1 if backward else 0
+        for m in out:
+            m.phase = ph[key]["T" if m.writes is not None else "A"]
     # drop empty transforms (0-sized blocks)
     return [m for m in out if m.tasks and (m.writes is None or m.writes.size)]
 
@@ -129,7 +137,14 @@ class _Pass:
         if not micro:
             self.scratch_len = 0
             return
-        ph = _schedule(micro, n)
+        if all(m.phase is not None for m in micro):
+            # engine factors: phases follow the level / wave structure
+            # (same dependency order as the sequential reference, no search)
+            ph = np.asarray([m.phase for m in micro], dtype=np.int64)
+            uniq = np.unique(ph)
+            ph = np.searchsorted(uniq, ph)
+        else:
+            ph = _schedule(micro, n)
         nph = int(ph.max()) + 1
         by_phase = [[] for _ in range(nph)]
         for i, p in enumerate(ph):
@@ -138,9 +153,9 @@ class _Pass:
         scratch_len = 0
         for plist in by_phase:
             tiles = []
-            dst_parts, src_parts, mode_parts, key_parts = [], [], [], []
+            dst_parts, lens, modes = [], [], []
             pos = 0
-            for seq, m in enumerate(plist):
+            for m in plist:
                 for (v, optrans, in_dofs, out_dofs) in m.tasks:
                     trans = bool(v.trans) != bool(optrans)
                     nout = v.cols if trans else v.rows
@@ -150,42 +165,44 @@ class _Pass:
                     tid = len(task_rows)
                     task_rows.append([v.addr, v.ld, v.rows, v.cols, int(trans),
                                       v.rot, 0, idx_pool.addr(in_dofs)])
+                    nkt = max(1, -(-nk // TILE_K))
                     for ob in range(0, nout, TILE_OUT):
                         oc = min(TILE_OUT, nout - ob)
-                        kbs = range(0, max(nk, 1), TILE_K)
-                        for kb in kbs:
-                            kc = min(TILE_K, nk - kb)
-                            tiles.append([tid, ob, oc, kb, kc, pos, 0, 0])
-                            dst_parts.append(out_dofs[ob:ob + oc])
-                            src_parts.append(np.arange(pos, pos + oc))
-                            key_parts.append(np.full(oc, seq))
-                            mode_parts.append(m.mode)
+                        for kb in range(0, nkt * TILE_K, TILE_K):
+                            tiles.append([tid, ob, oc, kb, min(TILE_K, nk - kb) if nk else 0,
+                                          pos, 0, 0])
                             pos += oc
+                    if nkt == 1:
+                        dst_parts.append(out_dofs[:nout])
+                    else:
+                        dst_parts.append(np.concatenate(
+                            [np.tile(out_dofs[ob:ob + TILE_OUT], nkt)
+                             for ob in range(0, nout, TILE_OUT)]))
+                    lens.append(nout * nkt)
+                    modes.append(m.mode)
             scratch_len = max(scratch_len, pos)
             tile_lists.append(np.asarray(tiles, dtype=np.int64).reshape(-1, 8))
             if dst_parts:
                 dst = np.concatenate(dst_parts)
-                src = np.concatenate(src_parts)
-                key = np.concatenate(key_parts)
-                mode = np.concatenate([np.full(len(d), md, np.int8) for d, md
-                                       in zip(dst_parts, mode_parts)])
-                order = np.lexsort((key, dst))  # stable: sequence order kept
+                src = np.arange(dst.size, dtype=np.int64)   # tiles are laid out in order
+                mode = np.repeat(np.asarray(modes, dtype=np.int8), lens)
+                order = np.argsort(dst, kind="stable")      # keeps sequence order
                 dst, src, mode = dst[order], src[order], mode[order]
                 first = np.r_[True, dst[1:] != dst[:-1]]
                 starts = np.flatnonzero(first)
                 ptrs = np.r_[starts, dst.size].astype(np.int64)
                 scat.append((dst[starts].astype(np.int32), mode[starts],
-                             ptrs, src.astype(np.int64)))
+                             ptrs, src))
             else:
                 scat.append(None)
         self.scratch_len = scratch_len
-        self.tasks = to_dev(np.asarray(task_rows, dtype=np.int64).reshape(-1, 8))
+        self.tasks = to_dev_async(np.asarray(task_rows, dtype=np.int64).reshape(-1, 8))
         for tl, sc in zip(tile_lists, scat):
             if tl.shape[0] == 0:
                 continue
             dst, mode, ptrs, src = sc
-            self.phases.append((to_dev(tl), tl.shape[0], to_dev(dst),
-                                to_dev(mode), to_dev(ptrs), to_dev(src),
+            self.phases.append((to_dev_async(tl), tl.shape[0], to_dev_async(dst),
+                                to_dev_async(mode), to_dev_async(ptrs), to_dev_async(src),
                                 dst.size))
 
     def run(self, x, scratch, ldx, ldscr, nvec):
@@ -249,6 +266,7 @@ class ApplyPlan:
         self.bwd = _Pass(self.n, bwd, pool)
         self.scratch_len = max(self.fwd.scratch_len, self.bwd.scratch_len, 1)
         self._scratch = None
+        self._graph = None
 
     @property
     def launches(self):
@@ -260,6 +278,29 @@ class ApplyPlan:
         if self._scratch is None or self._scratch.numel() < need:
             self._scratch = t.empty(need, dtype=t.float64, device=dev())
         return self._scratch
+
+    def run_graph(self, xd):
+        """apply_m in place on a contiguous (n,) fp64 device tensor through a
+        CUDA graph of the whole pass (captured on first use: ~2 launches
+        per phase collapse into one graph launch)."""
+        t = require_cuda()
+        if self._graph is None:
+            self._xbuf = t.zeros(self.n, dtype=t.float64, device=dev())
+            scr = self._scr(1)
+            side = t.cuda.Stream()
+            side.wait_stream(t.cuda.current_stream())
+            g = t.cuda.CUDAGraph()
+            with t.cuda.graph(g, stream=side):
+                self.fwd.run(self._xbuf, scr, self.n, self.scratch_len, 1)
+                self.bwd.run(self._xbuf, scr, self.n, self.scratch_len, 1)
+            t.cuda.current_stream().wait_stream(side)
+            self._graph = g
+        self._xbuf.copy_(xd)
+        self._graph.replay()
+        _lib.COUNTS["apply_graph_kernels"] = (_lib.COUNTS.get("apply_graph_kernels", 0)
+                                              + self.launches)
+        xd.copy_(self._xbuf)
+        return xd
 
     def run(self, xd, forward=True, backward=True):
         """In-place on a device tensor of shape (n,) or (n, k) (fp64)."""

@@ -55,6 +55,18 @@ def to_dev(arr, dtype=None):
     return t.from_numpy(a).to(dev(), non_blocking=False)
 
 
+def to_dev_async(arr, dtype=None):
+    """numpy -> device tensor without blocking the host: the array is
+    staged in (cached) pinned memory and copied with non_blocking=True on the
+    current stream, so host-side planning overlaps device work.  The caching
+    host allocator keeps the staging block until the copy has completed."""
+    t = torch()
+    a = np.ascontiguousarray(arr if dtype is None else arr.astype(dtype))
+    if a.nbytes == 0:
+        return t.from_numpy(a).to(dev())
+    return t.from_numpy(a).pin_memory().to(dev(), non_blocking=True)
+
+
 def as_device_vector(x, n):
     """Accept numpy or torch input of shape (n,) or (n, k); return a
     contiguous fp64 device tensor and a tag telling how to hand back."""

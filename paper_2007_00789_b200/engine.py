@@ -36,7 +36,7 @@ import numpy as np
 
 from . import _lib
 from .dense import SCHEME_CODE, SchemeKind
-from .device import dev, ptr, require_cuda, stream, to_dev
+from .device import dev, ptr, require_cuda, stream, to_dev, to_dev_async
 from .errors import NotSPD
 from .kernels import Geometry, TILE, opnd
 from .schemes import (Elimination, ErrorCorrection, MatView, Orthogonal,
@@ -319,9 +319,9 @@ class Engine:
         fin = sym.final
         if fin:
             index = {c: k for k, c in enumerate(fin)}
-            cl = to_dev(np.asarray(fin, dtype=np.int64))
+            cl = to_dev_async(np.asarray(fin, dtype=np.int64))
             rows = [[index[i], index[j], blk(i, j), 0] for i, j in sym.final_blocks]
-            brows = to_dev(np.asarray(rows, dtype=np.int64).reshape(-1, 4))
+            brows = to_dev_async(np.asarray(rows, dtype=np.int64).reshape(-1, 4))
             _lib.call("spand_assemble_final", len(fin), ptr(cl), len(rows),
                       ptr(brows), ptr(geo.m0), ptr(geo.off), F,
                       ctypes_ptr(fb + 8 * self.f_off), stream())
@@ -402,8 +402,8 @@ class Engine:
             if vmax > MAX_PANEL_ROWS:
                 raise NotImplementedError(
                     f"interface of {vmax} dofs exceeds the RRQR kernel limit")
-            pd = to_dev(np.asarray(prow, dtype=np.int64).reshape(-1, RRQR_ROW))
-            nd = to_dev(np.asarray(nrow if nrow else [[0, 0, 0, 0]],
+            pd = to_dev_async(np.asarray(prow, dtype=np.int64).reshape(-1, RRQR_ROW))
+            nd = to_dev_async(np.asarray(nrow if nrow else [[0, 0, 0, 0]],
                                    dtype=np.int64).reshape(-1, 4))
             if WAVE_LOG is not None:
                 e0 = t.cuda.Event(enable_timing=True)
@@ -449,7 +449,7 @@ class Engine:
         del bid_arr
         where = self.boff[pos] + slot[r] + slot[c] * sym.m0[ci]
         vals = a.values[up]
-        wd, vd = to_dev(where, np.int64), to_dev(vals, np.float64)
+        wd, vd = to_dev_async(where, np.int64), to_dev_async(vals, np.float64)
         self.pool[wd] = vd
         if a._dev is not None:
             a._dev[key] = (self.h, wd, vd)
@@ -484,7 +484,32 @@ class Engine:
             return MatView(fac, at + off[c] + off[c] * m0[c], m0[c], size, size)
 
         scheme = self.scheme
-        for rec in sym.level_recs:
+        # structural apply phases (see apply.py): forward per level
+        # [G-T][G-A]([D]([Q-T][E-A]) per wave); backward mirrored
+        recs = sym.level_recs
+        cnt = [2 + (0 if r["skipped"] else 1 + 2 * r["nwaves"]) for r in recs]
+        fbase = np.concatenate([[0], np.cumsum(cnt)]).astype(int)
+        bbase = [1 + int(sum(cnt[i + 1:])) for i in range(len(recs))]
+        self.n_phases = int(fbase[-1]) + 1
+        wave_of = {}
+        for r in recs:
+            for p, _, wv in r.get("spars", []):
+                wave_of[(r["level"], p)] = wv
+
+        def phases(ri, kind, wave=0):
+            r, fb, bb = recs[ri], int(fbase[ri]), bbase[ri]
+            nw = 0 if r["skipped"] else r["nwaves"]
+            if kind == "G":
+                return ({"T": fb, "A": fb + 1},
+                        {"A": bb + (2 * nw + 1 if not r["skipped"] else 0),
+                         "T": bb + (2 * nw + 2 if not r["skipped"] else 1)})
+            if kind == "D":
+                return ({"T": fb + 2}, {"T": bb + 2 * nw})
+            back = bb + 2 * (nw - 1 - wave)
+            return ({"T": fb + 3 + 2 * wave, "A": fb + 4 + 2 * wave},
+                    {"A": back, "T": back + 1})
+
+        for ri, rec in enumerate(sym.level_recs):
             lvl = rec["level"]
             nint, ndofs = 0, 0
             for s, nbrs in rec["elim"]:
@@ -504,6 +529,7 @@ class Engine:
                 low = bview(s, s, off[s], off[s], ns, ns)
                 linv = fview(self.linv_off[s], s, ns)
                 op = Elimination(live(s), w_dofs, low, pv, linv=linv)
+                op._phases = phases(ri, "G")
                 ops.append(op)
                 perm_parts.append(live(s))
             faces = []
@@ -512,8 +538,9 @@ class Engine:
                 for p in act:
                     lo = self.resc_off[(lvl, p)]
                     mp = m0[p] - off[p]
-                    ops.append(Scaling(live(p), fview(lo[0], p, mp),
-                                       linv=fview(lo[1], p, mp)))
+                    op = Scaling(live(p), fview(lo[0], p, mp), linv=fview(lo[1], p, mp))
+                    op._phases = phases(ri, "D")
+                    ops.append(op)
                 nbr_of = {p: nb for p, nb, _ in rec["spars"]}
                 for p in act:
                     e = ev[self.event_slot[(lvl, p)]]
@@ -523,7 +550,9 @@ class Engine:
                     old = live(p)
                     q = MatView(fac, self.q_off[(lvl, p)], max(mp, 1), mp, mp,
                                 rot=k_c if mp else 0)
-                    ops.append(Orthogonal(old, q))
+                    qop = Orthogonal(old, q)
+                    qop._phases = phases(ri, "Q", wave_of[(lvl, p)])
+                    ops.append(qop)
                     if scheme is SchemeKind.SECOND_ORDER_FULL:
                         ncorr = n_fine
                     elif scheme is SchemeKind.SECOND_ORDER_SUPERFINE:
@@ -543,7 +572,9 @@ class Engine:
                             evs.append((v, c0))
                             c0 += nw
                         w_dofs = np.concatenate([live(w) for w in wl])
-                        ops.append(ErrorCorrection(old[:ncorr], w_dofs, evs))
+                        eop = ErrorCorrection(old[:ncorr], w_dofs, evs)
+                        eop._phases = qop._phases
+                        ops.append(eop)
                     if n_fine:
                         perm_parts.append(old[:n_fine])
                     faces.append({"cluster": int(p), "size_before": int(mp),
@@ -571,7 +602,10 @@ class Engine:
             linv = MatView(fac, self.flinv_off + foff + foff * self.fcap, self.fcap,
                            total, total)
             fd = np.concatenate([live(c) for c in fin])
-            ops.append(Elimination(fd, np.empty(0, np.int64), low, [], linv=linv))
+            fop = Elimination(fd, np.empty(0, np.int64), low, [], linv=linv)
+            fop._phases = ({"T": self.n_phases - 1, "A": self.n_phases - 1},
+                           {"T": 0, "A": 0})
+            ops.append(fop)
             perm_parts.append(fd)
         perm = (np.concatenate(perm_parts) if perm_parts else np.empty(0, np.int64))
         nnz = self._count(ops)

@@ -65,7 +65,9 @@ class Factorization:
         return self._run(x, True, True)
 
     def apply_m_device(self, xd):
-        """In-place M x on a contiguous fp64 CUDA tensor (no copies)."""
+        """In-place M x on a contiguous fp64 CUDA vector (graph replay)."""
+        if xd.dim() == 1:
+            return self.plan.run_graph(xd)
         return self.plan.run(xd)
 
 

@@ -9,7 +9,7 @@ run a single task (the reference's per-block dense API in ``dense.py``).
 import numpy as np
 
 from . import _lib
-from .device import dev, ptr, require_cuda, stream, to_dev
+from .device import dev, ptr, require_cuda, stream, to_dev, to_dev_async
 
 
 def opnd(p, rc, cc, rskip=0, cskip=0, rcount=-1, ccount=-1):
@@ -35,7 +35,7 @@ class Geometry:
 
 
 def _rows(rows, width):
-    return to_dev(np.asarray(rows, dtype=np.int64).reshape(-1, width))
+    return to_dev_async(np.asarray(rows, dtype=np.int64).reshape(-1, width))
 
 
 def potrf_batched(geo, ops, info):
@@ -119,6 +119,25 @@ def copy_batched(geo, tasks):
 TILE = 64
 
 
+def _tile_grid(mm, nn, lower_only=False):
+    """All (target, i0, j0) 64x64 tiles of targets with extents mm x nn."""
+    tm = np.maximum(-(-mm // TILE), 0)
+    tn = np.maximum(-(-nn // TILE), 0)
+    cnt = tm * tn
+    tot = int(cnt.sum())
+    if tot == 0:
+        return np.zeros((0, 3), dtype=np.int64)
+    tgt = np.repeat(np.arange(mm.size, dtype=np.int64), cnt)
+    local = np.arange(tot, dtype=np.int64) - np.repeat(np.cumsum(cnt) - cnt, cnt)
+    ntile_n = np.repeat(tn, cnt)
+    i0 = (local // ntile_n) * TILE
+    j0 = (local % ntile_n) * TILE
+    out = np.stack([tgt, i0, j0], axis=1)
+    if lower_only:
+        out = out[j0 <= i0]
+    return out
+
+
 def gemm_grouped(geo, targets, alpha, beta, bT, lower_only=False,
                  max_rows=None, max_cols=None):
     """targets: [(C operand, [(A operand, B operand), ...], (max_m, max_n))].
@@ -127,23 +146,22 @@ def gemm_grouped(geo, targets, alpha, beta, bT, lower_only=False,
     target's live size exit immediately on the device."""
     if not targets:
         return
-    trow, srow, tiles = [], [], []
-    for t, (c, segs, (mm, nn)) in enumerate(targets):
+    trow, srow = [], []
+    mm = np.empty(len(targets), dtype=np.int64)
+    nn = np.empty(len(targets), dtype=np.int64)
+    for t, (c, segs, (mt, nt)) in enumerate(targets):
         trow.append(c + [len(srow)])
         for a, b in segs:
             srow.append(a + b)
-        for i in range(0, max(mm, 0), TILE):
-            for j in range(0, max(nn, 0), TILE):
-                if lower_only and j > i:
-                    continue
-                tiles.append([t, i, j])
+        mm[t], nn[t] = mt, nt
     trow.append([0] * 7 + [len(srow)])
-    if not tiles:
+    tiles = _tile_grid(mm, nn, lower_only)
+    if tiles.shape[0] == 0:
         return
     if not srow:
         srow.append([0] * 14)
     td, sd, tl = _rows(trow, 8), _rows(srow, 14), _rows(tiles, 3)
-    _lib.call("spand_gemm_grouped", len(tiles), ptr(tl), ptr(td), ptr(sd),
+    _lib.call("spand_gemm_grouped", int(tiles.shape[0]), ptr(tl), ptr(td), ptr(sd),
               ptr(geo.m0), ptr(geo.off), float(alpha), float(beta), int(bT),
               int(bool(lower_only)), stream())
 
