@@ -509,6 +509,17 @@ class Engine:
             return ({"T": fb + 3 + 2 * wave, "A": fb + 4 + 2 * wave},
                     {"A": back, "T": back + 1})
 
+        # apply records in the cluster-contiguous (permuted) numbering used by
+        # the fast apply plan (fastplan.py): cluster c's slots live at
+        # cstart[c] + [off[c], m0[c])
+        cstart = np.concatenate([[0], np.cumsum(m0)[:-1]]).astype(np.int64)
+        self.cstart = cstart
+        arecs = []
+        self.arecs = arecs
+
+        def pst(c):
+            return int(cstart[c] + off[c])
+
         for ri, rec in enumerate(sym.level_recs):
             lvl = rec["level"]
             nint, ndofs = 0, 0
@@ -531,6 +542,8 @@ class Engine:
                 op = Elimination(live(s), w_dofs, low, pv, linv=linv)
                 op._phases = phases(ri, "G")
                 ops.append(op)
+                arecs.append(("G", op._phases, pst(s), int(ns), linv,
+                              [(pst(w), int(v.rows), v) for w, (v, _) in zip(wl, pv)]))
                 perm_parts.append(live(s))
             faces = []
             if not rec["skipped"]:
@@ -541,6 +554,7 @@ class Engine:
                     op = Scaling(live(p), fview(lo[0], p, mp), linv=fview(lo[1], p, mp))
                     op._phases = phases(ri, "D")
                     ops.append(op)
+                    arecs.append(("D", op._phases, pst(p), int(mp), op.linv_view))
                 nbr_of = {p: nb for p, nb, _ in rec["spars"]}
                 for p in act:
                     e = ev[self.event_slot[(lvl, p)]]
@@ -553,6 +567,7 @@ class Engine:
                     qop = Orthogonal(old, q)
                     qop._phases = phases(ri, "Q", wave_of[(lvl, p)])
                     ops.append(qop)
+                    arecs.append(("Q", qop._phases, pst(p), int(mp), q))
                     if scheme is SchemeKind.SECOND_ORDER_FULL:
                         ncorr = n_fine
                     elif scheme is SchemeKind.SECOND_ORDER_SUPERFINE:
@@ -575,6 +590,9 @@ class Engine:
                         eop = ErrorCorrection(old[:ncorr], w_dofs, evs)
                         eop._phases = qop._phases
                         ops.append(eop)
+                        arecs.append(("E", qop._phases, pst(p), int(ncorr),
+                                      [(pst(w), int(m0[w] - off[w]), v)
+                                       for w, (v, _) in zip(wl, evs)]))
                     if n_fine:
                         perm_parts.append(old[:n_fine])
                     faces.append({"cluster": int(p), "size_before": int(mp),
@@ -606,6 +624,8 @@ class Engine:
             fop._phases = ({"T": self.n_phases - 1, "A": self.n_phases - 1},
                            {"T": 0, "A": 0})
             ops.append(fop)
+            fidx = np.concatenate([np.arange(pst(c), cstart[c] + m0[c]) for c in fin])
+            arecs.append(("F", fop._phases, fidx, total, linv))
             perm_parts.append(fd)
         perm = (np.concatenate(perm_parts) if perm_parts else np.empty(0, np.int64))
         nnz = self._count(ops)
@@ -652,4 +672,12 @@ def run_factorization(a, h, eps, scheme, skip_levels, collect_local_errors=False
                       skip_levels=int(skip_levels), nnz_factor=int(nnz),
                       diagnostics=diag,
                       _keep=(eng.pool, eng.facbuf, eng.geo), timings=eng.timings)
+    perm_c = np.concatenate(eng.sym.dofs) if eng.sym.dofs else np.empty(0, np.int64)
+    arecs, nph = eng.arecs, eng.n_phases
+
+    def factory():
+        from .fastplan import FastPlan
+        return FastPlan(a.n, perm_c, arecs, nph)
+
+    f._plan_factory = factory
     return f

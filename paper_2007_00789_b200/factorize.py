@@ -42,12 +42,18 @@ class Factorization:
     _plan: object = field(default=None, repr=False, compare=False)
     _keep: object = field(default=None, repr=False, compare=False)
     timings: dict | None = field(default=None, repr=False, compare=False)
+    _plan_factory: object = field(default=None, repr=False, compare=False)
 
     @property
     def plan(self):
+        """Device apply plan: the structured fast plan for factors built by
+        the engine, the generic scheduled plan for loaded factors."""
         if self._plan is None:
-            from .apply import ApplyPlan
-            self._plan = ApplyPlan(self.n, self.ops)
+            if self._plan_factory is not None:
+                self._plan = self._plan_factory()
+            else:
+                from .apply import ApplyPlan
+                self._plan = ApplyPlan(self.n, self.ops)
         return self._plan
 
     def _run(self, x, fwd, bwd):

@@ -20,6 +20,6 @@ e1.record(); torch.cuda.synchronize()
 ms = e0.elapsed_time(e1) / 10
 from paper_2007_00789_b200.metrics import apply_bytes
 B = apply_bytes(f.nnz_factor, a.n)
-print(json.dumps({"plan_s": t_plan, "launches": plan.launches, "phases": (len(plan.fwd.phases), len(plan.bwd.phases)), "apply_ms_graph": ms, "GBs": B / ms / 1e6, "B_apply_GB": B / 1e9}))
+print(json.dumps({"plan_s": t_plan, "launches": plan.launches, "apply_ms_graph": ms, "GBs": B / ms / 1e6, "B_apply_GB": B / 1e9}))
 t0 = time.perf_counter(); xs, rep = sp.pcg(a, bd, m=f.apply_m, tol=1e-12); torch.cuda.synchronize()
 print("pcg", rep.n_cg, time.perf_counter() - t0)
