@@ -23,6 +23,7 @@
 // formulas; only summation order differs, so ranks match except within
 // ~1e-15 relative of a threshold (the events record the margins).
 #include <cooperative_groups.h>
+#include <cstdio>
 
 #include "common.cuh"
 #include "../../include/spand_b200.h"
@@ -43,7 +44,14 @@ constexpr int kMaxM = 6144;  // v in shared memory
 // event row (12 int64): {p, m, n, k_stop, k_c, rank_f2, n_fine,
 //  bits(eta_stop), bits(r11), 0, 0, 0}
 
+constexpr int kBB = 32;        // reflectors per delayed block update
+constexpr int kCR = kBB + 2;   // candidate record (doubles)
+
 struct Sh {
+  double g[kBB];
+  double vk[kBB + 1];
+  double wrow[kBB];
+  double fw[kWarps][kBB];
   double red[kWarps];
   double bval[kWarps];
   int64_t bpos[kWarps];
@@ -57,7 +65,8 @@ __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
   return v;
 }
 
-__device__ __forceinline__ void group_barrier(unsigned* ctr, int G, unsigned& gen) {
+__device__ __forceinline__ void group_barrier(unsigned* ctr, int G, unsigned& gen,
+                                              int tag = -1, int64_t* flag = nullptr) {
   __syncthreads();
   if (G > 1) {
     if (threadIdx.x == 0) {
@@ -65,7 +74,16 @@ __device__ __forceinline__ void group_barrier(unsigned* ctr, int G, unsigned& ge
       ++gen;
       atomicAdd(ctr, 1u);
       const unsigned target = gen * (unsigned)G;
+      const long long t0 = clock64();
       while (ld_acquire(ctr) < target) {
+        // watchdog: a group that never completes a barrier is a bug; report
+        // and fall through (~2 s) instead of hanging the device
+        if (clock64() - t0 > 4000000000ll) {
+          printf("[spand rrqr] barrier timeout block %d tag %d gen %u ctr %u G %d\n",
+                 (int)blockIdx.x, tag, gen, ld_acquire(ctr), G);
+          if (flag) atomicExch(reinterpret_cast<unsigned long long*>(flag), 1ull);
+          break;
+        }
       }
       __threadfence();
     }
@@ -125,12 +143,13 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
   double* cur = aux;
   double* ref = aux + ncap;
   double* piv = aux + 2 * ncap;
-  // candidates, double-buffered by step parity: value, position, column
-  double* cand_v = aux + 2 * ncap + mcap;                      // 2G values
-  int64_t* cand_p = reinterpret_cast<int64_t*>(cand_v + 2 * G);  // 2G (pos << 32 | col)
-  double* betas = reinterpret_cast<double*>(cand_p + 2 * G);   // mcap
+  // candidates, double-buffered by step parity (kCR doubles each)
+  double* betas = aux + 2 * ncap + mcap;                       // mcap
   double* taus = betas + mcap;                                 // mcap
+  double* cand = taus + mcap;                                  // 2 G kCR
   double* V = W + (int64_t)mcap * ncap;                        // m x kmax reflectors
+  double* Fb = V + (int64_t)mcap * mcap;                       // ncap x kBB (block F)
+  double* pf = Fb + (int64_t)ncap * kBB;                       // mcap x kBB (F rows at pivot)
   int32_t* perm = iaux;
   int32_t* pos = iaux + ncap;
   int32_t* done = iaux + 2 * ncap;
@@ -211,7 +230,8 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
       }
     }
   }
-  auto publish = [&](double v, int64_t ps, int c, int parity) {
+  // candidate record: {value, (pos << 32 | col), F row of that column (jn)}
+  auto publish = [&](double v, int64_t ps, int c, int parity, int jn) {
     if (lane == 0) {
       sh.bval[warp] = v;
       sh.bpos[warp] = ps;
@@ -228,37 +248,57 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
           pp = sh.bpos[q];
           cc = sh.bcol[q];
         }
-      cand_v[parity * G + rank] = vv;
-      cand_p[parity * G + rank] = (pp << 32) | (int64_t)(uint32_t)cc;
+      sh.bcol[0] = cc;
+      double* rec = cand + (int64_t)(parity * G + rank) * kCR;
+      rec[0] = vv;
+      reinterpret_cast<int64_t*>(rec)[1] = (pp << 32) | (int64_t)(uint32_t)cc;
     }
+    __syncthreads();
+    const int cc = sh.bcol[0];
+    if (tid < jn && cc >= 0) cand[(int64_t)(parity * G + rank) * kCR + 2 + tid] = Fb[(int64_t)cc * kBB + tid];
+    __syncthreads();
   };
-  publish(bv, bp, bc, 0);
-  group_barrier(ctr, G, gen);
+  publish(bv, bp, bc, 0, 0);
+  group_barrier(ctr, G, gen, -1, events + 12 * slot + 9);
 
+  // ---- blocked elimination: the trailing matrix is updated only every kBB
+  // steps (A <- A - V_blk F^T, LAPACK dlaqps style); in between, each step
+  // needs one read of the owned columns (F column = tau v^T A_current) and
+  // the pivot column is rebuilt from A, V and the winner's F row.
   const double stop_tol = (scheme == 2) ? eps * eps : eps;
   double r11 = 0.0, eta_last = 0.0;
-  int k = 0;
+  int k = 0, k0 = 0;
   while (k < kmax) {
+    const int jb = k - k0;  // reflectors of the current block before this step
     // ---- winning column: max value, smallest current position
     double wv = -1.0;
     int64_t wp = 0x7fffffffffffLL, wpc = 0;
+    int wq = 0;
     const int par = k & 1;
     for (int q = 0; q < G; ++q) {
-      const double v = __ldcg(cand_v + par * G + q);
-      const int64_t pc = __ldcg(reinterpret_cast<const long long*>(cand_p) + par * G + q);
+      const double* rec = cand + (int64_t)(par * G + q) * kCR;
+      const double v = __ldcg(rec);
+      const int64_t pc = __ldcg(reinterpret_cast<const long long*>(rec) + 1);
       const int64_t ps = pc >> 32;
       if (better(v, ps, wv, wp)) {
         wv = v;
         wp = ps;
         wpc = pc;
+        wq = q;
       }
     }
     const int jpos = (int)wp;
     const int j = (int)(uint32_t)(wpc & 0xffffffffLL);
-    const double* colj = W + (int64_t)j * m;
+    if (tid < jb) sh.wrow[tid] = __ldcg(cand + (int64_t)(par * G + wq) * kCR + 2 + tid);
+    __syncthreads();
+    // pivot column as of this step: A[:, j] - V_blk F[j, :]^T, rows k..m-1
+    const int len = m - k;
+    const double* colj = W + (int64_t)j * m + k;
     double s = 0.0;
-    for (int i = k + tid; i < m; i += kT) {
-      const double x = __ldcg(colj + i);
+    for (int i = tid; i < len; i += kT) {
+      double x = __ldcg(colj + i);
+      for (int q = 0; q < jb; ++q) x -= __ldcg(V + (int64_t)(k0 + q) * m + k + i) * sh.wrow[q];
+      vsh[i] = x;
       s += x * x;
     }
     const double eta = sqrt(block_sum<kT>(s, sh.red));
@@ -268,135 +308,183 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
       if (r11 == 0.0) break;
     }
     if (eta < stop_tol * r11) break;
-    // ---- swap bookkeeping (reference: r[:, [k, j]], perm[[k, j]] ...):
-    // the column at position k moves to j's old position; owners update
-    // their own columns' positions (no shared permutation array)
+    // ---- swap bookkeeping (reference: r[:, [k, j]], perm[[k, j]] ...): the
+    // column at position k moves to j's old position; owners update their
+    // own columns' positions (no shared permutation array)
     const bool own_j = j >= c0 && j < c1;
-    if (tid == 0) {
-      if (own_j) {
+    if (own_j) {
+      if (tid == 0) {
         pos[j] = k;
         done[j] = 1;
       }
-      if (rank == 0) piv[k] = eta;
+      if (tid < jb) pf[(int64_t)k * kBB + tid] = sh.wrow[tid];
     }
+    if (rank == 0 && tid == 0) piv[k] = eta;
     __syncthreads();
     for (int c = c0 + tid; c < c1; c += kT)
       if (c != j && !done[c] && pos[c] == k) pos[c] = jpos;
+    // ---- reflector v = x - beta e1, beta = -sign(x0) eta (dense.py:155-159)
+    double beta = 0.0, tau = 0.0;
+    if (eta > 0.0) {
+      const double x0 = vsh[0];
+      beta = x0 >= 0.0 ? -eta : eta;
+      __syncthreads();
+      if (tid == 0) vsh[0] = x0 - beta;
+      __syncthreads();
+      double vv = 0.0;
+      for (int i = tid; i < len; i += kT) vv += vsh[i] * vsh[i];
+      tau = 2.0 / block_sum<kT>(vv, sh.red);
+    } else {
+      __syncthreads();
+      for (int i = tid; i < len; i += kT) vsh[i] = 0.0;
+    }
     __syncthreads();
+    if (rank == 0) {
+      for (int i = tid; i < len; i += kT) V[(int64_t)k * m + k + i] = vsh[i];
+      if (tid == 0) {
+        taus[k] = tau;
+        betas[k] = beta;
+      }
+    }
+    // g[q] = v^T v_q (rows k..), V row k of the block (and v[0] itself)
+    for (int q = warp; q < jb; q += kWarps) {
+      const double* vq = V + (int64_t)(k0 + q) * m + k;
+      double d = 0.0;
+      for (int i = lane; i < len; i += 32) d += vsh[i] * __ldcg(vq + i);
+      d = warp_sum(d);
+      if (lane == 0) {
+        sh.g[q] = d;
+        sh.vk[q] = __ldcg(vq);
+      }
+    }
+    if (tid == 0) sh.vk[jb] = vsh[0];
+    __syncthreads();
+    // ---- owned columns: F column, row-k entry, norm downdate / refresh
     bv = -1.0;
     bp = 0x7fffffffffffLL;
     bc = -1;
-    if (eta > 0.0) {
-      // ---- reflector v = x - beta e1, beta = -sign(x0) eta (dense.py:155-159)
-      const double x0 = __ldcg(colj + k);
-      const double beta = x0 >= 0.0 ? -eta : eta;
-      const int len = m - k;
-      double vv = 0.0;
-      for (int i = tid; i < len; i += kT) {
-        double x = __ldcg(colj + k + i);
-        if (i == 0) x -= beta;
-        vsh[i] = x;
-        vv += x * x;
-      }
-      const double tau = 2.0 / block_sum<kT>(vv, sh.red);
-      if (rank == 0 && tid == 0) betas[k] = beta;
-      __syncthreads();
-      if (rank == 0) {
-        for (int i = tid; i < len; i += kT) V[(int64_t)k + i + (int64_t)k * m] = vsh[i];
-        if (tid == 0) taus[k] = tau;
-      }
-      // ---- my columns: apply H_k, row-k entry, norm downdate / refresh.
-      // One warp per column; rows are streamed 8 per lane per round so each
-      // lane keeps 8 independent loads in flight (the pass is bandwidth-bound).
-      for (int c = c0 + warp; c < c1; c += kWarps) {
-        if (c == j) continue;
-        if (done[c]) continue;
-        double* col = W + (int64_t)c * m + k;
-        double d = 0.0;
-        for (int base = 0; base < len; base += 256) {
-          double x[8];
+    for (int c = c0 + warp; c < c1; c += kWarps) {
+      if (c == j || done[c]) continue;
+      const double* col = W + (int64_t)c * m + k;
+      const double wl = lane < jb ? Fb[(int64_t)c * kBB + lane] : 0.0;
+      double d = 0.0, a0k = 0.0;
+      for (int base = 0; base < len; base += 256) {
+        double x[8];
 #pragma unroll
-          for (int u = 0; u < 8; ++u) {
-            const int i = base + lane + 32 * u;
-            x[u] = i < len ? col[i] : 0.0;
-          }
-#pragma unroll
-          for (int u = 0; u < 8; ++u) {
-            const int i = base + lane + 32 * u;
-            if (i < len) d += vsh[i] * x[u];
-          }
+        for (int u = 0; u < 8; ++u) {
+          const int i = base + lane + 32 * u;
+          x[u] = i < len ? col[i] : 0.0;
         }
-        d = warp_sum(d) * tau;
-        double rk = 0.0, tail = 0.0;
-        for (int base = 0; base < len; base += 256) {
-          double x[8];
+        if (base == 0) a0k = x[0];
 #pragma unroll
-          for (int u = 0; u < 8; ++u) {
-            const int i = base + lane + 32 * u;
-            x[u] = i < len ? col[i] : 0.0;
-          }
-#pragma unroll
-          for (int u = 0; u < 8; ++u) {
-            const int i = base + lane + 32 * u;
-            if (i < len) {
-              const double nv = x[u] - d * vsh[i];
-              col[i] = nv;
-              if (i == 0) rk = nv;
-              else tail += nv * nv;
-            }
-          }
+        for (int u = 0; u < 8; ++u) {
+          const int i = base + lane + 32 * u;
+          if (i < len) d += vsh[i] * x[u];
+        }
+      }
+      d = warp_sum(d);
+      const double corr = warp_sum(lane < jb ? sh.g[lane] * wl : 0.0);
+      const double wj = tau * (d - corr);
+      a0k = __shfl_sync(0xffffffffu, a0k, 0);
+      const double rk = a0k - warp_sum(lane < jb ? sh.vk[lane] * wl : 0.0) - sh.vk[jb] * wj;
+      double cn = cur[c] - rk * rk;
+      if (cn < 0.0) cn = 0.0;
+      if (cn < 0.01 * ref[c]) {
+        // exact tail norm of the updated column (dense.py:172-178)
+        if (lane < jb) sh.fw[warp][lane] = wl;
+        __syncwarp();
+        double tail = 0.0;
+        for (int i = 1 + lane; i < len; i += 32) {
+          double x = col[i] - vsh[i] * wj;
+          for (int q = 0; q < jb; ++q)
+            x -= __ldcg(V + (int64_t)(k0 + q) * m + k + i) * sh.fw[warp][q];
+          tail += x * x;
         }
         tail = warp_sum(tail);
-        rk = __shfl_sync(0xffffffffu, rk, 0);
-        if (lane == 0) {
-          double cn = cur[c] - rk * rk;
-          if (cn < 0.0) cn = 0.0;
-          if (cn < 0.01 * ref[c]) {
-            cn = tail;
-            ref[c] = tail;
-          }
-          cur[c] = cn;
-          const int64_t ps = pos[c];
-          if (better(cn, ps, bv, bp)) {
-            bv = cn;
-            bp = ps;
-            bc = c;
-          }
-        }
+        cn = tail;
+        if (lane == 0) ref[c] = tail;
+        __syncwarp();
       }
-    } else {
-      // zero pivot (only when stop_tol * r11 == 0): no reflector
-      if (rank == 0 && tid == 0) {
-        betas[k] = 0.0;
-        taus[k] = 0.0;
-      }
-      for (int c = c0 + warp; c < c1; c += kWarps) {
-        if (lane == 0 && c != j && !done[c]) {
-          const int64_t ps = pos[c];
-          if (better(cur[c], ps, bv, bp)) {
-            bv = cur[c];
-            bp = ps;
-            bc = c;
-          }
+      if (lane == 0) {
+        Fb[(int64_t)c * kBB + jb] = wj;
+        cur[c] = cn;
+        const int64_t ps = pos[c];
+        if (better(cn, ps, bv, bp)) {
+          bv = cn;
+          bp = ps;
+          bc = c;
         }
       }
     }
     __syncthreads();
-    publish(bv, bp, bc, (k + 1) & 1);
+    const int jn = jb + 1;
+    const bool block_end = (jn == kBB) || (k + 1 == kmax);
+    if (block_end) {
+      // A[k0:, c] -= V[k0:, blk] F[c, :]^T for owned, non-pivoted columns
+      // (this step's reflector comes from shared memory: rank 0's global
+      // copy is only guaranteed visible after the group barrier)
+      for (int c = c0 + warp; c < c1; c += kWarps) {
+        if (done[c]) continue;
+        const double wl = lane < jn ? Fb[(int64_t)c * kBB + lane] : 0.0;
+        if (lane < jn) sh.fw[warp][lane] = wl;
+        __syncwarp();
+        double* col = W + (int64_t)c * m;
+        for (int i = k0 + lane; i < m; i += 32) {
+          double x = col[i];
+          // reflector k0+q is zero above row k0+q (never stored there)
+          const int qe = min(jb, i - k0 + 1);
+          for (int q = 0; q < qe; ++q) x -= __ldcg(V + (int64_t)(k0 + q) * m + i) * sh.fw[warp][q];
+          if (i >= k) x -= vsh[i - k] * sh.fw[warp][jb];
+          col[i] = x;
+        }
+        __syncwarp();
+      }
+      k0 = k + 1;
+    }
+    publish(bv, bp, bc, (k + 1) & 1, block_end ? 0 : jn);
     ++k;
-    group_barrier(ctr, G, gen);
+    group_barrier(ctr, G, gen, k, events + 12 * slot + 9);
   }
   const int k_stop = k;
-  // all CTAs are done reading pivot columns: finish the pivoted columns of
-  // R (row t = beta_t, zeros below; dense.py:163-164) and the permutation
-  group_barrier(ctr, G, gen);
+  // every CTA must be done reading this step's pivot column (the loop may
+  // have stopped on it) before owners update or patch their columns
+  group_barrier(ctr, G, gen, 100000 + k, events + 12 * slot + 9);
+  // pending partial block (the loop stopped before its block end)
+  if (k > k0) {
+    const int jn = k - k0;
+    for (int c = c0 + warp; c < c1; c += kWarps) {
+      if (done[c]) continue;
+      const double wl = lane < jn ? Fb[(int64_t)c * kBB + lane] : 0.0;
+      if (lane < jn) sh.fw[warp][lane] = wl;
+      __syncwarp();
+      double* col = W + (int64_t)c * m;
+      for (int i = k0 + lane; i < m; i += 32) {
+        double x = col[i];
+        const int qe = min(jn, i - k0 + 1);
+        for (int q = 0; q < qe; ++q) x -= __ldcg(V + (int64_t)(k0 + q) * m + i) * sh.fw[warp][q];
+        col[i] = x;
+      }
+      __syncwarp();
+    }
+  }
   for (int c = c0 + warp; c < c1; c += kWarps) {
     const int t = pos[c];
     if (done[c]) {
-      const double bt = __ldcg(betas + t);
+      const int tb = t - (t % kBB);
+      const int jq = t - tb;
+      if (lane < jq) sh.fw[warp][lane] = __ldcg(pf + (int64_t)t * kBB + lane);
+      __syncwarp();
       double* col = W + (int64_t)c * m;
-      if (bt != 0.0)
+      for (int i = tb + lane; i < t; i += 32) {
+        double x = col[i];
+        const int qe = min(jq, i - tb + 1);
+        for (int q = 0; q < qe; ++q) x -= __ldcg(V + (int64_t)(tb + q) * m + i) * sh.fw[warp][q];
+        col[i] = x;
+      }
+      const double bt = __ldcg(betas + t);
+      if (__ldcg(taus + t) != 0.0)
         for (int i = t + lane; i < m; i += 32) col[i] = (i == t) ? bt : 0.0;
+      __syncwarp();
     }
     if (lane == 0) perm[t] = c;
   }
@@ -482,7 +570,7 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
     ev[8] = __double_as_longlong(r11);
   }
   // every CTA of the group must finish reading off[p] before it moves
-  group_barrier(ctr, G, gen);
+  group_barrier(ctr, G, gen, -1, events + 12 * slot + 9);
   if (rank == 0 && tid == 0) off[p] = offp + n_fine;
 }
 }  // namespace

@@ -44,6 +44,9 @@ from .schemes import (Elimination, ErrorCorrection, MatView, Orthogonal,
 
 RRQR_ROW = 16
 WAVE_LOG = None      # set to [] to record per-wave CUDA events (profiling)
+import os as _os
+DEBUG_WAVES = bool(_os.environ.get("SPAND_DEBUG_WAVES"))   # test-only cross-check
+DEBUG_RRQR_PAD = bool(_os.environ.get("SPAND_RRQR_DEBUG"))
 EVENT_ROW = 12
 MAX_PANEL_ROWS = 6144
 
@@ -205,6 +208,9 @@ class Engine:
         self.pool_size, self.fac_size = pool.size, fac.size
         self.temp_need = temp_need
         self.cta_cap = max(1, _lib.load().spand_rrqr_cta_count())
+        import os
+        if os.environ.get("SPAND_RRQR_CAP"):
+            self.cta_cap = min(self.cta_cap, int(os.environ["SPAND_RRQR_CAP"]))
 
     # -------------------------------------------------------------- numeric
     def run(self):
@@ -374,8 +380,8 @@ class Engine:
             for (p, nbrs, evs), g in zip(chunk, gs):
                 ncap = int(sum(m0[w] for w in nbrs))
                 mc = int(m0[p])
-                wsz = mc * max(ncap, 1) + mc * mc
-                asz = 2 * ncap + 3 * mc + 4 * g + 4
+                wsz = mc * max(ncap, 1) + mc * mc + 32 * (ncap + mc)
+                asz = 2 * ncap + 3 * mc + 2 * g * 34 + 8
                 isz = (3 * ncap + 1) // 2 + 1
                 lay.append((need, wsz, asz, isz, ncap, mc))
                 need += wsz + asz + isz + 1
@@ -405,6 +411,15 @@ class Engine:
             pd = to_dev_async(np.asarray(prow, dtype=np.int64).reshape(-1, RRQR_ROW))
             nd = to_dev_async(np.asarray(nrow if nrow else [[0, 0, 0, 0]],
                                    dtype=np.int64).reshape(-1, 4))
+            dbg = None
+            if DEBUG_WAVES:
+                dbg = [self._debug_panel(p, nbrs) for p, nbrs, _ in chunk]
+                if _os.environ.get("SPAND_DUMP_WAVES"):
+                    import pickle
+                    self._dump_n = getattr(self, "_dump_n", 0) + 1
+                    with open(f"gpurun_out/wave_{self._dump_n}.pkl", "wb") as fh:
+                        pickle.dump({"panels": dbg, "groups": gs, "eps": self.eps,
+                                     "code": code}, fh)
             if WAVE_LOG is not None:
                 e0 = t.cuda.Event(enable_timing=True)
                 e1 = t.cuda.Event(enable_timing=True)
@@ -412,12 +427,78 @@ class Engine:
             _lib.call("spand_rrqr_wave", len(chunk), gbeg, vmax, ptr(pd), ptr(nd),
                       ptr(self.geo.m0), ptr(self.geo.off), float(self.eps), code,
                       ptr(self.events), stream())
+            if dbg is not None:
+                self._debug_check(chunk, dbg)
             if WAVE_LOG is not None:
                 e1.record()
                 WAVE_LOG.append((lvl, len(chunk), gbeg, vmax,
                                  [(int(m0[p]), int(sum(m0[w] for w in nb)), g)
                                   for (p, nb, _), g in zip(chunk, gs)], e0, e1))
         return temp
+
+    def _debug_panel(self, p, nbrs):
+        """Host copy of interface p's current panel (debug only)."""
+        t = self.t
+        t.cuda.synchronize()
+        m0 = self.sym.m0
+        off = self.geo.off.cpu().numpy()
+        pool = self.pool.cpu().numpy()
+        cols = []
+        for w in nbrs:
+            if w > p:
+                b = int(self.boff[self.sym.bid[(p, w)]])
+                blk = pool[b:b + m0[p] * m0[w]].reshape(m0[w], m0[p]).T
+                cols.append(blk[off[p]:, off[w]:])
+            else:
+                b = int(self.boff[self.sym.bid[(w, p)]])
+                blk = pool[b:b + m0[w] * m0[p]].reshape(m0[p], m0[w]).T
+                cols.append(blk[off[w]:, off[p]:].T)
+        mp = m0[p] - off[p]
+        return np.hstack(cols) if cols else np.zeros((mp, 0))
+
+    def _debug_check(self, chunk, panels):
+        from oracle import spand_oracle as orc
+        self.t.cuda.synchronize()
+        ev = self.events.cpu().numpy().reshape(-1, EVENT_ROW)
+        for (p, nbrs, evs), a in zip(chunk, panels):
+            ref = orc.sparsify_panel(a, self.eps, self.scheme.value)
+            e = ev[evs]
+            if int(e[4]) != ref["rank_c"] or int(e[3]) != ref["k_stop"]:
+                print("DEBUG mismatch p", p, "shape", a.shape, "k_c", int(e[4]), ref["rank_c"],
+                      "k_stop", int(e[3]), ref["k_stop"], flush=True)
+                np.save(f"gpurun_out/bad_panel_{p}.npy", a)
+            # coarse rows written back into the blocks: rows [n_fine, m) of
+            # the panel at the OLD offset
+            m0 = self.sym.m0
+            offn = self.geo.off.cpu().numpy()
+            n_fine = int(e[6])
+            old_off = offn[p] - n_fine
+            pool = self.pool.cpu().numpy()
+            cols = []
+            for w in nbrs:
+                if w > p:
+                    b = int(self.boff[self.sym.bid[(p, w)]])
+                    blk = pool[b:b + m0[p] * m0[w]].reshape(m0[w], m0[p]).T
+                    cols.append(blk[old_off:, offn[w]:])
+                else:
+                    b = int(self.boff[self.sym.bid[(w, p)]])
+                    blk = pool[b:b + m0[w] * m0[p]].reshape(m0[p], m0[w]).T
+                    cols.append(blk[offn[w]:, old_off:].T)
+            got = np.hstack(cols) if cols else np.zeros((m0[p] - old_off, 0))
+            rc = got[n_fine:, :]
+            if rc.shape == ref["r_coarse"].shape and rc.size:
+                err = np.abs(rc - ref["r_coarse"]).max() / max(np.abs(ref["r_coarse"]).max(), 1e-300)
+                if err > 1e-9:
+                    print("DEBUG r_coarse mismatch p", p, "err", err, "shape", rc.shape, flush=True)
+                    np.save(f"gpurun_out/bad_rc_panel_{p}.npy", a)
+                    if not getattr(self, "_dumped", False):
+                        self._dumped = True
+                        print("event", e[:7].tolist(), "ref k_stop", ref["k_stop"], "nbrs", nbrs,
+                              "offs", [int(offn[w]) for w in nbrs], "old_off", old_off)
+                        np.set_printoptions(precision=3, linewidth=200, suppress=True)
+                        print("got rows\n", got[:, :14])
+                        print("ref r_coarse\n", ref["r_coarse"][:, :14])
+                        print("ref e\n", ref["e_tilde"][:, :14])
 
     def _scatter_a(self):
         """Initial blocks from the entries of A (factorize.py:61-96).
@@ -461,6 +542,8 @@ class Engine:
         m0 = sym.m0
         t0 = time.perf_counter()
         ev = self.events.cpu().numpy().reshape(-1, EVENT_ROW)
+        if np.any(ev[:, 9] != 0):
+            raise RuntimeError("RRQR group barrier watchdog fired (kernel bug)")
         # first non-SPD pivot in operator order
         for kind, lvl, ids, info in self.infos:
             iv = info.cpu().numpy()

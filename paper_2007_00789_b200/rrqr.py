@@ -16,18 +16,24 @@ from .kernels import Geometry
 MAX_ROWS = 6144
 
 
-def rrqr_single(a, eps, scheme, group=None):
+def rrqr_single(a, eps, scheme, group=None, pad=0):
+    """``pad`` > 0 stores the panel inside a larger block (live window at an
+    offset, as for an interface sparsified for the second time)."""
     t = require_cuda()
     m, n = a.shape
     if m > MAX_ROWS:
         raise NotImplementedError(f"panel of {m} rows exceeds the kernel limit")
-    geo = Geometry(np.array([m, n], dtype=np.int32))
-    blk = to_dev(np.ascontiguousarray(a.T).ravel() if a.size else np.zeros(1))
+    mp, np_ = m + pad, n + pad
+    geo = Geometry(np.array([mp, np_], dtype=np.int32),
+                   np.array([pad, pad], dtype=np.int32))
+    big = np.zeros((mp, np_))
+    big[pad:, pad:] = a
+    blk = to_dev(np.ascontiguousarray(big.T).ravel() if big.size else np.zeros(1))
     cap = max(1, _lib.load().spand_rrqr_cta_count())
     g = group or max(1, min(cap, n // 64, (m * n) // 65536 + 1))
-    ncap, mcap = max(n, 1), max(m, 1)
-    wsz = mcap * ncap + mcap * mcap
-    asz = 2 * ncap + 3 * mcap + 4 * g + 4
+    ncap, mcap = max(np_, 1), max(mp, 1)
+    wsz = mcap * ncap + mcap * mcap + 32 * (ncap + mcap)
+    asz = 2 * ncap + 3 * mcap + 2 * g * 34 + 8
     isz = (3 * ncap + 1) // 2 + 1
     work = t.zeros(wsz + asz + isz + 1, dtype=t.float64, device=dev())
     q = t.zeros(mcap * mcap, dtype=t.float64, device=dev())
@@ -46,7 +52,8 @@ def rrqr_single(a, eps, scheme, group=None):
     ev = events.cpu().numpy()
     k_stop, k_c, n_fine = int(ev[3]), int(ev[4]), int(ev[6])
     qh = q[:m * m].cpu().numpy().reshape(m, m).T.copy() if m else np.zeros((0, 0))
-    bh = blk[:m * n].cpu().numpy().reshape(n, m).T.copy() if m * n else np.zeros((m, n))
+    bh = (blk[:mp * np_].cpu().numpy().reshape(np_, mp).T[pad:, pad:].copy()
+          if m * n else np.zeros((m, n)))
     iaux = work[wsz + asz:wsz + asz + isz].cpu().numpy().view(np.int32)
     perm = iaux[:n].astype(np.int64)
     r_coarse = np.ascontiguousarray(bh[n_fine:, :]) if k_c else np.zeros((0, n))
