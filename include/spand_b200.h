@@ -147,6 +147,9 @@ int spand_rrqr_wave(int npanel, int grid, int vmax, const int64_t* panels,
                     const int64_t* nbrs, int32_t* m0, int32_t* off, double eps,
                     int scheme, int64_t* events, void* stream);
 int spand_rrqr_cta_count(void);
+/* co-resident CTA capacity of one wave launch whose tallest panel has vmax
+ * live rows (the cooperative grid must not exceed it) */
+int spand_rrqr_capacity(int vmax);
 
 /* Final dense block (factorize.py:198-220): assemble the live parts of the
  * remaining clusters (cl[ncl] cluster ids, ascending) into the virtual

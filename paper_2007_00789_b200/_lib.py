@@ -10,7 +10,7 @@ import os
 from .errors import NativeUnavailable
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libspand_b200.so")
+LIB_PATH = os.environ.get("SPAND_LIB_PATH") or os.path.join(HERE, "libspand_b200.so")
 
 _c_int, _c_dbl, _c_i64 = ctypes.c_int, ctypes.c_double, ctypes.c_int64
 _P = ctypes.c_void_p
@@ -39,6 +39,7 @@ SIGNATURES = {
                            _c_int, _P],
     "spand_rrqr_wave": [_c_int, _c_int, _c_int, _P, _P, _P, _P, _c_dbl, _c_int, _P, _P],
     "spand_rrqr_cta_count": [],
+    "spand_rrqr_capacity": [_c_int],
     "spand_assemble_final": [_c_int, _P, _c_i64, _P, _P, _P, _c_int, _P, _P],
     "spand_count_nonzero": [_c_int, _P, _P, _P],
     "spand_nd_partition": [_c_i64, _P, _P, _c_int, _P, _P, _P, _P],
@@ -74,7 +75,7 @@ _PROFILE = None
 
 # host-only entry points (no kernel launch)
 _HOST_ONLY = {"spand_nd_partition", "spand_version", "spand_device_sm_count",
-              "spand_rrqr_cta_count", "spand_spmv_blocks", "spand_dot_blocks"}
+              "spand_rrqr_cta_count", "spand_rrqr_capacity", "spand_spmv_blocks", "spand_dot_blocks"}
 
 
 def call(name, *args):

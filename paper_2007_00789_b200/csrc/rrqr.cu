@@ -28,6 +28,16 @@
 #include "common.cuh"
 #include "../../include/spand_b200.h"
 
+#ifndef COLLOAD
+#define COLLOAD(p) (*(p))
+#endif
+#ifndef BLKLOAD
+#define BLKLOAD(p) (*(p))
+#endif
+#ifndef BLKSTORE
+#define BLKSTORE(p, v) (*(p) = (v))
+#endif
+
 namespace {
 constexpr int kT = 256;
 constexpr int kWarps = kT / 32;
@@ -55,7 +65,10 @@ struct Sh {
   double red[kWarps];
   double bval[kWarps];
   int64_t bpos[kWarps];
+  int64_t bpc[kWarps];
+  int bq[kWarps];
   int bcol[kWarps];
+  double vt[32][kBB + 1];    // block-update staging: 32 rows x block reflectors
   int nb_start[65];  // column start of each neighbour (first 64)
 };
 
@@ -96,13 +109,14 @@ __device__ __forceinline__ bool better(double va, int64_t pa, double vb, int64_t
   return va > vb || (va == vb && pa < pb);
 }
 
-__global__ void __launch_bounds__(kT)
+__global__ void __launch_bounds__(kT, 4)
 rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* __restrict__ nbrs,
                  int32_t* __restrict__ m0, int32_t* __restrict__ off, double eps, int scheme,
                  int64_t* __restrict__ events) {
   extern __shared__ double vsh[];
   __shared__ Sh sh;
-  __shared__ double tile[kWarps][16][33];
+  // gather / write-back staging aliases the reflector buffer (disjoint phases)
+  double (*tile)[16][33] = reinterpret_cast<double (*)[16][33]>(vsh);
   // ---- locate my panel and rank in its group
   int lo = 0, hi = npanel - 1;
   while (lo < hi) {
@@ -258,6 +272,38 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
     if (tid < jn && cc >= 0) cand[(int64_t)(parity * G + rank) * kCR + 2 + tid] = Fb[(int64_t)cc * kBB + tid];
     __syncthreads();
   };
+  // A[k0:, c] -= V[k0:, k0:k0+jn] F[c, :jn]^T on owned, non-pivoted columns,
+  // 32 rows at a time: the rows' reflector entries are staged in shared
+  // memory once per CTA; lane = row, the F row of a column lives in lane q
+  // and is broadcast with shuffles.  With `last_in_smem` the newest
+  // reflector is taken from vsh (rank 0's global copy is only guaranteed
+  // visible after the next group barrier).
+  int k = 0, k0 = 0;
+  auto block_update = [&](int jn, bool last_in_smem) {
+    const int kk = k0 + jn - 1;   // row offset of vsh when last_in_smem
+    for (int r0 = k0; r0 < m; r0 += 32) {
+      __syncthreads();
+      for (int e = tid; e < 32 * jn; e += kT) {
+        const int r = e % 32, q = e / 32, i = r0 + r;
+        double v = 0.0;
+        if (i < m && i >= k0 + q) {
+          if (last_in_smem && q == jn - 1) v = vsh[i - kk];
+          else v = __ldcg(V + (int64_t)(k0 + q) * m + i);
+        }
+        sh.vt[r][q] = v;
+      }
+      __syncthreads();
+      const int i = r0 + lane;
+      for (int c = c0 + warp; c < c1; c += kWarps) {
+        if (done[c]) continue;
+        const double fq = lane < jn ? Fb[(int64_t)c * kBB + lane] : 0.0;
+        double acc = 0.0;
+        for (int q = 0; q < jn; ++q) acc += sh.vt[lane][q] * __shfl_sync(0xffffffffu, fq, q);
+        if (i < m) BLKSTORE(W + (int64_t)c * m + i, BLKLOAD(W + (int64_t)c * m + i) - acc);
+      }
+    }
+    __syncthreads();
+  };
   publish(bv, bp, bc, 0, 0);
   group_barrier(ctr, G, gen, -1, events + 12 * slot + 9);
 
@@ -267,26 +313,72 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
   // the pivot column is rebuilt from A, V and the winner's F row.
   const double stop_tol = (scheme == 2) ? eps * eps : eps;
   double r11 = 0.0, eta_last = 0.0;
-  int k = 0, k0 = 0;
+#ifdef SPAND_RRQR_PHASES
+  long long ph_t[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  long long ph_last = clock64();
+  int ph_cur = 7;
+#define PH(x) do { long long _n = clock64(); ph_t[ph_cur] += _n - ph_last; ph_last = _n; ph_cur = (x); } while (0)
+#else
+#define PH(x) do {} while (0)
+#endif
   while (k < kmax) {
+    PH(0);
     const int jb = k - k0;  // reflectors of the current block before this step
-    // ---- winning column: max value, smallest current position
+    // ---- winning column: max value, smallest current position (ties in
+    // both: lowest record, as a sequential scan).  Records are scanned in
+    // parallel and reduced over the CTA.
     double wv = -1.0;
     int64_t wp = 0x7fffffffffffLL, wpc = 0;
-    int wq = 0;
+    int wq = 0x7fffffff;
     const int par = k & 1;
-    for (int q = 0; q < G; ++q) {
+    for (int q = tid; q < G; q += kT) {
       const double* rec = cand + (int64_t)(par * G + q) * kCR;
       const double v = __ldcg(rec);
       const int64_t pc = __ldcg(reinterpret_cast<const long long*>(rec) + 1);
       const int64_t ps = pc >> 32;
-      if (better(v, ps, wv, wp)) {
+      if (better(v, ps, wv, wp) || (v == wv && ps == wp && q < wq)) {
         wv = v;
         wp = ps;
         wpc = pc;
         wq = q;
       }
     }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double v2 = __shfl_xor_sync(0xffffffffu, wv, o);
+      const int64_t p2 = __shfl_xor_sync(0xffffffffu, wp, o);
+      const int64_t c2 = __shfl_xor_sync(0xffffffffu, wpc, o);
+      const int q2 = __shfl_xor_sync(0xffffffffu, wq, o);
+      if (better(v2, p2, wv, wp) || (v2 == wv && p2 == wp && q2 < wq)) {
+        wv = v2;
+        wp = p2;
+        wpc = c2;
+        wq = q2;
+      }
+    }
+    if (lane == 0) {
+      sh.bval[warp] = wv;
+      sh.bpos[warp] = wp;
+      sh.bpc[warp] = wpc;
+      sh.bq[warp] = wq;
+    }
+    __syncthreads();
+    wv = sh.bval[0];
+    wp = sh.bpos[0];
+    wpc = sh.bpc[0];
+    wq = sh.bq[0];
+    for (int w2 = 1; w2 < kWarps; ++w2) {
+      const double v2 = sh.bval[w2];
+      const int64_t p2 = sh.bpos[w2];
+      const int q2 = sh.bq[w2];
+      if (better(v2, p2, wv, wp) || (v2 == wv && p2 == wp && q2 < wq)) {
+        wv = v2;
+        wp = p2;
+        wpc = sh.bpc[w2];
+        wq = q2;
+      }
+    }
+    __syncthreads();
     const int jpos = (int)wp;
     const int j = (int)(uint32_t)(wpc & 0xffffffffLL);
     if (tid < jb) sh.wrow[tid] = __ldcg(cand + (int64_t)(par * G + wq) * kCR + 2 + tid);
@@ -297,11 +389,21 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
     double s = 0.0;
     for (int i = tid; i < len; i += kT) {
       double x = __ldcg(colj + i);
-      for (int q = 0; q < jb; ++q) x -= __ldcg(V + (int64_t)(k0 + q) * m + k + i) * sh.wrow[q];
+      // 8 independent reflector loads in flight per row
+      for (int q0 = 0; q0 < jb; q0 += 8) {
+        double vv[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          vv[u] = (q0 + u < jb) ? __ldcg(V + (int64_t)(k0 + q0 + u) * m + k + i) : 0.0;
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (q0 + u < jb) x -= vv[u] * sh.wrow[q0 + u];
+      }
       vsh[i] = x;
       s += x * x;
     }
     const double eta = sqrt(block_sum<kT>(s, sh.red));
+    PH(1);
     eta_last = eta;
     if (k == 0) {
       r11 = eta;
@@ -346,19 +448,40 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
         betas[k] = beta;
       }
     }
+    PH(2);
     // g[q] = v^T v_q (rows k..), V row k of the block (and v[0] itself)
-    for (int q = warp; q < jb; q += kWarps) {
-      const double* vq = V + (int64_t)(k0 + q) * m + k;
-      double d = 0.0;
-      for (int i = lane; i < len; i += 32) d += vsh[i] * __ldcg(vq + i);
-      d = warp_sum(d);
-      if (lane == 0) {
-        sh.g[q] = d;
-        sh.vk[q] = __ldcg(vq);
+    // (row-parallel: each thread streams its rows of 8 reflectors at once,
+    // partial sums reduced across the CTA; V is read once per CTA)
+    for (int q0 = 0; q0 < jb; q0 += 8) {
+      double acc[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) acc[u] = 0.0;
+      for (int i = tid; i < len; i += kT) {
+        const double vi = vsh[i];
+        double vv[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          vv[u] = (q0 + u < jb) ? __ldcg(V + (int64_t)(k0 + q0 + u) * m + k + i) : 0.0;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) acc[u] += vi * vv[u];
       }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const double w = warp_sum(acc[u]);
+        if (lane == 0) sh.fw[warp][u] = w;
+      }
+      __syncthreads();
+      if (tid < 8 && q0 + tid < jb) {
+        double t = 0.0;
+        for (int q = 0; q < kWarps; ++q) t += sh.fw[q][tid];
+        sh.g[q0 + tid] = t;
+        sh.vk[q0 + tid] = __ldcg(V + (int64_t)(k0 + q0 + tid) * m + k);
+      }
+      __syncthreads();
     }
     if (tid == 0) sh.vk[jb] = vsh[0];
     __syncthreads();
+    PH(3);
     // ---- owned columns: F column, row-k entry, norm downdate / refresh
     bv = -1.0;
     bp = 0x7fffffffffffLL;
@@ -373,7 +496,7 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
           const int i = base + lane + 32 * u;
-          x[u] = i < len ? col[i] : 0.0;
+          x[u] = i < len ? COLLOAD(col + i) : 0.0;
         }
         if (base == 0) a0k = x[0];
 #pragma unroll
@@ -402,7 +525,10 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
         }
         tail = warp_sum(tail);
         cn = tail;
-        if (lane == 0) ref[c] = tail;
+        if (lane == 0) {
+          ref[c] = tail;
+          atomicAdd(reinterpret_cast<unsigned long long*>(events + 12 * slot + 10), 1ull);
+        }
         __syncwarp();
       }
       if (lane == 0) {
@@ -417,56 +543,32 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
       }
     }
     __syncthreads();
+    PH(4);
     const int jn = jb + 1;
     const bool block_end = (jn == kBB) || (k + 1 == kmax);
     if (block_end) {
-      // A[k0:, c] -= V[k0:, blk] F[c, :]^T for owned, non-pivoted columns
-      // (this step's reflector comes from shared memory: rank 0's global
-      // copy is only guaranteed visible after the group barrier)
-      for (int c = c0 + warp; c < c1; c += kWarps) {
-        if (done[c]) continue;
-        const double wl = lane < jn ? Fb[(int64_t)c * kBB + lane] : 0.0;
-        if (lane < jn) sh.fw[warp][lane] = wl;
-        __syncwarp();
-        double* col = W + (int64_t)c * m;
-        for (int i = k0 + lane; i < m; i += 32) {
-          double x = col[i];
-          // reflector k0+q is zero above row k0+q (never stored there)
-          const int qe = min(jb, i - k0 + 1);
-          for (int q = 0; q < qe; ++q) x -= __ldcg(V + (int64_t)(k0 + q) * m + i) * sh.fw[warp][q];
-          if (i >= k) x -= vsh[i - k] * sh.fw[warp][jb];
-          col[i] = x;
-        }
-        __syncwarp();
-      }
+      block_update(jn, true);
       k0 = k + 1;
     }
+    PH(5);
     publish(bv, bp, bc, (k + 1) & 1, block_end ? 0 : jn);
     ++k;
+    PH(6);
     group_barrier(ctr, G, gen, k, events + 12 * slot + 9);
   }
   const int k_stop = k;
+#ifdef SPAND_RRQR_PHASES
+  PH(7);
+  if (tid == 0 && (rank == 0 || rank == G / 2))
+    printf("[rrqr phases] p %d rank %d k %d kcycles: cand+pivcol %lld refl %lld g %lld colpass %lld blockend %lld publish %lld barrier %lld\n",
+           p, rank, k, ph_t[0] / 1000, ph_t[1] / 1000, ph_t[2] / 1000, ph_t[3] / 1000, ph_t[4] / 1000,
+           ph_t[5] / 1000, ph_t[6] / 1000);
+#endif
   // every CTA must be done reading this step's pivot column (the loop may
   // have stopped on it) before owners update or patch their columns
   group_barrier(ctr, G, gen, 100000 + k, events + 12 * slot + 9);
   // pending partial block (the loop stopped before its block end)
-  if (k > k0) {
-    const int jn = k - k0;
-    for (int c = c0 + warp; c < c1; c += kWarps) {
-      if (done[c]) continue;
-      const double wl = lane < jn ? Fb[(int64_t)c * kBB + lane] : 0.0;
-      if (lane < jn) sh.fw[warp][lane] = wl;
-      __syncwarp();
-      double* col = W + (int64_t)c * m;
-      for (int i = k0 + lane; i < m; i += 32) {
-        double x = col[i];
-        const int qe = min(jn, i - k0 + 1);
-        for (int q = 0; q < qe; ++q) x -= __ldcg(V + (int64_t)(k0 + q) * m + i) * sh.fw[warp][q];
-        col[i] = x;
-      }
-      __syncwarp();
-    }
-  }
+  if (k > k0) block_update(k - k0, false);
   for (int c = c0 + warp; c < c1; c += kWarps) {
     const int t = pos[c];
     if (done[c]) {
@@ -581,8 +683,24 @@ int spand_rrqr_cta_count(void) {
   int dev = 0, sms = 0, per = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return -1;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const size_t smem = kMaxM * sizeof(double);
-  cudaFuncSetAttribute(rrqr_wave_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  // capacity for panels up to 4224 rows (the tile staging size); taller
+  // panels need more shared memory and are launched with smaller groups
+  const size_t smem = (size_t)kWarps * 16 * 33 * sizeof(double);
+  cudaFuncSetAttribute(rrqr_wave_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)(kMaxM * sizeof(double)));
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, rrqr_wave_kernel, kT, smem) != cudaSuccess)
+    return -1;
+  return per * sms;
+}
+
+int spand_rrqr_capacity(int vmax) {
+  int dev = 0, sms = 0, per = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return -1;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  size_t smem = (size_t)kWarps * 16 * 33 * sizeof(double);
+  if ((size_t)vmax * sizeof(double) > smem) smem = (size_t)vmax * sizeof(double);
+  cudaFuncSetAttribute(rrqr_wave_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)(kMaxM * sizeof(double)));
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, rrqr_wave_kernel, kT, smem) != cudaSuccess)
     return -1;
   return per * sms;
@@ -593,7 +711,9 @@ int spand_rrqr_wave(int npanel, int grid, int vmax, const int64_t* panels, const
                     void* stream) {
   if (npanel < 0 || grid < 0 || vmax < 0 || vmax > kMaxM) return -1;
   if (npanel == 0 || grid == 0) return 0;
-  const size_t smem = (size_t)(vmax > 0 ? vmax : 1) * sizeof(double);
+  const size_t tile_bytes = (size_t)kWarps * 16 * 33 * sizeof(double);
+  size_t smem = (size_t)(vmax > 0 ? vmax : 1) * sizeof(double);
+  if (smem < tile_bytes) smem = tile_bytes;
   cudaError_t e = cudaFuncSetAttribute(rrqr_wave_kernel,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)(kMaxM * sizeof(double)));

@@ -207,10 +207,7 @@ class Engine:
         self.flinv_off = fac.take(self.fcap ** 2)
         self.pool_size, self.fac_size = pool.size, fac.size
         self.temp_need = temp_need
-        self.cta_cap = max(1, _lib.load().spand_rrqr_cta_count())
-        import os
-        if os.environ.get("SPAND_RRQR_CAP"):
-            self.cta_cap = min(self.cta_cap, int(os.environ["SPAND_RRQR_CAP"]))
+        self.cta_cap_override = int(_os.environ.get("SPAND_RRQR_CAP", "0"))
 
     # -------------------------------------------------------------- numeric
     def run(self):
@@ -364,8 +361,11 @@ class Engine:
         t = self.t
         sym = self.sym
         m0 = sym.m0
-        cap = self.cta_cap
         code = SCHEME_CODE[self.scheme]
+        vm = int(max(m0[p] for p, _, _ in panels)) if panels else 1
+        cap = max(1, _lib.load().spand_rrqr_capacity(vm))
+        if self.cta_cap_override:
+            cap = min(cap, self.cta_cap_override)
         # split a wave into launches of at most `cap` panels
         for c0 in range(0, len(panels), cap):
             chunk = panels[c0:c0 + cap]

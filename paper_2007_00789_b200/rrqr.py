@@ -29,7 +29,7 @@ def rrqr_single(a, eps, scheme, group=None, pad=0):
     big = np.zeros((mp, np_))
     big[pad:, pad:] = a
     blk = to_dev(np.ascontiguousarray(big.T).ravel() if big.size else np.zeros(1))
-    cap = max(1, _lib.load().spand_rrqr_cta_count())
+    cap = max(1, _lib.load().spand_rrqr_capacity(max(m, 1)))
     g = group or max(1, min(cap, n // 64, (m * n) // 65536 + 1))
     ncap, mcap = max(np_, 1), max(mp, 1)
     wsz = mcap * ncap + mcap * mcap + 32 * (ncap + mcap)
