@@ -43,6 +43,10 @@ SIGNATURES = {
     "spand_assemble_final": [_c_int, _P, _c_i64, _P, _P, _P, _c_int, _P, _P],
     "spand_count_nonzero": [_c_int, _P, _P, _P],
     "spand_nd_partition": [_c_i64, _P, _P, _c_int, _P, _P, _P, _P],
+    "spand_plan_sizes": [_P, _P],
+    "spand_plan_emit": [_P, _c_i64, _c_i64, _c_i64, _c_i64],
+    "spand_plan_program": [_P, _P, _P],
+    "spand_plan_meta": [_P, _P],
 }
 
 _lib = None
@@ -74,7 +78,8 @@ COUNTS = {}
 _PROFILE = None
 
 # host-only entry points (no kernel launch)
-_HOST_ONLY = {"spand_nd_partition", "spand_version", "spand_device_sm_count",
+_HOST_ONLY = {"spand_plan_sizes", "spand_plan_emit", "spand_plan_program",
+              "spand_plan_meta", "spand_nd_partition", "spand_version", "spand_device_sm_count",
               "spand_rrqr_cta_count", "spand_rrqr_capacity", "spand_spmv_blocks", "spand_dot_blocks"}
 
 

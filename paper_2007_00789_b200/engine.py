@@ -42,131 +42,103 @@ from .kernels import Geometry, TILE, opnd
 from .schemes import (Elimination, ErrorCorrection, MatView, Orthogonal,
                       Scaling)
 
-RRQR_ROW = 16
-WAVE_LOG = None      # set to [] to record per-wave CUDA events (profiling)
 import os as _os
-DEBUG_WAVES = bool(_os.environ.get("SPAND_DEBUG_WAVES"))   # test-only cross-check
-DEBUG_RRQR_PAD = bool(_os.environ.get("SPAND_RRQR_DEBUG"))
+
+WAVE_LOG = None      # set to [] to record per-wave CUDA events (profiling)
 EVENT_ROW = 12
 MAX_PANEL_ROWS = 6144
 
 
-class Symbolic:
-    """Rank-independent schedule of the factorization (host)."""
+class NativePlan:
+    """Handle on the C++ level scheduler (csrc/planner.cpp).
 
-    def __init__(self, a, h, skip_levels):
+    ``meta`` decodes the scheduler's structure export into per-level
+    records used by ``collect`` (operator assembly on the host)."""
+
+    def __init__(self, a, h, skip_levels, cap_override=0):
+        import ctypes
         t0 = time.perf_counter()
-        self.levels = h.levels
+        lib = _lib.load()
         self.ncl = ncl = len(h.clusters)
         self.m0 = np.array([c.dofs.size for c in h.clusters], dtype=np.int64)
-        self.depth = np.array([c.depth for c in h.clusters], dtype=np.int64)
+        self.depth = np.array([c.depth for c in h.clusters], dtype=np.int32)
         self.dofs = [np.asarray(c.dofs, dtype=np.int64) for c in h.clusters]
         self.cluster_of = h.cluster_of
-        n = a.n
-        rows = np.repeat(np.arange(n, dtype=np.int64), np.diff(a.row_ptr))
+        self.levels = h.levels
+        rows = np.repeat(np.arange(a.n, dtype=np.int64), np.diff(a.row_ptr))
         ci, cj = h.cluster_of[rows], h.cluster_of[a.col_idx]
         up = ci <= cj
-        keys = np.unique(ci[up] * ncl + cj[up])
-        self.bkeys = []
-        self.bid = {}
-        adj = [set() for _ in range(ncl)]
-        cblocks = [set() for _ in range(ncl)]
-        for key in keys.tolist():
-            i, j = divmod(key, ncl)
-            self._new_block(i, j, cblocks)
-            if i != j:
-                adj[i].add(j)
-                adj[j].add(i)
-        for c in range(ncl):                 # every cluster owns a diagonal block
-            if (c, c) not in self.bid:
-                self._new_block(c, c, cblocks)
-        alive = set(range(ncl))
-        self.level_recs = []
-        L = h.levels
-        for level in range(L, 0, -1):
-            interiors = sorted(c for c in alive if self.depth[c] == level)
-            elim = []
-            schur = {}
-            for s in interiors:
-                nbrs = sorted(adj[s])
-                elim.append((s, tuple(nbrs)))
-                for ii, wa in enumerate(nbrs):
-                    for wb in nbrs[ii:]:
-                        key = (wa, wb)
-                        if key not in self.bid:
-                            self._new_block(wa, wb, cblocks)
-                            if wa != wb:
-                                adj[wa].add(wb)
-                                adj[wb].add(wa)
-                        schur.setdefault(key, []).append(s)
-                for w in nbrs:
-                    adj[w].discard(s)
-                for key in cblocks[s]:
-                    other = key[0] if key[1] == s else key[1]
-                    if other != s:
-                        cblocks[other].discard(key)
-                cblocks[s] = set()
-                adj[s] = set()
-                alive.discard(s)
-            skipped = (L - level) < skip_levels
-            rec = {"level": level, "elim": elim, "schur": schur,
-                   "skipped": skipped}
-            if not skipped:
-                active = sorted(alive)
-                rec["active"] = active
-                rec["rescale_blocks"] = sorted(
-                    {key for c in active for key in cblocks[c] if key[0] != key[1]})
-                wave = {}
-                spars = []
-                for p in active:
-                    nb = sorted(adj[p])
-                    wv = 0
-                    for q in nb:
-                        if q < p:
-                            wv = max(wv, wave[q] + 1)
-                    wave[p] = wv
-                    spars.append((p, tuple(nb), wv))
-                rec["spars"] = spars
-                rec["nwaves"] = (max(wave.values()) + 1) if wave else 0
-            self.level_recs.append(rec)
-        self.final = sorted(alive)
-        self.final_blocks = sorted({key for c in self.final for key in cblocks[c]})
+        keys = np.ascontiguousarray(np.unique(ci[up] * ncl + cj[up]), dtype=np.int64)
+        vp = lambda x: x.ctypes.data_as(ctypes.c_void_p)  # noqa: E731
+        lib.spand_plan_create.restype = ctypes.c_void_p
+        lib.spand_plan_create.argtypes = [ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p,
+                                          ctypes.c_int, ctypes.c_int, ctypes.c_int64,
+                                          ctypes.c_void_p, ctypes.c_int]
+        lib.spand_plan_destroy.argtypes = [ctypes.c_void_p]
+        for nm, n in (("spand_plan_sizes", 2), ("spand_plan_program", 3),
+                      ("spand_plan_meta", 2)):
+            getattr(lib, nm).argtypes = [ctypes.c_void_p] * n
+        lib.spand_plan_emit.argtypes = [ctypes.c_void_p] + [ctypes.c_int64] * 4
+        self.h = ctypes.c_void_p(lib.spand_plan_create(
+            ncl, vp(self.m0), vp(self.depth), int(h.levels), int(skip_levels),
+            keys.size, vp(keys), int(cap_override)))
+        self._lib = lib
+        self._vp = vp
+        self.sizes()
+        self._decode_meta()
         self.seconds = time.perf_counter() - t0
 
-    def _new_block(self, i, j, cblocks):
-        b = len(self.bkeys)
-        self.bkeys.append((i, j))
-        self.bid[(i, j)] = b
-        cblocks[i].add((i, j))
-        cblocks[j].add((i, j))
-        return b
+    def __del__(self):
+        try:
+            self._lib.spand_plan_destroy(self.h)
+        except Exception:
+            pass
 
+    def sizes(self):
+        out = np.zeros(16, dtype=np.int64)
+        self._lib.spand_plan_sizes(self.h, self._vp(out))
+        (self.pool_size, self.fac_size, self.temp_size, self.n_events, self.n_info,
+         self.n_ctr, self.nblocks, self.nlevels, self.fcap, self.f_off,
+         self.flinv_off, self.nfinal, self.prog_len, self.n_launch,
+         self.meta_len, _) = [int(x) for x in out]
 
-class _Alloc:
-    """Bump allocator of fp64 element offsets within one device pool."""
+    def emit(self, pool_base, fac_base, temp_base, ctr_base):
+        self._lib.spand_plan_emit(self.h, pool_base, fac_base, temp_base, ctr_base)
+        self.sizes()
 
-    def __init__(self):
-        self.size = 0
+    def program(self):
+        prog = np.zeros(max(self.prog_len, 1), dtype=np.int64)
+        lau = np.zeros(max(self.n_launch, 1) * 16, dtype=np.int64)
+        self._lib.spand_plan_program(self.h, self._vp(prog), self._vp(lau))
+        return prog, lau.reshape(-1, 16)[:self.n_launch]
 
-    def take(self, count):
-        at = self.size
-        self.size += int(count)
-        return at
-
-
-def _groups(works, capacity):
-    """CTA group sizes proportional to work, at least 1, sum <= capacity."""
-    total = float(sum(works))
-    sizes = []
-    for w in works:
-        g = int(capacity * w / total) if total > 0 else 1
-        sizes.append(max(1, g))
-    while sum(sizes) > capacity:
-        k = int(np.argmax(sizes))
-        if sizes[k] == 1:
-            break
-        sizes[k] -= 1
-    return sizes
+    def _decode_meta(self):
+        meta = np.zeros(max(self.meta_len, 1), dtype=np.int64)
+        self._lib.spand_plan_meta(self.h, self._vp(meta))
+        ncl, nb, nlev, nfin, nfinb = (int(x) for x in meta[:5])
+        i = 9
+        self.bi = meta[i:i + nb]; i += nb
+        self.bj = meta[i:i + nb]; i += nb
+        self.boff = meta[i:i + nb]; i += nb
+        self.elim_linv = meta[i:i + ncl]; i += ncl
+        self.bid = {(int(x), int(y)): k for k, (x, y) in enumerate(zip(self.bi, self.bj))}
+        m = meta.tolist()
+        recs = []
+        for _ in range(nlev):
+            level, skipped, nint, nact, nwaves = m[i:i + 5]; i += 5
+            elim = []
+            for _ in range(nint):
+                s, nn = m[i], m[i + 1]; i += 2
+                elim.append((s, tuple(m[i:i + nn]))); i += nn
+            act = []
+            for _ in range(nact):
+                p, wv, lo, li, qo, sl, nn = m[i:i + 7]; i += 7
+                act.append((p, wv, lo, li, qo, sl, tuple(m[i:i + nn]))); i += nn
+            recs.append({"level": level, "skipped": bool(skipped), "elim": elim,
+                         "active": act, "nwaves": nwaves})
+        self.level_recs = recs
+        self.final = m[i:i + nfin]; i += nfin
+        self.final_blocks = m[i:i + nfinb]
 
 
 class Engine:
@@ -174,331 +146,75 @@ class Engine:
         self.t = require_cuda()
         self.a, self.h = a, h
         self.eps, self.scheme, self.skip = eps, scheme, skip_levels
-        self.sym = Symbolic(a, h, skip_levels)
+        self.sym = NativePlan(a, h, skip_levels,
+                              int(_os.environ.get("SPAND_RRQR_CAP", "0")))
         self.timings = {"symbolic_s": self.sym.seconds}
-
-    # ------------------------------------------------------------------ plan
-    def plan(self):
-        sym = self.sym
-        m0 = sym.m0
-        ncl = sym.ncl
-        pool = _Alloc()
-        self.boff = np.array([pool.take(m0[i] * m0[j]) for i, j in sym.bkeys],
-                             dtype=np.int64)
-        fac = _Alloc()
-        self.linv_off = {}           # eliminated s -> Linv offset
-        self.resc_off = {}           # (level, p) -> (L offset, Linv offset)
-        self.q_off = {}              # (level, p) -> Q offset
-        temp_need = 0
-        for rec in sym.level_recs:
-            for s, nbrs in rec["elim"]:
-                self.linv_off[s] = fac.take(m0[s] * m0[s])
-            trsm = sum(m0[w] * m0[s] for s, nbrs in rec["elim"] for w in nbrs)
-            temp_need = max(temp_need, trsm)
-            if not rec["skipped"]:
-                for p in rec["active"]:
-                    self.resc_off[(rec["level"], p)] = (fac.take(m0[p] ** 2),
-                                                        fac.take(m0[p] ** 2))
-                    self.q_off[(rec["level"], p)] = fac.take(m0[p] ** 2)
-                resc = sum(m0[i] * m0[j] for i, j in rec["rescale_blocks"])
-                temp_need = max(temp_need, resc)
-        self.fcap = int(sum(m0[c] for c in sym.final))
-        self.f_off = fac.take(self.fcap ** 2)
-        self.flinv_off = fac.take(self.fcap ** 2)
-        self.pool_size, self.fac_size = pool.size, fac.size
-        self.temp_need = temp_need
-        self.cta_cap_override = int(_os.environ.get("SPAND_RRQR_CAP", "0"))
 
     # -------------------------------------------------------------- numeric
     def run(self):
+        """Allocate, emit the native program, upload it once, launch it."""
         t = self.t
         sym = self.sym
         m0 = sym.m0
         ncl = sym.ncl
         tstart = time.perf_counter()
-        self.plan()
-        self.timings["plan_s"] = time.perf_counter() - tstart
-        # geometry: clusters + final block (virtual cluster F = ncl)
         self.F = ncl
-        geo_m0 = np.concatenate([m0, [self.fcap]]).astype(np.int32)
-        self.geo = geo = Geometry(geo_m0)
+        self.fcap = sym.fcap
+        self.geo = geo = Geometry(np.concatenate([m0, [sym.fcap]]).astype(np.int32))
         d = dev()
-        self.pool = pool = t.zeros(max(self.pool_size, 1), dtype=t.float64, device=d)
-        self.facbuf = fac = t.zeros(max(self.fac_size, 1), dtype=t.float64, device=d)
+        self.pool = pool = t.zeros(max(sym.pool_size, 1), dtype=t.float64, device=d)
+        self.facbuf = fac = t.zeros(max(sym.fac_size, 1), dtype=t.float64, device=d)
+        self.boff = sym.boff
         self._scatter_a()
+        self.events = t.zeros(max(sym.n_events, 1) * EVENT_ROW, dtype=t.int64, device=d)
+        self.info = t.zeros(max(sym.n_info, 1), dtype=t.int32, device=d)
+        ctr = t.zeros(max(sym.n_ctr, 1), dtype=t.int32, device=d)
         pb, fb = pool.data_ptr(), fac.data_ptr()
-        self.pb, self.fb = pb, fb
-
-        def blk(i, j):
-            return pb + 8 * int(self.boff[sym.bid[(i, j)]])
-
-        self.blk = blk
-        infos = []          # (kind, key, device int32 tensor)
-        rrqr_waves = []
-        n_events = sum(len(r.get("spars", [])) for r in sym.level_recs)
-        self.events = t.zeros(max(n_events, 1) * EVENT_ROW, dtype=t.int64, device=d)
-        self.event_slot = {}
-        temp = None
-        ev = 0
-        for rec in sym.level_recs:
-            lvl = rec["level"]
-            elim = rec["elim"]
-            # ---------------- interior eliminations
-            if elim:
-                info = t.zeros(len(elim), dtype=t.int32, device=d)
-                from .kernels import potrf_batched, trtri_batched, gemm_grouped, copy_batched
-                potrf_batched(geo, [opnd(blk(s, s), s, s) for s, _ in elim], info)
-                infos.append(("G", lvl, [s for s, _ in elim], info))
-                trtri_batched(geo, [(opnd(blk(s, s), s, s),
-                                     opnd(fb + 8 * self.linv_off[s], s, s))
-                                    for s, _ in elim])
-                pairs = [(s, w) for s, nbrs in elim for w in nbrs]
-                if pairs:
-                    need = sum(m0[w] * m0[s] for s, w in pairs)
-                    temp = self._temp(temp, need)
-                    tb = temp.data_ptr()
-                    toff, acc = {}, 0
-                    for s, w in pairs:
-                        toff[(s, w)] = acc
-                        acc += m0[w] * m0[s]
-                    targets = [(opnd(tb + 8 * toff[(s, w)], w, s),
-                                [(opnd(blk(w, s), w, s),
-                                  opnd(fb + 8 * self.linv_off[s], s, s))],
-                                (m0[w], m0[s])) for s, w in pairs]
-                    gemm_grouped(geo, targets, 1.0, 0.0, bT=1)
-                    copy_batched(geo, [(opnd(tb + 8 * toff[(s, w)], w, s),
-                                        opnd(blk(w, s), w, s), 0) for s, w in pairs])
-                # grouped Schur / fill update
-                targets = []
-                for (wa, wb), slist in rec["schur"].items():
-                    segs = [(opnd(blk(wa, s), wa, s), opnd(blk(wb, s), wb, s))
-                            for s in slist]
-                    targets.append((opnd(blk(wa, wb), wa, wb), segs,
-                                    (m0[wa], m0[wb])))
-                self._schur(targets)
-            if rec["skipped"]:
-                continue
-            from .kernels import potrf_batched, trtri_batched, gemm_grouped, copy_batched
-            active = rec["active"]
-            # ---------------- rescale every active interface
-            lo = {p: self.resc_off[(lvl, p)] for p in active}
-            copy_batched(geo, [(opnd(blk(p, p), p, p), opnd(fb + 8 * lo[p][0], p, p), 1)
-                               for p in active])
-            info = t.zeros(len(active), dtype=t.int32, device=d)
-            potrf_batched(geo, [opnd(fb + 8 * lo[p][0], p, p) for p in active], info)
-            infos.append(("D", lvl, list(active), info))
-            trtri_batched(geo, [(opnd(fb + 8 * lo[p][0], p, p),
-                                 opnd(fb + 8 * lo[p][1], p, p)) for p in active])
-            copy_batched(geo, [(opnd(blk(p, p), p, p), opnd(blk(p, p), p, p), 2)
-                               for p in active])
-            rb = rec["rescale_blocks"]
-            if rb:
-                need = sum(m0[i] * m0[j] for i, j in rb)
-                temp = self._temp(temp, need)
-                tb = temp.data_ptr()
-                toff, acc = {}, 0
-                for i, j in rb:
-                    toff[(i, j)] = acc
-                    acc += m0[i] * m0[j]
-                # T = Z_i^-1 B  (NN), then B = T Z_j^-T (NT)
-                gemm_grouped(geo, [(opnd(tb + 8 * toff[(i, j)], i, j),
-                                    [(opnd(fb + 8 * lo[i][1], i, i), opnd(blk(i, j), i, j))],
-                                    (m0[i], m0[j])) for i, j in rb], 1.0, 0.0, bT=0)
-                gemm_grouped(geo, [(opnd(blk(i, j), i, j),
-                                    [(opnd(tb + 8 * toff[(i, j)], i, j),
-                                      opnd(fb + 8 * lo[j][1], j, j))],
-                                    (m0[i], m0[j])) for i, j in rb], 1.0, 0.0, bT=1)
-            # ---------------- sparsify, wave by wave
-            by_wave = [[] for _ in range(rec["nwaves"])]
-            for p, nbrs, wv in rec["spars"]:
-                self.event_slot[(lvl, p)] = ev
-                by_wave[wv].append((p, nbrs, ev))
-                ev += 1
-            for panels in by_wave:
-                temp = self._rrqr_wave(panels, lvl, temp)
-        # ---------------- final dense block
-        from .kernels import potrf_batched, trtri_batched
-        F = self.F
-        fin = sym.final
-        if fin:
-            index = {c: k for k, c in enumerate(fin)}
-            cl = to_dev_async(np.asarray(fin, dtype=np.int64))
-            rows = [[index[i], index[j], blk(i, j), 0] for i, j in sym.final_blocks]
-            brows = to_dev_async(np.asarray(rows, dtype=np.int64).reshape(-1, 4))
-            _lib.call("spand_assemble_final", len(fin), ptr(cl), len(rows),
-                      ptr(brows), ptr(geo.m0), ptr(geo.off), F,
-                      ctypes_ptr(fb + 8 * self.f_off), stream())
-            info = t.zeros(1, dtype=t.int32, device=d)
-            potrf_batched(geo, [opnd(fb + 8 * self.f_off, F, F)], info)
-            infos.append(("F", 0, [F], info))
-            trtri_batched(geo, [(opnd(fb + 8 * self.f_off, F, F),
-                                 opnd(fb + 8 * self.flinv_off, F, F))])
-        self.infos = infos
-        self._temp_keep = temp
+        sym.emit(pb, fb, 0, ctr.data_ptr())          # sizing pass (temp size)
+        temp = t.empty(max(sym.temp_size, 1), dtype=t.float64, device=d)
+        sym.emit(pb, fb, temp.data_ptr(), ctr.data_ptr())
+        prog, launches = sym.program()
+        self.timings["plan_s"] = time.perf_counter() - tstart
+        progd = to_dev_async(prog)
+        base = progd.data_ptr()
+        st = stream()
+        gm0, goff = ptr(geo.m0), ptr(geo.off)
+        ib, evb = self.info.data_ptr(), self.events.data_ptr()
+        import ctypes
+        P = lambda off: ctypes.c_void_p(base + 8 * int(off))  # noqa: E731
+        for rec in launches:
+            typ, cnt, ao, bo, co, x0, x1, x2 = (int(v) for v in rec[:8])
+            if typ == 1:
+                _lib.call("spand_potrf_batched", cnt, P(ao), gm0, goff,
+                          ctypes.c_void_p(ib + 4 * x0), st)
+            elif typ == 2:
+                _lib.call("spand_trtri_tiles", cnt, P(ao), gm0, goff, st)
+            elif typ == 3:
+                alpha = float(np.int64(rec[8]).view(np.float64))
+                beta = float(np.int64(rec[9]).view(np.float64))
+                _lib.call("spand_gemm_grouped", cnt, P(ao), P(bo), P(co), gm0, goff,
+                          alpha, beta, x0, x1, st)
+            elif typ == 4:
+                _lib.call("spand_copy_batched", cnt, P(ao), gm0, goff, st)
+            elif typ == 5:
+                if WAVE_LOG is not None:
+                    e0 = t.cuda.Event(enable_timing=True)
+                    e1 = t.cuda.Event(enable_timing=True)
+                    e0.record()
+                _lib.call("spand_rrqr_wave", cnt, x0, x1, P(ao), P(bo), gm0, goff,
+                          float(self.eps), SCHEME_CODE[self.scheme],
+                          ctypes.c_void_p(evb), st)
+                if WAVE_LOG is not None:
+                    e1.record()
+                    WAVE_LOG.append((cnt, x0, x1, e0, e1))
+            elif typ == 6:
+                _lib.call("spand_assemble_final", cnt, P(ao), x0, P(bo), gm0, goff,
+                          x1, ctypes.c_void_p(fb + 8 * x2), st)
+            else:
+                raise RuntimeError(f"unknown launch type {typ}")
+        self._keep_run = (temp, ctr, progd)
         t.cuda.synchronize()
         self.timings["device_s"] = time.perf_counter() - tstart
-
-    def _temp(self, temp, need):
-        t = self.t
-        need = max(int(need), 1)
-        if temp is None or temp.numel() < need:
-            temp = t.empty(need, dtype=t.float64, device=dev())
-        return temp
-
-    def _schur(self, targets):
-        from .kernels import gemm_grouped
-        if not targets:
-            return
-        # diagonal targets: lower tiles only (potrf reads the lower triangle)
-        diag = [tg for tg in targets if tg[0][1] == tg[0][2]]
-        off = [tg for tg in targets if tg[0][1] != tg[0][2]]
-        if off:
-            gemm_grouped(self.geo, off, -1.0, 1.0, bT=1)
-        if diag:
-            gemm_grouped(self.geo, diag, -1.0, 1.0, bT=1, lower_only=True)
-
-    def _rrqr_wave(self, panels, lvl, temp):
-        t = self.t
-        sym = self.sym
-        m0 = sym.m0
-        code = SCHEME_CODE[self.scheme]
-        vm = int(max(m0[p] for p, _, _ in panels)) if panels else 1
-        cap = max(1, _lib.load().spand_rrqr_capacity(vm))
-        if self.cta_cap_override:
-            cap = min(cap, self.cta_cap_override)
-        # split a wave into launches of at most `cap` panels
-        for c0 in range(0, len(panels), cap):
-            chunk = panels[c0:c0 + cap]
-            works = []
-            for p, nbrs, _ in chunk:
-                ncap = int(sum(m0[w] for w in nbrs))
-                works.append(max(1, int(m0[p]) * max(ncap, 1)))
-            gs = _groups(works, cap)
-            # workspace layout per panel (doubles)
-            need = 0
-            lay = []
-            for (p, nbrs, evs), g in zip(chunk, gs):
-                ncap = int(sum(m0[w] for w in nbrs))
-                mc = int(m0[p])
-                wsz = mc * max(ncap, 1) + mc * mc + 32 * (ncap + mc)
-                asz = 2 * ncap + 3 * mc + 2 * g * 34 + 8
-                isz = (3 * ncap + 1) // 2 + 1
-                lay.append((need, wsz, asz, isz, ncap, mc))
-                need += wsz + asz + isz + 1
-            temp = self._temp(temp, need)
-            tb = temp.data_ptr()
-            ctr = t.zeros(len(chunk), dtype=t.int32, device=dev())
-            prow, nrow = [], []
-            gbeg = 0
-            vmax = 1
-            for k, ((p, nbrs, evs), g, (at, wsz, asz, isz, ncap, mc)) in enumerate(
-                    zip(chunk, gs, lay)):
-                nb0 = len(nrow)
-                for w in nbrs:
-                    if w > p:
-                        nrow.append([w, self.blk(p, w), 0, 0])
-                    else:
-                        nrow.append([w, self.blk(w, p), 1, 0])
-                qoff = self.fb + 8 * self.q_off[(lvl, p)]
-                prow.append([p, nb0, len(nrow), tb + 8 * at, qoff,
-                             tb + 8 * (at + wsz), tb + 8 * (at + wsz + asz),
-                             gbeg, g, ctr.data_ptr() + 4 * k, evs, ncap, mc, 0, 0, 0])
-                gbeg += g
-                vmax = max(vmax, mc)
-            if vmax > MAX_PANEL_ROWS:
-                raise NotImplementedError(
-                    f"interface of {vmax} dofs exceeds the RRQR kernel limit")
-            pd = to_dev_async(np.asarray(prow, dtype=np.int64).reshape(-1, RRQR_ROW))
-            nd = to_dev_async(np.asarray(nrow if nrow else [[0, 0, 0, 0]],
-                                   dtype=np.int64).reshape(-1, 4))
-            dbg = None
-            if DEBUG_WAVES:
-                dbg = [self._debug_panel(p, nbrs) for p, nbrs, _ in chunk]
-                if _os.environ.get("SPAND_DUMP_WAVES"):
-                    import pickle
-                    self._dump_n = getattr(self, "_dump_n", 0) + 1
-                    with open(f"gpurun_out/wave_{self._dump_n}.pkl", "wb") as fh:
-                        pickle.dump({"panels": dbg, "groups": gs, "eps": self.eps,
-                                     "code": code}, fh)
-            if WAVE_LOG is not None:
-                e0 = t.cuda.Event(enable_timing=True)
-                e1 = t.cuda.Event(enable_timing=True)
-                e0.record()
-            _lib.call("spand_rrqr_wave", len(chunk), gbeg, vmax, ptr(pd), ptr(nd),
-                      ptr(self.geo.m0), ptr(self.geo.off), float(self.eps), code,
-                      ptr(self.events), stream())
-            if dbg is not None:
-                self._debug_check(chunk, dbg)
-            if WAVE_LOG is not None:
-                e1.record()
-                WAVE_LOG.append((lvl, len(chunk), gbeg, vmax,
-                                 [(int(m0[p]), int(sum(m0[w] for w in nb)), g)
-                                  for (p, nb, _), g in zip(chunk, gs)], e0, e1))
-        return temp
-
-    def _debug_panel(self, p, nbrs):
-        """Host copy of interface p's current panel (debug only)."""
-        t = self.t
-        t.cuda.synchronize()
-        m0 = self.sym.m0
-        off = self.geo.off.cpu().numpy()
-        pool = self.pool.cpu().numpy()
-        cols = []
-        for w in nbrs:
-            if w > p:
-                b = int(self.boff[self.sym.bid[(p, w)]])
-                blk = pool[b:b + m0[p] * m0[w]].reshape(m0[w], m0[p]).T
-                cols.append(blk[off[p]:, off[w]:])
-            else:
-                b = int(self.boff[self.sym.bid[(w, p)]])
-                blk = pool[b:b + m0[w] * m0[p]].reshape(m0[p], m0[w]).T
-                cols.append(blk[off[w]:, off[p]:].T)
-        mp = m0[p] - off[p]
-        return np.hstack(cols) if cols else np.zeros((mp, 0))
-
-    def _debug_check(self, chunk, panels):
-        from oracle import spand_oracle as orc
-        self.t.cuda.synchronize()
-        ev = self.events.cpu().numpy().reshape(-1, EVENT_ROW)
-        for (p, nbrs, evs), a in zip(chunk, panels):
-            ref = orc.sparsify_panel(a, self.eps, self.scheme.value)
-            e = ev[evs]
-            if int(e[4]) != ref["rank_c"] or int(e[3]) != ref["k_stop"]:
-                print("DEBUG mismatch p", p, "shape", a.shape, "k_c", int(e[4]), ref["rank_c"],
-                      "k_stop", int(e[3]), ref["k_stop"], flush=True)
-                np.save(f"gpurun_out/bad_panel_{p}.npy", a)
-            # coarse rows written back into the blocks: rows [n_fine, m) of
-            # the panel at the OLD offset
-            m0 = self.sym.m0
-            offn = self.geo.off.cpu().numpy()
-            n_fine = int(e[6])
-            old_off = offn[p] - n_fine
-            pool = self.pool.cpu().numpy()
-            cols = []
-            for w in nbrs:
-                if w > p:
-                    b = int(self.boff[self.sym.bid[(p, w)]])
-                    blk = pool[b:b + m0[p] * m0[w]].reshape(m0[w], m0[p]).T
-                    cols.append(blk[old_off:, offn[w]:])
-                else:
-                    b = int(self.boff[self.sym.bid[(w, p)]])
-                    blk = pool[b:b + m0[w] * m0[p]].reshape(m0[p], m0[w]).T
-                    cols.append(blk[offn[w]:, old_off:].T)
-            got = np.hstack(cols) if cols else np.zeros((m0[p] - old_off, 0))
-            rc = got[n_fine:, :]
-            if rc.shape == ref["r_coarse"].shape and rc.size:
-                err = np.abs(rc - ref["r_coarse"]).max() / max(np.abs(ref["r_coarse"]).max(), 1e-300)
-                if err > 1e-9:
-                    print("DEBUG r_coarse mismatch p", p, "err", err, "shape", rc.shape, flush=True)
-                    np.save(f"gpurun_out/bad_rc_panel_{p}.npy", a)
-                    if not getattr(self, "_dumped", False):
-                        self._dumped = True
-                        print("event", e[:7].tolist(), "ref k_stop", ref["k_stop"], "nbrs", nbrs,
-                              "offs", [int(offn[w]) for w in nbrs], "old_off", old_off)
-                        np.set_printoptions(precision=3, linewidth=200, suppress=True)
-                        print("got rows\n", got[:, :14])
-                        print("ref r_coarse\n", ref["r_coarse"][:, :14])
-                        print("ref e\n", ref["e_tilde"][:, :14])
 
     def _scatter_a(self):
         """Initial blocks from the entries of A (factorize.py:61-96).
@@ -507,7 +223,7 @@ class Engine:
         cache per hierarchy, so refactorizing resident inputs does no
         host->device traffic."""
         sym, a = self.sym, self.a
-        key = ("scatter", id(self.h), self.pool_size)
+        key = ("scatter", id(self.h), sym.pool_size)
         cached = a._dev.get(key) if a._dev is not None else None
         if cached is not None and cached[0] is self.h:
             self.pool[cached[1]] = cached[2]
@@ -517,18 +233,16 @@ class Engine:
         cols = a.col_idx
         cl = sym.cluster_of
         slot = np.empty(n, dtype=np.int64)
-        for c, d in enumerate(sym.dofs):
-            slot[d] = np.arange(d.size)
+        for c, dd in enumerate(sym.dofs):
+            slot[dd] = np.arange(dd.size)
         ci, cj = cl[rows], cl[cols]
         up = ci <= cj
         ci, cj, r, c = ci[up], cj[up], rows[up], cols[up]
         keys = ci * sym.ncl + cj
-        bid_arr = np.empty(len(sym.bkeys), dtype=np.int64)
-        kk = np.array([i * sym.ncl + j for i, j in sym.bkeys], dtype=np.int64)
+        kk = sym.bi * sym.ncl + sym.bj
         order = np.argsort(kk)
         pos = order[np.searchsorted(kk[order], keys)]
-        del bid_arr
-        where = self.boff[pos] + slot[r] + slot[c] * sym.m0[ci]
+        where = sym.boff[pos] + slot[r] + slot[c] * sym.m0[ci]
         vals = a.values[up]
         wd, vd = to_dev_async(where, np.int64), to_dev_async(vals, np.float64)
         self.pool[wd] = vd
@@ -544,12 +258,11 @@ class Engine:
         ev = self.events.cpu().numpy().reshape(-1, EVENT_ROW)
         if np.any(ev[:, 9] != 0):
             raise RuntimeError("RRQR group barrier watchdog fired (kernel bug)")
-        # first non-SPD pivot in operator order
-        for kind, lvl, ids, info in self.infos:
-            iv = info.cpu().numpy()
-            bad = np.flatnonzero(iv)
-            if bad.size:
-                raise NotSPD(int(iv[bad[0]]) - 1)
+        # first non-SPD pivot in operator order (info slots follow launch order)
+        iv = self.info.cpu().numpy()
+        bad = np.flatnonzero(iv)
+        if bad.size:
+            raise NotSPD(int(iv[bad[0]]) - 1)
         off = np.zeros(sym.ncl, dtype=np.int64)
         pool, fac = self.pool, self.facbuf
         ops, perm_parts, diags = [], [], []
@@ -560,7 +273,7 @@ class Engine:
             return dofs[c][off[c]:]
 
         def bview(i, j, r0, c0, rows, cols, trans=False):
-            b = int(self.boff[sym.bid[(i, j)]])
+            b = int(sym.boff[sym.bid[(i, j)]])
             return MatView(pool, b + r0 + c0 * m0[i], m0[i], rows, cols, trans)
 
         def fview(at, c, size):
@@ -574,10 +287,6 @@ class Engine:
         fbase = np.concatenate([[0], np.cumsum(cnt)]).astype(int)
         bbase = [1 + int(sum(cnt[i + 1:])) for i in range(len(recs))]
         self.n_phases = int(fbase[-1]) + 1
-        wave_of = {}
-        for r in recs:
-            for p, _, wv in r.get("spars", []):
-                wave_of[(r["level"], p)] = wv
 
         def phases(ri, kind, wave=0):
             r, fb, bb = recs[ri], int(fbase[ri]), bbase[ri]
@@ -621,7 +330,7 @@ class Engine:
                     pv.append((bview(w, s, off[w], off[s], nw, ns), r0))
                     r0 += nw
                 low = bview(s, s, off[s], off[s], ns, ns)
-                linv = fview(self.linv_off[s], s, ns)
+                linv = fview(int(sym.elim_linv[s]), s, ns)
                 op = Elimination(live(s), w_dofs, low, pv, linv=linv)
                 op._phases = phases(ri, "G")
                 ops.append(op)
@@ -630,25 +339,22 @@ class Engine:
                 perm_parts.append(live(s))
             faces = []
             if not rec["skipped"]:
-                act = [p for p in rec["active"] if m0[p] - off[p] > 0]
-                for p in act:
-                    lo = self.resc_off[(lvl, p)]
+                act = [x for x in rec["active"] if m0[x[0]] - off[x[0]] > 0]
+                for p, wv, lo, li, qo, sl, nb in act:
                     mp = m0[p] - off[p]
-                    op = Scaling(live(p), fview(lo[0], p, mp), linv=fview(lo[1], p, mp))
+                    op = Scaling(live(p), fview(lo, p, mp), linv=fview(li, p, mp))
                     op._phases = phases(ri, "D")
                     ops.append(op)
                     arecs.append(("D", op._phases, pst(p), int(mp), op.linv_view))
-                nbr_of = {p: nb for p, nb, _ in rec["spars"]}
-                for p in act:
-                    e = ev[self.event_slot[(lvl, p)]]
+                for p, wv, lo, li, qo, sl, nb in act:
+                    e = ev[sl]
                     mp, k_stop, k_c, rf2, n_fine = (int(e[1]), int(e[3]), int(e[4]),
                                                     int(e[5]), int(e[6]))
                     assert mp == m0[p] - off[p], "event / host offset mismatch"
                     old = live(p)
-                    q = MatView(fac, self.q_off[(lvl, p)], max(mp, 1), mp, mp,
-                                rot=k_c if mp else 0)
+                    q = MatView(fac, qo, max(mp, 1), mp, mp, rot=k_c if mp else 0)
                     qop = Orthogonal(old, q)
-                    qop._phases = phases(ri, "Q", wave_of[(lvl, p)])
+                    qop._phases = phases(ri, "Q", wv)
                     ops.append(qop)
                     arecs.append(("Q", qop._phases, pst(p), int(mp), q))
                     if scheme is SchemeKind.SECOND_ORDER_FULL:
@@ -657,7 +363,7 @@ class Engine:
                         ncorr = k_stop - k_c
                     else:
                         ncorr = 0
-                    wl = [w for w in nbr_of[p] if m0[w] - off[w] > 0]
+                    wl = [w for w in nb if m0[w] - off[w] > 0]
                     ntot = int(sum(m0[w] - off[w] for w in wl))
                     if ncorr and ntot:
                         evs, c0 = [], 0
@@ -697,10 +403,9 @@ class Engine:
         fin = [c for c in sym.final if m0[c] - off[c] > 0]
         total = int(sum(m0[c] - off[c] for c in fin))
         if total:
-            F = self.F
-            foff = self.fcap - total
-            low = MatView(fac, self.f_off + foff + foff * self.fcap, self.fcap, total, total)
-            linv = MatView(fac, self.flinv_off + foff + foff * self.fcap, self.fcap,
+            foff = sym.fcap - total
+            low = MatView(fac, sym.f_off + foff + foff * sym.fcap, sym.fcap, total, total)
+            linv = MatView(fac, sym.flinv_off + foff + foff * sym.fcap, sym.fcap,
                            total, total)
             fd = np.concatenate([live(c) for c in fin])
             fop = Elimination(fd, np.empty(0, np.int64), low, [], linv=linv)

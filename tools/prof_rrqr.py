@@ -12,10 +12,9 @@ engine.WAVE_LOG = []
 f = sp.factorize(a, h, eps, scheme)
 torch.cuda.synchronize()
 rows = []
-for lvl, np_, grid, vmax, panels, e0, e1 in engine.WAVE_LOG:
+for np_, grid, vmax, e0, e1 in engine.WAVE_LOG:
     ms = e0.elapsed_time(e1)
-    big = max(panels, key=lambda t: t[0] * t[1])
-    rows.append((ms, lvl, np_, grid, big))
+    rows.append((ms, np_, grid, vmax))
 rows.sort(reverse=True)
 tot = sum(r[0] for r in rows)
 print("total_ms", tot, "waves", len(rows))
