@@ -93,7 +93,7 @@ int spand_gemv_tiles(int ntiles, const int64_t* tiles, const int64_t* tasks,
 /* for e in [0, nout): s = sum_{t in [ptr[e], ptr[e+1])} scratch[src[t]]
  * (summed in the stored order: deterministic); mode[e] == 0: x[dst[e]] = s,
  * mode[e] == 1: x[dst[e]] -= s. */
-int spand_apply_scatter(int nout, const int32_t* dst, const int8_t* mode,
+int spand_apply_scatter(int nout, const int64_t* dst, const int64_t* mode,
                         const int64_t* ptr, const int64_t* src, double* x,
                         int64_t ldx, const double* scratch, int64_t ldscr,
                         int nvec, void* stream);
@@ -128,7 +128,7 @@ int spand_copy_batched(int ntask, const int64_t* ops, const int32_t* m0,
  * after the last carries only seg_begin at column 7).
  * segment row (14 int64): {A operand(7), B operand(7)}; A is M x K; B is N x K
  * (bT = 1: op(B) = B^T, "NT") or K x N (bT = 0, "NN").
- * tile row (3 int64): {target, m0_tile, n0_tile}; tile 64 x 64.
+ * tile (1 int64, packed): target << 32 | (i0 / 64) << 16 | (j0 / 64); tile 64 x 64.
  * lower_only: skip tiles strictly above the diagonal (SYRK use). */
 int spand_gemm_grouped(int ntile, const int64_t* tiles, const int64_t* targets,
                        const int64_t* segs, const int32_t* m0,
@@ -175,6 +175,28 @@ int spand_count_nonzero(int nview, const int64_t* views, unsigned long long* out
 int spand_nd_partition(int64_t n, const int64_t* row_ptr, const int64_t* col_idx,
                        int levels, int64_t* dofs_out, int64_t* cptr_out,
                        int32_t* depth_out, int64_t* ncl_out);
+
+/* ---- native level scheduler (planner.cpp) and collector (collect.cpp) ----
+ * Host-side runtime of the factorization: symbolic structure, the launch
+ * program, and after the run the operator tables / permutation /
+ * diagnostics / apply image.  Layouts are documented in the sources. */
+void* spand_plan_create(int ncl, const int64_t* m0, const int32_t* depth, int levels,
+                        int skip, int64_t npairs, const int64_t* pairs, int cap_override);
+void spand_plan_destroy(void* h);
+int spand_plan_set_dofs(void* h, const int64_t* dofs, const int64_t* dptr);
+int spand_plan_sizes(void* h, int64_t* out);
+int spand_plan_emit(void* h, int64_t pool_base, int64_t fac_base, int64_t temp_base,
+                    int64_t ctr_base, int dry);
+int spand_plan_program(void* h, int64_t* prog, int64_t* launches);
+int spand_plan_meta(void* h, int64_t* out);
+void* spand_collect_create(void* plan, const int64_t* events, int scheme);
+void spand_collect_destroy(void* h);
+int spand_collect_sizes(void* h, int64_t* out);
+int spand_collect_get(void* h, int64_t* ops, int64_t* segs, int64_t* perm, int64_t* diag,
+                      int64_t* lsum, int64_t* views, int64_t* fidx);
+int spand_collect_apply(void* h, int64_t pool_base, int64_t fac_base, int64_t xbuf,
+                        int64_t idx_addr, int64_t* out);
+int spand_collect_apply_get(void* h, int64_t* image, int64_t* phases);
 
 #ifdef __cplusplus
 }

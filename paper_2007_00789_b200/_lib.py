@@ -44,7 +44,7 @@ SIGNATURES = {
     "spand_count_nonzero": [_c_int, _P, _P, _P],
     "spand_nd_partition": [_c_i64, _P, _P, _c_int, _P, _P, _P, _P],
     "spand_plan_sizes": [_P, _P],
-    "spand_plan_emit": [_P, _c_i64, _c_i64, _c_i64, _c_i64],
+    "spand_plan_emit": [_P, _c_i64, _c_i64, _c_i64, _c_i64, _c_int],
     "spand_plan_program": [_P, _P, _P],
     "spand_plan_meta": [_P, _P],
 }

@@ -185,13 +185,13 @@ class _Pass:
             if dst_parts:
                 dst = np.concatenate(dst_parts)
                 src = np.arange(dst.size, dtype=np.int64)   # tiles are laid out in order
-                mode = np.repeat(np.asarray(modes, dtype=np.int8), lens)
+                mode = np.repeat(np.asarray(modes, dtype=np.int64), lens)
                 order = np.argsort(dst, kind="stable")      # keeps sequence order
                 dst, src, mode = dst[order], src[order], mode[order]
                 first = np.r_[True, dst[1:] != dst[:-1]]
                 starts = np.flatnonzero(first)
                 ptrs = np.r_[starts, dst.size].astype(np.int64)
-                scat.append((dst[starts].astype(np.int32), mode[starts],
+                scat.append((dst[starts].astype(np.int64), mode[starts],
                              ptrs, src))
             else:
                 scat.append(None)

@@ -100,15 +100,15 @@ gemv_tiles_kernel(const int64_t* __restrict__ tiles, const int64_t* __restrict__
 }
 
 __global__ void __launch_bounds__(kThreads)
-scatter_kernel(int nout, const int32_t* __restrict__ dst, const int8_t* __restrict__ mode,
+scatter_kernel(int nout, const int64_t* __restrict__ dst, const int64_t* __restrict__ mode,
                const int64_t* __restrict__ ptr, const int64_t* __restrict__ src,
                double* __restrict__ x, int64_t ldx, const double* __restrict__ scratch,
                int64_t ldscr, int nvec) {
   const int e = blockIdx.x * kThreads + threadIdx.x;
   if (e >= nout) return;
   const int64_t b = ptr[e], f = ptr[e + 1];
-  const int d = dst[e];
-  const int md = mode[e];
+  const int64_t d = dst[e];
+  const int md = (int)mode[e];
   for (int v = 0; v < nvec; ++v) {
     double s = 0.0;
     for (int64_t t = b; t < f; ++t) s += scratch[src[t] + v * ldscr];
@@ -131,7 +131,7 @@ int spand_gemv_tiles(int ntiles, const int64_t* tiles, const int64_t* tasks, con
   return 0;
 }
 
-int spand_apply_scatter(int nout, const int32_t* dst, const int8_t* mode, const int64_t* ptr,
+int spand_apply_scatter(int nout, const int64_t* dst, const int64_t* mode, const int64_t* ptr,
                         const int64_t* src, double* x, int64_t ldx, const double* scratch,
                         int64_t ldscr, int nvec, void* stream) {
   if (nout < 0 || nvec < 1) return -1;

@@ -1,0 +1,356 @@
+// Native collection of a finished device factorization (host C++).
+//
+// After the factorization program has run, the only data the host needs from
+// the device are the per-interface events (rank k_c, fine count, k_stop).
+// This file replays the live offsets (the reference keeps dofs[n_fine:],
+// factorize.py:187-190) and produces, in the reference's operator order
+// (factorize.py:309-366):
+//   * an operator table + neighbour-segment table (payload windows inside the
+//     device block pool / factor buffer) from which the Python host builds
+//     the Elimination / Scaling / Orthogonal / ErrorCorrection objects lazily;
+//   * the permutation, per-interface diagnostics and per-level summaries;
+//   * the payload windows whose nonzeros the device counts (nnz_factor);
+//   * the structured apply plan (phases of GEMV tiles + ordered scatters in
+//     the cluster-contiguous numbering, see apply.cu / fastplan.py).
+#include <algorithm>
+#include <cstdint>
+#include <cstring>
+#include <vector>
+
+#include "planner.h"
+
+namespace {
+
+struct Task {
+  int64_t M, ld, rows, cols, trans, rot, in_kind, in_ptr;
+  int64_t out_start;   // permuted start of the outputs, or -1: index list
+  int64_t out_idx;     // offset into the index store when out_start < 0
+  int64_t mode;
+};
+
+struct Collected {
+  std::vector<int64_t> ops;    // 16 per op
+  std::vector<int64_t> segs;   // 8 per segment
+  std::vector<int64_t> perm;
+  std::vector<int64_t> diag;   // 10 per sparsified interface
+  std::vector<int64_t> lsum;   // 4 per level: level, n_interiors, interior dofs, skipped
+  std::vector<int64_t> views;  // 4 per payload window: base(0 pool,1 fac) | off, ld, rows, cols
+  int64_t final_total = 0;
+  // apply
+  std::vector<std::vector<Task>> fph, bph;
+  std::vector<int64_t> fidx;   // permuted indices of the final block
+  std::vector<int64_t> plan;   // device image (int64)
+  std::vector<int64_t> phases; // 10 per phase (see spand_collect_apply_get)
+  int64_t scratch_len = 0;
+};
+
+}  // namespace
+
+extern "C" {
+
+void* spand_collect_create(void* plan, const int64_t* events, int scheme) {
+  const spand::Plan& pv = *static_cast<spand::Plan*>(plan);
+  Collected* C = new Collected();
+  const int ncl = pv.ncl;
+  std::vector<int64_t> off(ncl, 0), cstart(ncl + 1, 0);
+  for (int c = 0; c < ncl; ++c) cstart[c + 1] = cstart[c] + pv.m0[c];
+  auto live = [&](int c) { return pv.m0[c] - off[c]; };
+  auto pst = [&](int c) { return cstart[c] + off[c]; };
+  // apply phase numbering (forward per level: [G-T][G-A]([D]([Q-T][E-A])*waves))
+  const int nlev = (int)pv.lv.size();
+  std::vector<int64_t> cnt(nlev), fbase(nlev + 1, 0), bbase(nlev);
+  for (int li = 0; li < nlev; ++li) {
+    const spand::Level& L = pv.lv[li];
+    cnt[li] = 2 + (L.skipped ? 0 : 1 + 2 * L.nwaves);
+    fbase[li + 1] = fbase[li] + cnt[li];
+  }
+  const int64_t nph = fbase[nlev] + 1;
+  for (int li = 0; li < nlev; ++li) {
+    int64_t s = 1;
+    for (int lj = li + 1; lj < nlev; ++lj) s += cnt[lj];
+    bbase[li] = s;
+  }
+  C->fph.assign(nph, {});
+  C->bph.assign(nph, {});
+  auto add = [&](std::vector<Task>& ph, int64_t M, int64_t ld, int64_t rows, int64_t cols,
+                 int vtrans, int optrans, int64_t rot, int64_t in_start, int64_t out_start,
+                 int64_t mode) {
+    Task t;
+    t.M = M;
+    t.ld = ld;
+    t.rows = rows;
+    t.cols = cols;
+    t.trans = (vtrans != optrans) ? 1 : 0;
+    t.rot = rot;
+    t.in_kind = 1;
+    t.in_ptr = in_start;        // permuted index; turned into an address at build
+    t.out_start = out_start;
+    t.out_idx = 0;
+    t.mode = mode;
+    ph.push_back(t);
+  };
+  for (int li = 0; li < nlev; ++li) {
+    const spand::Level& L = pv.lv[li];
+    const int64_t fb = fbase[li], bb = bbase[li];
+    const int64_t nw = L.skipped ? 0 : L.nwaves;
+    const int64_t gfT = fb, gfA = fb + 1;
+    const int64_t gbA = bb + (L.skipped ? 0 : 2 * nw + 1), gbT = bb + (L.skipped ? 1 : 2 * nw + 2);
+    int64_t nint = 0, ndofs = 0;
+    for (int k = 0; k < (int)L.interiors.size(); ++k) {
+      const int s = L.interiors[k];
+      const int64_t ns = live(s);
+      if (ns == 0) continue;
+      ++nint;
+      ndofs += ns;
+      const int64_t m0s = pv.m0[s];
+      const int64_t lower = pv.boff[pv.block(s, s)] + off[s] + off[s] * m0s;
+      const int64_t linv = pv.elim_linv[s] + off[s] + off[s] * m0s;
+      const int64_t sb = (int64_t)C->segs.size() / 8;
+      for (int w : L.inbrs[k]) {
+        const int64_t lw = live(w);
+        if (lw == 0) continue;
+        const int64_t a = pv.boff[pv.block(w, s)] + off[w] + off[s] * pv.m0[w];
+        C->segs.insert(C->segs.end(), {w, off[w], lw, a, pv.m0[w], lw, ns, 0});
+        C->views.insert(C->views.end(), {a, pv.m0[w], lw, ns});
+        add(C->fph[gfA], a, pv.m0[w], lw, ns, 0, 0, 0, pst(s), pst(w), 1);
+        add(C->bph[gbA], a, pv.m0[w], lw, ns, 0, 1, 0, pst(w), pst(s), 1);
+      }
+      const int64_t se = (int64_t)C->segs.size() / 8;
+      C->ops.insert(C->ops.end(), {0, s, li, 0, off[s], ns, 0, lower, m0s, linv, -1, 0, sb, se, 0, 0});
+      C->views.insert(C->views.end(), {lower, m0s, ns, ns});
+      add(C->fph[gfT], linv | (int64_t(1) << 62), m0s, ns, ns, 0, 0, 0, pst(s), pst(s), 0);
+      add(C->bph[gbT], linv | (int64_t(1) << 62), m0s, ns, ns, 0, 1, 0, pst(s), pst(s), 0);
+      for (int64_t i = 0; i < ns; ++i) C->perm.push_back(pv.dofs[pv.dptr[s] + off[s] + i]);
+    }
+    C->lsum.insert(C->lsum.end(), {L.level, nint, ndofs, L.skipped});
+    if (L.skipped) continue;
+    // rescales
+    for (int k = 0; k < (int)L.active.size(); ++k) {
+      const int p = L.active[k];
+      const int64_t mp = live(p);
+      if (mp == 0) continue;
+      const int64_t m0p = pv.m0[p];
+      const int64_t lo = L.l_off[k] + off[p] + off[p] * m0p;
+      const int64_t li2 = L.linv_off[k] + off[p] + off[p] * m0p;
+      C->ops.insert(C->ops.end(), {1, p, li, 0, off[p], mp, 0, lo, m0p, li2, -1, 0, 0, 0, 1, 0});
+      C->views.insert(C->views.end(), {lo | (int64_t(1) << 62), m0p, mp, mp});
+      add(C->fph[fb + 2], li2 | (int64_t(1) << 62), m0p, mp, mp, 0, 0, 0, pst(p), pst(p), 0);
+      add(C->bph[bb + 2 * nw], li2 | (int64_t(1) << 62), m0p, mp, mp, 0, 1, 0, pst(p), pst(p), 0);
+    }
+    // sparsifications in ascending id order
+    for (int k = 0; k < (int)L.active.size(); ++k) {
+      const int p = L.active[k];
+      const int64_t mp = live(p);
+      if (mp == 0) continue;
+      const int64_t* e = events + 12 * L.slot[k];
+      const int64_t k_stop = e[3], k_c = e[4], rf2 = e[5], n_fine = e[6];
+      const int wv = L.wave[k];
+      const int64_t qfT = fb + 3 + 2 * wv, efA = fb + 4 + 2 * wv;
+      const int64_t back = bb + 2 * (nw - 1 - wv), ebA = back, qbT = back + 1;
+      const int64_t qo = L.q_off[k];
+      C->ops.insert(C->ops.end(), {2, p, li, wv, off[p], mp, 0, 0, mp, 0, qo, k_c, 0, 0, 0, 0});
+      C->views.insert(C->views.end(), {qo | (int64_t(1) << 62), mp, mp, mp});
+      add(C->fph[qfT], qo | (int64_t(1) << 62), mp, mp, mp, 0, 1, k_c, pst(p), pst(p), 0);
+      add(C->bph[qbT], qo | (int64_t(1) << 62), mp, mp, mp, 0, 0, k_c, pst(p), pst(p), 0);
+      int64_t ncorr = 0;
+      if (scheme == 1) ncorr = n_fine;
+      else if (scheme == 2) ncorr = k_stop - k_c;
+      int64_t ntot = 0;
+      for (int w : L.anbrs[k]) ntot += live(w);
+      if (ncorr && ntot) {
+        const int64_t sb = (int64_t)C->segs.size() / 8;
+        for (int w : L.anbrs[k]) {
+          const int64_t lw = live(w);
+          if (lw == 0) continue;
+          if (w > p) {
+            const int64_t a = pv.boff[pv.block(p, w)] + off[p] + off[w] * pv.m0[p];
+            C->segs.insert(C->segs.end(), {w, off[w], lw, a, pv.m0[p], ncorr, lw, 0});
+            C->views.insert(C->views.end(), {a, pv.m0[p], ncorr, lw});
+            add(C->fph[efA], a, pv.m0[p], ncorr, lw, 0, 1, 0, pst(p), pst(w), 1);
+            add(C->bph[ebA], a, pv.m0[p], ncorr, lw, 0, 0, 0, pst(w), pst(p), 1);
+          } else {
+            const int64_t a = pv.boff[pv.block(w, p)] + off[w] + off[p] * pv.m0[w];
+            C->segs.insert(C->segs.end(), {w, off[w], lw, a, pv.m0[w], lw, ncorr, 1});
+            C->views.insert(C->views.end(), {a, pv.m0[w], lw, ncorr});
+            add(C->fph[efA], a, pv.m0[w], lw, ncorr, 1, 1, 0, pst(p), pst(w), 1);
+            add(C->bph[ebA], a, pv.m0[w], lw, ncorr, 1, 0, 0, pst(w), pst(p), 1);
+          }
+        }
+        const int64_t se = (int64_t)C->segs.size() / 8;
+        C->ops.insert(C->ops.end(), {3, p, li, wv, off[p], ncorr, 0, 0, 0, 0, -1, 0, sb, se, 0, 0});
+      }
+      for (int64_t i = 0; i < n_fine; ++i) C->perm.push_back(pv.dofs[pv.dptr[p] + off[p] + i]);
+      C->diag.insert(C->diag.end(), {li, p, mp, k_c, rf2, e[7], e[8], k_stop, e[2], 0});
+      off[p] += n_fine;
+    }
+  }
+  // final dense block
+  int64_t total = 0;
+  for (int c : pv.fin) total += live(c);
+  C->final_total = total;
+  if (total) {
+    const int64_t foff = pv.fcap - total;
+    const int64_t lower = pv.f_off + foff + foff * pv.fcap;
+    const int64_t linv = pv.flinv_off + foff + foff * pv.fcap;
+    C->ops.insert(C->ops.end(), {4, -1, nlev, 0, 0, total, 0, lower, pv.fcap, linv, -1, 0, 0, 0, 1, 0});
+    C->views.insert(C->views.end(), {lower | (int64_t(1) << 62), pv.fcap, total, total});
+    for (int c : pv.fin) {
+      for (int64_t i = 0; i < live(c); ++i) {
+        C->perm.push_back(pv.dofs[pv.dptr[c] + off[c] + i]);
+        C->fidx.push_back(pst(c) + i);
+      }
+    }
+    Task tf;
+    tf.M = linv | (int64_t(1) << 62);
+    tf.ld = pv.fcap;
+    tf.rows = tf.cols = total;
+    tf.trans = 0;
+    tf.rot = 0;
+    tf.in_kind = 0;
+    tf.in_ptr = 0;
+    tf.out_start = -1;
+    tf.out_idx = 0;
+    tf.mode = 0;
+    C->fph[nph - 1].push_back(tf);
+    tf.trans = 1;
+    C->bph[0].push_back(tf);
+  }
+  return C;
+}
+
+void spand_collect_destroy(void* h) { delete static_cast<Collected*>(h); }
+
+// out[8]: nops, nsegs, nperm, ndiag, nlsum, nviews, final_total, 0
+int spand_collect_sizes(void* h, int64_t* out) {
+  Collected* C = static_cast<Collected*>(h);
+  out[0] = (int64_t)C->ops.size() / 16;
+  out[1] = (int64_t)C->segs.size() / 8;
+  out[2] = (int64_t)C->perm.size();
+  out[3] = (int64_t)C->diag.size() / 10;
+  out[4] = (int64_t)C->lsum.size() / 4;
+  out[5] = (int64_t)C->views.size() / 4;
+  out[6] = C->final_total;
+  out[7] = 0;
+  return 0;
+}
+
+int spand_collect_get(void* h, int64_t* ops, int64_t* segs, int64_t* perm, int64_t* diag,
+                      int64_t* lsum, int64_t* views, int64_t* fidx) {
+  Collected* C = static_cast<Collected*>(h);
+  auto cp = [](int64_t* dst, const std::vector<int64_t>& v) {
+    if (dst && !v.empty()) std::memcpy(dst, v.data(), v.size() * sizeof(int64_t));
+  };
+  cp(ops, C->ops);
+  cp(segs, C->segs);
+  cp(perm, C->perm);
+  cp(diag, C->diag);
+  cp(lsum, C->lsum);
+  cp(views, C->views);
+  cp(fidx, C->fidx);
+  return 0;
+}
+
+// ---- structured apply plan ------------------------------------------------
+// Device image (int64): per phase {task rows (8 each), packed tile rows
+// (8 each, apply.cu layout), scatter dst[nout], mode[nout], ptr[nout+1],
+// src[nsrc]} + the final block's index list (int32 pairs packed in int64).
+// Addresses: payload windows pool_base/fac_base (bit 62 of the window offset
+// selects the factor buffer), inputs xbuf + 8 * permuted index.
+static void compile_phase(Collected* C, const std::vector<Task>& ph, int64_t pool_base,
+                          int64_t fac_base, int64_t xbuf, int64_t idx_addr) {
+  constexpr int64_t TO = 64, TK = 2048;
+  std::vector<int64_t> rows, tiles, dst, mode, src;
+  int64_t pos = 0;
+  std::vector<std::pair<int64_t, int64_t>> ent;   // (dst, src) in task order
+  std::vector<int64_t> emode;
+  for (const Task& t : ph) {
+    const int64_t nout = t.trans ? t.cols : t.rows;
+    const int64_t nk = t.trans ? t.rows : t.cols;
+    if (nout == 0) continue;
+    const bool in_fac = (t.M >> 62) & 1;
+    const int64_t moff = t.M & ((int64_t(1) << 62) - 1);
+    const int64_t maddr = (in_fac ? fac_base : pool_base) + 8 * moff;
+    const int64_t inp = t.in_kind == 1 ? xbuf + 8 * t.in_ptr : idx_addr;
+    const int64_t tid = (int64_t)rows.size() / 8;
+    rows.insert(rows.end(), {maddr, t.ld, t.rows, t.cols, t.trans, t.rot, t.in_kind, inp});
+    const int64_t nkt = std::max<int64_t>(1, (nk + TK - 1) / TK);
+    for (int64_t kb = 0; kb < nkt; ++kb)
+      for (int64_t ob = 0; ob < nout; ob += TO) {
+        const int64_t oc = std::min(TO, nout - ob);
+        const int64_t kc = std::max<int64_t>(0, std::min(TK, nk - kb * TK));
+        tiles.insert(tiles.end(), {tid, ob, oc, kb * TK, kc, pos + kb * nout + ob, 0, 0});
+      }
+    for (int64_t kb = 0; kb < nkt; ++kb)
+      for (int64_t o = 0; o < nout; ++o) {
+        const int64_t d = t.out_start >= 0 ? t.out_start + o : C->fidx[o];
+        ent.push_back({d, pos + kb * nout + o});
+        emode.push_back(t.mode);
+      }
+    pos += nout * nkt;
+  }
+  if (rows.empty()) return;
+  // stable order by destination: sequence order kept inside a destination
+  std::vector<int64_t> order(ent.size());
+  for (size_t i = 0; i < order.size(); ++i) order[i] = (int64_t)i;
+  std::stable_sort(order.begin(), order.end(),
+                   [&](int64_t a, int64_t b) { return ent[a].first < ent[b].first; });
+  std::vector<int64_t> ptr;
+  for (size_t u = 0; u < order.size(); ++u) {
+    const auto& e = ent[order[u]];
+    if (u == 0 || e.first != ent[order[u - 1]].first) {
+      dst.push_back(e.first);
+      mode.push_back(emode[order[u]]);
+      ptr.push_back((int64_t)u);
+    }
+    src.push_back(e.second);
+  }
+  ptr.push_back((int64_t)order.size());
+  auto put = [&](const std::vector<int64_t>& v) {
+    const int64_t at = (int64_t)C->plan.size();
+    C->plan.insert(C->plan.end(), v.begin(), v.end());
+    return at;
+  };
+  const int64_t a = put(rows), b = put(tiles), c = put(dst), d = put(mode), e = put(ptr),
+                f = put(src);
+  C->phases.insert(C->phases.end(), {a, (int64_t)rows.size() / 8, b, (int64_t)tiles.size() / 8,
+                                     c, (int64_t)dst.size(), d, e, f, pos});
+  C->scratch_len = std::max(C->scratch_len, pos);
+}
+
+// Build the apply image.  idx_addr: device address of the final block's
+// permuted index list (int32, spand_collect_get's fidx).  out[4]: image
+// length, number of forward phases, number of backward phases, scratch.
+int spand_collect_apply(void* h, int64_t pool_base, int64_t fac_base, int64_t xbuf,
+                        int64_t idx_addr, int64_t* out) {
+  Collected* C = static_cast<Collected*>(h);
+  C->plan.clear();
+  C->phases.clear();
+  C->scratch_len = 1;
+  int64_t nfw = 0, nbw = 0;
+  for (const auto& ph : C->fph) {
+    const size_t before = C->phases.size();
+    compile_phase(C, ph, pool_base, fac_base, xbuf, idx_addr);
+    nfw += (C->phases.size() > before);
+  }
+  for (const auto& ph : C->bph) {
+    const size_t before = C->phases.size();
+    compile_phase(C, ph, pool_base, fac_base, xbuf, idx_addr);
+    nbw += (C->phases.size() > before);
+  }
+  out[0] = (int64_t)C->plan.size();
+  out[1] = nfw;
+  out[2] = nbw;
+  out[3] = C->scratch_len;
+  return 0;
+}
+
+// phase rows (10 int64): tasks_off, ntask, tiles_off, ntile, dst_off, nout,
+// mode_off, ptr_off, src_off, scratch_used
+int spand_collect_apply_get(void* h, int64_t* image, int64_t* phases) {
+  Collected* C = static_cast<Collected*>(h);
+  std::memcpy(image, C->plan.data(), C->plan.size() * sizeof(int64_t));
+  std::memcpy(phases, C->phases.data(), C->phases.size() * sizeof(int64_t));
+  return 0;
+}
+
+}  // extern "C"

@@ -41,9 +41,10 @@ gemm_grouped_kernel(const int64_t* __restrict__ tiles, const int64_t* __restrict
                     int lower_only) {
   __shared__ __align__(16) double As[2][BK][LDS];
   __shared__ __align__(16) double Bs[2][BK][LDS];
-  const int64_t* tr = tiles + 3 * (int64_t)blockIdx.x;
-  const int64_t t = tr[0];
-  const int i0 = (int)tr[1], j0 = (int)tr[2];
+  // packed tile: target << 32 | (i0 / 64) << 16 | (j0 / 64)
+  const int64_t tr = tiles[blockIdx.x];
+  const int64_t t = tr >> 32;
+  const int i0 = (int)((tr >> 16) & 0xffff) * BM, j0 = (int)(tr & 0xffff) * BN;
   if (lower_only && j0 > i0) return;
   const int64_t* trow = targets + 8 * t;
   const Opnd C = load_opnd(trow, m0, off);

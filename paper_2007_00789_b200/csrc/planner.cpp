@@ -14,6 +14,7 @@
 //   [7] x2  [8] bits(alpha)  [9] bits(beta)  [10..15] 0
 // types: 1 potrf(a=ops, x0=info index)  2 trtri tiles(a=ops)
 //        3 gemm(a=tiles, b=targets, c=segs, x0=bT, x1=lower_only, alpha, beta)
+//          (tile rows are packed: target << 32 | (i0 / 64) << 16 | (j0 / 64))
 //        4 copy(a=ops)  5 rrqr wave(a=panels, b=nbrs, x0=grid, x1=vmax)
 //        6 assemble final(a=cluster ids, b=block rows, x0=nblk, x1=final id,
 //          x2=fac offset of the dense block)
@@ -28,499 +29,9 @@
 
 extern "C" int spand_rrqr_capacity(int vmax);
 
-namespace {
+#include "planner.h"
 
-constexpr int kTile = 64;
-
-struct Level {
-  int level = 0;
-  bool skipped = true;
-  std::vector<int> interiors;
-  std::vector<std::vector<int>> inbrs;      // neighbours of each interior
-  std::vector<int> targets;                 // Schur target block ids (creation order)
-  std::vector<std::vector<int>> tsegs;      // contributing interiors per target
-  std::vector<int> active;
-  std::vector<int> resc_blocks;             // off-diagonal blocks among active
-  std::vector<int> wave;                    // per active cluster
-  std::vector<std::vector<int>> anbrs;      // neighbours of each active cluster
-  int nwaves = 0;
-  // layout
-  std::vector<int64_t> l_off, linv_off, q_off, slot;   // per active
-};
-
-struct Plan {
-  int ncl = 0, levels = 0, skip = 0;
-  std::vector<int64_t> m0;
-  std::vector<int32_t> depth;
-  std::vector<int32_t> bi, bj;
-  std::unordered_map<int64_t, int32_t> bid;
-  std::vector<Level> lv;
-  std::vector<int> fin, fin_blocks;
-  // layout
-  std::vector<int64_t> boff, elim_linv;
-  int64_t pool_size = 0, fac_size = 0, fcap = 0, f_off = 0, flinv_off = 0;
-  int64_t n_events = 0, n_info = 0, temp_size = 0;
-  // program
-  std::vector<int64_t> prog, launches;
-  int cap_override = 0;
-
-  int64_t key(int i, int j) const { return (int64_t)i * ncl + j; }
-  int block(int i, int j) const { return bid.at(key(i, j)); }
-  int new_block(int i, int j, std::vector<std::set<int>>& cb) {
-    const int b = (int)bi.size();
-    bi.push_back(i);
-    bj.push_back(j);
-    bid[key(i, j)] = b;
-    cb[i].insert(b);
-    cb[j].insert(b);
-    return b;
-  }
-
-  void symbolic(int64_t npairs, const int64_t* pairs) {
-    std::vector<std::set<int>> adj(ncl), cb(ncl);
-    for (int64_t t = 0; t < npairs; ++t) {
-      const int i = (int)(pairs[t] / ncl), j = (int)(pairs[t] % ncl);
-      new_block(i, j, cb);
-      if (i != j) {
-        adj[i].insert(j);
-        adj[j].insert(i);
-      }
-    }
-    for (int c = 0; c < ncl; ++c)
-      if (!bid.count(key(c, c))) new_block(c, c, cb);
-    std::vector<char> alive(ncl, 1);
-    for (int level = levels; level >= 1; --level) {
-      Level L;
-      L.level = level;
-      std::map<int, int> tindex;  // block id -> target index (order of first use)
-      for (int c = 0; c < ncl; ++c)
-        if (alive[c] && depth[c] == level) L.interiors.push_back(c);
-      for (int s : L.interiors) {
-        std::vector<int> nb(adj[s].begin(), adj[s].end());
-        L.inbrs.push_back(nb);
-        for (size_t a = 0; a < nb.size(); ++a)
-          for (size_t b = a; b < nb.size(); ++b) {
-            const int wa = nb[a], wb = nb[b];
-            auto it = bid.find(key(wa, wb));
-            int blk;
-            if (it == bid.end()) {
-              blk = new_block(wa, wb, cb);
-              if (wa != wb) {
-                adj[wa].insert(wb);
-                adj[wb].insert(wa);
-              }
-            } else {
-              blk = it->second;
-            }
-            auto ti = tindex.find(blk);
-            if (ti == tindex.end()) {
-              tindex[blk] = (int)L.targets.size();
-              L.targets.push_back(blk);
-              L.tsegs.push_back({s});
-            } else {
-              L.tsegs[ti->second].push_back(s);
-            }
-          }
-        for (int w : nb) adj[w].erase(s);
-        for (int b : cb[s]) {
-          const int other = bi[b] == s ? bj[b] : bi[b];
-          if (other != s) cb[other].erase(b);
-        }
-        cb[s].clear();
-        adj[s].clear();
-        alive[s] = 0;
-      }
-      L.skipped = (levels - level) < skip;
-      if (!L.skipped) {
-        for (int c = 0; c < ncl; ++c)
-          if (alive[c]) L.active.push_back(c);
-        std::set<std::pair<int, int>> rb;
-        for (int c : L.active)
-          for (int b : cb[c])
-            if (bi[b] != bj[b]) rb.insert({bi[b], bj[b]});
-        for (auto& pr : rb) L.resc_blocks.push_back(block(pr.first, pr.second));
-        std::unordered_map<int, int> wave;
-        for (int p : L.active) {
-          std::vector<int> nb(adj[p].begin(), adj[p].end());
-          int wv = 0;
-          for (int q : nb)
-            if (q < p) wv = std::max(wv, wave[q] + 1);
-          wave[p] = wv;
-          L.wave.push_back(wv);
-          L.anbrs.push_back(nb);
-          L.nwaves = std::max(L.nwaves, wv + 1);
-        }
-      }
-      lv.push_back(std::move(L));
-    }
-    for (int c = 0; c < ncl; ++c)
-      if (alive[c]) fin.push_back(c);
-    std::set<std::pair<int, int>> fb;
-    for (int c : fin)
-      for (int b : cb[c]) fb.insert({bi[b], bj[b]});
-    for (auto& pr : fb) fin_blocks.push_back(block(pr.first, pr.second));
-  }
-
-  void layout() {
-    boff.resize(bi.size());
-    pool_size = 0;
-    for (size_t b = 0; b < bi.size(); ++b) {
-      boff[b] = pool_size;
-      pool_size += m0[bi[b]] * m0[bj[b]];
-    }
-    elim_linv.assign(ncl, -1);
-    fac_size = 0;
-    n_events = n_info = 0;
-    for (auto& L : lv) {
-      for (int s : L.interiors) {
-        elim_linv[s] = fac_size;
-        fac_size += m0[s] * m0[s];
-      }
-      n_info += (int64_t)L.interiors.size();
-      if (!L.skipped) {
-        for (int p : L.active) {
-          L.l_off.push_back(fac_size);
-          fac_size += m0[p] * m0[p];
-          L.linv_off.push_back(fac_size);
-          fac_size += m0[p] * m0[p];
-          L.q_off.push_back(fac_size);
-          fac_size += m0[p] * m0[p];
-          L.slot.push_back(n_events++);
-        }
-        n_info += (int64_t)L.active.size();
-      }
-    }
-    fcap = 0;
-    for (int c : fin) fcap += m0[c];
-    f_off = fac_size;
-    fac_size += fcap * fcap;
-    flinv_off = fac_size;
-    fac_size += fcap * fcap;
-    n_info += 1;
-  }
-
-  // ---------------------------------------------------------------- emit
-  int64_t pool_base = 0, fac_base = 0, temp_base = 0, ctr_base = 0;
-  int64_t info_next = 0, ctr_next = 0;
-
-  int64_t blk_ptr(int i, int j) const { return pool_base + 8 * boff[block(i, j)]; }
-  static void opnd(std::vector<int64_t>& v, int64_t p, int rc, int cc, int64_t rs = 0,
-                   int64_t cs = 0, int64_t rn = -1, int64_t cn = -1) {
-    v.insert(v.end(), {p, rc, cc, rs, cs, rn, cn});
-  }
-  static void sub(std::vector<int64_t>& v, const int64_t* o, int64_t rs, int64_t cs, int64_t rn,
-                  int64_t cn) {
-    const int64_t r = o[5] < 0 ? rn : std::min(rn, std::max(o[5] - rs, (int64_t)0));
-    const int64_t c = o[6] < 0 ? cn : std::min(cn, std::max(o[6] - cs, (int64_t)0));
-    v.insert(v.end(), {o[0], o[1], o[2], o[3] + rs, o[4] + cs, r, c});
-  }
-  int64_t push(const std::vector<int64_t>& rows) {
-    const int64_t at = (int64_t)prog.size();
-    prog.insert(prog.end(), rows.begin(), rows.end());
-    return at;
-  }
-  void launch(int64_t type, int64_t count, int64_t a, int64_t b = 0, int64_t c = 0,
-              int64_t x0 = 0, int64_t x1 = 0, int64_t x2 = 0, double alpha = 0.0,
-              double beta = 0.0) {
-    int64_t ab, bb;
-    std::memcpy(&ab, &alpha, 8);
-    std::memcpy(&bb, &beta, 8);
-    launches.insert(launches.end(), {type, count, a, b, c, x0, x1, x2, ab, bb, 0, 0, 0, 0, 0, 0});
-  }
-
-  struct Target {
-    std::vector<int64_t> c;          // 7
-    std::vector<int64_t> segs;       // 14 per segment
-    int64_t mm, nn;
-  };
-  void gemm(const std::vector<Target>& ts, double alpha, double beta, int bT, int lower) {
-    if (ts.empty()) return;
-    std::vector<int64_t> trow, srow, tiles;
-    int64_t nseg = 0;
-    for (size_t t = 0; t < ts.size(); ++t) {
-      trow.insert(trow.end(), ts[t].c.begin(), ts[t].c.end());
-      trow.push_back(nseg);
-      srow.insert(srow.end(), ts[t].segs.begin(), ts[t].segs.end());
-      nseg += (int64_t)ts[t].segs.size() / 14;
-      for (int64_t i = 0; i < ts[t].mm; i += kTile)
-        for (int64_t j = 0; j < ts[t].nn; j += kTile) {
-          if (lower && j > i) continue;
-          tiles.insert(tiles.end(), {(int64_t)t, i, j});
-        }
-    }
-    trow.insert(trow.end(), {0, 0, 0, 0, 0, 0, 0, nseg});
-    if (tiles.empty()) return;
-    if (srow.empty()) srow.assign(14, 0);
-    const int64_t a = push(tiles), b = push(trow), c = push(srow);
-    launch(3, (int64_t)tiles.size() / 3, a, b, c, bT, lower, 0, alpha, beta);
-  }
-
-  // batched triangular inverses: 64-tiles + recursive doubling GEMMs
-  void trtri(const std::vector<std::vector<int64_t>>& Ls, const std::vector<std::vector<int64_t>>& Xs,
-             const std::vector<int64_t>& sizes, int64_t temp_at) {
-    if (Ls.empty()) return;
-    std::vector<int64_t> rows;
-    int64_t nmax = 0;
-    for (size_t t = 0; t < Ls.size(); ++t) {
-      nmax = std::max(nmax, sizes[t]);
-      for (int64_t o = 0; o < sizes[t]; o += kTile) {
-        sub(rows, Ls[t].data(), o, o, kTile, kTile);
-        sub(rows, Xs[t].data(), o, o, kTile, kTile);
-      }
-    }
-    if (!rows.empty()) launch(2, (int64_t)rows.size() / 14, push(rows));
-    if (nmax <= kTile) return;
-    std::vector<int64_t> toff;
-    int64_t acc = temp_at;
-    for (size_t t = 0; t < Ls.size(); ++t) {
-      toff.push_back(acc);
-      acc += m0v(Ls[t][1]) * m0v(Ls[t][1]);
-    }
-    temp_size = std::max(temp_size, acc);
-    for (int64_t s = kTile; s < nmax; s *= 2) {
-      std::vector<Target> g1, g2;
-      for (size_t t = 0; t < Ls.size(); ++t) {
-        std::vector<int64_t> tmp(Xs[t]);
-        tmp[0] = temp_base + 8 * toff[t];
-        for (int64_t o = 0; o < sizes[t] - s; o += 2 * s) {
-          Target a;
-          sub(a.c, tmp.data(), o + s, o, s, s);
-          sub(a.segs, Ls[t].data(), o + s, o, s, s);
-          sub(a.segs, Xs[t].data(), o, o, s, s);
-          a.mm = s;
-          a.nn = s;
-          g1.push_back(a);
-          Target b;
-          sub(b.c, Xs[t].data(), o + s, o, s, s);
-          sub(b.segs, Xs[t].data(), o + s, o + s, s, s);
-          sub(b.segs, tmp.data(), o + s, o, s, s);
-          b.mm = s;
-          b.nn = s;
-          g2.push_back(b);
-        }
-      }
-      gemm(g1, 1.0, 0.0, 0, 0);
-      gemm(g2, -1.0, 0.0, 0, 0);
-    }
-  }
-  int64_t m0v(int64_t c) const { return c < ncl ? m0[c] : fcap; }
-
-  static std::vector<int> groups(const std::vector<int64_t>& works, int cap) {
-    double total = 0;
-    for (auto w : works) total += (double)w;
-    std::vector<int> g;
-    for (auto w : works) g.push_back(std::max(1, total > 0 ? (int)(cap * (double)w / total) : 1));
-    int64_t sum = 0;
-    for (int x : g) sum += x;
-    while (sum > cap) {
-      auto it = std::max_element(g.begin(), g.end());
-      if (*it == 1) break;
-      --*it;
-      --sum;
-    }
-    return g;
-  }
-
-  void emit() {
-    prog.clear();
-    launches.clear();
-    info_next = ctr_next = 0;
-    temp_size = 1;
-    for (auto& L : lv) {
-      if (!L.interiors.empty()) {
-        std::vector<int64_t> ops;
-        for (int s : L.interiors) opnd(ops, blk_ptr(s, s), s, s);
-        launch(1, (int64_t)L.interiors.size(), push(ops), 0, 0, info_next);
-        info_next += (int64_t)L.interiors.size();
-        std::vector<std::vector<int64_t>> Ls, Xs;
-        std::vector<int64_t> sz;
-        for (int s : L.interiors) {
-          std::vector<int64_t> l, x;
-          opnd(l, blk_ptr(s, s), s, s);
-          opnd(x, fac_base + 8 * elim_linv[s], s, s);
-          Ls.push_back(l);
-          Xs.push_back(x);
-          sz.push_back(m0[s]);
-        }
-        trtri(Ls, Xs, sz, 0);
-        // panel TRSM as a product with the explicit inverse, into temp, copied back
-        std::vector<Target> tg;
-        std::vector<int64_t> cps;
-        int64_t acc = 0;
-        for (size_t k = 0; k < L.interiors.size(); ++k) {
-          const int s = L.interiors[k];
-          for (int w : L.inbrs[k]) {
-            Target t;
-            opnd(t.c, temp_base + 8 * acc, w, s);
-            opnd(t.segs, blk_ptr(w, s), w, s);
-            opnd(t.segs, fac_base + 8 * elim_linv[s], s, s);
-            t.mm = m0[w];
-            t.nn = m0[s];
-            tg.push_back(t);
-            opnd(cps, temp_base + 8 * acc, w, s);
-            opnd(cps, blk_ptr(w, s), w, s);
-            cps.push_back(0);
-            acc += m0[w] * m0[s];
-          }
-        }
-        temp_size = std::max(temp_size, acc);
-        gemm(tg, 1.0, 0.0, 1, 0);
-        if (!cps.empty()) launch(4, (int64_t)cps.size() / 15, push(cps));
-        // grouped Schur / fill update: off-diagonal targets, then diagonal
-        // ones (lower tiles only: potrf reads the lower triangle)
-        for (int diag = 0; diag < 2; ++diag) {
-          std::vector<Target> st;
-          for (size_t t = 0; t < L.targets.size(); ++t) {
-            const int b = L.targets[t];
-            const int wa = bi[b], wb = bj[b];
-            if ((wa == wb) != (diag == 1)) continue;
-            Target x;
-            opnd(x.c, pool_base + 8 * boff[b], wa, wb);
-            for (int s : L.tsegs[t]) {
-              opnd(x.segs, blk_ptr(wa, s), wa, s);
-              opnd(x.segs, blk_ptr(wb, s), wb, s);
-            }
-            x.mm = m0[wa];
-            x.nn = m0[wb];
-            st.push_back(x);
-          }
-          gemm(st, -1.0, 1.0, 1, diag);
-        }
-      }
-      if (L.skipped) continue;
-      // rescale every active interface (factorize.py:165-173)
-      const size_t na = L.active.size();
-      std::vector<int64_t> c1, ops, c2;
-      std::vector<std::vector<int64_t>> Ls, Xs;
-      std::vector<int64_t> sz;
-      for (size_t k = 0; k < na; ++k) {
-        const int p = L.active[k];
-        opnd(c1, blk_ptr(p, p), p, p);
-        opnd(c1, fac_base + 8 * L.l_off[k], p, p);
-        c1.push_back(1);
-        opnd(ops, fac_base + 8 * L.l_off[k], p, p);
-        std::vector<int64_t> l, x;
-        opnd(l, fac_base + 8 * L.l_off[k], p, p);
-        opnd(x, fac_base + 8 * L.linv_off[k], p, p);
-        Ls.push_back(l);
-        Xs.push_back(x);
-        sz.push_back(m0[p]);
-        opnd(c2, blk_ptr(p, p), p, p);
-        opnd(c2, blk_ptr(p, p), p, p);
-        c2.push_back(2);
-      }
-      if (na) {
-        launch(4, (int64_t)na, push(c1));
-        launch(1, (int64_t)na, push(ops), 0, 0, info_next);
-        info_next += (int64_t)na;
-        trtri(Ls, Xs, sz, 0);
-        launch(4, (int64_t)na, push(c2));
-      }
-      std::unordered_map<int, int64_t> linv_of;
-      for (size_t k = 0; k < na; ++k) linv_of[L.active[k]] = L.linv_off[k];
-      if (!L.resc_blocks.empty()) {
-        std::vector<Target> g1, g2;
-        int64_t acc = 0;
-        for (int b : L.resc_blocks) {
-          const int i = bi[b], j = bj[b];
-          Target t1;
-          opnd(t1.c, temp_base + 8 * acc, i, j);
-          opnd(t1.segs, fac_base + 8 * linv_of.at(i), i, i);
-          opnd(t1.segs, pool_base + 8 * boff[b], i, j);
-          t1.mm = m0[i];
-          t1.nn = m0[j];
-          g1.push_back(t1);
-          Target t2;
-          opnd(t2.c, pool_base + 8 * boff[b], i, j);
-          opnd(t2.segs, temp_base + 8 * acc, i, j);
-          opnd(t2.segs, fac_base + 8 * linv_of.at(j), j, j);
-          t2.mm = m0[i];
-          t2.nn = m0[j];
-          g2.push_back(t2);
-          acc += m0[i] * m0[j];
-        }
-        temp_size = std::max(temp_size, acc);
-        gemm(g1, 1.0, 0.0, 0, 0);   // T = Z_i^-1 B
-        gemm(g2, 1.0, 0.0, 1, 0);   // B = T Z_j^-T
-      }
-      // sparsify, wave by wave (factorize.py:323-340)
-      for (int wv = 0; wv < L.nwaves; ++wv) {
-        std::vector<size_t> pan;
-        int64_t vm = 1;
-        for (size_t k = 0; k < na; ++k)
-          if (L.wave[k] == wv) {
-            pan.push_back(k);
-            vm = std::max(vm, m0[L.active[k]]);
-          }
-        int cap = std::max(1, spand_rrqr_capacity((int)vm));
-        if (cap_override > 0) cap = std::min(cap, cap_override);
-        for (size_t c0 = 0; c0 < pan.size(); c0 += cap) {
-          const size_t c1e = std::min(pan.size(), c0 + (size_t)cap);
-          std::vector<int64_t> works;
-          for (size_t u = c0; u < c1e; ++u) {
-            const size_t k = pan[u];
-            int64_t ncap = 0;
-            for (int w : L.anbrs[k]) ncap += m0[w];
-            works.push_back(std::max<int64_t>(1, m0[L.active[k]] * std::max<int64_t>(ncap, 1)));
-          }
-          const std::vector<int> gs = groups(works, cap);
-          std::vector<int64_t> prow, nrow;
-          int64_t need = 0, gbeg = 0, vmax = 1;
-          for (size_t u = c0; u < c1e; ++u) {
-            const size_t k = pan[u];
-            const int p = L.active[k];
-            const int g = gs[u - c0];
-            int64_t ncap = 0;
-            for (int w : L.anbrs[k]) ncap += m0[w];
-            const int64_t mc = m0[p];
-            const int64_t wsz = mc * std::max<int64_t>(ncap, 1) + mc * mc + 32 * (ncap + mc);
-            const int64_t asz = 2 * ncap + 3 * mc + 68 * (int64_t)g + 8;
-            const int64_t isz = (3 * ncap + 1) / 2 + 1;
-            const int64_t nb0 = (int64_t)nrow.size() / 4;
-            for (int w : L.anbrs[k]) {
-              if (w > p) nrow.insert(nrow.end(), {w, blk_ptr(p, w), 0, 0});
-              else nrow.insert(nrow.end(), {w, blk_ptr(w, p), 1, 0});
-            }
-            const int64_t nb1 = (int64_t)nrow.size() / 4;
-            prow.insert(prow.end(),
-                        {p, nb0, nb1, temp_base + 8 * need, fac_base + 8 * L.q_off[k],
-                         temp_base + 8 * (need + wsz), temp_base + 8 * (need + wsz + asz), gbeg,
-                         g, ctr_base + 4 * ctr_next, L.slot[k], ncap, mc, 0, 0, 0});
-            ++ctr_next;
-            need += wsz + asz + isz + 1;
-            gbeg += g;
-            vmax = std::max(vmax, mc);
-          }
-          if (nrow.empty()) nrow.assign(4, 0);
-          temp_size = std::max(temp_size, need);
-          const int64_t a = push(prow), b = push(nrow);
-          launch(5, (int64_t)(c1e - c0), a, b, 0, gbeg, vmax);
-        }
-      }
-    }
-    // final dense block (factorize.py:198-220); virtual cluster id = ncl
-    if (!fin.empty()) {
-      std::unordered_map<int, int> index;
-      for (size_t k = 0; k < fin.size(); ++k) index[fin[k]] = (int)k;
-      std::vector<int64_t> cl(fin.begin(), fin.end()), br;
-      for (int b : fin_blocks)
-        br.insert(br.end(), {index.at(bi[b]), index.at(bj[b]), pool_base + 8 * boff[b], 0});
-      if (br.empty()) br.assign(4, 0);
-      const int64_t a = push(cl), b = push(br);
-      launch(6, (int64_t)fin.size(), a, b, 0, (int64_t)fin_blocks.size(), ncl, f_off);
-      std::vector<int64_t> ops;
-      opnd(ops, fac_base + 8 * f_off, ncl, ncl);
-      launch(1, 1, push(ops), 0, 0, info_next);
-      info_next += 1;
-      std::vector<int64_t> l, x;
-      opnd(l, fac_base + 8 * f_off, ncl, ncl);
-      opnd(x, fac_base + 8 * flinv_off, ncl, ncl);
-      trtri({l}, {x}, {fcap}, 0);
-    }
-  }
-};
-
-}  // namespace
+using spand::Plan;
 
 extern "C" {
 
@@ -540,8 +51,17 @@ void* spand_plan_create(int ncl, const int64_t* m0, const int32_t* depth, int le
 
 void spand_plan_destroy(void* h) { delete static_cast<Plan*>(h); }
 
+// cluster dofs (original numbering) concatenated in id order, dptr[ncl+1]
+int spand_plan_set_dofs(void* h, const int64_t* dofs, const int64_t* dptr) {
+  Plan* p = static_cast<Plan*>(h);
+  p->dptr.assign(dptr, dptr + p->ncl + 1);
+  p->dofs.assign(dofs, dofs + p->dptr[p->ncl]);
+  return 0;
+}
+
 // out[16]: pool_size, fac_size, temp_size, n_events, n_info, n_ctr, nblocks,
-// nlevels, fcap, f_off, flinv_off, nfinal, prog_len, n_launch, meta_len, 0
+// nlevels, fcap, f_off, flinv_off, nfinal, prog_len, n_launch, meta_len,
+// temp_bound (workspace upper bound known before emission)
 int spand_plan_sizes(void* h, int64_t* out) {
   Plan* p = static_cast<Plan*>(h);
   int64_t meta = 9 + 3 * (int64_t)p->bi.size() + p->ncl + (int64_t)p->fin.size() +
@@ -554,16 +74,17 @@ int spand_plan_sizes(void* h, int64_t* out) {
   const int64_t v[16] = {p->pool_size, p->fac_size, p->temp_size, p->n_events, p->n_info,
                          p->n_events, (int64_t)p->bi.size(), (int64_t)p->lv.size(), p->fcap,
                          p->f_off, p->flinv_off, (int64_t)p->fin.size(), (int64_t)p->prog.size(),
-                         (int64_t)p->launches.size() / 16, meta, 0};
+                         (int64_t)p->launches.size() / 16, meta, p->temp_bound};
   std::memcpy(out, v, sizeof(v));
   return 0;
 }
 
-// Build the program for the given device base addresses.  Call once with
-// any bases to learn temp_size (spand_plan_sizes), then with the real ones.
+// Build the program for the given device base addresses.  A dry call only
+// sizes the temporary workspace (spand_plan_sizes); then emit for real.
 int spand_plan_emit(void* h, int64_t pool_base, int64_t fac_base, int64_t temp_base,
-                    int64_t ctr_base) {
+                    int64_t ctr_base, int dry) {
   Plan* p = static_cast<Plan*>(h);
+  p->dry = dry != 0;
   p->pool_base = pool_base;
   p->fac_base = fac_base;
   p->temp_base = temp_base;

@@ -78,12 +78,18 @@ class NativePlan:
         for nm, n in (("spand_plan_sizes", 2), ("spand_plan_program", 3),
                       ("spand_plan_meta", 2)):
             getattr(lib, nm).argtypes = [ctypes.c_void_p] * n
-        lib.spand_plan_emit.argtypes = [ctypes.c_void_p] + [ctypes.c_int64] * 4
+        lib.spand_plan_emit.argtypes = [ctypes.c_void_p] + [ctypes.c_int64] * 4 + [ctypes.c_int]
         self.h = ctypes.c_void_p(lib.spand_plan_create(
             ncl, vp(self.m0), vp(self.depth), int(h.levels), int(skip_levels),
             keys.size, vp(keys), int(cap_override)))
         self._lib = lib
         self._vp = vp
+        dcat = np.ascontiguousarray(np.concatenate(self.dofs) if self.dofs
+                                    else np.zeros(1, np.int64), dtype=np.int64)
+        dptr = np.zeros(ncl + 1, dtype=np.int64)
+        np.cumsum(self.m0, out=dptr[1:])
+        lib.spand_plan_set_dofs.argtypes = [ctypes.c_void_p] * 3
+        lib.spand_plan_set_dofs(self.h, vp(dcat), vp(dptr))
         self.sizes()
         self._decode_meta()
         self.seconds = time.perf_counter() - t0
@@ -100,10 +106,11 @@ class NativePlan:
         (self.pool_size, self.fac_size, self.temp_size, self.n_events, self.n_info,
          self.n_ctr, self.nblocks, self.nlevels, self.fcap, self.f_off,
          self.flinv_off, self.nfinal, self.prog_len, self.n_launch,
-         self.meta_len, _) = [int(x) for x in out]
+         self.meta_len, self.temp_bound) = [int(x) for x in out]
 
-    def emit(self, pool_base, fac_base, temp_base, ctr_base):
-        self._lib.spand_plan_emit(self.h, pool_base, fac_base, temp_base, ctr_base)
+    def emit(self, pool_base, fac_base, temp_base, ctr_base, dry=False):
+        self._lib.spand_plan_emit(self.h, pool_base, fac_base, temp_base, ctr_base,
+                                  int(dry))
         self.sizes()
 
     def program(self):
@@ -170,9 +177,9 @@ class Engine:
         self.info = t.zeros(max(sym.n_info, 1), dtype=t.int32, device=d)
         ctr = t.zeros(max(sym.n_ctr, 1), dtype=t.int32, device=d)
         pb, fb = pool.data_ptr(), fac.data_ptr()
-        sym.emit(pb, fb, 0, ctr.data_ptr())          # sizing pass (temp size)
-        temp = t.empty(max(sym.temp_size, 1), dtype=t.float64, device=d)
+        temp = t.empty(max(sym.temp_bound, 1), dtype=t.float64, device=d)
         sym.emit(pb, fb, temp.data_ptr(), ctr.data_ptr())
+        assert sym.temp_size <= sym.temp_bound, (sym.temp_size, sym.temp_bound)
         prog, launches = sym.program()
         self.timings["plan_s"] = time.perf_counter() - tstart
         progd = to_dev_async(prog)
@@ -251,10 +258,12 @@ class Engine:
 
     # --------------------------------------------------------------- collect
     def collect(self):
-        t = self.t
-        sym = self.sym
-        m0 = sym.m0
+        """Operators, permutation, diagnostics and nnz from the native
+        collector (csrc/collect.cpp), payloads as lazy device views."""
+        import ctypes
         t0 = time.perf_counter()
+        sym = self.sym
+        lib = _lib.load()
         ev = self.events.cpu().numpy().reshape(-1, EVENT_ROW)
         if np.any(ev[:, 9] != 0):
             raise RuntimeError("RRQR group barrier watchdog fired (kernel bug)")
@@ -263,185 +272,135 @@ class Engine:
         bad = np.flatnonzero(iv)
         if bad.size:
             raise NotSPD(int(iv[bad[0]]) - 1)
-        off = np.zeros(sym.ncl, dtype=np.int64)
+        vp = lambda x: x.ctypes.data_as(ctypes.c_void_p)  # noqa: E731
+        lib.spand_collect_create.restype = ctypes.c_void_p
+        lib.spand_collect_create.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int]
+        lib.spand_collect_destroy.argtypes = [ctypes.c_void_p]
+        evc = np.ascontiguousarray(ev)
+        ch = ctypes.c_void_p(lib.spand_collect_create(sym.h, vp(evc),
+                                                      SCHEME_CODE[self.scheme]))
+        self.collected = Collected(lib, ch, vp)
+        col = self.collected
         pool, fac = self.pool, self.facbuf
-        ops, perm_parts, diags = [], [], []
-        views = []          # for the nonzero count: (MatView, op index)
         dofs = sym.dofs
-
-        def live(c):
-            return dofs[c][off[c]:]
-
-        def bview(i, j, r0, c0, rows, cols, trans=False):
-            b = int(sym.boff[sym.bid[(i, j)]])
-            return MatView(pool, b + r0 + c0 * m0[i], m0[i], rows, cols, trans)
-
-        def fview(at, c, size):
-            return MatView(fac, at + off[c] + off[c] * m0[c], m0[c], size, size)
-
-        scheme = self.scheme
-        # structural apply phases (see apply.py): forward per level
-        # [G-T][G-A]([D]([Q-T][E-A]) per wave); backward mirrored
-        recs = sym.level_recs
-        cnt = [2 + (0 if r["skipped"] else 1 + 2 * r["nwaves"]) for r in recs]
-        fbase = np.concatenate([[0], np.cumsum(cnt)]).astype(int)
-        bbase = [1 + int(sum(cnt[i + 1:])) for i in range(len(recs))]
-        self.n_phases = int(fbase[-1]) + 1
-
-        def phases(ri, kind, wave=0):
-            r, fb, bb = recs[ri], int(fbase[ri]), bbase[ri]
-            nw = 0 if r["skipped"] else r["nwaves"]
-            if kind == "G":
-                return ({"T": fb, "A": fb + 1},
-                        {"A": bb + (2 * nw + 1 if not r["skipped"] else 0),
-                         "T": bb + (2 * nw + 2 if not r["skipped"] else 1)})
-            if kind == "D":
-                return ({"T": fb + 2}, {"T": bb + 2 * nw})
-            back = bb + 2 * (nw - 1 - wave)
-            return ({"T": fb + 3 + 2 * wave, "A": fb + 4 + 2 * wave},
-                    {"A": back, "T": back + 1})
-
-        # apply records in the cluster-contiguous (permuted) numbering used by
-        # the fast apply plan (fastplan.py): cluster c's slots live at
-        # cstart[c] + [off[c], m0[c])
-        cstart = np.concatenate([[0], np.cumsum(m0)[:-1]]).astype(np.int64)
-        self.cstart = cstart
-        arecs = []
-        self.arecs = arecs
-
-        def pst(c):
-            return int(cstart[c] + off[c])
-
-        for ri, rec in enumerate(sym.level_recs):
-            lvl = rec["level"]
-            nint, ndofs = 0, 0
-            for s, nbrs in rec["elim"]:
-                ns = m0[s] - off[s]
-                if ns == 0:
-                    continue
-                nint += 1
-                ndofs += ns
-                wl = [w for w in nbrs if m0[w] - off[w] > 0]
-                w_dofs = (np.concatenate([live(w) for w in wl]) if wl
-                          else np.empty(0, np.int64))
-                pv, r0 = [], 0
-                for w in wl:
-                    nw = m0[w] - off[w]
-                    pv.append((bview(w, s, off[w], off[s], nw, ns), r0))
-                    r0 += nw
-                low = bview(s, s, off[s], off[s], ns, ns)
-                linv = fview(int(sym.elim_linv[s]), s, ns)
-                op = Elimination(live(s), w_dofs, low, pv, linv=linv)
-                op._phases = phases(ri, "G")
-                ops.append(op)
-                arecs.append(("G", op._phases, pst(s), int(ns), linv,
-                              [(pst(w), int(v.rows), v) for w, (v, _) in zip(wl, pv)]))
-                perm_parts.append(live(s))
-            faces = []
-            if not rec["skipped"]:
-                act = [x for x in rec["active"] if m0[x[0]] - off[x[0]] > 0]
-                for p, wv, lo, li, qo, sl, nb in act:
-                    mp = m0[p] - off[p]
-                    op = Scaling(live(p), fview(lo, p, mp), linv=fview(li, p, mp))
-                    op._phases = phases(ri, "D")
-                    ops.append(op)
-                    arecs.append(("D", op._phases, pst(p), int(mp), op.linv_view))
-                for p, wv, lo, li, qo, sl, nb in act:
-                    e = ev[sl]
-                    mp, k_stop, k_c, rf2, n_fine = (int(e[1]), int(e[3]), int(e[4]),
-                                                    int(e[5]), int(e[6]))
-                    assert mp == m0[p] - off[p], "event / host offset mismatch"
-                    old = live(p)
-                    q = MatView(fac, qo, max(mp, 1), mp, mp, rot=k_c if mp else 0)
-                    qop = Orthogonal(old, q)
-                    qop._phases = phases(ri, "Q", wv)
-                    ops.append(qop)
-                    arecs.append(("Q", qop._phases, pst(p), int(mp), q))
-                    if scheme is SchemeKind.SECOND_ORDER_FULL:
-                        ncorr = n_fine
-                    elif scheme is SchemeKind.SECOND_ORDER_SUPERFINE:
-                        ncorr = k_stop - k_c
-                    else:
-                        ncorr = 0
-                    wl = [w for w in nb if m0[w] - off[w] > 0]
-                    ntot = int(sum(m0[w] - off[w] for w in wl))
-                    if ncorr and ntot:
-                        evs, c0 = [], 0
-                        for w in wl:
-                            nw = m0[w] - off[w]
-                            if w > p:
-                                v = bview(p, w, off[p], off[w], ncorr, nw)
-                            else:
-                                v = bview(w, p, off[w], off[p], nw, ncorr, trans=True)
-                            evs.append((v, c0))
-                            c0 += nw
-                        w_dofs = np.concatenate([live(w) for w in wl])
-                        eop = ErrorCorrection(old[:ncorr], w_dofs, evs)
-                        eop._phases = qop._phases
-                        ops.append(eop)
-                        arecs.append(("E", qop._phases, pst(p), int(ncorr),
-                                      [(pst(w), int(m0[w] - off[w]), v)
-                                       for w, (v, _) in zip(wl, evs)]))
-                    if n_fine:
-                        perm_parts.append(old[:n_fine])
-                    faces.append({"cluster": int(p), "size_before": int(mp),
-                                  "size_after": int(k_c), "rank_f2": int(rf2),
-                                  "eta_stop": float(np.int64(e[7]).view(np.float64)),
-                                  "r11": float(np.int64(e[8]).view(np.float64)),
-                                  "k_stop": int(k_stop), "n_cols": int(e[2])})
-                    off[p] += n_fine
+        perm_c = np.concatenate(dofs) if dofs else np.empty(0, np.int64)
+        ops = []
+        segs = col.segs
+        for row in col.ops:
+            kind, c, li, wv, doff, size, _, lo, ld, linv, qo, rot, sb, se, lo_fac, _ = (
+                int(x) for x in row)
+            if kind == 0:
+                srows = segs[sb:se]
+                op = Elimination(
+                    dofs[c][doff:doff + size], _wd(dofs, srows),
+                    MatView(pool, lo, ld, size, size), _pv(pool, srows, 0),
+                    linv=MatView(fac, linv, ld, size, size))
+            elif kind == 1:
+                op = Scaling(dofs[c][doff:doff + size], MatView(fac, lo, ld, size, size),
+                             linv=MatView(fac, linv, ld, size, size))
+            elif kind == 2:
+                op = Orthogonal(dofs[c][doff:doff + size],
+                                MatView(fac, qo, max(ld, 1), size, size, rot=rot))
+            elif kind == 3:
+                srows = segs[sb:se]
+                op = ErrorCorrection(dofs[c][doff:doff + size], _wd(dofs, srows),
+                                     _pv(pool, srows, 1))
+            else:
+                op = Elimination(perm_c[col.fidx], np.empty(0, np.int64),
+                                 MatView(fac, lo, ld, size, size), [],
+                                 linv=MatView(fac, linv, ld, size, size))
+            ops.append(op)
+        # diagnostics (factorize.py:331-356) + margins of every decision
+        diags = []
+        by_level = {}
+        for d in col.diag:
+            li, p, mp, kc, rf2, eb, rb, ks, nc, _ = (int(x) for x in d)
+            by_level.setdefault(li, []).append({
+                "cluster": p, "size_before": mp, "size_after": kc, "rank_f2": rf2,
+                "eta_stop": float(np.int64(eb).view(np.float64)),
+                "r11": float(np.int64(rb).view(np.float64)), "k_stop": ks,
+                "n_cols": nc})
+        for li, (lvl, nint, ndofs, skipped) in enumerate(col.lsum.tolist()):
+            faces = by_level.get(li, [])
             digest = hashlib.sha256(repr([(f["cluster"], f["size_before"],
                                            f["size_after"], f["rank_f2"])
                                           for f in faces]).encode()).hexdigest()
-            diags.append({"level": int(lvl), "interior_clusters": nint,
-                          "interior_dofs": int(ndofs), "skipped": bool(rec["skipped"]),
+            diags.append({"level": lvl, "interior_clusters": nint,
+                          "interior_dofs": ndofs, "skipped": bool(skipped),
                           "interfaces": [{k: f[k] for k in ("cluster", "size_before",
                                                             "size_after", "rank_f2")}
                                          for f in faces],
-                          "margins": faces,
-                          "digest": digest})
-        fin = [c for c in sym.final if m0[c] - off[c] > 0]
-        total = int(sum(m0[c] - off[c] for c in fin))
-        if total:
-            foff = sym.fcap - total
-            low = MatView(fac, sym.f_off + foff + foff * sym.fcap, sym.fcap, total, total)
-            linv = MatView(fac, sym.flinv_off + foff + foff * sym.fcap, sym.fcap,
-                           total, total)
-            fd = np.concatenate([live(c) for c in fin])
-            fop = Elimination(fd, np.empty(0, np.int64), low, [], linv=linv)
-            fop._phases = ({"T": self.n_phases - 1, "A": self.n_phases - 1},
-                           {"T": 0, "A": 0})
-            ops.append(fop)
-            fidx = np.concatenate([np.arange(pst(c), cstart[c] + m0[c]) for c in fin])
-            arecs.append(("F", fop._phases, fidx, total, linv))
-            perm_parts.append(fd)
-        perm = (np.concatenate(perm_parts) if perm_parts else np.empty(0, np.int64))
-        nnz = self._count(ops)
+                          "margins": faces, "digest": digest})
+        nnz = self._count(col.views)
         self.timings["collect_s"] = time.perf_counter() - t0
-        return ops, perm, {"levels": diags, "final_block": total}, nnz
+        return ops, col.perm, {"levels": diags, "final_block": col.final_total}, nnz
 
-    def _count(self, ops):
+    def _count(self, views):
+        """nnz_factor: nonzeros of every payload window, counted on the device."""
         t = self.t
-        rows = []
-        for op in ops:
-            vs = []
-            if isinstance(op, Elimination):
-                vs = [op._lower] + [v for v, _ in op.panel_views]
-            elif isinstance(op, Scaling):
-                vs = [op._lower]
-            elif isinstance(op, Orthogonal):
-                vs = [op.q_view]
-            else:
-                vs = [v for v, _ in op.e_views]
-            for v in vs:
-                if v.rows and v.cols:
-                    rows.append([v.addr, v.ld, v.rows, v.cols])
-        if not rows:
+        if views.shape[0] == 0:
             return 0
-        vd = to_dev(np.asarray(rows, dtype=np.int64))
-        out = t.zeros(len(rows), dtype=t.int64, device=dev())
-        _lib.call("spand_count_nonzero", len(rows), ptr(vd), ptr(out), stream())
+        flag = np.int64(1) << np.int64(62)
+        in_fac = (views[:, 0] & flag) != 0
+        offs = views[:, 0] & (flag - 1)
+        addr = np.where(in_fac, self.facbuf.data_ptr() + 8 * offs,
+                        self.pool.data_ptr() + 8 * offs)
+        rows = np.stack([addr, views[:, 1], views[:, 2], views[:, 3]], axis=1)
+        keep = (rows[:, 2] > 0) & (rows[:, 3] > 0)
+        rows = np.ascontiguousarray(rows[keep])
+        if rows.shape[0] == 0:
+            return 0
+        vd = to_dev(rows)
+        out = t.zeros(rows.shape[0], dtype=t.int64, device=dev())
+        _lib.call("spand_count_nonzero", rows.shape[0], ptr(vd), ptr(out), stream())
         return int(out.sum().item())
+
+
+def _wd(dofs, srows):
+    """Lazy w_dofs: the neighbours' live dofs at the operator's time."""
+    def build():
+        if len(srows) == 0:
+            return np.empty(0, np.int64)
+        return np.concatenate([dofs[int(w)][int(wo):int(wo) + int(lw)]
+                               for w, wo, lw in srows[:, :3]])
+    return build
+
+
+def _pv(pool, srows, axis):
+    """Lazy payload views of a segment table: (MatView, offset) pairs stacked
+    along rows (panels, axis 0) or columns (corrections, axis 1)."""
+    def build():
+        out, acc = [], 0
+        for w, wo, lw, a, ld, r, c, tr in srows.tolist():
+            out.append((MatView(pool, a, ld, r, c, bool(tr)), acc))
+            acc += lw
+        return out
+    return build
+
+
+class Collected:
+    """Arrays of the native collector plus its handle (kept for the apply)."""
+
+    def __init__(self, lib, h, vp):
+        self.lib, self.h, self.vp = lib, h, vp
+        sz = np.zeros(8, dtype=np.int64)
+        lib.spand_collect_sizes(h, vp(sz))
+        nops, nsegs, nperm, ndiag, nlsum, nviews, self.final_total, _ = (int(x) for x in sz)
+        self.ops = np.zeros((nops, 16), dtype=np.int64)
+        self.segs = np.zeros((nsegs, 8), dtype=np.int64)
+        self.perm = np.zeros(nperm, dtype=np.int64)
+        self.diag = np.zeros((ndiag, 10), dtype=np.int64)
+        self.lsum = np.zeros((nlsum, 4), dtype=np.int64)
+        self.views = np.zeros((nviews, 4), dtype=np.int64)
+        self.fidx = np.zeros(self.final_total, dtype=np.int64)
+        lib.spand_collect_get(h, vp(self.ops), vp(self.segs), vp(self.perm), vp(self.diag),
+                              vp(self.lsum), vp(self.views), vp(self.fidx))
+
+    def __del__(self):
+        try:
+            self.lib.spand_collect_destroy(self.h)
+        except Exception:
+            pass
 
 
 def ctypes_ptr(addr):
@@ -461,11 +420,11 @@ def run_factorization(a, h, eps, scheme, skip_levels, collect_local_errors=False
                       diagnostics=diag,
                       _keep=(eng.pool, eng.facbuf, eng.geo), timings=eng.timings)
     perm_c = np.concatenate(eng.sym.dofs) if eng.sym.dofs else np.empty(0, np.int64)
-    arecs, nph = eng.arecs, eng.n_phases
+    col, pool, fac = eng.collected, eng.pool, eng.facbuf
 
     def factory():
-        from .fastplan import FastPlan
-        return FastPlan(a.n, perm_c, arecs, nph)
+        from .fastplan import NativeApplyPlan
+        return NativeApplyPlan(a.n, perm_c, col, pool, fac)
 
     f._plan_factory = factory
     return f

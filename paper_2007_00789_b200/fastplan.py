@@ -123,7 +123,7 @@ class FastPlan:
             keep = nout > 0
             tk, nout, nk = tk[keep], nout[keep], nk[keep]
             outs = [o for o, k in zip(ph.outs, keep) if k]
-            modes = np.asarray(ph.modes, dtype=np.int8)[keep]
+            modes = np.asarray(ph.modes, dtype=np.int64)[keep]
             if tk.shape[0] == 0:
                 continue
             nkt = np.maximum(1, -(-nk // TILE_K))
@@ -166,7 +166,7 @@ class FastPlan:
             st = np.flatnonzero(first)
             ptrs = np.r_[st, dst.size].astype(np.int64)
             out.append((to_dev_async(tk), to_dev_async(tiles), tiles.shape[0],
-                        to_dev_async(dst[st].astype(np.int32)), to_dev_async(mode[st]),
+                        to_dev_async(dst[st].astype(np.int64)), to_dev_async(mode[st]),
                         to_dev_async(ptrs), to_dev_async(src), int(st.size), tot))
         return out
 
@@ -224,3 +224,48 @@ class FastPlan:
             self._run1(cols[j], forward, backward)
         xd.copy_(cols.t())
         return xd
+
+
+class NativeApplyPlan(FastPlan):
+    """The same structured apply, with the task / tile / scatter image built
+    by the native collector (csrc/collect.cpp) instead of NumPy."""
+
+    def __init__(self, n, perm_new_to_old, collected, pool, fac):
+        import ctypes
+        t = require_cuda()
+        self.n = int(n)
+        self.perm = to_dev(np.asarray(perm_new_to_old, dtype=np.int32), np.int32)
+        self.xbuf = t.zeros(max(self.n, 1), dtype=t.float64, device=dev())
+        self._fidx = to_dev(np.asarray(collected.fidx if collected.fidx.size else [0],
+                                       dtype=np.int32), np.int32)
+        lib, vp = collected.lib, collected.vp
+        out = np.zeros(4, dtype=np.int64)
+        lib.spand_collect_apply.argtypes = [ctypes.c_void_p] + [ctypes.c_int64] * 4 + \
+            [ctypes.c_void_p]
+        lib.spand_collect_apply(collected.h, pool.data_ptr(), fac.data_ptr(),
+                                self.xbuf.data_ptr(), self._fidx.data_ptr(), vp(out))
+        ilen, nfw, nbw, self.scratch_len = (int(x) for x in out)
+        image = np.zeros(max(ilen, 1), dtype=np.int64)
+        ph = np.zeros((nfw + nbw, 10), dtype=np.int64)
+        lib.spand_collect_apply_get.argtypes = [ctypes.c_void_p] * 3
+        lib.spand_collect_apply_get(collected.h, vp(image), vp(ph))
+        self.image = to_dev_async(image)
+        base = self.image.data_ptr()
+        self.scratch = t.empty(max(self.scratch_len, 1), dtype=t.float64, device=dev())
+        rows = []
+        for r in ph.tolist():
+            to, nt, tio, ntile, do, nout, mo, po, so, _ = r
+            rows.append((ctypes.c_void_p(base + 8 * to), ctypes.c_void_p(base + 8 * tio),
+                         ntile, ctypes.c_void_p(base + 8 * do), ctypes.c_void_p(base + 8 * mo),
+                         ctypes.c_void_p(base + 8 * po), ctypes.c_void_p(base + 8 * so), nout))
+        self.fwd, self.bwd = rows[:nfw], rows[nfw:]
+        self._graph = None
+
+    def _run_pass(self, phases):
+        st = stream()
+        x = self.xbuf
+        for tasks, tiles, ntile, dst, mode, ptrs, src, nout in phases:
+            _lib.call("spand_gemv_tiles", ntile, tiles, tasks, ptr(x), self.n,
+                      ptr(self.scratch), self.scratch_len, 1, st)
+            _lib.call("spand_apply_scatter", nout, dst, mode, ptrs, src, ptr(x), self.n,
+                      ptr(self.scratch), self.scratch_len, 1, st)

@@ -126,13 +126,13 @@ def _tile_grid(mm, nn, lower_only=False):
     cnt = tm * tn
     tot = int(cnt.sum())
     if tot == 0:
-        return np.zeros((0, 3), dtype=np.int64)
+        return np.zeros(0, dtype=np.int64)
     tgt = np.repeat(np.arange(mm.size, dtype=np.int64), cnt)
     local = np.arange(tot, dtype=np.int64) - np.repeat(np.cumsum(cnt) - cnt, cnt)
     ntile_n = np.repeat(tn, cnt)
     i0 = (local // ntile_n) * TILE
     j0 = (local % ntile_n) * TILE
-    out = np.stack([tgt, i0, j0], axis=1)
+    out = (tgt << 32) | ((i0 // TILE) << 16) | (j0 // TILE)
     if lower_only:
         out = out[j0 <= i0]
     return out
@@ -160,7 +160,7 @@ def gemm_grouped(geo, targets, alpha, beta, bT, lower_only=False,
         return
     if not srow:
         srow.append([0] * 14)
-    td, sd, tl = _rows(trow, 8), _rows(srow, 14), _rows(tiles, 3)
+    td, sd, tl = _rows(trow, 8), _rows(srow, 14), _rows(tiles, 1)
     _lib.call("spand_gemm_grouped", int(tiles.shape[0]), ptr(tl), ptr(td), ptr(sd),
               ptr(geo.m0), ptr(geo.off), float(alpha), float(beta), int(bT),
               int(bool(lower_only)), stream())

@@ -117,11 +117,17 @@ class Elimination(BlockOperator):
 
     def __init__(self, dofs, w_dofs, lower, panel, linv=None):
         self.dofs = np.asarray(dofs, dtype=np.int64)
-        self.w_dofs = np.asarray(w_dofs, dtype=np.int64)
+        self._w_dofs = w_dofs if callable(w_dofs) else np.asarray(w_dofs, dtype=np.int64)
         self._lower = lower
-        self._panel = panel if isinstance(panel, list) else None
-        self._panel_host = None if isinstance(panel, list) else panel
+        self._panel = panel if (isinstance(panel, list) or callable(panel)) else None
+        self._panel_host = None if self._panel is not None else panel
         self.linv_view = linv
+
+    @property
+    def w_dofs(self):
+        if callable(self._w_dofs):
+            self._w_dofs = np.asarray(self._w_dofs(), dtype=np.int64)
+        return self._w_dofs
 
     @property
     def lower(self):
@@ -131,14 +137,17 @@ class Elimination(BlockOperator):
     def panel(self):
         if self._panel_host is None:
             ns = self.dofs.size
-            if not self._panel:
+            views = self.panel_views
+            if not views:
                 self._panel_host = np.zeros((self.w_dofs.size, ns))
             else:
-                self._panel_host = np.vstack([v.host() for v, _ in self._panel])
+                self._panel_host = np.vstack([v.host() for v, _ in views])
         return self._panel_host
 
     @property
     def panel_views(self):
+        if callable(self._panel):
+            self._panel = self._panel()
         return self._panel
 
     @property
@@ -146,7 +155,7 @@ class Elimination(BlockOperator):
         low = (self._lower.count_nonzero() if isinstance(self._lower, MatView)
                else int(np.count_nonzero(self._lower)))
         if self._panel is not None:
-            pan = sum(v.count_nonzero() for v, _ in self._panel)
+            pan = sum(v.count_nonzero() for v, _ in self.panel_views)
         else:
             pan = int(np.count_nonzero(self._panel_host))
         return int(low + pan)
@@ -208,22 +217,30 @@ class ErrorCorrection(BlockOperator):
 
     def __init__(self, dofs, w_dofs, e_tilde):
         self.dofs = np.asarray(dofs, dtype=np.int64)
-        self.w_dofs = np.asarray(w_dofs, dtype=np.int64)
-        self._e = e_tilde if isinstance(e_tilde, list) else None
-        self._e_host = None if isinstance(e_tilde, list) else e_tilde
+        self._w_dofs = w_dofs if callable(w_dofs) else np.asarray(w_dofs, dtype=np.int64)
+        self._e = e_tilde if (isinstance(e_tilde, list) or callable(e_tilde)) else None
+        self._e_host = None if self._e is not None else e_tilde
+
+    @property
+    def w_dofs(self):
+        if callable(self._w_dofs):
+            self._w_dofs = np.asarray(self._w_dofs(), dtype=np.int64)
+        return self._w_dofs
 
     @property
     def e_tilde(self):
         if self._e_host is None:
-            self._e_host = np.hstack([v.host() for v, _ in self._e])
+            self._e_host = np.hstack([v.host() for v, _ in self.e_views])
         return self._e_host
 
     @property
     def e_views(self):
+        if callable(self._e):
+            self._e = self._e()
         return self._e
 
     @property
     def nnz(self):
         if self._e is not None:
-            return int(sum(v.count_nonzero() for v, _ in self._e))
+            return int(sum(v.count_nonzero() for v, _ in self.e_views))
         return int(np.count_nonzero(self._e_host))
