@@ -232,7 +232,9 @@ class NativeApplyPlan(FastPlan):
 
     def __init__(self, n, perm_new_to_old, collected, pool, fac):
         import ctypes
+        import time
         t = require_cuda()
+        tm = [time.perf_counter()]
         self.n = int(n)
         self.perm = to_dev(np.asarray(perm_new_to_old, dtype=np.int32), np.int32)
         self.xbuf = t.zeros(max(self.n, 1), dtype=t.float64, device=dev())
@@ -244,11 +246,13 @@ class NativeApplyPlan(FastPlan):
             [ctypes.c_void_p]
         lib.spand_collect_apply(collected.h, pool.data_ptr(), fac.data_ptr(),
                                 self.xbuf.data_ptr(), self._fidx.data_ptr(), vp(out))
+        tm.append(time.perf_counter())
         ilen, nfw, nbw, self.scratch_len = (int(x) for x in out)
         image = np.zeros(max(ilen, 1), dtype=np.int64)
         ph = np.zeros((nfw + nbw, 10), dtype=np.int64)
         lib.spand_collect_apply_get.argtypes = [ctypes.c_void_p] * 3
         lib.spand_collect_apply_get(collected.h, vp(image), vp(ph))
+        tm.append(time.perf_counter())
         self.image = to_dev_async(image)
         base = self.image.data_ptr()
         self.scratch = t.empty(max(self.scratch_len, 1), dtype=t.float64, device=dev())
@@ -260,6 +264,9 @@ class NativeApplyPlan(FastPlan):
                          ctypes.c_void_p(base + 8 * po), ctypes.c_void_p(base + 8 * so), nout))
         self.fwd, self.bwd = rows[:nfw], rows[nfw:]
         self._graph = None
+        tm.append(time.perf_counter())
+        self.build_times = {"setup_s": tm[1] - tm[0], "image_s": tm[2] - tm[1],
+                            "upload_s": tm[3] - tm[2], "image_mb": image.nbytes / 1e6}
 
     def _run_pass(self, phases):
         st = stream()

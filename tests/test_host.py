@@ -1,0 +1,224 @@
+"""Host-side logic on the CPU (no GPU needed).
+
+- the C-ABI library loads and exports every symbol include/spand_b200.h
+  declares (no compute calls);
+- the native nested dissection (csrc/partition.cpp, reference
+  partition.py:135-268) reproduces the reference's cluster lists bit for
+  bit on every golden fixture, C4-L15 included;
+- the native level scheduler (csrc/planner.cpp, reference factorize.py:285-366)
+  produces the reference's operator order: per level the G ops of the
+  interiors, then (outside skip_levels) one D per active interface and one Q
+  per interface, compared with the golden op-kind strings (E ops depend on
+  the ranks and are stripped);
+- argument validation and SPDF parse errors raise the reference's errors
+  before any device work (factorize.py:299-304, :408-467).
+"""
+
+import ctypes
+import hashlib
+import io
+import os
+import re
+import struct
+
+import numpy as np
+import pytest
+
+import paper_2007_00789_b200 as sp
+from paper_2007_00789_b200 import _lib
+from paper_2007_00789_b200.errors import DimensionMismatch, ParseError
+from tests.golden_cases import config_tags, load, matrix_for, small_tags
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "spand_b200.h")
+
+
+def _declared():
+    text = open(HEADER).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(spand_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_library_exports_every_header_symbol():
+    lib = _lib.load()
+    names = _declared()
+    assert len(names) >= 30
+    missing = [nm for nm in names if not hasattr(lib, nm)]
+    assert not missing, missing
+    assert lib.spand_version() > 0
+
+
+def test_header_symbols_are_typed_or_handle_based():
+    """Every declared entry point is either in the ctypes signature table or
+    bound with explicit argtypes where it is used (handle-returning ones)."""
+    handle_based = {"spand_plan_create", "spand_plan_destroy", "spand_plan_set_dofs",
+                    "spand_collect_create", "spand_collect_destroy", "spand_collect_sizes",
+                    "spand_collect_get", "spand_collect_apply", "spand_collect_apply_get"}
+    for nm in _declared():
+        assert nm in _lib.SIGNATURES or nm in handle_based, nm
+
+
+def _sha(arr):
+    arr = np.ascontiguousarray(arr)
+    h = hashlib.sha256()
+    h.update(str(arr.dtype).encode())
+    h.update(str(arr.shape).encode())
+    h.update(arr.tobytes())
+    return h.hexdigest()
+
+
+@pytest.mark.parametrize("tag", small_tags() + config_tags())
+def test_native_hierarchy_matches_reference(tag):
+    rec, _ = load(tag)
+    a = matrix_for(tag)
+    assert (a.n, a.nnz) == (rec["n"], rec["nnz_a"])
+    h = sp.build_hierarchy(a, rec["levels"])
+    sizes = np.array([c.dofs.size for c in h.clusters], dtype=np.int64)
+    depth = np.array([c.depth for c in h.clusters], dtype=np.int64)
+    dofs = np.concatenate([c.dofs for c in h.clusters]).astype(np.int64)
+    assert [c.id for c in h.clusters] == list(range(len(h.clusters)))
+    assert _sha(sizes) == rec["hierarchy"]["sizes_sha"]
+    assert _sha(depth) == rec["hierarchy"]["depth_sha"]
+    assert _sha(dofs) == rec["hierarchy"]["dofs_sha"]
+
+
+def _plan(tag):
+    from paper_2007_00789_b200.engine import NativePlan
+    rec, _ = load(tag)
+    a = matrix_for(tag)
+    h = sp.build_hierarchy(a, rec["levels"])
+    # capacity override: the RRQR group size query needs a device
+    return rec, NativePlan(a, h, rec["skip_levels"], cap_override=148 * 4)
+
+
+@pytest.mark.parametrize("tag", small_tags() + config_tags())
+def test_scheduler_operator_order(tag):
+    rec, plan = _plan(tag)
+    kinds = []
+    for lv in plan.level_recs:
+        kinds += ["G"] * len(lv["elim"])
+        if not lv["skipped"]:
+            kinds += ["D"] * len(lv["active"])
+            kinds += ["Q"] * len(lv["active"])
+    # the leftover dense block (factorize.py:358-362) exists iff some
+    # coarse dofs survive, which depends on the ranks
+    if plan.nfinal and rec["final_block"] > 0:
+        kinds.append("G")
+    want = rec["op_kinds"].replace("E", "")
+    assert "".join(kinds) == want
+
+
+@pytest.mark.parametrize("tag", ["lap2d_d32_L5_e0.01_k1_second-full",
+                                 "C2_L10_e0.01_second-full"])
+def test_scheduler_program_is_self_consistent(tag):
+    """Dry emission sizes the workspace within the a-priori bound; the real
+    emission (fake base addresses, nothing launched) produces a launch list
+    whose record offsets stay inside the program."""
+    _, plan = _plan(tag)
+    bound = plan.temp_bound
+    plan.emit(1 << 40, 2 << 40, 3 << 40, 4 << 40, dry=True)
+    assert 0 < plan.temp_size <= bound
+    plan.emit(1 << 40, 2 << 40, 3 << 40, 4 << 40, dry=False)
+    prog, lau = plan.program()
+    assert lau.shape[0] == plan.n_launch > 0
+    assert set(np.unique(lau[:, 0])) <= {1, 2, 3, 4, 5, 6}
+    for rec in lau:
+        for off in rec[2:5]:
+            assert 0 <= off <= prog.size
+    # every level contributes at least one potrf launch (its interiors)
+    assert int((lau[:, 0] == 1).sum()) >= sum(1 for lv in plan.level_recs if lv["elim"])
+
+
+def test_wave_numbers_respect_id_order():
+    """Sparsification waves: an interface's wave exceeds that of every
+    smaller-id active neighbour (ascending-id semantics, factorize.py:209-220)."""
+    _, plan = _plan("C2_L10_e0.01_second-full")
+    for lv in plan.level_recs:
+        if lv["skipped"]:
+            continue
+        wave = {p: wv for p, wv, *_ in lv["active"]}
+        for p, wv, *_, nbrs in lv["active"]:
+            for w in nbrs:
+                if w in wave and w < p:
+                    assert wave[w] < wv
+
+
+def test_default_levels():
+    assert sp.default_levels(16384) == 9
+    assert sp.default_levels(25) == 1
+    with pytest.raises(ValueError):
+        sp.default_levels(1)
+
+
+def test_factorize_argument_errors():
+    a = sp.laplacian_2d(8)
+    h = sp.build_hierarchy(a, 3)
+    with pytest.raises(ValueError):
+        sp.factorize(a, h, -0.1, "first")
+    with pytest.raises(ValueError):
+        sp.factorize(a, h, 1.5, "first")
+    with pytest.raises(ValueError):
+        sp.factorize(a, h, 0.1, "first", skip_levels=-1)
+    with pytest.raises(ValueError):
+        sp.factorize(a, h, 0.1, "third-order")
+    h2 = sp.build_hierarchy(sp.laplacian_2d(9), 3)
+    with pytest.raises(DimensionMismatch):
+        sp.factorize(a, h2, 0.1, "first")
+
+
+def _spdf_header(version=1, scheme=1, nops=0):
+    return b"SPDF" + struct.pack("<HqdBHIq", version, 4, 0.1, scheme, 4, nops, 0)
+
+
+@pytest.mark.parametrize("blob,msg", [
+    (b"XXXX", "magic"),
+    (_spdf_header(version=2), "version"),
+    (_spdf_header(scheme=9), "scheme"),
+    (_spdf_header()[:-3], "truncated"),
+])
+def test_load_factor_parse_errors(tmp_path, blob, msg):
+    p = tmp_path / "bad.spdf"
+    p.write_bytes(blob)
+    with pytest.raises(ParseError, match=msg):
+        sp.load_factor(str(p))
+
+
+def test_load_factor_unknown_tag(tmp_path):
+    buf = io.BytesIO()
+    buf.write(_spdf_header(nops=1))
+    perm = np.arange(4, dtype=np.int64)
+    buf.write(struct.pack("<B", 1) + struct.pack("<q", 4) + perm.tobytes())
+    buf.write(struct.pack("<B", 7))
+    p = tmp_path / "tag.spdf"
+    p.write_bytes(buf.getvalue())
+    with pytest.raises(ParseError, match="tag"):
+        sp.load_factor(str(p))
+
+
+def test_matrix_market_round_trip(tmp_path):
+    a = sp.laplacian_2d(6)
+    p = tmp_path / "a.mtx"
+    sp.write_matrix_market(str(p), a)
+    b = sp.read_matrix_market(str(p))
+    assert b.n == a.n
+    assert np.array_equal(b.row_ptr, a.row_ptr)
+    assert np.array_equal(b.col_idx, a.col_idx)
+    assert np.array_equal(b.values, a.values)
+
+
+def test_jacobi_prescale_unit_diagonal():
+    r = np.random.default_rng(5)
+    a = sp.diffusion_fv(sp.log_uniform_block_field((8, 8), 4, 3.0, r))
+    b = r.standard_normal(a.n)
+    s, bs = sp.jacobi_prescale(a, b)[:2]
+    assert np.allclose(s.diagonal(), 1.0, rtol=0, atol=1e-15)
+
+
+def test_nd_partition_rejects_bad_input():
+    """The C-ABI partitioner returns -1 for a negative size (no crash)."""
+    lib = _lib.load()
+    z = np.zeros(4, dtype=np.int64)
+    d = np.zeros(4, dtype=np.int32)
+    vp = lambda x: x.ctypes.data_as(ctypes.c_void_p)  # noqa: E731
+    rc = lib.spand_nd_partition(ctypes.c_int64(-1), vp(z), vp(z), 3, vp(z), vp(z), vp(d), vp(z))
+    assert rc == -1
