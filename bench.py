@@ -135,6 +135,22 @@ class Clocks:
                 "reasons": sorted(reasons), "samples": len(self.samples)}
 
 
+def reduce_max(v, dist, device):
+    """Max of a per-rank scalar over all ranks (the step time of the job)."""
+    if dist is None:
+        return v
+    import torch
+    tv = torch.tensor([v], dtype=torch.float64, device=device)
+    dist.all_reduce(tv, op=dist.ReduceOp.MAX)
+    return float(tv.item())
+
+
+def whole_job_rate(work_per_rank, world, ms_step):
+    """Replicas: every rank does the same work; the job's rate is the work of
+    all ranks over the slowest rank's step time."""
+    return world * work_per_rank / (ms_step / 1000.0)
+
+
 def problem(args):
     import paper_2007_00789_b200 as sp
     a, b, lv = sp.baseline_problem(args.config)
@@ -261,11 +277,7 @@ def main():
         torch.cuda.synchronize()
 
     def max_over_ranks(v):
-        if dist is None:
-            return v
-        tv = torch.tensor([v], dtype=torch.float64, device="cuda")
-        dist.all_reduce(tv, op=dist.ReduceOp.MAX)
-        return float(tv.item())
+        return reduce_max(v, dist, "cuda")
 
     for _ in range(args.warmup):
         step_resident()
@@ -343,7 +355,7 @@ def main():
     n_apply = (rep.n_cg + 1) * args.steps
     apply_gbs = counts["B_apply"] * n_apply / (apply_ms / 1000.0) / 1e9 if apply_ms else None
     line = {
-        "metric": METRIC, "value": world * f_step / (ms_step / 1000.0) / 1e9,
+        "metric": METRIC, "value": whole_job_rate(f_step, world, ms_step) / 1e9,
         "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
@@ -358,8 +370,8 @@ def main():
         "apply_gbs": apply_gbs,
         "kernels_ms_per_step": {k: round(v["ms"] / args.steps, 3) for k, v in kern.items()},
         "flops_per_step": ff | {"F_step": f_step},
-        "dof_per_s": world * a.n / (ms_step / 1000.0),
-        "e2e": {"value": world * f_step / (e2e_step / 1000.0) / 1e9, "unit": "GFLOP/s",
+        "dof_per_s": whole_job_rate(a.n, world, ms_step),
+        "e2e": {"value": whole_job_rate(f_step, world, e2e_step) / 1e9, "unit": "GFLOP/s",
                 "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                 "ms_per_step": e2e_step},
         "roofline": roof, "gpu_launches": int(launches),

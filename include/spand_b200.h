@@ -97,6 +97,15 @@ int spand_apply_scatter(int nout, const int64_t* dst, const int64_t* mode,
                         const int64_t* ptr, const int64_t* src, double* x,
                         int64_t ldx, const double* scratch, int64_t ldscr,
                         int nvec, void* stream);
+/* Run-structured variant used by the structured (engine-built) plans: the
+ * outputs of a phase are contiguous destination runs (whole live cluster
+ * ranges in the cluster-contiguous numbering), so one row describes up to
+ * 256 outputs.  chunk row (8 x int64): {dst, len <= 256, mode, cb, ce, eoff,
+ * idx, 0}: for i < len, x[d] (d = dst + i, or ((int32*)idx)[eoff + i] when idx
+ * != 0) = or -= sum_{c in [cb, ce)} scratch[contrib[c] + eoff + i], in order. */
+int spand_apply_runs(int nchunk, const int64_t* chunks, const int64_t* contrib, double* x,
+                     int64_t ldx, const double* scratch, int64_t ldscr, int nvec,
+                     void* stream);
 
 /* ---- factorization kernels (replace dense.py:45-183 and the BLAS calls of
  *      schemes.py:199-236, factorize.py:131-220) ---------------------------- */

@@ -117,9 +117,43 @@ scatter_kernel(int nout, const int64_t* __restrict__ dst, const int64_t* __restr
     else *xd -= s;
   }
 }
+
+// Run-structured ordered accumulation: chunk row (8 int64)
+// {dst, len, mode, cb, ce, eoff, idx, 0}; element i < len of the chunk is
+// x[d] with d = dst + i (idx == 0) or ((int32*)idx)[eoff + i]; the value is
+// sum_{c in [cb, ce)} scratch[contrib[c] + eoff + i], summed in order.
+__global__ void __launch_bounds__(kThreads)
+runs_kernel(const int64_t* __restrict__ chunks, const int64_t* __restrict__ contrib,
+            double* __restrict__ x, int64_t ldx, const double* __restrict__ scratch,
+            int64_t ldscr, int nvec) {
+  const int64_t* ch = chunks + 8 * (int64_t)blockIdx.x;
+  const int len = (int)ch[1];
+  const int i = threadIdx.x;
+  if (i >= len) return;
+  const int64_t dst = ch[0], cb = ch[3], ce = ch[4], eoff = ch[5], idx = ch[6];
+  const int md = (int)ch[2];
+  const int64_t d = idx ? (int64_t)reinterpret_cast<const int32_t*>(idx)[eoff + i] : dst + i;
+  for (int v = 0; v < nvec; ++v) {
+    double s = 0.0;
+    for (int64_t c = cb; c < ce; ++c) s += scratch[__ldg(contrib + c) + eoff + i + v * ldscr];
+    double* xd = x + d + v * ldx;
+    if (md == 0) *xd = s;
+    else *xd -= s;
+  }
+}
 }  // namespace
 
 extern "C" {
+
+int spand_apply_runs(int nchunk, const int64_t* chunks, const int64_t* contrib, double* x,
+                     int64_t ldx, const double* scratch, int64_t ldscr, int nvec, void* stream) {
+  if (nchunk < 0 || nvec < 1) return -1;
+  if (nchunk == 0) return 0;
+  runs_kernel<<<nchunk, kThreads, 0, as_stream(stream)>>>(chunks, contrib, x, ldx, scratch,
+                                                          ldscr, nvec);
+  SPAND_CHECK_LAUNCH();
+  return 0;
+}
 
 int spand_gemv_tiles(int ntiles, const int64_t* tiles, const int64_t* tasks, const double* x,
                      int64_t ldx, double* scratch, int64_t ldscr, int nvec, void* stream) {

@@ -15,6 +15,7 @@
 #include <algorithm>
 #include <cstdint>
 #include <cstring>
+#include <unordered_map>
 #include <vector>
 
 #include "planner.h"
@@ -251,18 +252,22 @@ int spand_collect_get(void* h, int64_t* ops, int64_t* segs, int64_t* perm, int64
 }
 
 // ---- structured apply plan ------------------------------------------------
-// Device image (int64): per phase {task rows (8 each), packed tile rows
-// (8 each, apply.cu layout), scatter dst[nout], mode[nout], ptr[nout+1],
-// src[nsrc]} + the final block's index list (int32 pairs packed in int64).
+// Device image (int64): per phase {task rows (8 each), tile rows (8 each,
+// apply.cu layout), run chunks (8 each, spand_apply_runs), contribution
+// bases}.  Every task writes one whole destination run (a live cluster range
+// in the cluster-contiguous numbering, or the final block's index list), so
+// the ordered accumulation is described per run, not per element: tasks that
+// hit the same run contribute their scratch blocks in task order.
 // Addresses: payload windows pool_base/fac_base (bit 62 of the window offset
 // selects the factor buffer), inputs xbuf + 8 * permuted index.
 static void compile_phase(Collected* C, const std::vector<Task>& ph, int64_t pool_base,
                           int64_t fac_base, int64_t xbuf, int64_t idx_addr) {
-  constexpr int64_t TO = 64, TK = 2048;
-  std::vector<int64_t> rows, tiles, dst, mode, src;
+  constexpr int64_t TO = 64, TK = 2048, RUN = 256;
+  std::vector<int64_t> rows, tiles, chunks, contrib;
+  struct Run { int64_t dst, len, mode; bool idx; std::vector<int64_t> parts; };
+  std::vector<Run> runs;
+  std::unordered_map<int64_t, int> run_of;   // destination start -> run
   int64_t pos = 0;
-  std::vector<std::pair<int64_t, int64_t>> ent;   // (dst, src) in task order
-  std::vector<int64_t> emode;
   for (const Task& t : ph) {
     const int64_t nout = t.trans ? t.cols : t.rows;
     const int64_t nk = t.trans ? t.rows : t.cols;
@@ -280,40 +285,36 @@ static void compile_phase(Collected* C, const std::vector<Task>& ph, int64_t poo
         const int64_t kc = std::max<int64_t>(0, std::min(TK, nk - kb * TK));
         tiles.insert(tiles.end(), {tid, ob, oc, kb * TK, kc, pos + kb * nout + ob, 0, 0});
       }
-    for (int64_t kb = 0; kb < nkt; ++kb)
-      for (int64_t o = 0; o < nout; ++o) {
-        const int64_t d = t.out_start >= 0 ? t.out_start + o : C->fidx[o];
-        ent.push_back({d, pos + kb * nout + o});
-        emode.push_back(t.mode);
-      }
+    const int64_t key = t.out_start >= 0 ? t.out_start : -1;
+    auto it = run_of.find(key);
+    int r;
+    if (it == run_of.end()) {
+      r = (int)runs.size();
+      run_of.emplace(key, r);
+      runs.push_back({t.out_start >= 0 ? t.out_start : 0, nout, t.mode, t.out_start < 0, {}});
+    } else {
+      r = it->second;
+    }
+    for (int64_t kb = 0; kb < nkt; ++kb) runs[r].parts.push_back(pos + kb * nout);
     pos += nout * nkt;
   }
   if (rows.empty()) return;
-  // stable order by destination: sequence order kept inside a destination
-  std::vector<int64_t> order(ent.size());
-  for (size_t i = 0; i < order.size(); ++i) order[i] = (int64_t)i;
-  std::stable_sort(order.begin(), order.end(),
-                   [&](int64_t a, int64_t b) { return ent[a].first < ent[b].first; });
-  std::vector<int64_t> ptr;
-  for (size_t u = 0; u < order.size(); ++u) {
-    const auto& e = ent[order[u]];
-    if (u == 0 || e.first != ent[order[u - 1]].first) {
-      dst.push_back(e.first);
-      mode.push_back(emode[order[u]]);
-      ptr.push_back((int64_t)u);
-    }
-    src.push_back(e.second);
+  for (const Run& R : runs) {
+    const int64_t cb = (int64_t)contrib.size();
+    contrib.insert(contrib.end(), R.parts.begin(), R.parts.end());
+    const int64_t ce = (int64_t)contrib.size();
+    for (int64_t e = 0; e < R.len; e += RUN)
+      chunks.insert(chunks.end(), {R.dst, std::min(RUN, R.len - e), R.mode, cb, ce, e,
+                                   R.idx ? idx_addr : 0, 0});
   }
-  ptr.push_back((int64_t)order.size());
   auto put = [&](const std::vector<int64_t>& v) {
     const int64_t at = (int64_t)C->plan.size();
     C->plan.insert(C->plan.end(), v.begin(), v.end());
     return at;
   };
-  const int64_t a = put(rows), b = put(tiles), c = put(dst), d = put(mode), e = put(ptr),
-                f = put(src);
+  const int64_t a = put(rows), b = put(tiles), c = put(chunks), d = put(contrib);
   C->phases.insert(C->phases.end(), {a, (int64_t)rows.size() / 8, b, (int64_t)tiles.size() / 8,
-                                     c, (int64_t)dst.size(), d, e, f, pos});
+                                     c, (int64_t)chunks.size() / 8, d, 0, 0, pos});
   C->scratch_len = std::max(C->scratch_len, pos);
 }
 
@@ -344,8 +345,8 @@ int spand_collect_apply(void* h, int64_t pool_base, int64_t fac_base, int64_t xb
   return 0;
 }
 
-// phase rows (10 int64): tasks_off, ntask, tiles_off, ntile, dst_off, nout,
-// mode_off, ptr_off, src_off, scratch_used
+// phase rows (10 int64): tasks_off, ntask, tiles_off, ntile, chunks_off,
+// nchunk, contrib_off, 0, 0, scratch_used
 int spand_collect_apply_get(void* h, int64_t* image, int64_t* phases) {
   Collected* C = static_cast<Collected*>(h);
   std::memcpy(image, C->plan.data(), C->plan.size() * sizeof(int64_t));

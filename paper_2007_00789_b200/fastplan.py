@@ -254,14 +254,16 @@ class NativeApplyPlan(FastPlan):
         lib.spand_collect_apply_get(collected.h, vp(image), vp(ph))
         tm.append(time.perf_counter())
         self.image = to_dev_async(image)
+        self.image_host = image
         base = self.image.data_ptr()
         self.scratch = t.empty(max(self.scratch_len, 1), dtype=t.float64, device=dev())
         rows = []
         for r in ph.tolist():
-            to, nt, tio, ntile, do, nout, mo, po, so, _ = r
+            to, nt, tio, ntile, co, nch, cbo, _, _, _ = r
             rows.append((ctypes.c_void_p(base + 8 * to), ctypes.c_void_p(base + 8 * tio),
-                         ntile, ctypes.c_void_p(base + 8 * do), ctypes.c_void_p(base + 8 * mo),
-                         ctypes.c_void_p(base + 8 * po), ctypes.c_void_p(base + 8 * so), nout))
+                         ntile, ctypes.c_void_p(base + 8 * co), nch,
+                         ctypes.c_void_p(base + 8 * cbo)))
+        self.phase_table = ph
         self.fwd, self.bwd = rows[:nfw], rows[nfw:]
         self._graph = None
         tm.append(time.perf_counter())
@@ -271,8 +273,8 @@ class NativeApplyPlan(FastPlan):
     def _run_pass(self, phases):
         st = stream()
         x = self.xbuf
-        for tasks, tiles, ntile, dst, mode, ptrs, src, nout in phases:
+        for tasks, tiles, ntile, chunks, nch, contrib in phases:
             _lib.call("spand_gemv_tiles", ntile, tiles, tasks, ptr(x), self.n,
                       ptr(self.scratch), self.scratch_len, 1, st)
-            _lib.call("spand_apply_scatter", nout, dst, mode, ptrs, src, ptr(x), self.n,
+            _lib.call("spand_apply_runs", nch, chunks, contrib, ptr(x), self.n,
                       ptr(self.scratch), self.scratch_len, 1, st)
