@@ -101,7 +101,7 @@ int spand_apply_scatter(int nout, const int64_t* dst, const int64_t* mode,
  * outputs of a phase are contiguous destination runs (whole live cluster
  * ranges in the cluster-contiguous numbering), so one row describes up to
  * 256 outputs.  chunk row (8 x int64): {dst, len <= 256, mode, cb, ce, eoff,
- * idx, 0}: for i < len, x[d] (d = dst + i, or ((int32*)idx)[eoff + i] when idx
+ * idx, 0}: for i < len, x[d] (d = dst + eoff + i, or ((int32*)idx)[eoff + i] when idx
  * != 0) = or -= sum_{c in [cb, ce)} scratch[contrib[c] + eoff + i], in order. */
 int spand_apply_runs(int nchunk, const int64_t* chunks, const int64_t* contrib, double* x,
                      int64_t ldx, const double* scratch, int64_t ldscr, int nvec,

@@ -120,7 +120,7 @@ scatter_kernel(int nout, const int64_t* __restrict__ dst, const int64_t* __restr
 
 // Run-structured ordered accumulation: chunk row (8 int64)
 // {dst, len, mode, cb, ce, eoff, idx, 0}; element i < len of the chunk is
-// x[d] with d = dst + i (idx == 0) or ((int32*)idx)[eoff + i]; the value is
+// x[d] with d = dst + eoff + i (idx == 0) or ((int32*)idx)[eoff + i]; the value is
 // sum_{c in [cb, ce)} scratch[contrib[c] + eoff + i], summed in order.
 __global__ void __launch_bounds__(kThreads)
 runs_kernel(const int64_t* __restrict__ chunks, const int64_t* __restrict__ contrib,
@@ -132,7 +132,7 @@ runs_kernel(const int64_t* __restrict__ chunks, const int64_t* __restrict__ cont
   if (i >= len) return;
   const int64_t dst = ch[0], cb = ch[3], ce = ch[4], eoff = ch[5], idx = ch[6];
   const int md = (int)ch[2];
-  const int64_t d = idx ? (int64_t)reinterpret_cast<const int32_t*>(idx)[eoff + i] : dst + i;
+  const int64_t d = idx ? (int64_t)reinterpret_cast<const int32_t*>(idx)[eoff + i] : dst + eoff + i;
   for (int v = 0; v < nvec; ++v) {
     double s = 0.0;
     for (int64_t c = cb; c < ce; ++c) s += scratch[__ldg(contrib + c) + eoff + i + v * ldscr];

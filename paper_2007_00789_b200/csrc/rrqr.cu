@@ -28,15 +28,6 @@
 #include "common.cuh"
 #include "../../include/spand_b200.h"
 
-#ifndef COLLOAD
-#define COLLOAD(p) (*(p))
-#endif
-#ifndef BLKLOAD
-#define BLKLOAD(p) (*(p))
-#endif
-#ifndef BLKSTORE
-#define BLKSTORE(p, v) (*(p) = (v))
-#endif
 
 namespace {
 constexpr int kT = 256;
@@ -54,22 +45,28 @@ constexpr int kMaxM = 6144;  // v in shared memory
 // event row (12 int64): {p, m, n, k_stop, k_c, rank_f2, n_fine,
 //  bits(eta_stop), bits(r11), 0, 0, 0}
 
-constexpr int kBB = 32;        // reflectors per delayed block update
-constexpr int kCR = kBB + 2;   // candidate record (doubles)
+constexpr int kBB = 32;        // column width of the Fb workspace region (frozen list)
+constexpr int kCR = kBB + 2;   // candidate record stride (doubles)
+constexpr int kLDS = 68;       // frozen-column DMMA tiles (conflict-free fragments)
+// dynamic shared memory floor: write-back staging (8 warps x 16 x 33) and
+// the frozen-GEMM epilogue tile (64 x 65)
+constexpr size_t kMinSmem = (size_t)kWarps * 16 * 33 * sizeof(double);
+static_assert(kMinSmem >= 64 * 65 * sizeof(double), "epilogue tile");
+static_assert(kMinSmem >= 2 * 16 * kLDS * sizeof(double), "operand tiles");
 
 struct Sh {
-  double g[kBB];
-  double vk[kBB + 1];
-  double wrow[kBB];
-  double fw[kWarps][kBB];
   double red[kWarps];
   double bval[kWarps];
   int64_t bpos[kWarps];
   int64_t bpc[kWarps];
+  double bfm[kWarps];
   int bq[kWarps];
   int bcol[kWarps];
-  double vt[32][kBB + 1];    // block-update staging: 32 rows x block reflectors
+  int nfrz;
+  unsigned long long fmax;   // bits of the max norm^2 of my frozen columns (>= 0)
   int nb_start[65];  // column start of each neighbour (first 64)
+  double* cbase[64];  // frozen GEMM epilogue: column base in the pool
+  int64_t cstride[64];
 };
 
 __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
@@ -107,6 +104,12 @@ __device__ __forceinline__ void group_barrier(unsigned* ctr, int G, unsigned& ge
 // better(a, b): larger value wins, ties -> smaller position
 __device__ __forceinline__ bool better(double va, int64_t pa, double vb, int64_t pb) {
   return va > vb || (va == vb && pa < pb);
+}
+
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
 }
 
 __global__ void __launch_bounds__(kT, 4)
@@ -151,22 +154,24 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
     if (j < 64 && tid == 0) sh.nb_start[j] = n;
     n += m0[w] - off[w];
   }
-  if (tid == 0 && nnb <= 64) sh.nb_start[nnb] = n;
+  if (tid == 0) {
+    if (nnb <= 64) sh.nb_start[nnb] = n;
+    sh.nfrz = 0;
+    sh.fmax = 0ull;
+  }
   __syncthreads();
 
   double* cur = aux;
   double* ref = aux + ncap;
   double* piv = aux + 2 * ncap;
-  // candidates, double-buffered by step parity (kCR doubles each)
   double* betas = aux + 2 * ncap + mcap;                       // mcap
   double* taus = betas + mcap;                                 // mcap
-  double* cand = taus + mcap;                                  // 2 G kCR
+  double* cand = taus + mcap;                                  // 2 G kCR, by step parity
   double* V = W + (int64_t)mcap * ncap;                        // m x kmax reflectors
-  double* Fb = V + (int64_t)mcap * mcap;                       // ncap x kBB (block F)
-  double* pf = Fb + (int64_t)ncap * kBB;                       // mcap x kBB (F rows at pivot)
+  int32_t* flist = reinterpret_cast<int32_t*>(V + (int64_t)mcap * mcap);  // frozen columns
   int32_t* perm = iaux;
   int32_t* pos = iaux + ncap;
-  int32_t* done = iaux + 2 * ncap;
+  int32_t* done = iaux + 2 * ncap;   // 0 active, 1 pivoted, 2 frozen
 
   const int c0 = (int)(((int64_t)n * rank) / G), c1 = (int)(((int64_t)n * (rank + 1)) / G);
   const int q0 = (int)(((int64_t)m * rank) / G), q1 = (int)(((int64_t)m * (rank + 1)) / G);
@@ -190,6 +195,22 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
     }
     j = jj;
     cc = c - start;
+  };
+  // element (i, c) of the ORIGINAL panel lives in the pool block until the
+  // final write-back: base + i * stride
+  auto pool_col = [&](int c, double*& base, int64_t& stride) {
+    int j, cc;
+    nbr_of(c, j, cc);
+    const int64_t* nr = nbrs + 4 * (int64_t)(nb0 + j);
+    const int w = (int)nr[0];
+    double* blk = reinterpret_cast<double*>(nr[1]);
+    if (nr[2] == 0) {
+      base = blk + (int64_t)offp + (int64_t)(off[w] + cc) * ldp;
+      stride = 1;
+    } else {
+      base = blk + (int64_t)(off[w] + cc) + (int64_t)offp * m0[w];
+      stride = m0[w];
+    }
   };
 
   // ---- gather my columns of the panel into W (ld = m), 32x32 tiles per warp
@@ -244,8 +265,8 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
       }
     }
   }
-  // candidate record: {value, (pos << 32 | col), F row of that column (jn)}
-  auto publish = [&](double v, int64_t ps, int c, int parity, int jn) {
+  // candidate record: {value, (pos << 32 | col), max norm^2 of my frozen columns}
+  auto publish = [&](double v, int64_t ps, int c, int parity) {
     if (lane == 0) {
       sh.bval[warp] = v;
       sh.bpos[warp] = ps;
@@ -262,72 +283,31 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
           pp = sh.bpos[q];
           cc = sh.bcol[q];
         }
-      sh.bcol[0] = cc;
       double* rec = cand + (int64_t)(parity * G + rank) * kCR;
       rec[0] = vv;
       reinterpret_cast<int64_t*>(rec)[1] = (pp << 32) | (int64_t)(uint32_t)cc;
-    }
-    __syncthreads();
-    const int cc = sh.bcol[0];
-    if (tid < jn && cc >= 0) cand[(int64_t)(parity * G + rank) * kCR + 2 + tid] = Fb[(int64_t)cc * kBB + tid];
-    __syncthreads();
-  };
-  // A[k0:, c] -= V[k0:, k0:k0+jn] F[c, :jn]^T on owned, non-pivoted columns,
-  // 32 rows at a time: the rows' reflector entries are staged in shared
-  // memory once per CTA; lane = row, the F row of a column lives in lane q
-  // and is broadcast with shuffles.  With `last_in_smem` the newest
-  // reflector is taken from vsh (rank 0's global copy is only guaranteed
-  // visible after the next group barrier).
-  int k = 0, k0 = 0;
-  auto block_update = [&](int jn, bool last_in_smem) {
-    const int kk = k0 + jn - 1;   // row offset of vsh when last_in_smem
-    for (int r0 = k0; r0 < m; r0 += 32) {
-      __syncthreads();
-      for (int e = tid; e < 32 * jn; e += kT) {
-        const int r = e % 32, q = e / 32, i = r0 + r;
-        double v = 0.0;
-        if (i < m && i >= k0 + q) {
-          if (last_in_smem && q == jn - 1) v = vsh[i - kk];
-          else v = __ldcg(V + (int64_t)(k0 + q) * m + i);
-        }
-        sh.vt[r][q] = v;
-      }
-      __syncthreads();
-      const int i = r0 + lane;
-      for (int c = c0 + warp; c < c1; c += kWarps) {
-        if (done[c]) continue;
-        const double fq = lane < jn ? Fb[(int64_t)c * kBB + lane] : 0.0;
-        double acc = 0.0;
-        for (int q = 0; q < jn; ++q) acc += sh.vt[lane][q] * __shfl_sync(0xffffffffu, fq, q);
-        if (i < m) BLKSTORE(W + (int64_t)c * m + i, BLKLOAD(W + (int64_t)c * m + i) - acc);
-      }
+      rec[2] = __longlong_as_double((long long)sh.fmax);
     }
     __syncthreads();
   };
-  publish(bv, bp, bc, 0, 0);
+  publish(bv, bp, bc, 0);
   group_barrier(ctr, G, gen, -1, events + 12 * slot + 9);
 
-  // ---- blocked elimination: the trailing matrix is updated only every kBB
-  // steps (A <- A - V_blk F^T, LAPACK dlaqps style); in between, each step
-  // needs one read of the owned columns (F column = tau v^T A_current) and
-  // the pivot column is rebuilt from A, V and the winner's F row.
+  // ---- elimination (unblocked Householder steps on the ACTIVE columns).
+  // A column whose running norm^2 is below a quarter of (stop_tol r11)^2 can
+  // never be a pivot again (running norms only decrease, and within the
+  // reference's 0.01 refresh rule they track the exact tail norm to ~1e-11
+  // relative): it is FROZEN -- no more per-step work -- and its final column
+  // Q^T a is produced at the end by one tensor-core product with Q.
   const double stop_tol = (scheme == 2) ? eps * eps : eps;
   double r11 = 0.0, eta_last = 0.0;
-#ifdef SPAND_RRQR_PHASES
-  long long ph_t[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  long long ph_last = clock64();
-  int ph_cur = 7;
-#define PH(x) do { long long _n = clock64(); ph_t[ph_cur] += _n - ph_last; ph_last = _n; ph_cur = (x); } while (0)
-#else
-#define PH(x) do {} while (0)
-#endif
+  double thr2 = 0.0;   // 0.25 (stop_tol r11)^2
+  int k = 0;
   while (k < kmax) {
-    PH(0);
-    const int jb = k - k0;  // reflectors of the current block before this step
     // ---- winning column: max value, smallest current position (ties in
     // both: lowest record, as a sequential scan).  Records are scanned in
     // parallel and reduced over the CTA.
-    double wv = -1.0;
+    double wv = -1.0, wf = -1.0;
     int64_t wp = 0x7fffffffffffLL, wpc = 0;
     int wq = 0x7fffffff;
     const int par = k & 1;
@@ -335,6 +315,8 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
       const double* rec = cand + (int64_t)(par * G + q) * kCR;
       const double v = __ldcg(rec);
       const int64_t pc = __ldcg(reinterpret_cast<const long long*>(rec) + 1);
+      const double fm = __ldcg(rec + 2);
+      if (fm > wf) wf = fm;
       const int64_t ps = pc >> 32;
       if (better(v, ps, wv, wp) || (v == wv && ps == wp && q < wq)) {
         wv = v;
@@ -349,6 +331,8 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
       const int64_t p2 = __shfl_xor_sync(0xffffffffu, wp, o);
       const int64_t c2 = __shfl_xor_sync(0xffffffffu, wpc, o);
       const int q2 = __shfl_xor_sync(0xffffffffu, wq, o);
+      const double f2 = __shfl_xor_sync(0xffffffffu, wf, o);
+      if (f2 > wf) wf = f2;
       if (better(v2, p2, wv, wp) || (v2 == wv && p2 == wp && q2 < wq)) {
         wv = v2;
         wp = p2;
@@ -361,16 +345,19 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
       sh.bpos[warp] = wp;
       sh.bpc[warp] = wpc;
       sh.bq[warp] = wq;
+      sh.bfm[warp] = wf;
     }
     __syncthreads();
     wv = sh.bval[0];
     wp = sh.bpos[0];
     wpc = sh.bpc[0];
     wq = sh.bq[0];
+    wf = sh.bfm[0];
     for (int w2 = 1; w2 < kWarps; ++w2) {
       const double v2 = sh.bval[w2];
       const int64_t p2 = sh.bpos[w2];
       const int q2 = sh.bq[w2];
+      if (sh.bfm[w2] > wf) wf = sh.bfm[w2];
       if (better(v2, p2, wv, wp) || (v2 == wv && p2 == wp && q2 < wq)) {
         wv = v2;
         wp = p2;
@@ -379,52 +366,44 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
       }
     }
     __syncthreads();
+    if (wv < 0.0) {
+      // every remaining column is frozen: the reference's next pivot is one
+      // of them and its eta (< stop_tol r11 / 2) stops the elimination
+      eta_last = sqrt(wf > 0.0 ? wf : 0.0);
+      break;
+    }
     const int jpos = (int)wp;
     const int j = (int)(uint32_t)(wpc & 0xffffffffLL);
-    if (tid < jb) sh.wrow[tid] = __ldcg(cand + (int64_t)(par * G + wq) * kCR + 2 + tid);
-    __syncthreads();
-    // pivot column as of this step: A[:, j] - V_blk F[j, :]^T, rows k..m-1
+    // pivot column rows k..m-1 (current: every active column is updated
+    // in place each step)
     const int len = m - k;
     const double* colj = W + (int64_t)j * m + k;
     double s = 0.0;
     for (int i = tid; i < len; i += kT) {
-      double x = __ldcg(colj + i);
-      // 8 independent reflector loads in flight per row
-      for (int q0 = 0; q0 < jb; q0 += 8) {
-        double vv[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u)
-          vv[u] = (q0 + u < jb) ? __ldcg(V + (int64_t)(k0 + q0 + u) * m + k + i) : 0.0;
-#pragma unroll
-        for (int u = 0; u < 8; ++u)
-          if (q0 + u < jb) x -= vv[u] * sh.wrow[q0 + u];
-      }
+      const double x = __ldcg(colj + i);
       vsh[i] = x;
       s += x * x;
     }
     const double eta = sqrt(block_sum<kT>(s, sh.red));
-    PH(1);
     eta_last = eta;
     if (k == 0) {
       r11 = eta;
       if (r11 == 0.0) break;
+      thr2 = 0.25 * (stop_tol * r11) * (stop_tol * r11);
     }
     if (eta < stop_tol * r11) break;
     // ---- swap bookkeeping (reference: r[:, [k, j]], perm[[k, j]] ...): the
     // column at position k moves to j's old position; owners update their
     // own columns' positions (no shared permutation array)
     const bool own_j = j >= c0 && j < c1;
-    if (own_j) {
-      if (tid == 0) {
-        pos[j] = k;
-        done[j] = 1;
-      }
-      if (tid < jb) pf[(int64_t)k * kBB + tid] = sh.wrow[tid];
+    if (own_j && tid == 0) {
+      pos[j] = k;
+      done[j] = 1;
     }
     if (rank == 0 && tid == 0) piv[k] = eta;
     __syncthreads();
     for (int c = c0 + tid; c < c1; c += kT)
-      if (c != j && !done[c] && pos[c] == k) pos[c] = jpos;
+      if (c != j && done[c] != 1 && pos[c] == k) pos[c] = jpos;
     // ---- reflector v = x - beta e1, beta = -sign(x0) eta (dense.py:155-159)
     double beta = 0.0, tau = 0.0;
     if (eta > 0.0) {
@@ -448,91 +427,77 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
         betas[k] = beta;
       }
     }
-    PH(2);
-    // g[q] = v^T v_q (rows k..), V row k of the block (and v[0] itself)
-    // (row-parallel: each thread streams its rows of 8 reflectors at once,
-    // partial sums reduced across the CTA; V is read once per CTA)
-    for (int q0 = 0; q0 < jb; q0 += 8) {
-      double acc[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) acc[u] = 0.0;
-      for (int i = tid; i < len; i += kT) {
-        const double vi = vsh[i];
-        double vv[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u)
-          vv[u] = (q0 + u < jb) ? __ldcg(V + (int64_t)(k0 + q0 + u) * m + k + i) : 0.0;
-#pragma unroll
-        for (int u = 0; u < 8; ++u) acc[u] += vi * vv[u];
-      }
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const double w = warp_sum(acc[u]);
-        if (lane == 0) sh.fw[warp][u] = w;
-      }
-      __syncthreads();
-      if (tid < 8 && q0 + tid < jb) {
-        double t = 0.0;
-        for (int q = 0; q < kWarps; ++q) t += sh.fw[q][tid];
-        sh.g[q0 + tid] = t;
-        sh.vk[q0 + tid] = __ldcg(V + (int64_t)(k0 + q0 + tid) * m + k);
-      }
-      __syncthreads();
-    }
-    if (tid == 0) sh.vk[jb] = vsh[0];
-    __syncthreads();
-    PH(3);
-    // ---- owned columns: F column, row-k entry, norm downdate / refresh
+    // ---- owned active columns: a -= tau (v.a) v, row-k entry, norm
+    // downdate with the reference's refresh rule (dense.py:160-178), freeze
     bv = -1.0;
     bp = 0x7fffffffffffLL;
     bc = -1;
     for (int c = c0 + warp; c < c1; c += kWarps) {
       if (c == j || done[c]) continue;
-      const double* col = W + (int64_t)c * m + k;
-      const double wl = lane < jb ? Fb[(int64_t)c * kBB + lane] : 0.0;
-      double d = 0.0, a0k = 0.0;
+      if (cur[c] < thr2) {
+        // freeze; the final column is recomputed from the ORIGINAL data,
+        // which stays in the pool block: restore it in W (k > 0 only)
+        if (lane == 0) {
+          done[c] = 2;
+          flist[c0 + atomicAdd(&sh.nfrz, 1)] = c;
+          atomicMax(&sh.fmax, (unsigned long long)__double_as_longlong(cur[c]));
+        }
+        if (k > 0) {
+          double* base;
+          int64_t stride;
+          pool_col(c, base, stride);
+          double* col = W + (int64_t)c * m;
+          for (int i = lane; i < m; i += 32) col[i] = base[(int64_t)i * stride];
+        }
+        __syncwarp();
+        continue;
+      }
+      double* col = W + (int64_t)c * m + k;
+      double d = 0.0;
       for (int base = 0; base < len; base += 256) {
         double x[8];
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
           const int i = base + lane + 32 * u;
-          x[u] = i < len ? COLLOAD(col + i) : 0.0;
+          x[u] = i < len ? col[i] : 0.0;
         }
-        if (base == 0) a0k = x[0];
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
           const int i = base + lane + 32 * u;
           if (i < len) d += vsh[i] * x[u];
         }
       }
-      d = warp_sum(d);
-      const double corr = warp_sum(lane < jb ? sh.g[lane] * wl : 0.0);
-      const double wj = tau * (d - corr);
-      a0k = __shfl_sync(0xffffffffu, a0k, 0);
-      const double rk = a0k - warp_sum(lane < jb ? sh.vk[lane] * wl : 0.0) - sh.vk[jb] * wj;
-      double cn = cur[c] - rk * rk;
-      if (cn < 0.0) cn = 0.0;
-      if (cn < 0.01 * ref[c]) {
-        // exact tail norm of the updated column (dense.py:172-178)
-        if (lane < jb) sh.fw[warp][lane] = wl;
-        __syncwarp();
-        double tail = 0.0;
-        for (int i = 1 + lane; i < len; i += 32) {
-          double x = col[i] - vsh[i] * wj;
-          for (int q = 0; q < jb; ++q)
-            x -= __ldcg(V + (int64_t)(k0 + q) * m + k + i) * sh.fw[warp][q];
-          tail += x * x;
+      const double wj = tau * warp_sum(d);
+      double tail = 0.0, rk = 0.0;
+      for (int base = 0; base < len; base += 256) {
+        double x[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int i = base + lane + 32 * u;
+          x[u] = i < len ? col[i] : 0.0;
         }
-        tail = warp_sum(tail);
-        cn = tail;
-        if (lane == 0) {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int i = base + lane + 32 * u;
+          if (i < len) {
+            const double y = x[u] - wj * vsh[i];
+            col[i] = y;
+            if (i == 0) rk = y;
+            else tail += y * y;
+          }
+        }
+      }
+      rk = __shfl_sync(0xffffffffu, rk, 0);
+      tail = warp_sum(tail);
+      if (lane == 0) {
+        double cn = cur[c] - rk * rk;
+        if (cn < 0.0) cn = 0.0;
+        if (cn < 0.01 * ref[c]) {
+          // exact tail norm of the updated column (dense.py:172-178)
+          cn = tail;
           ref[c] = tail;
           atomicAdd(reinterpret_cast<unsigned long long*>(events + 12 * slot + 10), 1ull);
         }
-        __syncwarp();
-      }
-      if (lane == 0) {
-        Fb[(int64_t)c * kBB + jb] = wj;
         cur[c] = cn;
         const int64_t ps = pos[c];
         if (better(cn, ps, bv, bp)) {
@@ -543,46 +508,19 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
       }
     }
     __syncthreads();
-    PH(4);
-    const int jn = jb + 1;
-    const bool block_end = (jn == kBB) || (k + 1 == kmax);
-    if (block_end) {
-      block_update(jn, true);
-      k0 = k + 1;
-    }
-    PH(5);
-    publish(bv, bp, bc, (k + 1) & 1, block_end ? 0 : jn);
+    publish(bv, bp, bc, (k + 1) & 1);
     ++k;
-    PH(6);
     group_barrier(ctr, G, gen, k, events + 12 * slot + 9);
   }
   const int k_stop = k;
-#ifdef SPAND_RRQR_PHASES
-  PH(7);
-  if (tid == 0 && (rank == 0 || rank == G / 2))
-    printf("[rrqr phases] p %d rank %d k %d kcycles: cand+pivcol %lld refl %lld g %lld colpass %lld blockend %lld publish %lld barrier %lld\n",
-           p, rank, k, ph_t[0] / 1000, ph_t[1] / 1000, ph_t[2] / 1000, ph_t[3] / 1000, ph_t[4] / 1000,
-           ph_t[5] / 1000, ph_t[6] / 1000);
-#endif
   // every CTA must be done reading this step's pivot column (the loop may
-  // have stopped on it) before owners update or patch their columns
+  // have stopped on it) before owners patch their columns
   group_barrier(ctr, G, gen, 100000 + k, events + 12 * slot + 9);
-  // pending partial block (the loop stopped before its block end)
-  if (k > k0) block_update(k - k0, false);
+  // pivoted columns: R(t, t) = beta, zeros below (dense.py:161-162)
   for (int c = c0 + warp; c < c1; c += kWarps) {
     const int t = pos[c];
-    if (done[c]) {
-      const int tb = t - (t % kBB);
-      const int jq = t - tb;
-      if (lane < jq) sh.fw[warp][lane] = __ldcg(pf + (int64_t)t * kBB + lane);
-      __syncwarp();
+    if (done[c] == 1) {
       double* col = W + (int64_t)c * m;
-      for (int i = tb + lane; i < t; i += 32) {
-        double x = col[i];
-        const int qe = min(jq, i - tb + 1);
-        for (int q = 0; q < qe; ++q) x -= __ldcg(V + (int64_t)(tb + q) * m + i) * sh.fw[warp][q];
-        col[i] = x;
-      }
       const double bt = __ldcg(betas + t);
       if (__ldcg(taus + t) != 0.0)
         for (int i = t + lane; i < m; i += 32) col[i] = (i == t) ? bt : 0.0;
@@ -626,8 +564,89 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
   int n_corr = 0;  // rows of e_tilde kept in the dead slots
   if (scheme == 1) n_corr = n_fine;
   else if (scheme == 2) n_corr = k_stop - k_c;
-  // ---- write back: new slot s < n_fine <- R row k_c + s (only s < n_corr
-  //      are read later); slot n_fine + t <- R row t (t < k_c)
+  // ---- frozen columns: R rows t < k_c + n_corr of Q^T a (a = original
+  // column, restored in W) on the tensor cores (DMMA), written straight to
+  // the pool in the write-back slot order: slot = t < k_c ? n_fine + t : t - k_c
+  const int nf = sh.nfrz;
+  group_barrier(ctr, G, gen, 200000, events + 12 * slot + 9);   // Q complete
+  if (nf > 0) {
+    const int T = k_c + n_corr;
+    double (*As)[kLDS] = reinterpret_cast<double (*)[kLDS]>(vsh);             // [16][kLDS]
+    double (*Bs)[kLDS] = reinterpret_cast<double (*)[kLDS]>(vsh + 16 * kLDS);  // [16][kLDS]
+    double (*Cs)[65] = reinterpret_cast<double (*)[65]>(vsh);                 // [64][65] (epilogue)
+    const int wm = warp >> 2, wn = warp & 3;
+    for (int ct = 0; ct < nf; ct += 64) {
+      __syncthreads();
+      if (tid < 64) {
+        if (ct + tid < nf) {
+          double* base;
+          int64_t stride;
+          pool_col(flist[c0 + ct + tid], base, stride);
+          sh.cbase[tid] = base;
+          sh.cstride[tid] = stride;
+        }
+      }
+      __syncthreads();
+      for (int rt = 0; rt < T; rt += 64) {
+        double acc[4][2][2];
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int b = 0; b < 2; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+        for (int i0 = 0; i0 < m; i0 += 16) {
+          __syncthreads();
+#pragma unroll
+          for (int r = 0; r < 4; ++r) {
+            const int e = tid + r * kT;
+            const int kk = e & 15, cl = e >> 4;
+            const int i = i0 + kk;
+            double av = 0.0, bv2 = 0.0;
+            if (i < m) {
+              if (rt + cl < T) av = __ldcg(Q + (int64_t)i + (int64_t)(rt + cl) * m);
+              if (ct + cl < nf) bv2 = W[(int64_t)i + (int64_t)flist[c0 + ct + cl] * m];
+            }
+            As[kk][cl] = av;
+            Bs[kk][cl] = bv2;
+          }
+          __syncthreads();
+#pragma unroll
+          for (int kq = 0; kq < 4; ++kq) {
+            const int kr = kq * 4 + (lane & 3);
+            double af[4], bf[2];
+#pragma unroll
+            for (int mi = 0; mi < 4; ++mi) af[mi] = As[kr][wm * 32 + mi * 8 + (lane >> 2)];
+#pragma unroll
+            for (int ni = 0; ni < 2; ++ni) bf[ni] = Bs[kr][wn * 16 + ni * 8 + (lane >> 2)];
+#pragma unroll
+            for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+              for (int ni = 0; ni < 2; ++ni) dmma(acc[mi][ni][0], acc[mi][ni][1], af[mi], bf[ni]);
+          }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+          for (int ni = 0; ni < 2; ++ni)
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+              Cs[wn * 16 + ni * 8 + (lane & 3) * 2 + h][wm * 32 + mi * 8 + (lane >> 2)] =
+                  acc[mi][ni][h];
+        __syncthreads();
+        for (int e = tid; e < 64 * 64; e += kT) {
+          const int r = e & 63, cl = e >> 6;
+          const int t = rt + r;
+          if (t < T && ct + cl < nf) {
+            const int sl = t < k_c ? n_fine + t : t - k_c;
+            sh.cbase[cl][(int64_t)sl * sh.cstride[cl]] = Cs[cl][r];
+          }
+        }
+      }
+    }
+  }
+  // ---- write back (non-frozen columns): new slot s < n_fine <- R row
+  //      k_c + s (only s < n_corr are read later); slot n_fine + t <- R row t
+  __syncthreads();
   {
     const int ntc = (c1 - c0 + 15) / 16, ntr = (m + 31) / 32;
     for (int tix = warp; tix < ntc * ntr; tix += kWarps) {
@@ -644,7 +663,7 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
       __syncwarp();
       for (int q = 0; q < 16; ++q) {
         const int c = tc + q;
-        if (c >= c1) continue;
+        if (c >= c1 || done[c] == 2) continue;
         int j, cc;
         nbr_of(c, j, cc);
         const int64_t* nr = nbrs + 4 * (int64_t)(nb0 + j);
@@ -659,6 +678,8 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
       __syncwarp();
     }
   }
+  if (tid == 0 && nf > 0)
+    atomicAdd(reinterpret_cast<unsigned long long*>(events + 12 * slot + 11), (unsigned long long)nf);
   if (rank == 0 && tid == 0) {
     int64_t* ev = events + 12 * slot;
     ev[0] = p;
@@ -685,7 +706,7 @@ int spand_rrqr_cta_count(void) {
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   // capacity for panels up to 4224 rows (the tile staging size); taller
   // panels need more shared memory and are launched with smaller groups
-  const size_t smem = (size_t)kWarps * 16 * 33 * sizeof(double);
+  const size_t smem = kMinSmem;
   cudaFuncSetAttribute(rrqr_wave_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)(kMaxM * sizeof(double)));
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, rrqr_wave_kernel, kT, smem) != cudaSuccess)
@@ -697,7 +718,7 @@ int spand_rrqr_capacity(int vmax) {
   int dev = 0, sms = 0, per = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return -1;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  size_t smem = (size_t)kWarps * 16 * 33 * sizeof(double);
+  size_t smem = kMinSmem;
   if ((size_t)vmax * sizeof(double) > smem) smem = (size_t)vmax * sizeof(double);
   cudaFuncSetAttribute(rrqr_wave_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)(kMaxM * sizeof(double)));
@@ -711,7 +732,7 @@ int spand_rrqr_wave(int npanel, int grid, int vmax, const int64_t* panels, const
                     void* stream) {
   if (npanel < 0 || grid < 0 || vmax < 0 || vmax > kMaxM) return -1;
   if (npanel == 0 || grid == 0) return 0;
-  const size_t tile_bytes = (size_t)kWarps * 16 * 33 * sizeof(double);
+  const size_t tile_bytes = kMinSmem;
   size_t smem = (size_t)(vmax > 0 ? vmax : 1) * sizeof(double);
   if (smem < tile_bytes) smem = tile_bytes;
   cudaError_t e = cudaFuncSetAttribute(rrqr_wave_kernel,
