@@ -294,6 +294,10 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
   group_barrier(ctr, G, gen, -1, events + 12 * slot + 9);
 
   // ---- elimination (unblocked Householder steps on the ACTIVE columns).
+  // Inside the loop column c belongs to CTA c % G (interleaved): the
+  // columns that stay active longest are those of the most strongly coupled
+  // neighbours, which are contiguous, so a contiguous split would leave a
+  // few CTAs with all the work.
   // A column whose running norm^2 is below a quarter of (stop_tol r11)^2 can
   // never be a pivot again (running norms only decrease, and within the
   // reference's 0.01 refresh rule they track the exact tail norm to ~1e-11
@@ -303,7 +307,16 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
   double r11 = 0.0, eta_last = 0.0;
   double thr2 = 0.0;   // 0.25 (stop_tol r11)^2
   int k = 0;
+#ifdef SPAND_RRQR_PHASES
+  long long ph_t[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  long long ph_last = clock64(), nact = 0;
+  int ph_cur = 7;
+#define PH(x) do { long long _n = clock64(); ph_t[ph_cur] += _n - ph_last; ph_last = _n; ph_cur = (x); } while (0)
+#else
+#define PH(x) do {} while (0)
+#endif
   while (k < kmax) {
+    PH(0);
     // ---- winning column: max value, smallest current position (ties in
     // both: lowest record, as a sequential scan).  Records are scanned in
     // parallel and reduced over the CTA.
@@ -374,6 +387,7 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
     }
     const int jpos = (int)wp;
     const int j = (int)(uint32_t)(wpc & 0xffffffffLL);
+    PH(1);
     // pivot column rows k..m-1 (current: every active column is updated
     // in place each step)
     const int len = m - k;
@@ -395,15 +409,16 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
     // ---- swap bookkeeping (reference: r[:, [k, j]], perm[[k, j]] ...): the
     // column at position k moves to j's old position; owners update their
     // own columns' positions (no shared permutation array)
-    const bool own_j = j >= c0 && j < c1;
+    const bool own_j = (j % G) == rank;   // loop ownership is interleaved
     if (own_j && tid == 0) {
       pos[j] = k;
       done[j] = 1;
     }
     if (rank == 0 && tid == 0) piv[k] = eta;
     __syncthreads();
-    for (int c = c0 + tid; c < c1; c += kT)
+    for (int c = rank + G * tid; c < n; c += G * kT)
       if (c != j && done[c] != 1 && pos[c] == k) pos[c] = jpos;
+    PH(2);
     // ---- reflector v = x - beta e1, beta = -sign(x0) eta (dense.py:155-159)
     double beta = 0.0, tau = 0.0;
     if (eta > 0.0) {
@@ -429,17 +444,21 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
     }
     // ---- owned active columns: a -= tau (v.a) v, row-k entry, norm
     // downdate with the reference's refresh rule (dense.py:160-178), freeze
+    PH(3);
     bv = -1.0;
     bp = 0x7fffffffffffLL;
     bc = -1;
-    for (int c = c0 + warp; c < c1; c += kWarps) {
+    for (int c = rank + G * warp; c < n; c += G * kWarps) {
       if (c == j || done[c]) continue;
+#ifdef SPAND_RRQR_PHASES
+      if (lane == 0) ++nact;
+#endif
       if (cur[c] < thr2) {
         // freeze; the final column is recomputed from the ORIGINAL data,
         // which stays in the pool block: restore it in W (k > 0 only)
         if (lane == 0) {
           done[c] = 2;
-          flist[c0 + atomicAdd(&sh.nfrz, 1)] = c;
+          flist[rank + G * atomicAdd(&sh.nfrz, 1)] = c;
           atomicMax(&sh.fmax, (unsigned long long)__double_as_longlong(cur[c]));
         }
         if (k > 0) {
@@ -508,11 +527,20 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
       }
     }
     __syncthreads();
+    PH(4);
     publish(bv, bp, bc, (k + 1) & 1);
     ++k;
+    PH(5);
     group_barrier(ctr, G, gen, k, events + 12 * slot + 9);
   }
   const int k_stop = k;
+#ifdef SPAND_RRQR_PHASES
+  PH(7);
+  if (lane == 0 && m >= 1000 && (rank == 0 || rank == G / 2))
+    printf("[rrqr phases] p %d m %d n %d G %d rank %d warp %d k %d active-col-steps %lld | kcycles: cand %lld pivcol %lld refl %lld colpass %lld publish %lld barrier %lld\n",
+           p, m, n, G, rank, warp, k, nact, ph_t[0] / 1000, ph_t[1] / 1000, ph_t[2] / 1000,
+           ph_t[3] / 1000, ph_t[4] / 1000, ph_t[5] / 1000);
+#endif
   // every CTA must be done reading this step's pivot column (the loop may
   // have stopped on it) before owners patch their columns
   group_barrier(ctr, G, gen, 100000 + k, events + 12 * slot + 9);
@@ -581,7 +609,7 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
         if (ct + tid < nf) {
           double* base;
           int64_t stride;
-          pool_col(flist[c0 + ct + tid], base, stride);
+          pool_col(flist[rank + G * (ct + tid)], base, stride);
           sh.cbase[tid] = base;
           sh.cstride[tid] = stride;
         }
@@ -603,7 +631,7 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
             double av = 0.0, bv2 = 0.0;
             if (i < m) {
               if (rt + cl < T) av = __ldcg(Q + (int64_t)i + (int64_t)(rt + cl) * m);
-              if (ct + cl < nf) bv2 = W[(int64_t)i + (int64_t)flist[c0 + ct + cl] * m];
+              if (ct + cl < nf) bv2 = W[(int64_t)i + (int64_t)flist[rank + G * (ct + cl)] * m];
             }
             As[kk][cl] = av;
             Bs[kk][cl] = bv2;
