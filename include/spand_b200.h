@@ -110,10 +110,15 @@ int spand_apply_runs(int nchunk, const int64_t* chunks, const int64_t* contrib, 
 /* ---- factorization kernels (replace dense.py:45-183 and the BLAS calls of
  *      schemes.py:199-236, factorize.py:131-220) ---------------------------- */
 
-/* Batched in-place Cholesky (lower) of square operands (7 int64 each).
- * info[t] = 0 or failing pivot + 1 (dense.py:53-55). */
+/* Batched in-place Cholesky (lower) of square operands.  Task row (8 int64):
+ * {operand(7), info slot}.  The failing pivot p (0-based, within the operand)
+ * is reported as info[slot] = p + piv_off + 1 (LAPACK convention,
+ * dense.py:53-55); first_only = 0 overwrites the slot (0 on success),
+ * first_only = 1 only records the first failure (blocked factorizations of
+ * large blocks, piv_off = the diagonal block's row offset). */
 int spand_potrf_batched(int ntask, const int64_t* ops, const int32_t* m0,
-                        const int32_t* off, int32_t* info, void* stream);
+                        const int32_t* off, int32_t* info, int piv_off, int first_only,
+                        void* stream);
 /* Batched lower-triangular inverse: task row = {L operand(7), Linv operand(7)}.
  * Upper triangle of Linv is written with zeros (dense.py:85-93). */
 int spand_trtri_batched(int ntask, const int64_t* ops, const int32_t* m0,
@@ -197,6 +202,13 @@ int spand_plan_sizes(void* h, int64_t* out);
 int spand_plan_emit(void* h, int64_t pool_base, int64_t fac_base, int64_t temp_base,
                     int64_t ctr_base, int dry);
 int spand_plan_program(void* h, int64_t* prog, int64_t* launches);
+/* incremental emission (one level per call, then the final block):
+ * chunk_sizes[3] = {program length, launch count, workspace used so far};
+ * spand_plan_chunk copies the chunk with chunk-relative program offsets. */
+int spand_plan_emit_begin(void* h, int64_t pool_base, int64_t fac_base, int64_t temp_base,
+                          int64_t ctr_base);
+int spand_plan_emit_next(void* h, int64_t* chunk_sizes);
+int spand_plan_chunk(void* h, int64_t* prog, int64_t* launches);
 int spand_plan_meta(void* h, int64_t* out);
 void* spand_collect_create(void* plan, const int64_t* events, int scheme);
 void spand_collect_destroy(void* h);

@@ -32,7 +32,7 @@ SIGNATURES = {
     "spand_apply_scatter": [_c_int, _P, _P, _P, _P, _P, _c_i64, _P, _c_i64,
                             _c_int, _P],
     "spand_apply_runs": [_c_int, _P, _P, _P, _c_i64, _P, _c_i64, _c_int, _P],
-    "spand_potrf_batched": [_c_int, _P, _P, _P, _P, _P],
+    "spand_potrf_batched": [_c_int, _P, _P, _P, _P, _c_int, _c_int, _P],
     "spand_trtri_batched": [_c_int, _P, _P, _P, _P],
     "spand_trtri_tiles": [_c_int, _P, _P, _P, _P],
     "spand_copy_batched": [_c_int, _P, _P, _P, _P],

@@ -14,11 +14,13 @@ constexpr int NB = 32;
 // Left-looking blocked Cholesky of one live window (in place, lower).
 __global__ void __launch_bounds__(kT)
 potrf_kernel(const int64_t* __restrict__ ops, const int32_t* __restrict__ m0,
-             const int32_t* __restrict__ off, int32_t* __restrict__ info) {
+             const int32_t* __restrict__ off, int32_t* __restrict__ info, int piv_off,
+             int first_only) {
   __shared__ double Bk[NB][65];     // rows jb..jb+NB of columns kb..kb+64
   __shared__ double D[NB][NB + 1];  // diagonal tile
   __shared__ int bad;
-  const Opnd A = load_opnd(ops + 7 * (int64_t)blockIdx.x, m0, off);
+  const int64_t* row = ops + 8 * (int64_t)blockIdx.x;
+  const Opnd A = load_opnd(row, m0, off);
   const int n = A.rows < A.cols ? A.rows : A.cols;
   const int ld = A.ld;
   double* a = A.p;
@@ -114,7 +116,11 @@ potrf_kernel(const int64_t* __restrict__ ops, const int32_t* __restrict__ m0,
       if (r < c) a[r + (int64_t)c * ld] = 0.0;
     }
   }
-  if (threadIdx.x == 0) info[blockIdx.x] = bad;
+  if (threadIdx.x == 0) {
+    int32_t* slot = info + row[7];
+    if (!first_only) *slot = bad ? bad + piv_off : 0;
+    else if (bad && *slot == 0) *slot = bad + piv_off;
+  }
 }
 
 // Lower-triangular inverse, one thread per column (forward substitution),
@@ -161,10 +167,10 @@ copy_kernel(const int64_t* __restrict__ ops, const int32_t* __restrict__ m0,
 extern "C" {
 
 int spand_potrf_batched(int ntask, const int64_t* ops, const int32_t* m0, const int32_t* off,
-                        int32_t* info, void* stream) {
+                        int32_t* info, int piv_off, int first_only, void* stream) {
   if (ntask < 0) return -1;
   if (ntask == 0) return 0;
-  potrf_kernel<<<ntask, kT, 0, as_stream(stream)>>>(ops, m0, off, info);
+  potrf_kernel<<<ntask, kT, 0, as_stream(stream)>>>(ops, m0, off, info, piv_off, first_only);
   SPAND_CHECK_LAUNCH();
   return 0;
 }

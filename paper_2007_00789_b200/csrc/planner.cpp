@@ -93,6 +93,44 @@ int spand_plan_emit(void* h, int64_t pool_base, int64_t fac_base, int64_t temp_b
   return 0;
 }
 
+// Incremental emission: begin, then next() until it returns 0; after each
+// next(), chunk_sizes gives {chunk program length, chunk launch count} and
+// chunk() copies them with program offsets RELATIVE to the chunk start.
+int spand_plan_emit_begin(void* h, int64_t pool_base, int64_t fac_base, int64_t temp_base,
+                          int64_t ctr_base) {
+  Plan* p = static_cast<Plan*>(h);
+  p->dry = false;
+  p->pool_base = pool_base;
+  p->fac_base = fac_base;
+  p->temp_base = temp_base;
+  p->ctr_base = ctr_base;
+  p->emit_begin();
+  return 0;
+}
+
+int spand_plan_emit_next(void* h, int64_t* chunk_sizes) {
+  Plan* p = static_cast<Plan*>(h);
+  const bool more = p->emit_next();
+  chunk_sizes[0] = (int64_t)(p->prog.size() - p->chunk_prog0);
+  chunk_sizes[1] = (int64_t)(p->launches.size() - p->chunk_launch0) / 16;
+  chunk_sizes[2] = p->temp_size;
+  return more ? 1 : 0;
+}
+
+int spand_plan_chunk(void* h, int64_t* prog, int64_t* launches) {
+  Plan* p = static_cast<Plan*>(h);
+  const int64_t base = (int64_t)p->chunk_prog0;
+  std::memcpy(prog, p->prog.data() + base, (p->prog.size() - base) * sizeof(int64_t));
+  const size_t l0 = p->chunk_launch0;
+  for (size_t r = l0; r < p->launches.size(); r += 16) {
+    int64_t* o = launches + (r - l0);
+    std::memcpy(o, p->launches.data() + r, 16 * sizeof(int64_t));
+    // program offsets a, b, c (fields 2..4) become chunk-relative
+    for (int f = 2; f <= 4; ++f) o[f] -= base;
+  }
+  return 0;
+}
+
 int spand_plan_program(void* h, int64_t* prog, int64_t* launches) {
   Plan* p = static_cast<Plan*>(h);
   std::memcpy(prog, p->prog.data(), p->prog.size() * sizeof(int64_t));

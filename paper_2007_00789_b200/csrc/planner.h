@@ -14,6 +14,7 @@ extern "C" int spand_rrqr_capacity(int vmax);
 namespace spand {
 
 constexpr int kTile = 64;
+constexpr int kBigPotrf = 256;   // larger diagonal blocks use the blocked (multi-CTA) Cholesky
 constexpr int kMaxGroupTotal = 148 * 16;   // >= any cooperative RRQR grid
 
 struct Level {
@@ -223,10 +224,13 @@ struct Plan {
                    int64_t cs = 0, int64_t rn = -1, int64_t cn = -1) {
     v.insert(v.end(), {p, rc, cc, rs, cs, rn, cn});
   }
+  // sub-operand at (rs, cs) of o, clamped to rn x cn (< 0: to o's extent)
   static void sub(std::vector<int64_t>& v, const int64_t* o, int64_t rs, int64_t cs, int64_t rn,
                   int64_t cn) {
-    const int64_t r = o[5] < 0 ? rn : std::min(rn, std::max(o[5] - rs, (int64_t)0));
-    const int64_t c = o[6] < 0 ? cn : std::min(cn, std::max(o[6] - cs, (int64_t)0));
+    const int64_t rl = o[5] < 0 ? -1 : std::max(o[5] - rs, (int64_t)0);
+    const int64_t cl = o[6] < 0 ? -1 : std::max(o[6] - cs, (int64_t)0);
+    const int64_t r = rn < 0 ? rl : (rl < 0 ? rn : std::min(rn, rl));
+    const int64_t c = cn < 0 ? cl : (cl < 0 ? cn : std::min(cn, cl));
     v.insert(v.end(), {o[0], o[1], o[2], o[3] + rs, o[4] + cs, r, c});
   }
   bool dry = false;   // sizing pass: compute temp_size only, emit nothing
@@ -324,6 +328,86 @@ struct Plan {
   }
   int64_t m0v(int64_t c) const { return c < ncl ? m0[c] : fcap; }
 
+  // Cholesky of a batch of diagonal operands (full live windows, 7 int64
+  // each) with info slots info_next.. in operator order.  Blocks up to
+  // kBigPotrf rows: one CTA each.  Larger blocks: right-looking blocked
+  // Cholesky over 64-wide panels -- diagonal potrf, 64x64 inverse, panel
+  // TRSM and lower trailing update as tensor-core GEMMs -- so a 3000-row
+  // block uses the whole GPU instead of one SM.  Scratch: an m0 x m0 image
+  // in temp per large block (temp_at on).
+  void potrf(const std::vector<std::vector<int64_t>>& ops, int64_t temp_at) {
+    std::vector<int64_t> small;
+    std::vector<size_t> big;
+    for (size_t t = 0; t < ops.size(); ++t) {
+      const int64_t sz = m0v(ops[t][1]);
+      if (sz > kBigPotrf) big.push_back(t);
+      else {
+        small.insert(small.end(), ops[t].begin(), ops[t].end());
+        small.push_back(info_next + (int64_t)t);
+      }
+    }
+    if (!small.empty()) launch(1, (int64_t)small.size() / 8, push(small), 0, 0, 0, 0);
+    if (!big.empty()) {
+      std::vector<int64_t> scr;
+      int64_t acc = temp_at, smax = 0;
+      for (size_t t : big) {
+        scr.push_back(acc);
+        const int64_t sz = m0v(ops[t][1]);
+        acc += sz * sz;
+        smax = std::max(smax, sz);
+      }
+      temp_size = std::max(temp_size, acc);
+      for (int64_t o = 0; o < smax; o += kTile) {
+        std::vector<int64_t> diag, tri, cps;
+        std::vector<Target> pan, trail;
+        for (size_t u = 0; u < big.size(); ++u) {
+          const size_t t = big[u];
+          const int64_t sz = m0v(ops[t][1]);
+          if (sz <= o) continue;
+          const int64_t* op = ops[t].data();
+          std::vector<int64_t> tmp(ops[t]);
+          tmp[0] = temp_base + 8 * scr[u];
+          sub(diag, op, o, o, kTile, kTile);
+          diag.push_back(info_next + (int64_t)t);
+          sub(tri, op, o, o, kTile, kTile);
+          sub(tri, tmp.data(), o, o, kTile, kTile);
+          if (sz > o + kTile) {
+            sub(cps, op, o + kTile, o, -1, kTile);
+            sub(cps, tmp.data(), o + kTile, o, -1, kTile);
+            cps.push_back(0);
+            Target a;
+            sub(a.c, op, o + kTile, o, -1, kTile);
+            sub(a.segs, tmp.data(), o + kTile, o, -1, kTile);
+            sub(a.segs, tmp.data(), o, o, kTile, kTile);
+            a.mm = sz - o - kTile;
+            a.nn = kTile;
+            pan.push_back(a);
+            Target b;
+            sub(b.c, op, o + kTile, o + kTile, -1, -1);
+            sub(b.segs, op, o + kTile, o, -1, kTile);
+            sub(b.segs, op, o + kTile, o, -1, kTile);
+            b.mm = b.nn = sz - o - kTile;
+            trail.push_back(b);
+          }
+        }
+        launch(1, (int64_t)diag.size() / 8, push(diag), 0, 0, o, 1);
+        launch(2, (int64_t)tri.size() / 14, push(tri));
+        if (!cps.empty()) launch(4, (int64_t)cps.size() / 15, push(cps));
+        gemm(pan, 1.0, 0.0, 1, 0);      // L21 = A21 L11^-T
+        gemm(trail, -1.0, 1.0, 1, 1);   // A22 -= L21 L21^T (lower tiles)
+      }
+      // zero the strict upper triangles (dpotrf clean, dense.py:53)
+      std::vector<int64_t> z;
+      for (size_t t : big) {
+        z.insert(z.end(), ops[t].begin(), ops[t].end());
+        z.insert(z.end(), ops[t].begin(), ops[t].end());
+        z.push_back(1);
+      }
+      launch(4, (int64_t)z.size() / 15, push(z));
+    }
+    info_next += (int64_t)ops.size();
+  }
+
   static std::vector<int> groups(const std::vector<int64_t>& works, int cap) {
     double total = 0;
     for (auto w : works) total += (double)w;
@@ -341,16 +425,47 @@ struct Plan {
   }
 
   void emit() {
+    emit_begin();
+    while (emit_next()) {
+    }
+  }
+  // Incremental emission, one level per call (then the final block), so
+  // the host can launch level l while it emits level l + 1.  The chunk of a
+  // call is prog[chunk_prog0:] / launches[chunk_launch0:].
+  size_t next_level = 0, chunk_prog0 = 0, chunk_launch0 = 0;
+  bool final_done = false;
+  void emit_begin() {
     prog.clear();
     launches.clear();
     info_next = ctr_next = 0;
     temp_size = 1;
-    for (auto& L : lv) {
+    next_level = 0;
+    final_done = false;
+    chunk_prog0 = chunk_launch0 = 0;
+  }
+  bool emit_next() {
+    chunk_prog0 = prog.size();
+    chunk_launch0 = launches.size();
+    if (next_level < lv.size()) {
+      emit_level(lv[next_level++]);
+      return true;
+    }
+    if (!final_done) {
+      final_done = true;
+      emit_final();
+      return true;
+    }
+    return false;
+  }
+  void emit_level(Level& L) {
+    {
       if (!L.interiors.empty()) {
-        std::vector<int64_t> ops;
-        for (int s : L.interiors) opnd(ops, blk_ptr(s, s), s, s);
-        launch(1, (int64_t)L.interiors.size(), push(ops), 0, 0, info_next);
-        info_next += (int64_t)L.interiors.size();
+        std::vector<std::vector<int64_t>> pops;
+        for (int s : L.interiors) {
+          pops.emplace_back();
+          opnd(pops.back(), blk_ptr(s, s), s, s);
+        }
+        potrf(pops, 0);
         std::vector<std::vector<int64_t>> Ls, Xs;
         std::vector<int64_t> sz;
         for (int s : L.interiors) {
@@ -406,10 +521,11 @@ struct Plan {
           gemm(st, -1.0, 1.0, 1, diag);
         }
       }
-      if (L.skipped) continue;
+      if (L.skipped) return;
       // rescale every active interface (factorize.py:165-173)
       const size_t na = L.active.size();
-      std::vector<int64_t> c1, ops, c2;
+      std::vector<int64_t> c1, c2;
+      std::vector<std::vector<int64_t>> pops;
       std::vector<std::vector<int64_t>> Ls, Xs;
       std::vector<int64_t> sz;
       for (size_t k = 0; k < na; ++k) {
@@ -417,7 +533,8 @@ struct Plan {
         opnd(c1, blk_ptr(p, p), p, p);
         opnd(c1, fac_base + 8 * L.l_off[k], p, p);
         c1.push_back(1);
-        opnd(ops, fac_base + 8 * L.l_off[k], p, p);
+        pops.emplace_back();
+        opnd(pops.back(), fac_base + 8 * L.l_off[k], p, p);
         std::vector<int64_t> l, x;
         opnd(l, fac_base + 8 * L.l_off[k], p, p);
         opnd(x, fac_base + 8 * L.linv_off[k], p, p);
@@ -430,8 +547,7 @@ struct Plan {
       }
       if (na) {
         launch(4, (int64_t)na, push(c1));
-        launch(1, (int64_t)na, push(ops), 0, 0, info_next);
-        info_next += (int64_t)na;
+        potrf(pops, 0);
         trtri(Ls, Xs, sz, 0);
         launch(4, (int64_t)na, push(c2));
       }
@@ -517,6 +633,8 @@ struct Plan {
         }
       }
     }
+  }
+  void emit_final() {
     // final dense block (factorize.py:198-220); virtual cluster id = ncl
     if (!fin.empty()) {
       std::unordered_map<int, int> index;
@@ -527,10 +645,9 @@ struct Plan {
       if (br.empty()) br.assign(4, 0);
       const int64_t a = push(cl), b = push(br);
       launch(6, (int64_t)fin.size(), a, b, 0, (int64_t)fin_blocks.size(), ncl, f_off);
-      std::vector<int64_t> ops;
-      opnd(ops, fac_base + 8 * f_off, ncl, ncl);
-      launch(1, 1, push(ops), 0, 0, info_next);
-      info_next += 1;
+      std::vector<std::vector<int64_t>> pops(1);
+      opnd(pops[0], fac_base + 8 * f_off, ncl, ncl);
+      potrf(pops, 0);
       std::vector<int64_t> l, x;
       opnd(l, fac_base + 8 * f_off, ncl, ncl);
       opnd(x, fac_base + 8 * flinv_off, ncl, ncl);

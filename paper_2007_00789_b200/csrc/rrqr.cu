@@ -50,9 +50,9 @@ constexpr int kCR = kBB + 2;   // candidate record stride (doubles)
 constexpr int kLDS = 68;       // frozen-column DMMA tiles (conflict-free fragments)
 // dynamic shared memory floor: write-back staging (8 warps x 16 x 33) and
 // the frozen-GEMM epilogue tile (64 x 65)
-constexpr size_t kMinSmem = (size_t)kWarps * 16 * 33 * sizeof(double);
+constexpr size_t kMinSmem = (size_t)4 * 16 * kLDS * sizeof(double);   // 2 stages x (A, B)
 static_assert(kMinSmem >= 64 * 65 * sizeof(double), "epilogue tile");
-static_assert(kMinSmem >= 2 * 16 * kLDS * sizeof(double), "operand tiles");
+static_assert(kMinSmem >= (size_t)kWarps * 16 * 33 * sizeof(double), "gather tiles");
 
 struct Sh {
   double red[kWarps];
@@ -63,10 +63,15 @@ struct Sh {
   int bq[kWarps];
   int bcol[kWarps];
   int nfrz;
+  int nact;
+  double red8[kWarps][8];   // multi-value block reductions of the column pass
+  double tot8[8];
   unsigned long long fmax;   // bits of the max norm^2 of my frozen columns (>= 0)
-  int nb_start[65];  // column start of each neighbour (first 64)
+  int nb_start[1025];  // column start of each neighbour (panels with <= 1024)
+  int wsum[kWarps];
   double* cbase[64];  // frozen GEMM epilogue: column base in the pool
   int64_t cstride[64];
+  int fcol[64];
 };
 
 __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
@@ -106,13 +111,223 @@ __device__ __forceinline__ bool better(double va, int64_t pa, double vb, int64_t
   return va > vb || (va == vb && pa < pb);
 }
 
+__device__ __forceinline__ void cp_async8(double* smem, const double* gmem, bool pred) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  const int sz = pred ? 8 : 0;
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(gmem), "r"(sz));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::); }
+
 __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                : "+d"(d0), "+d"(d1)
                : "d"(a), "d"(b));
 }
 
-__global__ void __launch_bounds__(kT, 4)
+// N (<= 8) block-wide sums at once, fixed order, result in every thread
+template <int N>
+__device__ __forceinline__ void block_reduce_n(double (&v)[N], Sh& sh) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int q = 0; q < N; ++q) v[q] = warp_sum(v[q]);
+  if (lane == 0) {
+#pragma unroll
+    for (int q = 0; q < N; ++q) sh.red8[warp][q] = v[q];
+  }
+  __syncthreads();
+  if (threadIdx.x < N) {
+    double t = 0.0;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) t += sh.red8[w][threadIdx.x];
+    sh.tot8[threadIdx.x] = t;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < N; ++q) v[q] = sh.tot8[q];
+}
+
+struct ColCtx {
+  double* W;
+  int m, k, len;
+  double tau;
+  const double* v;        // reflector (shared memory), rows k..m-1
+  double* cur;
+  double* ref;
+  const int32_t* pos;
+  const int32_t* list;    // this step's active columns, interleaved slots
+  int rank, G;
+  unsigned long long* refresh_ctr;
+};
+
+// Householder update of B active columns at a time by the whole CTA: every
+// thread holds E rows of each column in registers (one read, one write per
+// step), dot products and tail norms are reduced CTA-wide.  Thread b < B
+// then applies the reference's norm downdate / refresh rule (dense.py:
+// 168-178) to column b and keeps the best candidate it has seen.
+template <int B, int E>
+__device__ void colpass_batch(const ColCtx& X, int a0, int nb, Sh& sh, double& bv,
+                              int64_t& bp, int& bc) {
+  const int tid = threadIdx.x;
+  int cs[B];
+  double x[B][E];
+#pragma unroll
+  for (int b = 0; b < B; ++b) cs[b] = b < nb ? X.list[X.rank + X.G * (a0 + b)] : -1;
+#pragma unroll
+  for (int b = 0; b < B; ++b) {
+    const double* col = X.W + (int64_t)(cs[b] < 0 ? 0 : cs[b]) * X.m + X.k;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const int i = tid + kT * e;
+      x[b][e] = (cs[b] >= 0 && i < X.len) ? col[i] : 0.0;
+    }
+  }
+  double d[B];
+#pragma unroll
+  for (int b = 0; b < B; ++b) {
+    d[b] = 0.0;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const int i = tid + kT * e;
+      if (i < X.len) d[b] += X.v[i] * x[b][e];
+    }
+  }
+  block_reduce_n<B>(d, sh);
+  double t[2 * B];
+#pragma unroll
+  for (int b = 0; b < B; ++b) {
+    const double w = X.tau * d[b];
+    double* col = X.W + (int64_t)(cs[b] < 0 ? 0 : cs[b]) * X.m + X.k;
+    double tail = 0.0, rk = 0.0;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const int i = tid + kT * e;
+      if (cs[b] >= 0 && i < X.len) {
+        const double y = x[b][e] - w * X.v[i];
+        col[i] = y;
+        if (i == 0) rk = y;
+        else tail += y * y;
+      }
+    }
+    t[b] = tail;
+    t[B + b] = rk;   // only thread 0 holds row k: the sum is exact
+  }
+  block_reduce_n<2 * B>(t, sh);
+#pragma unroll
+  for (int b = 0; b < B; ++b) {
+    if (tid == b && b < nb) {
+      const int c = cs[b];
+      const double rk = t[B + b], tail = t[b];
+      double cn = X.cur[c] - rk * rk;
+      if (cn < 0.0) cn = 0.0;
+      if (cn < 0.01 * X.ref[c]) {
+        // exact tail norm of the updated column (dense.py:172-178)
+        cn = tail;
+        X.ref[c] = tail;
+        atomicAdd(X.refresh_ctr, 1ull);
+      }
+      X.cur[c] = cn;
+      const int64_t ps = X.pos[c];
+      if (better(cn, ps, bv, bp)) {
+        bv = cn;
+        bp = ps;
+        bc = c;
+      }
+    }
+  }
+}
+
+// columns longer than 16 rows per thread: chunked, the update re-reads
+__device__ void colpass_long(const ColCtx& X, int a0, Sh& sh, double& bv, int64_t& bp, int& bc) {
+  const int tid = threadIdx.x;
+  const int c = X.list[X.rank + X.G * a0];
+  double* col = X.W + (int64_t)c * X.m + X.k;
+  double d[1] = {0.0};
+  for (int i = tid; i < X.len; i += kT) d[0] += X.v[i] * col[i];
+  block_reduce_n<1>(d, sh);
+  const double w = X.tau * d[0];
+  double t[2] = {0.0, 0.0};
+  for (int i = tid; i < X.len; i += kT) {
+    const double y = col[i] - w * X.v[i];
+    col[i] = y;
+    if (i == 0) t[1] = y;
+    else t[0] += y * y;
+  }
+  block_reduce_n<2>(t, sh);
+  if (tid == 0) {
+    double cn = X.cur[c] - t[1] * t[1];
+    if (cn < 0.0) cn = 0.0;
+    if (cn < 0.01 * X.ref[c]) {
+      cn = t[0];
+      X.ref[c] = t[0];
+      atomicAdd(X.refresh_ctr, 1ull);
+    }
+    X.cur[c] = cn;
+    const int64_t ps = X.pos[c];
+    if (better(cn, ps, bv, bp)) {
+      bv = cn;
+      bp = ps;
+      bc = c;
+    }
+  }
+}
+
+template <int B, int E>
+__device__ void qform_batched(double* Q, const double* V, const double* taus, int m, int kst,
+                              int rank, int G, Sh& sh) {
+  const int tid = threadIdx.x;
+  for (int u0 = 0; rank + G * u0 < m; u0 += B) {
+    int cs[B];
+    int cmax = 0;
+#pragma unroll
+    for (int b = 0; b < B; ++b) {
+      const int c = rank + G * (u0 + b);
+      cs[b] = c < m ? c : -1;
+      if (c < m) cmax = c;
+    }
+    double x[B][E];
+#pragma unroll
+    for (int b = 0; b < B; ++b)
+#pragma unroll
+      for (int e = 0; e < E; ++e) x[b][e] = (tid + kT * e == cs[b]) ? 1.0 : 0.0;
+    for (int t = min(kst - 1, cmax); t >= 0; --t) {
+      const double tt = __ldcg(taus + t);
+      if (tt == 0.0) continue;
+      double v[E];
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const int i = tid + kT * e;
+        v[e] = (i >= t && i < m) ? __ldcg(V + (int64_t)t * m + i) : 0.0;
+      }
+      double d[B];
+#pragma unroll
+      for (int b = 0; b < B; ++b) {
+        d[b] = 0.0;
+#pragma unroll
+        for (int e = 0; e < E; ++e) d[b] += v[e] * x[b][e];
+      }
+      block_reduce_n<B>(d, sh);
+#pragma unroll
+      for (int b = 0; b < B; ++b) {
+        const double f = tt * d[b];
+#pragma unroll
+        for (int e = 0; e < E; ++e) x[b][e] -= f * v[e];
+      }
+    }
+#pragma unroll
+    for (int b = 0; b < B; ++b) {
+      if (cs[b] < 0) continue;
+      double* col = Q + (int64_t)cs[b] * m;
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const int i = tid + kT * e;
+        if (i < m) col[i] = x[b][e];
+      }
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kT, 2)
 rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* __restrict__ nbrs,
                  int32_t* __restrict__ m0, int32_t* __restrict__ off, double eps, int scheme,
                  int64_t* __restrict__ events) {
@@ -146,16 +361,42 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
   const int offp = off[p];
   const int ldp = m0[p];
   const int m = ldp - offp;
-  // column layout over neighbours (live columns at kernel start)
-  int n = 0;
+  // column layout over neighbours (live columns at kernel start): block
+  // prefix scan of the live widths
+  constexpr int kMaxNb = 1024;
   const int nnb = nb1 - nb0;
-  for (int j = 0; j < nnb; ++j) {
-    const int w = (int)nbrs[4 * (int64_t)(nb0 + j)];
-    if (j < 64 && tid == 0) sh.nb_start[j] = n;
-    n += m0[w] - off[w];
+  int n = 0;
+  for (int base = 0; base < nnb; base += kT) {
+    const int j = base + tid;
+    int len = 0;
+    if (j < nnb) {
+      const int w = (int)nbrs[4 * (int64_t)(nb0 + j)];
+      len = m0[w] - off[w];
+    }
+    int x = len;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) sh.wsum[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+      int y = lane < kWarps ? sh.wsum[lane] : 0;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int z = __shfl_up_sync(0xffffffffu, y, o);
+        if (lane >= o) y += z;
+      }
+      if (lane < kWarps) sh.wsum[lane] = y;
+    }
+    __syncthreads();
+    if (j < nnb && j < kMaxNb) sh.nb_start[j] = n + (warp ? sh.wsum[warp - 1] : 0) + x - len;
+    n += sh.wsum[kWarps - 1];
+    __syncthreads();
   }
   if (tid == 0) {
-    if (nnb <= 64) sh.nb_start[nnb] = n;
+    if (nnb <= kMaxNb) sh.nb_start[nnb] = n;
     sh.nfrz = 0;
     sh.fmax = 0ull;
   }
@@ -177,11 +418,18 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
   const int q0 = (int)(((int64_t)m * rank) / G), q1 = (int)(((int64_t)m * (rank + 1)) / G);
   const int kmax = m < n ? m : n;
 
-  // neighbour of column c (linear scan; <= a few dozen neighbours)
+  // neighbour of column c: binary search of the column starts (the last
+  // neighbour starting at or before c; zero-width neighbours are skipped)
   auto nbr_of = [&](int c, int& j, int& cc) {
     int jj = 0, start = 0;
-    if (nnb <= 64) {
-      while (jj + 1 < nnb && sh.nb_start[jj + 1] <= c) ++jj;
+    if (nnb <= kMaxNb) {
+      int lo2 = 0, hi2 = nnb - 1;
+      while (lo2 < hi2) {
+        const int mid = (lo2 + hi2 + 1) >> 1;
+        if (sh.nb_start[mid] <= c) lo2 = mid;
+        else hi2 = mid - 1;
+      }
+      jj = lo2;
       start = sh.nb_start[jj];
     } else {
       int s = 0;
@@ -309,7 +557,7 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
   int k = 0;
 #ifdef SPAND_RRQR_PHASES
   long long ph_t[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  long long ph_last = clock64(), nact = 0;
+  long long ph_last = clock64(), nact_sum = 0;
   int ph_cur = 7;
 #define PH(x) do { long long _n = clock64(); ph_t[ph_cur] += _n - ph_last; ph_last = _n; ph_cur = (x); } while (0)
 #else
@@ -448,81 +696,51 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
     bv = -1.0;
     bp = 0x7fffffffffffLL;
     bc = -1;
-    for (int c = rank + G * warp; c < n; c += G * kWarps) {
+    // (a) this step's active columns (list in the perm array, which is only
+    // written after the loop); freeze the ones below the threshold
+    __syncthreads();
+    if (tid == 0) sh.nact = 0;
+    __syncthreads();
+    for (int c = rank + G * tid; c < n; c += G * kT) {
       if (c == j || done[c]) continue;
-#ifdef SPAND_RRQR_PHASES
-      if (lane == 0) ++nact;
-#endif
       if (cur[c] < thr2) {
-        // freeze; the final column is recomputed from the ORIGINAL data,
-        // which stays in the pool block: restore it in W (k > 0 only)
-        if (lane == 0) {
-          done[c] = 2;
-          flist[rank + G * atomicAdd(&sh.nfrz, 1)] = c;
-          atomicMax(&sh.fmax, (unsigned long long)__double_as_longlong(cur[c]));
-        }
-        if (k > 0) {
-          double* base;
-          int64_t stride;
-          pool_col(c, base, stride);
-          double* col = W + (int64_t)c * m;
-          for (int i = lane; i < m; i += 32) col[i] = base[(int64_t)i * stride];
-        }
-        __syncwarp();
-        continue;
+        done[c] = 2;
+        flist[rank + G * atomicAdd(&sh.nfrz, 1)] = c;
+        atomicMax(&sh.fmax, (unsigned long long)__double_as_longlong(cur[c]));
+      } else {
+        perm[rank + G * atomicAdd(&sh.nact, 1)] = c;
       }
-      double* col = W + (int64_t)c * m + k;
-      double d = 0.0;
-      for (int base = 0; base < len; base += 256) {
-        double x[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const int i = base + lane + 32 * u;
-          x[u] = i < len ? col[i] : 0.0;
-        }
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const int i = base + lane + 32 * u;
-          if (i < len) d += vsh[i] * x[u];
-        }
+    }
+    __syncthreads();
+    const int nact = sh.nact;
+#ifdef SPAND_RRQR_PHASES
+    if (tid == 0) nact_sum += nact;
+#endif
+    // (c) CTA-wide batched updates
+    {
+      ColCtx X{W, m, k, len, tau, vsh, cur, ref, pos, perm, rank, G,
+               reinterpret_cast<unsigned long long*>(events + 12 * slot + 10)};
+      if (len <= 8 * kT) {
+        for (int a0 = 0; a0 < nact; a0 += 4)
+          colpass_batch<4, 8>(X, a0, min(4, nact - a0), sh, bv, bp, bc);
+      } else if (len <= 16 * kT) {
+        for (int a0 = 0; a0 < nact; a0 += 2)
+          colpass_batch<2, 16>(X, a0, min(2, nact - a0), sh, bv, bp, bc);
+      } else {
+        for (int a0 = 0; a0 < nact; ++a0) colpass_long(X, a0, sh, bv, bp, bc);
       }
-      const double wj = tau * warp_sum(d);
-      double tail = 0.0, rk = 0.0;
-      for (int base = 0; base < len; base += 256) {
-        double x[8];
+    }
+    // candidates live in lanes 0..3 of warp 0: reduce to lane 0
+    if (warp == 0) {
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const int i = base + lane + 32 * u;
-          x[u] = i < len ? col[i] : 0.0;
-        }
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const int i = base + lane + 32 * u;
-          if (i < len) {
-            const double y = x[u] - wj * vsh[i];
-            col[i] = y;
-            if (i == 0) rk = y;
-            else tail += y * y;
-          }
-        }
-      }
-      rk = __shfl_sync(0xffffffffu, rk, 0);
-      tail = warp_sum(tail);
-      if (lane == 0) {
-        double cn = cur[c] - rk * rk;
-        if (cn < 0.0) cn = 0.0;
-        if (cn < 0.01 * ref[c]) {
-          // exact tail norm of the updated column (dense.py:172-178)
-          cn = tail;
-          ref[c] = tail;
-          atomicAdd(reinterpret_cast<unsigned long long*>(events + 12 * slot + 10), 1ull);
-        }
-        cur[c] = cn;
-        const int64_t ps = pos[c];
-        if (better(cn, ps, bv, bp)) {
-          bv = cn;
-          bp = ps;
-          bc = c;
+      for (int o = 16; o > 0; o >>= 1) {
+        const double v2 = __shfl_xor_sync(0xffffffffu, bv, o);
+        const int64_t p2 = __shfl_xor_sync(0xffffffffu, bp, o);
+        const int c2 = __shfl_xor_sync(0xffffffffu, bc, o);
+        if (better(v2, p2, bv, bp)) {
+          bv = v2;
+          bp = p2;
+          bc = c2;
         }
       }
     }
@@ -536,10 +754,10 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
   const int k_stop = k;
 #ifdef SPAND_RRQR_PHASES
   PH(7);
-  if (lane == 0 && m >= 1000 && (rank == 0 || rank == G / 2))
-    printf("[rrqr phases] p %d m %d n %d G %d rank %d warp %d k %d active-col-steps %lld | kcycles: cand %lld pivcol %lld refl %lld colpass %lld publish %lld barrier %lld\n",
-           p, m, n, G, rank, warp, k, nact, ph_t[0] / 1000, ph_t[1] / 1000, ph_t[2] / 1000,
-           ph_t[3] / 1000, ph_t[4] / 1000, ph_t[5] / 1000);
+  long long tl = clock64(), tq = 0, trs = 0, tg = 0, twb = 0;
+#define TL(var) do { long long _n = clock64(); var += _n - tl; tl = _n; } while (0)
+#else
+#define TL(var) do {} while (0)
 #endif
   // every CTA must be done reading this step's pivot column (the loop may
   // have stopped on it) before owners patch their columns
@@ -557,30 +775,37 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
     if (lane == 0) perm[t] = c;
   }
   __syncthreads();
-  // ---- Q = H_0 H_1 ... H_{k_stop-1}, accumulated backwards (dorg2r order)
-  // on my column range: H_t only touches rows/columns >= t, columns are
-  // independent, so no group synchronisation is needed.
-  for (int64_t e = tid; e < (int64_t)(q1 - q0) * m; e += kT) {
-    const int i = (int)(e % m), c = q0 + (int)(e / m);
-    Q[(int64_t)i + (int64_t)c * m] = (i == c) ? 1.0 : 0.0;
-  }
-  for (int t = k_stop - 1; t >= 0; --t) {
-    const double tt = __ldcg(taus + t);
-    if (tt == 0.0) continue;
-    if (q1 <= t) continue;
-    const int len = m - t;
-    __syncthreads();
-    for (int i = tid; i < len; i += kT) vsh[i] = __ldcg(V + (int64_t)t + i + (int64_t)t * m);
-    __syncthreads();
-    for (int c = max(q0, t) + warp; c < q1; c += kWarps) {
-      double* col = Q + (int64_t)c * m + t;
-      double d = 0.0;
-      for (int i = lane; i < len; i += 32) d += vsh[i] * col[i];
-      d = warp_sum(d) * tt;
-      for (int i = lane; i < len; i += 32) col[i] -= d * vsh[i];
+  TL(twb);   // (patch: counted with the write-back)
+  // ---- Q = H_0 H_1 ... H_{k_stop-1}, accumulated backwards (dorg2r order).
+  // Column c of Q is H_0 ... H_{k-1} e_c, and H_t leaves e_c alone for t > c.
+  // Columns are interleaved over the group (c = rank + G u) for balance;
+  // each CTA keeps 4 columns in registers and streams the reflectors.
+  if (m <= 8 * kT) qform_batched<4, 8>(Q, V, taus, m, k_stop, rank, G, sh);
+  else if (m <= 16 * kT) qform_batched<2, 16>(Q, V, taus, m, k_stop, rank, G, sh);
+  else {
+    for (int64_t e = tid; e < (int64_t)(q1 - q0) * m; e += kT) {
+      const int i = (int)(e % m), c = q0 + (int)(e / m);
+      Q[(int64_t)i + (int64_t)c * m] = (i == c) ? 1.0 : 0.0;
+    }
+    for (int t = k_stop - 1; t >= 0; --t) {
+      const double tt = __ldcg(taus + t);
+      if (tt == 0.0) continue;
+      if (q1 <= t) continue;
+      const int len = m - t;
+      __syncthreads();
+      for (int i = tid; i < len; i += kT) vsh[i] = __ldcg(V + (int64_t)t + i + (int64_t)t * m);
+      __syncthreads();
+      for (int c = max(q0, t) + warp; c < q1; c += kWarps) {
+        double* col = Q + (int64_t)c * m + t;
+        double d = 0.0;
+        for (int i = lane; i < len; i += 32) d += vsh[i] * col[i];
+        d = warp_sum(d) * tt;
+        for (int i = lane; i < len; i += 32) col[i] -= d * vsh[i];
+      }
     }
   }
   __syncthreads();
+  TL(tq);
   // k_c: first pivot below eps * r11 (dense.py:181-182)
   int k_c = k_stop;
   for (int t = 0; t < k_stop; ++t)
@@ -596,11 +821,48 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
   // column, restored in W) on the tensor cores (DMMA), written straight to
   // the pool in the write-back slot order: slot = t < k_c ? n_fine + t : t - k_c
   const int nf = sh.nfrz;
-  group_barrier(ctr, G, gen, 200000, events + 12 * slot + 9);   // Q complete
+  // frozen columns: restore the ORIGINAL data (still in the pool blocks; a
+  // column frozen after step 0 was already updated in W) with the coalesced
+  // tile gather, for my contiguous column range
+  {
+    const int ntc = (c1 - c0 + 15) / 16, ntr = (m + 31) / 32;
+    for (int tix = warp; tix < ntc * ntr; tix += kWarps) {
+      const int tc = c0 + (tix / ntr) * 16, tr = (tix % ntr) * 32;
+      bool any = false;
+      for (int q = 0; q < 16; ++q) any |= (tc + q < c1) && done[tc + q] == 2;
+      if (!any) continue;
+      for (int q = 0; q < 16; ++q) {
+        const int c = tc + q;
+        double val = 0.0;
+        if (c < c1 && done[c] == 2) {
+          int j, cc;
+          nbr_of(c, j, cc);
+          const int64_t* nr = nbrs + 4 * (int64_t)(nb0 + j);
+          const int w = (int)nr[0];
+          const double* blk = reinterpret_cast<const double*>(nr[1]);
+          const int i = tr + lane;
+          if (i < m) {
+            if (nr[2] == 0) val = blk[(int64_t)(offp + i) + (int64_t)(off[w] + cc) * ldp];
+            else val = blk[(int64_t)(off[w] + cc) + (int64_t)(offp + i) * m0[w]];
+          }
+        }
+        tile[warp][q][lane] = val;
+      }
+      __syncwarp();
+      for (int q = 0; q < 16; ++q) {
+        const int c = tc + q, i = tr + lane;
+        if (c < c1 && i < m && done[c] == 2) W[(int64_t)i + (int64_t)c * m] = tile[warp][q][lane];
+      }
+      __syncwarp();
+    }
+  }
+  group_barrier(ctr, G, gen, 200000, events + 12 * slot + 9);   // Q and W complete
+  TL(trs);
   if (nf > 0) {
     const int T = k_c + n_corr;
-    double (*As)[kLDS] = reinterpret_cast<double (*)[kLDS]>(vsh);             // [16][kLDS]
-    double (*Bs)[kLDS] = reinterpret_cast<double (*)[kLDS]>(vsh + 16 * kLDS);  // [16][kLDS]
+    // two cp.async stages of A (Q^T rows) and B (original columns) tiles
+    double (*As)[16][kLDS] = reinterpret_cast<double (*)[16][kLDS]>(vsh);               // [2][16][kLDS]
+    double (*Bs)[16][kLDS] = reinterpret_cast<double (*)[16][kLDS]>(vsh + 2 * 16 * kLDS);  // [2][16][kLDS]
     double (*Cs)[65] = reinterpret_cast<double (*)[65]>(vsh);                 // [64][65] (epilogue)
     const int wm = warp >> 2, wn = warp & 3;
     for (int ct = 0; ct < nf; ct += 64) {
@@ -609,9 +871,13 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
         if (ct + tid < nf) {
           double* base;
           int64_t stride;
-          pool_col(flist[rank + G * (ct + tid)], base, stride);
+          const int c = flist[rank + G * (ct + tid)];
+          pool_col(c, base, stride);
           sh.cbase[tid] = base;
           sh.cstride[tid] = stride;
+          sh.fcol[tid] = c;
+        } else {
+          sh.fcol[tid] = -1;
         }
       }
       __syncthreads();
@@ -621,35 +887,41 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
         for (int a = 0; a < 4; ++a)
 #pragma unroll
           for (int b = 0; b < 2; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
-        for (int i0 = 0; i0 < m; i0 += 16) {
-          __syncthreads();
+        auto load_stage = [&](int st, int i0) {
 #pragma unroll
           for (int r = 0; r < 4; ++r) {
             const int e = tid + r * kT;
             const int kk = e & 15, cl = e >> 4;
             const int i = i0 + kk;
-            double av = 0.0, bv2 = 0.0;
-            if (i < m) {
-              if (rt + cl < T) av = __ldcg(Q + (int64_t)i + (int64_t)(rt + cl) * m);
-              if (ct + cl < nf) bv2 = W[(int64_t)i + (int64_t)flist[rank + G * (ct + cl)] * m];
-            }
-            As[kk][cl] = av;
-            Bs[kk][cl] = bv2;
+            const bool oka = i < m && rt + cl < T;
+            cp_async8(&As[st][kk][cl], oka ? Q + (int64_t)i + (int64_t)(rt + cl) * m : Q, oka);
+            const int fc = sh.fcol[cl];
+            const bool okb = i < m && fc >= 0;
+            cp_async8(&Bs[st][kk][cl], okb ? W + (int64_t)i + (int64_t)fc * m : W, okb);
           }
+          cp_commit();
+        };
+        __syncthreads();
+        load_stage(0, 0);
+        int st = 0;
+        for (int i0 = 0; i0 < m; i0 += 16) {
+          cp_wait_all();
           __syncthreads();
+          if (i0 + 16 < m) load_stage(st ^ 1, i0 + 16);
 #pragma unroll
           for (int kq = 0; kq < 4; ++kq) {
             const int kr = kq * 4 + (lane & 3);
             double af[4], bf[2];
 #pragma unroll
-            for (int mi = 0; mi < 4; ++mi) af[mi] = As[kr][wm * 32 + mi * 8 + (lane >> 2)];
+            for (int mi = 0; mi < 4; ++mi) af[mi] = As[st][kr][wm * 32 + mi * 8 + (lane >> 2)];
 #pragma unroll
-            for (int ni = 0; ni < 2; ++ni) bf[ni] = Bs[kr][wn * 16 + ni * 8 + (lane >> 2)];
+            for (int ni = 0; ni < 2; ++ni) bf[ni] = Bs[st][kr][wn * 16 + ni * 8 + (lane >> 2)];
 #pragma unroll
             for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
               for (int ni = 0; ni < 2; ++ni) dmma(acc[mi][ni][0], acc[mi][ni][1], af[mi], bf[ni]);
           }
+          st ^= 1;
         }
         __syncthreads();
 #pragma unroll
@@ -672,6 +944,7 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
       }
     }
   }
+  TL(tg);
   // ---- write back (non-frozen columns): new slot s < n_fine <- R row
   //      k_c + s (only s < n_corr are read later); slot n_fine + t <- R row t
   __syncthreads();
@@ -708,6 +981,14 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
   }
   if (tid == 0 && nf > 0)
     atomicAdd(reinterpret_cast<unsigned long long*>(events + 12 * slot + 11), (unsigned long long)nf);
+  TL(twb);
+#ifdef SPAND_RRQR_PHASES
+  if (lane == 0 && warp == 0 && m >= 1000 && (rank == 0 || rank == G / 2))
+    printf("[rrqr phases] p %d m %d n %d G %d rank %d k %d nf %d act-steps %lld | kcycles: cand %lld pivcol %lld refl %lld colpass %lld publish %lld barrier %lld | Q %lld restore %lld frozen-gemm %lld writeback %lld\n",
+           p, m, n, G, rank, k_stop, nf, nact_sum, ph_t[0] / 1000, ph_t[1] / 1000, ph_t[2] / 1000,
+           ph_t[3] / 1000, ph_t[4] / 1000, ph_t[5] / 1000, tq / 1000, trs / 1000, tg / 1000,
+           twb / 1000);
+#endif
   if (rank == 0 && tid == 0) {
     int64_t* ev = events + 12 * slot;
     ev[0] = p;

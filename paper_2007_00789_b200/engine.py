@@ -120,15 +120,43 @@ class NativePlan:
         return prog, lau.reshape(-1, 16)[:self.n_launch]
 
     def _decode_meta(self):
+        """Block arrays (needed by every factorization); the per-level
+        records are decoded lazily (tools and structural tests only)."""
         meta = np.zeros(max(self.meta_len, 1), dtype=np.int64)
         self._lib.spand_plan_meta(self.h, self._vp(meta))
-        ncl, nb, nlev, nfin, nfinb = (int(x) for x in meta[:5])
+        ncl, nb = (int(x) for x in meta[:2])
         i = 9
         self.bi = meta[i:i + nb]; i += nb
         self.bj = meta[i:i + nb]; i += nb
         self.boff = meta[i:i + nb]; i += nb
         self.elim_linv = meta[i:i + ncl]; i += ncl
-        self.bid = {(int(x), int(y)): k for k, (x, y) in enumerate(zip(self.bi, self.bj))}
+        self._meta, self._meta_at, self._recs = meta, i, None
+
+    @property
+    def bid(self):
+        return {(int(x), int(y)): k for k, (x, y) in enumerate(zip(self.bi, self.bj))}
+
+    @property
+    def level_recs(self):
+        if self._recs is None:
+            self._decode_levels()
+        return self._recs
+
+    @property
+    def final(self):
+        if self._recs is None:
+            self._decode_levels()
+        return self._final
+
+    @property
+    def final_blocks(self):
+        if self._recs is None:
+            self._decode_levels()
+        return self._final_blocks
+
+    def _decode_levels(self):
+        meta, i = self._meta, self._meta_at
+        nlev, nfin, nfinb = (int(x) for x in meta[2:5])
         m = meta.tolist()
         recs = []
         for _ in range(nlev):
@@ -143,9 +171,9 @@ class NativePlan:
                 act.append((p, wv, lo, li, qo, sl, tuple(m[i:i + nn]))); i += nn
             recs.append({"level": level, "skipped": bool(skipped), "elim": elim,
                          "active": act, "nwaves": nwaves})
-        self.level_recs = recs
-        self.final = m[i:i + nfin]; i += nfin
-        self.final_blocks = m[i:i + nfinb]
+        self._recs = recs
+        self._final = m[i:i + nfin]; i += nfin
+        self._final_blocks = m[i:i + nfinb]
 
 
 class Engine:
@@ -178,22 +206,51 @@ class Engine:
         ctr = t.zeros(max(sym.n_ctr, 1), dtype=t.int32, device=d)
         pb, fb = pool.data_ptr(), fac.data_ptr()
         temp = t.empty(max(sym.temp_bound, 1), dtype=t.float64, device=d)
-        sym.emit(pb, fb, temp.data_ptr(), ctr.data_ptr())
-        assert sym.temp_size <= sym.temp_bound, (sym.temp_size, sym.temp_bound)
-        prog, launches = sym.program()
-        self.timings["plan_s"] = time.perf_counter() - tstart
-        progd = to_dev_async(prog)
-        base = progd.data_ptr()
         st = stream()
         gm0, goff = ptr(geo.m0), ptr(geo.off)
         ib, evb = self.info.data_ptr(), self.events.data_ptr()
         import ctypes
+        lib = sym._lib
+        vp = sym._vp
+        # incremental emission: level l + 1 is planned on the host while the
+        # device runs level l (all launches are asynchronous)
+        lib.spand_plan_emit_begin.argtypes = [ctypes.c_void_p] + [ctypes.c_int64] * 4
+        lib.spand_plan_emit_next.argtypes = [ctypes.c_void_p, ctypes.c_void_p]
+        lib.spand_plan_chunk.argtypes = [ctypes.c_void_p] * 3
+        lib.spand_plan_emit_begin(sym.h, pb, fb, temp.data_ptr(), ctr.data_ptr())
+        sizes = np.zeros(3, dtype=np.int64)
+        keep = []
+        t_plan = 0.0
+        while True:
+            tp = time.perf_counter()
+            more = lib.spand_plan_emit_next(sym.h, vp(sizes))
+            plen, nlau, used = (int(x) for x in sizes)
+            if nlau:
+                prog = np.empty(max(plen, 1), dtype=np.int64)
+                launches = np.empty((nlau, 16), dtype=np.int64)
+                lib.spand_plan_chunk(sym.h, vp(prog), vp(launches))
+            t_plan += time.perf_counter() - tp
+            if nlau:
+                progd = to_dev_async(prog)
+                keep.append(progd)
+                self._launch(launches, progd.data_ptr(), gm0, goff, ib, evb, fb, st)
+            if not more:
+                break
+        assert used <= sym.temp_bound, (used, sym.temp_bound)
+        self.timings["plan_s"] = t_plan
+        self._keep_run = (temp, ctr, keep)
+        t.cuda.synchronize()
+        self.timings["device_s"] = time.perf_counter() - tstart
+
+    def _launch(self, launches, base, gm0, goff, ib, evb, fb, st):
+        import ctypes
+        t = self.t
         P = lambda off: ctypes.c_void_p(base + 8 * int(off))  # noqa: E731
         for rec in launches:
             typ, cnt, ao, bo, co, x0, x1, x2 = (int(v) for v in rec[:8])
             if typ == 1:
                 _lib.call("spand_potrf_batched", cnt, P(ao), gm0, goff,
-                          ctypes.c_void_p(ib + 4 * x0), st)
+                          ctypes.c_void_p(ib), x0, x1, st)
             elif typ == 2:
                 _lib.call("spand_trtri_tiles", cnt, P(ao), gm0, goff, st)
             elif typ == 3:
@@ -219,9 +276,6 @@ class Engine:
                           x1, ctypes.c_void_p(fb + 8 * x2), st)
             else:
                 raise RuntimeError(f"unknown launch type {typ}")
-        self._keep_run = (temp, ctr, progd)
-        t.cuda.synchronize()
-        self.timings["device_s"] = time.perf_counter() - tstart
 
     def _scatter_a(self):
         """Initial blocks from the entries of A (factorize.py:61-96).

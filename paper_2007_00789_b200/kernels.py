@@ -42,9 +42,9 @@ def potrf_batched(geo, ops, info):
     n = len(ops)
     if n == 0:
         return
-    d = _rows(ops, 7)
+    d = _rows([list(o) + [i] for i, o in enumerate(ops)], 8)
     _lib.call("spand_potrf_batched", n, ptr(d), ptr(geo.m0), ptr(geo.off),
-              ptr(info), stream())
+              ptr(info), 0, 0, stream())
 
 
 def trtri_batched(geo, pairs, sizes=None):

@@ -106,3 +106,25 @@ def test_factorize_matches_reference(tag):
     x, rep = sp.pcg(a, arr["b"], m=f.apply_m, tol=rec["tol"])
     assert abs(rep.n_cg - rec["n_cg"]) <= 1
     assert rep.converged == rec["converged"]
+
+
+def test_not_spd_pivot_in_large_block():
+    """A shifted 3D Laplacian (lambda_min < shift < the subdomains'
+    lambda_min) first fails in the 400-dof top separator, which goes through
+    the blocked multi-CTA Cholesky; the reported pivot (within the block)
+    must be the reference's (factorize.py:131-163 -> dense.py:53-55)."""
+    import paper_2007_00789_b200 as sp
+    from oracle import spand_oracle as orc
+    a0 = sp.laplacian_3d(20)
+    rows = np.repeat(np.arange(a0.n), np.diff(a0.row_ptr))
+    vals = a0.values.copy()
+    vals[rows == a0.col_idx] -= 0.08
+    a = sp.SparseSymMatrix(a0.n, a0.row_ptr.copy(), a0.col_idx.copy(), vals)
+    h = sp.build_hierarchy(a, 3)
+    assert max(c.dofs.size for c in h.clusters) > 256
+    with pytest.raises(sp.NotSPD) as mine:
+        sp.factorize(a, h, 0.0, "first", skip_levels=4)
+    cl = [(c.id, c.dofs, c.depth) for c in h.clusters]
+    with pytest.raises(orc.OracleNotSPD) as ref:
+        orc.factorize(a.n, a.row_ptr, a.col_idx, a.values, cl, 3, 0.0, "first", 4)
+    assert mine.value.pivot == ref.value.pivot
