@@ -237,6 +237,75 @@ __device__ void colpass_batch(const ColCtx& X, int a0, int nb, Sh& sh, double& b
   }
 }
 
+// short columns (len <= 256): a warp per column, U columns in flight per
+// warp, warp reductions only; lane u applies the norm logic of column u and
+// keeps its best candidate (reduced per warp afterwards)
+template <int U>
+__device__ void colpass_warp(const ColCtx& X, int nact, double& bv, int64_t& bp, int& bc) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int a0 = warp * U; a0 < nact; a0 += kWarps * U) {
+    int cs[U];
+    double x[U][8];
+#pragma unroll
+    for (int u = 0; u < U; ++u) cs[u] = a0 + u < nact ? X.list[X.rank + X.G * (a0 + u)] : -1;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const double* col = X.W + (int64_t)(cs[u] < 0 ? 0 : cs[u]) * X.m + X.k;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const int i = lane + 32 * e;
+        x[u][e] = (cs[u] >= 0 && i < X.len) ? col[i] : 0.0;
+      }
+    }
+    double d[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      double a = 0.0;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const int i = lane + 32 * e;
+        if (i < X.len) a += X.v[i] * x[u][e];
+      }
+      d[u] = warp_sum(a);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const double w = X.tau * d[u];
+      double* col = X.W + (int64_t)(cs[u] < 0 ? 0 : cs[u]) * X.m + X.k;
+      double tail = 0.0, rk = 0.0;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const int i = lane + 32 * e;
+        if (cs[u] >= 0 && i < X.len) {
+          const double y = x[u][e] - w * X.v[i];
+          col[i] = y;
+          if (i == 0) rk = y;
+          else tail += y * y;
+        }
+      }
+      tail = warp_sum(tail);
+      rk = __shfl_sync(0xffffffffu, rk, 0);
+      if (lane == u && cs[u] >= 0) {
+        const int c = cs[u];
+        double cn = X.cur[c] - rk * rk;
+        if (cn < 0.0) cn = 0.0;
+        if (cn < 0.01 * X.ref[c]) {
+          cn = tail;
+          X.ref[c] = tail;
+          atomicAdd(X.refresh_ctr, 1ull);
+        }
+        X.cur[c] = cn;
+        const int64_t ps = X.pos[c];
+        if (better(cn, ps, bv, bp)) {
+          bv = cn;
+          bp = ps;
+          bc = c;
+        }
+      }
+    }
+  }
+}
+
 // columns longer than 16 rows per thread: chunked, the update re-reads
 __device__ void colpass_long(const ColCtx& X, int a0, Sh& sh, double& bv, int64_t& bp, int& bc) {
   const int tid = threadIdx.x;
@@ -398,6 +467,7 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
   if (tid == 0) {
     if (nnb <= kMaxNb) sh.nb_start[nnb] = n;
     sh.nfrz = 0;
+    sh.nact = 0;
     sh.fmax = 0ull;
   }
   __syncthreads();
@@ -696,31 +766,44 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
     bv = -1.0;
     bp = 0x7fffffffffffLL;
     bc = -1;
-    // (a) this step's active columns (list in the perm array, which is only
-    // written after the loop); freeze the ones below the threshold
+    // (a) this step's active columns: filter the previous step's list (the
+    // set only shrinks; lists ping-pong between the perm array, written only
+    // after the loop, and a spare region); freeze columns below the threshold
+    int32_t* list_out = (k & 1) ? flist + 2 * ncap : perm;
+    const int32_t* list_in = (k & 1) ? perm : flist + 2 * ncap;
+    __syncthreads();
+    const int nprev = sh.nact;
     __syncthreads();
     if (tid == 0) sh.nact = 0;
     __syncthreads();
-    for (int c = rank + G * tid; c < n; c += G * kT) {
-      if (c == j || done[c]) continue;
+    auto consider = [&](int c) {
+      if (c == j || done[c]) return;
       if (cur[c] < thr2) {
         done[c] = 2;
         flist[rank + G * atomicAdd(&sh.nfrz, 1)] = c;
         atomicMax(&sh.fmax, (unsigned long long)__double_as_longlong(cur[c]));
       } else {
-        perm[rank + G * atomicAdd(&sh.nact, 1)] = c;
+        list_out[rank + G * atomicAdd(&sh.nact, 1)] = c;
       }
+    };
+    if (k == 0) {
+      for (int c = rank + G * tid; c < n; c += G * kT) consider(c);
+    } else {
+      for (int u = tid; u < nprev; u += kT) consider(list_in[rank + G * u]);
     }
     __syncthreads();
     const int nact = sh.nact;
 #ifdef SPAND_RRQR_PHASES
     if (tid == 0) nact_sum += nact;
 #endif
-    // (c) CTA-wide batched updates
+    // (b) Householder updates: warp per column for short columns, CTA-wide
+    // batches for long ones
     {
-      ColCtx X{W, m, k, len, tau, vsh, cur, ref, pos, perm, rank, G,
+      ColCtx X{W, m, k, len, tau, vsh, cur, ref, pos, list_out, rank, G,
                reinterpret_cast<unsigned long long*>(events + 12 * slot + 10)};
-      if (len <= 8 * kT) {
+      if (len <= 256) {
+        colpass_warp<4>(X, nact, bv, bp, bc);
+      } else if (len <= 8 * kT) {
         for (int a0 = 0; a0 < nact; a0 += 4)
           colpass_batch<4, 8>(X, a0, min(4, nact - a0), sh, bv, bp, bc);
       } else if (len <= 16 * kT) {
@@ -730,8 +813,8 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
         for (int a0 = 0; a0 < nact; ++a0) colpass_long(X, a0, sh, bv, bp, bc);
       }
     }
-    // candidates live in lanes 0..3 of warp 0: reduce to lane 0
-    if (warp == 0) {
+    // candidates live in lanes of every warp: reduce to lane 0
+    {
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
         const double v2 = __shfl_xor_sync(0xffffffffu, bv, o);

@@ -233,7 +233,7 @@ class Engine:
             if nlau:
                 progd = to_dev_async(prog)
                 keep.append(progd)
-                self._launch(launches, progd.data_ptr(), gm0, goff, ib, evb, fb, st)
+                self._launch(launches, progd.data_ptr(), gm0, goff, ib, evb, fb, st, prog)
             if not more:
                 break
         assert used <= sym.temp_bound, (used, sym.temp_bound)
@@ -242,7 +242,7 @@ class Engine:
         t.cuda.synchronize()
         self.timings["device_s"] = time.perf_counter() - tstart
 
-    def _launch(self, launches, base, gm0, goff, ib, evb, fb, st):
+    def _launch(self, launches, base, gm0, goff, ib, evb, fb, st, prog=None):
         import ctypes
         t = self.t
         P = lambda off: ctypes.c_void_p(base + 8 * int(off))  # noqa: E731
@@ -270,7 +270,8 @@ class Engine:
                           ctypes.c_void_p(evb), st)
                 if WAVE_LOG is not None:
                     e1.record()
-                    WAVE_LOG.append((cnt, x0, x1, e0, e1))
+                    slots = [int(prog[ao + 16 * q + 10]) for q in range(cnt)] if prog is not None else []
+                    WAVE_LOG.append((cnt, x0, x1, e0, e1, slots))
             elif typ == 6:
                 _lib.call("spand_assemble_final", cnt, P(ao), x0, P(bo), gm0, goff,
                           x1, ctypes.c_void_p(fb + 8 * x2), st)

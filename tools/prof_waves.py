@@ -27,26 +27,17 @@ eng = keep["eng"]
 ev = eng.events.cpu().numpy().reshape(-1, E.EVENT_ROW)
 # event row: p, m, n, k_stop, k_c, rank_f2, n_fine, ...
 recs = []
-slot_of = {}
-for lvr in eng.sym.level_recs:
-    if lvr["skipped"]:
-        continue
-    for p, wv, lo, li, qo, sl, nb in lvr["active"]:
-        slot_of.setdefault((lvr["level"], wv), []).append(sl)
-waves = [(lvr["level"], w) for lvr in eng.sym.level_recs if not lvr["skipped"] for w in range(lvr["nwaves"])]
 tot = 0
-for (cnt, grid, vmax, e0, e1), key in zip(E.WAVE_LOG, waves):
+for (cnt, grid, vmax, e0, e1, sl) in E.WAVE_LOG:
     ms = e0.elapsed_time(e1)
     tot += ms
-    sl = slot_of.get(key, [])
     rows = ev[sl] if sl else np.zeros((0, E.EVENT_ROW), np.int64)
     m, n, ks = rows[:, 1], rows[:, 2], rows[:, 3]
-    steps_bytes = float(sum(8.0 * sum((mm - k) * max(nn - k, 0) for k in range(kk)) for mm, nn, kk in zip(m, n, ks))) if len(m) < 400 else None
-    recs.append({"level": key[0], "wave": key[1], "npanel": cnt, "grid": grid, "ms": round(ms, 3),
+    recs.append({"npanel": cnt, "grid": grid, "ms": round(ms, 3),
                  "m_max": int(m.max()) if len(m) else 0, "n_max": int(n.max()) if len(n) else 0,
-                 "ks_max": int(ks.max()) if len(ks) else 0,
-                 "frozen_frac": float(rows[:, 11].sum() / max(1, n.sum())), "sum_mn_MB": float((m * n).sum()) * 8 / 1e6,
-                 "one_read_GBs": (steps_bytes / (ms / 1000) / 1e9) if steps_bytes else None})
-print(json.dumps({"rrqr_total_ms": tot, "waves": len(recs)}))
-for r in sorted(recs, key=lambda r: -r["ms"])[:40]:
+                 "ks_max": int(ks.max()) if len(ks) else 0, "ks_sum": int(ks.sum()),
+                 "frozen_frac": float(rows[:, 11].sum() / max(1, n.sum())),
+                 "sum_mn_MB": float((m * n).sum()) * 8 / 1e6})
+print(json.dumps({"rrqr_total_ms": tot, "launches": len(recs)}))
+for r in sorted(recs, key=lambda r: -r["ms"])[:45]:
     print(json.dumps(r))
