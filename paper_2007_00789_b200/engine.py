@@ -43,6 +43,7 @@ from .schemes import (Elimination, ErrorCorrection, MatView, Orthogonal,
                       Scaling)
 
 import os as _os
+from collections.abc import Sequence
 
 WAVE_LOG = None      # set to [] to record per-wave CUDA events (profiling)
 EVENT_ROW = 12
@@ -336,44 +337,18 @@ class Engine:
                                                       SCHEME_CODE[self.scheme]))
         self.collected = Collected(lib, ch, vp)
         col = self.collected
-        pool, fac = self.pool, self.facbuf
-        dofs = sym.dofs
-        perm_c = np.concatenate(dofs) if dofs else np.empty(0, np.int64)
-        ops = []
-        segs = col.segs
-        for row in col.ops:
-            kind, c, li, wv, doff, size, _, lo, ld, linv, qo, rot, sb, se, lo_fac, _ = (
-                int(x) for x in row)
-            if kind == 0:
-                srows = segs[sb:se]
-                op = Elimination(
-                    dofs[c][doff:doff + size], _wd(dofs, srows),
-                    MatView(pool, lo, ld, size, size), _pv(pool, srows, 0),
-                    linv=MatView(fac, linv, ld, size, size))
-            elif kind == 1:
-                op = Scaling(dofs[c][doff:doff + size], MatView(fac, lo, ld, size, size),
-                             linv=MatView(fac, linv, ld, size, size))
-            elif kind == 2:
-                op = Orthogonal(dofs[c][doff:doff + size],
-                                MatView(fac, qo, max(ld, 1), size, size, rot=rot))
-            elif kind == 3:
-                srows = segs[sb:se]
-                op = ErrorCorrection(dofs[c][doff:doff + size], _wd(dofs, srows),
-                                     _pv(pool, srows, 1))
-            else:
-                op = Elimination(perm_c[col.fidx], np.empty(0, np.int64),
-                                 MatView(fac, lo, ld, size, size), [],
-                                 linv=MatView(fac, linv, ld, size, size))
-            ops.append(op)
+        ops = LazyOps(col, sym.dofs, self.pool, self.facbuf)
         # diagnostics (factorize.py:331-356) + margins of every decision
         diags = []
         by_level = {}
-        for d in col.diag:
-            li, p, mp, kc, rf2, eb, rb, ks, nc, _ = (int(x) for x in d)
+        dv = col.diag.copy()
+        etas = dv[:, 5].view(np.float64).tolist()
+        r11s = dv[:, 6].view(np.float64).tolist()
+        for q, d in enumerate(col.diag.tolist()):
+            li, p, mp, kc, rf2, eb, rb, ks, nc, _ = d
             by_level.setdefault(li, []).append({
                 "cluster": p, "size_before": mp, "size_after": kc, "rank_f2": rf2,
-                "eta_stop": float(np.int64(eb).view(np.float64)),
-                "r11": float(np.int64(rb).view(np.float64)), "k_stop": ks,
+                "eta_stop": etas[q], "r11": r11s[q], "k_stop": ks,
                 "n_cols": nc})
         for li, (lvl, nint, ndofs, skipped) in enumerate(col.lsum.tolist()):
             faces = by_level.get(li, [])
@@ -409,6 +384,58 @@ class Engine:
         out = t.zeros(rows.shape[0], dtype=t.int64, device=dev())
         _lib.call("spand_count_nonzero", rows.shape[0], ptr(vd), ptr(out), stream())
         return int(out.sum().item())
+
+
+class LazyOps(Sequence):
+    """The factor's operator list, built on access from the native
+    collector's tables (the device apply and nnz never need the Python
+    objects; tests, save_factor and user code get them on demand)."""
+
+    def __init__(self, col, dofs, pool, fac):
+        self.col, self.dofs, self.pool, self.fac = col, dofs, pool, fac
+        self._rows = col.ops
+        self._cache = {}
+        self._perm_c = None
+
+    def __len__(self):
+        return self._rows.shape[0]
+
+    def __getitem__(self, i):
+        if isinstance(i, slice):
+            return [self[j] for j in range(*i.indices(len(self)))]
+        if i < 0:
+            i += len(self)
+        if not 0 <= i < len(self):
+            raise IndexError(i)
+        op = self._cache.get(i)
+        if op is None:
+            op = self._cache[i] = self._build(i)
+        return op
+
+    def _build(self, i):
+        kind, c, li, wv, doff, size, _, lo, ld, linv, qo, rot, sb, se, lo_fac, _ = \
+            self._rows[i].tolist()
+        dofs, pool, fac, segs = self.dofs, self.pool, self.fac, self.col.segs
+        if kind == 0:
+            srows = segs[sb:se]
+            return Elimination(dofs[c][doff:doff + size], _wd(dofs, srows),
+                               MatView(pool, lo, ld, size, size), _pv(pool, srows, 0),
+                               linv=MatView(fac, linv, ld, size, size))
+        if kind == 1:
+            return Scaling(dofs[c][doff:doff + size], MatView(fac, lo, ld, size, size),
+                           linv=MatView(fac, linv, ld, size, size))
+        if kind == 2:
+            return Orthogonal(dofs[c][doff:doff + size],
+                              MatView(fac, qo, max(ld, 1), size, size, rot=rot))
+        if kind == 3:
+            srows = segs[sb:se]
+            return ErrorCorrection(dofs[c][doff:doff + size], _wd(dofs, srows),
+                                   _pv(pool, srows, 1))
+        if self._perm_c is None:
+            self._perm_c = np.concatenate(dofs) if dofs else np.empty(0, np.int64)
+        return Elimination(self._perm_c[self.col.fidx], np.empty(0, np.int64),
+                           MatView(fac, lo, ld, size, size), [],
+                           linv=MatView(fac, linv, ld, size, size))
 
 
 def _wd(dofs, srows):
