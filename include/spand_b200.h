@@ -143,11 +143,15 @@ int spand_copy_batched(int ntask, const int64_t* ops, const int32_t* m0,
  * segment row (14 int64): {A operand(7), B operand(7)}; A is M x K; B is N x K
  * (bT = 1: op(B) = B^T, "NT") or K x N (bT = 0, "NN").
  * tile (1 int64, packed): target << 32 | (i0 / 64) << 16 | (j0 / 64); tile 64 x 64.
- * lower_only: skip tiles strictly above the diagonal (SYRK use). */
+ * lower_only: skip tiles strictly above the diagonal (SYRK use).
+ * tri: triangular operands (zero above their diagonal) bound the K range of a
+ * tile at (i0, j0): 1 A lower -> k < i0 + 64; 2 B lower and bT = 1 ->
+ * k < j0 + 64; 4 B lower and bT = 0 -> k >= j0 (TRSM/TRMM as GEMM at the
+ * triangular flop count). */
 int spand_gemm_grouped(int ntile, const int64_t* tiles, const int64_t* targets,
                        const int64_t* segs, const int32_t* m0,
                        const int32_t* off, double alpha, double beta, int bT,
-                       int lower_only, void* stream);
+                       int lower_only, int tri, void* stream);
 
 /* One wave of the batched early-stopping column-pivoted Householder QR of
  * interface panels (restates dense.py:117-222, schemes.py:272-318,

@@ -38,7 +38,7 @@ __global__ void __launch_bounds__(kThreads)
 gemm_grouped_kernel(const int64_t* __restrict__ tiles, const int64_t* __restrict__ targets,
                     const int64_t* __restrict__ segs, const int32_t* __restrict__ m0,
                     const int32_t* __restrict__ off, double alpha, double beta, int bT,
-                    int lower_only) {
+                    int lower_only, int tri) {
   __shared__ __align__(16) double As[2][BK][LDS];
   __shared__ __align__(16) double Bs[2][BK][LDS];
   // packed tile: target << 32 | (i0 / 64) << 16 | (j0 / 64)
@@ -59,21 +59,30 @@ gemm_grouped_kernel(const int64_t* __restrict__ tiles, const int64_t* __restrict
 #pragma unroll
     for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
 
-  // chunk iterator over (segment, k0)
+  // chunk iterator over (segment, k0).  Triangular operands (explicit
+  // inverses, zero above the diagonal) bound each segment's K range:
+  // tri & 1: A lower -> k < i0 + BM; tri & 2: B lower, C = A B^T -> k < j0 + BN;
+  // tri & 4: B lower, C = A B -> k >= j0.  The skipped products are exact zeros.
+  auto krange = [&](const Opnd& a, const Opnd& b, int& klo, int& khi) {
+    khi = a.cols;
+    const int kb = bT ? b.cols : b.rows;
+    if (kb < khi) khi = kb;
+    if ((tri & 1) && i0 + BM < khi) khi = i0 + BM;
+    if ((tri & 2) && j0 + BN < khi) khi = j0 + BN;
+    klo = (tri & 4) ? j0 : 0;
+  };
   int seg = sb, k0 = 0;
   Opnd A, B;
   int K = 0;
   auto open_seg = [&](int s) {
     A = load_opnd(segs + 14 * (int64_t)s, m0, off);
     B = load_opnd(segs + 14 * (int64_t)s + 7, m0, off);
-    K = A.cols;
-    const int kb = bT ? B.cols : B.rows;
-    if (kb < K) K = kb;
+    krange(A, B, k0, K);
   };
   // skip empty segments
   while (seg < se) {
     open_seg(seg);
-    if (K > 0) break;
+    if (K > k0) break;
     ++seg;
   }
   auto load_stage = [&](int st, const Opnd& a, const Opnd& b, int kbase, int kmax) {
@@ -109,22 +118,19 @@ gemm_grouped_kernel(const int64_t* __restrict__ tiles, const int64_t* __restrict
 
   if (seg < se) {
     int st = 0;
-    load_stage(0, A, B, 0, K);
+    load_stage(0, A, B, k0, K);
     while (true) {
       // advance iterator to the next chunk and prefetch it
       Opnd An = A, Bn = B;
       int Kn = K, segn = seg, kn = k0 + BK;
       bool have_next = true;
       if (kn >= Kn) {
-        kn = 0;
         ++segn;
         while (segn < se) {
           An = load_opnd(segs + 14 * (int64_t)segn, m0, off);
           Bn = load_opnd(segs + 14 * (int64_t)segn + 7, m0, off);
-          Kn = An.cols;
-          const int kb = bT ? Bn.cols : Bn.rows;
-          if (kb < Kn) Kn = kb;
-          if (Kn > 0) break;
+          krange(An, Bn, kn, Kn);
+          if (Kn > kn) break;
           ++segn;
         }
         have_next = segn < se;
@@ -178,11 +184,12 @@ gemm_grouped_kernel(const int64_t* __restrict__ tiles, const int64_t* __restrict
 extern "C" int spand_gemm_grouped(int ntile, const int64_t* tiles, const int64_t* targets,
                                   const int64_t* segs, const int32_t* m0, const int32_t* off,
                                   double alpha, double beta, int bT, int lower_only,
-                                  void* stream) {
+                                  int tri, void* stream) {
   if (ntile < 0) return -1;
   if (ntile == 0) return 0;
   gemm_grouped_kernel<<<ntile, kThreads, 0, as_stream(stream)>>>(tiles, targets, segs, m0, off,
-                                                                 alpha, beta, bT, lower_only);
+                                                                 alpha, beta, bT, lower_only,
+                                                                 tri);
   SPAND_CHECK_LAUNCH();
   return 0;
 }

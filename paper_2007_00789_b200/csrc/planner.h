@@ -255,7 +255,10 @@ struct Plan {
     std::vector<int64_t> segs;       // 14 per segment
     int64_t mm, nn;
   };
-  void gemm(const std::vector<Target>& ts, double alpha, double beta, int bT, int lower) {
+  // tri: triangular-operand K bounds (gemm.cu): 1 A lower, 2 B lower with
+  // C = A B^T, 4 B lower with C = A B
+  void gemm(const std::vector<Target>& ts, double alpha, double beta, int bT, int lower,
+            int tri = 0) {
     if (ts.empty()) return;
     std::vector<int64_t> trow, srow, tiles;
     int64_t nseg = 0;
@@ -275,7 +278,7 @@ struct Plan {
     if (dry || tiles.empty()) return;
     if (srow.empty()) srow.assign(14, 0);
     const int64_t a = push(tiles), b = push(trow), c = push(srow);
-    launch(3, (int64_t)tiles.size(), a, b, c, bT, lower, 0, alpha, beta);
+    launch(3, (int64_t)tiles.size(), a, b, c, bT, lower, tri, alpha, beta);
   }
 
   // batched triangular inverses: 64-tiles + recursive doubling GEMMs
@@ -322,8 +325,8 @@ struct Plan {
           g2.push_back(b);
         }
       }
-      gemm(g1, 1.0, 0.0, 0, 0);
-      gemm(g2, -1.0, 0.0, 0, 0);
+      gemm(g1, 1.0, 0.0, 0, 0, 4);    // tmp = L21 X11 (X11 lower)
+      gemm(g2, -1.0, 0.0, 0, 0, 1);   // X21 = -X22 tmp (X22 lower)
     }
   }
   int64_t m0v(int64_t c) const { return c < ncl ? m0[c] : fcap; }
@@ -393,7 +396,7 @@ struct Plan {
         launch(1, (int64_t)diag.size() / 8, push(diag), 0, 0, o, 1);
         launch(2, (int64_t)tri.size() / 14, push(tri));
         if (!cps.empty()) launch(4, (int64_t)cps.size() / 15, push(cps));
-        gemm(pan, 1.0, 0.0, 1, 0);      // L21 = A21 L11^-T
+        gemm(pan, 1.0, 0.0, 1, 0, 2);   // L21 = A21 L11^-T
         gemm(trail, -1.0, 1.0, 1, 1);   // A22 -= L21 L21^T (lower tiles)
       }
       // zero the strict upper triangles (dpotrf clean, dense.py:53)
@@ -498,7 +501,7 @@ struct Plan {
           }
         }
         temp_size = std::max(temp_size, acc);
-        gemm(tg, 1.0, 0.0, 1, 0);
+        gemm(tg, 1.0, 0.0, 1, 0, 2);    // panel L_s^-T
         if (!cps.empty()) launch(4, (int64_t)cps.size() / 15, push(cps));
         // grouped Schur / fill update: off-diagonal targets, then diagonal
         // ones (lower tiles only: potrf reads the lower triangle)
@@ -575,8 +578,8 @@ struct Plan {
           acc += m0[i] * m0[j];
         }
         temp_size = std::max(temp_size, acc);
-        gemm(g1, 1.0, 0.0, 0, 0);   // T = Z_i^-1 B
-        gemm(g2, 1.0, 0.0, 1, 0);   // B = T Z_j^-T
+        gemm(g1, 1.0, 0.0, 0, 0, 1);   // T = Z_i^-1 B
+        gemm(g2, 1.0, 0.0, 1, 0, 2);   // B = T Z_j^-T
       }
       // sparsify, wave by wave (factorize.py:323-340)
       for (int wv = 0; wv < L.nwaves; ++wv) {

@@ -258,7 +258,7 @@ class Engine:
                 alpha = float(np.int64(rec[8]).view(np.float64))
                 beta = float(np.int64(rec[9]).view(np.float64))
                 _lib.call("spand_gemm_grouped", cnt, P(ao), P(bo), P(co), gm0, goff,
-                          alpha, beta, x0, x1, st)
+                          alpha, beta, x0, x1, x2, st)
             elif typ == 4:
                 _lib.call("spand_copy_batched", cnt, P(ao), gm0, goff, st)
             elif typ == 5:

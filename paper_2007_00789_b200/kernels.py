@@ -92,8 +92,8 @@ def trtri_batched(geo, pairs, sizes=None):
                 g2.append((_sub(x, o + s, o, s, s),
                            [(_sub(x, o + s, o + s, s, s), _sub(tmp, o + s, o, s, s))],
                            (s, s)))
-        gemm_grouped(geo, g1, 1.0, 0.0, bT=0)
-        gemm_grouped(geo, g2, -1.0, 0.0, bT=0)
+        gemm_grouped(geo, g1, 1.0, 0.0, bT=0, tri=4)
+        gemm_grouped(geo, g2, -1.0, 0.0, bT=0, tri=1)
         s *= 2
     # `temp` may be released now: the caching allocator hands the block to
     # later allocations on this stream only, i.e. after these GEMMs
@@ -139,7 +139,7 @@ def _tile_grid(mm, nn, lower_only=False):
 
 
 def gemm_grouped(geo, targets, alpha, beta, bT, lower_only=False,
-                 max_rows=None, max_cols=None):
+                 max_rows=None, max_cols=None, tri=0):
     """targets: [(C operand, [(A operand, B operand), ...], (max_m, max_n))].
 
     Tiles are laid out for the maximal (m0-geometry) sizes; tiles beyond a
@@ -163,7 +163,7 @@ def gemm_grouped(geo, targets, alpha, beta, bT, lower_only=False,
     td, sd, tl = _rows(trow, 8), _rows(srow, 14), _rows(tiles, 1)
     _lib.call("spand_gemm_grouped", int(tiles.shape[0]), ptr(tl), ptr(td), ptr(sd),
               ptr(geo.m0), ptr(geo.off), float(alpha), float(beta), int(bT),
-              int(bool(lower_only)), stream())
+              int(bool(lower_only)), int(tri), stream())
 
 
 # ---------------------------------------------------------------------------
