@@ -201,6 +201,11 @@ int spand_nd_partition(int64_t n, const int64_t* row_ptr, const int64_t* col_idx
 void* spand_plan_create(int ncl, const int64_t* m0, const int32_t* depth, int levels,
                         int skip, int64_t npairs, const int64_t* pairs, int cap_override);
 void spand_plan_destroy(void* h);
+/* cluster-pair keys of A's nonzeros (ci * ncl + cj, ci <= cj, sorted, unique);
+ * out holds nnz(A) entries; returns the count */
+int64_t spand_plan_pairs(int ncl, const int64_t* row_ptr, const int64_t* col_idx,
+                         const int64_t* cluster_of, const int64_t* cdofs, const int64_t* cptr,
+                         int64_t* out);
 int spand_plan_set_dofs(void* h, const int64_t* dofs, const int64_t* dptr);
 int spand_plan_sizes(void* h, int64_t* out);
 int spand_plan_emit(void* h, int64_t pool_base, int64_t fac_base, int64_t temp_base,

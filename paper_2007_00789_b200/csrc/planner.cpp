@@ -51,6 +51,33 @@ void* spand_plan_create(int ncl, const int64_t* m0, const int32_t* depth, int le
 
 void spand_plan_destroy(void* h) { delete static_cast<Plan*>(h); }
 
+// Cluster-pair keys (ci * ncl + cj, ci <= cj, ascending, unique) of the
+// nonzeros of A: the initial blocks of the symbolic elimination
+// (factorize.py:61-96).  cdofs/cptr: cluster dofs concatenated in id order.
+// out must hold nnz entries; returns the number of keys.
+int64_t spand_plan_pairs(int ncl, const int64_t* row_ptr, const int64_t* col_idx,
+                         const int64_t* cluster_of, const int64_t* cdofs, const int64_t* cptr,
+                         int64_t* out) {
+  std::vector<int> stamp(ncl, -1), list;
+  int64_t cnt = 0;
+  for (int ci = 0; ci < ncl; ++ci) {
+    list.clear();
+    for (int64_t u = cptr[ci]; u < cptr[ci + 1]; ++u) {
+      const int64_t r = cdofs[u];
+      for (int64_t e = row_ptr[r]; e < row_ptr[r + 1]; ++e) {
+        const int cj = (int)cluster_of[col_idx[e]];
+        if (cj >= ci && stamp[cj] != ci) {
+          stamp[cj] = ci;
+          list.push_back(cj);
+        }
+      }
+    }
+    std::sort(list.begin(), list.end());
+    for (int cj : list) out[cnt++] = (int64_t)ci * ncl + cj;
+  }
+  return cnt;
+}
+
 // cluster dofs (original numbering) concatenated in id order, dptr[ncl+1]
 int spand_plan_set_dofs(void* h, const int64_t* dofs, const int64_t* dptr) {
   Plan* p = static_cast<Plan*>(h);

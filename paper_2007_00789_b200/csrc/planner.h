@@ -52,86 +52,104 @@ struct Plan {
 
   int64_t key(int i, int j) const { return (int64_t)i * ncl + j; }
   int block(int i, int j) const { return bid.at(key(i, j)); }
-  int new_block(int i, int j, std::vector<std::set<int>>& cb) {
+  int new_block(int i, int j, std::vector<std::vector<int>>& cb) {
     const int b = (int)bi.size();
     bi.push_back(i);
     bj.push_back(j);
     bid[key(i, j)] = b;
-    cb[i].insert(b);
-    cb[j].insert(b);
+    cb[i].push_back(b);
+    if (j != i) cb[j].push_back(b);
     return b;
   }
 
+  // Symbolic elimination over the levels (factorize.py:309-362): which
+  // blocks exist, which interiors update which targets, the active sets and
+  // sparsification waves.  Adjacency and block lists use lazy deletion
+  // (eliminated clusters are filtered when read); the result is identical
+  // to the ordered-set formulation (neighbour lists are sorted on read).
   void symbolic(int64_t npairs, const int64_t* pairs) {
-    std::vector<std::set<int>> adj(ncl), cb(ncl);
+    std::vector<std::vector<int>> adj(ncl), cb(ncl);
+    bid.reserve((size_t)npairs * 4);
+    bi.reserve((size_t)npairs * 2);
+    bj.reserve((size_t)npairs * 2);
     for (int64_t t = 0; t < npairs; ++t) {
       const int i = (int)(pairs[t] / ncl), j = (int)(pairs[t] % ncl);
       new_block(i, j, cb);
       if (i != j) {
-        adj[i].insert(j);
-        adj[j].insert(i);
+        adj[i].push_back(j);
+        adj[j].push_back(i);
       }
     }
     for (int c = 0; c < ncl; ++c)
       if (!bid.count(key(c, c))) new_block(c, c, cb);
     std::vector<char> alive(ncl, 1);
+    auto live_nbrs = [&](int c) {
+      std::vector<int> nb;
+      nb.reserve(adj[c].size());
+      for (int w : adj[c])
+        if (alive[w]) nb.push_back(w);
+      std::sort(nb.begin(), nb.end());
+      adj[c] = nb;   // compact
+      return nb;
+    };
+    std::vector<int> tpos;      // block id -> target index at this level, stamped
+    std::vector<int> tstamp;
+    std::vector<int> wave_of(ncl, 0);
     for (int level = levels; level >= 1; --level) {
       Level L;
       L.level = level;
-      std::map<int, int> tindex;  // block id -> target index (order of first use)
       for (int c = 0; c < ncl; ++c)
         if (alive[c] && depth[c] == level) L.interiors.push_back(c);
       for (int s : L.interiors) {
-        std::vector<int> nb(adj[s].begin(), adj[s].end());
+        std::vector<int> nb = live_nbrs(s);
         L.inbrs.push_back(nb);
-        for (size_t a = 0; a < nb.size(); ++a)
-          for (size_t b = a; b < nb.size(); ++b) {
-            const int wa = nb[a], wb = nb[b];
+        for (size_t a2 = 0; a2 < nb.size(); ++a2)
+          for (size_t b2 = a2; b2 < nb.size(); ++b2) {
+            const int wa = nb[a2], wb = nb[b2];
             auto it = bid.find(key(wa, wb));
             int blk;
             if (it == bid.end()) {
               blk = new_block(wa, wb, cb);
               if (wa != wb) {
-                adj[wa].insert(wb);
-                adj[wb].insert(wa);
+                adj[wa].push_back(wb);
+                adj[wb].push_back(wa);
               }
             } else {
               blk = it->second;
             }
-            auto ti = tindex.find(blk);
-            if (ti == tindex.end()) {
-              tindex[blk] = (int)L.targets.size();
+            if ((int)tpos.size() <= blk) {
+              tpos.resize(bi.size() + 1024, -1);
+              tstamp.resize(bi.size() + 1024, -1);
+            }
+            if (tstamp[blk] != level) {
+              tstamp[blk] = level;
+              tpos[blk] = (int)L.targets.size();
               L.targets.push_back(blk);
               L.tsegs.push_back({s});
             } else {
-              L.tsegs[ti->second].push_back(s);
+              L.tsegs[tpos[blk]].push_back(s);
             }
           }
-        for (int w : nb) adj[w].erase(s);
-        for (int b : cb[s]) {
-          const int other = bi[b] == s ? bj[b] : bi[b];
-          if (other != s) cb[other].erase(b);
-        }
-        cb[s].clear();
-        adj[s].clear();
         alive[s] = 0;
+        adj[s].clear();
+        cb[s].clear();
       }
       L.skipped = (levels - level) < skip;
       if (!L.skipped) {
         for (int c = 0; c < ncl; ++c)
           if (alive[c]) L.active.push_back(c);
-        std::set<std::pair<int, int>> rb;
+        std::vector<std::pair<int, int>> rb;
         for (int c : L.active)
-          for (int b : cb[c])
-            if (bi[b] != bj[b]) rb.insert({bi[b], bj[b]});
+          for (int b2 : cb[c])
+            if (bi[b2] == c && bj[b2] != c && alive[bj[b2]]) rb.push_back({bi[b2], bj[b2]});
+        std::sort(rb.begin(), rb.end());
         for (auto& pr : rb) L.resc_blocks.push_back(block(pr.first, pr.second));
-        std::unordered_map<int, int> wave;
         for (int p : L.active) {
-          std::vector<int> nb(adj[p].begin(), adj[p].end());
+          std::vector<int> nb = live_nbrs(p);
           int wv = 0;
           for (int q : nb)
-            if (q < p) wv = std::max(wv, wave[q] + 1);
-          wave[p] = wv;
+            if (q < p) wv = std::max(wv, wave_of[q] + 1);
+          wave_of[p] = wv;
           L.wave.push_back(wv);
           L.anbrs.push_back(nb);
           L.nwaves = std::max(L.nwaves, wv + 1);
@@ -141,9 +159,11 @@ struct Plan {
     }
     for (int c = 0; c < ncl; ++c)
       if (alive[c]) fin.push_back(c);
-    std::set<std::pair<int, int>> fb;
+    std::vector<std::pair<int, int>> fb;
     for (int c : fin)
-      for (int b : cb[c]) fb.insert({bi[b], bj[b]});
+      for (int b2 : cb[c])
+        if (bi[b2] == c && alive[bj[b2]]) fb.push_back({bi[b2], bj[b2]});
+    std::sort(fb.begin(), fb.end());
     for (auto& pr : fb) fin_blocks.push_back(block(pr.first, pr.second));
   }
 

@@ -66,11 +66,19 @@ class NativePlan:
         self.dofs = [np.asarray(c.dofs, dtype=np.int64) for c in h.clusters]
         self.cluster_of = h.cluster_of
         self.levels = h.levels
-        rows = np.repeat(np.arange(a.n, dtype=np.int64), np.diff(a.row_ptr))
-        ci, cj = h.cluster_of[rows], h.cluster_of[a.col_idx]
-        up = ci <= cj
-        keys = np.ascontiguousarray(np.unique(ci[up] * ncl + cj[up]), dtype=np.int64)
         vp = lambda x: x.ctypes.data_as(ctypes.c_void_p)  # noqa: E731
+        dcat = np.ascontiguousarray(np.concatenate(self.dofs) if self.dofs
+                                    else np.zeros(1, np.int64), dtype=np.int64)
+        dptr = np.zeros(ncl + 1, dtype=np.int64)
+        np.cumsum(self.m0, out=dptr[1:])
+        rp = np.ascontiguousarray(a.row_ptr, dtype=np.int64)
+        cx = np.ascontiguousarray(a.col_idx, dtype=np.int64)
+        cof = np.ascontiguousarray(h.cluster_of, dtype=np.int64)
+        keys = np.empty(max(cx.size, 1), dtype=np.int64)
+        lib.spand_plan_pairs.restype = ctypes.c_int64
+        lib.spand_plan_pairs.argtypes = [ctypes.c_int] + [ctypes.c_void_p] * 6
+        npairs = lib.spand_plan_pairs(ncl, vp(rp), vp(cx), vp(cof), vp(dcat), vp(dptr), vp(keys))
+        keys = keys[:npairs]
         lib.spand_plan_create.restype = ctypes.c_void_p
         lib.spand_plan_create.argtypes = [ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p,
                                           ctypes.c_int, ctypes.c_int, ctypes.c_int64,
@@ -85,10 +93,6 @@ class NativePlan:
             keys.size, vp(keys), int(cap_override)))
         self._lib = lib
         self._vp = vp
-        dcat = np.ascontiguousarray(np.concatenate(self.dofs) if self.dofs
-                                    else np.zeros(1, np.int64), dtype=np.int64)
-        dptr = np.zeros(ncl + 1, dtype=np.int64)
-        np.cumsum(self.m0, out=dptr[1:])
         lib.spand_plan_set_dofs.argtypes = [ctypes.c_void_p] * 3
         lib.spand_plan_set_dofs(self.h, vp(dcat), vp(dptr))
         self.sizes()
