@@ -51,8 +51,16 @@ constexpr int kLDS = 68;       // frozen-column DMMA tiles (conflict-free fragme
 // dynamic shared memory floor: write-back staging (8 warps x 16 x 33) and
 // the frozen-GEMM epilogue tile (64 x 65)
 constexpr size_t kMinSmem = (size_t)4 * 16 * kLDS * sizeof(double);   // 2 stages x (A, B)
+// cold-column maintenance layout in the dynamic shared memory (doubles):
+// scratch [0, 4352) | T [32][33] | Y/Z [64][33] | R rows [64][33] | tails [64]
+constexpr int kCScr = 0, kCT = 4352, kCZ = kCT + 32 * 33, kCR2 = kCZ + 64 * 33,
+              kCTail = kCR2 + 64 * 33, kColdEnd = kCTail + 64;
+constexpr size_t kColdSmem = (size_t)kColdEnd * sizeof(double);
+constexpr int kBlk = 32;         // reflectors per cold-column block update
+constexpr double kHotRho = 0.2;  // hot iff running norm^2 >= kHotRho * pivot norm^2
 static_assert(kMinSmem >= 64 * 65 * sizeof(double), "epilogue tile");
 static_assert(kMinSmem >= (size_t)kWarps * 16 * 33 * sizeof(double), "gather tiles");
+static_assert(kColdSmem >= kMinSmem, "cold layout covers the other phases");
 
 struct Sh {
   double red[kWarps];
@@ -60,10 +68,14 @@ struct Sh {
   int64_t bpos[kWarps];
   int64_t bpc[kWarps];
   double bfm[kWarps];
+  double bcm[kWarps];
   int bq[kWarps];
   int bcol[kWarps];
   int nfrz;
   int nact;
+  int ncold;
+  double coldmax;
+  int nhot, nhot3;
   double red8[kWarps][8];   // multi-value block reductions of the column pass
   double tot8[8];
   unsigned long long fmax;   // bits of the max norm^2 of my frozen columns (>= 0)
@@ -468,6 +480,8 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
     if (nnb <= kMaxNb) sh.nb_start[nnb] = n;
     sh.nfrz = 0;
     sh.nact = 0;
+    sh.ncold = 0;
+    sh.coldmax = -1.0;
     sh.fmax = 0ull;
   }
   __syncthreads();
@@ -605,6 +619,7 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
       rec[0] = vv;
       reinterpret_cast<int64_t*>(rec)[1] = (pp << 32) | (int64_t)(uint32_t)cc;
       rec[2] = __longlong_as_double((long long)sh.fmax);
+      rec[3] = sh.coldmax;
     }
     __syncthreads();
   };
@@ -627,27 +642,303 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
   int k = 0;
 #ifdef SPAND_RRQR_PHASES
   long long ph_t[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  long long ph_last = clock64(), nact_sum = 0;
+  long long ph_last = clock64(), nact_sum = 0, hot_sum = 0, hot3_sum = 0;
+  if (tid == 0) sh.nhot = sh.nhot3 = 0;
   int ph_cur = 7;
 #define PH(x) do { long long _n = clock64(); ph_t[ph_cur] += _n - ph_last; ph_last = _n; ph_cur = (x); } while (0)
 #else
 #define PH(x) do {} while (0)
 #endif
+  // ---- hot / cold columns.  Only columns whose running norm^2 is within
+  // kHotRho of the current pivot value are updated every step (HOT); the
+  // others (COLD) cannot be the next pivots and are brought up to date every
+  // kBlk steps with the blocked reflectors Q_b^T X = X - V T^T V^T X (two
+  // tensor-core products), their running norms replayed step by step with the
+  // reference's downdate / refresh rule (exact tail norms are suffix sums of
+  // the updated column).  Each step checks that no cold column's (stale,
+  // larger) norm reaches the pivot value; if one does, the block ends early
+  // and every cold column becomes hot.
+  int32_t* coldA = flist + 4 * ncap;
+  int32_t* coldB = flist + 6 * ncap;
+  int32_t* coldl = coldA;
+  auto pass1 = [&](int na, auto colp, auto alo, int ka, int nb) {
+    // ZT[a][q] = sum_{i >= ka} A_a[i] V[i, ka + q]  (64 x 32 tile on DMMA)
+    double (*As)[16][kLDS] = reinterpret_cast<double (*)[16][kLDS]>(vsh + kCScr);
+    double (*Bs)[16][36] = reinterpret_cast<double (*)[16][36]>(vsh + kCScr + 2 * 16 * kLDS);
+    double (*ZT)[33] = reinterpret_cast<double (*)[33]>(vsh + kCZ);
+    const int wm = warp >> 2, wn = warp & 3;
+    double acc[4][2];
+#pragma unroll
+    for (int a = 0; a < 4; ++a) acc[a][0] = acc[a][1] = 0.0;
+    auto stage = [&](int st, int i0) {
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const int e = tid + r * kT;
+        const int kk = e & 15, a = e >> 4;
+        const int i = i0 + kk;
+        const bool ok = a < na && i < m && i >= alo(a);
+        cp_async8(&As[st][kk][a], ok ? colp(a) + i : W, ok);
+      }
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        const int e = tid + r * kT;
+        const int kk = e & 15, q = e >> 4;
+        const int i = i0 + kk;
+        const bool ok = q < nb && i < m && i >= ka + q;
+        cp_async8(&Bs[st][kk][q], ok ? V + (int64_t)i + (int64_t)(ka + q) * m : V, ok);
+      }
+      cp_commit();
+    };
+    __syncthreads();
+    stage(0, ka);
+    int st = 0;
+    for (int i0 = ka; i0 < m; i0 += 16) {
+      cp_wait_all();
+      __syncthreads();
+      if (i0 + 16 < m) stage(st ^ 1, i0 + 16);
+#pragma unroll
+      for (int kq = 0; kq < 4; ++kq) {
+        const int kr = kq * 4 + (lane & 3);
+        const double bf = Bs[st][kr][wn * 8 + (lane >> 2)];
+#pragma unroll
+        for (int mi = 0; mi < 4; ++mi)
+          dmma(acc[mi][0], acc[mi][1], As[st][kr][wm * 32 + mi * 8 + (lane >> 2)], bf);
+      }
+      st ^= 1;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+        ZT[wm * 32 + mi * 8 + (lane >> 2)][wn * 8 + (lane & 3) * 2 + h] = acc[mi][h];
+    __syncthreads();
+  };
+  auto cold_maint = [&](int ka, int kb) {
+    const int nb = kb - ka;
+    const int nc = sh.ncold;
+    if (nb <= 0 || nc == 0) return;
+    double (*TT)[33] = reinterpret_cast<double (*)[33]>(vsh + kCT);
+    double (*ZT)[33] = reinterpret_cast<double (*)[33]>(vsh + kCZ);
+    double (*RK)[33] = reinterpret_cast<double (*)[33]>(vsh + kCR2);
+    double* TAIL = vsh + kCTail;
+    const int wm = warp >> 2, wn = warp & 3;
+    // T of Q_b = H_ka ... H_{kb-1} = I - V T V^T (dlarft, forward columnwise)
+    pass1(nb, [&](int a) { return (const double*)(V + (int64_t)(ka + a) * m); },
+          [&](int a) { return ka + a; }, ka, nb);
+    if (warp == 0) {
+      for (int jj = 0; jj < nb; ++jj) {
+        const double tj = __ldcg(taus + ka + jj);
+        double v = 0.0;
+        if (lane < jj) {
+          for (int c = lane; c < jj; ++c) v += TT[lane][c] * ZT[c][jj];
+          v *= -tj;
+        }
+        __syncwarp();
+        if (lane < jj) TT[lane][jj] = v;
+        else if (lane == jj) TT[jj][jj] = tj;
+        else TT[lane][jj] = 0.0;
+        __syncwarp();
+      }
+    }
+    __syncthreads();
+    for (int ct = 0; ct < nc; ct += 64) {
+      const int ncl = min(64, nc - ct);
+      if (tid < 64) sh.fcol[tid] = tid < ncl ? coldl[rank + G * (ct + tid)] : -1;
+      __syncthreads();
+      // Y^T = X^T V, then Z^T = Y^T T
+      pass1(ncl, [&](int a) { return (const double*)(W + (int64_t)sh.fcol[a] * m); },
+            [&](int a) { return ka; }, ka, nb);
+      double zv[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int e = tid + kT * u;
+        const int c = e >> 5, q = e & 31;
+        double z = 0.0;
+        if (c < ncl && q < nb)
+          for (int pp = 0; pp <= q; ++pp) z += ZT[c][pp] * TT[pp][q];
+        zv[u] = z;
+      }
+      __syncthreads();
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int e = tid + kT * u;
+        ZT[e >> 5][e & 31] = zv[u];
+      }
+      if (tid < 64) TAIL[tid] = 0.0;
+      __syncthreads();
+      // X -= V Z, 64-row tiles; rows ka..kb-1 captured, sums of squares below
+      for (int r0 = ka; r0 < m; r0 += 64) {
+        double (*As2)[kLDS] = reinterpret_cast<double (*)[kLDS]>(vsh + kCScr);   // [32][68]
+        for (int e = tid; e < 32 * 64; e += kT) {
+          const int q = e >> 6, r = e & 63, i = r0 + r;
+          const bool ok = q < nb && i < m && i >= ka + q;
+          As2[q][r] = ok ? __ldcg(V + (int64_t)i + (int64_t)(ka + q) * m) : 0.0;
+        }
+        __syncthreads();
+        double acc[4][2][2];
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int b = 0; b < 2; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+        for (int kq = 0; kq < (nb + 3) / 4; ++kq) {
+          const int kr = kq * 4 + (lane & 3);
+          double af[4], bf[2];
+#pragma unroll
+          for (int mi = 0; mi < 4; ++mi) af[mi] = As2[kr][wm * 32 + mi * 8 + (lane >> 2)];
+#pragma unroll
+          for (int ni = 0; ni < 2; ++ni) bf[ni] = ZT[wn * 16 + ni * 8 + (lane >> 2)][kr];
+#pragma unroll
+          for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+            for (int ni = 0; ni < 2; ++ni) dmma(acc[mi][ni][0], acc[mi][ni][1], af[mi], bf[ni]);
+        }
+        __syncthreads();
+        double (*Xt)[65] = reinterpret_cast<double (*)[65]>(vsh + kCScr);   // [64][65]
+        for (int e = tid; e < 64 * 64; e += kT) {
+          const int r = e & 63, cl = e >> 6, i = r0 + r;
+          Xt[cl][r] = (cl < ncl && i < m) ? W[(int64_t)i + (int64_t)sh.fcol[cl] * m] : 0.0;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+          for (int ni = 0; ni < 2; ++ni)
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+              Xt[wn * 16 + ni * 8 + (lane & 3) * 2 + h][wm * 32 + mi * 8 + (lane >> 2)] -=
+                  acc[mi][ni][h];
+        __syncthreads();
+        for (int e = tid; e < 64 * 64; e += kT) {
+          const int r = e & 63, cl = e >> 6, i = r0 + r;
+          if (cl < ncl && i < m) W[(int64_t)i + (int64_t)sh.fcol[cl] * m] = Xt[cl][r];
+        }
+        if (tid < ncl) {
+          double sq = 0.0;
+          for (int r = 0; r < 64 && r0 + r < m; ++r) {
+            const int i = r0 + r;
+            const double xv = Xt[tid][r];
+            if (i < kb) RK[tid][i - ka] = xv;
+            else sq += xv * xv;
+          }
+          TAIL[tid] += sq;
+        }
+        __syncthreads();
+      }
+      // replay the running norms of the block's steps (dense.py:168-178):
+      // the exact tail at step t is the suffix norm of the updated column
+      if (tid < ncl) {
+        const int c = sh.fcol[tid];
+        double suf = TAIL[tid];
+        for (int t = kb - 1; t >= ka; --t) {
+          ZT[tid][t - ka] = suf;
+          suf += RK[tid][t - ka] * RK[tid][t - ka];
+        }
+        double cn = cur[c], rf = ref[c];
+        for (int t = ka; t < kb; ++t) {
+          const double rk = RK[tid][t - ka];
+          double d = cn - rk * rk;
+          if (d < 0.0) d = 0.0;
+          if (d < 0.01 * rf) {
+            d = ZT[tid][t - ka];
+            rf = d;
+            atomicAdd(reinterpret_cast<unsigned long long*>(events + 12 * slot + 10), 1ull);
+          }
+          cn = d;
+        }
+        cur[c] = cn;
+        ref[c] = rf;
+      }
+      __syncthreads();
+    }
+  };
+  int k0 = 0, maint = 0, cpar = 0;
+  double last_wv = 0.0;
   while (k < kmax) {
     PH(0);
+    if (maint) {
+      // bring the cold columns up to date (reflectors k0..k-1), then either
+      // reclassify (block end) or make every column hot (a cold column could
+      // have won), and republish this CTA's candidate
+      int32_t* hot_in = (k & 1) ? perm : flist + 2 * ncap;
+      int32_t* tmpl = flist + 8 * ncap;
+      cold_maint(k0, k);
+      const int nh = sh.nact, ncd = sh.ncold;
+      __syncthreads();
+      if (tid == 0) {
+        sh.nact = 0;
+        sh.ncold = 0;
+        sh.coldmax = 0.0;   // bits of a non-negative max (atomicMax below)
+      }
+      __syncthreads();
+      int32_t* cold_out = (coldl == coldA) ? coldB : coldA;
+      const double tau_hot = (maint == 2) ? -1.0 : kHotRho * last_wv;
+      for (int u = tid; u < nh + ncd; u += kT) {
+        const int c = u < nh ? hot_in[rank + G * u] : coldl[rank + G * (u - nh)];
+        if (done[c]) continue;
+        if (cur[c] < thr2) {
+          done[c] = 2;
+          flist[rank + G * atomicAdd(&sh.nfrz, 1)] = c;
+          atomicMax(&sh.fmax, (unsigned long long)__double_as_longlong(cur[c]));
+        } else if (cur[c] >= tau_hot) {
+          tmpl[rank + G * atomicAdd(&sh.nact, 1)] = c;
+        } else {
+          cold_out[rank + G * atomicAdd(&sh.ncold, 1)] = c;
+          atomicMax(reinterpret_cast<unsigned long long*>(&sh.coldmax),
+                    (unsigned long long)__double_as_longlong(cur[c]));
+        }
+      }
+      __syncthreads();
+      if (sh.ncold == 0 && tid == 0) sh.coldmax = -1.0;
+      const int nh2 = sh.nact;
+      for (int u = tid; u < nh2; u += kT) hot_in[rank + G * u] = tmpl[rank + G * u];
+      coldl = cold_out;
+      k0 = k;
+      maint = 0;
+      bv = -1.0;
+      bp = 0x7fffffffffffLL;
+      bc = -1;
+      for (int u = tid; u < nh2; u += kT) {
+        const int c = tmpl[rank + G * u];
+        const double cv = cur[c];
+        const int64_t ps = pos[c];
+        if (better(cv, ps, bv, bp)) {
+          bv = cv;
+          bp = ps;
+          bc = c;
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double v2 = __shfl_xor_sync(0xffffffffu, bv, o);
+        const int64_t p2 = __shfl_xor_sync(0xffffffffu, bp, o);
+        const int c2 = __shfl_xor_sync(0xffffffffu, bc, o);
+        if (better(v2, p2, bv, bp)) {
+          bv = v2;
+          bp = p2;
+          bc = c2;
+        }
+      }
+      __syncthreads();
+      publish(bv, bp, bc, cpar ^ 1);
+      cpar ^= 1;
+      group_barrier(ctr, G, gen, -2, events + 12 * slot + 9);
+    }
     // ---- winning column: max value, smallest current position (ties in
     // both: lowest record, as a sequential scan).  Records are scanned in
     // parallel and reduced over the CTA.
-    double wv = -1.0, wf = -1.0;
+    double wv = -1.0, wf = -1.0, wc = -1.0;
     int64_t wp = 0x7fffffffffffLL, wpc = 0;
     int wq = 0x7fffffff;
-    const int par = k & 1;
+    const int par = cpar;
     for (int q = tid; q < G; q += kT) {
       const double* rec = cand + (int64_t)(par * G + q) * kCR;
       const double v = __ldcg(rec);
       const int64_t pc = __ldcg(reinterpret_cast<const long long*>(rec) + 1);
       const double fm = __ldcg(rec + 2);
       if (fm > wf) wf = fm;
+      const double cm = __ldcg(rec + 3);
+      if (cm > wc) wc = cm;
       const int64_t ps = pc >> 32;
       if (better(v, ps, wv, wp) || (v == wv && ps == wp && q < wq)) {
         wv = v;
@@ -664,6 +955,8 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
       const int q2 = __shfl_xor_sync(0xffffffffu, wq, o);
       const double f2 = __shfl_xor_sync(0xffffffffu, wf, o);
       if (f2 > wf) wf = f2;
+      const double c3 = __shfl_xor_sync(0xffffffffu, wc, o);
+      if (c3 > wc) wc = c3;
       if (better(v2, p2, wv, wp) || (v2 == wv && p2 == wp && q2 < wq)) {
         wv = v2;
         wp = p2;
@@ -677,6 +970,7 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
       sh.bpc[warp] = wpc;
       sh.bq[warp] = wq;
       sh.bfm[warp] = wf;
+      sh.bcm[warp] = wc;
     }
     __syncthreads();
     wv = sh.bval[0];
@@ -684,11 +978,13 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
     wpc = sh.bpc[0];
     wq = sh.bq[0];
     wf = sh.bfm[0];
+    wc = sh.bcm[0];
     for (int w2 = 1; w2 < kWarps; ++w2) {
       const double v2 = sh.bval[w2];
       const int64_t p2 = sh.bpos[w2];
       const int q2 = sh.bq[w2];
       if (sh.bfm[w2] > wf) wf = sh.bfm[w2];
+      if (sh.bcm[w2] > wc) wc = sh.bcm[w2];
       if (better(v2, p2, wv, wp) || (v2 == wv && p2 == wp && q2 < wq)) {
         wv = v2;
         wp = p2;
@@ -697,6 +993,11 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
       }
     }
     __syncthreads();
+    if (wc >= 0.0 && wc >= wv) {
+      // a cold column's (upper-bound) norm reaches the pivot value
+      maint = 2;
+      continue;
+    }
     if (wv < 0.0) {
       // every remaining column is frozen: the reference's next pivot is one
       // of them and its eta (< stop_tol r11 / 2) stops the elimination
@@ -784,6 +1085,10 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
         atomicMax(&sh.fmax, (unsigned long long)__double_as_longlong(cur[c]));
       } else {
         list_out[rank + G * atomicAdd(&sh.nact, 1)] = c;
+#ifdef SPAND_RRQR_PHASES
+        if (cur[c] >= 0.25 * wv) atomicAdd(&sh.nhot, 1);
+        if (cur[c] >= 0.09 * wv) atomicAdd(&sh.nhot3, 1);
+#endif
       }
     };
     if (k == 0) {
@@ -794,7 +1099,12 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
     __syncthreads();
     const int nact = sh.nact;
 #ifdef SPAND_RRQR_PHASES
-    if (tid == 0) nact_sum += nact;
+    if (tid == 0) {
+      nact_sum += nact;
+      hot_sum += sh.nhot;
+      hot3_sum += sh.nhot3;
+      sh.nhot = sh.nhot3 = 0;
+    }
 #endif
     // (b) Householder updates: warp per column for short columns, CTA-wide
     // batches for long ones
@@ -829,12 +1139,22 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
     }
     __syncthreads();
     PH(4);
-    publish(bv, bp, bc, (k + 1) & 1);
+    publish(bv, bp, bc, cpar ^ 1);
+    cpar ^= 1;
+    last_wv = wv;
     ++k;
+    if (k - k0 >= kBlk) maint = 1;
     PH(5);
     group_barrier(ctr, G, gen, k, events + 12 * slot + 9);
   }
   const int k_stop = k;
+  // remaining cold columns finish like frozen ones (Q^T a from the original)
+  for (int u = tid; u < sh.ncold; u += kT) {
+    const int c = coldl[rank + G * u];
+    done[c] = 2;
+    flist[rank + G * atomicAdd(&sh.nfrz, 1)] = c;
+  }
+  __syncthreads();
 #ifdef SPAND_RRQR_PHASES
   PH(7);
   long long tl = clock64(), tq = 0, trs = 0, tg = 0, twb = 0;
@@ -1067,8 +1387,8 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
   TL(twb);
 #ifdef SPAND_RRQR_PHASES
   if (lane == 0 && warp == 0 && m >= 1000 && (rank == 0 || rank == G / 2))
-    printf("[rrqr phases] p %d m %d n %d G %d rank %d k %d nf %d act-steps %lld | kcycles: cand %lld pivcol %lld refl %lld colpass %lld publish %lld barrier %lld | Q %lld restore %lld frozen-gemm %lld writeback %lld\n",
-           p, m, n, G, rank, k_stop, nf, nact_sum, ph_t[0] / 1000, ph_t[1] / 1000, ph_t[2] / 1000,
+    printf("[rrqr phases] p %d m %d n %d G %d rank %d k %d nf %d act-steps %lld hot %lld hot3 %lld | kcycles: cand %lld pivcol %lld refl %lld colpass %lld publish %lld barrier %lld | Q %lld restore %lld frozen-gemm %lld writeback %lld\n",
+           p, m, n, G, rank, k_stop, nf, nact_sum, hot_sum, hot3_sum, ph_t[0] / 1000, ph_t[1] / 1000, ph_t[2] / 1000,
            ph_t[3] / 1000, ph_t[4] / 1000, ph_t[5] / 1000, tq / 1000, trs / 1000, tg / 1000,
            twb / 1000);
 #endif
@@ -1098,9 +1418,9 @@ int spand_rrqr_cta_count(void) {
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   // capacity for panels up to 4224 rows (the tile staging size); taller
   // panels need more shared memory and are launched with smaller groups
-  const size_t smem = kMinSmem;
+  const size_t smem = kColdSmem;
   cudaFuncSetAttribute(rrqr_wave_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)(kMaxM * sizeof(double)));
+                       (int)(kMaxM * sizeof(double) > kColdSmem ? kMaxM * sizeof(double) : kColdSmem));
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, rrqr_wave_kernel, kT, smem) != cudaSuccess)
     return -1;
   return per * sms;
@@ -1110,10 +1430,10 @@ int spand_rrqr_capacity(int vmax) {
   int dev = 0, sms = 0, per = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return -1;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  size_t smem = kMinSmem;
+  size_t smem = kColdSmem;
   if ((size_t)vmax * sizeof(double) > smem) smem = (size_t)vmax * sizeof(double);
   cudaFuncSetAttribute(rrqr_wave_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)(kMaxM * sizeof(double)));
+                       (int)(kMaxM * sizeof(double) > kColdSmem ? kMaxM * sizeof(double) : kColdSmem));
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, rrqr_wave_kernel, kT, smem) != cudaSuccess)
     return -1;
   return per * sms;
@@ -1124,12 +1444,12 @@ int spand_rrqr_wave(int npanel, int grid, int vmax, const int64_t* panels, const
                     void* stream) {
   if (npanel < 0 || grid < 0 || vmax < 0 || vmax > kMaxM) return -1;
   if (npanel == 0 || grid == 0) return 0;
-  const size_t tile_bytes = kMinSmem;
+  const size_t tile_bytes = kColdSmem;
   size_t smem = (size_t)(vmax > 0 ? vmax : 1) * sizeof(double);
   if (smem < tile_bytes) smem = tile_bytes;
-  cudaError_t e = cudaFuncSetAttribute(rrqr_wave_kernel,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)(kMaxM * sizeof(double)));
+  cudaError_t e = cudaFuncSetAttribute(
+      rrqr_wave_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      (int)(kMaxM * sizeof(double) > kColdSmem ? kMaxM * sizeof(double) : kColdSmem));
   if (e != cudaSuccess) return (int)e;
   void* args[] = {&npanel, &panels, &nbrs, &m0, &off, &eps, &scheme, &events};
   e = cudaLaunchCooperativeKernel((void*)rrqr_wave_kernel, dim3(grid), dim3(kT), args, smem,
