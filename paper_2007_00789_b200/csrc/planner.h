@@ -227,7 +227,7 @@ struct Plan {
           for (int w : L.anbrs[k]) ncap += m0[w];
           const int64_t mc = m0[L.active[k]];
           rq += mc * std::max<int64_t>(ncap, 1) + mc * mc + 32 * (ncap + mc) + 2 * ncap +
-                3 * mc + 8 + (3 * ncap + 1) / 2 + 1 + 1 + 68;
+                3 * mc + 8 + 1024 + (3 * ncap + 1) / 2 + 1 + 1 + 68;
         }
         need = std::max(need, rq);
       }
@@ -632,7 +632,7 @@ struct Plan {
             for (int w : L.anbrs[k]) ncap += m0[w];
             const int64_t mc = m0[p];
             const int64_t wsz = mc * std::max<int64_t>(ncap, 1) + mc * mc + 32 * (ncap + mc);
-            const int64_t asz = 2 * ncap + 3 * mc + 68 * (int64_t)g + 8;
+            const int64_t asz = 2 * ncap + 3 * mc + 68 * (int64_t)g + 8 + 1024;
             const int64_t isz = (3 * ncap + 1) / 2 + 1;
             const int64_t nb0 = (int64_t)nrow.size() / 4;
             for (int w : L.anbrs[k]) {
@@ -643,7 +643,7 @@ struct Plan {
             prow.insert(prow.end(),
                         {p, nb0, nb1, temp_base + 8 * need, fac_base + 8 * L.q_off[k],
                          temp_base + 8 * (need + wsz), temp_base + 8 * (need + wsz + asz), gbeg,
-                         g, ctr_base + 4 * ctr_next, L.slot[k], ncap, mc, 0, 0, 0});
+                         g, ctr_base + 8 * ctr_next, L.slot[k], ncap, mc, 0, 0, 0});
             ++ctr_next;
             need += wsz + asz + isz + 1;
             gbeg += g;

@@ -37,7 +37,7 @@ constexpr int kMaxM = 6144;  // v in shared memory
 // panel row (16 int64):
 //  0 p        1 nbr_begin  2 nbr_end   3 W (double*, temp, >= m*n)
 //  4 Q (double*, m*m, compact ld = m)  5 aux (double*)  6 iaux (int32*)
-//  7 group_begin  8 group_size  9 counter (uint32*)  10 event slot
+//  7 group_begin  8 group_size  9 counters (uint32[2]: arrivals, release)  10 event slot
 //  11 ncap (column capacity of aux arrays)  12 mcap  13-15 unused
 // nbr row (4 int64): {w, block ptr, orientation, 0}
 //  orientation 0: block (p, w) stored with rows of p (ld = m0[p])
@@ -52,8 +52,10 @@ constexpr int kLDS = 68;       // frozen-column DMMA tiles (conflict-free fragme
 // the frozen-GEMM epilogue tile (64 x 65)
 constexpr size_t kMinSmem = (size_t)4 * 16 * kLDS * sizeof(double);   // 2 stages x (A, B)
 // cold-column maintenance layout in the dynamic shared memory (doubles):
-// scratch [0, 4352) | T [32][33] | Y/Z [64][33] | R rows [64][33] | tails [64]
-constexpr int kCScr = 0, kCT = 4352, kCZ = kCT + 32 * 33, kCR2 = kCZ + 64 * 33,
+// scratch (2 stages x kPBK rows of the A (64) and V (32) operands, and the
+// 64 x 65 update tile) | T [32][33] | Y/Z [64][33] | R rows [64][33] | tails [64]
+constexpr int kPBK = 32;         // rows per stage of the cold-column product
+constexpr int kCScr = 0, kCT = 2 * kPBK * (kLDS + 36), kCZ = kCT + 32 * 33, kCR2 = kCZ + 64 * 33,
               kCTail = kCR2 + 64 * 33, kColdEnd = kCTail + 64;
 constexpr size_t kColdSmem = (size_t)kColdEnd * sizeof(double);
 constexpr int kBlk = 32;         // reflectors per cold-column block update
@@ -92,6 +94,13 @@ __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
   return v;
 }
 
+__device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
+}
+
+// Group barrier: ctr[0] counts arrivals, the last CTA of generation `gen`
+// publishes gen in ctr[1] (release); the others poll ctr[1] (acquire), so
+// the polled word changes once per barrier instead of once per arrival.
 __device__ __forceinline__ void group_barrier(unsigned* ctr, int G, unsigned& gen,
                                               int tag = -1, int64_t* flag = nullptr) {
   __syncthreads();
@@ -99,17 +108,20 @@ __device__ __forceinline__ void group_barrier(unsigned* ctr, int G, unsigned& ge
     if (threadIdx.x == 0) {
       __threadfence();
       ++gen;
-      atomicAdd(ctr, 1u);
-      const unsigned target = gen * (unsigned)G;
-      const long long t0 = clock64();
-      while (ld_acquire(ctr) < target) {
-        // watchdog: a group that never completes a barrier is a bug; report
-        // and fall through (~2 s) instead of hanging the device
-        if (clock64() - t0 > 4000000000ll) {
-          printf("[spand rrqr] barrier timeout block %d tag %d gen %u ctr %u G %d\n",
-                 (int)blockIdx.x, tag, gen, ld_acquire(ctr), G);
-          if (flag) atomicExch(reinterpret_cast<unsigned long long*>(flag), 1ull);
-          break;
+      const unsigned arrived = atomicAdd(ctr, 1u) + 1u;
+      if (arrived == gen * (unsigned)G) {
+        st_release(ctr + 1, gen);
+      } else {
+        const long long t0 = clock64();
+        while (ld_acquire(ctr + 1) < gen) {
+          // watchdog: a group that never completes a barrier is a bug; report
+          // and fall through (~2 s) instead of hanging the device
+          if (clock64() - t0 > 4000000000ll) {
+            printf("[spand rrqr] barrier timeout block %d tag %d gen %u ctr %u G %d\n",
+                   (int)blockIdx.x, tag, gen, ld_acquire(ctr), G);
+            if (flag) atomicExch(reinterpret_cast<unsigned long long*>(flag), 1ull);
+            break;
+          }
         }
       }
       __threadfence();
@@ -492,6 +504,7 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
   double* betas = aux + 2 * ncap + mcap;                       // mcap
   double* taus = betas + mcap;                                 // mcap
   double* cand = taus + mcap;                                  // 2 G kCR, by step parity
+  double* Gbuf = cand + (int64_t)2 * G * kCR;                  // 32 x 32: V_b^T V_b of the block
   double* V = W + (int64_t)mcap * ncap;                        // m x kmax reflectors
   int32_t* flist = reinterpret_cast<int32_t*>(V + (int64_t)mcap * mcap);  // frozen columns
   int32_t* perm = iaux;
@@ -663,8 +676,9 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
   int32_t* coldl = coldA;
   auto pass1 = [&](int na, auto colp, auto alo, int ka, int nb) {
     // ZT[a][q] = sum_{i >= ka} A_a[i] V[i, ka + q]  (64 x 32 tile on DMMA)
-    double (*As)[16][kLDS] = reinterpret_cast<double (*)[16][kLDS]>(vsh + kCScr);
-    double (*Bs)[16][36] = reinterpret_cast<double (*)[16][36]>(vsh + kCScr + 2 * 16 * kLDS);
+    double (*As)[kPBK][kLDS] = reinterpret_cast<double (*)[kPBK][kLDS]>(vsh + kCScr);
+    double (*Bs)[kPBK][36] =
+        reinterpret_cast<double (*)[kPBK][36]>(vsh + kCScr + 2 * kPBK * kLDS);
     double (*ZT)[33] = reinterpret_cast<double (*)[33]>(vsh + kCZ);
     const int wm = warp >> 2, wn = warp & 3;
     double acc[4][2];
@@ -672,17 +686,17 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
     for (int a = 0; a < 4; ++a) acc[a][0] = acc[a][1] = 0.0;
     auto stage = [&](int st, int i0) {
 #pragma unroll
-      for (int r = 0; r < 4; ++r) {
+      for (int r = 0; r < (kPBK * 64) / kT; ++r) {
         const int e = tid + r * kT;
-        const int kk = e & 15, a = e >> 4;
+        const int kk = e % kPBK, a = e / kPBK;
         const int i = i0 + kk;
         const bool ok = a < na && i < m && i >= alo(a);
         cp_async8(&As[st][kk][a], ok ? colp(a) + i : W, ok);
       }
 #pragma unroll
-      for (int r = 0; r < 2; ++r) {
+      for (int r = 0; r < (kPBK * 32) / kT; ++r) {
         const int e = tid + r * kT;
-        const int kk = e & 15, q = e >> 4;
+        const int kk = e % kPBK, q = e / kPBK;
         const int i = i0 + kk;
         const bool ok = q < nb && i < m && i >= ka + q;
         cp_async8(&Bs[st][kk][q], ok ? V + (int64_t)i + (int64_t)(ka + q) * m : V, ok);
@@ -692,12 +706,12 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
     __syncthreads();
     stage(0, ka);
     int st = 0;
-    for (int i0 = ka; i0 < m; i0 += 16) {
+    for (int i0 = ka; i0 < m; i0 += kPBK) {
       cp_wait_all();
       __syncthreads();
-      if (i0 + 16 < m) stage(st ^ 1, i0 + 16);
+      if (i0 + kPBK < m) stage(st ^ 1, i0 + kPBK);
 #pragma unroll
-      for (int kq = 0; kq < 4; ++kq) {
+      for (int kq = 0; kq < kPBK / 4; ++kq) {
         const int kr = kq * 4 + (lane & 3);
         const double bf = Bs[st][kr][wn * 8 + (lane >> 2)];
 #pragma unroll
@@ -724,8 +738,13 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
     double* TAIL = vsh + kCTail;
     const int wm = warp >> 2, wn = warp & 3;
     // T of Q_b = H_ka ... H_{kb-1} = I - V T V^T (dlarft, forward columnwise)
-    pass1(nb, [&](int a) { return (const double*)(V + (int64_t)(ka + a) * m); },
-          [&](int a) { return ka + a; }, ka, nb);
+    // from the Gram columns gathered during the block's steps
+    __syncthreads();
+    for (int e = tid; e < 32 * 32; e += kT) {
+      const int c = e >> 5, q = e & 31;
+      ZT[c][q] = (c < q && q < nb) ? __ldcg(Gbuf + c * 32 + q) : 0.0;
+    }
+    __syncthreads();
     if (warp == 0) {
       for (int jj = 0; jj < nb; ++jj) {
         const double tj = __ldcg(taus + ka + jj);
@@ -1059,6 +1078,18 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
       if (tid == 0) {
         taus[k] = tau;
         betas[k] = beta;
+      }
+    }
+    // ---- Gram column of the block's reflectors for the cold update:
+    // G[q][jb] = V[:, k0 + q] . v_k (q < jb), one dot per CTA
+    {
+      const int jb = k - k0;
+      for (int q = rank; q < jb; q += G) {
+        const double* vq = V + (int64_t)(k0 + q) * m + k;
+        double d = 0.0;
+        for (int i = tid; i < len; i += kT) d += __ldcg(vq + i) * vsh[i];
+        d = block_sum<kT>(d, sh.red);
+        if (tid == 0) Gbuf[q * 32 + jb] = d;
       }
     }
     // ---- owned active columns: a -= tau (v.a) v, row-k entry, norm

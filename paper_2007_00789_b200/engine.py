@@ -208,7 +208,7 @@ class Engine:
         self._scatter_a()
         self.events = t.zeros(max(sym.n_events, 1) * EVENT_ROW, dtype=t.int64, device=d)
         self.info = t.zeros(max(sym.n_info, 1), dtype=t.int32, device=d)
-        ctr = t.zeros(max(sym.n_ctr, 1), dtype=t.int32, device=d)
+        ctr = t.zeros(2 * max(sym.n_ctr, 1), dtype=t.int32, device=d)   # {arrivals, release} per panel
         pb, fb = pool.data_ptr(), fac.data_ptr()
         temp = t.empty(max(sym.temp_bound, 1), dtype=t.float64, device=d)
         st = stream()

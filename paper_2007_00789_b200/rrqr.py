@@ -33,11 +33,11 @@ def rrqr_single(a, eps, scheme, group=None, pad=0):
     g = group or max(1, min(cap, n // 64, (m * n) // 65536 + 1))
     ncap, mcap = max(np_, 1), max(mp, 1)
     wsz = mcap * ncap + mcap * mcap + 32 * (ncap + mcap)
-    asz = 2 * ncap + 3 * mcap + 2 * g * 34 + 8
+    asz = 2 * ncap + 3 * mcap + 2 * g * 34 + 8 + 1024
     isz = (3 * ncap + 1) // 2 + 1
     work = t.zeros(wsz + asz + isz + 1, dtype=t.float64, device=dev())
     q = t.zeros(mcap * mcap, dtype=t.float64, device=dev())
-    ctr = t.zeros(1, dtype=t.int32, device=dev())
+    ctr = t.zeros(2, dtype=t.int32, device=dev())
     events = t.zeros(12, dtype=t.int64, device=dev())
     wb = work.data_ptr()
     prow = [[0, 0, 1, wb, q.data_ptr(), wb + 8 * wsz, wb + 8 * (wsz + asz), 0, g,
