@@ -223,24 +223,42 @@ class Engine:
         lib.spand_plan_emit_next.argtypes = [ctypes.c_void_p, ctypes.c_void_p]
         lib.spand_plan_chunk.argtypes = [ctypes.c_void_p] * 3
         lib.spand_plan_emit_begin(sym.h, pb, fb, temp.data_ptr(), ctr.data_ptr())
-        sizes = np.zeros(3, dtype=np.int64)
-        keep = []
-        t_plan = 0.0
-        while True:
+        # the next level is emitted on a helper thread (ctypes releases the
+        # GIL) while this one uploads and launches the current level
+        from concurrent.futures import ThreadPoolExecutor
+        acc = {"plan": 0.0}
+
+        def produce():
             tp = time.perf_counter()
+            sizes = np.zeros(3, dtype=np.int64)
             more = lib.spand_plan_emit_next(sym.h, vp(sizes))
-            plen, nlau, used = (int(x) for x in sizes)
+            plen, nlau, used_ = (int(x) for x in sizes)
+            prog_ = launches_ = None
             if nlau:
-                prog = np.empty(max(plen, 1), dtype=np.int64)
-                launches = np.empty((nlau, 16), dtype=np.int64)
-                lib.spand_plan_chunk(sym.h, vp(prog), vp(launches))
-            t_plan += time.perf_counter() - tp
-            if nlau:
-                progd = to_dev_async(prog)
-                keep.append(progd)
-                self._launch(launches, progd.data_ptr(), gm0, goff, ib, evb, fb, st, prog)
-            if not more:
-                break
+                prog_ = np.empty(max(plen, 1), dtype=np.int64)
+                launches_ = np.empty((nlau, 16), dtype=np.int64)
+                lib.spand_plan_chunk(sym.h, vp(prog_), vp(launches_))
+            acc["plan"] += time.perf_counter() - tp
+            return more, prog_, launches_, used_
+
+        keep = []
+        t_launch = 0.0
+        with ThreadPoolExecutor(1) as ex:
+            fut = ex.submit(produce)
+            while True:
+                more, prog, launches, used = fut.result()
+                if more:
+                    fut = ex.submit(produce)
+                if launches is not None:
+                    tl = time.perf_counter()
+                    progd = to_dev_async(prog)
+                    keep.append(progd)
+                    self._launch(launches, progd.data_ptr(), gm0, goff, ib, evb, fb, st, prog)
+                    t_launch += time.perf_counter() - tl
+                if not more:
+                    break
+        t_plan = acc["plan"]
+        self.timings["launch_s"] = t_launch
         assert used <= sym.temp_bound, (used, sym.temp_bound)
         self.timings["plan_s"] = t_plan
         self._keep_run = (temp, ctr, keep)
