@@ -63,7 +63,23 @@ gemv_tiles_kernel(const int64_t* __restrict__ tiles, const int64_t* __restrict__
       double a0 = 0.0, a1 = 0.0;
       const int r0 = ob + lane, r1 = ob + lane + 32;
       const bool ok0 = lane < oc, ok1 = lane + 32 < oc;
-      for (int c = w; c < kc; c += kWarps) {
+      int c = w;
+      for (; c + 3 * kWarps < kc; c += 4 * kWarps) {
+        double m0v[4], m1v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const double* col = T.M + (int64_t)phys_col(kb + c + u * kWarps, T.rot, T.cols) * T.ld;
+          m0v[u] = ok0 ? __ldg(col + r0) : 0.0;
+          m1v[u] = ok1 ? __ldg(col + r1) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const double xi = vin[c + u * kWarps];
+          a0 += m0v[u] * xi;
+          a1 += m1v[u] * xi;
+        }
+      }
+      for (; c < kc; c += kWarps) {
         const double* col = T.M + (int64_t)phys_col(kb + c, T.rot, T.cols) * T.ld;
         const double xi = vin[c];
         if (ok0) a0 += __ldg(col + r0) * xi;
@@ -72,16 +88,39 @@ gemv_tiles_kernel(const int64_t* __restrict__ tiles, const int64_t* __restrict__
       part[w][lane] = a0;
       part[w][lane + 32] = a1;
     } else {
-      // y[j] = sum_r M[r, j] in[r]; warp w takes output columns w*8..w*8+7
-      for (int jj = 0; jj < kTileOut / kWarps; ++jj) {
-        const int j = w * (kTileOut / kWarps) + jj;
-        double a = 0.0;
-        if (j < oc) {
-          const double* col = T.M + (int64_t)phys_col(ob + j, T.rot, T.cols) * T.ld + kb;
-          for (int r = lane; r < kc; r += 32) a += __ldg(col + r) * vin[r];
+      // y[j] = sum_r M[r, j] in[r]
+      // warp w owns columns w, w + 8, ... (narrow tiles still use every warp)
+      for (int jj = 0; jj < kTileOut / kWarps; jj += 2) {
+        const int j = w + kWarps * jj, j1 = w + kWarps * (jj + 1);
+        if (j >= oc) break;
+        double a = 0.0, b = 0.0;
+        const bool okj = true, okj1 = j1 < oc;
+        const double* col = T.M + (int64_t)phys_col(ob + j, T.rot, T.cols) * T.ld + kb;
+        const double* col1 = T.M + (int64_t)phys_col(okj1 ? ob + j1 : ob, T.rot, T.cols) * T.ld + kb;
+        int r = lane;
+        for (; r + 96 < kc; r += 128) {
+          double p[4], q[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            p[u] = okj ? __ldg(col + r + 32 * u) : 0.0;
+            q[u] = okj1 ? __ldg(col1 + r + 32 * u) : 0.0;
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            a += p[u] * vin[r + 32 * u];
+            b += q[u] * vin[r + 32 * u];
+          }
+        }
+        for (; r < kc; r += 32) {
+          if (okj) a += __ldg(col + r) * vin[r];
+          if (okj1) b += __ldg(col1 + r) * vin[r];
         }
         a = warp_sum(a);
-        if (lane == 0) part[0][j] = a;
+        b = warp_sum(b);
+        if (lane == 0) {
+          part[0][j] = a;
+          if (okj1) part[0][j1] = b;
+        }
       }
     }
     __syncthreads();
@@ -126,19 +165,28 @@ __global__ void __launch_bounds__(kThreads)
 runs_kernel(const int64_t* __restrict__ chunks, const int64_t* __restrict__ contrib,
             double* __restrict__ x, int64_t ldx, const double* __restrict__ scratch,
             int64_t ldscr, int nvec) {
+  // chunk of <= 64 outputs; 4 thread groups split the contributions, the
+  // group partials are added in group order (deterministic)
+  __shared__ double part[kThreads];
   const int64_t* ch = chunks + 8 * (int64_t)blockIdx.x;
   const int len = (int)ch[1];
-  const int i = threadIdx.x;
-  if (i >= len) return;
+  const int i = threadIdx.x & 63, g = threadIdx.x >> 6;
   const int64_t dst = ch[0], cb = ch[3], ce = ch[4], eoff = ch[5], idx = ch[6];
   const int md = (int)ch[2];
-  const int64_t d = idx ? (int64_t)reinterpret_cast<const int32_t*>(idx)[eoff + i] : dst + eoff + i;
   for (int v = 0; v < nvec; ++v) {
     double s = 0.0;
-    for (int64_t c = cb; c < ce; ++c) s += scratch[__ldg(contrib + c) + eoff + i + v * ldscr];
-    double* xd = x + d + v * ldx;
-    if (md == 0) *xd = s;
-    else *xd -= s;
+    if (i < len)
+      for (int64_t c = cb + g; c < ce; c += 4) s += scratch[__ldg(contrib + c) + eoff + i + v * ldscr];
+    __syncthreads();
+    part[threadIdx.x] = s;
+    __syncthreads();
+    if (threadIdx.x < len) {
+      const double t = part[i] + part[i + 64] + part[i + 128] + part[i + 192];
+      const int64_t d = idx ? (int64_t)reinterpret_cast<const int32_t*>(idx)[eoff + i] : dst + eoff + i;
+      double* xd = x + d + v * ldx;
+      if (md == 0) *xd = t;
+      else *xd -= t;
+    }
   }
 }
 }  // namespace

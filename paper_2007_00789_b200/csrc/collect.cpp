@@ -262,7 +262,19 @@ int spand_collect_get(void* h, int64_t* ops, int64_t* segs, int64_t* perm, int64
 // selects the factor buffer), inputs xbuf + 8 * permuted index.
 static void compile_phase(Collected* C, const std::vector<Task>& ph, int64_t pool_base,
                           int64_t fac_base, int64_t xbuf, int64_t idx_addr) {
-  constexpr int64_t TO = 64, TK = 2048, RUN = 256;
+  constexpr int64_t TO = 64, RUN = 64;
+  // inner-dimension split: 2048 by default, finer (down to 256) when the
+  // phase would otherwise leave most of the 148 SMs idle
+  int64_t TK = 2048;
+  for (; TK > 256; TK /= 2) {
+    int64_t nt = 0;
+    for (const Task& t : ph) {
+      const int64_t nout = t.trans ? t.cols : t.rows;
+      const int64_t nk = t.trans ? t.rows : t.cols;
+      nt += ((nout + TO - 1) / TO) * std::max<int64_t>(1, (nk + TK - 1) / TK);
+    }
+    if (nt >= 4 * 148) break;
+  }
   std::vector<int64_t> rows, tiles, chunks, contrib;
   struct Run { int64_t dst, len, mode; bool idx; std::vector<int64_t> parts; };
   std::vector<Run> runs;
