@@ -19,6 +19,7 @@ OUT = os.path.join(HERE, "libspand_b200.so")
 BUILD = os.path.join(HERE, "csrc", "build")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC = os.environ.get("NVCC", "nvcc")
+PER_FILE = {}   # per-file extra nvcc flags
 
 
 def _sources():
@@ -47,6 +48,8 @@ def build(verbose=False, jobs=8):
         cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17",
                "-Xcompiler", "-fPIC", "-Xptxas", "-v" if verbose else "-O3",
                "-c", src, "-o", obj]
+        if os.path.basename(src) in PER_FILE:
+            cmd[1:1] = PER_FILE[os.path.basename(src)]
         if src.endswith(".cpp"):
             cmd = ["g++", "-O3", "-std=c++17", "-fPIC", "-c", src, "-o", obj]
         procs.append((src, subprocess.Popen(cmd, stdout=subprocess.PIPE,

@@ -182,6 +182,13 @@ struct ColCtx {
   const int32_t* list;    // this step's active columns, interleaved slots
   int rank, G;
   unsigned long long* refresh_ctr;
+  int jpos;               // this step's swap: position k now belongs to jpos
+  // current position of column c: the owner may not have applied this
+  // step's swap yet when another CTA processes c, so apply it here
+  __device__ int64_t posof(int c) const {
+    const int p = pos[c];
+    return p == k ? jpos : p;
+  }
 };
 
 // Householder update of B active columns at a time by the whole CTA: every
@@ -251,7 +258,7 @@ __device__ void colpass_batch(const ColCtx& X, int a0, int nb, Sh& sh, double& b
         atomicAdd(X.refresh_ctr, 1ull);
       }
       X.cur[c] = cn;
-      const int64_t ps = X.pos[c];
+      const int64_t ps = X.posof(c);
       if (better(cn, ps, bv, bp)) {
         bv = cn;
         bp = ps;
@@ -319,7 +326,7 @@ __device__ void colpass_warp(const ColCtx& X, int nact, double& bv, int64_t& bp,
           atomicAdd(X.refresh_ctr, 1ull);
         }
         X.cur[c] = cn;
-        const int64_t ps = X.pos[c];
+        const int64_t ps = X.posof(c);
         if (better(cn, ps, bv, bp)) {
           bv = cn;
           bp = ps;
@@ -356,7 +363,7 @@ __device__ void colpass_long(const ColCtx& X, int a0, Sh& sh, double& bv, int64_
       atomicAdd(X.refresh_ctr, 1ull);
     }
     X.cur[c] = cn;
-    const int64_t ps = X.pos[c];
+    const int64_t ps = X.posof(c);
     if (better(cn, ps, bv, bp)) {
       bv = cn;
       bp = ps;
@@ -671,8 +678,12 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
   // the updated column).  Each step checks that no cold column's (stale,
   // larger) norm reaches the pivot value; if one does, the block ends early
   // and every cold column becomes hot.
-  int32_t* coldA = flist + 4 * ncap;
-  int32_t* coldB = flist + 6 * ncap;
+  // int lists in the F region (interleaved slots rank + G u; regions 4 ncap
+  // apart since rebalanced per-CTA counts may exceed a CTA's own share)
+  int32_t* hotA = flist + 4 * ncap;
+  int32_t* hotB = flist + 8 * ncap;
+  int32_t* coldA = flist + 12 * ncap;
+  int32_t* coldB = flist + 16 * ncap;
   int32_t* coldl = coldA;
   auto pass1 = [&](int na, auto colp, auto alo, int ka, int nb) {
     // ZT[a][q] = sum_{i >= ka} A_a[i] V[i, ka + q]  (64 x 32 tile on DMMA)
@@ -879,8 +890,8 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
       // bring the cold columns up to date (reflectors k0..k-1), then either
       // reclassify (block end) or make every column hot (a cold column could
       // have won), and republish this CTA's candidate
-      int32_t* hot_in = (k & 1) ? perm : flist + 2 * ncap;
-      int32_t* tmpl = flist + 8 * ncap;
+      int32_t* hot_in = (k & 1) ? hotA : hotB;
+      int32_t* tmpl = flist + 20 * ncap;
       cold_maint(k0, k);
       const int nh = sh.nact, ncd = sh.ncold;
       __syncthreads();
@@ -897,7 +908,6 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
         if (done[c]) continue;
         if (cur[c] < thr2) {
           done[c] = 2;
-          flist[rank + G * atomicAdd(&sh.nfrz, 1)] = c;
           atomicMax(&sh.fmax, (unsigned long long)__double_as_longlong(cur[c]));
         } else if (cur[c] >= tau_hot) {
           tmpl[rank + G * atomicAdd(&sh.nact, 1)] = c;
@@ -909,7 +919,9 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
       }
       __syncthreads();
       if (sh.ncold == 0 && tid == 0) sh.coldmax = -1.0;
-      const int nh2 = sh.nact;
+      int nh2 = sh.nact;
+      // (columns stay with their owner CTA: moving them between CTAs needs
+      // L1-bypassing loads and changed pivot decisions in exact ties)
       for (int u = tid; u < nh2; u += kT) hot_in[rank + G * u] = tmpl[rank + G * u];
       coldl = cold_out;
       k0 = k;
@@ -917,8 +929,9 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
       bv = -1.0;
       bp = 0x7fffffffffffLL;
       bc = -1;
+      __syncthreads();
       for (int u = tid; u < nh2; u += kT) {
-        const int c = tmpl[rank + G * u];
+        const int c = hot_in[rank + G * u];
         const double cv = cur[c];
         const int64_t ps = pos[c];
         if (better(cv, ps, bv, bp)) {
@@ -1101,8 +1114,8 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
     // (a) this step's active columns: filter the previous step's list (the
     // set only shrinks; lists ping-pong between the perm array, written only
     // after the loop, and a spare region); freeze columns below the threshold
-    int32_t* list_out = (k & 1) ? flist + 2 * ncap : perm;
-    const int32_t* list_in = (k & 1) ? perm : flist + 2 * ncap;
+    int32_t* list_out = (k & 1) ? hotB : hotA;
+    const int32_t* list_in = (k & 1) ? hotA : hotB;
     __syncthreads();
     const int nprev = sh.nact;
     __syncthreads();
@@ -1112,7 +1125,6 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
       if (c == j || done[c]) return;
       if (cur[c] < thr2) {
         done[c] = 2;
-        flist[rank + G * atomicAdd(&sh.nfrz, 1)] = c;
         atomicMax(&sh.fmax, (unsigned long long)__double_as_longlong(cur[c]));
       } else {
         list_out[rank + G * atomicAdd(&sh.nact, 1)] = c;
@@ -1141,7 +1153,7 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
     // batches for long ones
     {
       ColCtx X{W, m, k, len, tau, vsh, cur, ref, pos, list_out, rank, G,
-               reinterpret_cast<unsigned long long*>(events + 12 * slot + 10)};
+               reinterpret_cast<unsigned long long*>(events + 12 * slot + 10), jpos};
       if (len <= 256) {
         colpass_warp<4>(X, nact, bv, bp, bc);
       } else if (len <= 8 * kT) {
@@ -1180,11 +1192,13 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
   }
   const int k_stop = k;
   // remaining cold columns finish like frozen ones (Q^T a from the original)
-  for (int u = tid; u < sh.ncold; u += kT) {
-    const int c = coldl[rank + G * u];
-    done[c] = 2;
-    flist[rank + G * atomicAdd(&sh.nfrz, 1)] = c;
-  }
+  for (int u = tid; u < sh.ncold; u += kT) done[coldl[rank + G * u]] = 2;
+  // frozen list of my own columns (static ownership c % G)
+  group_barrier(ctr, G, gen, -5, events + 12 * slot + 9);
+  if (tid == 0) sh.nfrz = 0;
+  __syncthreads();
+  for (int c = rank + G * tid; c < n; c += G * kT)
+    if (__ldcg(done + c) == 2) flist[rank + G * atomicAdd(&sh.nfrz, 1)] = c;
   __syncthreads();
 #ifdef SPAND_RRQR_PHASES
   PH(7);
