@@ -147,11 +147,15 @@ int spand_copy_batched(int ntask, const int64_t* ops, const int32_t* m0,
  * tri: triangular operands (zero above their diagonal) bound the K range of a
  * tile at (i0, j0): 1 A lower -> k < i0 + 64; 2 B lower and bT = 1 ->
  * k < j0 + 64; 4 B lower and bT = 0 -> k >= j0 (TRSM/TRMM as GEMM at the
- * triangular flop count). */
+ * triangular flop count).
+ * compact = 1: a segment is ONE int64 {A block << 32 | B block} indexing the
+ * block table btab (rows {ptr, rc, cc}: whole live blocks), the Schur-update
+ * form; compact = 0: 14 int64 operand rows (btab unused). */
 int spand_gemm_grouped(int ntile, const int64_t* tiles, const int64_t* targets,
                        const int64_t* segs, const int32_t* m0,
                        const int32_t* off, double alpha, double beta, int bT,
-                       int lower_only, int tri, void* stream);
+                       int lower_only, int tri, const int64_t* btab, int compact,
+                       void* stream);
 
 /* One wave of the batched early-stopping column-pivoted Householder QR of
  * interface panels (restates dense.py:117-222, schemes.py:272-318,

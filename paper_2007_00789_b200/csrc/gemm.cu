@@ -38,7 +38,7 @@ __global__ void __launch_bounds__(kThreads)
 gemm_grouped_kernel(const int64_t* __restrict__ tiles, const int64_t* __restrict__ targets,
                     const int64_t* __restrict__ segs, const int32_t* __restrict__ m0,
                     const int32_t* __restrict__ off, double alpha, double beta, int bT,
-                    int lower_only, int tri) {
+                    int lower_only, int tri, const int64_t* __restrict__ btab, int compact) {
   __shared__ __align__(16) double As[2][BK][LDS];
   __shared__ __align__(16) double Bs[2][BK][LDS];
   // packed tile: target << 32 | (i0 / 64) << 16 | (j0 / 64)
@@ -59,6 +59,22 @@ gemm_grouped_kernel(const int64_t* __restrict__ tiles, const int64_t* __restrict
 #pragma unroll
     for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
 
+  // segment operands: 14 int64 {A, B operand rows}, or (compact) one int64
+  // {A block << 32 | B block} into the block table (rows {ptr, rc, cc})
+  auto seg_opnds = [&](int s, Opnd& a, Opnd& b) {
+    if (!compact) {
+      a = load_opnd(segs + 14 * (int64_t)s, m0, off);
+      b = load_opnd(segs + 14 * (int64_t)s + 7, m0, off);
+    } else {
+      const int64_t e = segs[s];
+      const int64_t* ra = btab + 3 * (e >> 32);
+      const int64_t* rb = btab + 3 * (e & 0xffffffffLL);
+      const int64_t da[7] = {ra[0], ra[1], ra[2], 0, 0, -1, -1};
+      const int64_t db[7] = {rb[0], rb[1], rb[2], 0, 0, -1, -1};
+      a = load_opnd(da, m0, off);
+      b = load_opnd(db, m0, off);
+    }
+  };
   // chunk iterator over (segment, k0).  Triangular operands (explicit
   // inverses, zero above the diagonal) bound each segment's K range:
   // tri & 1: A lower -> k < i0 + BM; tri & 2: B lower, C = A B^T -> k < j0 + BN;
@@ -75,8 +91,7 @@ gemm_grouped_kernel(const int64_t* __restrict__ tiles, const int64_t* __restrict
   Opnd A, B;
   int K = 0;
   auto open_seg = [&](int s) {
-    A = load_opnd(segs + 14 * (int64_t)s, m0, off);
-    B = load_opnd(segs + 14 * (int64_t)s + 7, m0, off);
+    seg_opnds(s, A, B);
     krange(A, B, k0, K);
   };
   // skip empty segments
@@ -127,8 +142,7 @@ gemm_grouped_kernel(const int64_t* __restrict__ tiles, const int64_t* __restrict
       if (kn >= Kn) {
         ++segn;
         while (segn < se) {
-          An = load_opnd(segs + 14 * (int64_t)segn, m0, off);
-          Bn = load_opnd(segs + 14 * (int64_t)segn + 7, m0, off);
+          seg_opnds(segn, An, Bn);
           krange(An, Bn, kn, Kn);
           if (Kn > kn) break;
           ++segn;
@@ -184,12 +198,12 @@ gemm_grouped_kernel(const int64_t* __restrict__ tiles, const int64_t* __restrict
 extern "C" int spand_gemm_grouped(int ntile, const int64_t* tiles, const int64_t* targets,
                                   const int64_t* segs, const int32_t* m0, const int32_t* off,
                                   double alpha, double beta, int bT, int lower_only,
-                                  int tri, void* stream) {
+                                  int tri, const int64_t* btab, int compact, void* stream) {
   if (ntile < 0) return -1;
   if (ntile == 0) return 0;
   gemm_grouped_kernel<<<ntile, kThreads, 0, as_stream(stream)>>>(tiles, targets, segs, m0, off,
                                                                  alpha, beta, bT, lower_only,
-                                                                 tri);
+                                                                 tri, btab, compact);
   SPAND_CHECK_LAUNCH();
   return 0;
 }

@@ -272,21 +272,22 @@ struct Plan {
 
   struct Target {
     std::vector<int64_t> c;          // 7
-    std::vector<int64_t> segs;       // 14 per segment
+    std::vector<int64_t> segs;       // 14 per segment (or 1 per segment, compact)
     int64_t mm, nn;
   };
   // tri: triangular-operand K bounds (gemm.cu): 1 A lower, 2 B lower with
   // C = A B^T, 4 B lower with C = A B
   void gemm(const std::vector<Target>& ts, double alpha, double beta, int bT, int lower,
-            int tri = 0) {
+            int tri = 0, int compact = 0) {
     if (ts.empty()) return;
+    const int64_t sw = compact ? 1 : 14;
     std::vector<int64_t> trow, srow, tiles;
     int64_t nseg = 0;
     for (size_t t = 0; t < ts.size(); ++t) {
       trow.insert(trow.end(), ts[t].c.begin(), ts[t].c.end());
       trow.push_back(nseg);
       srow.insert(srow.end(), ts[t].segs.begin(), ts[t].segs.end());
-      nseg += (int64_t)ts[t].segs.size() / 14;
+      nseg += (int64_t)ts[t].segs.size() / sw;
       if (dry) continue;
       for (int64_t i = 0; i < ts[t].mm; i += kTile)
         for (int64_t j = 0; j < ts[t].nn; j += kTile) {
@@ -299,6 +300,7 @@ struct Plan {
     if (srow.empty()) srow.assign(14, 0);
     const int64_t a = push(tiles), b = push(trow), c = push(srow);
     launch(3, (int64_t)tiles.size(), a, b, c, bT, lower, tri, alpha, beta);
+    if (!dry) launches[launches.size() - 6] = compact;   // field 10
   }
 
   // batched triangular inverses: 64-tiles + recursive doubling GEMMs
@@ -533,15 +535,13 @@ struct Plan {
             if ((wa == wb) != (diag == 1)) continue;
             Target x;
             opnd(x.c, pool_base + 8 * boff[b], wa, wb);
-            for (int s : L.tsegs[t]) {
-              opnd(x.segs, blk_ptr(wa, s), wa, s);
-              opnd(x.segs, blk_ptr(wb, s), wb, s);
-            }
+            for (int s : L.tsegs[t])
+              x.segs.push_back(((int64_t)block(wa, s) << 32) | (int64_t)block(wb, s));
             x.mm = m0[wa];
             x.nn = m0[wb];
             st.push_back(x);
           }
-          gemm(st, -1.0, 1.0, 1, diag);
+          gemm(st, -1.0, 1.0, 1, diag, 0, 1);
         }
       }
       if (L.skipped) return;

@@ -55,16 +55,51 @@ def to_dev(arr, dtype=None):
     return t.from_numpy(a).to(dev(), non_blocking=False)
 
 
+class PinnedArena:
+    """Grow-only pinned host staging for asynchronous uploads.  Regions are
+    handed out sequentially and recycled by ``reset()``, which callers issue
+    only after a device synchronisation (so no copy still reads them)."""
+
+    def __init__(self):
+        self.buf = None
+        self.at = 0
+
+    def reset(self):
+        self.at = 0
+
+    def take(self, nbytes):
+        t = torch()
+        need = self.at + nbytes
+        if self.buf is None or need > self.buf.numel():
+            # a new (larger) block: earlier regions keep their old buffer
+            # alive through the tensors that reference them
+            size = max(need, 2 * (self.buf.numel() if self.buf is not None else 0), 1 << 24)
+            self.buf = t.empty(size, dtype=t.uint8, pin_memory=True)
+            self.at = 0
+            need = nbytes
+        view = self.buf[self.at:need]
+        self.at = (need + 255) // 256 * 256
+        return view
+
+
+ARENA = PinnedArena()
+
+
 def to_dev_async(arr, dtype=None):
-    """numpy -> device tensor without blocking the host: the array is
-    staged in (cached) pinned memory and copied with non_blocking=True on the
-    current stream, so host-side planning overlaps device work.  The caching
-    host allocator keeps the staging block until the copy has completed."""
+    """numpy -> device tensor without blocking the host: the array is staged
+    in the pinned arena and copied with non_blocking=True on the current
+    stream, so host-side planning overlaps device work."""
     t = torch()
     a = np.ascontiguousarray(arr if dtype is None else arr.astype(dtype))
     if a.nbytes == 0:
         return t.from_numpy(a).to(dev())
-    return t.from_numpy(a).pin_memory().to(dev(), non_blocking=True)
+    stage = ARENA.take(a.nbytes)
+    host = stage.view(t.from_numpy(a).dtype).view(a.shape)
+    host.copy_(t.from_numpy(a))
+    out = t.empty(a.shape, dtype=host.dtype, device=dev())
+    out.copy_(host, non_blocking=True)
+    out._spand_stage = stage   # the staging region outlives the copy
+    return out
 
 
 def as_device_vector(x, n):

@@ -36,7 +36,7 @@ import numpy as np
 
 from . import _lib
 from .dense import SCHEME_CODE, SchemeKind
-from .device import dev, ptr, require_cuda, stream, to_dev, to_dev_async
+from .device import ARENA, dev, ptr, require_cuda, stream, to_dev, to_dev_async
 from .errors import NotSPD
 from .kernels import Geometry, TILE, opnd
 from .schemes import (Elimination, ErrorCorrection, MatView, Orthogonal,
@@ -215,6 +215,12 @@ class Engine:
         gm0, goff = ptr(geo.m0), ptr(geo.off)
         ib, evb = self.info.data_ptr(), self.events.data_ptr()
         import ctypes
+        # block table of the compact Schur segments: {ptr, rc, cc} per block
+        btab = np.stack([pb + 8 * np.asarray(sym.boff, dtype=np.int64),
+                         np.asarray(sym.bi, dtype=np.int64),
+                         np.asarray(sym.bj, dtype=np.int64)], axis=1)
+        self._btab = to_dev_async(np.ascontiguousarray(btab))
+        self._btab_p = ptr(self._btab)
         lib = sym._lib
         vp = sym._vp
         # incremental emission: level l + 1 is planned on the host while the
@@ -263,6 +269,7 @@ class Engine:
         self.timings["plan_s"] = t_plan
         self._keep_run = (temp, ctr, keep)
         t.cuda.synchronize()
+        ARENA.reset()   # every staged upload has completed
         self.timings["device_s"] = time.perf_counter() - tstart
 
     def _launch(self, launches, base, gm0, goff, ib, evb, fb, st, prog=None):
@@ -280,7 +287,7 @@ class Engine:
                 alpha = float(np.int64(rec[8]).view(np.float64))
                 beta = float(np.int64(rec[9]).view(np.float64))
                 _lib.call("spand_gemm_grouped", cnt, P(ao), P(bo), P(co), gm0, goff,
-                          alpha, beta, x0, x1, x2, st)
+                          alpha, beta, x0, x1, x2, self._btab_p, int(rec[10]), st)
             elif typ == 4:
                 _lib.call("spand_copy_batched", cnt, P(ao), gm0, goff, st)
             elif typ == 5:

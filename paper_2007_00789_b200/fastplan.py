@@ -194,10 +194,18 @@ class FastPlan:
         _lib.call("spand_scatter_perm", self.n, ptr(self.perm), ptr(self.xbuf),
                   ptr(xd), st)
 
+    GRAPH_AFTER = 32   # eager applies before a CUDA graph is captured
+
     def run_graph(self, xd):
-        """apply_m in place on a contiguous (n,) fp64 device vector; the
-        whole pass is one CUDA graph (captured on first use)."""
+        """apply_m in place on a contiguous (n,) fp64 device vector.  The
+        first GRAPH_AFTER applies launch eagerly (capturing and instantiating
+        a graph of ~350 kernels costs more than a short PCG solve); a factor
+        reused for many solves switches to one CUDA graph replay."""
         t = require_cuda()
+        self._napply = getattr(self, "_napply", 0) + 1
+        if self._graph is None and self._napply <= self.GRAPH_AFTER:
+            self._run1(xd, True, True)
+            return xd
         if self._graph is None:
             self._gio = t.zeros(self.n, dtype=t.float64, device=dev())
             side = t.cuda.Stream()

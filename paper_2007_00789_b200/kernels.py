@@ -163,7 +163,7 @@ def gemm_grouped(geo, targets, alpha, beta, bT, lower_only=False,
     td, sd, tl = _rows(trow, 8), _rows(srow, 14), _rows(tiles, 1)
     _lib.call("spand_gemm_grouped", int(tiles.shape[0]), ptr(tl), ptr(td), ptr(sd),
               ptr(geo.m0), ptr(geo.off), float(alpha), float(beta), int(bT),
-              int(bool(lower_only)), int(tri), stream())
+              int(bool(lower_only)), int(tri), None, 0, stream())
 
 
 # ---------------------------------------------------------------------------
