@@ -173,6 +173,25 @@ int spand_rrqr_cta_count(void);
  * live rows (the cooperative grid must not exceed it) */
 int spand_rrqr_capacity(int vmax);
 
+/* ---- near-kernel preservation (EXTENSION, not in the reference; SURVEY.md
+ *      §8a-11; CPU restatement oracle/spand_oracle.py sparsify_panel_nk).
+ * U: near-kernel coordinates, column-major (ldu x k, k <= 16) in the
+ * cluster-contiguous numbering.  Row layouts: see nearkernel.cu. ---------- */
+/* u_p <- Z_p^T u_p for rescaled interfaces; rows {p, Z ptr, ustart} */
+int spand_nk_rescale(int ntask, const int64_t* rows, const int32_t* m0, const int32_t* off,
+                     double* U, int64_t ldu, int k, int vmax, void* stream);
+/* column-pivoted Householder basis of u_p (rank by rtol), u_p <- [0; R_u] */
+int spand_nk_basis(int npanel, const int64_t* rows, const int64_t* nbrs, const int32_t* m0,
+                   const int32_t* off, double* U, int64_t ldu, int k, double rtol,
+                   void* stream);
+/* panel W <- [U_perp^T W; U^T W] in the pool blocks (ncols: capacity grid) */
+int spand_nk_deflate(int npanel, int64_t ncols, const int64_t* rows, const int64_t* nbrs,
+                     const int32_t* m0, const int32_t* off, int vmax, void* stream);
+/* Orthogonal op factor [U_perp q2_c, U, U_perp q2_f] from the RRQR's q2 */
+int spand_nk_qform(int npanel, int64_t ncols, const int64_t* rows, const int64_t* events,
+                   int vmax, void* stream);
+int spand_plan_set_nk(void* h, int k);
+
 /* Final dense block (factorize.py:198-220): assemble the live parts of the
  * remaining clusters (cl[ncl] cluster ids, ascending) into the virtual
  * cluster final_id's m0^2 buffer `dst` (zeroed by the caller), packed at the

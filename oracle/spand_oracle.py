@@ -262,6 +262,89 @@ def sparsify_panel(panel, eps, scheme):
 
 
 # ---------------------------------------------------------------------------
+# near-kernel preservation (EXTENSION, not in the reference: SURVEY.md §8a-11;
+# the paper names it as compatible future work).
+# With no vectors every function below reduces to the reference path bitwise.
+
+NK_RTOL = 1e-8
+
+
+def nk_basis(u, rtol=NK_RTOL):
+    """Column-pivoted Householder QR of the restricted near-kernel block
+    ``u`` (m x k): reflectors (v_t on rows t.., tau_t), the rank r (stop when
+    the largest remaining column tail is <= rtol x the largest column norm)
+    and R_u = (H^T u)[:r] with H = H_0 ... H_{r-1}.  Reflector convention of
+    the reference RRQR (dense.py:155-159): beta = -sign(x0) eta."""
+    x = np.array(u, dtype=np.float64, copy=True)
+    m, k = x.shape
+    vs, taus = [], []
+    if m == 0 or k == 0:
+        return vs, taus, x[:0]
+    nrm0 = float(np.sqrt(np.max(np.einsum("ij,ij->j", x, x))))
+    used = np.zeros(k, dtype=bool)
+    for t in range(min(m, k)):
+        tails = np.einsum("ij,ij->j", x[t:], x[t:])
+        tails[used] = -1.0
+        c = int(np.argmax(tails))
+        eta = float(np.sqrt(tails[c]))
+        if nrm0 == 0.0 or eta <= rtol * nrm0:
+            break
+        col = x[t:, c]
+        beta = -eta if col[0] >= 0.0 else eta
+        v = col.copy()
+        v[0] -= beta
+        tau = 2.0 / (v @ v)
+        x[t:, :] -= np.outer(v, tau * (v @ x[t:, :]))
+        used[c] = True
+        vs.append(v)
+        taus.append(tau)
+    return vs, taus, x[:len(vs)].copy()
+
+
+def nk_reflect(vs, taus, a):
+    """H^T a = H_{r-1} ... H_0 a (rows of a)."""
+    y = np.array(a, dtype=np.float64, copy=True)
+    for t, (v, tau) in enumerate(zip(vs, taus)):
+        y[t:] -= np.outer(v, tau * (v @ y[t:]))
+    return y
+
+
+def nk_explicit(vs, taus, m):
+    """H = H_0 ... H_{r-1} as an explicit m x m matrix."""
+    h = np.eye(m)
+    for t in range(len(vs) - 1, -1, -1):
+        v, tau = vs[t], taus[t]
+        h[t:] -= np.outer(v, tau * (v @ h[t:]))
+    return h
+
+
+def sparsify_panel_nk(panel, u, eps, scheme):
+    """Sparsification that keeps span(u) (the interface's restricted
+    near-kernel vectors, m x k) inside the coarse basis.
+
+    With H from ``nk_basis`` (U = H[:, :r], U_perp = H[:, r:]) the RRQR runs
+    on the deflated panel U_perp^T W; the coarse basis is [U_perp q2_c, U]
+    and the fine basis U_perp q2_f, so q = [q_f, q_c] stays orthogonal and
+    fine-first.  r_coarse gains the rows U^T W; e_tilde is the RRQR's
+    (q2_f^T U_perp^T W).  Returns (res, r, R_u); r == 0 is the reference
+    path exactly (``sparsify_panel``)."""
+    m, n = panel.shape
+    vs, taus, ru = nk_basis(u) if n else ([], [], np.zeros((0, u.shape[1])))
+    r = len(vs)
+    if r == 0:
+        return sparsify_panel(panel, eps, scheme), 0, ru
+    y = nk_reflect(vs, taus, panel)
+    res = sparsify_panel(y[r:], eps, scheme)
+    h = nk_explicit(vs, taus, m)
+    hp, hu = h[:, r:], h[:, :r]
+    res["q_f"] = np.ascontiguousarray(hp @ res["q_f"])
+    res["q_c"] = np.ascontiguousarray(np.hstack([hp @ res["q_c"], hu]))
+    res["r_coarse"] = np.ascontiguousarray(np.vstack([res["r_coarse"], y[:r]]))
+    res["rank_c"] += r
+    return res, r, ru
+
+
+# ---------------------------------------------------------------------------
 # operators  (schemes.py:78-196)
 
 
@@ -362,6 +445,7 @@ class _Trailing:
         self.depth = {cid: dep for cid, _, dep in clusters}
         self.alive = set(self.dofs)
         self.adj = {cid: set() for cid in self.alive}
+        self.nk = None          # near-kernel coordinates (extension), n x k
         owner = np.full(n, -1, dtype=np.int64)
         slot = np.empty(n, dtype=np.int64)
         for cid, d in self.dofs.items():
@@ -457,6 +541,10 @@ class _Trailing:
         nbrs = sorted(self.adj[cid])
         panel, _, offs = self.row(cid, nbrs)
         lower = chol(self.blk[(cid, cid)])
+        if self.nk is not None:
+            # near-kernel coordinates follow the congruence: u_p <- Z_p^T u_p
+            d = self.dofs[cid]
+            self.nk[d] = lower.T @ self.nk[d]
         if panel.size:
             scaled = solve_triangular(lower, panel, lower=True, trans=0,
                                       check_finite=False)
@@ -470,9 +558,16 @@ class _Trailing:
         """factorize.py:175-196 + schemes.py:272-318."""
         nbrs = sorted(self.adj[cid])
         panel, w_dofs, offs = self.row(cid, nbrs)
-        res = sparsify_panel(panel, eps, scheme)
         old = self.dofs[cid]
         m = old.size
+        if self.nk is None:
+            res = sparsify_panel(panel, eps, scheme)
+        else:
+            res, r, ru = sparsify_panel_nk(panel, self.nk[old], eps, scheme)
+            if r:
+                # new coordinates: 0 on every slot but the last r (= R_u)
+                self.nk[old] = 0.0
+                self.nk[old[m - r:]] = ru
         n_fine = m - res["rank_c"]
         ops = [Op("Q", old, q=np.hstack([res["q_f"], res["q_c"]]))]
         ops[0].pivots = res["pivots"][:res["k_stop"]]   # test-side metadata
@@ -516,9 +611,10 @@ class _Trailing:
 
 
 def factorize(n, row_ptr, col_idx, values, clusters, levels, eps, scheme,
-              skip_levels=4):
+              skip_levels=4, near_kernel=None):
     """Level loop L..1 (factorize.py:285-366).  ``clusters`` is the
-    [(id, dofs, depth)] list of ``nd_hierarchy``."""
+    [(id, dofs, depth)] list of ``nd_hierarchy``.  ``near_kernel`` (n or
+    n x k, EXTENSION) switches on ``sparsify_panel_nk``."""
     if scheme not in SCHEMES:
         raise ValueError(f"unknown scheme {scheme!r}")
     if not 0.0 <= eps <= 1.0:
@@ -527,6 +623,10 @@ def factorize(n, row_ptr, col_idx, values, clusters, levels, eps, scheme,
         raise ValueError("skip_levels must be nonnegative")
     st = _Trailing(n, np.asarray(row_ptr), np.asarray(col_idx),
                    np.asarray(values, dtype=np.float64), clusters)
+    if near_kernel is not None:
+        nk = np.array(near_kernel, dtype=np.float64, copy=True)
+        nk = nk.reshape(n, -1)
+        st.nk = nk if nk.shape[1] else None
     ops, perm_parts, diag = [], [], []
     for level in range(levels, 0, -1):
         inner = sorted(c for c in st.alive if st.depth[c] == level)

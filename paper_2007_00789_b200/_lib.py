@@ -48,6 +48,11 @@ SIGNATURES = {
     "spand_plan_emit": [_P, _c_i64, _c_i64, _c_i64, _c_i64, _c_int],
     "spand_plan_program": [_P, _P, _P],
     "spand_plan_meta": [_P, _P],
+    "spand_plan_set_nk": [_P, _c_int],
+    "spand_nk_rescale": [_c_int, _P, _P, _P, _P, _c_i64, _c_int, _c_int, _P],
+    "spand_nk_basis": [_c_int, _P, _P, _P, _P, _P, _c_i64, _c_int, _c_dbl, _P],
+    "spand_nk_deflate": [_c_int, _c_i64, _P, _P, _P, _P, _c_int, _P],
+    "spand_nk_qform": [_c_int, _c_i64, _P, _P, _c_int, _P],
 }
 
 _lib = None

@@ -18,6 +18,9 @@
 //        4 copy(a=ops)  5 rrqr wave(a=panels, b=nbrs, x0=grid, x1=vmax)
 //        6 assemble final(a=cluster ids, b=block rows, x0=nblk, x1=final id,
 //          x2=fac offset of the dense block)
+//        near-kernel extension (nearkernel.cu): 7 rescale(a=rows, x0=vmax)
+//        8 basis(a=nk rows, b=nbrs)  9 deflate(a, b, x0=grid, x1=vmax)
+//        10 qform(a=nk rows, x0=grid, x1=vmax)
 // Offsets are in int64 units into the program array.
 #include <algorithm>
 #include <cstdint>
@@ -76,6 +79,16 @@ int64_t spand_plan_pairs(int ncl, const int64_t* row_ptr, const int64_t* col_idx
     for (int cj : list) out[cnt++] = (int64_t)ci * ncl + cj;
   }
   return cnt;
+}
+
+// near-kernel extension: number of vectors (0 = reference path); resizes
+// the workspace bound, so call before spand_plan_sizes / emission
+int spand_plan_set_nk(void* h, int k) {
+  Plan* p = static_cast<Plan*>(h);
+  if (k < 0 || k > 16) return -1;
+  p->nk = k;
+  p->layout();
+  return 0;
 }
 
 // cluster dofs (original numbering) concatenated in id order, dptr[ncl+1]

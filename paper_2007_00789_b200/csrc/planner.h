@@ -49,6 +49,9 @@ struct Plan {
   // program
   std::vector<int64_t> prog, launches;
   int cap_override = 0;
+  int nk = 0;   // near-kernel vectors (extension; 0: reference path)
+  static constexpr int64_t kNkHead = 19;   // nearkernel.cu kWsHead
+  int64_t nk_ws(int64_t mc) const { return nk ? kNkHead + 2 * mc * nk + mc * mc : 0; }
 
   int64_t key(int i, int j) const { return (int64_t)i * ncl + j; }
   int block(int i, int j) const { return bid.at(key(i, j)); }
@@ -227,7 +230,7 @@ struct Plan {
           for (int w : L.anbrs[k]) ncap += m0[w];
           const int64_t mc = m0[L.active[k]];
           rq += mc * std::max<int64_t>(ncap, 1) + mc * mc + 32 * (ncap + mc) + 2 * ncap +
-                3 * mc + 8 + 1024 + (3 * ncap + 1) / 2 + 1 + 1 + 68;
+                3 * mc + 8 + 1024 + (3 * ncap + 1) / 2 + 1 + 1 + 68 + nk_ws(mc);
         }
         need = std::max(need, rq);
       }
@@ -571,6 +574,17 @@ struct Plan {
       if (na) {
         launch(4, (int64_t)na, push(c1));
         potrf(pops, 0);
+        if (nk) {
+          // near-kernel coordinates: u_p <- Z_p^T u_p (nearkernel.cu)
+          std::vector<int64_t> rr;
+          int64_t vm = 1;
+          for (size_t k = 0; k < na; ++k) {
+            const int p = L.active[k];
+            rr.insert(rr.end(), {p, fac_base + 8 * L.l_off[k], dptr[p]});
+            vm = std::max(vm, m0[p]);
+          }
+          launch(7, (int64_t)na, push(rr), 0, 0, vm);
+        }
         trtri(Ls, Xs, sz, 0);
         launch(4, (int64_t)na, push(c2));
       }
@@ -622,8 +636,8 @@ struct Plan {
             works.push_back(std::max<int64_t>(1, m0[L.active[k]] * std::max<int64_t>(ncap, 1)));
           }
           const std::vector<int> gs = groups(works, cap);
-          std::vector<int64_t> prow, nrow;
-          int64_t need = 0, gbeg = 0, vmax = 1;
+          std::vector<int64_t> prow, nrow, krow;
+          int64_t need = 0, gbeg = 0, vmax = 1, colbeg = 0, qbeg = 0;
           for (size_t u = c0; u < c1e; ++u) {
             const size_t k = pan[u];
             const int p = L.active[k];
@@ -640,19 +654,39 @@ struct Plan {
               else nrow.insert(nrow.end(), {w, blk_ptr(w, p), 1, 0});
             }
             const int64_t nb1 = (int64_t)nrow.size() / 4;
+            int64_t qdst = fac_base + 8 * L.q_off[k], nkws = 0;
+            if (nk) {
+              // near-kernel: the RRQR writes q2 into the workspace, nk_qform
+              // builds the Orthogonal op's factor in its fac slot
+              nkws = temp_base + 8 * (need + wsz + asz + isz + 1);
+              const int64_t q2 = nkws + 8 * (kNkHead + 2 * mc * nk);
+              krow.insert(krow.end(), {p, nkws, q2, qdst, nb0, nb1, colbeg, qbeg, L.slot[k],
+                                       dptr[p]});
+              colbeg += ncap;
+              qbeg += mc;
+              qdst = q2;
+            }
             prow.insert(prow.end(),
-                        {p, nb0, nb1, temp_base + 8 * need, fac_base + 8 * L.q_off[k],
+                        {p, nb0, nb1, temp_base + 8 * need, qdst,
                          temp_base + 8 * (need + wsz), temp_base + 8 * (need + wsz + asz), gbeg,
-                         g, ctr_base + 8 * ctr_next, L.slot[k], ncap, mc, 0, 0, 0});
+                         g, ctr_base + 8 * ctr_next, L.slot[k], ncap, mc, nkws, 0, 0});
             ++ctr_next;
-            need += wsz + asz + isz + 1;
+            need += wsz + asz + isz + 1 + nk_ws(mc);
             gbeg += g;
             vmax = std::max(vmax, mc);
           }
           if (nrow.empty()) nrow.assign(4, 0);
           temp_size = std::max(temp_size, need);
           const int64_t a = push(prow), b = push(nrow);
-          launch(5, (int64_t)(c1e - c0), a, b, 0, gbeg, vmax);
+          const int64_t np = (int64_t)(c1e - c0);
+          int64_t kr = 0;
+          if (nk) {
+            kr = push(krow);
+            launch(8, np, kr, b);                   // basis of u_p, rank r
+            launch(9, np, kr, b, 0, colbeg, vmax);  // W <- rotate(H^T W)
+          }
+          launch(5, np, a, b, 0, gbeg, vmax);
+          if (nk) launch(10, np, kr, 0, 0, qbeg, vmax);   // Q = [U_perp q2_c, U, U_perp q2_f]
         }
       }
     }

@@ -38,7 +38,8 @@ constexpr int kMaxM = 6144;  // v in shared memory
 //  0 p        1 nbr_begin  2 nbr_end   3 W (double*, temp, >= m*n)
 //  4 Q (double*, m*m, compact ld = m)  5 aux (double*)  6 iaux (int32*)
 //  7 group_begin  8 group_size  9 counters (uint32[2]: arrivals, release)  10 event slot
-//  11 ncap (column capacity of aux arrays)  12 mcap  13-15 unused
+//  11 ncap (column capacity of aux arrays)  12 mcap
+//  13 near-kernel workspace (nearkernel.cu; 0: none)  14-15 unused
 // nbr row (4 int64): {w, block ptr, orientation, 0}
 //  orientation 0: block (p, w) stored with rows of p (ld = m0[p])
 //  orientation 1: block (w, p) stored with rows of w (ld = m0[w])
@@ -460,7 +461,11 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
 
   const int offp = off[p];
   const int ldp = m0[p];
-  const int m = ldp - offp;
+  // near-kernel extension (nearkernel.cu): the last nkr live rows hold the
+  // near-kernel directions U^T W and stay coarse; only the first m rows are
+  // factored.  nkr = 0 (no workspace) is the reference path.
+  const int nkr = P[13] ? (int)reinterpret_cast<const double*>(P[13])[0] : 0;
+  const int m = ldp - offp - nkr;
   // column layout over neighbours (live columns at kernel start): block
   // prefix scan of the live widths
   constexpr int kMaxNb = 1024;
@@ -1440,10 +1445,10 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
   if (rank == 0 && tid == 0) {
     int64_t* ev = events + 12 * slot;
     ev[0] = p;
-    ev[1] = m;
+    ev[1] = m + nkr;
     ev[2] = n;
-    ev[3] = k_stop;
-    ev[4] = k_c;
+    ev[3] = k_stop + nkr;
+    ev[4] = k_c + nkr;
     ev[5] = (scheme == 2) ? k_stop - k_c : 0;
     ev[6] = n_fine;
     ev[7] = __double_as_longlong(eta_last);

@@ -46,6 +46,7 @@ import os as _os
 from collections.abc import Sequence
 
 WAVE_LOG = None      # set to [] to record per-wave CUDA events (profiling)
+NK_RTOL = 1e-8       # rank threshold of the near-kernel basis (oracle NK_RTOL)
 EVENT_ROW = 12
 MAX_PANEL_ROWS = 6144
 
@@ -56,7 +57,7 @@ class NativePlan:
     ``meta`` decodes the scheduler's structure export into per-level
     records used by ``collect`` (operator assembly on the host)."""
 
-    def __init__(self, a, h, skip_levels, cap_override=0):
+    def __init__(self, a, h, skip_levels, cap_override=0, nk=0):
         import ctypes
         t0 = time.perf_counter()
         lib = _lib.load()
@@ -95,6 +96,9 @@ class NativePlan:
         self._vp = vp
         lib.spand_plan_set_dofs.argtypes = [ctypes.c_void_p] * 3
         lib.spand_plan_set_dofs(self.h, vp(dcat), vp(dptr))
+        if nk:
+            if lib.spand_plan_set_nk(self.h, int(nk)) != 0:
+                raise ValueError(f"at most 16 near-kernel vectors, got {nk}")
         self.sizes()
         self._decode_meta()
         self.seconds = time.perf_counter() - t0
@@ -182,12 +186,14 @@ class NativePlan:
 
 
 class Engine:
-    def __init__(self, a, h, eps, scheme, skip_levels):
+    def __init__(self, a, h, eps, scheme, skip_levels, near_kernel=None):
         self.t = require_cuda()
         self.a, self.h = a, h
         self.eps, self.scheme, self.skip = eps, scheme, skip_levels
+        self.nk = near_kernel      # n x k host array (extension) or None
         self.sym = NativePlan(a, h, skip_levels,
-                              int(_os.environ.get("SPAND_RRQR_CAP", "0")))
+                              int(_os.environ.get("SPAND_RRQR_CAP", "0")),
+                              0 if near_kernel is None else near_kernel.shape[1])
         self.timings = {"symbolic_s": self.sym.seconds}
 
     # -------------------------------------------------------------- numeric
@@ -211,6 +217,11 @@ class Engine:
         ctr = t.zeros(2 * max(sym.n_ctr, 1), dtype=t.int32, device=d)   # {arrivals, release} per panel
         pb, fb = pool.data_ptr(), fac.data_ptr()
         temp = t.empty(max(sym.temp_bound, 1), dtype=t.float64, device=d)
+        if self.nk is not None:
+            # near-kernel coordinates in the cluster-contiguous numbering,
+            # column-major n x k (vector v at nkbuf[v])
+            perm_c = np.concatenate(sym.dofs)
+            self.nkbuf = to_dev(np.ascontiguousarray(self.nk[perm_c].T))
         st = stream()
         gm0, goff = ptr(geo.m0), ptr(geo.off)
         ib, evb = self.info.data_ptr(), self.events.data_ptr()
@@ -302,6 +313,18 @@ class Engine:
                     e1.record()
                     slots = [int(prog[ao + 16 * q + 10]) for q in range(cnt)] if prog is not None else []
                     WAVE_LOG.append((cnt, x0, x1, e0, e1, slots))
+            elif typ in (7, 8, 9, 10):
+                U, k = self.nkbuf, self.nkbuf.shape[0]
+                if typ == 7:
+                    _lib.call("spand_nk_rescale", cnt, P(ao), gm0, goff, ptr(U),
+                              U.shape[1], k, x0, st)
+                elif typ == 8:
+                    _lib.call("spand_nk_basis", cnt, P(ao), P(bo), gm0, goff, ptr(U),
+                              U.shape[1], k, NK_RTOL, st)
+                elif typ == 9:
+                    _lib.call("spand_nk_deflate", cnt, x0, P(ao), P(bo), gm0, goff, x1, st)
+                else:
+                    _lib.call("spand_nk_qform", cnt, x0, P(ao), ctypes.c_void_p(evb), x1, st)
             elif typ == 6:
                 _lib.call("spand_assemble_final", cnt, P(ao), x0, P(bo), gm0, goff,
                           x1, ctypes.c_void_p(fb + 8 * x2), st)
@@ -519,10 +542,11 @@ def ctypes_ptr(addr):
     return ctypes.c_void_p(int(addr))
 
 
-def run_factorization(a, h, eps, scheme, skip_levels, collect_local_errors=False):
+def run_factorization(a, h, eps, scheme, skip_levels, collect_local_errors=False,
+                      near_kernel=None):
     from .factorize import Factorization
     t0 = time.perf_counter()
-    eng = Engine(a, h, eps, scheme, skip_levels)
+    eng = Engine(a, h, eps, scheme, skip_levels, near_kernel)
     eng.run()
     ops, perm, diag, nnz = eng.collect()
     eng.timings["total_s"] = time.perf_counter() - t0

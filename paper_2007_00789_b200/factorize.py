@@ -98,8 +98,12 @@ def factorize(a, hierarchy, eps, scheme, skip_levels=4,
     finest to the coarsest, interiors eliminated, then (outside the first
     ``skip_levels`` levels) every active interface rescaled and sparsified
     in ascending id order; the leftover clusters form one dense block.
-    ``near_kernel`` (extension, off by default) is accepted for API
-    stability and must be None in this build.
+    ``near_kernel`` (EXTENSION, off by default; not in the reference): an
+    n-vector or n x k array (k <= 16) of near-kernel vectors, e.g. the
+    constant vector or rigid-body modes.  Each sparsification then keeps the
+    vectors' restriction to the interface (carried through the factor's
+    congruences) inside the coarse basis, so the preconditioner stays
+    accurate on them.  None or k = 0 is the reference path exactly.
     """
     if isinstance(scheme, str):
         scheme = SchemeKind.from_string(scheme)
@@ -110,11 +114,20 @@ def factorize(a, hierarchy, eps, scheme, skip_levels=4,
     if a.n != hierarchy.n:
         raise DimensionMismatch(
             f"matrix has {a.n} dofs but hierarchy covers {hierarchy.n}")
+    nk = None
     if near_kernel is not None:
-        raise NotImplementedError("near-kernel preservation is not built yet")
+        nk = np.asarray(near_kernel, dtype=np.float64)
+        if nk.ndim not in (1, 2) or nk.shape[0] != a.n:
+            raise DimensionMismatch(
+                f"near_kernel must have {a.n} rows, got shape {nk.shape}")
+        nk = nk.reshape(a.n, -1)
+        if nk.shape[1] > 16:
+            raise ValueError(f"at most 16 near-kernel vectors, got {nk.shape[1]}")
+        if nk.shape[1] == 0:
+            nk = None
     from .engine import run_factorization
     return run_factorization(a, hierarchy, float(eps), scheme, int(skip_levels),
-                             collect_local_errors)
+                             collect_local_errors, near_kernel=nk)
 
 
 # ---------------------------------------------------------------------------
