@@ -16,6 +16,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _lib
+from .errors import DimensionMismatch
 
 
 @dataclass(frozen=True)
@@ -114,12 +115,47 @@ def _adjacency(a):
     return ptr, np.ascontiguousarray(a.col_idx[keep], dtype=np.int64)
 
 
-def build_hierarchy(a, levels):
-    """Recursive vertex-separator dissection of the graph of A (native)."""
-    n = int(a.n)
+def node_graph(a, block):
+    """CSR pattern (row_ptr, col_idx, int64) of the graph whose vertices are
+    the dof blocks {block*v, ..., block*v + block - 1} (e.g. the 3 dofs of an
+    elasticity node): v ~ w iff any of their dofs are coupled in A."""
+    if a.n % block:
+        raise DimensionMismatch(f"n = {a.n} is not a multiple of block = {block}")
+    nv = a.n // block
+    rows = np.repeat(np.arange(a.n, dtype=np.int64), np.diff(a.row_ptr)) // block
+    cols = np.asarray(a.col_idx, dtype=np.int64) // block
+    key = np.unique(rows * nv + cols)
+    r, c = key // nv, key % nv
+    ptr = np.zeros(nv + 1, dtype=np.int64)
+    np.cumsum(np.bincount(r, minlength=nv), out=ptr[1:])
+    return nv, ptr, np.ascontiguousarray(c, dtype=np.int64)
+
+
+def build_hierarchy(a, levels, block=1):
+    """Recursive vertex-separator dissection of the graph of A (native).
+
+    ``block`` > 1 (EXTENSION for BASELINE config C5, not in the reference):
+    dissect the graph of dof blocks (``node_graph``) with the same
+    bisection, then expand every vertex to its ``block`` consecutive dofs, so
+    the dofs of one node always share a cluster."""
+    if block > 1:
+        nv, rp, ci = node_graph(a, block)
+        hn = _dissect(nv, rp, ci, levels)
+        clusters = [Cluster(id=c.id, dofs=(block * c.dofs[:, None] +
+                                            np.arange(block)).ravel(), depth=c.depth)
+                    for c in hn]
+        adj_ptr, adj_idx = _adjacency(a)
+        return PartitionHierarchy(int(levels), int(a.n), clusters, adj_ptr, adj_idx)
+    clusters = _dissect(int(a.n), a.row_ptr, a.col_idx, levels)
+    adj_ptr, adj_idx = _adjacency(a)
+    return PartitionHierarchy(int(levels), int(a.n), clusters, adj_ptr, adj_idx)
+
+
+def _dissect(n, row_ptr, col_idx, levels):
+    n = int(n)
     levels = int(levels)
-    rp = np.ascontiguousarray(a.row_ptr, dtype=np.int64)
-    ci = np.ascontiguousarray(a.col_idx, dtype=np.int64)
+    rp = np.ascontiguousarray(row_ptr, dtype=np.int64)
+    ci = np.ascontiguousarray(col_idx, dtype=np.int64)
     dofs = np.empty(n, dtype=np.int64)
     cptr = np.empty(n + 1, dtype=np.int64)
     depth = np.empty(max(n, 1), dtype=np.int32)
@@ -128,7 +164,5 @@ def build_hierarchy(a, levels):
     _lib.call("spand_nd_partition", n, p(rp), p(ci), levels, p(dofs), p(cptr),
               p(depth), p(ncl))
     k = int(ncl[0])
-    clusters = [Cluster(id=i, dofs=dofs[cptr[i]:cptr[i + 1]].copy(),
-                        depth=int(depth[i])) for i in range(k)]
-    adj_ptr, adj_idx = _adjacency(a)
-    return PartitionHierarchy(levels, n, clusters, adj_ptr, adj_idx)
+    return [Cluster(id=i, dofs=dofs[cptr[i]:cptr[i + 1]].copy(), depth=int(depth[i]))
+            for i in range(k)]

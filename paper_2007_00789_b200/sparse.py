@@ -326,6 +326,106 @@ def log_uniform_block_field(shape, block, decades, rng):
     return a
 
 
+def _q1_element_stiffness(h, nu):
+    """24 x 24 stiffness of a cube Q1 hexahedron of side h, E = 1, 2x2x2
+    Gauss points; dof order (node, component), local nodes lexicographic in
+    (x, y, z) with x fastest.  Exactly symmetric."""
+    lam = nu / ((1.0 + nu) * (1.0 - 2.0 * nu))
+    mu = 1.0 / (2.0 * (1.0 + nu))
+    d = np.zeros((6, 6))
+    d[:3, :3] = lam
+    d[np.arange(3), np.arange(3)] += 2.0 * mu
+    d[np.arange(3, 6), np.arange(3, 6)] = mu
+    corners = np.array([[a, b, c] for c in (0, 1) for b in (0, 1) for a in (0, 1)],
+                       dtype=np.float64) * 2.0 - 1.0
+    g = 1.0 / np.sqrt(3.0)
+    ke = np.zeros((24, 24))
+    for gz in (-g, g):
+        for gy in (-g, g):
+            for gx in (-g, g):
+                xi = np.array([gx, gy, gz])
+                # dN/dxi for the 8 nodes, then dN/dx = dN/dxi * 2 / h
+                dn = np.empty((8, 3))
+                for a in range(8):
+                    s = corners[a]
+                    f = 1.0 + s * xi
+                    dn[a, 0] = s[0] * f[1] * f[2] / 8.0
+                    dn[a, 1] = f[0] * s[1] * f[2] / 8.0
+                    dn[a, 2] = f[0] * f[1] * s[2] / 8.0
+                dn *= 2.0 / h
+                bm = np.zeros((6, 24))
+                for a in range(8):
+                    x, y, z = dn[a]
+                    c = 3 * a
+                    bm[0, c], bm[1, c + 1], bm[2, c + 2] = x, y, z
+                    bm[3, c], bm[3, c + 1] = y, x
+                    bm[4, c + 1], bm[4, c + 2] = z, y
+                    bm[5, c], bm[5, c + 2] = z, x
+                ke += bm.T @ d @ bm * (h ** 3 / 8.0)
+    return 0.5 * (ke + ke.T)
+
+
+def elasticity_q1(ne, block, decades, rng, nu=0.3):
+    """3D linear elasticity on ne^3 trilinear (Q1) hexahedra of the unit
+    cube, 3 dofs per node, clamped on the x = 0 face (BASELINE config C5).
+    Young's modulus is piecewise constant on block^3 elements, one value
+    10**U(-decades, decades) per block drawn from ``rng`` (drawn first).
+
+    Free nodes are numbered lexicographically (x fastest) over the
+    (ne+1)^3 grid minus the x = 0 face; dof = 3 * node + component.
+    Returns (A, coords[n_nodes, 3])."""
+    nb = ne // block
+    if nb * block != ne:
+        raise DimensionMismatch("element grid must be a multiple of the block size")
+    young = 10.0 ** rng.uniform(-decades, decades, size=(nb, nb, nb))
+    h = 1.0 / ne
+    ke = _q1_element_stiffness(h, nu)
+    nn = ne + 1
+    gid = np.arange(nn ** 3).reshape(nn, nn, nn)       # [z, y, x]
+    free = gid[:, :, 1:].ravel()
+    node_of = np.full(nn ** 3, -1, dtype=np.int64)
+    node_of[free] = np.arange(free.size)
+    ez, ey, ex = np.meshgrid(np.arange(ne), np.arange(ne), np.arange(ne), indexing="ij")
+    ez, ey, ex = ez.ravel(), ey.ravel(), ex.ravel()
+    loc = [(a, b, c) for c in (0, 1) for b in (0, 1) for a in (0, 1)]
+    enodes = np.stack([gid[ez + c, ey + b, ex + a] for a, b, c in loc], axis=1)
+    edofs = (3 * node_of[enodes][:, :, None] + np.arange(3)).reshape(-1, 24)
+    scale = young[ez // block, ey // block, ex // block]
+    rows = np.repeat(edofs, 24, axis=1).ravel()
+    cols = np.tile(edofs, (1, 24)).ravel()
+    vals = (scale[:, None, None] * ke[None]).ravel()
+    keep = (rows >= 0) & (cols >= 0)      # clamped dofs: homogeneous Dirichlet
+    import scipy.sparse as sps
+    n = 3 * free.size
+    m = sps.coo_matrix((vals[keep], (rows[keep], cols[keep])), shape=(n, n)).tocsr()
+    m.sum_duplicates()
+    # duplicate sums may round differently in the two triangles: average them
+    # (x + y == y + x in IEEE, so the result is exactly symmetric)
+    m = ((m + m.T) * 0.5).tocsr()
+    m.sort_indices()
+    zz, yy, xx = np.unravel_index(free, (nn, nn, nn))
+    coords = np.stack([xx, yy, zz], axis=1).astype(np.float64) * h
+    a = SparseSymMatrix(n, m.indptr.astype(np.int64), m.indices.astype(np.int64),
+                        m.data.astype(np.float64))
+    return a, coords
+
+
+def rigid_body_modes(coords, center=None):
+    """The 6 rigid-body modes (3 translations, 3 rotations about ``center``,
+    default the centroid of the full mesh) as an (3 n_nodes) x 6 array in the
+    node-major dof order of ``elasticity_q1``."""
+    c = np.full(3, 0.5) if center is None else np.asarray(center, dtype=np.float64)
+    x, y, z = (coords - c).T
+    nn = coords.shape[0]
+    r = np.zeros((nn, 3, 6))
+    for k in range(3):
+        r[:, k, k] = 1.0
+    r[:, 1, 3], r[:, 2, 3] = -z, y          # about x
+    r[:, 0, 4], r[:, 2, 4] = z, -x          # about y
+    r[:, 0, 5], r[:, 1, 5] = -y, x          # about z
+    return r.reshape(3 * nn, 6)
+
+
 BASELINE_CONFIGS = {
     # name: (grid, block, decades, seed, levels)
     "C1": ((128, 128), None, 0.0, 0, 7),
@@ -336,11 +436,17 @@ BASELINE_CONFIGS = {
 
 
 def baseline_problem(name, grid=None):
-    """(A, b, levels) for BASELINE.json config ``name`` (C1-C4).
+    """(A, b, levels) for BASELINE.json config ``name`` (C1-C5).
+
+    C5 (elasticity) levels refer to the NODE graph (``build_hierarchy(a,
+    levels, block=3)``); ``c5_problem`` also returns the coordinates.
 
     ``grid`` overrides the grid side (same construction, smaller size) for
     tests; the field is drawn first, then ``b = rng.standard_normal(n)``.
     """
+    if name == "C5":
+        a, b, levels, _ = c5_problem(grid)
+        return a, b, levels
     shape, block, decades, seed, levels = BASELINE_CONFIGS[name]
     if grid is not None:
         shape = tuple([grid] * len(shape))
@@ -353,3 +459,16 @@ def baseline_problem(name, grid=None):
         a = diffusion_fv(log_uniform_block_field(shape, block, decades, rng))
     b = rng.standard_normal(a.n)
     return a, b, levels
+
+
+def c5_problem(ne=None):
+    """BASELINE config C5: (A, b, levels, coords); ne elements per axis
+    (default 24), E blocks of 4^3 elements (ne // 6 for smaller ne), seed 4,
+    levels = default_levels(number of nodes) on the node graph."""
+    from .partition import default_levels
+    ne = 24 if ne is None else int(ne)
+    block = 4 if ne == 24 else max(1, ne // 6)
+    rng = np.random.default_rng(4)
+    a, coords = elasticity_q1(ne, block, 2.0, rng)
+    b = rng.standard_normal(a.n)
+    return a, b, default_levels(coords.shape[0]), coords

@@ -7,6 +7,7 @@ box, so its outputs travel as the fixtures written here):
     PYTHONDONTWRITEBYTECODE=1 OPENBLAS_NUM_THREADS=1 \
         PYTHONPATH=/root/reference/pkg/src:. python tests/golden/make_golden.py small
     ... python tests/golden/make_golden.py config C2 second-full 1e-2 [levels]
+    ... python tests/golden/make_golden.py c5 12|24
 
 Inputs come from this package's generators (``baseline_problem``;
 ``laplacian_2d`` is bit-identical to the reference's) and are handed to the
@@ -78,11 +79,22 @@ def op_record(op):
     return rec
 
 
+def to_ref_hierarchy(h):
+    """Our (node-blocked) hierarchy as the reference's own PartitionHierarchy
+    object: ``factorize`` takes the hierarchy as an argument
+    (factorize.py:285), so both sides see the same clusters."""
+    from spdkit.partition import Cluster as RCluster, PartitionHierarchy as RPH
+    cl = [RCluster(id=c.id, dofs=np.asarray(c.dofs, dtype=np.int64), depth=c.depth)
+          for c in h.clusters]
+    return RPH(h.levels, h.n, cl, h._adj_ptr, h._adj_idx)
+
+
 def run_case(tag, a, b, levels, eps, scheme, skip_levels=4, tol=1e-12,
-             full=True, store_factor=False, store_ops=True):
+             full=True, store_factor=False, store_ops=True, hierarchy=None):
     ra = to_ref(a)
     t0 = time.perf_counter()
-    h = spdkit.build_hierarchy(ra, levels)
+    h = (spdkit.build_hierarchy(ra, levels) if hierarchy is None
+         else to_ref_hierarchy(hierarchy))
     t_hier = time.perf_counter() - t0
     t0 = time.perf_counter()
     f = spdkit.factorize(ra, h, eps, scheme, skip_levels=skip_levels)
@@ -183,9 +195,22 @@ def config(name, scheme, eps, levels=None):
              full=(a.n <= 40000), store_ops=(a.n <= 40000))
 
 
+def c5(ne):
+    """BASELINE config C5 (Q1 elasticity, node-blocked hierarchy built by
+    this package's native ND on the node graph, handed to the reference)."""
+    from paper_2007_00789_b200.partition import build_hierarchy
+    a, b, lv, _ = gen.c5_problem(ne)
+    h = build_hierarchy(a, lv, block=3)
+    tag = f"C5_ne{ne}_L{lv}_e0.01_second-full"
+    run_case(tag, a, b, lv, 0.01, "second-full", full=(a.n <= 40000),
+             store_ops=(a.n <= 40000), hierarchy=h)
+
+
 if __name__ == "__main__":
     if sys.argv[1] == "small":
         small()
+    elif sys.argv[1] == "c5":
+        c5(int(sys.argv[2]))
     else:
         config(sys.argv[2], sys.argv[3], float(sys.argv[4]),
                sys.argv[5] if len(sys.argv) > 5 else None)

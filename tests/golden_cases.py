@@ -33,8 +33,17 @@ def matrix_for(tag):
         r = np.random.default_rng(3)
         return gen.diffusion_fv(
             gen.log_uniform_block_field((16, 16, 16), 4, 3.0, r))
+    if tag.startswith("C5_ne"):
+        return gen.c5_problem(int(tag.split("_")[1][2:]))[0]
     name = tag.split("_")[0]
     return gen.baseline_problem(name)[0]
+
+
+def hierarchy_for(tag, a, levels):
+    """The hierarchy make_golden.py handed to the reference: node-blocked
+    (3 dofs per node) for the C5 elasticity cases, plain ND otherwise."""
+    from paper_2007_00789_b200.partition import build_hierarchy
+    return build_hierarchy(a, levels, block=3 if tag.startswith("C5") else 1)
 
 
 def small_tags():

@@ -19,7 +19,7 @@ import hashlib
 import numpy as np
 import pytest
 
-from tests.golden_cases import config_tags, load, matrix_for
+from tests.golden_cases import config_tags, load, matrix_for, hierarchy_for
 
 pytestmark = pytest.mark.gpu
 
@@ -38,7 +38,7 @@ def test_config_matches_reference(tag):
     import paper_2007_00789_b200 as sp
     rec, arr = load(tag)
     a = matrix_for(tag)
-    h = sp.build_hierarchy(a, rec["levels"])
+    h = hierarchy_for(tag, a, rec["levels"])
     f = sp.factorize(a, h, rec["eps"], rec["scheme"], skip_levels=rec["skip_levels"])
     got = [[[e["cluster"], e["size_before"], e["size_after"], e["rank_f2"]]
             for e in lv["interfaces"]] for lv in f.diagnostics["levels"]]

@@ -8,7 +8,7 @@ import hashlib
 import numpy as np
 import pytest
 
-from tests.golden_cases import load, matrix_for, small_tags
+from tests.golden_cases import load, matrix_for, small_tags, hierarchy_for
 
 pytestmark = pytest.mark.gpu
 
@@ -60,7 +60,7 @@ def test_factorize_matches_reference(tag):
     from oracle import spand_oracle as orc
     rec, arr = load(tag)
     a = matrix_for(tag)
-    h = sp.build_hierarchy(a, rec["levels"])
+    h = hierarchy_for(tag, a, rec["levels"])
     f = sp.factorize(a, h, rec["eps"], rec["scheme"], skip_levels=rec["skip_levels"])
     got = [[[e["cluster"], e["size_before"], e["size_after"], e["rank_f2"]]
             for e in lv["interfaces"]] for lv in f.diagnostics["levels"]]

@@ -27,7 +27,7 @@ import pytest
 import paper_2007_00789_b200 as sp
 from paper_2007_00789_b200 import _lib
 from paper_2007_00789_b200.errors import DimensionMismatch, ParseError
-from tests.golden_cases import config_tags, load, matrix_for, small_tags
+from tests.golden_cases import config_tags, load, matrix_for, small_tags, hierarchy_for
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 HEADER = os.path.join(ROOT, "include", "spand_b200.h")
@@ -74,7 +74,7 @@ def test_native_hierarchy_matches_reference(tag):
     rec, _ = load(tag)
     a = matrix_for(tag)
     assert (a.n, a.nnz) == (rec["n"], rec["nnz_a"])
-    h = sp.build_hierarchy(a, rec["levels"])
+    h = hierarchy_for(tag, a, rec["levels"])
     sizes = np.array([c.dofs.size for c in h.clusters], dtype=np.int64)
     depth = np.array([c.depth for c in h.clusters], dtype=np.int64)
     dofs = np.concatenate([c.dofs for c in h.clusters]).astype(np.int64)
@@ -88,7 +88,7 @@ def _plan(tag):
     from paper_2007_00789_b200.engine import NativePlan
     rec, _ = load(tag)
     a = matrix_for(tag)
-    h = sp.build_hierarchy(a, rec["levels"])
+    h = hierarchy_for(tag, a, rec["levels"])
     # capacity override: the RRQR group size query needs a device
     return rec, NativePlan(a, h, rec["skip_levels"], cap_override=148 * 4)
 
