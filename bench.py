@@ -349,7 +349,7 @@ def main():
                 "basis": "B_rrqr,min = 8(2mn + m^2) per panel (SURVEY 8d) / RRQR time; the "
                          "pivoted QR needs k_stop sequential group-synchronised steps, so it "
                          "sits far below this bound; effective_tflops = F_rrqr / time"}
-    elif dom[0] == "spand_gemv_tiles":
+    elif dom[0] in ("spand_gemv_tiles", "spand_gemv_items"):
         achieved = counts["B_apply"] * (rep.n_cg + 1) / (dom[1]["ms"] / args.steps / 1000.0) / 1e9
         roof = {"kernel": dom[0], "bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"],
                 "unit": "GB/s", "frac": achieved / pk["hbm_gbs"], "peak_kind": pk_kind,

@@ -90,6 +90,13 @@ int spand_scatter_perm(int n, const int32_t* perm, const double* x, double* y,
 int spand_gemv_tiles(int ntiles, const int64_t* tiles, const int64_t* tasks,
                      const double* x, int64_t ldx, double* scratch,
                      int64_t ldscr, int nvec, void* stream);
+/* Warp-granular variant used by the engine-built plans: item rows have the
+ * tile layout, but one WARP processes an item (trans 0: oc <= 256 rows x kc
+ * columns; trans 1: oc <= 8 columns x kc rows); `grid` CTAs of 8 warps walk
+ * the items (grid 0: one warp per item). */
+int spand_gemv_items(int nitem, int grid, const int64_t* items, const int64_t* tasks,
+                     const double* x, int64_t ldx, double* scratch, int64_t ldscr,
+                     int nvec, void* stream);
 /* for e in [0, nout): s = sum_{t in [ptr[e], ptr[e+1])} scratch[src[t]]
  * (summed in the stored order: deterministic); mode[e] == 0: x[dst[e]] = s,
  * mode[e] == 1: x[dst[e]] -= s. */

@@ -29,6 +29,7 @@ SIGNATURES = {
     "spand_gather": [_c_int, _P, _P, _P, _P],
     "spand_scatter_perm": [_c_int, _P, _P, _P, _P],
     "spand_gemv_tiles": [_c_int, _P, _P, _P, _c_i64, _P, _c_i64, _c_int, _P],
+    "spand_gemv_items": [_c_int, _c_int, _P, _P, _P, _c_i64, _P, _c_i64, _c_int, _P],
     "spand_apply_scatter": [_c_int, _P, _P, _P, _P, _P, _c_i64, _P, _c_i64,
                             _c_int, _P],
     "spand_apply_runs": [_c_int, _P, _P, _P, _c_i64, _P, _c_i64, _c_int, _P],

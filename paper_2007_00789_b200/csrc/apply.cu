@@ -138,6 +138,117 @@ gemv_tiles_kernel(const int64_t* __restrict__ tiles, const int64_t* __restrict__
   }
 }
 
+// Warp-granular GEMV work items (the apply's hot kernel).  An item (task,
+// ob, oc, kb, kc, out_off) is a tile (packed in 2 int64, see below), but
+// it is processed by ONE warp and sized by the host to ~16-32 KB of payload:
+//   trans 0 (y = M x, outputs are rows): oc <= 128 rows, lane holds rows
+//     ob + lane + 32 q (q < 4), columns streamed two at a time;
+//   trans 1 (y = M^T x, outputs are columns): oc <= 4 columns, lanes stride
+//     the kc rows of all oc columns at once (one input load per row, two
+//     row steps in flight).
+// A grid of persistent warps walks the items (warp g takes g, g + W, ...),
+// so thousands of tiny operators share CTAs and big ones are split evenly.
+// <= 64 registers: 4 CTAs (32 warps) per SM.
+constexpr int kItemRows = 128;   // trans 0: max rows per item
+constexpr int kItemCols = 4;     // trans 1: max columns per item
+
+__device__ __forceinline__ double load_in(const Task& T, const double* xv, int64_t ldx, int v,
+                                          int kk) {
+  return T.in_kind == 0 ? xv[reinterpret_cast<const int32_t*>(T.in)[kk]]
+                        : __ldg(reinterpret_cast<const double*>(T.in) + kk + v * ldx);
+}
+
+__global__ void __launch_bounds__(kThreads, 4)
+gemv_items_kernel(int nitem, const int64_t* __restrict__ items, const int64_t* __restrict__ tasks,
+                  const double* __restrict__ x, int64_t ldx, double* __restrict__ scratch,
+                  int64_t ldscr, int nvec) {
+  const int lane = threadIdx.x & 31;
+  const int W = gridDim.x * kWarps;
+  for (int it = blockIdx.x * kWarps + (threadIdx.x >> 5); it < nitem; it += W) {
+    // packed item (2 x int64): {task << 32 | ob << 12 | oc, out_off << 28 | kb << 11 | kc}
+    const int64_t w0 = __ldg(items + 2 * (int64_t)it), w1 = __ldg(items + 2 * (int64_t)it + 1);
+    const int64_t t0 = w0 >> 32;
+    const int ob = (int)((w0 >> 12) & 0xfffff), oc = (int)(w0 & 0xfff);
+    const int kb = (int)((w1 >> 11) & 0x1ffff), kc = (int)(w1 & 0x7ff);
+    const int64_t oo = w1 >> 28;
+    const Task T = load_task(tasks + 8 * t0);
+    for (int v = 0; v < nvec; ++v) {
+      const double* xv = x + v * ldx;
+      double* out = scratch + oo + v * ldscr;
+      if (T.trans == 0) {
+        double acc[4] = {0.0, 0.0, 0.0, 0.0};
+        int c = 0;
+        for (; c + 1 < kc; c += 2) {
+          const double x0 = load_in(T, xv, ldx, v, kb + c);
+          const double x1 = load_in(T, xv, ldx, v, kb + c + 1);
+          const double* c0 = T.M + (int64_t)phys_col(kb + c, T.rot, T.cols) * T.ld + ob;
+          const double* c1 = T.M + (int64_t)phys_col(kb + c + 1, T.rot, T.cols) * T.ld + ob;
+          double m0v[4], m1v[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int r = lane + 32 * q;
+            m0v[q] = r < oc ? __ldg(c0 + r) : 0.0;
+            m1v[q] = r < oc ? __ldg(c1 + r) : 0.0;
+          }
+#pragma unroll
+          for (int q = 0; q < 4; ++q) acc[q] += m0v[q] * x0 + m1v[q] * x1;
+        }
+        if (c < kc) {
+          const double x0 = load_in(T, xv, ldx, v, kb + c);
+          const double* c0 = T.M + (int64_t)phys_col(kb + c, T.rot, T.cols) * T.ld + ob;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int r = lane + 32 * q;
+            if (r < oc) acc[q] += __ldg(c0 + r) * x0;
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int r = lane + 32 * q;
+          if (r < oc) out[r] = acc[q];
+        }
+      } else {
+        double acc[kItemCols];
+        const double* col[kItemCols];
+#pragma unroll
+        for (int j = 0; j < kItemCols; ++j) {
+          acc[j] = 0.0;
+          col[j] = T.M + (int64_t)phys_col(ob + (j < oc ? j : 0), T.rot, T.cols) * T.ld + kb;
+        }
+        int r = lane;
+        for (; r + 32 < kc; r += 64) {
+          double in2[2], p[2][kItemCols];
+#pragma unroll
+          for (int u = 0; u < 2; ++u) in2[u] = load_in(T, xv, ldx, v, kb + r + 32 * u);
+#pragma unroll
+          for (int u = 0; u < 2; ++u)
+#pragma unroll
+            for (int j = 0; j < kItemCols; ++j) p[u][j] = j < oc ? __ldg(col[j] + r + 32 * u) : 0.0;
+#pragma unroll
+          for (int u = 0; u < 2; ++u)
+#pragma unroll
+            for (int j = 0; j < kItemCols; ++j) acc[j] += p[u][j] * in2[u];
+        }
+        for (; r < kc; r += 32) {
+          const double i0 = load_in(T, xv, ldx, v, kb + r);
+#pragma unroll
+          for (int j = 0; j < kItemCols; ++j)
+            if (j < oc) acc[j] += __ldg(col[j] + r) * i0;
+        }
+#pragma unroll
+        for (int j = 0; j < kItemCols; ++j) acc[j] = warp_sum(acc[j]);
+        if (lane < oc) {
+          double s = acc[0];
+#pragma unroll
+          for (int j = 1; j < kItemCols; ++j)
+            if (lane == j) s = acc[j];
+          out[lane] = s;
+        }
+      }
+    }
+  }
+}
+
 __global__ void __launch_bounds__(kThreads)
 scatter_kernel(int nout, const int64_t* __restrict__ dst, const int64_t* __restrict__ mode,
                const int64_t* __restrict__ ptr, const int64_t* __restrict__ src,
@@ -174,9 +285,22 @@ runs_kernel(const int64_t* __restrict__ chunks, const int64_t* __restrict__ cont
   const int64_t dst = ch[0], cb = ch[3], ce = ch[4], eoff = ch[5], idx = ch[6];
   const int md = (int)ch[2];
   for (int v = 0; v < nvec; ++v) {
-    double s = 0.0;
-    if (i < len)
-      for (int64_t c = cb + g; c < ce; c += 4) s += scratch[__ldg(contrib + c) + eoff + i + v * ldscr];
+    // four independent partial sums per thread (fixed combination order)
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    if (i < len) {
+      const double* sv = scratch + eoff + i + v * ldscr;
+      int64_t c = cb + g;
+      for (; c + 12 < ce; c += 16) {
+        const int64_t a0 = __ldg(contrib + c), a1 = __ldg(contrib + c + 4),
+                      a2 = __ldg(contrib + c + 8), a3 = __ldg(contrib + c + 12);
+        s0 += sv[a0];
+        s1 += sv[a1];
+        s2 += sv[a2];
+        s3 += sv[a3];
+      }
+      for (; c < ce; c += 4) s0 += sv[__ldg(contrib + c)];
+    }
+    const double s = (s0 + s1) + (s2 + s3);
     __syncthreads();
     part[threadIdx.x] = s;
     __syncthreads();
@@ -209,6 +333,18 @@ int spand_gemv_tiles(int ntiles, const int64_t* tiles, const int64_t* tasks, con
   if (ntiles == 0) return 0;
   gemv_tiles_kernel<<<ntiles, kThreads, 0, as_stream(stream)>>>(tiles, tasks, x, ldx, scratch,
                                                                 ldscr, nvec);
+  SPAND_CHECK_LAUNCH();
+  return 0;
+}
+
+int spand_gemv_items(int nitem, int grid, const int64_t* items, const int64_t* tasks,
+                     const double* x, int64_t ldx, double* scratch, int64_t ldscr, int nvec,
+                     void* stream) {
+  if (nitem < 0 || grid < 0 || nvec < 1) return -1;
+  if (nitem == 0) return 0;
+  if (grid == 0) grid = (nitem + kWarps - 1) / kWarps;
+  gemv_items_kernel<<<grid, kThreads, 0, as_stream(stream)>>>(nitem, items, tasks, x, ldx,
+                                                              scratch, ldscr, nvec);
   SPAND_CHECK_LAUNCH();
   return 0;
 }

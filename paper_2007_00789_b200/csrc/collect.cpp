@@ -13,7 +13,9 @@
 //   * the structured apply plan (phases of GEMV tiles + ordered scatters in
 //     the cluster-contiguous numbering, see apply.cu / fastplan.py).
 #include <algorithm>
+#include <atomic>
 #include <cstdint>
+#include <thread>
 #include <cstring>
 #include <unordered_map>
 #include <vector>
@@ -260,42 +262,58 @@ int spand_collect_get(void* h, int64_t* ops, int64_t* segs, int64_t* perm, int64
 // hit the same run contribute their scratch blocks in task order.
 // Addresses: payload windows pool_base/fac_base (bit 62 of the window offset
 // selects the factor buffer), inputs xbuf + 8 * permuted index.
-static void compile_phase(Collected* C, const std::vector<Task>& ph, int64_t pool_base,
-                          int64_t fac_base, int64_t xbuf, int64_t idx_addr) {
-  constexpr int64_t TO = 64, RUN = 64;
-  // inner-dimension split: 2048 by default, finer (down to 256) when the
-  // phase would otherwise leave most of the 148 SMs idle
-  int64_t TK = 2048;
-  for (; TK > 256; TK /= 2) {
-    int64_t nt = 0;
-    for (const Task& t : ph) {
-      const int64_t nout = t.trans ? t.cols : t.rows;
-      const int64_t nk = t.trans ? t.rows : t.cols;
-      nt += ((nout + TO - 1) / TO) * std::max<int64_t>(1, (nk + TK - 1) / TK);
-    }
-    if (nt >= 4 * 148) break;
-  }
+struct PhaseImage {
   std::vector<int64_t> rows, tiles, chunks, contrib;
+  int64_t pos = 0;
+  bool overflow = false;
+};
+
+static void compile_phase(PhaseImage& P, const std::vector<Task>& ph, int64_t pool_base,
+                          int64_t fac_base, int64_t xbuf, int64_t idx_addr) {
+  constexpr int64_t RUN = 64;
+  // warp work items of ~32 KB of payload (apply.cu gemv_items_kernel):
+  //   trans 0: kc <= 64 columns x oc <= 128 rows (64 rows for wide tasks)
+  //   trans 1: oc <= 4 columns x kc <= 1024 rows
+  std::vector<int64_t>& rows = P.rows;
+  std::vector<int64_t>& tiles = P.tiles;
+  std::vector<int64_t>& chunks = P.chunks;
+  std::vector<int64_t>& contrib = P.contrib;
   struct Run { int64_t dst, len, mode; bool idx; std::vector<int64_t> parts; };
   std::vector<Run> runs;
   std::unordered_map<int64_t, int> run_of;   // destination start -> run
   int64_t pos = 0;
+  // item size: ~32 KB, smaller when the phase is small, so that every phase
+  // offers about one item per resident warp (148 SMs x 32 warps)
+  int64_t payload = 0;
+  for (const Task& t : ph) payload += t.rows * t.cols * 8;
+  const int64_t isz = std::max<int64_t>(4096, std::min<int64_t>(32768, payload / (148 * 32)));
   for (const Task& t : ph) {
     const int64_t nout = t.trans ? t.cols : t.rows;
     const int64_t nk = t.trans ? t.rows : t.cols;
     if (nout == 0) continue;
+    if (nout >= (int64_t(1) << 20) || nk >= (int64_t(1) << 17)) P.overflow = true;
     const bool in_fac = (t.M >> 62) & 1;
     const int64_t moff = t.M & ((int64_t(1) << 62) - 1);
     const int64_t maddr = (in_fac ? fac_base : pool_base) + 8 * moff;
     const int64_t inp = t.in_kind == 1 ? xbuf + 8 * t.in_ptr : idx_addr;
     const int64_t tid = (int64_t)rows.size() / 8;
     rows.insert(rows.end(), {maddr, t.ld, t.rows, t.cols, t.trans, t.rot, t.in_kind, inp});
+    int64_t TO, TK;
+    if (t.trans) {
+      TO = 4;
+      TK = std::max<int64_t>(64, std::min<int64_t>(1024, isz / (8 * TO) / 32 * 32));
+    } else {
+      TO = nk <= 32 ? 128 : 64;
+      TK = std::max<int64_t>(8, std::min<int64_t>(64, isz / (8 * TO)));
+    }
     const int64_t nkt = std::max<int64_t>(1, (nk + TK - 1) / TK);
     for (int64_t kb = 0; kb < nkt; ++kb)
       for (int64_t ob = 0; ob < nout; ob += TO) {
         const int64_t oc = std::min(TO, nout - ob);
         const int64_t kc = std::max<int64_t>(0, std::min(TK, nk - kb * TK));
-        tiles.insert(tiles.end(), {tid, ob, oc, kb * TK, kc, pos + kb * nout + ob, 0, 0});
+        // packed item (apply.cu): task | ob | oc, out_off | kb | kc
+        tiles.insert(tiles.end(), {(tid << 32) | (ob << 12) | oc,
+                                   ((pos + kb * nout + ob) << 28) | ((kb * TK) << 11) | kc});
       }
     const int64_t key = t.out_start >= 0 ? t.out_start : -1;
     auto it = run_of.find(key);
@@ -311,6 +329,9 @@ static void compile_phase(Collected* C, const std::vector<Task>& ph, int64_t poo
     pos += nout * nkt;
   }
   if (rows.empty()) return;
+  // packed-item field limits (apply.cu): ob < 2^20, inner offset < 2^17,
+  // scratch offset < 2^35
+  if (pos >= (int64_t(1) << 35)) P.overflow = true;
   for (const Run& R : runs) {
     const int64_t cb = (int64_t)contrib.size();
     contrib.insert(contrib.end(), R.parts.begin(), R.parts.end());
@@ -319,15 +340,22 @@ static void compile_phase(Collected* C, const std::vector<Task>& ph, int64_t poo
       chunks.insert(chunks.end(), {R.dst, std::min(RUN, R.len - e), R.mode, cb, ce, e,
                                    R.idx ? idx_addr : 0, 0});
   }
+  P.pos = pos;
+}
+
+static void append_phase(Collected* C, const PhaseImage& P) {
   auto put = [&](const std::vector<int64_t>& v) {
     const int64_t at = (int64_t)C->plan.size();
     C->plan.insert(C->plan.end(), v.begin(), v.end());
     return at;
   };
-  const int64_t a = put(rows), b = put(tiles), c = put(chunks), d = put(contrib);
-  C->phases.insert(C->phases.end(), {a, (int64_t)rows.size() / 8, b, (int64_t)tiles.size() / 8,
-                                     c, (int64_t)chunks.size() / 8, d, 0, 0, pos});
-  C->scratch_len = std::max(C->scratch_len, pos);
+  const int64_t a = put(P.rows), b = put(P.tiles), c = put(P.chunks), d = put(P.contrib);
+  // persistent warps: 4 CTAs (32 warps) per SM, one warp per item below that
+  const int64_t nitem = (int64_t)P.tiles.size() / 2;
+  const int64_t grid = std::min<int64_t>((nitem + 7) / 8, 148 * 4);
+  C->phases.insert(C->phases.end(), {a, (int64_t)P.rows.size() / 8, b, nitem,
+                                     c, (int64_t)P.chunks.size() / 8, d, grid, 0, P.pos});
+  C->scratch_len = std::max(C->scratch_len, P.pos);
 }
 
 // Build the apply image.  idx_addr: device address of the final block's
@@ -339,16 +367,32 @@ int spand_collect_apply(void* h, int64_t pool_base, int64_t fac_base, int64_t xb
   C->plan.clear();
   C->phases.clear();
   C->scratch_len = 1;
+  // phases compile independently (host threads), then concatenate in order
+  const size_t nf = C->fph.size(), nt = nf + C->bph.size();
+  std::vector<PhaseImage> imgs(nt);
+  std::atomic<size_t> next{0};
+  auto work = [&]() {
+    for (size_t k = next++; k < nt; k = next++)
+      compile_phase(imgs[k], k < nf ? C->fph[k] : C->bph[k - nf], pool_base, fac_base, xbuf,
+                    idx_addr);
+  };
+  const unsigned nth = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+  std::vector<std::thread> pool;
+  for (unsigned i = 1; i < nth; ++i) pool.emplace_back(work);
+  work();
+  for (auto& th : pool) th.join();
+  size_t total = 0;
+  for (const auto& P : imgs)
+    total += P.rows.size() + P.tiles.size() + P.chunks.size() + P.contrib.size();
+  C->plan.reserve(total);
+  for (const auto& P : imgs)
+    if (P.overflow) return -2;   // operator too large for the packed item format
   int64_t nfw = 0, nbw = 0;
-  for (const auto& ph : C->fph) {
-    const size_t before = C->phases.size();
-    compile_phase(C, ph, pool_base, fac_base, xbuf, idx_addr);
-    nfw += (C->phases.size() > before);
-  }
-  for (const auto& ph : C->bph) {
-    const size_t before = C->phases.size();
-    compile_phase(C, ph, pool_base, fac_base, xbuf, idx_addr);
-    nbw += (C->phases.size() > before);
+  for (size_t k = 0; k < nt; ++k) {
+    if (imgs[k].rows.empty()) continue;
+    append_phase(C, imgs[k]);
+    if (k < nf) ++nfw;
+    else ++nbw;
   }
   out[0] = (int64_t)C->plan.size();
   out[1] = nfw;
@@ -357,8 +401,8 @@ int spand_collect_apply(void* h, int64_t pool_base, int64_t fac_base, int64_t xb
   return 0;
 }
 
-// phase rows (10 int64): tasks_off, ntask, tiles_off, ntile, chunks_off,
-// nchunk, contrib_off, 0, 0, scratch_used
+// phase rows (10 int64): tasks_off, ntask, items_off, nitem, chunks_off,
+// nchunk, contrib_off, grid (gemv_items CTAs), 0, scratch_used
 int spand_collect_apply_get(void* h, int64_t* image, int64_t* phases) {
   Collected* C = static_cast<Collected*>(h);
   std::memcpy(image, C->plan.data(), C->plan.size() * sizeof(int64_t));

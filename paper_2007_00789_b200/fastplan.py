@@ -252,8 +252,11 @@ class NativeApplyPlan(FastPlan):
         out = np.zeros(4, dtype=np.int64)
         lib.spand_collect_apply.argtypes = [ctypes.c_void_p] + [ctypes.c_int64] * 4 + \
             [ctypes.c_void_p]
-        lib.spand_collect_apply(collected.h, pool.data_ptr(), fac.data_ptr(),
-                                self.xbuf.data_ptr(), self._fidx.data_ptr(), vp(out))
+        rc = lib.spand_collect_apply(collected.h, pool.data_ptr(), fac.data_ptr(),
+                                     self.xbuf.data_ptr(), self._fidx.data_ptr(), vp(out))
+        if rc != 0:
+            raise RuntimeError(f"apply image build failed ({rc}): an operator exceeds "
+                               "the packed work-item limits")
         tm.append(time.perf_counter())
         ilen, nfw, nbw, self.scratch_len = (int(x) for x in out)
         image = np.zeros(max(ilen, 1), dtype=np.int64)
@@ -267,10 +270,10 @@ class NativeApplyPlan(FastPlan):
         self.scratch = t.empty(max(self.scratch_len, 1), dtype=t.float64, device=dev())
         rows = []
         for r in ph.tolist():
-            to, nt, tio, ntile, co, nch, cbo, _, _, _ = r
+            to, nt, tio, nitem, co, nch, cbo, grid, _, _ = r
             rows.append((ctypes.c_void_p(base + 8 * to), ctypes.c_void_p(base + 8 * tio),
-                         ntile, ctypes.c_void_p(base + 8 * co), nch,
-                         ctypes.c_void_p(base + 8 * cbo)))
+                         nitem, ctypes.c_void_p(base + 8 * co), nch,
+                         ctypes.c_void_p(base + 8 * cbo), grid))
         self.phase_table = ph
         self.fwd, self.bwd = rows[:nfw], rows[nfw:]
         self._graph = None
@@ -281,8 +284,8 @@ class NativeApplyPlan(FastPlan):
     def _run_pass(self, phases):
         st = stream()
         x = self.xbuf
-        for tasks, tiles, ntile, chunks, nch, contrib in phases:
-            _lib.call("spand_gemv_tiles", ntile, tiles, tasks, ptr(x), self.n,
+        for tasks, items, nitem, chunks, nch, contrib, grid in phases:
+            _lib.call("spand_gemv_items", nitem, grid, items, tasks, ptr(x), self.n,
                       ptr(self.scratch), self.scratch_len, 1, st)
             _lib.call("spand_apply_runs", nch, chunks, contrib, ptr(x), self.n,
                       ptr(self.scratch), self.scratch_len, 1, st)

@@ -21,10 +21,10 @@ st = stream()
 for rep in range(3):
     xb = plan.xbuf
     evs = []
-    for k, (tasks, tiles, ntile, chunks, nch, contrib) in enumerate(plan.fwd + plan.bwd):
+    for k, (tasks, tiles, ntile, chunks, nch, contrib, grid) in enumerate(plan.fwd + plan.bwd):
         e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
         e0.record()
-        _lib.call("spand_gemv_tiles", ntile, tiles, tasks, ptr(xb), plan.n, ptr(plan.scratch), plan.scratch_len, 1, st)
+        _lib.call("spand_gemv_items", ntile, grid, tiles, tasks, ptr(xb), plan.n, ptr(plan.scratch), plan.scratch_len, 1, st)
         e1.record()
         _lib.call("spand_apply_runs", nch, chunks, contrib, ptr(xb), plan.n, ptr(plan.scratch), plan.scratch_len, 1, st)
         e2.record()
