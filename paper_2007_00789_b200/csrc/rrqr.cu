@@ -81,6 +81,7 @@ struct Sh {
   int nhot, nhot3;
   double red8[kWarps][8];   // multi-value block reductions of the column pass
   double tot8[8];
+  double xk[2][4];          // row k of the column-pass batch (by batch parity)
   unsigned long long fmax;   // bits of the max norm^2 of my frozen columns (>= 0)
   int nb_start[1025];  // column start of each neighbour (panels with <= 1024)
   int wsum[kWarps];
@@ -214,6 +215,21 @@ __device__ void colpass_batch(const ColCtx& X, int a0, int nb, Sh& sh, double& b
       x[b][e] = (cs[b] >= 0 && i < X.len) ? col[i] : 0.0;
     }
   }
+  // running norms of the batch (broadcast loads; only thread b writes them,
+  // after the reductions) and row k of each column (thread 0 holds it)
+  double cur0[B], ref0[B];
+#pragma unroll
+  for (int b = 0; b < B; ++b) {
+    cur0[b] = cs[b] >= 0 ? X.cur[cs[b]] : 0.0;
+    ref0[b] = cs[b] >= 0 ? X.ref[cs[b]] : 0.0;
+  }
+  // (double-buffered by batch parity: the previous batch may still read its
+  // copy when no second reduction separates the batches)
+  double* xk = sh.xk[(a0 / B) & 1];
+  if (tid == 0) {
+#pragma unroll
+    for (int b = 0; b < B; ++b) xk[b] = x[b][0];
+  }
   double d[B];
 #pragma unroll
   for (int b = 0; b < B; ++b) {
@@ -225,34 +241,43 @@ __device__ void colpass_batch(const ColCtx& X, int a0, int nb, Sh& sh, double& b
     }
   }
   block_reduce_n<B>(d, sh);
-  double t[2 * B];
+  // row-k entry r_k = x_k - tau d v_k in every thread: the norm downdate
+  // needs the exact tail only when the refresh rule fires (dense.py:172-178)
+  double rkv[B];
+  bool need = false;
+#pragma unroll
+  for (int b = 0; b < B; ++b) {
+    rkv[b] = xk[b] - X.tau * d[b] * X.v[0];
+    double cn = cur0[b] - rkv[b] * rkv[b];
+    if (cn < 0.0) cn = 0.0;
+    need |= (b < nb) && (cn < 0.01 * ref0[b]);
+  }
+  double t[B];
 #pragma unroll
   for (int b = 0; b < B; ++b) {
     const double w = X.tau * d[b];
     double* col = X.W + (int64_t)(cs[b] < 0 ? 0 : cs[b]) * X.m + X.k;
-    double tail = 0.0, rk = 0.0;
+    double tail = 0.0;
 #pragma unroll
     for (int e = 0; e < E; ++e) {
       const int i = tid + kT * e;
       if (cs[b] >= 0 && i < X.len) {
         const double y = x[b][e] - w * X.v[i];
         col[i] = y;
-        if (i == 0) rk = y;
-        else tail += y * y;
+        if (i != 0) tail += y * y;
       }
     }
     t[b] = tail;
-    t[B + b] = rk;   // only thread 0 holds row k: the sum is exact
   }
-  block_reduce_n<2 * B>(t, sh);
+  if (need) block_reduce_n<B>(t, sh);
 #pragma unroll
   for (int b = 0; b < B; ++b) {
     if (tid == b && b < nb) {
       const int c = cs[b];
-      const double rk = t[B + b], tail = t[b];
-      double cn = X.cur[c] - rk * rk;
+      const double rk = rkv[b], tail = t[b];
+      double cn = cur0[b] - rk * rk;
       if (cn < 0.0) cn = 0.0;
-      if (cn < 0.01 * X.ref[c]) {
+      if (cn < 0.01 * ref0[b]) {
         // exact tail norm of the updated column (dense.py:172-178)
         cn = tail;
         X.ref[c] = tail;
@@ -1054,7 +1079,8 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
       vsh[i] = x;
       s += x * x;
     }
-    const double eta = sqrt(block_sum<kT>(s, sh.red));
+    const double s2 = block_sum<kT>(s, sh.red);
+    const double eta = sqrt(s2);
     eta_last = eta;
     if (k == 0) {
       r11 = eta;
@@ -1080,12 +1106,12 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
     if (eta > 0.0) {
       const double x0 = vsh[0];
       beta = x0 >= 0.0 ? -eta : eta;
+      // v.v = |x|^2 - x0^2 + (x0 - beta)^2: no second reduction
+      const double v0 = x0 - beta;
+      tau = 2.0 / (s2 - x0 * x0 + v0 * v0);
       __syncthreads();
-      if (tid == 0) vsh[0] = x0 - beta;
+      if (tid == 0) vsh[0] = v0;
       __syncthreads();
-      double vv = 0.0;
-      for (int i = tid; i < len; i += kT) vv += vsh[i] * vsh[i];
-      tau = 2.0 / block_sum<kT>(vv, sh.red);
     } else {
       __syncthreads();
       for (int i = tid; i < len; i += kT) vsh[i] = 0.0;
