@@ -715,60 +715,6 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
   int32_t* coldA = flist + 12 * ncap;
   int32_t* coldB = flist + 16 * ncap;
   int32_t* coldl = coldA;
-  auto pass1 = [&](int na, auto colp, auto alo, int ka, int nb) {
-    // ZT[a][q] = sum_{i >= ka} A_a[i] V[i, ka + q]  (64 x 32 tile on DMMA)
-    double (*As)[kPBK][kLDS] = reinterpret_cast<double (*)[kPBK][kLDS]>(vsh + kCScr);
-    double (*Bs)[kPBK][36] =
-        reinterpret_cast<double (*)[kPBK][36]>(vsh + kCScr + 2 * kPBK * kLDS);
-    double (*ZT)[33] = reinterpret_cast<double (*)[33]>(vsh + kCZ);
-    const int wm = warp >> 2, wn = warp & 3;
-    double acc[4][2];
-#pragma unroll
-    for (int a = 0; a < 4; ++a) acc[a][0] = acc[a][1] = 0.0;
-    auto stage = [&](int st, int i0) {
-#pragma unroll
-      for (int r = 0; r < (kPBK * 64) / kT; ++r) {
-        const int e = tid + r * kT;
-        const int kk = e % kPBK, a = e / kPBK;
-        const int i = i0 + kk;
-        const bool ok = a < na && i < m && i >= alo(a);
-        cp_async8(&As[st][kk][a], ok ? colp(a) + i : W, ok);
-      }
-#pragma unroll
-      for (int r = 0; r < (kPBK * 32) / kT; ++r) {
-        const int e = tid + r * kT;
-        const int kk = e % kPBK, q = e / kPBK;
-        const int i = i0 + kk;
-        const bool ok = q < nb && i < m && i >= ka + q;
-        cp_async8(&Bs[st][kk][q], ok ? V + (int64_t)i + (int64_t)(ka + q) * m : V, ok);
-      }
-      cp_commit();
-    };
-    __syncthreads();
-    stage(0, ka);
-    int st = 0;
-    for (int i0 = ka; i0 < m; i0 += kPBK) {
-      cp_wait_all();
-      __syncthreads();
-      if (i0 + kPBK < m) stage(st ^ 1, i0 + kPBK);
-#pragma unroll
-      for (int kq = 0; kq < kPBK / 4; ++kq) {
-        const int kr = kq * 4 + (lane & 3);
-        const double bf = Bs[st][kr][wn * 8 + (lane >> 2)];
-#pragma unroll
-        for (int mi = 0; mi < 4; ++mi)
-          dmma(acc[mi][0], acc[mi][1], As[st][kr][wm * 32 + mi * 8 + (lane >> 2)], bf);
-      }
-      st ^= 1;
-    }
-    __syncthreads();
-#pragma unroll
-    for (int mi = 0; mi < 4; ++mi)
-#pragma unroll
-      for (int h = 0; h < 2; ++h)
-        ZT[wm * 32 + mi * 8 + (lane >> 2)][wn * 8 + (lane & 3) * 2 + h] = acc[mi][h];
-    __syncthreads();
-  };
   auto cold_maint = [&](int ka, int kb) {
     const int nb = kb - ka;
     const int nc = sh.ncold;
@@ -777,7 +723,10 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
     double (*ZT)[33] = reinterpret_cast<double (*)[33]>(vsh + kCZ);
     double (*RK)[33] = reinterpret_cast<double (*)[33]>(vsh + kCR2);
     double* TAIL = vsh + kCTail;
-    const int wm = warp >> 2, wn = warp & 3;
+    // per-warp partials (fixed-order reductions): [warp][16][32] for Y^T,
+    // [warp][16] for the tails
+    double (*RED)[16][32] = reinterpret_cast<double (*)[16][32]>(vsh + kCScr);
+    double (*RED2)[16] = reinterpret_cast<double (*)[16]>(vsh + kCScr);
     // T of Q_b = H_ka ... H_{kb-1} = I - V T V^T (dlarft, forward columnwise)
     // from the Gram columns gathered during the block's steps
     __syncthreads();
@@ -802,16 +751,77 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
       }
     }
     __syncthreads();
-    for (int ct = 0; ct < nc; ct += 64) {
-      const int ncl = min(64, nc - ct);
-      if (tid < 64) sh.fcol[tid] = tid < ncl ? coldl[rank + G * (ct + tid)] : -1;
+    // rows ka..m-1 split over the 8 warps (4-row aligned chunks): every warp
+    // streams its own rows of the cold columns and of V through DMMA
+    // fragments straight from L2 -- no block barriers inside the row loops
+    const int L = m - ka;
+    const int chunk = ((L + 4 * kWarps - 1) / (4 * kWarps)) * 4;
+    const int rb = ka + warp * chunk, re = min(m, rb + chunk);
+    const int l4 = lane & 3, l8 = lane >> 2;
+    for (int ct = 0; ct < nc; ct += 16) {
+      const int ncl = min(16, nc - ct);
+      if (tid < 16) sh.fcol[tid] = tid < ncl ? coldl[rank + G * (ct + tid)] : -1;
       __syncthreads();
-      // Y^T = X^T V, then Z^T = Y^T T
-      pass1(ncl, [&](int a) { return (const double*)(W + (int64_t)sh.fcol[a] * m); },
-            [&](int a) { return ka; }, ka, nb);
-      double zv[8];
+      // ---- Y^T[c][q] = sum_{i >= ka} X_c[i] V[i, ka + q]: M = columns (2 x 8),
+      // N = reflectors (4 x 8), K = rows
+      {
+        double acc[2][4][2];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
+        for (int a = 0; a < 2; ++a)
+#pragma unroll
+          for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+        const double* xa[2];
+        bool oka[2];
+#pragma unroll
+        for (int mi = 0; mi < 2; ++mi) {
+          const int c = sh.fcol[mi * 8 + l8];
+          oka[mi] = c >= 0;
+          xa[mi] = W + (int64_t)(c >= 0 ? c : 0) * m;
+        }
+        for (int r = rb; r < re; r += 8) {
+          double af[2][2], bf[2][4];
+#pragma unroll
+          for (int s = 0; s < 2; ++s) {
+            const int i = r + 4 * s + l4;
+            const bool okr = i < re;
+#pragma unroll
+            for (int mi = 0; mi < 2; ++mi) af[s][mi] = (okr && oka[mi]) ? __ldcg(xa[mi] + i) : 0.0;
+#pragma unroll
+            for (int ni = 0; ni < 4; ++ni) {
+              const int q = ni * 8 + l8;
+              bf[s][ni] = (okr && q < nb && i >= ka + q) ? __ldcg(V + (int64_t)(ka + q) * m + i)
+                                                         : 0.0;
+            }
+          }
+#pragma unroll
+          for (int s = 0; s < 2; ++s)
+#pragma unroll
+            for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+              for (int ni = 0; ni < 4; ++ni)
+                dmma(acc[mi][ni][0], acc[mi][ni][1], af[s][mi], bf[s][ni]);
+        }
+        // C[row = column l8 (+8 mi)][col = reflector 2 l4 + h (+8 ni)]
+#pragma unroll
+        for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+          for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) RED[warp][mi * 8 + l8][ni * 8 + 2 * l4 + h] = acc[mi][ni][h];
+      }
+      __syncthreads();
+      for (int e = tid; e < 16 * 32; e += kT) {
+        const int c = e >> 5, q = e & 31;
+        double s = 0.0;
+#pragma unroll
+        for (int w2 = 0; w2 < kWarps; ++w2) s += RED[w2][c][q];
+        ZT[c][q] = s;
+      }
+      __syncthreads();
+      // ---- Z^T = Y^T T
+      double zv[2];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
         const int e = tid + kT * u;
         const int c = e >> 5, q = e & 31;
         double z = 0.0;
@@ -821,70 +831,92 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
       }
       __syncthreads();
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
+      for (int u = 0; u < 2; ++u) {
         const int e = tid + kT * u;
         ZT[e >> 5][e & 31] = zv[u];
       }
-      if (tid < 64) TAIL[tid] = 0.0;
       __syncthreads();
-      // X -= V Z, 64-row tiles; rows ka..kb-1 captured, sums of squares below
-      for (int r0 = ka; r0 < m; r0 += 64) {
-        double (*As2)[kLDS] = reinterpret_cast<double (*)[kLDS]>(vsh + kCScr);   // [32][68]
-        for (int e = tid; e < 32 * 64; e += kT) {
-          const int q = e >> 6, r = e & 63, i = r0 + r;
-          const bool ok = q < nb && i < m && i >= ka + q;
-          As2[q][r] = ok ? __ldcg(V + (int64_t)i + (int64_t)(ka + q) * m) : 0.0;
-        }
-        __syncthreads();
-        double acc[4][2][2];
+      // ---- X -= V Z: M = rows (8-row tiles of the warp's chunk), N = columns
+      // (2 x 8), K = reflectors; rows ka..kb-1 captured, squares below summed
+      {
+        double tail[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+        double bz[8][2];
 #pragma unroll
-        for (int a = 0; a < 4; ++a)
+        for (int kq = 0; kq < 8; ++kq)
 #pragma unroll
-          for (int b = 0; b < 2; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
-        for (int kq = 0; kq < (nb + 3) / 4; ++kq) {
-          const int kr = kq * 4 + (lane & 3);
-          double af[4], bf[2];
+          for (int ni = 0; ni < 2; ++ni) bz[kq][ni] = ZT[ni * 8 + l8][kq * 4 + l4];
+        double* xc[2][2];
+        bool okc[2][2];
 #pragma unroll
-          for (int mi = 0; mi < 4; ++mi) af[mi] = As2[kr][wm * 32 + mi * 8 + (lane >> 2)];
+        for (int ni = 0; ni < 2; ++ni)
 #pragma unroll
-          for (int ni = 0; ni < 2; ++ni) bf[ni] = ZT[wn * 16 + ni * 8 + (lane >> 2)][kr];
+          for (int h = 0; h < 2; ++h) {
+            const int c = sh.fcol[ni * 8 + 2 * l4 + h];
+            okc[ni][h] = c >= 0;
+            xc[ni][h] = W + (int64_t)(c >= 0 ? c : 0) * m;
+          }
+        const int nkq = (nb + 3) >> 2;
+        for (int r0 = rb; r0 < re; r0 += 8) {
+          const int i = r0 + l8;   // this lane's A row and C row
+          double af[8];
 #pragma unroll
-          for (int mi = 0; mi < 4; ++mi)
-#pragma unroll
-            for (int ni = 0; ni < 2; ++ni) dmma(acc[mi][ni][0], acc[mi][ni][1], af[mi], bf[ni]);
-        }
-        __syncthreads();
-        double (*Xt)[65] = reinterpret_cast<double (*)[65]>(vsh + kCScr);   // [64][65]
-        for (int e = tid; e < 64 * 64; e += kT) {
-          const int r = e & 63, cl = e >> 6, i = r0 + r;
-          Xt[cl][r] = (cl < ncl && i < m) ? W[(int64_t)i + (int64_t)sh.fcol[cl] * m] : 0.0;
-        }
-        __syncthreads();
-#pragma unroll
-        for (int mi = 0; mi < 4; ++mi)
+          for (int kq = 0; kq < 8; ++kq) {
+            const int q = kq * 4 + l4;
+            af[kq] = (kq < nkq && i < re && q < nb && i >= ka + q)
+                         ? __ldcg(V + (int64_t)(ka + q) * m + i)
+                         : 0.0;
+          }
+          double xo[2][2];
 #pragma unroll
           for (int ni = 0; ni < 2; ++ni)
 #pragma unroll
             for (int h = 0; h < 2; ++h)
-              Xt[wn * 16 + ni * 8 + (lane & 3) * 2 + h][wm * 32 + mi * 8 + (lane >> 2)] -=
-                  acc[mi][ni][h];
-        __syncthreads();
-        for (int e = tid; e < 64 * 64; e += kT) {
-          const int r = e & 63, cl = e >> 6, i = r0 + r;
-          if (cl < ncl && i < m) W[(int64_t)i + (int64_t)sh.fcol[cl] * m] = Xt[cl][r];
-        }
-        if (tid < ncl) {
-          double sq = 0.0;
-          for (int r = 0; r < 64 && r0 + r < m; ++r) {
-            const int i = r0 + r;
-            const double xv = Xt[tid][r];
-            if (i < kb) RK[tid][i - ka] = xv;
-            else sq += xv * xv;
+              xo[ni][h] = (i < re && okc[ni][h]) ? xc[ni][h][i] : 0.0;
+          double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+#pragma unroll
+          for (int kq = 0; kq < 8; ++kq)
+#pragma unroll
+            for (int ni = 0; ni < 2; ++ni) dmma(acc[ni][0], acc[ni][1], af[kq], bz[kq][ni]);
+          if (i < re) {
+#pragma unroll
+            for (int ni = 0; ni < 2; ++ni)
+#pragma unroll
+              for (int h = 0; h < 2; ++h) {
+                if (!okc[ni][h]) continue;
+                const double xv = xo[ni][h] - acc[ni][h];
+                xc[ni][h][i] = xv;
+                if (i < kb) RK[ni * 8 + 2 * l4 + h][i - ka] = xv;
+                else tail[ni][h] += xv * xv;
+              }
           }
-          TAIL[tid] += sq;
         }
-        __syncthreads();
+        // lanes sharing l4 hold the same columns: reduce over l8
+#pragma unroll
+        for (int ni = 0; ni < 2; ++ni)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            double t = tail[ni][h];
+            t += __shfl_xor_sync(0xffffffffu, t, 4);
+            t += __shfl_xor_sync(0xffffffffu, t, 8);
+            t += __shfl_xor_sync(0xffffffffu, t, 16);
+            tail[ni][h] = t;
+          }
+        __syncthreads();   // RED (aliased by RED2) fully consumed
+        if (l8 == 0) {
+#pragma unroll
+          for (int ni = 0; ni < 2; ++ni)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) RED2[warp][ni * 8 + 2 * l4 + h] = tail[ni][h];
+        }
       }
+      __syncthreads();
+      if (tid < 16) {
+        double s = 0.0;
+#pragma unroll
+        for (int w2 = 0; w2 < kWarps; ++w2) s += RED2[w2][tid];
+        TAIL[tid] = s;
+      }
+      __syncthreads();
       // replay the running norms of the block's steps (dense.py:168-178):
       // the exact tail at step t is the suffix norm of the updated column
       if (tid < ncl) {
@@ -917,6 +949,7 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
   while (k < kmax) {
     PH(0);
     if (maint) {
+      PH(6);
       // bring the cold columns up to date (reflectors k0..k-1), then either
       // reclassify (block end) or make every column hot (a cold column could
       // have won), and republish this CTA's candidate
@@ -985,6 +1018,7 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
       publish(bv, bp, bc, cpar ^ 1);
       cpar ^= 1;
       group_barrier(ctr, G, gen, -2, events + 12 * slot + 9);
+      PH(0);
     }
     // ---- winning column: max value, smallest current position (ties in
     // both: lowest record, as a sequential scan).  Records are scanned in
@@ -1463,8 +1497,8 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
   TL(twb);
 #ifdef SPAND_RRQR_PHASES
   if (lane == 0 && warp == 0 && m >= 1000 && (rank == 0 || rank == G / 2))
-    printf("[rrqr phases] p %d m %d n %d G %d rank %d k %d nf %d act-steps %lld hot %lld hot3 %lld | kcycles: cand %lld pivcol %lld refl %lld colpass %lld publish %lld barrier %lld | Q %lld restore %lld frozen-gemm %lld writeback %lld\n",
-           p, m, n, G, rank, k_stop, nf, nact_sum, hot_sum, hot3_sum, ph_t[0] / 1000, ph_t[1] / 1000, ph_t[2] / 1000,
+    printf("[rrqr phases] p %d m %d n %d G %d rank %d k %d nf %d act-steps %lld hot %lld hot3 %lld | kcycles: cand %lld maint %lld pivcol %lld refl %lld colpass %lld publish %lld barrier %lld | Q %lld restore %lld frozen-gemm %lld writeback %lld\n",
+           p, m, n, G, rank, k_stop, nf, nact_sum, hot_sum, hot3_sum, ph_t[0] / 1000, ph_t[6] / 1000, ph_t[1] / 1000, ph_t[2] / 1000,
            ph_t[3] / 1000, ph_t[4] / 1000, ph_t[5] / 1000, tq / 1000, trs / 1000, tg / 1000,
            twb / 1000);
 #endif
