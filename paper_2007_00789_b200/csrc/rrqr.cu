@@ -47,7 +47,7 @@ constexpr int kMaxM = 6144;  // v in shared memory
 //  bits(eta_stop), bits(r11), 0, 0, 0}
 
 constexpr int kBB = 32;        // column width of the Fb workspace region (frozen list)
-constexpr int kCR = kBB + 2;   // candidate record stride (doubles)
+constexpr int kCR = 4;   // candidate record stride (doubles): contiguous, coalesced scans
 constexpr int kLDS = 68;       // frozen-column DMMA tiles (conflict-free fragments)
 // dynamic shared memory floor: write-back staging (8 warps x 16 x 33) and
 // the frozen-GEMM epilogue tile (64 x 65)
