@@ -158,10 +158,14 @@ __device__ __forceinline__ double load_in(const Task& T, const double* xv, int64
                         : __ldg(reinterpret_cast<const double*>(T.in) + kk + v * ldx);
 }
 
-__global__ void __launch_bounds__(kThreads, 4)
+// NV right-hand sides per launch (x and scratch column-major with leading
+// dimensions ldx / ldscr): every payload element is loaded once and used
+// for all NV vectors (multi-RHS apply, reference factorize.py:262-267).
+template <int NV>
+__global__ void __launch_bounds__(kThreads, NV == 1 ? 4 : 2)
 gemv_items_kernel(int nitem, const int64_t* __restrict__ items, const int64_t* __restrict__ tasks,
                   const double* __restrict__ x, int64_t ldx, double* __restrict__ scratch,
-                  int64_t ldscr, int nvec) {
+                  int64_t ldscr, int v0) {
   const int lane = threadIdx.x & 31;
   const int W = gridDim.x * kWarps;
   for (int it = blockIdx.x * kWarps + (threadIdx.x >> 5); it < nitem; it += W) {
@@ -172,77 +176,104 @@ gemv_items_kernel(int nitem, const int64_t* __restrict__ items, const int64_t* _
     const int kb = (int)((w1 >> 11) & 0x1ffff), kc = (int)(w1 & 0x7ff);
     const int64_t oo = w1 >> 28;
     const Task T = load_task(tasks + 8 * t0);
-    for (int v = 0; v < nvec; ++v) {
-      const double* xv = x + v * ldx;
-      double* out = scratch + oo + v * ldscr;
-      if (T.trans == 0) {
-        double acc[4] = {0.0, 0.0, 0.0, 0.0};
-        int c = 0;
-        for (; c + 1 < kc; c += 2) {
-          const double x0 = load_in(T, xv, ldx, v, kb + c);
-          const double x1 = load_in(T, xv, ldx, v, kb + c + 1);
-          const double* c0 = T.M + (int64_t)phys_col(kb + c, T.rot, T.cols) * T.ld + ob;
-          const double* c1 = T.M + (int64_t)phys_col(kb + c + 1, T.rot, T.cols) * T.ld + ob;
-          double m0v[4], m1v[4];
+    if (T.trans == 0) {
+      double acc[NV][4];
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const int r = lane + 32 * q;
-            m0v[q] = r < oc ? __ldg(c0 + r) : 0.0;
-            m1v[q] = r < oc ? __ldg(c1 + r) : 0.0;
-          }
+      for (int v = 0; v < NV; ++v)
 #pragma unroll
-          for (int q = 0; q < 4; ++q) acc[q] += m0v[q] * x0 + m1v[q] * x1;
+        for (int q = 0; q < 4; ++q) acc[v][q] = 0.0;
+      int c = 0;
+      for (; c + 1 < kc; c += 2) {
+        double x0[NV], x1[NV];
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+          x0[v] = load_in(T, x + (v0 + v) * ldx, ldx, v0 + v, kb + c);
+          x1[v] = load_in(T, x + (v0 + v) * ldx, ldx, v0 + v, kb + c + 1);
         }
-        if (c < kc) {
-          const double x0 = load_in(T, xv, ldx, v, kb + c);
-          const double* c0 = T.M + (int64_t)phys_col(kb + c, T.rot, T.cols) * T.ld + ob;
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const int r = lane + 32 * q;
-            if (r < oc) acc[q] += __ldg(c0 + r) * x0;
-          }
-        }
+        const double* c0 = T.M + (int64_t)phys_col(kb + c, T.rot, T.cols) * T.ld + ob;
+        const double* c1 = T.M + (int64_t)phys_col(kb + c + 1, T.rot, T.cols) * T.ld + ob;
+        double m0v[4], m1v[4];
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           const int r = lane + 32 * q;
-          if (r < oc) out[r] = acc[q];
+          m0v[q] = r < oc ? __ldg(c0 + r) : 0.0;
+          m1v[q] = r < oc ? __ldg(c1 + r) : 0.0;
         }
-      } else {
-        double acc[kItemCols];
-        const double* col[kItemCols];
 #pragma unroll
-        for (int j = 0; j < kItemCols; ++j) {
-          acc[j] = 0.0;
-          col[j] = T.M + (int64_t)phys_col(ob + (j < oc ? j : 0), T.rot, T.cols) * T.ld + kb;
+        for (int v = 0; v < NV; ++v)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) acc[v][q] += m0v[q] * x0[v] + m1v[q] * x1[v];
+      }
+      if (c < kc) {
+        const double* c0 = T.M + (int64_t)phys_col(kb + c, T.rot, T.cols) * T.ld + ob;
+        double m0v[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int r = lane + 32 * q;
+          m0v[q] = r < oc ? __ldg(c0 + r) : 0.0;
         }
-        int r = lane;
-        for (; r + 32 < kc; r += 64) {
-          double in2[2], p[2][kItemCols];
 #pragma unroll
-          for (int u = 0; u < 2; ++u) in2[u] = load_in(T, xv, ldx, v, kb + r + 32 * u);
+        for (int v = 0; v < NV; ++v) {
+          const double x0 = load_in(T, x + (v0 + v) * ldx, ldx, v0 + v, kb + c);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) acc[v][q] += m0v[q] * x0;
+        }
+      }
+#pragma unroll
+      for (int v = 0; v < NV; ++v)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int r = lane + 32 * q;
+          if (r < oc) scratch[oo + (v0 + v) * ldscr + r] = acc[v][q];
+        }
+    } else {
+      double acc[NV][kItemCols];
+      const double* col[kItemCols];
+#pragma unroll
+      for (int j = 0; j < kItemCols; ++j) {
+#pragma unroll
+        for (int v = 0; v < NV; ++v) acc[v][j] = 0.0;
+        col[j] = T.M + (int64_t)phys_col(ob + (j < oc ? j : 0), T.rot, T.cols) * T.ld + kb;
+      }
+      int r = lane;
+      for (; r + 32 < kc; r += 64) {
+        double in2[NV][2], p[2][kItemCols];
+#pragma unroll
+        for (int v = 0; v < NV; ++v)
+#pragma unroll
+          for (int u = 0; u < 2; ++u) in2[v][u] = load_in(T, x + (v0 + v) * ldx, ldx, v0 + v, kb + r + 32 * u);
+#pragma unroll
+        for (int u = 0; u < 2; ++u)
+#pragma unroll
+          for (int j = 0; j < kItemCols; ++j) p[u][j] = j < oc ? __ldg(col[j] + r + 32 * u) : 0.0;
+#pragma unroll
+        for (int v = 0; v < NV; ++v)
 #pragma unroll
           for (int u = 0; u < 2; ++u)
 #pragma unroll
-            for (int j = 0; j < kItemCols; ++j) p[u][j] = j < oc ? __ldg(col[j] + r + 32 * u) : 0.0;
+            for (int j = 0; j < kItemCols; ++j) acc[v][j] += p[u][j] * in2[v][u];
+      }
+      for (; r < kc; r += 32) {
+        double p[kItemCols];
 #pragma unroll
-          for (int u = 0; u < 2; ++u)
+        for (int j = 0; j < kItemCols; ++j) p[j] = j < oc ? __ldg(col[j] + r) : 0.0;
 #pragma unroll
-            for (int j = 0; j < kItemCols; ++j) acc[j] += p[u][j] * in2[u];
+        for (int v = 0; v < NV; ++v) {
+          const double i0 = load_in(T, x + (v0 + v) * ldx, ldx, v0 + v, kb + r);
+#pragma unroll
+          for (int j = 0; j < kItemCols; ++j) acc[v][j] += p[j] * i0;
         }
-        for (; r < kc; r += 32) {
-          const double i0 = load_in(T, xv, ldx, v, kb + r);
+      }
 #pragma unroll
-          for (int j = 0; j < kItemCols; ++j)
-            if (j < oc) acc[j] += __ldg(col[j] + r) * i0;
-        }
+      for (int v = 0; v < NV; ++v) {
 #pragma unroll
-        for (int j = 0; j < kItemCols; ++j) acc[j] = warp_sum(acc[j]);
+        for (int j = 0; j < kItemCols; ++j) acc[v][j] = warp_sum(acc[v][j]);
         if (lane < oc) {
-          double s = acc[0];
+          double s = acc[v][0];
 #pragma unroll
           for (int j = 1; j < kItemCols; ++j)
-            if (lane == j) s = acc[j];
-          out[lane] = s;
+            if (lane == j) s = acc[v][j];
+          scratch[oo + (v0 + v) * ldscr + lane] = s;
         }
       }
     }
@@ -343,9 +374,25 @@ int spand_gemv_items(int nitem, int grid, const int64_t* items, const int64_t* t
   if (nitem < 0 || grid < 0 || nvec < 1) return -1;
   if (nitem == 0) return 0;
   if (grid == 0) grid = (nitem + kWarps - 1) / kWarps;
-  gemv_items_kernel<<<grid, kThreads, 0, as_stream(stream)>>>(nitem, items, tasks, x, ldx,
-                                                              scratch, ldscr, nvec);
-  SPAND_CHECK_LAUNCH();
+  // vectors in groups of 4 (then 2, 1), payload read once per group
+  // (task rows address vector 0; the kernel offsets by (v0 + v) * ldx)
+  for (int v0 = 0; v0 < nvec;) {
+    const int left = nvec - v0;
+    if (left >= 4) {
+      gemv_items_kernel<4><<<grid, kThreads, 0, as_stream(stream)>>>(nitem, items, tasks, x, ldx,
+                                                                    scratch, ldscr, v0);
+      v0 += 4;
+    } else if (left >= 2) {
+      gemv_items_kernel<2><<<grid, kThreads, 0, as_stream(stream)>>>(nitem, items, tasks, x, ldx,
+                                                                    scratch, ldscr, v0);
+      v0 += 2;
+    } else {
+      gemv_items_kernel<1><<<grid, kThreads, 0, as_stream(stream)>>>(nitem, items, tasks, x, ldx,
+                                                                    scratch, ldscr, v0);
+      v0 += 1;
+    }
+    SPAND_CHECK_LAUNCH();
+  }
   return 0;
 }
 

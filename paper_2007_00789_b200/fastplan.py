@@ -15,6 +15,11 @@ import numpy as np
 from . import _lib
 from .device import dev, ptr, require_cuda, stream, to_dev, to_dev_async
 
+
+def ctypes_ptr(addr):
+    import ctypes
+    return ctypes.c_void_p(int(addr))
+
 TILE_OUT = 64
 TILE_K = 2048
 
@@ -245,7 +250,9 @@ class NativeApplyPlan(FastPlan):
         tm = [time.perf_counter()]
         self.n = int(n)
         self.perm = to_dev(np.asarray(perm_new_to_old, dtype=np.int32), np.int32)
-        self.xbuf = t.zeros(max(self.n, 1), dtype=t.float64, device=dev())
+        # NVEC_MAX permuted vectors, column-major (leading dimension n): the
+        # image addresses column 0, the kernels step by n per right-hand side
+        self.xbuf = t.zeros(max(self.n, 1) * self.NVEC_MAX, dtype=t.float64, device=dev())
         self._fidx = to_dev(np.asarray(collected.fidx if collected.fidx.size else [0],
                                        dtype=np.int32), np.int32)
         lib, vp = collected.lib, collected.vp
@@ -281,11 +288,43 @@ class NativeApplyPlan(FastPlan):
         self.build_times = {"setup_s": tm[1] - tm[0], "image_s": tm[2] - tm[1],
                             "upload_s": tm[3] - tm[2], "image_mb": image.nbytes / 1e6}
 
-    def _run_pass(self, phases):
+    NVEC_MAX = 8   # right-hand sides per multi-vector pass
+
+    def _run_pass(self, phases, nvec=1):
         st = stream()
         x = self.xbuf
+        scr = self.scratch if nvec == 1 else self._scratch_multi
         for tasks, items, nitem, chunks, nch, contrib, grid in phases:
             _lib.call("spand_gemv_items", nitem, grid, items, tasks, ptr(x), self.n,
-                      ptr(self.scratch), self.scratch_len, 1, st)
+                      ptr(scr), self.scratch_len, nvec, st)
             _lib.call("spand_apply_runs", nch, chunks, contrib, ptr(x), self.n,
-                      ptr(self.scratch), self.scratch_len, 1, st)
+                      ptr(scr), self.scratch_len, nvec, st)
+
+    def run(self, xd, forward=True, backward=True):
+        """In place on a device tensor of shape (n,) or (n, k); column stacks
+        go through the factor NVEC_MAX vectors at a time (each payload
+        element is read once per group of up to 4: GEMM-like reuse)."""
+        if xd.dim() == 1:
+            self._run1(xd, forward, backward)
+            return xd
+        t = require_cuda()
+        if getattr(self, "_scratch_multi", None) is None:
+            self._scratch_multi = t.empty(max(self.scratch_len, 1) * self.NVEC_MAX,
+                                          dtype=t.float64, device=dev())
+        cols = xd.t().contiguous()          # (k, n): vector j contiguous
+        st = stream()
+        n = self.n
+        for j0 in range(0, cols.shape[0], self.NVEC_MAX):
+            nv = min(self.NVEC_MAX, cols.shape[0] - j0)
+            for v in range(nv):
+                _lib.call("spand_gather", n, ptr(self.perm), ptr(cols[j0 + v]),
+                          ctypes_ptr(self.xbuf.data_ptr() + 8 * n * v), st)
+            if forward:
+                self._run_pass(self.fwd, nv)
+            if backward:
+                self._run_pass(self.bwd, nv)
+            for v in range(nv):
+                _lib.call("spand_scatter_perm", n, ptr(self.perm),
+                          ctypes_ptr(self.xbuf.data_ptr() + 8 * n * v), ptr(cols[j0 + v]), st)
+        xd.copy_(cols.t())
+        return xd
