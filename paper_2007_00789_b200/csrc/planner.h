@@ -229,7 +229,8 @@ struct Plan {
           int64_t ncap = 0;
           for (int w : L.anbrs[k]) ncap += m0[w];
           const int64_t mc = m0[L.active[k]];
-          rq += mc * std::max<int64_t>(ncap, 1) + mc * mc + 32 * (ncap + mc) + 2 * ncap +
+          rq += mc * std::max<int64_t>(ncap, 1) + mc * mc + 32 * (ncap + mc) + 32 * mc + 1024 +
+                2 * ncap +
                 3 * mc + 8 + 1024 + (3 * ncap + 1) / 2 + 1 + 1 + 68 + nk_ws(mc);
         }
         need = std::max(need, rq);
@@ -645,7 +646,9 @@ struct Plan {
             int64_t ncap = 0;
             for (int w : L.anbrs[k]) ncap += m0[w];
             const int64_t mc = m0[p];
-            const int64_t wsz = mc * std::max<int64_t>(ncap, 1) + mc * mc + 32 * (ncap + mc);
+            // W | V | int lists (32 (ncap + mc)) | WY T blocks of Q (32 mc + 1024)
+            const int64_t wsz =
+                mc * std::max<int64_t>(ncap, 1) + mc * mc + 32 * (ncap + mc) + 32 * mc + 1024;
             const int64_t asz = 2 * ncap + 3 * mc + 68 * (int64_t)g + 8 + 1024;
             const int64_t isz = (3 * ncap + 1) / 2 + 1;
             const int64_t nb0 = (int64_t)nrow.size() / 4;

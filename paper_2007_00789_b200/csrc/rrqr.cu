@@ -944,6 +944,233 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
       __syncthreads();
     }
   };
+  // ---- blocked Q formation (large panels): Q = Q_0 Q_1 ... with
+  // Q_b = H_ka ... H_{kb-1} = I - V_b T_b V_b^T over 32-reflector blocks.
+  // T_b (dlarft, forward columnwise) is built by CTA b % G from the Gram
+  // matrix of V_b and shared through global memory; then every CTA applies
+  // the blocks from the last to the first to its own columns
+  // X = Q[:, rank + G u] (initially e_c) as X -= V_b (T_b (V_b^T X)), rows
+  // split over the warps with DMMA fragments streamed from L2 (same scheme
+  // as cold_maint).  Blocks with ka > max(c) leave e_c unchanged.
+  auto qform_blocked = [&](int kst) {
+    double* Tbuf = V + (int64_t)mcap * mcap + 32 * (ncap + mcap);
+    double (*TT)[33] = reinterpret_cast<double (*)[33]>(vsh + kCT);
+    double (*ZT)[33] = reinterpret_cast<double (*)[33]>(vsh + kCZ);
+    double (*RED)[16][32] = reinterpret_cast<double (*)[16][32]>(vsh + kCScr);
+    const int nblk = (kst + 31) / 32;
+    const int l4 = lane & 3, l8 = lane >> 2;
+    // (1) T of my blocks
+    for (int b = rank; b < nblk; b += G) {
+      const int ka = 32 * b, nb = min(32, kst - ka);
+      // Gram V_b^T V_b over rows ka..m-1: 4 x 4 tiles of 8, rows split over warps
+      const int L = m - ka;
+      const int chunk = ((L + 4 * kWarps - 1) / (4 * kWarps)) * 4;
+      const int rb = ka + warp * chunk, re = min(m, rb + chunk);
+      double acc[4][4][2];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) acc[a][c][0] = acc[a][c][1] = 0.0;
+      for (int r = rb; r < re; r += 4) {
+        const int i = r + l4;
+        double f[4];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          const int q = t * 8 + l8;
+          f[t] = (i < re && q < nb && i >= ka + q) ? __ldcg(V + (int64_t)(ka + q) * m + i) : 0.0;
+        }
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int c = 0; c < 4; ++c) dmma(acc[a][c][0], acc[a][c][1], f[a], f[c]);
+      }
+      __syncthreads();
+      // partials of the 32 x 32 Gram: 4 slots [4][32][32] in the scratch
+      // region; warps w and w + 4 share slot w (fixed order)
+      double* R2 = vsh + kCScr;
+      if (warp < 4) {
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+              R2[warp * 1024 + (a * 8 + l8) * 32 + c * 8 + 2 * l4 + h] = acc[a][c][h];
+      }
+      __syncthreads();
+      if (warp >= 4) {
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+              R2[(warp - 4) * 1024 + (a * 8 + l8) * 32 + c * 8 + 2 * l4 + h] += acc[a][c][h];
+      }
+      __syncthreads();
+      for (int e = tid; e < 32 * 32; e += kT) {
+        const int c = e >> 5, q = e & 31;
+        const double s = (R2[e] + R2[1024 + e]) + (R2[2048 + e] + R2[3072 + e]);
+        ZT[c][q] = (c < q && q < nb) ? s : 0.0;
+      }
+      __syncthreads();
+      if (warp == 0) {
+        for (int jj = 0; jj < nb; ++jj) {
+          const double tj = __ldcg(taus + ka + jj);
+          double v = 0.0;
+          if (lane < jj) {
+            for (int c = lane; c < jj; ++c) v += TT[lane][c] * ZT[c][jj];
+            v *= -tj;
+          }
+          __syncwarp();
+          if (lane < jj) TT[lane][jj] = v;
+          else if (lane == jj) TT[jj][jj] = tj;
+          else TT[lane][jj] = 0.0;
+          __syncwarp();
+        }
+      }
+      __syncthreads();
+      for (int e = tid; e < 32 * 32; e += kT) {
+        const int p = e >> 5, q = e & 31;
+        Tbuf[(int64_t)b * 1024 + e] = (p < nb && q < nb) ? TT[p][q] : 0.0;
+      }
+      __syncthreads();
+    }
+    // my columns start as e_c
+    for (int u = 0; rank + G * u < m; ++u) {
+      double* col = Q + (int64_t)(rank + G * u) * m;
+      const int c = rank + G * u;
+      for (int i = tid; i < m; i += kT) col[i] = (i == c) ? 1.0 : 0.0;
+    }
+    group_barrier(ctr, G, gen, 300000, events + 12 * slot + 9);   // every T_b published
+    const int nown = (m - rank + G - 1) / G;
+    for (int u0 = 0; u0 < nown; u0 += 16) {
+      const int ncl = min(16, nown - u0);
+      const int cmax = rank + G * (u0 + ncl - 1);
+      __syncthreads();
+      if (tid < 16) sh.fcol[tid] = tid < ncl ? rank + G * (u0 + tid) : -1;
+      __syncthreads();
+      for (int b = min(nblk - 1, cmax / 32); b >= 0; --b) {
+        const int ka = 32 * b, nb = min(32, kst - ka);
+        for (int e = tid; e < 32 * 32; e += kT) TT[e >> 5][e & 31] = __ldcg(Tbuf + (int64_t)b * 1024 + e);
+        const int L = m - ka;
+        const int chunk = ((L + 4 * kWarps - 1) / (4 * kWarps)) * 4;
+        const int rb = ka + warp * chunk, re = min(m, rb + chunk);
+        // Y^T = X^T V_b
+        {
+          double acc[2][4][2];
+#pragma unroll
+          for (int a = 0; a < 2; ++a)
+#pragma unroll
+            for (int c = 0; c < 4; ++c) acc[a][c][0] = acc[a][c][1] = 0.0;
+          const double* xa[2];
+          bool oka[2];
+#pragma unroll
+          for (int mi = 0; mi < 2; ++mi) {
+            const int c = sh.fcol[mi * 8 + l8];
+            oka[mi] = c >= 0;
+            xa[mi] = Q + (int64_t)(c >= 0 ? c : 0) * m;
+          }
+          for (int r = rb; r < re; r += 8) {
+            double af[2][2], bf[2][4];
+#pragma unroll
+            for (int s = 0; s < 2; ++s) {
+              const int i = r + 4 * s + l4;
+              const bool okr = i < re;
+#pragma unroll
+              for (int mi = 0; mi < 2; ++mi) af[s][mi] = (okr && oka[mi]) ? __ldcg(xa[mi] + i) : 0.0;
+#pragma unroll
+              for (int ni = 0; ni < 4; ++ni) {
+                const int q = ni * 8 + l8;
+                bf[s][ni] = (okr && q < nb && i >= ka + q) ? __ldcg(V + (int64_t)(ka + q) * m + i)
+                                                           : 0.0;
+              }
+            }
+#pragma unroll
+            for (int s = 0; s < 2; ++s)
+#pragma unroll
+              for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+                for (int ni = 0; ni < 4; ++ni)
+                  dmma(acc[mi][ni][0], acc[mi][ni][1], af[s][mi], bf[s][ni]);
+          }
+#pragma unroll
+          for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+            for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+              for (int h = 0; h < 2; ++h) RED[warp][mi * 8 + l8][ni * 8 + 2 * l4 + h] = acc[mi][ni][h];
+        }
+        __syncthreads();
+        // Z^T[c][q] = sum_{p >= q} Y^T[c][p] T[q][p]  (Z = T Y)
+        double zv[2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int e = tid + kT * u;
+          const int c = e >> 5, q = e & 31;
+          double z = 0.0;
+          if (c < ncl && q < nb)
+            for (int p = q; p < nb; ++p) {
+              double y = 0.0;
+#pragma unroll
+              for (int w2 = 0; w2 < kWarps; ++w2) y += RED[w2][c][p];
+              z += y * TT[q][p];
+            }
+          zv[u] = z;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int e = tid + kT * u;
+          ZT[e >> 5][e & 31] = zv[u];
+        }
+        __syncthreads();
+        // X -= V_b Z
+        {
+          double bz[8][2];
+#pragma unroll
+          for (int kq = 0; kq < 8; ++kq)
+#pragma unroll
+            for (int ni = 0; ni < 2; ++ni) bz[kq][ni] = ZT[ni * 8 + l8][kq * 4 + l4];
+          double* xc[2][2];
+          bool okc[2][2];
+#pragma unroll
+          for (int ni = 0; ni < 2; ++ni)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const int c = sh.fcol[ni * 8 + 2 * l4 + h];
+              okc[ni][h] = c >= 0;
+              xc[ni][h] = Q + (int64_t)(c >= 0 ? c : 0) * m;
+            }
+          const int nkq = (nb + 3) >> 2;
+          for (int r0 = rb; r0 < re; r0 += 8) {
+            const int i = r0 + l8;
+            double af[8];
+#pragma unroll
+            for (int kq = 0; kq < 8; ++kq) {
+              const int q = kq * 4 + l4;
+              af[kq] = (kq < nkq && i < re && q < nb && i >= ka + q)
+                           ? __ldcg(V + (int64_t)(ka + q) * m + i)
+                           : 0.0;
+            }
+            double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+#pragma unroll
+            for (int kq = 0; kq < 8; ++kq)
+#pragma unroll
+              for (int ni = 0; ni < 2; ++ni) dmma(acc[ni][0], acc[ni][1], af[kq], bz[kq][ni]);
+            if (i < re) {
+#pragma unroll
+              for (int ni = 0; ni < 2; ++ni)
+#pragma unroll
+                for (int h = 0; h < 2; ++h)
+                  if (okc[ni][h]) xc[ni][h][i] -= acc[ni][h];
+            }
+          }
+        }
+        __syncthreads();
+      }
+    }
+  };
   int k0 = 0, maint = 0, cpar = 0;
   double last_wv = 0.0;
   while (k < kmax) {
@@ -1293,7 +1520,8 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
   // Column c of Q is H_0 ... H_{k-1} e_c, and H_t leaves e_c alone for t > c.
   // Columns are interleaved over the group (c = rank + G u) for balance;
   // each CTA keeps 4 columns in registers and streams the reflectors.
-  if (m <= 8 * kT) qform_batched<4, 8>(Q, V, taus, m, k_stop, rank, G, sh);
+  if (k_stop >= 64 && m >= 512) qform_blocked(k_stop);
+  else if (m <= 8 * kT) qform_batched<4, 8>(Q, V, taus, m, k_stop, rank, G, sh);
   else if (m <= 16 * kT) qform_batched<2, 16>(Q, V, taus, m, k_stop, rank, G, sh);
   else {
     for (int64_t e = tid; e < (int64_t)(q1 - q0) * m; e += kT) {
