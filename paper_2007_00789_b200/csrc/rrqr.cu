@@ -82,6 +82,7 @@ struct Sh {
   double red8[kWarps][8];   // multi-value block reductions of the column pass
   double tot8[8];
   double xk[2][4];          // row k of the column-pass batch (by batch parity)
+  int nfrz_tmp;             // k_c search
   unsigned long long fmax;   // bits of the max norm^2 of my frozen columns (>= 0)
   int nb_start[1025];  // column start of each neighbour (panels with <= 1024)
   int wsum[kWarps];
@@ -1548,12 +1549,17 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
   __syncthreads();
   TL(tq);
   // k_c: first pivot below eps * r11 (dense.py:181-182)
-  int k_c = k_stop;
-  for (int t = 0; t < k_stop; ++t)
+  // (parallel first-index search: a sequential scan of k_stop dependent
+  // L2 loads cost ~1.5 ms on the largest panels)
+  if (tid == 0) sh.nfrz_tmp = k_stop;
+  __syncthreads();
+  for (int t = tid; t < k_stop; t += kT)
     if (__ldcg(piv + t) < eps * r11) {
-      k_c = t;
+      atomicMin(&sh.nfrz_tmp, t);
       break;
     }
+  __syncthreads();
+  const int k_c = sh.nfrz_tmp;
   const int n_fine = m - k_c;
   int n_corr = 0;  // rows of e_tilde kept in the dead slots
   if (scheme == 1) n_corr = n_fine;
