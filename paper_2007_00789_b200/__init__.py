@@ -45,13 +45,16 @@ from .schemes import OpKind
 from .sparse import (
     SparseSymMatrix,
     baseline_problem,
+    c5_problem,
     diffusion_fv,
+    elasticity_q1,
     from_coo,
     jacobi_prescale,
     laplacian_2d,
     laplacian_3d,
     log_uniform_block_field,
     read_matrix_market,
+    rigid_body_modes,
     write_matrix_market,
 )
 

@@ -14,34 +14,41 @@ int vec_blocks(int n) {
   return b < 1 ? 1 : (b > kVecBlocksMax ? kVecBlocksMax : b);
 }
 
-// one warp per row; lanes stride the row's nonzeros (rows have 5-81 entries)
+// four lanes per row (a 256-thread CTA takes 64 rows): the BASELINE
+// matrices have 5-81 entries per row, so a full warp per row left most lanes
+// idle on the 5/7-point stencils; lanes stride the row's nonzeros and the
+// 4-lane sum is a fixed shuffle tree (reproducible)
 constexpr int kSpmvThreads = 256;
-constexpr int kRowsPerBlock = kSpmvThreads / 32;
+constexpr int kLanesPerRow = 4;
+constexpr int kRowsPerBlock = kSpmvThreads / kLanesPerRow;
 
 __global__ void __launch_bounds__(kSpmvThreads)
 spmv_kernel(int n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
             const double* __restrict__ va, const double* __restrict__ x,
             double* __restrict__ y, double* __restrict__ pdot) {
-  __shared__ double sh[kRowsPerBlock];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int row = blockIdx.x * kRowsPerBlock + w;
+  __shared__ double sh[kSpmvThreads / 32];
+  const int sub = threadIdx.x & (kLanesPerRow - 1);
+  const int row = blockIdx.x * kRowsPerBlock + (threadIdx.x / kLanesPerRow);
   double dotc = 0.0;
+  double s = 0.0;
   if (row < n) {
     const int b = __ldg(rp + row), e = __ldg(rp + row + 1);
-    double s = 0.0;
-    for (int k = b + lane; k < e; k += 32) s += __ldg(va + k) * __ldg(x + __ldg(ci + k));
-    s = warp_sum(s);
-    if (lane == 0) {
-      y[row] = s;
-      dotc = s * __ldg(x + row);
-    }
+    for (int k = b + sub; k < e; k += kLanesPerRow) s += __ldg(va + k) * __ldg(x + __ldg(ci + k));
+  }
+  s += __shfl_xor_sync(0xffffffffu, s, 1);
+  s += __shfl_xor_sync(0xffffffffu, s, 2);
+  if (row < n && sub == 0) {
+    y[row] = s;
+    dotc = s * __ldg(x + row);
   }
   if (pdot) {
-    if (lane == 0) sh[w] = dotc;
+    // rows of this CTA in order: warp sums (lanes 0, 4, ...) then warps
+    dotc = warp_sum(dotc);
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = dotc;
     __syncthreads();
     if (threadIdx.x == 0) {
       double t = 0.0;
-      for (int i = 0; i < kRowsPerBlock; ++i) t += sh[i];
+      for (int i = 0; i < kSpmvThreads / 32; ++i) t += sh[i];
       pdot[blockIdx.x] = t;
     }
   }
