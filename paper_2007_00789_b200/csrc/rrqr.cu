@@ -46,7 +46,6 @@ constexpr int kMaxM = 6144;  // v in shared memory
 // event row (12 int64): {p, m, n, k_stop, k_c, rank_f2, n_fine,
 //  bits(eta_stop), bits(r11), 0, 0, 0}
 
-constexpr int kBB = 32;        // column width of the Fb workspace region (frozen list)
 constexpr int kCR = 4;   // candidate record stride (doubles): contiguous, coalesced scans
 constexpr int kLDS = 68;       // frozen-column DMMA tiles (conflict-free fragments)
 // dynamic shared memory floor: write-back staging (8 warps x 16 x 33) and
@@ -60,7 +59,17 @@ constexpr int kCScr = 0, kCT = 2 * kPBK * (kLDS + 36), kCZ = kCT + 32 * 33, kCR2
               kCTail = kCR2 + 64 * 33, kColdEnd = kCTail + 64;
 constexpr size_t kColdSmem = (size_t)kColdEnd * sizeof(double);
 constexpr int kBlk = 32;         // reflectors per cold-column block update
-constexpr double kHotRho = 0.2;  // hot iff running norm^2 >= kHotRho * pivot norm^2
+// hot iff running norm^2 >= rho * pivot norm^2; rho grows with the panel
+// height (cheaper blocked cold updates vs. per-step column work; measured on
+// C4-L15 with rho in {0.1 .. 0.9}: best 0.35 below 700 rows, 0.5 below 1200,
+// 0.65 below 2000, 0.75 above)
+__device__ __forceinline__ double hot_rho(int m) {
+#ifdef SPAND_HOT_RHO
+  return SPAND_HOT_RHO;
+#else
+  return m < 700 ? 0.35 : (m < 1200 ? 0.5 : (m < 2000 ? 0.65 : 0.75));
+#endif
+}
 static_assert(kMinSmem >= 64 * 65 * sizeof(double), "epilogue tile");
 static_assert(kMinSmem >= (size_t)kWarps * 16 * 33 * sizeof(double), "gather tiles");
 static_assert(kColdSmem >= kMinSmem, "cold layout covers the other phases");
@@ -1193,7 +1202,7 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
       }
       __syncthreads();
       int32_t* cold_out = (coldl == coldA) ? coldB : coldA;
-      const double tau_hot = (maint == 2) ? -1.0 : kHotRho * last_wv;
+      const double tau_hot = (maint == 2) ? -1.0 : hot_rho(m) * last_wv;
       for (int u = tid; u < nh + ncd; u += kT) {
         const int c = u < nh ? hot_in[rank + G * u] : coldl[rank + G * (u - nh)];
         if (done[c]) continue;
