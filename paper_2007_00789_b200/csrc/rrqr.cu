@@ -304,22 +304,22 @@ __device__ void colpass_batch(const ColCtx& X, int a0, int nb, Sh& sh, double& b
   }
 }
 
-// short columns (len <= 256): a warp per column, U columns in flight per
+// short / medium columns (len <= 32 R): a warp per column, U columns in flight per
 // warp, warp reductions only; lane u applies the norm logic of column u and
 // keeps its best candidate (reduced per warp afterwards)
-template <int U>
+template <int U, int R>
 __device__ void colpass_warp(const ColCtx& X, int nact, double& bv, int64_t& bp, int& bc) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (int a0 = warp * U; a0 < nact; a0 += kWarps * U) {
     int cs[U];
-    double x[U][8];
+    double x[U][R];
 #pragma unroll
     for (int u = 0; u < U; ++u) cs[u] = a0 + u < nact ? X.list[X.rank + X.G * (a0 + u)] : -1;
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const double* col = X.W + (int64_t)(cs[u] < 0 ? 0 : cs[u]) * X.m + X.k;
 #pragma unroll
-      for (int e = 0; e < 8; ++e) {
+      for (int e = 0; e < R; ++e) {
         const int i = lane + 32 * e;
         x[u][e] = (cs[u] >= 0 && i < X.len) ? col[i] : 0.0;
       }
@@ -329,7 +329,7 @@ __device__ void colpass_warp(const ColCtx& X, int nact, double& bv, int64_t& bp,
     for (int u = 0; u < U; ++u) {
       double a = 0.0;
 #pragma unroll
-      for (int e = 0; e < 8; ++e) {
+      for (int e = 0; e < R; ++e) {
         const int i = lane + 32 * e;
         if (i < X.len) a += X.v[i] * x[u][e];
       }
@@ -341,7 +341,7 @@ __device__ void colpass_warp(const ColCtx& X, int nact, double& bv, int64_t& bp,
       double* col = X.W + (int64_t)(cs[u] < 0 ? 0 : cs[u]) * X.m + X.k;
       double tail = 0.0, rk = 0.0;
 #pragma unroll
-      for (int e = 0; e < 8; ++e) {
+      for (int e = 0; e < R; ++e) {
         const int i = lane + 32 * e;
         if (cs[u] >= 0 && i < X.len) {
           const double y = x[u][e] - w * X.v[i];
@@ -1457,7 +1457,11 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
       ColCtx X{W, m, k, len, tau, vsh, cur, ref, pos, list_out, rank, G,
                reinterpret_cast<unsigned long long*>(events + 12 * slot + 10), jpos};
       if (len <= 256) {
-        colpass_warp<4>(X, nact, bv, bp, bc);
+        colpass_warp<4, 8>(X, nact, bv, bp, bc);
+      } else if (len <= 512) {
+        colpass_warp<2, 16>(X, nact, bv, bp, bc);
+      } else if (len <= 1024) {
+        colpass_warp<1, 32>(X, nact, bv, bp, bc);
       } else if (len <= 8 * kT) {
         for (int a0 = 0; a0 < nact; a0 += 4)
           colpass_batch<4, 8>(X, a0, min(4, nact - a0), sh, bv, bp, bc);
