@@ -67,7 +67,13 @@ __device__ __forceinline__ double hot_rho(int m) {
 #ifdef SPAND_HOT_RHO
   return SPAND_HOT_RHO;
 #else
-  return m < 700 ? 0.35 : (m < 1200 ? 0.5 : (m < 2000 ? 0.65 : 0.75));
+#ifndef SPAND_RHO_A
+#define SPAND_RHO_A 0.35
+#define SPAND_RHO_B 0.5
+#define SPAND_RHO_C 0.65
+#define SPAND_RHO_D 0.75
+#endif
+  return m < 700 ? SPAND_RHO_A : (m < 1200 ? SPAND_RHO_B : (m < 2000 ? SPAND_RHO_C : SPAND_RHO_D));
 #endif
 }
 static_assert(kMinSmem >= 64 * 65 * sizeof(double), "epilogue tile");
