@@ -83,6 +83,7 @@ def load(path=LIB_PATH):
 COUNTS = {}
 # optional per-entry-point CUDA-event timing (profile() context manager)
 _PROFILE = None
+_PROFILE_NAMES = None
 
 # host-only entry points (no kernel launch)
 _HOST_ONLY = {"spand_plan_sizes", "spand_plan_emit", "spand_plan_program",
@@ -93,7 +94,8 @@ _HOST_ONLY = {"spand_plan_sizes", "spand_plan_emit", "spand_plan_program",
 def call(name, *args):
     """Invoke an entry point; nonzero status raises RuntimeError."""
     fn = getattr(load(), name)
-    if _PROFILE is not None and name not in _HOST_ONLY and not _capturing():
+    if (_PROFILE is not None and name not in _HOST_ONLY
+            and (_PROFILE_NAMES is None or name in _PROFILE_NAMES) and not _capturing()):
         import torch
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
@@ -121,11 +123,18 @@ def launches():
 
 class profile:
     """Context manager: per-entry-point device time (ms) on the current
-    stream, measured with CUDA events around every call()."""
+    stream, measured with CUDA events around every call() (or only around
+    the entry points in ``names``: events around ~10k launches per step cost
+    host time and launch gaps, so a timed region profiles only the kernel
+    whose roofline it reports)."""
+
+    def __init__(self, names=None):
+        self.names = None if names is None else set(names)
 
     def __enter__(self):
-        global _PROFILE
+        global _PROFILE, _PROFILE_NAMES
         _PROFILE = []
+        _PROFILE_NAMES = self.names
         self.result = {}
         return self
 
