@@ -17,13 +17,64 @@ constexpr int kTile = 64;
 constexpr int kBigPotrf = 256;   // larger diagonal blocks use the blocked (multi-CTA) Cholesky
 constexpr int kMaxGroupTotal = 148 * 16;   // >= any cooperative RRQR grid
 
+// Open-addressing hash map int64 -> int32 (linear probing, splitmix64),
+// for the block-id lookups of the symbolic analysis and the emission (an
+// std::unordered_map spent most of the analysis in node allocation and
+// pointer chasing, and its teardown took ~20 ms on C4-L15).
+struct BlockMap {
+  std::vector<int64_t> keys;
+  std::vector<int32_t> vals;
+  size_t mask = 0, used = 0;
+  static uint64_t mix(uint64_t x) {
+    x += 0x9e3779b97f4a7c15ull;
+    x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
+    x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
+    return x ^ (x >> 31);
+  }
+  void reserve(size_t n) {
+    size_t cap = 16;
+    while (cap < 2 * n) cap <<= 1;
+    if (cap <= keys.size()) return;
+    std::vector<int64_t> ok;
+    std::vector<int32_t> ov;
+    ok.swap(keys);
+    ov.swap(vals);
+    keys.assign(cap, -1);
+    vals.assign(cap, -1);
+    mask = cap - 1;
+    used = 0;
+    for (size_t s = 0; s < ok.size(); ++s)
+      if (ok[s] >= 0) put(ok[s], ov[s]);
+  }
+  void put(int64_t k, int32_t v) {
+    if (2 * (used + 1) > keys.size()) reserve(keys.empty() ? 16 : keys.size());
+    size_t s = mix((uint64_t)k) & mask;
+    while (keys[s] >= 0 && keys[s] != k) s = (s + 1) & mask;
+    if (keys[s] < 0) {
+      keys[s] = k;
+      ++used;
+    }
+    vals[s] = v;
+  }
+  int32_t find(int64_t k) const {
+    if (keys.empty()) return -1;
+    size_t s = mix((uint64_t)k) & mask;
+    while (keys[s] >= 0) {
+      if (keys[s] == k) return vals[s];
+      s = (s + 1) & mask;
+    }
+    return -1;
+  }
+};
+
 struct Level {
   int level = 0;
   bool skipped = true;
   std::vector<int> interiors;
   std::vector<std::vector<int>> inbrs;      // neighbours of each interior
   std::vector<int> targets;                 // Schur target block ids (creation order)
-  std::vector<std::vector<int>> tsegs;      // contributing interiors per target
+  // contributing interiors per target, CSR: tseg_idx[tseg_ptr[t] .. tseg_ptr[t + 1])
+  std::vector<int> tseg_ptr, tseg_idx;
   std::vector<int> active;
   std::vector<int> resc_blocks;             // off-diagonal blocks among active
   std::vector<int> wave;                    // per active cluster
@@ -39,7 +90,7 @@ struct Plan {
   std::vector<int32_t> depth;
   std::vector<int64_t> dofs, dptr;   // cluster dofs (original numbering), concatenated
   std::vector<int32_t> bi, bj;
-  std::unordered_map<int64_t, int32_t> bid;
+  BlockMap bid;
   std::vector<Level> lv;
   std::vector<int> fin, fin_blocks;
   // layout
@@ -54,12 +105,12 @@ struct Plan {
   int64_t nk_ws(int64_t mc) const { return nk ? kNkHead + 2 * mc * nk + mc * mc : 0; }
 
   int64_t key(int i, int j) const { return (int64_t)i * ncl + j; }
-  int block(int i, int j) const { return bid.at(key(i, j)); }
+  int block(int i, int j) const { return bid.find(key(i, j)); }
   int new_block(int i, int j, std::vector<std::vector<int>>& cb) {
     const int b = (int)bi.size();
     bi.push_back(i);
     bj.push_back(j);
-    bid[key(i, j)] = b;
+    bid.put(key(i, j), b);
     cb[i].push_back(b);
     if (j != i) cb[j].push_back(b);
     return b;
@@ -72,6 +123,17 @@ struct Plan {
   // to the ordered-set formulation (neighbour lists are sorted on read).
   void symbolic(int64_t npairs, const int64_t* pairs) {
     std::vector<std::vector<int>> adj(ncl), cb(ncl);
+    {
+      std::vector<int> cnt(ncl, 1);
+      for (int64_t t = 0; t < npairs; ++t) {
+        ++cnt[pairs[t] / ncl];
+        ++cnt[pairs[t] % ncl];
+      }
+      for (int c = 0; c < ncl; ++c) {
+        cb[c].reserve(2 * cnt[c]);
+        adj[c].reserve(2 * cnt[c]);
+      }
+    }
     bid.reserve((size_t)npairs * 4);
     bi.reserve((size_t)npairs * 2);
     bj.reserve((size_t)npairs * 2);
@@ -84,7 +146,7 @@ struct Plan {
       }
     }
     for (int c = 0; c < ncl; ++c)
-      if (!bid.count(key(c, c))) new_block(c, c, cb);
+      if (bid.find(key(c, c)) < 0) new_block(c, c, cb);
     std::vector<char> alive(ncl, 1);
     auto live_nbrs = [&](int c) {
       std::vector<int> nb;
@@ -95,10 +157,17 @@ struct Plan {
       adj[c] = nb;   // compact
       return nb;
     };
+    std::vector<int> seg_t, seg_s;   // (target index, interior) pairs of a level
     std::vector<int> tpos;      // block id -> target index at this level, stamped
     std::vector<int> tstamp;
     std::vector<int> wave_of(ncl, 0);
+#ifdef SPAND_PLAN_TIMING
+    double t_int = 0, t_act = 0;
+#endif
     for (int level = levels; level >= 1; --level) {
+#ifdef SPAND_PLAN_TIMING
+      auto c0 = std::chrono::steady_clock::now();
+#endif
       Level L;
       L.level = level;
       for (int c = 0; c < ncl; ++c)
@@ -109,16 +178,13 @@ struct Plan {
         for (size_t a2 = 0; a2 < nb.size(); ++a2)
           for (size_t b2 = a2; b2 < nb.size(); ++b2) {
             const int wa = nb[a2], wb = nb[b2];
-            auto it = bid.find(key(wa, wb));
-            int blk;
-            if (it == bid.end()) {
+            int blk = bid.find(key(wa, wb));
+            if (blk < 0) {
               blk = new_block(wa, wb, cb);
               if (wa != wb) {
                 adj[wa].push_back(wb);
                 adj[wb].push_back(wa);
               }
-            } else {
-              blk = it->second;
             }
             if ((int)tpos.size() <= blk) {
               tpos.resize(bi.size() + 1024, -1);
@@ -128,16 +194,30 @@ struct Plan {
               tstamp[blk] = level;
               tpos[blk] = (int)L.targets.size();
               L.targets.push_back(blk);
-              L.tsegs.push_back({s});
-            } else {
-              L.tsegs[tpos[blk]].push_back(s);
             }
+            seg_t.push_back(tpos[blk]);
+            seg_s.push_back(s);
           }
         alive[s] = 0;
         adj[s].clear();
         cb[s].clear();
       }
+      // group the (target, interior) pairs by target, interior order kept
+      L.tseg_ptr.assign(L.targets.size() + 1, 0);
+      for (int t2 : seg_t) ++L.tseg_ptr[t2 + 1];
+      for (size_t t2 = 0; t2 < L.targets.size(); ++t2) L.tseg_ptr[t2 + 1] += L.tseg_ptr[t2];
+      L.tseg_idx.resize(seg_s.size());
+      {
+        std::vector<int> fillp(L.tseg_ptr.begin(), L.tseg_ptr.end() - 1);
+        for (size_t q = 0; q < seg_s.size(); ++q) L.tseg_idx[fillp[seg_t[q]]++] = seg_s[q];
+      }
+      seg_t.clear();
+      seg_s.clear();
       L.skipped = (levels - level) < skip;
+#ifdef SPAND_PLAN_TIMING
+      auto c1 = std::chrono::steady_clock::now();
+      t_int += std::chrono::duration<double>(c1 - c0).count();
+#endif
       if (!L.skipped) {
         for (int c = 0; c < ncl; ++c)
           if (alive[c]) L.active.push_back(c);
@@ -158,8 +238,14 @@ struct Plan {
           L.nwaves = std::max(L.nwaves, wv + 1);
         }
       }
+#ifdef SPAND_PLAN_TIMING
+      t_act += std::chrono::duration<double>(std::chrono::steady_clock::now() - c1).count();
+#endif
       lv.push_back(std::move(L));
     }
+#ifdef SPAND_PLAN_TIMING
+    printf("interiors %.4f actives %.4f\n", t_int, t_act);
+#endif
     for (int c = 0; c < ncl; ++c)
       if (alive[c]) fin.push_back(c);
     std::vector<std::pair<int, int>> fb;
@@ -539,8 +625,10 @@ struct Plan {
             if ((wa == wb) != (diag == 1)) continue;
             Target x;
             opnd(x.c, pool_base + 8 * boff[b], wa, wb);
-            for (int s : L.tsegs[t])
+            for (int q = L.tseg_ptr[t]; q < L.tseg_ptr[t + 1]; ++q) {
+              const int s = L.tseg_idx[q];
               x.segs.push_back(((int64_t)block(wa, s) << 32) | (int64_t)block(wb, s));
+            }
             x.mm = m0[wa];
             x.nn = m0[wb];
             st.push_back(x);
