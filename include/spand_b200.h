@@ -237,6 +237,9 @@ int64_t spand_plan_pairs(int ncl, const int64_t* row_ptr, const int64_t* col_idx
                          const int64_t* cluster_of, const int64_t* cdofs, const int64_t* cptr,
                          int64_t* out);
 int spand_plan_set_dofs(void* h, const int64_t* dofs, const int64_t* dptr);
+/* pool offsets of A's upper-block entries in CSR order (-1: other triangle) */
+int spand_plan_scatter(void* h, const int64_t* row_ptr, const int64_t* col_idx,
+                       const int64_t* cluster_of, int64_t* where);
 int spand_plan_sizes(void* h, int64_t* out);
 int spand_plan_emit(void* h, int64_t pool_base, int64_t fac_base, int64_t temp_base,
                     int64_t ctr_base, int dry);

@@ -81,6 +81,43 @@ int64_t spand_plan_pairs(int ncl, const int64_t* row_ptr, const int64_t* col_idx
   return cnt;
 }
 
+// Pool positions of A's entries (factorize.py:61-96, the initial blocks):
+// where[e] for CSR entry e = (r, c) with cluster(r) <= cluster(c) is the
+// column-major offset of (slot(r), slot(c)) inside block (cluster(r),
+// cluster(c)); -1 for the other triangle.  Needs spand_plan_set_dofs.
+int spand_plan_scatter(void* h, const int64_t* row_ptr, const int64_t* col_idx,
+                       const int64_t* cluster_of, int64_t* where) {
+  Plan* p = static_cast<Plan*>(h);
+  const int ncl = p->ncl;
+  const int64_t n = p->dptr[ncl];
+  std::vector<int64_t> slot(n);
+  for (int c = 0; c < ncl; ++c)
+    for (int64_t u = p->dptr[c]; u < p->dptr[c + 1]; ++u) slot[p->dofs[u]] = u - p->dptr[c];
+  std::vector<int> stamp(ncl, -1);
+  std::vector<int64_t> base(ncl, 0);
+  for (int ci = 0; ci < ncl; ++ci) {
+    for (int64_t u = p->dptr[ci]; u < p->dptr[ci + 1]; ++u) {
+      const int64_t r = p->dofs[u];
+      for (int64_t e = row_ptr[r]; e < row_ptr[r + 1]; ++e) {
+        const int64_t c = col_idx[e];
+        const int cj = (int)cluster_of[c];
+        if (cj < ci) {
+          where[e] = -1;
+          continue;
+        }
+        if (stamp[cj] != ci) {
+          stamp[cj] = ci;
+          const int b = p->block(ci, cj);
+          if (b < 0) return -1;
+          base[cj] = p->boff[b];
+        }
+        where[e] = base[cj] + slot[r] + slot[c] * p->m0[ci];
+      }
+    }
+  }
+  return 0;
+}
+
 // near-kernel extension: number of vectors (0 = reference path); resizes
 // the workspace bound, so call before spand_plan_sizes / emission
 int spand_plan_set_nk(void* h, int k) {

@@ -343,21 +343,19 @@ class Engine:
         if cached is not None and cached[0] is self.h:
             self.pool[cached[1]] = cached[2]
             return
-        n = a.n
-        rows = np.repeat(np.arange(n, dtype=np.int64), np.diff(a.row_ptr))
-        cols = a.col_idx
-        cl = sym.cluster_of
-        slot = np.empty(n, dtype=np.int64)
-        for c, dd in enumerate(sym.dofs):
-            slot[dd] = np.arange(dd.size)
-        ci, cj = cl[rows], cl[cols]
-        up = ci <= cj
-        ci, cj, r, c = ci[up], cj[up], rows[up], cols[up]
-        keys = ci * sym.ncl + cj
-        kk = sym.bi * sym.ncl + sym.bj
-        order = np.argsort(kk)
-        pos = order[np.searchsorted(kk[order], keys)]
-        where = sym.boff[pos] + slot[r] + slot[c] * sym.m0[ci]
+        import ctypes
+        lib = sym._lib
+        rp = np.ascontiguousarray(a.row_ptr, dtype=np.int64)
+        cx = np.ascontiguousarray(a.col_idx, dtype=np.int64)
+        cof = np.ascontiguousarray(sym.cluster_of, dtype=np.int64)
+        where = np.empty(max(cx.size, 1), dtype=np.int64)
+        lib.spand_plan_scatter.argtypes = [ctypes.c_void_p] * 5
+        if lib.spand_plan_scatter(sym.h, sym._vp(rp), sym._vp(cx), sym._vp(cof),
+                                  sym._vp(where)) != 0:
+            raise RuntimeError("block of a nonzero of A missing from the symbolic structure")
+        where = where[:cx.size]
+        up = where >= 0
+        where = where[up]
         vals = a.values[up]
         wd, vd = to_dev_async(where, np.int64), to_dev_async(vals, np.float64)
         self.pool[wd] = vd

@@ -62,13 +62,13 @@ class SparseSymMatrix:
         same_row = rows[1:] == rows[:-1]
         if np.any(np.diff(ci)[same_row] <= 0):
             raise ParseError("column indices must be strictly increasing per row")
-        # exact symmetry of pattern and values: sort the transpose's
-        # triplets into row-major order and compare elementwise
-        key_t = ci * n + rows
-        order = np.argsort(key_t, kind="stable")
-        if not (np.array_equal(ci[order], rows) and
-                np.array_equal(rows[order], ci) and
-                np.array_equal(va[order], va)):
+        # exact symmetry of pattern and values: the CSC form of the matrix is
+        # the CSR form of its transpose (scipy's O(nnz) conversion, sorted
+        # indices), compared array by array
+        import scipy.sparse as sps
+        mt = sps.csr_matrix((va, ci, rp), shape=(n, n)).tocsc()
+        if not (np.array_equal(mt.indptr, rp) and np.array_equal(mt.indices, ci) and
+                np.array_equal(mt.data, va)):
             raise AsymmetricValues("stored pattern or values are not symmetric")
         diag_pos = np.flatnonzero(rows == ci)
         if diag_pos.size != n or np.any(va[diag_pos] <= 0.0):

@@ -53,7 +53,7 @@ def test_header_symbols_are_typed_or_handle_based():
     bound with explicit argtypes where it is used (handle-returning ones)."""
     handle_based = {"spand_plan_create", "spand_plan_destroy", "spand_plan_set_dofs",
                     "spand_plan_emit_begin", "spand_plan_emit_next", "spand_plan_chunk",
-                    "spand_plan_pairs",
+                    "spand_plan_pairs", "spand_plan_scatter",
                     "spand_collect_create", "spand_collect_destroy", "spand_collect_sizes",
                     "spand_collect_get", "spand_collect_apply", "spand_collect_apply_get"}
     for nm in _declared():
@@ -224,3 +224,35 @@ def test_nd_partition_rejects_bad_input():
     vp = lambda x: x.ctypes.data_as(ctypes.c_void_p)  # noqa: E731
     rc = lib.spand_nd_partition(ctypes.c_int64(-1), vp(z), vp(z), 3, vp(z), vp(z), vp(d), vp(z))
     assert rc == -1
+
+
+@pytest.mark.parametrize("tag", ["lap3d_d8_L6_e0.01_k1_second-full", "C5_ne12_L6_e0.01_second-full"])
+def test_native_scatter_positions(tag):
+    """spand_plan_scatter (the initial blocks, factorize.py:61-96) against a
+    NumPy restatement: every upper-block entry of A lands at its cluster
+    slots inside its block, column-major at the original block size."""
+    rec, plan = _plan(tag)
+    a = matrix_for(tag)
+    n = a.n
+    rows = np.repeat(np.arange(n, dtype=np.int64), np.diff(a.row_ptr))
+    cols = a.col_idx
+    cl = plan.cluster_of
+    slot = np.empty(n, dtype=np.int64)
+    for c, dd in enumerate(plan.dofs):
+        slot[dd] = np.arange(dd.size)
+    ci, cj = cl[rows], cl[cols]
+    up = ci <= cj
+    bid = plan.bid
+    want = np.full(cols.size, -1, dtype=np.int64)
+    for e in np.flatnonzero(up):
+        b = bid[(int(ci[e]), int(cj[e]))]
+        want[e] = plan.boff[b] + slot[rows[e]] + slot[cols[e]] * plan.m0[ci[e]]
+    got = np.empty(cols.size, dtype=np.int64)
+    vp = lambda x: x.ctypes.data_as(ctypes.c_void_p)  # noqa: E731
+    lib = _lib.load()
+    lib.spand_plan_scatter.argtypes = [ctypes.c_void_p] * 5
+    rp = np.ascontiguousarray(a.row_ptr, dtype=np.int64)
+    cx = np.ascontiguousarray(a.col_idx, dtype=np.int64)
+    cof = np.ascontiguousarray(cl, dtype=np.int64)
+    assert lib.spand_plan_scatter(plan.h, vp(rp), vp(cx), vp(cof), vp(got)) == 0
+    assert np.array_equal(got, want)
