@@ -58,7 +58,10 @@ constexpr int kPBK = 32;         // rows per stage of the cold-column product
 constexpr int kCScr = 0, kCT = 2 * kPBK * (kLDS + 36), kCZ = kCT + 32 * 33, kCR2 = kCZ + 64 * 33,
               kCTail = kCR2 + 64 * 33, kColdEnd = kCTail + 64;
 constexpr size_t kColdSmem = (size_t)kColdEnd * sizeof(double);
-constexpr int kBlk = 32;         // reflectors per cold-column block update
+#ifndef SPAND_BLK
+#define SPAND_BLK 32
+#endif
+constexpr int kBlk = SPAND_BLK;  // reflectors per cold-column block update (<= 32)
 // hot iff running norm^2 >= rho * pivot norm^2; rho grows with the panel
 // height (cheaper blocked cold updates vs. per-step column work; measured on
 // C4-L15 with rho in {0.1 .. 0.9}: best 0.35 below 700 rows, 0.5 below 1200,
