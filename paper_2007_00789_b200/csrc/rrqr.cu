@@ -1543,7 +1543,10 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
   // Column c of Q is H_0 ... H_{k-1} e_c, and H_t leaves e_c alone for t > c.
   // Columns are interleaved over the group (c = rank + G u) for balance;
   // each CTA keeps 4 columns in registers and streams the reflectors.
-  if (k_stop >= 64 && m >= 512) qform_blocked(k_stop);
+#ifndef SPAND_QB_MMIN
+#define SPAND_QB_MMIN 64
+#endif
+  if (k_stop >= 64 && m >= SPAND_QB_MMIN) qform_blocked(k_stop);
   else if (m <= 8 * kT) qform_batched<4, 8>(Q, V, taus, m, k_stop, rank, G, sh);
   else if (m <= 16 * kT) qform_batched<2, 16>(Q, V, taus, m, k_stop, rank, G, sh);
   else {
@@ -1752,7 +1755,7 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
     atomicAdd(reinterpret_cast<unsigned long long*>(events + 12 * slot + 11), (unsigned long long)nf);
   TL(twb);
 #ifdef SPAND_RRQR_PHASES
-  if (lane == 0 && warp == 0 && m >= 1000 && (rank == 0 || rank == G / 2))
+  if (lane == 0 && warp == 0 && m >= SPAND_PHASE_MMIN && (rank == 0 || rank == G / 2))
     printf("[rrqr phases] p %d m %d n %d G %d rank %d k %d nf %d act-steps %lld hot %lld hot3 %lld | kcycles: cand %lld maint %lld pivcol %lld refl %lld colpass %lld publish %lld barrier %lld | Q %lld restore %lld frozen-gemm %lld writeback %lld\n",
            p, m, n, G, rank, k_stop, nf, nact_sum, hot_sum, hot3_sum, ph_t[0] / 1000, ph_t[6] / 1000, ph_t[1] / 1000, ph_t[2] / 1000,
            ph_t[3] / 1000, ph_t[4] / 1000, ph_t[5] / 1000, tq / 1000, trs / 1000, tg / 1000,
