@@ -387,6 +387,11 @@ class Engine:
                                                       SCHEME_CODE[self.scheme]))
         self.collected = Collected(lib, ch, vp)
         col = self.collected
+        # the apply image compiles on a host thread while the diagnostics and
+        # the nonzero count below run (the first apply waits for it)
+        from .fastplan import NativeApplyPlan
+        perm_c = np.concatenate(sym.dofs) if sym.dofs else np.empty(0, np.int64)
+        self.apply_plan = NativeApplyPlan(self.a.n, perm_c, col, self.pool, self.facbuf)
         ops = LazyOps(col, sym.dofs, self.pool, self.facbuf)
         # diagnostics (factorize.py:331-356) + margins of every decision
         diags = []
@@ -552,12 +557,5 @@ def run_factorization(a, h, eps, scheme, skip_levels, collect_local_errors=False
                       skip_levels=int(skip_levels), nnz_factor=int(nnz),
                       diagnostics=diag,
                       _keep=(eng.pool, eng.facbuf, eng.geo), timings=eng.timings)
-    perm_c = np.concatenate(eng.sym.dofs) if eng.sym.dofs else np.empty(0, np.int64)
-    col, pool, fac = eng.collected, eng.pool, eng.facbuf
-
-    def factory():
-        from .fastplan import NativeApplyPlan
-        return NativeApplyPlan(a.n, perm_c, col, pool, fac)
-
-    f._plan_factory = factory
+    f._plan = eng.apply_plan
     return f

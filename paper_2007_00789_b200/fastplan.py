@@ -10,6 +10,9 @@ vector (no index arrays), task and tile arrays are generated with NumPy in
 bulk (no per-tile Python), and the vector is permuted in/out once per call.
 """
 
+import time
+from concurrent.futures import ThreadPoolExecutor
+
 import numpy as np
 
 from . import _lib
@@ -239,15 +242,24 @@ class FastPlan:
         return xd
 
 
+_COMPILER = ThreadPoolExecutor(1, thread_name_prefix="spand-apply-image")
+
+
 class NativeApplyPlan(FastPlan):
     """The same structured apply, with the task / tile / scatter image built
     by the native collector (csrc/collect.cpp) instead of NumPy."""
 
+    # attributes available once the host-compiled image is uploaded
+    _LAZY = frozenset(("fwd", "bwd", "scratch", "scratch_len", "image", "image_host",
+                       "phase_table", "build_times"))
+
     def __init__(self, n, perm_new_to_old, collected, pool, fac):
-        import ctypes
-        import time
+        """Allocate the device vectors and start compiling the apply image on
+        a host thread (ctypes releases the GIL): the compile overlaps the rest
+        of the factorization's host work (diagnostics, nnz count); the image
+        is uploaded at the first apply."""
         t = require_cuda()
-        tm = [time.perf_counter()]
+        self._t0 = time.perf_counter()
         self.n = int(n)
         self.perm = to_dev(np.asarray(perm_new_to_old, dtype=np.int32), np.int32)
         # NVEC_MAX permuted vectors, column-major (leading dimension n): the
@@ -255,26 +267,50 @@ class NativeApplyPlan(FastPlan):
         self.xbuf = t.zeros(max(self.n, 1) * self.NVEC_MAX, dtype=t.float64, device=dev())
         self._fidx = to_dev(np.asarray(collected.fidx if collected.fidx.size else [0],
                                        dtype=np.int32), np.int32)
+        self._graph = None
+        self._collected = collected
+        self._future = _COMPILER.submit(self._compile_image, collected, pool.data_ptr(),
+                                        fac.data_ptr(), self.xbuf.data_ptr(),
+                                        self._fidx.data_ptr())
+
+    @staticmethod
+    def _compile_image(collected, pool_base, fac_base, xbuf, fidx):
+        import ctypes
         lib, vp = collected.lib, collected.vp
+        t0 = time.perf_counter()
         out = np.zeros(4, dtype=np.int64)
         lib.spand_collect_apply.argtypes = [ctypes.c_void_p] + [ctypes.c_int64] * 4 + \
             [ctypes.c_void_p]
-        rc = lib.spand_collect_apply(collected.h, pool.data_ptr(), fac.data_ptr(),
-                                     self.xbuf.data_ptr(), self._fidx.data_ptr(), vp(out))
+        rc = lib.spand_collect_apply(collected.h, pool_base, fac_base, xbuf, fidx, vp(out))
         if rc != 0:
             raise RuntimeError(f"apply image build failed ({rc}): an operator exceeds "
                                "the packed work-item limits")
-        tm.append(time.perf_counter())
-        ilen, nfw, nbw, self.scratch_len = (int(x) for x in out)
+        t1 = time.perf_counter()
+        ilen, nfw, nbw, scratch_len = (int(x) for x in out)
         image = np.zeros(max(ilen, 1), dtype=np.int64)
         ph = np.zeros((nfw + nbw, 10), dtype=np.int64)
         lib.spand_collect_apply_get.argtypes = [ctypes.c_void_p] * 3
         lib.spand_collect_apply_get(collected.h, vp(image), vp(ph))
-        tm.append(time.perf_counter())
+        return image, ph, nfw, scratch_len, (t1 - t0, time.perf_counter() - t1)
+
+    def __getattr__(self, name):
+        if name in NativeApplyPlan._LAZY:
+            self._ensure()
+            return object.__getattribute__(self, name)
+        raise AttributeError(name)
+
+    def _ensure(self):
+        import ctypes
+        if "fwd" in self.__dict__:
+            return
+        t = require_cuda()
+        image, ph, nfw, scratch_len, (t_setup, t_image) = self._future.result()
+        t0 = time.perf_counter()
+        self.scratch_len = scratch_len
         self.image = to_dev_async(image)
         self.image_host = image
         base = self.image.data_ptr()
-        self.scratch = t.empty(max(self.scratch_len, 1), dtype=t.float64, device=dev())
+        self.scratch = t.empty(max(scratch_len, 1), dtype=t.float64, device=dev())
         rows = []
         for r in ph.tolist():
             to, nt, tio, nitem, co, nch, cbo, grid, _, _ = r
@@ -282,11 +318,11 @@ class NativeApplyPlan(FastPlan):
                          nitem, ctypes.c_void_p(base + 8 * co), nch,
                          ctypes.c_void_p(base + 8 * cbo), grid))
         self.phase_table = ph
-        self.fwd, self.bwd = rows[:nfw], rows[nfw:]
-        self._graph = None
-        tm.append(time.perf_counter())
-        self.build_times = {"setup_s": tm[1] - tm[0], "image_s": tm[2] - tm[1],
-                            "upload_s": tm[3] - tm[2], "image_mb": image.nbytes / 1e6}
+        self.build_times = {"setup_s": t_setup, "image_s": t_image,
+                            "upload_s": time.perf_counter() - t0, "image_mb": image.nbytes / 1e6,
+                            "since_factor_s": time.perf_counter() - self._t0}
+        self.bwd = rows[nfw:]
+        self.fwd = rows[:nfw]
 
     NVEC_MAX = 8   # right-hand sides per multi-vector pass
 
