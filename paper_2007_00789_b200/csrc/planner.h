@@ -7,6 +7,7 @@
 #include <map>
 #include <set>
 #include <unordered_map>
+#include <utility>
 #include <vector>
 
 extern "C" int spand_rrqr_capacity(int vmax);
@@ -73,8 +74,12 @@ struct Level {
   std::vector<int> interiors;
   std::vector<std::vector<int>> inbrs;      // neighbours of each interior
   std::vector<int> targets;                 // Schur target block ids (creation order)
-  // contributing interiors per target, CSR: tseg_idx[tseg_ptr[t] .. tseg_ptr[t + 1])
+  // contributing interiors per target, CSR: tseg_idx[tseg_ptr[t] .. tseg_ptr[t + 1]);
+  // tseg_blk holds the segment's two panel blocks {block(wa, s) << 32 | block(wb, s)}
   std::vector<int> tseg_ptr, tseg_idx;
+  std::vector<int64_t> tseg_blk;
+  // panel blocks block(w, s) of each interior, aligned with inbrs (CSR)
+  std::vector<int> inb_ptr, inb_blk;
   std::vector<int> active;
   std::vector<int> resc_blocks;             // off-diagonal blocks among active
   std::vector<int> wave;                    // per active cluster
@@ -158,6 +163,7 @@ struct Plan {
       return nb;
     };
     std::vector<int> seg_t, seg_s;   // (target index, interior) pairs of a level
+    std::vector<int64_t> seg_b;      // their panel blocks
     std::vector<int> tpos;      // block id -> target index at this level, stamped
     std::vector<int> tstamp;
     std::vector<int> wave_of(ncl, 0);
@@ -172,9 +178,13 @@ struct Plan {
       L.level = level;
       for (int c = 0; c < ncl; ++c)
         if (alive[c] && depth[c] == level) L.interiors.push_back(c);
+      L.inb_ptr.assign(1, 0);
       for (int s : L.interiors) {
         std::vector<int> nb = live_nbrs(s);
         L.inbrs.push_back(nb);
+        const size_t ib0 = L.inb_blk.size();
+        for (int w : nb) L.inb_blk.push_back(bid.find(key(w, s)));
+        L.inb_ptr.push_back((int)L.inb_blk.size());
         for (size_t a2 = 0; a2 < nb.size(); ++a2)
           for (size_t b2 = a2; b2 < nb.size(); ++b2) {
             const int wa = nb[a2], wb = nb[b2];
@@ -197,6 +207,8 @@ struct Plan {
             }
             seg_t.push_back(tpos[blk]);
             seg_s.push_back(s);
+            seg_b.push_back(((int64_t)L.inb_blk[ib0 + a2] << 32) |
+                            (int64_t)L.inb_blk[ib0 + b2]);
           }
         alive[s] = 0;
         adj[s].clear();
@@ -207,12 +219,18 @@ struct Plan {
       for (int t2 : seg_t) ++L.tseg_ptr[t2 + 1];
       for (size_t t2 = 0; t2 < L.targets.size(); ++t2) L.tseg_ptr[t2 + 1] += L.tseg_ptr[t2];
       L.tseg_idx.resize(seg_s.size());
+      L.tseg_blk.resize(seg_s.size());
       {
         std::vector<int> fillp(L.tseg_ptr.begin(), L.tseg_ptr.end() - 1);
-        for (size_t q = 0; q < seg_s.size(); ++q) L.tseg_idx[fillp[seg_t[q]]++] = seg_s[q];
+        for (size_t q = 0; q < seg_s.size(); ++q) {
+          const int at = fillp[seg_t[q]]++;
+          L.tseg_idx[at] = seg_s[q];
+          L.tseg_blk[at] = seg_b[q];
+        }
       }
       seg_t.clear();
       seg_s.clear();
+      seg_b.clear();
       L.skipped = (levels - level) < skip;
 #ifdef SPAND_PLAN_TIMING
       auto c1 = std::chrono::steady_clock::now();
@@ -330,18 +348,41 @@ struct Plan {
   int64_t info_next = 0, ctr_next = 0;
 
   int64_t blk_ptr(int i, int j) const { return pool_base + 8 * boff[block(i, j)]; }
-  static void opnd(std::vector<int64_t>& v, int64_t p, int rc, int cc, int64_t rs = 0,
-                   int64_t cs = 0, int64_t rn = -1, int64_t cn = -1) {
-    v.insert(v.end(), {p, rc, cc, rs, cs, rn, cn});
+  // Small vector with inline storage: GEMM targets are built by the hundred
+  // thousand per level, and two heap vectors per target dominated the emission
+  struct SmallVec {
+    static constexpr int kIn = 16;
+    int64_t buf[kIn];
+    std::vector<int64_t> heap;
+    int n = 0;
+    void push_back(int64_t x) {
+      if (n < kIn) {
+        buf[n] = x;
+      } else {
+        if (n == kIn) heap.assign(buf, buf + kIn);
+        heap.push_back(x);
+      }
+      ++n;
+    }
+    const int64_t* data() const { return n <= kIn ? buf : heap.data(); }
+    size_t size() const { return (size_t)n; }
+    bool empty() const { return n == 0; }
+  };
+  template <class V>
+  static void opnd(V& v, int64_t p, int rc, int cc, int64_t rs = 0, int64_t cs = 0,
+                   int64_t rn = -1, int64_t cn = -1) {
+    const int64_t e[7] = {p, rc, cc, rs, cs, rn, cn};
+    for (int64_t x : e) v.push_back(x);
   }
   // sub-operand at (rs, cs) of o, clamped to rn x cn (< 0: to o's extent)
-  static void sub(std::vector<int64_t>& v, const int64_t* o, int64_t rs, int64_t cs, int64_t rn,
-                  int64_t cn) {
+  template <class V>
+  static void sub(V& v, const int64_t* o, int64_t rs, int64_t cs, int64_t rn, int64_t cn) {
     const int64_t rl = o[5] < 0 ? -1 : std::max(o[5] - rs, (int64_t)0);
     const int64_t cl = o[6] < 0 ? -1 : std::max(o[6] - cs, (int64_t)0);
     const int64_t r = rn < 0 ? rl : (rl < 0 ? rn : std::min(rn, rl));
     const int64_t c = cn < 0 ? cl : (cl < 0 ? cn : std::min(cn, cl));
-    v.insert(v.end(), {o[0], o[1], o[2], o[3] + rs, o[4] + cs, r, c});
+    const int64_t e[7] = {o[0], o[1], o[2], o[3] + rs, o[4] + cs, r, c};
+    for (int64_t x : e) v.push_back(x);
   }
   bool dry = false;   // sizing pass: compute temp_size only, emit nothing
   int64_t push(const std::vector<int64_t>& rows) {
@@ -361,8 +402,8 @@ struct Plan {
   }
 
   struct Target {
-    std::vector<int64_t> c;          // 7
-    std::vector<int64_t> segs;       // 14 per segment (or 1 per segment, compact)
+    SmallVec c;          // 7
+    SmallVec segs;       // 14 per segment (or 1 per segment, compact)
     int64_t mm, nn;
   };
   // tri: triangular-operand K bounds (gemm.cu): 1 A lower, 2 B lower with
@@ -373,10 +414,11 @@ struct Plan {
     const int64_t sw = compact ? 1 : 14;
     std::vector<int64_t> trow, srow, tiles;
     int64_t nseg = 0;
+    trow.reserve(8 * ts.size() + 8);
     for (size_t t = 0; t < ts.size(); ++t) {
-      trow.insert(trow.end(), ts[t].c.begin(), ts[t].c.end());
+      trow.insert(trow.end(), ts[t].c.data(), ts[t].c.data() + ts[t].c.size());
       trow.push_back(nseg);
-      srow.insert(srow.end(), ts[t].segs.begin(), ts[t].segs.end());
+      srow.insert(srow.end(), ts[t].segs.data(), ts[t].segs.data() + ts[t].segs.size());
       nseg += (int64_t)ts[t].segs.size() / sw;
       if (dry) continue;
       for (int64_t i = 0; i < ts[t].mm; i += kTile)
@@ -427,14 +469,14 @@ struct Plan {
           sub(a.segs, Xs[t].data(), o, o, s, s);
           a.mm = s;
           a.nn = s;
-          g1.push_back(a);
+          g1.push_back(std::move(a));
           Target b;
           sub(b.c, Xs[t].data(), o + s, o, s, s);
           sub(b.segs, Xs[t].data(), o + s, o + s, s, s);
           sub(b.segs, tmp.data(), o + s, o, s, s);
           b.mm = s;
           b.nn = s;
-          g2.push_back(b);
+          g2.push_back(std::move(b));
         }
       }
       gemm(g1, 1.0, 0.0, 0, 0, 4);    // tmp = L21 X11 (X11 lower)
@@ -496,13 +538,13 @@ struct Plan {
             sub(a.segs, tmp.data(), o, o, kTile, kTile);
             a.mm = sz - o - kTile;
             a.nn = kTile;
-            pan.push_back(a);
+            pan.push_back(std::move(a));
             Target b;
             sub(b.c, op, o + kTile, o + kTile, -1, -1);
             sub(b.segs, op, o + kTile, o, -1, kTile);
             sub(b.segs, op, o + kTile, o, -1, kTile);
             b.mm = b.nn = sz - o - kTile;
-            trail.push_back(b);
+            trail.push_back(std::move(b));
           }
         }
         launch(1, (int64_t)diag.size() / 8, push(diag), 0, 0, o, 1);
@@ -587,8 +629,8 @@ struct Plan {
           std::vector<int64_t> l, x;
           opnd(l, blk_ptr(s, s), s, s);
           opnd(x, fac_base + 8 * elim_linv[s], s, s);
-          Ls.push_back(l);
-          Xs.push_back(x);
+          Ls.push_back(std::move(l));
+          Xs.push_back(std::move(x));
           sz.push_back(m0[s]);
         }
         trtri(Ls, Xs, sz, 0);
@@ -596,18 +638,22 @@ struct Plan {
         std::vector<Target> tg;
         std::vector<int64_t> cps;
         int64_t acc = 0;
+        tg.reserve(L.inb_blk.size());
+        cps.reserve(15 * L.inb_blk.size());
         for (size_t k = 0; k < L.interiors.size(); ++k) {
           const int s = L.interiors[k];
-          for (int w : L.inbrs[k]) {
+          for (size_t u = 0; u < L.inbrs[k].size(); ++u) {
+            const int w = L.inbrs[k][u];
+            const int64_t pws = pool_base + 8 * boff[L.inb_blk[L.inb_ptr[k] + u]];
             Target t;
             opnd(t.c, temp_base + 8 * acc, w, s);
-            opnd(t.segs, blk_ptr(w, s), w, s);
+            opnd(t.segs, pws, w, s);
             opnd(t.segs, fac_base + 8 * elim_linv[s], s, s);
             t.mm = m0[w];
             t.nn = m0[s];
-            tg.push_back(t);
+            tg.push_back(std::move(t));
             opnd(cps, temp_base + 8 * acc, w, s);
-            opnd(cps, blk_ptr(w, s), w, s);
+            opnd(cps, pws, w, s);
             cps.push_back(0);
             acc += m0[w] * m0[s];
           }
@@ -625,13 +671,10 @@ struct Plan {
             if ((wa == wb) != (diag == 1)) continue;
             Target x;
             opnd(x.c, pool_base + 8 * boff[b], wa, wb);
-            for (int q = L.tseg_ptr[t]; q < L.tseg_ptr[t + 1]; ++q) {
-              const int s = L.tseg_idx[q];
-              x.segs.push_back(((int64_t)block(wa, s) << 32) | (int64_t)block(wb, s));
-            }
+            for (int q = L.tseg_ptr[t]; q < L.tseg_ptr[t + 1]; ++q) x.segs.push_back(L.tseg_blk[q]);
             x.mm = m0[wa];
             x.nn = m0[wb];
-            st.push_back(x);
+            st.push_back(std::move(x));
           }
           gemm(st, -1.0, 1.0, 1, diag, 0, 1);
         }
@@ -653,8 +696,8 @@ struct Plan {
         std::vector<int64_t> l, x;
         opnd(l, fac_base + 8 * L.l_off[k], p, p);
         opnd(x, fac_base + 8 * L.linv_off[k], p, p);
-        Ls.push_back(l);
-        Xs.push_back(x);
+        Ls.push_back(std::move(l));
+        Xs.push_back(std::move(x));
         sz.push_back(m0[p]);
         opnd(c2, blk_ptr(p, p), p, p);
         opnd(c2, blk_ptr(p, p), p, p);
@@ -690,14 +733,14 @@ struct Plan {
           opnd(t1.segs, pool_base + 8 * boff[b], i, j);
           t1.mm = m0[i];
           t1.nn = m0[j];
-          g1.push_back(t1);
+          g1.push_back(std::move(t1));
           Target t2;
           opnd(t2.c, pool_base + 8 * boff[b], i, j);
           opnd(t2.segs, temp_base + 8 * acc, i, j);
           opnd(t2.segs, fac_base + 8 * linv_of.at(j), j, j);
           t2.mm = m0[i];
           t2.nn = m0[j];
-          g2.push_back(t2);
+          g2.push_back(std::move(t2));
           acc += m0[i] * m0[j];
         }
         temp_size = std::max(temp_size, acc);
