@@ -211,27 +211,15 @@ class Engine:
         self.pool = pool = t.zeros(max(sym.pool_size, 1), dtype=t.float64, device=d)
         self.facbuf = fac = t.zeros(max(sym.fac_size, 1), dtype=t.float64, device=d)
         self.boff = sym.boff
-        self._scatter_a()
         self.events = t.zeros(max(sym.n_events, 1) * EVENT_ROW, dtype=t.int64, device=d)
         self.info = t.zeros(max(sym.n_info, 1), dtype=t.int32, device=d)
         ctr = t.zeros(2 * max(sym.n_ctr, 1), dtype=t.int32, device=d)   # {arrivals, release} per panel
         pb, fb = pool.data_ptr(), fac.data_ptr()
         temp = t.empty(max(sym.temp_bound, 1), dtype=t.float64, device=d)
-        if self.nk is not None:
-            # near-kernel coordinates in the cluster-contiguous numbering,
-            # column-major n x k (vector v at nkbuf[v])
-            perm_c = np.concatenate(sym.dofs)
-            self.nkbuf = to_dev(np.ascontiguousarray(self.nk[perm_c].T))
         st = stream()
         gm0, goff = ptr(geo.m0), ptr(geo.off)
         ib, evb = self.info.data_ptr(), self.events.data_ptr()
         import ctypes
-        # block table of the compact Schur segments: {ptr, rc, cc} per block
-        btab = np.stack([pb + 8 * np.asarray(sym.boff, dtype=np.int64),
-                         np.asarray(sym.bi, dtype=np.int64),
-                         np.asarray(sym.bj, dtype=np.int64)], axis=1)
-        self._btab = to_dev_async(np.ascontiguousarray(btab))
-        self._btab_p = ptr(self._btab)
         lib = sym._lib
         vp = sym._vp
         # incremental emission: level l + 1 is planned on the host while the
@@ -258,10 +246,25 @@ class Engine:
             acc["plan"] += time.perf_counter() - tp
             return more, prog_, launches_, used_
 
+        ex = ThreadPoolExecutor(1)
+        # the first level is emitted while A's entries are scattered into the pool
+        fut = ex.submit(produce)
+        self._scatter_a()
+        if self.nk is not None:
+            # near-kernel coordinates in the cluster-contiguous numbering,
+            # column-major n x k (vector v at nkbuf[v])
+            perm_c = np.concatenate(sym.dofs)
+            self.nkbuf = to_dev(np.ascontiguousarray(self.nk[perm_c].T))
+        # block table of the compact Schur segments: {ptr, rc, cc} per block
+        btab = np.stack([pb + 8 * np.asarray(sym.boff, dtype=np.int64),
+                         np.asarray(sym.bi, dtype=np.int64),
+                         np.asarray(sym.bj, dtype=np.int64)], axis=1)
+        self._btab = to_dev_async(np.ascontiguousarray(btab))
+        self._btab_p = ptr(self._btab)
+
         keep = []
         t_launch = 0.0
-        with ThreadPoolExecutor(1) as ex:
-            fut = ex.submit(produce)
+        with ex:
             while True:
                 more, prog, launches, used = fut.result()
                 if more:
