@@ -58,6 +58,10 @@ constexpr int kPBK = 32;         // rows per stage of the cold-column product
 constexpr int kCScr = 0, kCT = 2 * kPBK * (kLDS + 36), kCZ = kCT + 32 * 33, kCR2 = kCZ + 64 * 33,
               kCTail = kCR2 + 64 * 33, kColdEnd = kCTail + 64;
 constexpr size_t kColdSmem = (size_t)kColdEnd * sizeof(double);
+#ifndef SPAND_ROW_UNROLL
+#define SPAND_ROW_UNROLL 1
+#endif
+constexpr int kRowUnroll = SPAND_ROW_UNROLL;   // row loops of the DMMA block updates
 #ifndef SPAND_BLK
 #define SPAND_BLK 32
 #endif
@@ -797,6 +801,7 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
           oka[mi] = c >= 0;
           xa[mi] = W + (int64_t)(c >= 0 ? c : 0) * m;
         }
+        #pragma unroll kRowUnroll
         for (int r = rb; r < re; r += 8) {
           double af[2][2], bf[2][4];
 #pragma unroll
@@ -875,6 +880,7 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
             xc[ni][h] = W + (int64_t)(c >= 0 ? c : 0) * m;
           }
         const int nkq = (nb + 3) >> 2;
+        #pragma unroll kRowUnroll
         for (int r0 = rb; r0 < re; r0 += 8) {
           const int i = r0 + l8;   // this lane's A row and C row
           double af[8];
@@ -990,6 +996,7 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
       for (int a = 0; a < 4; ++a)
 #pragma unroll
         for (int c = 0; c < 4; ++c) acc[a][c][0] = acc[a][c][1] = 0.0;
+      #pragma unroll kRowUnroll
       for (int r = rb; r < re; r += 4) {
         const int i = r + l4;
         double f[4];
@@ -1090,6 +1097,7 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
             oka[mi] = c >= 0;
             xa[mi] = Q + (int64_t)(c >= 0 ? c : 0) * m;
           }
+          #pragma unroll kRowUnroll
           for (int r = rb; r < re; r += 8) {
             double af[2][2], bf[2][4];
 #pragma unroll
@@ -1162,6 +1170,7 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
               xc[ni][h] = Q + (int64_t)(c >= 0 ? c : 0) * m;
             }
           const int nkq = (nb + 3) >> 2;
+          #pragma unroll kRowUnroll
           for (int r0 = rb; r0 < re; r0 += 8) {
             const int i = r0 + l8;
             double af[8];
