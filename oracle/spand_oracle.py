@@ -446,6 +446,7 @@ class _Trailing:
         self.alive = set(self.dofs)
         self.adj = {cid: set() for cid in self.alive}
         self.nk = None          # near-kernel coordinates (extension), n x k
+        self.local_errors = False
         owner = np.full(n, -1, dtype=np.int64)
         slot = np.empty(n, dtype=np.int64)
         for cid, d in self.dofs.items():
@@ -569,6 +570,8 @@ class _Trailing:
                 self.nk[old] = 0.0
                 self.nk[old[m - r:]] = ru
         n_fine = m - res["rank_c"]
+        if self.local_errors:
+            res["local_error"] = local_error(panel, res, scheme)
         ops = [Op("Q", old, q=np.hstack([res["q_f"], res["q_c"]]))]
         ops[0].pivots = res["pivots"][:res["k_stop"]]   # test-side metadata
         ops[0].k_c = res["rank_c"]
@@ -610,8 +613,23 @@ class _Trailing:
         return op, dofs
 
 
+def local_error(panel, res, scheme):
+    """Spectral norm of the dropped term (schemes.py:297-306, 321-340):
+    first order ||Q_f^T W||, full second order ||E||^2, superfine
+    max(||E||^2, ||Q_f1^T W||) with Q_f1 = Q_f[:, rank_f2:]."""
+    def spec(a):
+        return 0.0 if min(a.shape) == 0 else float(np.linalg.norm(a, 2))
+    if scheme == FIRST:
+        return spec(res["q_f"].T @ panel) if res["q_f"].size else 0.0
+    if scheme == FULL:
+        return spec(res["e_tilde"]) ** 2
+    q_f1 = res["q_f"][:, res["rank_f2"]:]
+    e1 = spec(q_f1.T @ panel) if q_f1.size else 0.0
+    return max(spec(res["e_tilde"]) ** 2, e1)
+
+
 def factorize(n, row_ptr, col_idx, values, clusters, levels, eps, scheme,
-              skip_levels=4, near_kernel=None):
+              skip_levels=4, near_kernel=None, collect_local_errors=False):
     """Level loop L..1 (factorize.py:285-366).  ``clusters`` is the
     [(id, dofs, depth)] list of ``nd_hierarchy``.  ``near_kernel`` (n or
     n x k, EXTENSION) switches on ``sparsify_panel_nk``."""
@@ -623,6 +641,8 @@ def factorize(n, row_ptr, col_idx, values, clusters, levels, eps, scheme,
         raise ValueError("skip_levels must be nonnegative")
     st = _Trailing(n, np.asarray(row_ptr), np.asarray(col_idx),
                    np.asarray(values, dtype=np.float64), clusters)
+    st.local_errors = bool(collect_local_errors)
+    lerr = []
     if near_kernel is not None:
         nk = np.array(near_kernel, dtype=np.float64, copy=True)
         nk = nk.reshape(n, -1)
@@ -650,6 +670,8 @@ def factorize(n, row_ptr, col_idx, values, clusters, levels, eps, scheme,
                     perm_parts.append(fine)
                 faces.append([int(cid), int(before), int(res["rank_c"]),
                               int(res["rank_f2"])])
+                if collect_local_errors:
+                    lerr.append(res["local_error"])
         diag.append({"level": level, "interior_clusters": len(inner),
                      "interior_dofs": int(ndofs), "skipped": bool(skipped),
                      "interfaces": faces})
@@ -659,8 +681,10 @@ def factorize(n, row_ptr, col_idx, values, clusters, levels, eps, scheme,
         perm_parts.append(last_dofs)
     perm = (np.concatenate(perm_parts) if perm_parts
             else np.empty(0, np.int64))
-    return Factor(ops, perm, n, {"levels": diag,
-                                 "final_block": int(last_dofs.size)})
+    out = {"levels": diag, "final_block": int(last_dofs.size)}
+    if collect_local_errors:
+        out["local_errors"] = lerr
+    return Factor(ops, perm, n, out)
 
 
 # ---------------------------------------------------------------------------

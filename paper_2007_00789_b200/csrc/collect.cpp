@@ -38,6 +38,8 @@ struct Collected {
   std::vector<int64_t> diag;   // 10 per sparsified interface
   std::vector<int64_t> lsum;   // 4 per level: level, n_interiors, interior dofs, skipped
   std::vector<int64_t> views;  // 4 per payload window: base(0 pool,1 fac) | off, ld, rows, cols
+  std::vector<int64_t> fine;   // 8 per (interface, neighbour): the fine rows Q_f^T W
+                               // {diag row, w, pool off, ld, rows, cols, trans, 0}
   int64_t final_total = 0;
   // apply
   std::vector<std::vector<Task>> fph, bph;
@@ -183,6 +185,22 @@ void* spand_collect_create(void* plan, const int64_t* events, int scheme) {
         C->ops.insert(C->ops.end(), {3, p, li, wv, off[p], ncorr, 0, 0, 0, 0, -1, 0, sb, se, 0, 0});
       }
       for (int64_t i = 0; i < n_fine; ++i) C->perm.push_back(pv.dofs[pv.dptr[p] + off[p] + i]);
+      // fine rows of every neighbour block (all schemes; filled by the RRQR
+      // only for the correction rows unless local errors are requested)
+      if (n_fine) {
+        const int64_t drow = (int64_t)C->diag.size() / 10;
+        for (int w : L.anbrs[k]) {
+          const int64_t lw = live(w);
+          if (lw == 0) continue;
+          if (w > p) {
+            const int64_t a = pv.boff[pv.block(p, w)] + off[p] + off[w] * pv.m0[p];
+            C->fine.insert(C->fine.end(), {drow, w, a, pv.m0[p], n_fine, lw, 0, 0});
+          } else {
+            const int64_t a = pv.boff[pv.block(w, p)] + off[w] + off[p] * pv.m0[w];
+            C->fine.insert(C->fine.end(), {drow, w, a, pv.m0[w], lw, n_fine, 1, 0});
+          }
+        }
+      }
       C->diag.insert(C->diag.end(), {li, p, mp, k_c, rf2, e[7], e[8], k_stop, e[2], 0});
       off[p] += n_fine;
     }
@@ -223,7 +241,7 @@ void* spand_collect_create(void* plan, const int64_t* events, int scheme) {
 
 void spand_collect_destroy(void* h) { delete static_cast<Collected*>(h); }
 
-// out[8]: nops, nsegs, nperm, ndiag, nlsum, nviews, final_total, 0
+// out[8]: nops, nsegs, nperm, ndiag, nlsum, nviews, final_total, nfine
 int spand_collect_sizes(void* h, int64_t* out) {
   Collected* C = static_cast<Collected*>(h);
   out[0] = (int64_t)C->ops.size() / 16;
@@ -233,7 +251,14 @@ int spand_collect_sizes(void* h, int64_t* out) {
   out[4] = (int64_t)C->lsum.size() / 4;
   out[5] = (int64_t)C->views.size() / 4;
   out[6] = C->final_total;
-  out[7] = 0;
+  out[7] = (int64_t)C->fine.size() / 8;
+  return 0;
+}
+
+// fine-row views of the sparsified interfaces (8 int64 each, see Collected)
+int spand_collect_fine(void* h, int64_t* out) {
+  Collected* C = static_cast<Collected*>(h);
+  if (!C->fine.empty()) std::memcpy(out, C->fine.data(), C->fine.size() * sizeof(int64_t));
   return 0;
 }
 

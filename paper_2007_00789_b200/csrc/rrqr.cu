@@ -478,8 +478,13 @@ __device__ void qform_batched(double* Q, const double* V, const double* taus, in
 
 __global__ void __launch_bounds__(kT, 2)
 rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* __restrict__ nbrs,
-                 int32_t* __restrict__ m0, int32_t* __restrict__ off, double eps, int scheme,
+                 int32_t* __restrict__ m0, int32_t* __restrict__ off, double eps, int scheme_flags,
                  int64_t* __restrict__ events) {
+  // scheme_flags: scheme (0 first, 1 second-full, 2 superfine) | 4: keep every
+  // fine row of Q^T W in the dead slots (local-error diagnostics,
+  // schemes.py:297-306), not only the correction rows
+  const int scheme = scheme_flags & 3;
+  const bool keep_fine = (scheme_flags & 4) != 0;
   extern __shared__ double vsh[];
   __shared__ Sh sh;
   // gather / write-back staging aliases the reflector buffer (disjoint phases)
@@ -1596,7 +1601,7 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
   const int k_c = sh.nfrz_tmp;
   const int n_fine = m - k_c;
   int n_corr = 0;  // rows of e_tilde kept in the dead slots
-  if (scheme == 1) n_corr = n_fine;
+  if (scheme == 1 || keep_fine) n_corr = n_fine;
   else if (scheme == 2) n_corr = k_stop - k_c;
   // ---- frozen columns: R rows t < k_c + n_corr of Q^T a (a = original
   // column, restored in W) on the tensor cores (DMMA), written straight to

@@ -186,9 +186,11 @@ class NativePlan:
 
 
 class Engine:
-    def __init__(self, a, h, eps, scheme, skip_levels, near_kernel=None):
+    def __init__(self, a, h, eps, scheme, skip_levels, near_kernel=None,
+                 collect_local_errors=False):
         self.t = require_cuda()
         self.a, self.h = a, h
+        self.local_errors = bool(collect_local_errors)
         self.eps, self.scheme, self.skip = eps, scheme, skip_levels
         self.nk = near_kernel      # n x k host array (extension) or None
         self.sym = NativePlan(a, h, skip_levels,
@@ -310,7 +312,8 @@ class Engine:
                     e1 = t.cuda.Event(enable_timing=True)
                     e0.record()
                 _lib.call("spand_rrqr_wave", cnt, x0, x1, P(ao), P(bo), gm0, goff,
-                          float(self.eps), SCHEME_CODE[self.scheme],
+                          float(self.eps),
+                          SCHEME_CODE[self.scheme] | (4 if self.local_errors else 0),
                           ctypes.c_void_p(evb), st)
                 if WAVE_LOG is not None:
                     e1.record()
@@ -402,12 +405,18 @@ class Engine:
         dv = col.diag.copy()
         etas = dv[:, 5].view(np.float64).tolist()
         r11s = dv[:, 6].view(np.float64).tolist()
+        entries = []
         for q, d in enumerate(col.diag.tolist()):
             li, p, mp, kc, rf2, eb, rb, ks, nc, _ = d
-            by_level.setdefault(li, []).append({
+            entries.append({
                 "cluster": p, "size_before": mp, "size_after": kc, "rank_f2": rf2,
                 "eta_stop": etas[q], "r11": r11s[q], "k_stop": ks,
                 "n_cols": nc})
+            by_level.setdefault(li, []).append(entries[-1])
+        if self.local_errors:
+            errs = self._local_errors(col)
+            for q, ent in enumerate(entries):
+                ent["local_error"] = errs[q]
         for li, (lvl, nint, ndofs, skipped) in enumerate(col.lsum.tolist()):
             faces = by_level.get(li, [])
             digest = hashlib.sha256(repr([(f["cluster"], f["size_before"],
@@ -416,12 +425,57 @@ class Engine:
             diags.append({"level": lvl, "interior_clusters": nint,
                           "interior_dofs": ndofs, "skipped": bool(skipped),
                           "interfaces": [{k: f[k] for k in ("cluster", "size_before",
-                                                            "size_after", "rank_f2")}
+                                                            "size_after", "rank_f2",
+                                                            "local_error") if k in f}
                                          for f in faces],
                           "margins": faces, "digest": digest})
         nnz = self._count(col.views)
         self.timings["collect_s"] = time.perf_counter() - t0
         return ops, col.perm, {"levels": diags, "final_block": col.final_total}, nnz
+
+    def _local_errors(self, col):
+        """Spectral norm of the dropped term of every sparsification
+        (reference `local_error`, schemes.py:321-340, from the norms of
+        schemes.py:297-306): first order ||Q_f^T W||, full second order
+        ||E||^2, superfine max(||E||^2, ||Q_f1^T W||).  The fine rows Q_f^T W
+        are kept in the dead slots by the RRQR (flag 4); the norm is
+        sqrt(lambda_max(F F^T)) on the device (diagnostics only)."""
+        import ctypes
+        t = self.t
+        nd = col.diag.shape[0]
+        out = [0.0] * nd
+        if col.nfine == 0:
+            return out
+        fine = np.zeros((col.nfine, 8), dtype=np.int64)
+        col.lib.spand_collect_fine.argtypes = [ctypes.c_void_p, ctypes.c_void_p]
+        col.lib.spand_collect_fine(col.h, col.vp(fine))
+        pool = self.pool
+        code = SCHEME_CODE[self.scheme]
+        starts = np.flatnonzero(np.r_[True, fine[1:, 0] != fine[:-1, 0]])
+        ends = np.r_[starts[1:], fine.shape[0]]
+        for s0, s1 in zip(starts, ends):
+            q = int(fine[s0, 0])
+            parts = []
+            for _, _, off, ld, r, c, tr, _ in fine[s0:s1].tolist():
+                # F is n_fine x (neighbour columns); a transposed block (w, p)
+                # holds F's columns as rows of w
+                parts.append(pool.as_strided((c, r), (ld, 1), off) if tr
+                             else pool.as_strided((r, c), (1, ld), off))
+            f = t.cat(parts, dim=1)
+            rf2 = int(col.diag[q, 4])
+
+            def spec(m):
+                if m.shape[0] == 0 or m.shape[1] == 0:
+                    return 0.0
+                g = m @ m.t() if m.shape[0] <= m.shape[1] else m.t() @ m
+                return float(t.linalg.eigvalsh(g)[-1].clamp_min(0).sqrt().item())
+            if code == 0:
+                out[q] = spec(f)
+            elif code == 1:
+                out[q] = spec(f) ** 2
+            else:
+                out[q] = max(spec(f[:rf2]) ** 2, spec(f[rf2:]))
+        return out
 
     def _count(self, views):
         """nnz_factor: nonzeros of every payload window, counted on the device."""
@@ -525,7 +579,8 @@ class Collected:
         self.lib, self.h, self.vp = lib, h, vp
         sz = np.zeros(8, dtype=np.int64)
         lib.spand_collect_sizes(h, vp(sz))
-        nops, nsegs, nperm, ndiag, nlsum, nviews, self.final_total, _ = (int(x) for x in sz)
+        nops, nsegs, nperm, ndiag, nlsum, nviews, self.final_total, self.nfine = \
+            (int(x) for x in sz)
         self.ops = np.zeros((nops, 16), dtype=np.int64)
         self.segs = np.zeros((nsegs, 8), dtype=np.int64)
         self.perm = np.zeros(nperm, dtype=np.int64)
@@ -552,7 +607,7 @@ def run_factorization(a, h, eps, scheme, skip_levels, collect_local_errors=False
                       near_kernel=None):
     from .factorize import Factorization
     t0 = time.perf_counter()
-    eng = Engine(a, h, eps, scheme, skip_levels, near_kernel)
+    eng = Engine(a, h, eps, scheme, skip_levels, near_kernel, collect_local_errors)
     eng.run()
     ops, perm, diag, nnz = eng.collect()
     eng.timings["total_s"] = time.perf_counter() - t0

@@ -206,9 +206,29 @@ def c5(ne):
              store_ops=(a.n <= 40000), hierarchy=h)
 
 
+def local_errors():
+    """Per-interface local errors (collect_local_errors=True,
+    factorize.py:338-339) of small cases, all schemes."""
+    out = {}
+    for d, lv, eps, skip in [(16, 4, 0.1, 0), (32, 5, 0.05, 1)]:
+        a = gen.laplacian_2d(d)
+        ra = to_ref(a)
+        h = spdkit.build_hierarchy(ra, lv)
+        for s in ["first", "second-full", "second-superfine"]:
+            f = spdkit.factorize(ra, h, eps, s, skip_levels=skip, collect_local_errors=True)
+            out[f"lap2d_d{d}_L{lv}_e{eps:g}_k{skip}_{s}"] = [
+                [e["cluster"], e["local_error"]] for lvd in f.diagnostics["levels"]
+                for e in lvd["interfaces"]]
+    with open(os.path.join(HERE, "local_errors.json"), "w") as fh:
+        json.dump(out, fh, indent=1)
+    print({k: len(v) for k, v in out.items()})
+
+
 if __name__ == "__main__":
     if sys.argv[1] == "small":
         small()
+    elif sys.argv[1] == "local_errors":
+        local_errors()
     elif sys.argv[1] == "c5":
         c5(int(sys.argv[2]))
     else:
