@@ -41,7 +41,14 @@ from .factorize import (
 )
 from .krylov import SolveReport, cg_bound_rate, default_maxit, pcg
 from .partition import Cluster, PartitionHierarchy, build_hierarchy, default_levels
-from .schemes import OpKind
+from .schemes import (
+    OpKind,
+    SparsificationResult,
+    local_error,
+    make_elimination,
+    make_scaling,
+    make_sparsification,
+)
 from .sparse import (
     SparseSymMatrix,
     baseline_problem,

@@ -9,6 +9,7 @@ preconditioner never touches the host copies; it runs the batched apply
 plan of ``apply.py`` on the device.
 """
 
+from dataclasses import dataclass, field
 from enum import Enum
 
 import numpy as np
@@ -244,3 +245,126 @@ class ErrorCorrection(BlockOperator):
         if self._e is not None:
             return int(sum(v.count_nonzero() for v, _ in self.e_views))
         return int(np.count_nonzero(self._e_host))
+
+
+# ---------------------------------------------------------------------------
+# single-block constructors (reference schemes.py:199-340), on the device
+# kernels through dense.py; the factorization itself batches these steps
+# (engine.py), these are the per-block API of the reference.
+
+
+def make_elimination(a_ss, a_ws, s_dofs=None, w_dofs=None):
+    """Eliminate an interior block by one step of block Cholesky (reference
+    `schemes.py:199-221`): returns (Elimination, Schur update panel panel^T)."""
+    from . import kernels
+    from .dense import cholesky, tri_solve
+    a_ss = np.asarray(a_ss, dtype=np.float64)
+    a_ws = np.asarray(a_ws, dtype=np.float64)
+    ns, nw = a_ss.shape[0], a_ws.shape[0]
+    s_dofs = np.arange(ns) if s_dofs is None else s_dofs
+    w_dofs = ns + np.arange(nw) if w_dofs is None else w_dofs
+    lower = cholesky(a_ss)
+    if nw:
+        panel = tri_solve(lower, a_ws, trans=True, side="right")
+        update = kernels.gemm_one(panel, panel, trans_b=True)
+    else:
+        panel = np.zeros((0, ns))
+        update = np.zeros((0, 0))
+    return Elimination(s_dofs, w_dofs, lower, panel), update
+
+
+def make_scaling(a_pp, a_pw, p_dofs=None):
+    """Rescale an interface block to the identity (reference
+    `schemes.py:224-236`): returns (Scaling, Z^-1 A_pw)."""
+    from .dense import cholesky, tri_solve
+    a_pp = np.asarray(a_pp, dtype=np.float64)
+    a_pw = np.asarray(a_pw, dtype=np.float64)
+    p_dofs = np.arange(a_pp.shape[0]) if p_dofs is None else p_dofs
+    lower = cholesky(a_pp)
+    panel = tri_solve(lower, a_pw) if a_pw.size else np.zeros(a_pw.shape)
+    return Scaling(p_dofs, lower), panel
+
+
+def _spectral(a):
+    """Largest singular value on the device (sqrt of the top eigenvalue of
+    the smaller Gram matrix)."""
+    from .device import require_cuda, dev
+    if min(a.shape) == 0:
+        return 0.0
+    t = require_cuda()
+    m = t.as_tensor(np.ascontiguousarray(a), dtype=t.float64, device=dev())
+    g = m @ m.t() if m.shape[0] <= m.shape[1] else m.t() @ m
+    return float(t.linalg.eigvalsh(g)[-1].clamp_min(0).sqrt().item())
+
+
+@dataclass(frozen=True)
+class SparsificationResult:
+    """Operators and bookkeeping of one sparsification (reference
+    `schemes.py:245-269`)."""
+
+    orthogonal: "Orthogonal"
+    correction: "ErrorCorrection | None"
+    coarse_rows: np.ndarray
+    n_fine: int
+    rank_c: int
+    rank_f2: int
+    scheme: object
+    e_norm: float | None = field(default=None)
+    e1_norm: float | None = field(default=None)
+    e2_norm: float | None = field(default=None)
+
+
+def make_sparsification(panel, eps, scheme, p_dofs=None, w_dofs=None,
+                        keep_error_info=True):
+    """Compress one rescaled interface panel (reference `schemes.py:272-318`)
+    with the device RRQR; dropped-term norms on request."""
+    from .dense import SchemeKind, rrqr_sparsify
+    if isinstance(scheme, str):
+        scheme = SchemeKind.from_string(scheme)
+    panel = np.asarray(panel, dtype=np.float64)
+    m, nw = panel.shape
+    p_dofs = np.arange(m) if p_dofs is None else np.asarray(p_dofs)
+    w_dofs = m + np.arange(nw) if w_dofs is None else w_dofs
+    res = rrqr_sparsify(panel, eps, scheme)
+    n_fine = m - res.rank_c
+    orthogonal = Orthogonal(p_dofs, np.hstack([res.q_f, res.q_c]))
+    n_corr = res.e_tilde.shape[0]
+    correction = None
+    if n_corr and res.e_tilde.size:
+        correction = ErrorCorrection(p_dofs[:n_corr], w_dofs, res.e_tilde)
+    e_norm = e1_norm = e2_norm = None
+    if keep_error_info:
+        from . import kernels
+        if scheme is SchemeKind.SECOND_ORDER_SUPERFINE:
+            e2_norm = _spectral(res.e_tilde)
+            q_f1 = res.q_f[:, res.rank_f2:]
+            e1_norm = (_spectral(kernels.gemm_one(q_f1, panel, trans_a=True))
+                       if q_f1.size else 0.0)
+        elif scheme is SchemeKind.SECOND_ORDER_FULL:
+            e_norm = _spectral(res.e_tilde)
+        else:
+            e_norm = (_spectral(kernels.gemm_one(res.q_f, panel, trans_a=True))
+                      if res.q_f.size else 0.0)
+    return SparsificationResult(orthogonal, correction, res.r_coarse, n_fine, res.rank_c,
+                                res.rank_f2, scheme, e_norm, e1_norm, e2_norm)
+
+
+def local_error(scheme, result):
+    """Spectral norm of the exactly dropped term (reference
+    `schemes.py:321-340`)."""
+    from .dense import SchemeKind
+    if isinstance(scheme, str):
+        scheme = SchemeKind.from_string(scheme)
+    if scheme is SchemeKind.FIRST_ORDER:
+        if result.e_norm is None:
+            raise ValueError("sparsification ran without error info")
+        return result.e_norm
+    if scheme is SchemeKind.SECOND_ORDER_FULL:
+        if result.e_norm is None:
+            raise ValueError("sparsification ran without error info")
+        return result.e_norm ** 2
+    if scheme is SchemeKind.SECOND_ORDER_SUPERFINE:
+        if result.e1_norm is None or result.e2_norm is None:
+            raise ValueError("sparsification ran without error info")
+        return max(result.e2_norm ** 2, result.e1_norm)
+    raise ValueError(f"unknown scheme {scheme!r}")
