@@ -224,6 +224,12 @@ int spand_nd_partition(int64_t n, const int64_t* row_ptr, const int64_t* col_idx
                        int levels, int64_t* dofs_out, int64_t* cptr_out,
                        int32_t* depth_out, int64_t* ncl_out);
 
+/* Symmetric CSR input validation (sparse.py:40-58), host memory: 0 ok,
+ * 1 column out of range, 2 columns not increasing, 3 not symmetric,
+ * 4 missing / nonpositive diagonal (first failing property). */
+int spand_csr_check(int64_t n, const int64_t* row_ptr, const int64_t* col_idx,
+                    const double* values);
+
 /* ---- native level scheduler (planner.cpp) and collector (collect.cpp) ----
  * Host-side runtime of the factorization: symbolic structure, the launch
  * program, and after the run the operator tables / permutation /

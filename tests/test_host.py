@@ -53,7 +53,7 @@ def test_header_symbols_are_typed_or_handle_based():
     bound with explicit argtypes where it is used (handle-returning ones)."""
     handle_based = {"spand_plan_create", "spand_plan_destroy", "spand_plan_set_dofs",
                     "spand_plan_emit_begin", "spand_plan_emit_next", "spand_plan_chunk",
-                    "spand_plan_pairs", "spand_plan_scatter",
+                    "spand_plan_pairs", "spand_plan_scatter", "spand_csr_check",
                     "spand_collect_create", "spand_collect_destroy", "spand_collect_sizes",
                     "spand_collect_get", "spand_collect_apply", "spand_collect_apply_get",
                     "spand_collect_fine"}
@@ -257,3 +257,25 @@ def test_native_scatter_positions(tag):
     cof = np.ascontiguousarray(cl, dtype=np.int64)
     assert lib.spand_plan_scatter(plan.h, vp(rp), vp(cx), vp(cof), vp(got)) == 0
     assert np.array_equal(got, want)
+
+
+def test_sparse_sym_matrix_validation_errors():
+    """The reference constructor's checks (sparse.py:40-58), first failing
+    property reported (native pass per property)."""
+    from paper_2007_00789_b200.errors import AsymmetricValues, NonpositiveDiagonal
+    mk = lambda rp, ci, va: sp.SparseSymMatrix(3, np.array(rp), np.array(ci),  # noqa: E731
+                                                np.array(va, dtype=float))
+    good = mk([0, 2, 4, 5], [0, 1, 0, 1, 2], [2.0, -1.0, -1.0, 2.0, 1.0])
+    assert good.nnz == 5
+    with pytest.raises(ParseError):
+        mk([0, 2, 4, 5], [0, 3, 0, 1, 2], [2.0, -1.0, -1.0, 2.0, 1.0])   # out of range
+    with pytest.raises(ParseError):
+        mk([0, 2, 4, 5], [1, 0, 0, 1, 2], [-1.0, 2.0, -1.0, 2.0, 1.0])   # decreasing
+    with pytest.raises(AsymmetricValues):
+        mk([0, 2, 4, 5], [0, 1, 0, 1, 2], [2.0, -1.0, -0.5, 2.0, 1.0])   # values
+    with pytest.raises(AsymmetricValues):
+        mk([0, 2, 3, 4], [0, 1, 1, 2], [2.0, -1.0, 2.0, 1.0])            # pattern
+    with pytest.raises(NonpositiveDiagonal):
+        mk([0, 2, 4, 5], [0, 1, 0, 1, 2], [2.0, -1.0, -1.0, 2.0, -1.0])  # sign
+    with pytest.raises(NonpositiveDiagonal):                           # missing diagonal
+        sp.SparseSymMatrix(2, np.array([0, 1, 2]), np.array([1, 0]), np.array([1.0, 1.0]))
