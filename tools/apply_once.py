@@ -19,7 +19,6 @@ stats = []
 for r in ph.tolist():
     to, nt, io, ni, co, nch, cbo, grid, _, used = r
     tr = img[to:to + 8 * nt].reshape(-1, 8)
-    it = img[io:io + 8 * ni].reshape(-1, 8)
     stats.append({"ntask": nt, "nitem": ni, "grid": grid, "nchunk": nch,
                   "MB": float((tr[:, 2] * tr[:, 3]).sum()) * 8 / 1e6,
                   "trans_frac": float(tr[:, 4].mean()),
