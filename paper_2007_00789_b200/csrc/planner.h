@@ -435,6 +435,52 @@ struct Plan {
     if (!dry) launches[launches.size() - 6] = compact;   // field 10
   }
 
+  // Flat GEMM target list, written in place (the per-level hot paths: the
+  // panel TRSMs and the grouped Schur updates emit ~10^5 targets each on the
+  // leaf levels; no intermediate Target objects)
+  struct FlatGemm {
+    std::vector<int64_t> trow, srow, tiles;
+    int64_t nseg = 0, sw = 14, ntarget = 0;
+    bool lower = false;
+    void reserve(size_t nt, size_t nsegs) {
+      trow.reserve(8 * nt + 8);
+      srow.reserve(sw * nsegs + 14);
+      tiles.reserve(nt + 16);
+    }
+    // begin a target: C operand (7 values), extents for the tile grid
+    template <class... A>
+    void target(int64_t mm, int64_t nn, bool dry, A... c) {
+      const int64_t e[7] = {c...};
+      trow.insert(trow.end(), e, e + 7);
+      trow.push_back(nseg);
+      if (!dry)
+        for (int64_t i = 0; i < mm; i += kTile)
+          for (int64_t j = 0; j < nn; j += kTile) {
+            if (lower && j > i) continue;
+            tiles.push_back((ntarget << 32) | ((i / kTile) << 16) | (j / kTile));
+          }
+      ++ntarget;
+    }
+    void seg(int64_t s) {
+      srow.push_back(s);
+      if (sw == 1) ++nseg;
+    }
+    void seg_opnds(const int64_t* a, const int64_t* b) {
+      srow.insert(srow.end(), a, a + 7);
+      srow.insert(srow.end(), b, b + 7);
+      ++nseg;
+    }
+  };
+  void gemm_flat(FlatGemm& g, double alpha, double beta, int bT, int tri = 0) {
+    if (g.ntarget == 0) return;
+    g.trow.insert(g.trow.end(), {0, 0, 0, 0, 0, 0, 0, g.nseg});
+    if (dry || g.tiles.empty()) return;
+    if (g.srow.empty()) g.srow.assign(14, 0);
+    const int64_t a = push(g.tiles), b = push(g.trow), c = push(g.srow);
+    launch(3, (int64_t)g.tiles.size(), a, b, c, bT, g.lower ? 1 : 0, tri, alpha, beta);
+    launches[launches.size() - 6] = g.sw == 1 ? 1 : 0;   // field 10: compact
+  }
+
   // batched triangular inverses: 64-tiles + recursive doubling GEMMs
   void trtri(const std::vector<std::vector<int64_t>>& Ls, const std::vector<std::vector<int64_t>>& Xs,
              const std::vector<int64_t>& sizes, int64_t temp_at) {
@@ -635,48 +681,46 @@ struct Plan {
         }
         trtri(Ls, Xs, sz, 0);
         // panel TRSM as a product with the explicit inverse, into temp, copied back
-        std::vector<Target> tg;
+        FlatGemm tg;
         std::vector<int64_t> cps;
         int64_t acc = 0;
-        tg.reserve(L.inb_blk.size());
+        tg.reserve(L.inb_blk.size(), L.inb_blk.size());
         cps.reserve(15 * L.inb_blk.size());
         for (size_t k = 0; k < L.interiors.size(); ++k) {
           const int s = L.interiors[k];
+          const int64_t linv_s = fac_base + 8 * elim_linv[s];
           for (size_t u = 0; u < L.inbrs[k].size(); ++u) {
             const int w = L.inbrs[k][u];
             const int64_t pws = pool_base + 8 * boff[L.inb_blk[L.inb_ptr[k] + u]];
-            Target t;
-            opnd(t.c, temp_base + 8 * acc, w, s);
-            opnd(t.segs, pws, w, s);
-            opnd(t.segs, fac_base + 8 * elim_linv[s], s, s);
-            t.mm = m0[w];
-            t.nn = m0[s];
-            tg.push_back(std::move(t));
-            opnd(cps, temp_base + 8 * acc, w, s);
-            opnd(cps, pws, w, s);
-            cps.push_back(0);
+            const int64_t tmp = temp_base + 8 * acc;
+            tg.target(m0[w], m0[s], dry, tmp, (int64_t)w, (int64_t)s, (int64_t)0, (int64_t)0,
+                      (int64_t)-1, (int64_t)-1);
+            const int64_t oa[7] = {pws, w, s, 0, 0, -1, -1};
+            const int64_t ob[7] = {linv_s, s, s, 0, 0, -1, -1};
+            tg.seg_opnds(oa, ob);
+            cps.insert(cps.end(), {tmp, w, s, 0, 0, -1, -1, pws, w, s, 0, 0, -1, -1, 0});
             acc += m0[w] * m0[s];
           }
         }
         temp_size = std::max(temp_size, acc);
-        gemm(tg, 1.0, 0.0, 1, 0, 2);    // panel L_s^-T
+        gemm_flat(tg, 1.0, 0.0, 1, 2);    // panel L_s^-T
         if (!cps.empty()) launch(4, (int64_t)cps.size() / 15, push(cps));
         // grouped Schur / fill update: off-diagonal targets, then diagonal
         // ones (lower tiles only: potrf reads the lower triangle)
         for (int diag = 0; diag < 2; ++diag) {
-          std::vector<Target> st;
+          FlatGemm st;
+          st.sw = 1;
+          st.lower = diag == 1;
+          st.reserve(L.targets.size(), L.tseg_idx.size());
           for (size_t t = 0; t < L.targets.size(); ++t) {
             const int b = L.targets[t];
             const int wa = bi[b], wb = bj[b];
             if ((wa == wb) != (diag == 1)) continue;
-            Target x;
-            opnd(x.c, pool_base + 8 * boff[b], wa, wb);
-            for (int q = L.tseg_ptr[t]; q < L.tseg_ptr[t + 1]; ++q) x.segs.push_back(L.tseg_blk[q]);
-            x.mm = m0[wa];
-            x.nn = m0[wb];
-            st.push_back(std::move(x));
+            st.target(m0[wa], m0[wb], dry, pool_base + 8 * boff[b], (int64_t)wa, (int64_t)wb,
+                      (int64_t)0, (int64_t)0, (int64_t)-1, (int64_t)-1);
+            for (int q = L.tseg_ptr[t]; q < L.tseg_ptr[t + 1]; ++q) st.seg(L.tseg_blk[q]);
           }
-          gemm(st, -1.0, 1.0, 1, diag, 0, 1);
+          gemm_flat(st, -1.0, 1.0, 1);
         }
       }
       if (L.skipped) return;
