@@ -1810,8 +1810,20 @@ int spand_rrqr_cta_count(void) {
 }
 
 int spand_rrqr_capacity(int vmax) {
+  // the occupancy only depends on the dynamic shared memory size; cache it
+  // per (device, size) -- the planner asks once per sparsification wave
+  static int cached_dev = -1, cached_per = -1;
+  static size_t cached_smem = 0;
   int dev = 0, sms = 0, per = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return -1;
+  {
+    size_t smem0 = kColdSmem;
+    if ((size_t)vmax * sizeof(double) > smem0) smem0 = (size_t)vmax * sizeof(double);
+    if (dev == cached_dev && smem0 == cached_smem && cached_per > 0) {
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      return cached_per * sms;
+    }
+  }
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   size_t smem = kColdSmem;
   if ((size_t)vmax * sizeof(double) > smem) smem = (size_t)vmax * sizeof(double);
@@ -1819,6 +1831,9 @@ int spand_rrqr_capacity(int vmax) {
                        (int)(kMaxM * sizeof(double) > kColdSmem ? kMaxM * sizeof(double) : kColdSmem));
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, rrqr_wave_kernel, kT, smem) != cudaSuccess)
     return -1;
+  cached_dev = dev;
+  cached_smem = smem;
+  cached_per = per;
   return per * sms;
 }
 

@@ -243,6 +243,18 @@ class FastPlan:
 
 
 _COMPILER = ThreadPoolExecutor(1, thread_name_prefix="spand-apply-image")
+_PINNED = [None]
+
+
+def _pinned_image(n):
+    """Grow-only pinned int64 buffer for the apply images (compile thread)."""
+    t = require_cuda()
+    buf = _PINNED[0]
+    if buf is None or buf.numel() < n:
+        buf = t.empty(max(n, 2 * (buf.numel() if buf is not None else 0)), dtype=t.int64,
+                      pin_memory=True)
+        _PINNED[0] = buf
+    return buf[:n]
 
 
 class NativeApplyPlan(FastPlan):
@@ -287,11 +299,15 @@ class NativeApplyPlan(FastPlan):
                                "the packed work-item limits")
         t1 = time.perf_counter()
         ilen, nfw, nbw, scratch_len = (int(x) for x in out)
-        image = np.zeros(max(ilen, 1), dtype=np.int64)
+        # the image is written straight into pinned memory (reused between
+        # factorizations: the previous plan's upload completed before the
+        # next factorization's collect, which synchronises)
+        pinned = _pinned_image(max(ilen, 1))
+        image = pinned.numpy()
         ph = np.zeros((nfw + nbw, 10), dtype=np.int64)
         lib.spand_collect_apply_get.argtypes = [ctypes.c_void_p] * 3
         lib.spand_collect_apply_get(collected.h, vp(image), vp(ph))
-        return image, ph, nfw, scratch_len, (t1 - t0, time.perf_counter() - t1)
+        return pinned, ph, nfw, scratch_len, (t1 - t0, time.perf_counter() - t1)
 
     def __getattr__(self, name):
         if name in NativeApplyPlan._LAZY:
@@ -304,11 +320,13 @@ class NativeApplyPlan(FastPlan):
         if "fwd" in self.__dict__:
             return
         t = require_cuda()
-        image, ph, nfw, scratch_len, (t_setup, t_image) = self._future.result()
+        pinned, ph, nfw, scratch_len, (t_setup, t_image) = self._future.result()
         t0 = time.perf_counter()
         self.scratch_len = scratch_len
-        self.image = to_dev_async(image)
-        self.image_host = image
+        self.image = t.empty(pinned.shape, dtype=t.int64, device=dev())
+        self.image.copy_(pinned, non_blocking=True)
+        image = pinned.numpy()
+        self.image_host = image   # (overwritten by the next factorization's image)
         base = self.image.data_ptr()
         self.scratch = t.empty(max(scratch_len, 1), dtype=t.float64, device=dev())
         rows = []
