@@ -46,6 +46,7 @@ import os as _os
 from collections.abc import Sequence
 
 WAVE_LOG = None      # set to [] to record per-wave CUDA events (profiling)
+PROG_ARENA = None    # pinned staging of the program chunks (emission thread)
 NK_RTOL = 1e-8       # rank threshold of the near-kernel basis (oracle NK_RTOL)
 EVENT_ROW = 12
 MAX_PANEL_ROWS = 6144
@@ -236,18 +237,26 @@ class Engine:
         acc = {"plan": 0.0}
 
         def produce():
+            # the chunk is written straight into pinned memory (PROG_ARENA:
+            # used by this helper thread only, recycled after the run's sync)
             tp = time.perf_counter()
             sizes = np.zeros(3, dtype=np.int64)
             more = lib.spand_plan_emit_next(sym.h, vp(sizes))
             plen, nlau, used_ = (int(x) for x in sizes)
             prog_ = launches_ = None
             if nlau:
-                prog_ = np.empty(max(plen, 1), dtype=np.int64)
+                stage = PROG_ARENA.take(8 * max(plen, 1)).view(t.int64)
+                prog_ = stage.numpy()
                 launches_ = np.empty((nlau, 16), dtype=np.int64)
                 lib.spand_plan_chunk(sym.h, vp(prog_), vp(launches_))
+                prog_ = (prog_, stage)
             acc["plan"] += time.perf_counter() - tp
             return more, prog_, launches_, used_
 
+        global PROG_ARENA
+        if PROG_ARENA is None:
+            from .device import PinnedArena
+            PROG_ARENA = PinnedArena()
         ex = ThreadPoolExecutor(1)
         # the first level is emitted while A's entries are scattered into the pool
         fut = ex.submit(produce)
@@ -273,7 +282,9 @@ class Engine:
                     fut = ex.submit(produce)
                 if launches is not None:
                     tl = time.perf_counter()
-                    progd = to_dev_async(prog)
+                    prog, stage = prog
+                    progd = t.empty(stage.shape, dtype=t.int64, device=d)
+                    progd.copy_(stage, non_blocking=True)
                     keep.append(progd)
                     self._launch(launches, progd.data_ptr(), gm0, goff, ib, evb, fb, st, prog)
                     t_launch += time.perf_counter() - tl
@@ -286,6 +297,7 @@ class Engine:
         self._keep_run = (temp, ctr, keep)
         t.cuda.synchronize()
         ARENA.reset()   # every staged upload has completed
+        PROG_ARENA.reset()
         self.timings["device_s"] = time.perf_counter() - tstart
 
     def _launch(self, launches, base, gm0, goff, ib, evb, fb, st, prog=None):
