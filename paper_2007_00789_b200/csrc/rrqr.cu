@@ -169,7 +169,12 @@ __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_grou
 __device__ __forceinline__ void cp_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::); }
 
 __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+#ifdef SPAND_DMMA_VOLATILE
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+#else
+  // not volatile: the scheduler may hoist the next fragments' loads above it
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+#endif
                : "+d"(d0), "+d"(d1)
                : "d"(a), "d"(b));
 }
