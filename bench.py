@@ -369,6 +369,25 @@ def main():
     else:
         roof = {"kernel": dom[0], "bound": "tensor", "achieved": None, "peak": FP64_PEAK_TFLOPS,
                 "unit": "TFLOP/s", "frac": None, "traffic": None}
+    # latency floor of the RRQR: its critical path is the sum over waves of
+    # the largest k_stop, each step at least one group synchronisation
+    # (tools/rrqr_step_probe.cu: barrier + candidate scan + pivot-column read
+    # with no column work, measured on this GPU model)
+    probe_path = os.path.join(HERE, "profiles", "rrqr_step_probe_r01.jsonl")
+    if dom[0] == "spand_rrqr_wave" and os.path.exists(probe_path):
+        try:
+            pr = [json.loads(l) for l in open(probe_path) if l.strip()]
+            step_us = [p["ns_per_step"] for p in pr if p["G"] == 296][0] / 1000.0
+            steps = f.timings.get("rrqr_critical_steps", 0)
+            floor_ms = steps * step_us / 1000.0
+            roof["latency_bound"] = {
+                "critical_steps": steps, "step_floor_us": step_us, "floor_ms": floor_ms,
+                "frac": floor_ms / roof["ms_per_step"],
+                "basis": "critical path = sum over waves of the largest k_stop; each step "
+                         "needs one 296-CTA group barrier + candidate scan + pivot-column "
+                         "read (profiles/rrqr_step_probe_r01.jsonl)"}
+        except Exception:
+            pass
     prof_path = os.path.join(HERE, "profiles", "ncu_r01_summary.json")
     if os.path.exists(prof_path):
         try:

@@ -264,6 +264,7 @@ int spand_collect_sizes(void* h, int64_t* out);
 int spand_collect_get(void* h, int64_t* ops, int64_t* segs, int64_t* perm, int64_t* diag,
                       int64_t* lsum, int64_t* views, int64_t* fidx);
 int spand_collect_fine(void* h, int64_t* out);
+int spand_collect_stats(void* h, int64_t* out);
 int spand_collect_apply(void* h, int64_t pool_base, int64_t fac_base, int64_t xbuf,
                         int64_t idx_addr, int64_t* out);
 int spand_collect_apply_get(void* h, int64_t* image, int64_t* phases);

@@ -41,6 +41,7 @@ struct Collected {
   std::vector<int64_t> fine;   // 8 per (interface, neighbour): the fine rows Q_f^T W
                                // {diag row, w, pool off, ld, rows, cols, trans, 0}
   int64_t final_total = 0;
+  int64_t critical_steps = 0;  // sum over waves of the largest k_stop (RRQR critical path)
   // apply
   std::vector<std::vector<Task>> fph, bph;
   std::vector<int64_t> fidx;   // permuted indices of the final block
@@ -141,6 +142,14 @@ void* spand_collect_create(void* plan, const int64_t* events, int scheme) {
       C->views.insert(C->views.end(), {lo | (int64_t(1) << 62), m0p, mp, mp});
       add(C->fph[fb + 2], li2 | (int64_t(1) << 62), m0p, mp, mp, 0, 0, 0, pst(p), pst(p), 0);
       add(C->bph[bb + 2 * nw], li2 | (int64_t(1) << 62), m0p, mp, mp, 0, 1, 0, pst(p), pst(p), 0);
+    }
+    // RRQR critical path: waves run one after the other, panels of a wave
+    // concurrently
+    {
+      std::vector<int64_t> wmax(L.nwaves, 0);
+      for (int k = 0; k < (int)L.active.size(); ++k)
+        wmax[L.wave[k]] = std::max(wmax[L.wave[k]], events[12 * L.slot[k] + 3]);
+      for (int64_t v : wmax) C->critical_steps += v;
     }
     // sparsifications in ascending id order
     for (int k = 0; k < (int)L.active.size(); ++k) {
@@ -252,6 +261,12 @@ int spand_collect_sizes(void* h, int64_t* out) {
   out[5] = (int64_t)C->views.size() / 4;
   out[6] = C->final_total;
   out[7] = (int64_t)C->fine.size() / 8;
+  return 0;
+}
+
+// out[1]: RRQR critical-path steps (sum over waves of the largest k_stop)
+int spand_collect_stats(void* h, int64_t* out) {
+  out[0] = static_cast<Collected*>(h)->critical_steps;
   return 0;
 }
 

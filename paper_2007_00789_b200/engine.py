@@ -405,6 +405,10 @@ class Engine:
                                                       SCHEME_CODE[self.scheme]))
         self.collected = Collected(lib, ch, vp)
         col = self.collected
+        stats = np.zeros(1, dtype=np.int64)
+        lib.spand_collect_stats.argtypes = [ctypes.c_void_p, ctypes.c_void_p]
+        lib.spand_collect_stats(ch, vp(stats))
+        self.timings["rrqr_critical_steps"] = int(stats[0])
         # the apply image compiles on a host thread while the diagnostics and
         # the nonzero count below run (the first apply waits for it)
         from .fastplan import NativeApplyPlan

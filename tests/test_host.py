@@ -56,7 +56,7 @@ def test_header_symbols_are_typed_or_handle_based():
                     "spand_plan_pairs", "spand_plan_scatter", "spand_csr_check",
                     "spand_collect_create", "spand_collect_destroy", "spand_collect_sizes",
                     "spand_collect_get", "spand_collect_apply", "spand_collect_apply_get",
-                    "spand_collect_fine"}
+                    "spand_collect_fine", "spand_collect_stats"}
     for nm in _declared():
         assert nm in _lib.SIGNATURES or nm in handle_based, nm
 
