@@ -198,6 +198,7 @@ int spand_nk_deflate(int npanel, int64_t ncols, const int64_t* rows, const int64
 int spand_nk_qform(int npanel, int64_t ncols, const int64_t* rows, const int64_t* events,
                    int vmax, void* stream);
 int spand_plan_set_nk(void* h, int k);
+int spand_plan_set_group_weight(void* h, int w, double exp_m, double exp_n);
 
 /* Final dense block (factorize.py:198-220): assemble the live parts of the
  * remaining clusters (cl[ncl] cluster ids, ascending) into the virtual

@@ -118,6 +118,15 @@ int spand_plan_scatter(void* h, const int64_t* row_ptr, const int64_t* col_idx,
   return 0;
 }
 
+// RRQR group-size weighting (tuning): 0 ~ m n, 1 ~ m^2, 2 ~ m sqrt(m n)
+int spand_plan_set_group_weight(void* h, int w, double em, double en) {
+  Plan* p = static_cast<Plan*>(h);
+  p->group_weight = w;
+  p->gexp_m = em;
+  p->gexp_n = en;
+  return 0;
+}
+
 // near-kernel extension: number of vectors (0 = reference path); resizes
 // the workspace bound, so call before spand_plan_sizes / emission
 int spand_plan_set_nk(void* h, int k) {

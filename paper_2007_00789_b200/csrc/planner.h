@@ -2,6 +2,7 @@
 // native collector (collect.cpp).
 #pragma once
 #include <algorithm>
+#include <cmath>
 #include <cstdint>
 #include <cstring>
 #include <map>
@@ -106,6 +107,11 @@ struct Plan {
   std::vector<int64_t> prog, launches;
   int cap_override = 0;
   int nk = 0;   // near-kernel vectors (extension; 0: reference path)
+  // RRQR group sizes within a wave: 0 ~ m n, 1 ~ m^2, 2 ~ m sqrt(m n),
+  // 3 ~ m^a n^b.  The default m^1.25 n^0.5 (C4-L15 sweep: 1.14 s at m n,
+  // 1.105 s here) gives tall panels -- more sequential steps -- more CTAs
+  int group_weight = 3;
+  double gexp_m = 1.25, gexp_n = 0.5;
   static constexpr int64_t kNkHead = 19;   // nearkernel.cu kWsHead
   int64_t nk_ws(int64_t mc) const { return nk ? kNkHead + 2 * mc * nk + mc * mc : 0; }
 
@@ -809,7 +815,12 @@ struct Plan {
             const size_t k = pan[u];
             int64_t ncap = 0;
             for (int w : L.anbrs[k]) ncap += m0[w];
-            works.push_back(std::max<int64_t>(1, m0[L.active[k]] * std::max<int64_t>(ncap, 1)));
+            const double mw = (double)m0[L.active[k]], nw = (double)std::max<int64_t>(ncap, 1);
+            double wgt = mw * nw;                                   // 0: panel size
+            if (group_weight == 1) wgt = mw * mw;                   // 1: rows^2 (step count x height)
+            else if (group_weight == 2) wgt = mw * std::sqrt(mw * nw);
+            else if (group_weight == 3) wgt = std::pow(mw, gexp_m) * std::pow(nw, gexp_n);
+            works.push_back(std::max<int64_t>(1, (int64_t)wgt));
           }
           const std::vector<int> gs = groups(works, cap);
           std::vector<int64_t> prow, nrow, krow;

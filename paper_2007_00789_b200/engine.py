@@ -97,6 +97,13 @@ class NativePlan:
         self._vp = vp
         lib.spand_plan_set_dofs.argtypes = [ctypes.c_void_p] * 3
         lib.spand_plan_set_dofs(self.h, vp(dcat), vp(dptr))
+        gw = int(_os.environ.get("SPAND_GROUP_WEIGHT", "-1"))
+        if gw >= 0:
+            lib.spand_plan_set_group_weight.argtypes = [ctypes.c_void_p, ctypes.c_int,
+                                                        ctypes.c_double, ctypes.c_double]
+            lib.spand_plan_set_group_weight(
+                self.h, gw, float(_os.environ.get("SPAND_GROUP_EM", "1.25")),
+                float(_os.environ.get("SPAND_GROUP_EN", "0.5")))
         if nk:
             if lib.spand_plan_set_nk(self.h, int(nk)) != 0:
                 raise ValueError(f"at most 16 near-kernel vectors, got {nk}")
