@@ -1424,15 +1424,26 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
       }
     }
     // ---- Gram column of the block's reflectors for the cold update:
-    // G[q][jb] = V[:, k0 + q] . v_k (q < jb), one dot per CTA
+    // G[q][jb] = V[:, k0 + q] . v_k (q < jb), dots q = rank (mod G).  One dot:
+    // the whole CTA; several (small groups): a warp per dot, no block barriers
     {
       const int jb = k - k0;
-      for (int q = rank; q < jb; q += G) {
-        const double* vq = V + (int64_t)(k0 + q) * m + k;
+      const int nd = rank < jb ? (jb - 1 - rank) / G + 1 : 0;
+      if (nd == 1) {
+        const double* vq = V + (int64_t)(k0 + rank) * m + k;
         double d = 0.0;
         for (int i = tid; i < len; i += kT) d += __ldcg(vq + i) * vsh[i];
         d = block_sum<kT>(d, sh.red);
-        if (tid == 0) Gbuf[q * 32 + jb] = d;
+        if (tid == 0) Gbuf[rank * 32 + jb] = d;
+      } else if (nd > 1) {
+        for (int u = warp; u < nd; u += kWarps) {
+          const int q = rank + G * u;
+          const double* vq = V + (int64_t)(k0 + q) * m + k;
+          double d = 0.0;
+          for (int i = lane; i < len; i += 32) d += __ldcg(vq + i) * vsh[i];
+          d = warp_sum(d);
+          if (lane == 0) Gbuf[q * 32 + jb] = d;
+        }
       }
     }
     // ---- owned active columns: a -= tau (v.a) v, row-k entry, norm
