@@ -6,14 +6,18 @@
 // (as products with explicit triangular inverses) and the trailing updates
 // of the blocked factorizations.
 //
-// CTA tile 64x64, 4 warps (2x2) of 32x32, K staged 16 at a time through a
+// CTA tile BM x BN, 4 warps of WM x WN, K staged 16 at a time through a
 // 2-deep cp.async shared-memory pipeline; live sizes come from the device
-// geometry so tiles past a block's live extent exit at once.
+// geometry so tiles past a block's live extent exit at once.  Tile shapes
+// (tri >> 4): 0 64x64 (the default), 1 64x16, 2 32x32, 3 16x16, 4 16x64,
+// 5 64x32, 6 32x64 --
+// the leaf levels' targets are a few rows or columns wide, and a 64x64 tile
+// on a 6-column target spends 90 % of its tensor work on padding.
 #include "common.cuh"
 #include "../../include/spand_b200.h"
 
 namespace {
-constexpr int BM = 64, BN = 64, BK = 16, LDS = 68;  // LDS padding: conflict-free frags
+constexpr int BK = 16;
 constexpr int kThreads = 128;
 
 __device__ __forceinline__ void cp_async8(double* smem, const double* gmem, bool pred) {
@@ -34,30 +38,34 @@ struct SegIter {
   int seg, seg_end, k0;
 };
 
+template <int BM, int BN, int WM, int WN>
 __global__ void __launch_bounds__(kThreads)
 gemm_grouped_kernel(const int64_t* __restrict__ tiles, const int64_t* __restrict__ targets,
                     const int64_t* __restrict__ segs, const int32_t* __restrict__ m0,
                     const int32_t* __restrict__ off, double alpha, double beta, int bT,
                     int lower_only, int tri, const int64_t* __restrict__ btab, int compact) {
-  __shared__ __align__(16) double As[2][BK][LDS];
-  __shared__ __align__(16) double Bs[2][BK][LDS];
-  // packed tile: target << 32 | (i0 / 64) << 16 | (j0 / 64)
+  static_assert((BM / WM) * (BN / WN) == kThreads / 32, "4 warps per tile");
+  constexpr int FM = WM / 8, FN = WN / 8;              // 8x8 fragments per warp
+  constexpr int LDA = BM + 4, LDB = BN + 4;            // padding: conflict-free frags
+  __shared__ __align__(16) double As[2][BK][LDA];
+  __shared__ __align__(16) double Bs[2][BK][LDB];
+  // packed tile: target << 32 | (i0 / BM) << 16 | (j0 / BN)
   const int64_t tr = tiles[blockIdx.x];
   const int64_t t = tr >> 32;
   const int i0 = (int)((tr >> 16) & 0xffff) * BM, j0 = (int)(tr & 0xffff) * BN;
-  if (lower_only && j0 > i0) return;
+  if (lower_only && j0 >= i0 + BM) return;
   const int64_t* trow = targets + 8 * t;
   const Opnd C = load_opnd(trow, m0, off);
   if (i0 >= C.rows || j0 >= C.cols) return;
   const int sb = (int)trow[7], se = (int)targets[8 * (t + 1) + 7];
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int wm = warp >> 1, wn = warp & 1;
-  double acc[4][4][2];
+  const int wm = warp / (BN / WN), wn = warp % (BN / WN);
+  double acc[FM][FN][2];
 #pragma unroll
-  for (int a = 0; a < 4; ++a)
+  for (int a = 0; a < FM; ++a)
 #pragma unroll
-    for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+    for (int b = 0; b < FN; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
 
   // segment operands: 14 int64 {A, B operand rows}, or (compact) one int64
   // {A block << 32 | B block} into the block table (rows {ptr, rc, cc})
@@ -154,16 +162,16 @@ gemm_grouped_kernel(const int64_t* __restrict__ tiles, const int64_t* __restrict
       if (have_next) load_stage(st ^ 1, An, Bn, kn, Kn);
 #pragma unroll
       for (int kk = 0; kk < BK / 4; ++kk) {
-        double af[4], bf[4];
+        double af[FM], bf[FN];
         const int kr = kk * 4 + (lane & 3);
 #pragma unroll
-        for (int mi = 0; mi < 4; ++mi) af[mi] = As[st][kr][wm * 32 + mi * 8 + (lane >> 2)];
+        for (int mi = 0; mi < FM; ++mi) af[mi] = As[st][kr][wm * WM + mi * 8 + (lane >> 2)];
 #pragma unroll
-        for (int ni = 0; ni < 4; ++ni) bf[ni] = Bs[st][kr][wn * 32 + ni * 8 + (lane >> 2)];
+        for (int ni = 0; ni < FN; ++ni) bf[ni] = Bs[st][kr][wn * WN + ni * 8 + (lane >> 2)];
 #pragma unroll
-        for (int mi = 0; mi < 4; ++mi)
+        for (int mi = 0; mi < FM; ++mi)
 #pragma unroll
-          for (int ni = 0; ni < 4; ++ni) dmma(acc[mi][ni][0], acc[mi][ni][1], af[mi], bf[ni]);
+          for (int ni = 0; ni < FN; ++ni) dmma(acc[mi][ni][0], acc[mi][ni][1], af[mi], bf[ni]);
       }
       __syncthreads();
       if (!have_next) break;
@@ -177,14 +185,14 @@ gemm_grouped_kernel(const int64_t* __restrict__ tiles, const int64_t* __restrict
   }
   // epilogue: C = beta C + alpha acc
 #pragma unroll
-  for (int mi = 0; mi < 4; ++mi) {
-    const int r = i0 + wm * 32 + mi * 8 + (lane >> 2);
+  for (int mi = 0; mi < FM; ++mi) {
+    const int r = i0 + wm * WM + mi * 8 + (lane >> 2);
     if (r >= C.rows) continue;
 #pragma unroll
-    for (int ni = 0; ni < 4; ++ni) {
+    for (int ni = 0; ni < FN; ++ni) {
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        const int c = j0 + wn * 32 + ni * 8 + (lane & 3) * 2 + h;
+        const int c = j0 + wn * WN + ni * 8 + (lane & 3) * 2 + h;
         if (c >= C.cols) continue;
         double* pc = C.p + r + (int64_t)c * C.ld;
         const double v = alpha * acc[mi][ni][h];
@@ -201,9 +209,23 @@ extern "C" int spand_gemm_grouped(int ntile, const int64_t* tiles, const int64_t
                                   int tri, const int64_t* btab, int compact, void* stream) {
   if (ntile < 0) return -1;
   if (ntile == 0) return 0;
-  gemm_grouped_kernel<<<ntile, kThreads, 0, as_stream(stream)>>>(tiles, targets, segs, m0, off,
-                                                                 alpha, beta, bT, lower_only,
-                                                                 tri, btab, compact);
+  const int shape = (tri >> 4) & 7;
+  tri &= 7;
+  cudaStream_t st = as_stream(stream);
+#define SPAND_GEMM_LAUNCH(BM_, BN_, WM_, WN_)                                             \
+  gemm_grouped_kernel<BM_, BN_, WM_, WN_><<<ntile, kThreads, 0, st>>>(                    \
+      tiles, targets, segs, m0, off, alpha, beta, bT, lower_only, tri, btab, compact)
+  switch (shape) {
+    case 0: SPAND_GEMM_LAUNCH(64, 64, 32, 32); break;
+    case 1: SPAND_GEMM_LAUNCH(64, 16, 16, 16); break;
+    case 2: SPAND_GEMM_LAUNCH(32, 32, 16, 16); break;
+    case 3: SPAND_GEMM_LAUNCH(16, 16, 8, 8); break;
+    case 4: SPAND_GEMM_LAUNCH(16, 64, 16, 16); break;
+    case 5: SPAND_GEMM_LAUNCH(64, 32, 32, 16); break;
+    case 6: SPAND_GEMM_LAUNCH(32, 64, 16, 32); break;
+    default: return -1;
+  }
+#undef SPAND_GEMM_LAUNCH
   SPAND_CHECK_LAUNCH();
   return 0;
 }

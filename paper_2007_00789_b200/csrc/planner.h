@@ -16,6 +16,30 @@ extern "C" int spand_rrqr_capacity(int vmax);
 namespace spand {
 
 constexpr int kTile = 64;
+// grouped-GEMM tile shapes (gemm.cu, launch tri >> 4): 64x64, 64x16, 32x32,
+// 16x16, 16x64, 64x32, 32x64.  Each target gets the smallest shape that covers a narrow
+// side; the targets of one logical GEMM are launched once per shape used.
+constexpr int kNShape = 7;
+constexpr int kShapeM[kNShape] = {64, 64, 32, 16, 16, 64, 32};
+constexpr int kShapeN[kNShape] = {64, 16, 32, 16, 64, 32, 64};
+inline int tile_shape(int64_t mm, int64_t nn) {
+  if (mm <= 16 && nn <= 16) return 3;
+  if (nn <= 16) return 1;
+  if (mm <= 16) return 4;
+  if (mm <= 32 && nn <= 32) return 2;
+  if (nn <= 32) return 5;
+  if (mm <= 32) return 6;
+  return 0;
+}
+inline void push_tiles(std::vector<int64_t>& v, int64_t t, int64_t mm, int64_t nn, int s,
+                       bool lower) {
+  const int tm = kShapeM[s], tn = kShapeN[s];
+  for (int64_t i = 0; i < mm; i += tm)
+    for (int64_t j = 0; j < nn; j += tn) {
+      if (lower && j >= i + tm) continue;
+      v.push_back((t << 32) | ((i / tm) << 16) | (j / tn));
+    }
+}
 constexpr int kBigPotrf = 256;   // larger diagonal blocks use the blocked (multi-CTA) Cholesky
 constexpr int kMaxGroupTotal = 148 * 16;   // >= any cooperative RRQR grid
 
@@ -418,7 +442,7 @@ struct Plan {
             int tri = 0, int compact = 0) {
     if (ts.empty()) return;
     const int64_t sw = compact ? 1 : 14;
-    std::vector<int64_t> trow, srow, tiles;
+    std::vector<int64_t> trow, srow, tiles[kNShape];
     int64_t nseg = 0;
     trow.reserve(8 * ts.size() + 8);
     for (size_t t = 0; t < ts.size(); ++t) {
@@ -427,31 +451,41 @@ struct Plan {
       srow.insert(srow.end(), ts[t].segs.data(), ts[t].segs.data() + ts[t].segs.size());
       nseg += (int64_t)ts[t].segs.size() / sw;
       if (dry) continue;
-      for (int64_t i = 0; i < ts[t].mm; i += kTile)
-        for (int64_t j = 0; j < ts[t].nn; j += kTile) {
-          if (lower && j > i) continue;
-          tiles.push_back(((int64_t)t << 32) | ((i / kTile) << 16) | (j / kTile));
-        }
+      push_tiles(tiles[tile_shape(ts[t].mm, ts[t].nn)], (int64_t)t, ts[t].mm, ts[t].nn,
+                 tile_shape(ts[t].mm, ts[t].nn), lower != 0);
     }
     trow.insert(trow.end(), {0, 0, 0, 0, 0, 0, 0, nseg});
-    if (dry || tiles.empty()) return;
-    if (srow.empty()) srow.assign(14, 0);
-    const int64_t a = push(tiles), b = push(trow), c = push(srow);
-    launch(3, (int64_t)tiles.size(), a, b, c, bT, lower, tri, alpha, beta);
-    if (!dry) launches[launches.size() - 6] = compact;   // field 10
+    if (dry) return;
+    emit_gemm(tiles, trow, srow, alpha, beta, bT, lower, tri, compact);
+  }
+  void emit_gemm(std::vector<int64_t> (&tiles)[kNShape], std::vector<int64_t>& trow,
+                 std::vector<int64_t>& srow, double alpha, double beta, int bT, int lower,
+                 int tri, int compact) {
+    int64_t b = -1, c = -1;
+    for (int s = 0; s < kNShape; ++s) {
+      if (tiles[s].empty()) continue;
+      if (b < 0) {
+        if (srow.empty()) srow.assign(14, 0);
+        b = push(trow);
+        c = push(srow);
+      }
+      const int64_t a = push(tiles[s]);
+      launch(3, (int64_t)tiles[s].size(), a, b, c, bT, lower, tri | (s << 4), alpha, beta);
+      launches[launches.size() - 6] = compact;   // field 10
+    }
   }
 
   // Flat GEMM target list, written in place (the per-level hot paths: the
   // panel TRSMs and the grouped Schur updates emit ~10^5 targets each on the
   // leaf levels; no intermediate Target objects)
   struct FlatGemm {
-    std::vector<int64_t> trow, srow, tiles;
+    std::vector<int64_t> trow, srow, tiles[kNShape];
     int64_t nseg = 0, sw = 14, ntarget = 0;
     bool lower = false;
     void reserve(size_t nt, size_t nsegs) {
       trow.reserve(8 * nt + 8);
       srow.reserve(sw * nsegs + 14);
-      tiles.reserve(nt + 16);
+      tiles[0].reserve(nt / 4 + 16);
     }
     // begin a target: C operand (7 values), extents for the tile grid
     template <class... A>
@@ -459,12 +493,10 @@ struct Plan {
       const int64_t e[7] = {c...};
       trow.insert(trow.end(), e, e + 7);
       trow.push_back(nseg);
-      if (!dry)
-        for (int64_t i = 0; i < mm; i += kTile)
-          for (int64_t j = 0; j < nn; j += kTile) {
-            if (lower && j > i) continue;
-            tiles.push_back((ntarget << 32) | ((i / kTile) << 16) | (j / kTile));
-          }
+      if (!dry) {
+        const int s = tile_shape(mm, nn);
+        push_tiles(tiles[s], ntarget, mm, nn, s, lower);
+      }
       ++ntarget;
     }
     void seg(int64_t s) {
@@ -480,11 +512,8 @@ struct Plan {
   void gemm_flat(FlatGemm& g, double alpha, double beta, int bT, int tri = 0) {
     if (g.ntarget == 0) return;
     g.trow.insert(g.trow.end(), {0, 0, 0, 0, 0, 0, 0, g.nseg});
-    if (dry || g.tiles.empty()) return;
-    if (g.srow.empty()) g.srow.assign(14, 0);
-    const int64_t a = push(g.tiles), b = push(g.trow), c = push(g.srow);
-    launch(3, (int64_t)g.tiles.size(), a, b, c, bT, g.lower ? 1 : 0, tri, alpha, beta);
-    launches[launches.size() - 6] = g.sw == 1 ? 1 : 0;   // field 10: compact
+    if (dry) return;
+    emit_gemm(g.tiles, g.trow, g.srow, alpha, beta, bT, g.lower ? 1 : 0, tri, g.sw == 1 ? 1 : 0);
   }
 
   // batched triangular inverses: 64-tiles + recursive doubling GEMMs

@@ -32,7 +32,7 @@ def rrqr_single(a, eps, scheme, group=None, pad=0):
     cap = max(1, _lib.load().spand_rrqr_capacity(max(m, 1)))
     g = group or max(1, min(cap, n // 64, (m * n) // 65536 + 1))
     ncap, mcap = max(np_, 1), max(mp, 1)
-    wsz = mcap * ncap + mcap * mcap + 32 * (ncap + mcap)
+    wsz = mcap * ncap + mcap * mcap + 32 * (ncap + mcap) + 32 * mcap + 1024   # + T blocks
     asz = 2 * ncap + 3 * mcap + 2 * g * 34 + 8 + 1024
     isz = (3 * ncap + 1) // 2 + 1
     work = t.zeros(wsz + asz + isz + 1, dtype=t.float64, device=dev())
