@@ -111,7 +111,6 @@ struct Sh {
   double* cbase[64];  // frozen GEMM epilogue: column base in the pool
   int64_t cstride[64];
   int fcol[64];
-  int rbh, rbc;        // hot / cold pool offsets of this CTA (rebalancing)
 };
 
 __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
@@ -202,18 +201,6 @@ __device__ __forceinline__ void block_reduce_n(double (&v)[N], Sh& sh) {
   for (int q = 0; q < N; ++q) v[q] = sh.tot8[q];
 }
 
-// Re-dealing the hot / cold columns evenly over the group at each block end
-// (SPAND_REBALANCE=1, panels of >= SPAND_REB_MMIN rows) keeps the pivots bit
-// for bit (a column's arithmetic does not depend on its CTA) and shortens the
-// root panel by ~6 %, but the L1-bypassing loads it needs slow the other
-// panels by more: off by default (measured C4-L15 RRQR 1115 vs 1133 ms).
-#ifndef SPAND_REBALANCE
-#define SPAND_REBALANCE 0
-#endif
-#ifndef SPAND_REB_MMIN
-#define SPAND_REB_MMIN 2048
-#endif
-
 struct ColCtx {
   double* W;
   int m, k, len;
@@ -226,14 +213,10 @@ struct ColCtx {
   int rank, G;
   unsigned long long* refresh_ctr;
   int jpos;               // this step's swap: position k now belongs to jpos
-  bool cg;                // columns migrate between CTAs: bypass L1
-  __device__ __forceinline__ double ld(const double* p) const {
-    return (SPAND_REBALANCE && cg) ? __ldcg(p) : *p;
-  }
   // current position of column c: the owner may not have applied this
   // step's swap yet when another CTA processes c, so apply it here
   __device__ int64_t posof(int c) const {
-    const int p = (SPAND_REBALANCE && cg) ? __ldcg(pos + c) : pos[c];
+    const int p = pos[c];
     return p == k ? jpos : p;
   }
 };
@@ -257,7 +240,7 @@ __device__ void colpass_batch(const ColCtx& X, int a0, int nb, Sh& sh, double& b
 #pragma unroll
     for (int e = 0; e < E; ++e) {
       const int i = tid + kT * e;
-      x[b][e] = (cs[b] >= 0 && i < X.len) ? X.ld(col + i) : 0.0;
+      x[b][e] = (cs[b] >= 0 && i < X.len) ? col[i] : 0.0;
     }
   }
   // running norms of the batch (broadcast loads; only thread b writes them,
@@ -265,8 +248,8 @@ __device__ void colpass_batch(const ColCtx& X, int a0, int nb, Sh& sh, double& b
   double cur0[B], ref0[B];
 #pragma unroll
   for (int b = 0; b < B; ++b) {
-    cur0[b] = cs[b] >= 0 ? X.ld(X.cur + cs[b]) : 0.0;
-    ref0[b] = cs[b] >= 0 ? X.ld(X.ref + cs[b]) : 0.0;
+    cur0[b] = cs[b] >= 0 ? X.cur[cs[b]] : 0.0;
+    ref0[b] = cs[b] >= 0 ? X.ref[cs[b]] : 0.0;
   }
   // (double-buffered by batch parity: the previous batch may still read its
   // copy when no second reduction separates the batches)
@@ -356,7 +339,7 @@ __device__ void colpass_warp(const ColCtx& X, int nact, double& bv, int64_t& bp,
 #pragma unroll
       for (int e = 0; e < R; ++e) {
         const int i = lane + 32 * e;
-        x[u][e] = (cs[u] >= 0 && i < X.len) ? X.ld(col + i) : 0.0;
+        x[u][e] = (cs[u] >= 0 && i < X.len) ? col[i] : 0.0;
       }
     }
     double d[U];
@@ -389,9 +372,9 @@ __device__ void colpass_warp(const ColCtx& X, int nact, double& bv, int64_t& bp,
       rk = __shfl_sync(0xffffffffu, rk, 0);
       if (lane == u && cs[u] >= 0) {
         const int c = cs[u];
-        double cn = X.ld(X.cur + c) - rk * rk;
+        double cn = X.cur[c] - rk * rk;
         if (cn < 0.0) cn = 0.0;
-        if (cn < 0.01 * X.ld(X.ref + c)) {
+        if (cn < 0.01 * X.ref[c]) {
           cn = tail;
           X.ref[c] = tail;
           atomicAdd(X.refresh_ctr, 1ull);
@@ -414,21 +397,21 @@ __device__ void colpass_long(const ColCtx& X, int a0, Sh& sh, double& bv, int64_
   const int c = X.list[X.rank + X.G * a0];
   double* col = X.W + (int64_t)c * X.m + X.k;
   double d[1] = {0.0};
-  for (int i = tid; i < X.len; i += kT) d[0] += X.v[i] * X.ld(col + i);
+  for (int i = tid; i < X.len; i += kT) d[0] += X.v[i] * col[i];
   block_reduce_n<1>(d, sh);
   const double w = X.tau * d[0];
   double t[2] = {0.0, 0.0};
   for (int i = tid; i < X.len; i += kT) {
-    const double y = X.ld(col + i) - w * X.v[i];
+    const double y = col[i] - w * X.v[i];
     col[i] = y;
     if (i == 0) t[1] = y;
     else t[0] += y * y;
   }
   block_reduce_n<2>(t, sh);
   if (tid == 0) {
-    double cn = X.ld(X.cur + c) - t[1] * t[1];
+    double cn = X.cur[c] - t[1] * t[1];
     if (cn < 0.0) cn = 0.0;
-    if (cn < 0.01 * X.ld(X.ref + c)) {
+    if (cn < 0.01 * X.ref[c]) {
       cn = t[0];
       X.ref[c] = t[0];
       atomicAdd(X.refresh_ctr, 1ull);
@@ -601,10 +584,6 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
   const int c0 = (int)(((int64_t)n * rank) / G), c1 = (int)(((int64_t)n * (rank + 1)) / G);
   const int q0 = (int)(((int64_t)m * rank) / G), q1 = (int)(((int64_t)m * (rank + 1)) / G);
   const int kmax = m < n ? m : n;
-  // optional (SPAND_REBALANCE): hot / cold columns re-dealt evenly over the
-  // group at every block end; columns then change CTA, so their loads bypass L1
-  const bool reb = SPAND_REBALANCE && G >= 8 && m >= SPAND_REB_MMIN;
-  auto ldv = [&](const double* p2) -> double { return reb ? __ldcg(p2) : *p2; };
 
   // neighbour of column c: binary search of the column starts (the last
   // neighbour starting at or before c; zero-width neighbours are skipped)
@@ -728,8 +707,6 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
     __syncthreads();
   };
   publish(bv, bp, bc, 0);
-  int32_t* const rb_cnt = flist + 28 * ncap;   // pool sizes (hot, cold)
-  if (reb && rank == 0 && tid < 2) rb_cnt[tid] = 0;
   group_barrier(ctr, G, gen, -1, events + 12 * slot + 9);
 
   // ---- elimination (unblocked Householder steps on the ACTIVE columns).
@@ -929,7 +906,7 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
           for (int ni = 0; ni < 2; ++ni)
 #pragma unroll
             for (int h = 0; h < 2; ++h)
-              xo[ni][h] = (i < re && okc[ni][h]) ? ldv(xc[ni][h] + i) : 0.0;
+              xo[ni][h] = (i < re && okc[ni][h]) ? xc[ni][h][i] : 0.0;
           double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
 #pragma unroll
           for (int kq = 0; kq < 8; ++kq)
@@ -984,7 +961,7 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
           ZT[tid][t - ka] = suf;
           suf += RK[tid][t - ka] * RK[tid][t - ka];
         }
-        double cn = ldv(cur + c), rf = ldv(ref + c);
+        double cn = cur[c], rf = ref[c];
         for (int t = ka; t < kb; ++t) {
           const double rk = RK[tid][t - ka];
           double d = cn - rk * rk;
@@ -1257,58 +1234,26 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
       for (int u = tid; u < nh + ncd; u += kT) {
         const int c = u < nh ? hot_in[rank + G * u] : coldl[rank + G * (u - nh)];
         if (done[c]) continue;
-        const double cc = ldv(cur + c);
-        if (cc < thr2) {
+        if (cur[c] < thr2) {
           done[c] = 2;
-          atomicMax(&sh.fmax, (unsigned long long)__double_as_longlong(cc));
-        } else if (cc >= tau_hot) {
+          atomicMax(&sh.fmax, (unsigned long long)__double_as_longlong(cur[c]));
+        } else if (cur[c] >= tau_hot) {
           tmpl[rank + G * atomicAdd(&sh.nact, 1)] = c;
         } else {
           cold_out[rank + G * atomicAdd(&sh.ncold, 1)] = c;
-          if (!reb)
-            atomicMax(reinterpret_cast<unsigned long long*>(&sh.coldmax),
-                      (unsigned long long)__double_as_longlong(cc));
+          atomicMax(reinterpret_cast<unsigned long long*>(&sh.coldmax),
+                    (unsigned long long)__double_as_longlong(cur[c]));
         }
       }
       __syncthreads();
-      int nh2 = sh.nact;
-      if (reb) {
-        // deal the group's hot and cold columns out evenly: append to two
-        // pools, then every CTA takes a contiguous slice of each.  A column's
-        // arithmetic does not depend on which CTA runs it, so the pivots
-        // are the same as without re-dealing.
-        int32_t* hpool = flist + 24 * ncap;
-        int32_t* cpool = flist + 26 * ncap;
-        const int nc2 = sh.ncold;
-        if (tid == 0) {
-          sh.rbh = atomicAdd(rb_cnt, nh2);
-          sh.rbc = atomicAdd(rb_cnt + 1, nc2);
-        }
-        __syncthreads();
-        for (int u = tid; u < nh2; u += kT) hpool[sh.rbh + u] = tmpl[rank + G * u];
-        for (int u = tid; u < nc2; u += kT) cpool[sh.rbc + u] = cold_out[rank + G * u];
-        group_barrier(ctr, G, gen, -3, events + 12 * slot + 9);
-        const int th = (int)__ldcg(rb_cnt), tc = (int)__ldcg(rb_cnt + 1);
-        const int h0 = (int)((int64_t)th * rank / G), h1 = (int)((int64_t)th * (rank + 1) / G);
-        const int e0 = (int)((int64_t)tc * rank / G), e1 = (int)((int64_t)tc * (rank + 1) / G);
-        for (int u = tid; u < h1 - h0; u += kT) hot_in[rank + G * u] = __ldcg(hpool + h0 + u);
-        for (int u = tid; u < e1 - e0; u += kT) cold_out[rank + G * u] = __ldcg(cpool + e0 + u);
-        nh2 = h1 - h0;
-        __syncthreads();
-        if (tid == 0) {
-          sh.nact = nh2;
-          sh.ncold = e1 - e0;
-        }
-        __syncthreads();
-        // max running norm^2 of the cold columns dealt to me
-        for (int u = tid; u < e1 - e0; u += kT)
-          atomicMax(reinterpret_cast<unsigned long long*>(&sh.coldmax),
-                    (unsigned long long)__double_as_longlong(ldv(cur + cold_out[rank + G * u])));
-        __syncthreads();
-      } else {
-        for (int u = tid; u < nh2; u += kT) hot_in[rank + G * u] = tmpl[rank + G * u];
-      }
       if (sh.ncold == 0 && tid == 0) sh.coldmax = -1.0;
+      int nh2 = sh.nact;
+      // (columns stay with their owner CTA.  Re-dealing hot / cold columns
+      // evenly over the group here keeps the pivots bit for bit and shortens
+      // the root panel by ~6 %, but its extra barrier and L1-bypassing loads
+      // cost the other panels more: 1108 -> 1136 ms over C4-L15, commit
+      // 5ae96c5 has it as SPAND_REBALANCE)
+      for (int u = tid; u < nh2; u += kT) hot_in[rank + G * u] = tmpl[rank + G * u];
       coldl = cold_out;
       k0 = k;
       maint = 0;
@@ -1318,8 +1263,8 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
       __syncthreads();
       for (int u = tid; u < nh2; u += kT) {
         const int c = hot_in[rank + G * u];
-        const double cv = ldv(cur + c);
-        const int64_t ps = reb ? __ldcg(pos + c) : pos[c];
+        const double cv = cur[c];
+        const int64_t ps = pos[c];
         if (better(cv, ps, bv, bp)) {
           bv = cv;
           bp = ps;
@@ -1341,8 +1286,6 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
       publish(bv, bp, bc, cpar ^ 1);
       cpar ^= 1;
       group_barrier(ctr, G, gen, -2, events + 12 * slot + 9);
-      // (every CTA has read the pool sizes: reset them for the next block)
-      if (reb && rank == 0 && tid < 2) rb_cnt[tid] = 0;
       PH(0);
     }
     // ---- winning column: max value, smallest current position (ties in
@@ -1524,15 +1467,14 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
     __syncthreads();
     auto consider = [&](int c) {
       if (c == j || done[c]) return;
-      const double cc = ldv(cur + c);
-      if (cc < thr2) {
+      if (cur[c] < thr2) {
         done[c] = 2;
-        atomicMax(&sh.fmax, (unsigned long long)__double_as_longlong(cc));
+        atomicMax(&sh.fmax, (unsigned long long)__double_as_longlong(cur[c]));
       } else {
         list_out[rank + G * atomicAdd(&sh.nact, 1)] = c;
 #ifdef SPAND_RRQR_PHASES
-        if (cc >= 0.25 * wv) atomicAdd(&sh.nhot, 1);
-        if (cc >= 0.09 * wv) atomicAdd(&sh.nhot3, 1);
+        if (cur[c] >= 0.25 * wv) atomicAdd(&sh.nhot, 1);
+        if (cur[c] >= 0.09 * wv) atomicAdd(&sh.nhot3, 1);
 #endif
       }
     };
@@ -1555,7 +1497,7 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
     // batches for long ones
     {
       ColCtx X{W, m, k, len, tau, vsh, cur, ref, pos, list_out, rank, G,
-               reinterpret_cast<unsigned long long*>(events + 12 * slot + 10), jpos, reb};
+               reinterpret_cast<unsigned long long*>(events + 12 * slot + 10), jpos};
       if (len <= 256) {
         colpass_warp<4, 8>(X, nact, bv, bp, bc);
       } else if (len <= 512) {
