@@ -113,6 +113,13 @@ int spand_apply_scatter(int nout, const int64_t* dst, const int64_t* mode,
 int spand_apply_runs(int nchunk, const int64_t* chunks, const int64_t* contrib, double* x,
                      int64_t ldx, const double* scratch, int64_t ldscr, int nvec,
                      void* stream);
+/* A whole forward or backward pass of a structured plan: for each of the
+ * nphase rows of the HOST phase table ph (10 int64: {tasks, ntask, items,
+ * nitem, chunks, nchunk, contrib, grid, 0, 0}, offsets in int64 units into
+ * the device image), spand_gemv_items then spand_apply_runs on `stream`.
+ * Same result as issuing the 2 nphase calls one by one. */
+int spand_apply_pass(int nphase, const int64_t* ph, const int64_t* image, double* x,
+                     int64_t ldx, double* scratch, int64_t ldscr, int nvec, void* stream);
 
 /* ---- factorization kernels (replace dense.py:45-183 and the BLAS calls of
  *      schemes.py:199-236, factorize.py:131-220) ---------------------------- */

@@ -396,6 +396,24 @@ int spand_gemv_items(int nitem, int grid, const int64_t* items, const int64_t* t
   return 0;
 }
 
+// one whole pass (forward or backward) of a structured plan from its phase
+// table: the per-phase gemv + runs launches are issued here, not from Python
+int spand_apply_pass(int nphase, const int64_t* ph, const int64_t* image, double* x, int64_t ldx,
+                     double* scratch, int64_t ldscr, int nvec, void* stream) {
+  if (nphase < 0 || nvec < 1) return -1;
+  for (int q = 0; q < nphase; ++q) {
+    const int64_t* r = ph + 10 * (int64_t)q;
+    // {tasks, ntask, items, nitem, chunks, nchunk, contrib, grid, -, -} (image offsets)
+    const int st1 = spand_gemv_items((int)r[3], (int)r[7], image + r[2], image + r[0], x, ldx,
+                                     scratch, ldscr, nvec, stream);
+    if (st1 != 0) return st1;
+    const int st2 = spand_apply_runs((int)r[5], image + r[4], image + r[6], x, ldx, scratch,
+                                     ldscr, nvec, stream);
+    if (st2 != 0) return st2;
+  }
+  return 0;
+}
+
 int spand_apply_scatter(int nout, const int64_t* dst, const int64_t* mode, const int64_t* ptr,
                         const int64_t* src, double* x, int64_t ldx, const double* scratch,
                         int64_t ldscr, int nvec, void* stream) {

@@ -163,6 +163,8 @@ class NativeApplyPlan(FastPlan):
                          nitem, ctypes.c_void_p(base + 8 * co), nch,
                          ctypes.c_void_p(base + 8 * cbo), grid))
         self.phase_table = ph
+        # host phase tables of the two passes (spand_apply_pass)
+        self._ph = (np.ascontiguousarray(ph[:nfw]), np.ascontiguousarray(ph[nfw:]))
         self.build_times = {"setup_s": t_setup, "image_s": t_image,
                             "upload_s": time.perf_counter() - t0, "image_mb": image.nbytes / 1e6,
                             "since_factor_s": time.perf_counter() - self._t0}
@@ -175,6 +177,17 @@ class NativeApplyPlan(FastPlan):
         st = stream()
         x = self.xbuf
         scr = self.scratch if nvec == 1 else self._scratch_multi
+        tab = getattr(self, "_ph", None)
+        if tab is not None:
+            # the whole pass in one native call (launch cost ~2 us per kernel
+            # instead of ~5 us through ctypes per call)
+            ph = tab[0] if phases is self.fwd else tab[1]
+            _lib.call("spand_apply_pass", len(ph), ph.ctypes.data, ptr(self.image), ptr(x),
+                      self.n, ptr(scr), self.scratch_len, nvec, st)
+            ngv = (nvec // 4) + ((nvec % 4) // 2) + (nvec % 2)   # gemv launches per phase
+            _lib.COUNTS["spand_gemv_items"] = _lib.COUNTS.get("spand_gemv_items", 0) + ngv * len(ph)
+            _lib.COUNTS["spand_apply_runs"] = _lib.COUNTS.get("spand_apply_runs", 0) + len(ph)
+            return
         for tasks, items, nitem, chunks, nch, contrib, grid in phases:
             _lib.call("spand_gemv_items", nitem, grid, items, tasks, ptr(x), self.n,
                       ptr(scr), self.scratch_len, nvec, st)
