@@ -13,6 +13,9 @@
 //   * the structured apply plan (phases of GEMV tiles + ordered scatters in
 //     the cluster-contiguous numbering, see apply.cu / fastplan.py).
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <atomic>
 #include <cstdint>
 #include <thread>
@@ -31,6 +34,12 @@ struct Task {
   int64_t mode;
 };
 
+struct PhaseImage {
+  std::vector<int64_t> rows, tiles, chunks, contrib;
+  int64_t pos = 0;
+  bool overflow = false;
+};
+
 struct Collected {
   std::vector<int64_t> ops;    // 16 per op
   std::vector<int64_t> segs;   // 8 per segment
@@ -45,7 +54,9 @@ struct Collected {
   // apply
   std::vector<std::vector<Task>> fph, bph;
   std::vector<int64_t> fidx;   // permuted indices of the final block
-  std::vector<int64_t> plan;   // device image (int64)
+  std::vector<PhaseImage> imgs;  // compiled phases (concatenated by spand_collect_apply_get)
+  std::vector<int64_t> img_at;   // image offset of each compiled phase (-1: empty)
+  int64_t img_len = 0;
   std::vector<int64_t> phases; // 10 per phase (see spand_collect_apply_get)
   int64_t scratch_len = 0;
 };
@@ -78,6 +89,18 @@ void* spand_collect_create(void* plan, const int64_t* events, int scheme) {
   }
   C->fph.assign(nph, {});
   C->bph.assign(nph, {});
+  {
+    size_t nin = 0, nint = 0, nact = 0;
+    for (const spand::Level& L : pv.lv) {
+      nin += L.inb_blk.size();
+      nint += L.interiors.size();
+      nact += L.active.size();
+    }
+    C->segs.reserve(8 * nin + 8 * 16 * nact);
+    C->views.reserve(4 * (nin + nint + 2 * nact) + 64 * nact);
+    C->ops.reserve(16 * (nint + 3 * nact + 1));
+    C->perm.reserve(pv.dofs.size());
+  }
   auto add = [&](std::vector<Task>& ph, int64_t M, int64_t ld, int64_t rows, int64_t cols,
                  int vtrans, int optrans, int64_t rot, int64_t in_start, int64_t out_start,
                  int64_t mode) {
@@ -95,13 +118,20 @@ void* spand_collect_create(void* plan, const int64_t* events, int scheme) {
     t.mode = mode;
     ph.push_back(t);
   };
+  auto T0 = std::chrono::steady_clock::now();
+  double tint = 0, tres = 0, tsp = 0;
   for (int li = 0; li < nlev; ++li) {
+    auto Ta = std::chrono::steady_clock::now();
     const spand::Level& L = pv.lv[li];
     const int64_t fb = fbase[li], bb = bbase[li];
     const int64_t nw = L.skipped ? 0 : L.nwaves;
     const int64_t gfT = fb, gfA = fb + 1;
     const int64_t gbA = bb + (L.skipped ? 0 : 2 * nw + 1), gbT = bb + (L.skipped ? 1 : 2 * nw + 2);
     int64_t nint = 0, ndofs = 0;
+    C->fph[gfA].reserve(L.inb_blk.size());
+    C->bph[gbA].reserve(L.inb_blk.size());
+    C->fph[gfT].reserve(L.interiors.size());
+    C->bph[gbT].reserve(L.interiors.size());
     for (int k = 0; k < (int)L.interiors.size(); ++k) {
       const int s = L.interiors[k];
       const int64_t ns = live(s);
@@ -112,10 +142,12 @@ void* spand_collect_create(void* plan, const int64_t* events, int scheme) {
       const int64_t lower = pv.boff[pv.block(s, s)] + off[s] + off[s] * m0s;
       const int64_t linv = pv.elim_linv[s] + off[s] + off[s] * m0s;
       const int64_t sb = (int64_t)C->segs.size() / 8;
-      for (int w : L.inbrs[k]) {
+      const int* blk = L.inb_blk.data() + L.inb_ptr[k];   // block(w, s), from the planner
+      for (size_t u = 0; u < L.inbrs[k].size(); ++u) {
+        const int w = L.inbrs[k][u];
         const int64_t lw = live(w);
         if (lw == 0) continue;
-        const int64_t a = pv.boff[pv.block(w, s)] + off[w] + off[s] * pv.m0[w];
+        const int64_t a = pv.boff[blk[u]] + off[w] + off[s] * pv.m0[w];
         C->segs.insert(C->segs.end(), {w, off[w], lw, a, pv.m0[w], lw, ns, 0});
         C->views.insert(C->views.end(), {a, pv.m0[w], lw, ns});
         add(C->fph[gfA], a, pv.m0[w], lw, ns, 0, 0, 0, pst(s), pst(w), 1);
@@ -129,6 +161,8 @@ void* spand_collect_create(void* plan, const int64_t* events, int scheme) {
       for (int64_t i = 0; i < ns; ++i) C->perm.push_back(pv.dofs[pv.dptr[s] + off[s] + i]);
     }
     C->lsum.insert(C->lsum.end(), {L.level, nint, ndofs, L.skipped});
+    auto Tb = std::chrono::steady_clock::now();
+    tint += std::chrono::duration<double>(Tb - Ta).count();
     if (L.skipped) continue;
     // rescales
     for (int k = 0; k < (int)L.active.size(); ++k) {
@@ -151,6 +185,8 @@ void* spand_collect_create(void* plan, const int64_t* events, int scheme) {
         wmax[L.wave[k]] = std::max(wmax[L.wave[k]], events[12 * L.slot[k] + 3]);
       for (int64_t v : wmax) C->critical_steps += v;
     }
+    auto Tc = std::chrono::steady_clock::now();
+    tres += std::chrono::duration<double>(Tc - Tb).count();
     // sparsifications in ascending id order
     for (int k = 0; k < (int)L.active.size(); ++k) {
       const int p = L.active[k];
@@ -213,7 +249,12 @@ void* spand_collect_create(void* plan, const int64_t* events, int scheme) {
       C->diag.insert(C->diag.end(), {li, p, mp, k_c, rf2, e[7], e[8], k_stop, e[2], 0});
       off[p] += n_fine;
     }
+    tsp += std::chrono::duration<double>(std::chrono::steady_clock::now() - Tc).count();
   }
+  if (getenv("SPAND_COLLECT_TIMES"))
+    fprintf(stderr, "collect: interiors %.1f ms rescale %.1f sparsify %.1f total %.1f\n", 1e3 * tint,
+            1e3 * tres, 1e3 * tsp,
+            1e3 * std::chrono::duration<double>(std::chrono::steady_clock::now() - T0).count());
   // final dense block
   int64_t total = 0;
   for (int c : pv.fin) total += live(c);
@@ -302,11 +343,6 @@ int spand_collect_get(void* h, int64_t* ops, int64_t* segs, int64_t* perm, int64
 // hit the same run contribute their scratch blocks in task order.
 // Addresses: payload windows pool_base/fac_base (bit 62 of the window offset
 // selects the factor buffer), inputs xbuf + 8 * permuted index.
-struct PhaseImage {
-  std::vector<int64_t> rows, tiles, chunks, contrib;
-  int64_t pos = 0;
-  bool overflow = false;
-};
 
 static void compile_phase(PhaseImage& P, const std::vector<Task>& ph, int64_t pool_base,
                           int64_t fac_base, int64_t xbuf, int64_t idx_addr) {
@@ -384,12 +420,11 @@ static void compile_phase(PhaseImage& P, const std::vector<Task>& ph, int64_t po
 }
 
 static void append_phase(Collected* C, const PhaseImage& P) {
-  auto put = [&](const std::vector<int64_t>& v) {
-    const int64_t at = (int64_t)C->plan.size();
-    C->plan.insert(C->plan.end(), v.begin(), v.end());
-    return at;
-  };
-  const int64_t a = put(P.rows), b = put(P.tiles), c = put(P.chunks), d = put(P.contrib);
+  // image layout of the phase: rows, items, chunks, contributions (copied
+  // into place by spand_collect_apply_get)
+  const int64_t a = C->img_len, b = a + (int64_t)P.rows.size(), c = b + (int64_t)P.tiles.size(),
+                d = c + (int64_t)P.chunks.size();
+  C->img_len = d + (int64_t)P.contrib.size();
   // persistent warps: 4 CTAs (32 warps) per SM, one warp per item below that
   const int64_t nitem = (int64_t)P.tiles.size() / 2;
   const int64_t grid = std::min<int64_t>((nitem + 7) / 8, 148 * 4);
@@ -404,37 +439,41 @@ static void append_phase(Collected* C, const PhaseImage& P) {
 int spand_collect_apply(void* h, int64_t pool_base, int64_t fac_base, int64_t xbuf,
                         int64_t idx_addr, int64_t* out) {
   Collected* C = static_cast<Collected*>(h);
-  C->plan.clear();
   C->phases.clear();
+  C->img_len = 0;
   C->scratch_len = 1;
-  // phases compile independently (host threads), then concatenate in order
+  // phases compile independently (host threads, largest first), then are
+  // laid out in order
   const size_t nf = C->fph.size(), nt = nf + C->bph.size();
-  std::vector<PhaseImage> imgs(nt);
+  auto phase = [&](size_t k) -> const std::vector<Task>& { return k < nf ? C->fph[k] : C->bph[k - nf]; };
+  std::vector<size_t> order(nt);
+  for (size_t k = 0; k < nt; ++k) order[k] = k;
+  std::stable_sort(order.begin(), order.end(),
+                   [&](size_t x, size_t y) { return phase(x).size() > phase(y).size(); });
+  C->imgs.assign(nt, PhaseImage());
+  std::vector<PhaseImage>& imgs = C->imgs;
   std::atomic<size_t> next{0};
   auto work = [&]() {
-    for (size_t k = next++; k < nt; k = next++)
-      compile_phase(imgs[k], k < nf ? C->fph[k] : C->bph[k - nf], pool_base, fac_base, xbuf,
-                    idx_addr);
+    for (size_t q = next++; q < nt; q = next++)
+      compile_phase(imgs[order[q]], phase(order[q]), pool_base, fac_base, xbuf, idx_addr);
   };
   const unsigned nth = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
   std::vector<std::thread> pool;
   for (unsigned i = 1; i < nth; ++i) pool.emplace_back(work);
   work();
   for (auto& th : pool) th.join();
-  size_t total = 0;
-  for (const auto& P : imgs)
-    total += P.rows.size() + P.tiles.size() + P.chunks.size() + P.contrib.size();
-  C->plan.reserve(total);
   for (const auto& P : imgs)
     if (P.overflow) return -2;   // operator too large for the packed item format
   int64_t nfw = 0, nbw = 0;
+  C->img_at.assign(nt, -1);
   for (size_t k = 0; k < nt; ++k) {
     if (imgs[k].rows.empty()) continue;
+    C->img_at[k] = C->img_len;
     append_phase(C, imgs[k]);
     if (k < nf) ++nfw;
     else ++nbw;
   }
-  out[0] = (int64_t)C->plan.size();
+  out[0] = C->img_len;
   out[1] = nfw;
   out[2] = nbw;
   out[3] = C->scratch_len;
@@ -445,8 +484,30 @@ int spand_collect_apply(void* h, int64_t pool_base, int64_t fac_base, int64_t xb
 // nchunk, contrib_off, grid (gemv_items CTAs), 0, scratch_used
 int spand_collect_apply_get(void* h, int64_t* image, int64_t* phases) {
   Collected* C = static_cast<Collected*>(h);
-  std::memcpy(image, C->plan.data(), C->plan.size() * sizeof(int64_t));
+  if (C->imgs.size() != C->img_at.size()) return -1;   // once per spand_collect_apply
+  // each phase's four arrays straight into the caller's (pinned) image, in
+  // parallel over phases
+  const size_t nt = C->imgs.size();
+  std::atomic<size_t> next{0};
+  auto work = [&]() {
+    for (size_t k = next++; k < nt; k = next++) {
+      if (C->img_at[k] < 0) continue;
+      int64_t* dst = image + C->img_at[k];
+      const PhaseImage& P = C->imgs[k];
+      for (const std::vector<int64_t>* v : {&P.rows, &P.tiles, &P.chunks, &P.contrib}) {
+        if (!v->empty()) std::memcpy(dst, v->data(), v->size() * sizeof(int64_t));
+        dst += v->size();
+      }
+    }
+  };
+  const unsigned nth = std::max(1u, std::min(8u, std::thread::hardware_concurrency()));
+  std::vector<std::thread> pool;
+  for (unsigned i = 1; i < nth; ++i) pool.emplace_back(work);
+  work();
+  for (auto& th : pool) th.join();
   std::memcpy(phases, C->phases.data(), C->phases.size() * sizeof(int64_t));
+  // the compiled phases are no longer needed
+  std::vector<PhaseImage>().swap(C->imgs);
   return 0;
 }
 

@@ -412,6 +412,7 @@ class Engine:
                                                       SCHEME_CODE[self.scheme]))
         self.collected = Collected(lib, ch, vp)
         col = self.collected
+        t1 = time.perf_counter()
         stats = np.zeros(1, dtype=np.int64)
         lib.spand_collect_stats.argtypes = [ctypes.c_void_p, ctypes.c_void_p]
         lib.spand_collect_stats(ch, vp(stats))
@@ -422,6 +423,7 @@ class Engine:
         perm_c = np.concatenate(sym.dofs) if sym.dofs else np.empty(0, np.int64)
         self.apply_plan = NativeApplyPlan(self.a.n, perm_c, col, self.pool, self.facbuf)
         ops = LazyOps(col, sym.dofs, self.pool, self.facbuf)
+        t2 = time.perf_counter()
         # diagnostics (factorize.py:331-356) + margins of every decision
         diags = []
         by_level = {}
@@ -452,8 +454,12 @@ class Engine:
                                                             "local_error") if k in f}
                                          for f in faces],
                           "margins": faces, "digest": digest})
+        t3 = time.perf_counter()
         nnz = self._count(col.views)
-        self.timings["collect_s"] = time.perf_counter() - t0
+        t4 = time.perf_counter()
+        self.timings.update(collect_s=t4 - t0, collect_native_s=t1 - t0,
+                            collect_apply_start_s=t2 - t1, collect_diag_s=t3 - t2,
+                            collect_count_s=t4 - t3)
         return ops, col.perm, {"levels": diags, "final_block": col.final_total}, nnz
 
     def _local_errors(self, col):

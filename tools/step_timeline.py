@@ -19,6 +19,7 @@ for rep in range(3):
     eng.run()            # ends with a synchronize
     T["run"] = time.perf_counter() - t1
     T.update({k: v for k, v in eng.timings.items() if k in ("launch_s", "plan_s")})
+    TC = eng.timings
     t2 = time.perf_counter()
     ops, perm, diag, nnz = eng.collect()
     T["collect"] = time.perf_counter() - t2
@@ -35,4 +36,5 @@ for rep in range(3):
     torch.cuda.synchronize()
     T["pcg"] = time.perf_counter() - t4
     T["total"] = time.perf_counter() - t0
-    print({k: round(v, 4) for k, v in T.items()}, "n_cg", rep_.n_cg, {k: round(v, 4) for k, v in f._plan.build_times.items()}, flush=True)
+    print({k: round(v, 4) for k, v in T.items()}, "n_cg", rep_.n_cg, {k: round(v, 4) for k, v in f._plan.build_times.items()},
+          {k: round(v, 4) for k, v in TC.items() if k.startswith("collect")}, flush=True)
