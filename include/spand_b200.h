@@ -222,6 +222,14 @@ int spand_assemble_final(int ncl, const int64_t* cl, int64_t nblk,
  * nnz properties, schemes.py:114-117,142-144,168-170,194-196.) */
 int spand_count_nonzero(int nview, const int64_t* views, unsigned long long* out,
                         void* stream);
+/* Total nonzero count of payload windows, load-balanced.  View rows are the
+ * collector's {offset (bit 62 set: in fac, else in pool; in doubles), ld,
+ * rows, cols}; view v is cut into ceil(cols / max(1, 65536 / max(rows, 1)))
+ * column pieces, pstart (nview + 1, device) is the exclusive prefix sum of
+ * those counts and npiece = pstart[nview]; the count is ADDED to *total. */
+int spand_count_nonzero_pieces(int nview, const int64_t* views, const int64_t* pstart,
+                               int64_t npiece, const double* pool, const double* fac,
+                               unsigned long long* total, void* stream);
 
 /* ---- host-side integer structure (partition.py:118-268) ------------------ */
 

@@ -252,9 +252,62 @@ count_kernel(const int64_t* __restrict__ views, unsigned long long* __restrict__
   for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
   if ((threadIdx.x & 31) == 0 && c) atomicAdd(out + blockIdx.x, c);
 }
+
+// Balanced variant: views are split into pieces of <= kCountPiece elements
+// (whole columns; pstart[v] = first piece of view v, exclusive prefix sum of
+// ceil(cols / max(1, kCountPiece / rows))), one CTA per piece, one total.
+constexpr int kCountPiece = 65536;
+__global__ void __launch_bounds__(kT)
+count_pieces_kernel(const int64_t* __restrict__ views, const int64_t* __restrict__ pstart,
+                    int nview, const double* pool, const double* fac,
+                    unsigned long long* __restrict__ total) {
+  const int64_t pc = blockIdx.x;
+  int lo = 0, hi = nview - 1;
+  while (lo < hi) {   // last view whose first piece is <= pc
+    const int mid = (lo + hi + 1) >> 1;
+    if (pstart[mid] <= pc) lo = mid;
+    else hi = mid - 1;
+  }
+  const int64_t* v = views + 4 * (int64_t)lo;
+  const int64_t ld = v[1], rows = v[2], cols = v[3];
+  const int64_t cpp = rows >= kCountPiece ? 1 : kCountPiece / rows;
+  const int64_t c0 = (pc - pstart[lo]) * cpp, c1 = min(cols, c0 + cpp);
+  // view offset: bit 62 selects the factor buffer (collector convention)
+  const int64_t o = v[0] & ((int64_t(1) << 62) - 1);
+  const double* p = (((v[0] >> 62) & 1) ? fac : pool) + o + c0 * ld;
+  unsigned long long c = 0;
+  if (rows >= 64) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int64_t q = warp; q < c1 - c0; q += kT / 32)
+      for (int64_t r = lane; r < rows; r += 32) c += p[r + q * ld] != 0.0;
+  } else {
+    const int rr = (int)rows, ne = (int)((c1 - c0) * rows);
+    for (int e = threadIdx.x; e < ne; e += kT) c += p[e % rr + (int64_t)(e / rr) * ld] != 0.0;
+  }
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  __shared__ unsigned long long part[kT / 32];
+  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = c;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long t = 0;
+    for (int w = 0; w < kT / 32; ++w) t += part[w];
+    if (t) atomicAdd(total, t);
+  }
+}
 }  // namespace
 
 extern "C" {
+
+int spand_count_nonzero_pieces(int nview, const int64_t* views, const int64_t* pstart,
+                               int64_t npiece, const double* pool, const double* fac,
+                               unsigned long long* total, void* stream) {
+  if (nview < 0 || npiece < 0 || npiece >= (int64_t(1) << 31)) return -1;
+  if (nview == 0 || npiece == 0) return 0;
+  count_pieces_kernel<<<(unsigned)npiece, kT, 0, as_stream(stream)>>>(views, pstart, nview, pool,
+                                                                      fac, total);
+  SPAND_CHECK_LAUNCH();
+  return 0;
+}
 
 int spand_assemble_final(int ncl, const int64_t* cl, int64_t nblk, const int64_t* blocks,
                          const int32_t* m0, int32_t* off, int32_t final_id, double* dst,

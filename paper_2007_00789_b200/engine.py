@@ -511,20 +511,21 @@ class Engine:
         t = self.t
         if views.shape[0] == 0:
             return 0
-        flag = np.int64(1) << np.int64(62)
-        in_fac = (views[:, 0] & flag) != 0
-        offs = views[:, 0] & (flag - 1)
-        addr = np.where(in_fac, self.facbuf.data_ptr() + 8 * offs,
-                        self.pool.data_ptr() + 8 * offs)
-        rows = np.stack([addr, views[:, 1], views[:, 2], views[:, 3]], axis=1)
-        keep = (rows[:, 2] > 0) & (rows[:, 3] > 0)
-        rows = np.ascontiguousarray(rows[keep])
-        if rows.shape[0] == 0:
+        # column pieces of <= 65536 entries (dense_small.cu count_pieces_kernel);
+        # the kernel resolves the pool / factor-buffer offsets itself
+        views = np.ascontiguousarray(views, dtype=np.int64)
+        cpp = np.maximum(1, 65536 // np.maximum(views[:, 2], 1))
+        pstart = np.zeros(views.shape[0] + 1, dtype=np.int64)
+        np.cumsum(np.where(views[:, 2] > 0, -(-views[:, 3] // cpp), 0), out=pstart[1:])
+        if pstart[-1] == 0:
             return 0
-        vd = to_dev(rows)
-        out = t.zeros(rows.shape[0], dtype=t.int64, device=dev())
-        _lib.call("spand_count_nonzero", rows.shape[0], ptr(vd), ptr(out), stream())
-        return int(out.sum().item())
+        vd = to_dev(views)
+        pd = to_dev(pstart)
+        out = t.zeros(1, dtype=t.int64, device=dev())
+        _lib.call("spand_count_nonzero_pieces", views.shape[0], ptr(vd), ptr(pd),
+                  int(pstart[-1]), self.pool.data_ptr(), self.facbuf.data_ptr(), ptr(out),
+                  stream())
+        return int(out.item())
 
 
 class LazyOps(Sequence):
