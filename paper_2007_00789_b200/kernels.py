@@ -117,12 +117,15 @@ def copy_batched(geo, tasks):
 
 
 TILE = 64
+# grouped-GEMM tile shapes (gemm.cu, `tri >> 4`; planner.h kShapeM / kShapeN)
+SHAPES = ((64, 64), (64, 16), (32, 32), (16, 16), (16, 64), (64, 32), (32, 64))
 
 
-def _tile_grid(mm, nn, lower_only=False):
-    """All (target, i0, j0) 64x64 tiles of targets with extents mm x nn."""
-    tm = np.maximum(-(-mm // TILE), 0)
-    tn = np.maximum(-(-nn // TILE), 0)
+def _tile_grid(mm, nn, lower_only=False, shape=0):
+    """All (target, i0, j0) tiles of targets with extents mm x nn."""
+    TM, TN = SHAPES[shape]
+    tm = np.maximum(-(-mm // TM), 0)
+    tn = np.maximum(-(-nn // TN), 0)
     cnt = tm * tn
     tot = int(cnt.sum())
     if tot == 0:
@@ -130,16 +133,16 @@ def _tile_grid(mm, nn, lower_only=False):
     tgt = np.repeat(np.arange(mm.size, dtype=np.int64), cnt)
     local = np.arange(tot, dtype=np.int64) - np.repeat(np.cumsum(cnt) - cnt, cnt)
     ntile_n = np.repeat(tn, cnt)
-    i0 = (local // ntile_n) * TILE
-    j0 = (local % ntile_n) * TILE
-    out = (tgt << 32) | ((i0 // TILE) << 16) | (j0 // TILE)
+    i0 = (local // ntile_n) * TM
+    j0 = (local % ntile_n) * TN
+    out = (tgt << 32) | ((i0 // TM) << 16) | (j0 // TN)
     if lower_only:
-        out = out[j0 <= i0]
+        out = out[j0 < i0 + TM]
     return out
 
 
 def gemm_grouped(geo, targets, alpha, beta, bT, lower_only=False,
-                 max_rows=None, max_cols=None, tri=0):
+                 max_rows=None, max_cols=None, tri=0, shape=0):
     """targets: [(C operand, [(A operand, B operand), ...], (max_m, max_n))].
 
     Tiles are laid out for the maximal (m0-geometry) sizes; tiles beyond a
@@ -155,7 +158,7 @@ def gemm_grouped(geo, targets, alpha, beta, bT, lower_only=False,
             srow.append(a + b)
         mm[t], nn[t] = mt, nt
     trow.append([0] * 7 + [len(srow)])
-    tiles = _tile_grid(mm, nn, lower_only)
+    tiles = _tile_grid(mm, nn, lower_only, shape)
     if tiles.shape[0] == 0:
         return
     if not srow:
@@ -163,7 +166,7 @@ def gemm_grouped(geo, targets, alpha, beta, bT, lower_only=False,
     td, sd, tl = _rows(trow, 8), _rows(srow, 14), _rows(tiles, 1)
     _lib.call("spand_gemm_grouped", int(tiles.shape[0]), ptr(tl), ptr(td), ptr(sd),
               ptr(geo.m0), ptr(geo.off), float(alpha), float(beta), int(bT),
-              int(bool(lower_only)), int(tri), None, 0, stream())
+              int(bool(lower_only)), int(tri) | (int(shape) << 4), None, 0, stream())
 
 
 # ---------------------------------------------------------------------------
