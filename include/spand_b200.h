@@ -156,11 +156,14 @@ int spand_copy_batched(int ntask, const int64_t* ops, const int32_t* m0,
  * after the last carries only seg_begin at column 7).
  * segment row (14 int64): {A operand(7), B operand(7)}; A is M x K; B is N x K
  * (bT = 1: op(B) = B^T, "NT") or K x N (bT = 0, "NN").
- * tile (1 int64, packed): target << 32 | (i0 / 64) << 16 | (j0 / 64); tile 64 x 64.
- * lower_only: skip tiles strictly above the diagonal (SYRK use).
- * tri: triangular operands (zero above their diagonal) bound the K range of a
- * tile at (i0, j0): 1 A lower -> k < i0 + 64; 2 B lower and bT = 1 ->
- * k < j0 + 64; 4 B lower and bT = 0 -> k >= j0 (TRSM/TRMM as GEMM at the
+ * tile (1 int64, packed): target << 32 | (i0 / BM) << 16 | (j0 / BN); the
+ * tile shape BM x BN is tri >> 4: 0 64x64, 1 64x16, 2 32x32, 3 16x16,
+ * 4 16x64, 5 64x32, 6 32x64 (one shape per launch; the planner launches each
+ * logical GEMM once per shape its targets use).
+ * lower_only: skip tiles strictly above the diagonal (j0 >= i0 + BM; SYRK use).
+ * tri & 7: triangular operands (zero above their diagonal) bound the K range
+ * of a tile at (i0, j0): 1 A lower -> k < i0 + BM; 2 B lower and bT = 1 ->
+ * k < j0 + BN; 4 B lower and bT = 0 -> k >= j0 (TRSM/TRMM as GEMM at the
  * triangular flop count).
  * compact = 1: a segment is ONE int64 {A block << 32 | B block} indexing the
  * block table btab (rows {ptr, rc, cc}: whole live blocks), the Schur-update
