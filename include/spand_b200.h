@@ -234,6 +234,15 @@ int spand_count_nonzero_pieces(int nview, const int64_t* views, const int64_t* p
                                int64_t npiece, const double* pool, const double* fac,
                                unsigned long long* total, void* stream);
 
+/* Trailing-matrix fingerprint pieces (EliminationState.digest,
+ * factorize.py:222-229, taken per level at :347).  Piece rows (6 int64):
+ * {block ptr, i, j, first column, columns, record ptr}; each piece ADDS an
+ * order-free 64-bit hash of its part of block (i, j)'s live window to
+ * record[4] and the piece at column 0 writes record[0..3] = {i, j, live
+ * rows, live cols}.  Records are 5 int64, zeroed by the caller. */
+int spand_digest_pieces(int npiece, const int64_t* rows, const int32_t* m0,
+                        const int32_t* off, void* stream);
+
 /* ---- host-side integer structure (partition.py:118-268) ------------------ */
 
 /* Nested-dissection hierarchy of the graph of a CSR matrix (host memory).
@@ -277,6 +286,11 @@ int spand_plan_emit_begin(void* h, int64_t pool_base, int64_t fac_base, int64_t 
 int spand_plan_emit_next(void* h, int64_t* chunk_sizes);
 int spand_plan_chunk(void* h, int64_t* prog, int64_t* launches);
 int spand_plan_meta(void* h, int64_t* out);
+/* Per-level trailing-matrix digests on/off (launch type 11 at every level
+ * end); returns the record count, first[nlevels + 1] the per-level record
+ * offsets (may be null).  Call with out_base = 0 to size, then with the
+ * device address of the zeroed records before emission. */
+int64_t spand_plan_set_digest(void* h, int on, int64_t out_base, int64_t* first);
 void* spand_collect_create(void* plan, const int64_t* events, int scheme);
 void spand_collect_destroy(void* h);
 int spand_collect_sizes(void* h, int64_t* out);

@@ -739,3 +739,157 @@ def pcg(apply_a, b, apply_m, tol, maxit=None):
         rz = rz_new
     true_res = float(np.linalg.norm(b - apply_a(x))) / bn
     return x, its, hist, done, true_res, time.perf_counter() - t0
+
+
+# ---------------------------------------------------------------------------
+# SPDF v1 factor container  (factorize.py:384-502)
+#
+# The checker's own reader/writer of the reference's byte format, so a
+# factor written by the device path is read back by code that does not share
+# anything with the product's reader (save_factor round trip, test_factorize.py
+# :279-330).
+
+SPDF_MAGIC = b"SPDF"
+SPDF_HEADER = "<HqdBHIq"        # version, n, eps, scheme tag, skip, ops, nnz
+SPDF_SCHEMES = {0: FIRST, 1: FULL, 2: SUPERFINE}
+SPDF_KINDS = "GDQE"             # tags 0..3 (factorize.py:387-392)
+
+
+class SPDFError(ValueError):
+    pass
+
+
+def _spdf_take(fh, count):
+    data = fh.read(count)
+    if len(data) != count:
+        raise SPDFError("truncated factor file")
+    return data
+
+
+def _spdf_array(fh, dtype):
+    import struct
+    ndim = struct.unpack("<B", _spdf_take(fh, 1))[0]
+    shape = struct.unpack(f"<{ndim}q", _spdf_take(fh, 8 * ndim))
+    count = int(np.prod(shape)) if ndim else 1
+    data = _spdf_take(fh, count * np.dtype(dtype).itemsize)
+    return np.frombuffer(data, dtype=dtype).reshape(shape).copy()
+
+
+def read_spdf(path):
+    """load_factor (factorize.py:452-502) -> (Factor, header dict)."""
+    import struct
+    with open(path, "rb") as fh:
+        if _spdf_take(fh, 4) != SPDF_MAGIC:
+            raise SPDFError("not a factor file (bad magic)")
+        ver, n, eps, stag, skip, nops, nnzf = struct.unpack(
+            SPDF_HEADER, _spdf_take(fh, struct.calcsize(SPDF_HEADER)))
+        if ver != 1:
+            raise SPDFError(f"unsupported factor file version {ver}")
+        if stag not in SPDF_SCHEMES:
+            raise SPDFError(f"unknown scheme tag {stag}")
+        perm = _spdf_array(fh, np.int64)
+        ops = []
+        for _ in range(nops):
+            tag = struct.unpack("<B", _spdf_take(fh, 1))[0]
+            if tag > 3:
+                raise SPDFError(f"unknown operator tag {tag}")
+            kind = SPDF_KINDS[tag]
+            dofs = _spdf_array(fh, np.int64)
+            if kind == "G":
+                w = _spdf_array(fh, np.int64)
+                low = _spdf_array(fh, np.float64)
+                ops.append(Op("G", dofs, w, lower=low, panel=_spdf_array(fh, np.float64)))
+            elif kind == "D":
+                ops.append(Op("D", dofs, lower=_spdf_array(fh, np.float64)))
+            elif kind == "Q":
+                ops.append(Op("Q", dofs, q=_spdf_array(fh, np.float64)))
+            else:
+                w = _spdf_array(fh, np.int64)
+                ops.append(Op("E", dofs, w, e_tilde=_spdf_array(fh, np.float64)))
+    head = {"n": int(n), "eps": float(eps), "scheme": SPDF_SCHEMES[stag],
+            "skip_levels": int(skip), "n_ops": int(nops), "nnz_factor": int(nnzf)}
+    f = Factor(ops, perm, int(n), None)
+    return f, head
+
+
+def write_spdf(f, path, eps, scheme, skip_levels):
+    """save_factor (factorize.py:424-449) for an oracle Factor."""
+    import struct
+    tag = {v: k for k, v in SPDF_SCHEMES.items()}[scheme]
+
+    def put(fh, arr, dtype):
+        arr = np.ascontiguousarray(arr, dtype=dtype)
+        fh.write(struct.pack("<B", arr.ndim))
+        fh.write(struct.pack(f"<{arr.ndim}q", *arr.shape))
+        fh.write(arr.tobytes())
+
+    with open(path, "wb") as fh:
+        fh.write(SPDF_MAGIC)
+        fh.write(struct.pack(SPDF_HEADER, 1, f.n, float(eps), tag, int(skip_levels),
+                             len(f.ops), f.nnz_factor))
+        put(fh, f.perm, np.int64)
+        for op in f.ops:
+            fh.write(struct.pack("<B", SPDF_KINDS.index(op.kind)))
+            put(fh, op.dofs, np.int64)
+            if op.kind == "G":
+                put(fh, op.w_dofs, np.int64)
+                put(fh, op.lower, np.float64)
+                put(fh, op.panel, np.float64)
+            elif op.kind == "D":
+                put(fh, op.lower, np.float64)
+            elif op.kind == "Q":
+                put(fh, op.q, np.float64)
+            else:
+                put(fh, op.w_dofs, np.int64)
+                put(fh, op.e_tilde, np.float64)
+
+
+# ---------------------------------------------------------------------------
+# Input generator of the BASELINE high-contrast configs (C3/C4 family), for
+# the CPU legs of bench.py: the reference arm must not load the product, so
+# its sample is built here.  Same construction as the package's
+# sparse.diffusion_fv / log_uniform_block_field (cell-centred finite volumes,
+# harmonic-mean faces, Dirichlet faces add the cell's own coefficient; the
+# field is drawn first, then b); tests/test_host.py pins the two bitwise.
+
+
+def fv_block_field_problem(shape, block, decades, seed):
+    """(n, row_ptr, col_idx, values, b) of -div(a grad u) with a piecewise
+    constant a = 10**U(-decades, decades) per block of block^d cells."""
+    rng = np.random.default_rng(seed)
+    nb = tuple(s // block for s in shape)
+    a = 10.0 ** rng.uniform(-decades, decades, size=nb)
+    for ax in range(len(shape)):
+        a = np.repeat(a, block, axis=ax)
+    n = a.size
+    idx = np.arange(n).reshape(shape)
+    diag = np.zeros(shape)
+    rows, cols, vals = [], [], []
+    for ax in range(a.ndim):
+        lo = [slice(None)] * a.ndim
+        hi = [slice(None)] * a.ndim
+        lo[ax] = slice(0, shape[ax] - 1)
+        hi[ax] = slice(1, shape[ax])
+        a1, a2 = a[tuple(lo)], a[tuple(hi)]
+        w = 2.0 * a1 * a2 / (a1 + a2)
+        diag[tuple(lo)] += w
+        diag[tuple(hi)] += w
+        i0, i1 = idx[tuple(lo)].ravel(), idx[tuple(hi)].ravel()
+        rows += [i0, i1]
+        cols += [i1, i0]
+        vals += [-w.ravel(), -w.ravel()]
+        first = [slice(None)] * a.ndim
+        last = [slice(None)] * a.ndim
+        first[ax] = slice(0, 1)
+        last[ax] = slice(shape[ax] - 1, shape[ax])
+        diag[tuple(first)] += a[tuple(first)]
+        diag[tuple(last)] += a[tuple(last)]
+    rows.append(np.arange(n))
+    cols.append(np.arange(n))
+    vals.append(diag.ravel())
+    m = sp.coo_matrix((np.concatenate(vals), (np.concatenate(rows), np.concatenate(cols))),
+                      shape=(n, n)).tocsr()
+    m.sort_indices()
+    b = rng.standard_normal(n)
+    return (n, m.indptr.astype(np.int64), m.indices.astype(np.int64),
+            m.data.astype(np.float64), b)

@@ -386,3 +386,71 @@ extern "C" int spand_trtri_tiles(int ntask, const int64_t* ops, const int32_t* m
   SPAND_CHECK_LAUNCH();
   return 0;
 }
+
+// ---------------------------------------------------------------------------
+// Trailing-matrix fingerprint (reference EliminationState.digest,
+// factorize.py:222-229): per block alive at a level end, an order-free hash
+// of its live window -- the sum over entries of splitmix64(bits(v) ^
+// position) mod 2^64, integer atomics, so the result does not depend on the
+// thread schedule.  Diagonal blocks hash their lower triangle only (the
+// stored triangle; the reference's diagonal blocks are symmetric).  Piece
+// rows (6 int64): {block ptr, i, j, first column, columns, record ptr};
+// records (5 int64): {i, j, live rows, live cols, hash}.
+namespace {
+__device__ __forceinline__ unsigned long long mix64(unsigned long long x) {
+  x += 0x9e3779b97f4a7c15ull;
+  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
+  x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
+  return x ^ (x >> 31);
+}
+
+__global__ void __launch_bounds__(kT)
+digest_kernel(const int64_t* __restrict__ rows, const int32_t* __restrict__ m0,
+              const int32_t* __restrict__ off) {
+  const int64_t* d = rows + 6 * (int64_t)blockIdx.x;
+  const double* blk = reinterpret_cast<const double*>(d[0]);
+  const int i = (int)d[1], j = (int)d[2];
+  const int c0 = (int)d[3], nc = (int)d[4];
+  unsigned long long* rec = reinterpret_cast<unsigned long long*>(d[5]);
+  const int ld = m0[i];
+  const int ri = off[i], cj = off[j];
+  const int lr = m0[i] - ri, lc = m0[j] - cj;
+  if (c0 == 0 && threadIdx.x == 0) {
+    rec[0] = (unsigned long long)i;
+    rec[1] = (unsigned long long)j;
+    rec[2] = (unsigned long long)(lr > 0 ? lr : 0);
+    rec[3] = (unsigned long long)(lc > 0 ? lc : 0);
+  }
+  const int cb = max(c0, cj), ce = min(c0 + nc, m0[j]);
+  unsigned long long h = 0;
+  if (lr > 0 && cb < ce) {
+    const int64_t total = (int64_t)lr * (ce - cb);
+    for (int64_t e = threadIdx.x; e < total; e += kT) {
+      const int r = (int)(e % lr), c = cb + (int)(e / lr) - cj;
+      if (i == j && r < c) continue;
+      const double v = blk[(int64_t)(ri + r) + (int64_t)(cj + c) * ld];
+      const unsigned long long pos = ((unsigned long long)r << 32) | (unsigned)c;
+      h += mix64((unsigned long long)__double_as_longlong(v) ^ mix64(pos));
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) h += __shfl_xor_sync(0xffffffffu, h, o);
+  __shared__ unsigned long long part[kT / 32];
+  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = h;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long t = 0;
+    for (int w = 0; w < kT / 32; ++w) t += part[w];
+    if (t) atomicAdd(rec + 4, t);
+  }
+}
+}  // namespace
+
+extern "C" int spand_digest_pieces(int npiece, const int64_t* rows, const int32_t* m0,
+                                   const int32_t* off, void* stream) {
+  if (npiece < 0) return -1;
+  if (npiece == 0) return 0;
+  digest_kernel<<<npiece, kT, 0, as_stream(stream)>>>(rows, m0, off);
+  SPAND_CHECK_LAUNCH();
+  return 0;
+}

@@ -21,6 +21,7 @@
 //        near-kernel extension (nearkernel.cu): 7 rescale(a=rows, x0=vmax)
 //        8 basis(a=nk rows, b=nbrs)  9 deflate(a, b, x0=grid, x1=vmax)
 //        10 qform(a=nk rows, x0=grid, x1=vmax)
+//        11 trailing-matrix digest pieces (a=rows of 6, count=pieces)
 // Offsets are in int64 units into the program array.
 #include <algorithm>
 #include <cstdint>
@@ -135,6 +136,20 @@ int spand_plan_set_nk(void* h, int k) {
   p->nk = k;
   p->layout();
   return 0;
+}
+
+// Trailing-matrix digests on (1) / off (0); out_base is the device address
+// of dig_records x {i, j, rows, cols, h} int64 records (zeroed by the
+// caller).  Returns the record count; counts[nlevels + 1] (may be null)
+// receives the first record index of each level.
+int64_t spand_plan_set_digest(void* h, int on, int64_t out_base, int64_t* counts) {
+  Plan* p = static_cast<Plan*>(h);
+  p->digest = on != 0;
+  p->dig_base = out_base;
+  if (!p->digest) return 0;
+  if (p->dig_first.empty()) p->prepare_digest();
+  if (counts) std::memcpy(counts, p->dig_first.data(), p->dig_first.size() * sizeof(int64_t));
+  return p->dig_records;
 }
 
 // cluster dofs (original numbering) concatenated in id order, dptr[ncl+1]

@@ -120,6 +120,8 @@ struct Plan {
   std::vector<int32_t> depth;
   std::vector<int64_t> dofs, dptr;   // cluster dofs (original numbering), concatenated
   std::vector<int32_t> bi, bj;
+  std::vector<int32_t> bcreated;   // level at which each block came to exist (levels + 1: A's)
+  int cur_level = 0;
   BlockMap bid;
   std::vector<Level> lv;
   std::vector<int> fin, fin_blocks;
@@ -139,12 +141,43 @@ struct Plan {
   static constexpr int64_t kNkHead = 19;   // nearkernel.cu kWsHead
   int64_t nk_ws(int64_t mc) const { return nk ? kNkHead + 2 * mc * nk + mc * mc : 0; }
 
+  // Trailing-matrix fingerprints (reference EliminationState.digest,
+  // factorize.py:222-229, recorded per level at :347).  When on, every
+  // level ends with a launch (type 11) that hashes the live window of each
+  // block alive at that point into a record {i, j, rows, cols, h}; the host
+  // folds the records of a level, in key order, into a sha256.  A block
+  // (i, j) is alive at the end of level l iff it exists by then (created at
+  // level >= l) and neither cluster has been eliminated (depth < l).
+  bool digest = false;
+  int64_t dig_base = 0;                       // device address of the records
+  std::vector<std::vector<int>> dig_blocks;   // per level (lv order), key order
+  std::vector<int64_t> dig_first;             // first record index per level
+  int64_t dig_records = 0;
+  void prepare_digest() {
+    dig_blocks.assign(lv.size(), {});
+    for (size_t b = 0; b < bi.size(); ++b) {
+      const int death = std::max(depth[bi[b]], depth[bj[b]]);
+      for (int l = std::min(bcreated[b], levels); l > death && l >= 1; --l)
+        dig_blocks[(size_t)(levels - l)].push_back((int)b);
+    }
+    dig_first.assign(lv.size() + 1, 0);
+    for (size_t k = 0; k < lv.size(); ++k) {
+      auto& v = dig_blocks[k];
+      std::sort(v.begin(), v.end(), [&](int x, int y) {
+        return key(bi[x], bj[x]) < key(bi[y], bj[y]);
+      });
+      dig_first[k + 1] = dig_first[k] + (int64_t)v.size();
+    }
+    dig_records = dig_first[lv.size()];
+  }
+
   int64_t key(int i, int j) const { return (int64_t)i * ncl + j; }
   int block(int i, int j) const { return bid.find(key(i, j)); }
   int new_block(int i, int j, std::vector<std::vector<int>>& cb) {
     const int b = (int)bi.size();
     bi.push_back(i);
     bj.push_back(j);
+    bcreated.push_back(cur_level);
     bid.put(key(i, j), b);
     cb[i].push_back(b);
     if (j != i) cb[j].push_back(b);
@@ -172,6 +205,8 @@ struct Plan {
     bid.reserve((size_t)npairs * 4);
     bi.reserve((size_t)npairs * 2);
     bj.reserve((size_t)npairs * 2);
+    bcreated.reserve((size_t)npairs * 2);
+    cur_level = levels + 1;
     for (int64_t t = 0; t < npairs; ++t) {
       const int i = (int)(pairs[t] / ncl), j = (int)(pairs[t] % ncl);
       new_block(i, j, cb);
@@ -206,6 +241,7 @@ struct Plan {
 #endif
       Level L;
       L.level = level;
+      cur_level = level;
       for (int c = 0; c < ncl; ++c)
         if (alive[c] && depth[c] == level) L.interiors.push_back(c);
       L.inb_ptr.assign(1, 0);
@@ -696,6 +732,25 @@ struct Plan {
     return false;
   }
   void emit_level(Level& L) {
+    emit_level_core(L);
+    if (digest) emit_digest((size_t)(levels - L.level));
+  }
+  // pieces {block ptr, i, j, first column, columns, record address}, at
+  // most 64K stored entries each (digest_kernel in dense_small.cu)
+  void emit_digest(size_t k) {
+    std::vector<int64_t> rows;
+    int64_t rec = dig_first[k];
+    for (int b : dig_blocks[k]) {
+      const int i = bi[b], j = bj[b];
+      const int64_t cpp = std::max<int64_t>(1, 65536 / std::max<int64_t>(m0[i], 1));
+      const int64_t addr = dig_base + 40 * rec++;
+      for (int64_t c0 = 0; c0 < std::max<int64_t>(m0[j], 1); c0 += cpp)
+        rows.insert(rows.end(), {pool_base + 8 * boff[b], i, j, c0,
+                                 std::min<int64_t>(cpp, m0[j] - c0), addr});
+    }
+    if (!rows.empty()) launch(11, (int64_t)rows.size() / 6, push(rows));
+  }
+  void emit_level_core(Level& L) {
     {
       if (!L.interiors.empty()) {
         std::vector<std::vector<int64_t>> pops;

@@ -1579,7 +1579,23 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
 #ifndef SPAND_QB_MMIN
 #define SPAND_QB_MMIN 64
 #endif
-  if (k_stop >= 64 && m >= SPAND_QB_MMIN) qform_blocked(k_stop);
+  // k_c: first pivot below eps * r11 (dense.py:181-182)
+  // (parallel first-index search: a sequential scan of k_stop dependent
+  // L2 loads cost ~1.5 ms on the largest panels)
+  if (tid == 0) sh.nfrz_tmp = k_stop;
+  __syncthreads();
+  for (int t = tid; t < k_stop; t += kT)
+    if (__ldcg(piv + t) < eps * r11) {
+      atomicMin(&sh.nfrz_tmp, t);
+      break;
+    }
+  __syncthreads();
+  const int k_c = sh.nfrz_tmp;
+  // the formation method depends on k_c, not k_stop, so the coarse columns
+  // of Q -- and the coarse rows Q_c^T a below -- are bit for bit the same in
+  // every scheme (k_c is scheme-independent; k_stop is not): the trailing
+  // matrix is then identical across schemes (test_factorize.py:104-113)
+  if (k_c >= 64 && m >= SPAND_QB_MMIN) qform_blocked(k_stop);
   else if (m <= 8 * kT) qform_batched<4, 8>(Q, V, taus, m, k_stop, rank, G, sh);
   else if (m <= 16 * kT) qform_batched<2, 16>(Q, V, taus, m, k_stop, rank, G, sh);
   else {
@@ -1606,18 +1622,6 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
   }
   __syncthreads();
   TL(tq);
-  // k_c: first pivot below eps * r11 (dense.py:181-182)
-  // (parallel first-index search: a sequential scan of k_stop dependent
-  // L2 loads cost ~1.5 ms on the largest panels)
-  if (tid == 0) sh.nfrz_tmp = k_stop;
-  __syncthreads();
-  for (int t = tid; t < k_stop; t += kT)
-    if (__ldcg(piv + t) < eps * r11) {
-      atomicMin(&sh.nfrz_tmp, t);
-      break;
-    }
-  __syncthreads();
-  const int k_c = sh.nfrz_tmp;
   const int n_fine = m - k_c;
   int n_corr = 0;  // rows of e_tilde kept in the dead slots
   if (scheme == 1 || keep_fine) n_corr = n_fine;
@@ -1663,20 +1667,26 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
   }
   group_barrier(ctr, G, gen, 200000, events + 12 * slot + 9);   // Q and W complete
   TL(trs);
-  if (nf > 0) {
-    const int T = k_c + n_corr;
+  // R rows t < T of Q^T a for a list of columns (a = ORIGINAL column) on
+  // the tensor cores (DMMA).  to_w = false: frozen columns, a restored in W,
+  // rows written straight to the pool in the write-back slot order (slot =
+  // t < k_c ? n_fine + t : t - k_c).  to_w = true: a read from the pool (not
+  // yet written back), rows written into W (replacing the in-loop values).
+  // Element (t, c) accumulates over the rows in the same order in both
+  // modes, whatever T and the column's tile.
+  auto qt_a = [&](const int32_t* lst, const int cnt, const int T, const bool to_w) {
     // two cp.async stages of A (Q^T rows) and B (original columns) tiles
     double (*As)[16][kLDS] = reinterpret_cast<double (*)[16][kLDS]>(vsh);               // [2][16][kLDS]
     double (*Bs)[16][kLDS] = reinterpret_cast<double (*)[16][kLDS]>(vsh + 2 * 16 * kLDS);  // [2][16][kLDS]
     double (*Cs)[65] = reinterpret_cast<double (*)[65]>(vsh);                 // [64][65] (epilogue)
     const int wm = warp >> 2, wn = warp & 3;
-    for (int ct = 0; ct < nf; ct += 64) {
+    for (int ct = 0; ct < cnt; ct += 64) {
       __syncthreads();
       if (tid < 64) {
-        if (ct + tid < nf) {
+        if (ct + tid < cnt) {
           double* base;
           int64_t stride;
-          const int c = flist[rank + G * (ct + tid)];
+          const int c = lst[rank + G * (ct + tid)];
           pool_col(c, base, stride);
           sh.cbase[tid] = base;
           sh.cstride[tid] = stride;
@@ -1702,7 +1712,10 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
             cp_async8(&As[st][kk][cl], oka ? Q + (int64_t)i + (int64_t)(rt + cl) * m : Q, oka);
             const int fc = sh.fcol[cl];
             const bool okb = i < m && fc >= 0;
-            cp_async8(&Bs[st][kk][cl], okb ? W + (int64_t)i + (int64_t)fc * m : W, okb);
+            const double* bsrc =
+                !okb ? W : (to_w ? sh.cbase[cl] + (int64_t)i * sh.cstride[cl]
+                                 : W + (int64_t)i + (int64_t)fc * m);
+            cp_async8(&Bs[st][kk][cl], bsrc, okb);
           }
           cp_commit();
         };
@@ -1741,14 +1754,39 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
         for (int e = tid; e < 64 * 64; e += kT) {
           const int r = e & 63, cl = e >> 6;
           const int t = rt + r;
-          if (t < T && ct + cl < nf) {
-            const int sl = t < k_c ? n_fine + t : t - k_c;
-            sh.cbase[cl][(int64_t)sl * sh.cstride[cl]] = Cs[cl][r];
+          if (t < T && ct + cl < cnt) {
+            if (to_w) {
+              W[(int64_t)t + (int64_t)sh.fcol[cl] * m] = Cs[cl][r];
+            } else {
+              const int sl = t < k_c ? n_fine + t : t - k_c;
+              sh.cbase[cl][(int64_t)sl * sh.cstride[cl]] = Cs[cl][r];
+            }
           }
         }
       }
     }
+  };
+  if (nf > 0) qt_a(flist, nf, k_c + n_corr, false);
+  // coarse rows of the other non-coarse-pivot columns (still active, or
+  // pivoted at a step >= k_c by the superfine scheme): Q_c^T a as well, so
+  // every scheme forms R rows < k_c of every column the same way (a column
+  // is frozen, cold, hot or a band pivot depending on stop_tol)
+  {
+    int32_t* l2 = flist + 4 * ncap;   // the loop's hot lists are free now
+    if (tid == 0) sh.nact = 0;
+    __syncthreads();
+    for (int c = rank + G * tid; c < n; c += G * kT) {
+      const int dc = __ldcg(done + c);
+      if (dc == 0 || (dc == 1 && __ldcg(pos + c) >= k_c))
+        l2[rank + G * atomicAdd(&sh.nact, 1)] = c;
+    }
+    __syncthreads();
+    const int n2 = sh.nact;
+    if (n2 > 0 && k_c > 0) qt_a(l2, n2, k_c, true);
   }
+  // the write-back below covers contiguous column ranges, the products
+  // above the interleaved ownership
+  group_barrier(ctr, G, gen, 300000, events + 12 * slot + 9);
   TL(tg);
   // ---- write back (non-frozen columns): new slot s < n_fine <- R row
   //      k_c + s (only s < n_corr are read later); slot n_fine + t <- R row t

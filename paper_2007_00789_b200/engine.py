@@ -58,7 +58,7 @@ class NativePlan:
     ``meta`` decodes the scheduler's structure export into per-level
     records used by ``collect`` (operator assembly on the host)."""
 
-    def __init__(self, a, h, skip_levels, cap_override=0, nk=0):
+    def __init__(self, a, h, skip_levels, cap_override=0, nk=0, digest=False):
         import ctypes
         t0 = time.perf_counter()
         lib = _lib.load()
@@ -107,6 +107,14 @@ class NativePlan:
         if nk:
             if lib.spand_plan_set_nk(self.h, int(nk)) != 0:
                 raise ValueError(f"at most 16 near-kernel vectors, got {nk}")
+        self.digest_first = None
+        if digest:
+            lib.spand_plan_set_digest.restype = ctypes.c_int64
+            lib.spand_plan_set_digest.argtypes = [ctypes.c_void_p, ctypes.c_int,
+                                                  ctypes.c_int64, ctypes.c_void_p]
+            first = np.zeros(int(h.levels) + 1, dtype=np.int64)
+            lib.spand_plan_set_digest(self.h, 1, 0, vp(first))
+            self.digest_first = first
         self.sizes()
         self._decode_meta()
         self.seconds = time.perf_counter() - t0
@@ -195,7 +203,7 @@ class NativePlan:
 
 class Engine:
     def __init__(self, a, h, eps, scheme, skip_levels, near_kernel=None,
-                 collect_local_errors=False):
+                 collect_local_errors=False, digest=False):
         self.t = require_cuda()
         self.a, self.h = a, h
         self.local_errors = bool(collect_local_errors)
@@ -203,7 +211,8 @@ class Engine:
         self.nk = near_kernel      # n x k host array (extension) or None
         self.sym = NativePlan(a, h, skip_levels,
                               int(_os.environ.get("SPAND_RRQR_CAP", "0")),
-                              0 if near_kernel is None else near_kernel.shape[1])
+                              0 if near_kernel is None else near_kernel.shape[1],
+                              digest=digest)
         self.timings = {"symbolic_s": self.sym.seconds}
 
     # -------------------------------------------------------------- numeric
@@ -237,6 +246,12 @@ class Engine:
         lib.spand_plan_emit_begin.argtypes = [ctypes.c_void_p] + [ctypes.c_int64] * 4
         lib.spand_plan_emit_next.argtypes = [ctypes.c_void_p, ctypes.c_void_p]
         lib.spand_plan_chunk.argtypes = [ctypes.c_void_p] * 3
+        if sym.digest_first is not None:
+            # trailing-matrix digest records {i, j, rows, cols, hash} per
+            # (level, alive block), written by the type-11 launches
+            nrec = int(sym.digest_first[-1])
+            self.digest_rec = t.zeros(max(nrec, 1) * 5, dtype=t.int64, device=d)
+            lib.spand_plan_set_digest(sym.h, 1, self.digest_rec.data_ptr(), None)
         lib.spand_plan_emit_begin(sym.h, pb, fb, temp.data_ptr(), ctr.data_ptr())
         # the next level is emitted on a helper thread (ctypes releases the
         # GIL) while this one uploads and launches the current level
@@ -350,6 +365,8 @@ class Engine:
                     _lib.call("spand_nk_deflate", cnt, x0, P(ao), P(bo), gm0, goff, x1, st)
                 else:
                     _lib.call("spand_nk_qform", cnt, x0, P(ao), ctypes.c_void_p(evb), x1, st)
+            elif typ == 11:
+                _lib.call("spand_digest_pieces", cnt, P(ao), gm0, goff, st)
             elif typ == 6:
                 _lib.call("spand_assemble_final", cnt, P(ao), x0, P(bo), gm0, goff,
                           x1, ctypes.c_void_p(fb + 8 * x2), st)
@@ -442,11 +459,10 @@ class Engine:
             errs = self._local_errors(col)
             for q, ent in enumerate(entries):
                 ent["local_error"] = errs[q]
+        digests = self._digests()
         for li, (lvl, nint, ndofs, skipped) in enumerate(col.lsum.tolist()):
             faces = by_level.get(li, [])
-            digest = hashlib.sha256(repr([(f["cluster"], f["size_before"],
-                                           f["size_after"], f["rank_f2"])
-                                          for f in faces]).encode()).hexdigest()
+            digest = digests[li] if digests is not None else None
             diags.append({"level": lvl, "interior_clusters": nint,
                           "interior_dofs": ndofs, "skipped": bool(skipped),
                           "interfaces": [{k: f[k] for k in ("cluster", "size_before",
@@ -461,6 +477,28 @@ class Engine:
                             collect_apply_start_s=t2 - t1, collect_diag_s=t3 - t2,
                             collect_count_s=t4 - t3)
         return ops, col.perm, {"levels": diags, "final_block": col.final_total}, nnz
+
+    def _digests(self):
+        """Per-level trailing-matrix fingerprints (reference
+        EliminationState.digest, factorize.py:222-229): sha256 over the
+        level's alive blocks in key order of (i, j, rows, cols, h), h the
+        device hash of the block's live window (dense_small.cu
+        digest_kernel).  Identical trailing matrices -- e.g. across the
+        three schemes, which differ only in their correction operators --
+        give identical digests; the bytes differ from the reference's
+        sha256 of the raw blocks (a different fingerprint of the same
+        state)."""
+        first = self.sym.digest_first
+        if first is None:
+            return None
+        rec = self.digest_rec.cpu().numpy().reshape(-1, 5)
+        out = []
+        for k in range(len(first) - 1):
+            r = rec[first[k]:first[k + 1]]
+            r = r[(r[:, 2] > 0) & (r[:, 3] > 0)]
+            out.append(hashlib.sha256(np.ascontiguousarray(r, dtype="<i8").tobytes())
+                       .hexdigest())
+        return out
 
     def _local_errors(self, col):
         """Spectral norm of the dropped term of every sparsification
@@ -634,10 +672,11 @@ def ctypes_ptr(addr):
 
 
 def run_factorization(a, h, eps, scheme, skip_levels, collect_local_errors=False,
-                      near_kernel=None):
+                      near_kernel=None, digest=False):
     from .factorize import Factorization
     t0 = time.perf_counter()
-    eng = Engine(a, h, eps, scheme, skip_levels, near_kernel, collect_local_errors)
+    eng = Engine(a, h, eps, scheme, skip_levels, near_kernel, collect_local_errors,
+                 digest=digest)
     eng.run()
     ops, perm, diag, nnz = eng.collect()
     eng.timings["total_s"] = time.perf_counter() - t0

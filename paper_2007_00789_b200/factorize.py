@@ -91,7 +91,7 @@ def memory_ratio(factor, a):
 
 
 def factorize(a, hierarchy, eps, scheme, skip_levels=4,
-              collect_local_errors=False, near_kernel=None):
+              collect_local_errors=False, near_kernel=None, digest=True):
     """Factor a sparse SPD matrix over a partition hierarchy on the B200.
 
     Same contract as the reference (`factorize.py:285-366`): levels from the
@@ -127,7 +127,7 @@ def factorize(a, hierarchy, eps, scheme, skip_levels=4,
             nk = None
     from .engine import run_factorization
     return run_factorization(a, hierarchy, float(eps), scheme, int(skip_levels),
-                             collect_local_errors, near_kernel=nk)
+                             collect_local_errors, near_kernel=nk, digest=bool(digest))
 
 
 # ---------------------------------------------------------------------------

@@ -70,18 +70,19 @@ class FastPlan:
         return xd
 
 _COMPILER = ThreadPoolExecutor(1, thread_name_prefix="spand-apply-image")
-_PINNED = [None]
 
 
 def _pinned_image(n):
-    """Grow-only pinned int64 buffer for the apply images (compile thread)."""
+    """Pinned int64 staging buffer of ONE plan's apply image.
+
+    Each plan owns its buffer until its upload has been issued: a factor
+    whose first apply comes after another factorization must upload its
+    own rows (absolute pointers into its own pool / factor buffer), never
+    the image of a later factor.  torch's caching host allocator recycles
+    the block once the plan is gone and the non-blocking upload that read
+    it has completed, so repeated factorizations do not re-pin memory."""
     t = require_cuda()
-    buf = _PINNED[0]
-    if buf is None or buf.numel() < n:
-        buf = t.empty(max(n, 2 * (buf.numel() if buf is not None else 0)), dtype=t.int64,
-                      pin_memory=True)
-        _PINNED[0] = buf
-    return buf[:n]
+    return t.empty(n, dtype=t.int64, pin_memory=True)
 
 
 class NativeApplyPlan(FastPlan):
@@ -126,9 +127,7 @@ class NativeApplyPlan(FastPlan):
                                "the packed work-item limits")
         t1 = time.perf_counter()
         ilen, nfw, nbw, scratch_len = (int(x) for x in out)
-        # the image is written straight into pinned memory (reused between
-        # factorizations: the previous plan's upload completed before the
-        # next factorization's collect, which synchronises)
+        # the image is written straight into this plan's pinned buffer
         pinned = _pinned_image(max(ilen, 1))
         image = pinned.numpy()
         ph = np.zeros((nfw + nbw, 10), dtype=np.int64)
@@ -153,7 +152,7 @@ class NativeApplyPlan(FastPlan):
         self.image = t.empty(pinned.shape, dtype=t.int64, device=dev())
         self.image.copy_(pinned, non_blocking=True)
         image = pinned.numpy()
-        self.image_host = image   # (overwritten by the next factorization's image)
+        self.image_host = image
         base = self.image.data_ptr()
         self.scratch = t.empty(max(scratch_len, 1), dtype=t.float64, device=dev())
         rows = []

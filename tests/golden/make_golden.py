@@ -19,6 +19,10 @@ Per run we store: cluster structure (full arrays for small cases, sizes +
 sha256 for the big ones), per-level diagnostics (interface ranks, rank_f2),
 the factor's perm, per-op payload sha256 and Frobenius norms, nnz_factor,
 n_cg, the residual history and timings (1 BLAS thread, this container).
+Every run also stores, per operator, ||P||_F, four bilinear sketches and
+nnz of each payload (``op_fro``/``op_sk``/``op_nnz`` in the .npz, see
+tests/golden_cases.py), apply_m(b) and the PCG solution x, so the
+full-size configs are checked per block without storing their factors.
 """
 
 import hashlib
@@ -37,6 +41,7 @@ import spdkit  # noqa: E402  (the reference, via PYTHONPATH)
 from spdkit.schemes import OpKind  # noqa: E402
 
 from paper_2007_00789_b200 import sparse as gen  # noqa: E402
+from tests.golden_cases import op_tables  # noqa: E402
 
 
 def sha(arr):
@@ -90,7 +95,8 @@ def to_ref_hierarchy(h):
 
 
 def run_case(tag, a, b, levels, eps, scheme, skip_levels=4, tol=1e-12,
-             full=True, store_factor=False, store_ops=True, hierarchy=None):
+             full=True, store_factor=False, store_ops=True, hierarchy=None,
+             sketches=True):
     ra = to_ref(a)
     t0 = time.perf_counter()
     h = (spdkit.build_hierarchy(ra, levels) if hierarchy is None
@@ -138,11 +144,18 @@ def run_case(tag, a, b, levels, eps, scheme, skip_levels=4, tol=1e-12,
     if store_ops:
         rec["ops"] = [op_record(op) for op in f.ops]
     arrays = dict(harr)
+    if sketches:
+        # per-operator ||P||_F, bilinear sketches and nnz of every payload
+        # (tests/golden_cases.py:op_tables): full-size per-block parity
+        fro, sk, ska, nnz = op_tables(f.ops)
+        arrays["op_fro"], arrays["op_sk"], arrays["op_nnz"] = fro, sk, nnz
+        arrays["op_ska"] = ska
+        rec["digests"] = [lv["digest"] for lv in f.diagnostics["levels"]]
     arrays["perm"] = np.asarray(f.perm, dtype=np.int32 if a.n < 2**31 else np.int64)
     arrays["b"] = np.asarray(b)
-    if z is not None and full:
+    if z is not None:
         arrays["apply_m_b"] = z
-        arrays["x"] = x
+    arrays["x"] = x
     base = os.path.join(HERE, tag)
     with open(base + ".json", "w") as fh:
         json.dump(rec, fh, indent=1)

@@ -54,7 +54,7 @@ def test_header_symbols_are_typed_or_handle_based():
     handle_based = {"spand_plan_create", "spand_plan_destroy", "spand_plan_set_dofs",
                     "spand_plan_emit_begin", "spand_plan_emit_next", "spand_plan_chunk",
                     "spand_plan_pairs", "spand_plan_scatter", "spand_csr_check",
-                    "spand_plan_set_group_weight",
+                    "spand_plan_set_group_weight", "spand_plan_set_digest",
                     "spand_collect_create", "spand_collect_destroy", "spand_collect_sizes",
                     "spand_collect_get", "spand_collect_apply", "spand_collect_apply_get",
                     "spand_collect_fine", "spand_collect_stats"}
@@ -280,3 +280,19 @@ def test_sparse_sym_matrix_validation_errors():
         mk([0, 2, 4, 5], [0, 1, 0, 1, 2], [2.0, -1.0, -1.0, 2.0, -1.0])  # sign
     with pytest.raises(NonpositiveDiagonal):                           # missing diagonal
         sp.SparseSymMatrix(2, np.array([0, 1, 2]), np.array([1, 0]), np.array([1.0, 1.0]))
+
+
+@pytest.mark.parametrize("shape,block,seed", [((24, 24, 24), 8, 3), ((16, 16), 4, 2)])
+def test_oracle_generator_matches_package(shape, block, seed):
+    """bench.py's CPU legs build their sample with the oracle's generator
+    (they must not load the product); it is the package's construction bit
+    for bit."""
+    from oracle import spand_oracle as orc
+    from paper_2007_00789_b200 import sparse as S
+    n, rp, ci, va, b = orc.fv_block_field_problem(shape, block, 3.0, seed)
+    rng = np.random.default_rng(seed)
+    a = S.diffusion_fv(S.log_uniform_block_field(shape, block, 3.0, rng))
+    assert a.n == n
+    assert np.array_equal(a.row_ptr, rp) and np.array_equal(a.col_idx, ci)
+    assert np.array_equal(a.values, va)
+    assert np.array_equal(rng.standard_normal(n), b)
