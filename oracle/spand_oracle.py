@@ -893,3 +893,75 @@ def fv_block_field_problem(shape, block, decades, seed):
     b = rng.standard_normal(n)
     return (n, m.indptr.astype(np.int64), m.indices.astype(np.int64),
             m.data.astype(np.float64), b)
+
+
+# ---------------------------------------------------------------------------
+# Matrix Market reader  (sparse.py:98-160), the checker for csrc/mmio.cpp
+
+
+class MMError(ValueError):
+    """kind: 'ParseError' | 'NotSymmetricReal' | 'AsymmetricValues'."""
+
+    def __init__(self, kind, msg):
+        super().__init__(msg)
+        self.kind = kind
+
+
+def mm_read(path):
+    """-> (n, row_ptr, col_idx, values) in CSR (both triangles, sorted)."""
+    with open(path, "r") as fh:
+        head = fh.readline()
+        tok = head.strip().split()
+        if len(tok) != 5 or tok[0] != "%%MatrixMarket":
+            raise MMError("ParseError", f"bad Matrix Market header: {head.strip()!r}")
+        if tok[1].lower() != "matrix" or tok[2].lower() != "coordinate":
+            raise MMError("ParseError", f"unsupported object/format: {head.strip()!r}")
+        if tok[3].lower() != "real" or tok[4].lower() != "symmetric":
+            raise MMError("NotSymmetricReal", f"only real symmetric matrices are "
+                          f"supported, got {tok[3]} {tok[4]}")
+        line = fh.readline()
+        while line and (line.startswith("%") or not line.strip()):
+            line = fh.readline()
+        try:
+            m, n, nnz = (int(t) for t in line.split())
+        except ValueError:
+            raise MMError("ParseError", f"bad size line: {line.strip()!r}") from None
+        if m != n:
+            raise MMError("NotSymmetricReal", "matrix must be square")
+        seen = {}
+        for _ in range(nnz):
+            line = fh.readline()
+            if not line:
+                raise MMError("ParseError", "file ends before declared entry count")
+            t = line.split()
+            if len(t) != 3:
+                raise MMError("ParseError", f"bad entry line: {line.strip()!r}")
+            try:
+                i, j, v = int(t[0]), int(t[1]), float(t[2])
+            except ValueError:
+                raise MMError("ParseError", f"bad entry line: {line.strip()!r}") from None
+            if not (1 <= i <= n and 1 <= j <= n):
+                raise MMError("ParseError", f"index out of range: ({i}, {j})")
+            if (i - 1, j - 1) in seen:
+                raise MMError("ParseError", f"duplicate entry ({i}, {j})")
+            mir = (j - 1, i - 1)
+            if i != j and mir in seen and seen[mir] != v:
+                raise MMError("AsymmetricValues", f"entries ({j}, {i}) and ({i}, {j}) "
+                              f"disagree: {seen[mir]} vs {v}")
+            seen[(i - 1, j - 1)] = v
+    rows, cols, vals = [], [], []
+    for (i, j), v in seen.items():
+        rows.append(i)
+        cols.append(j)
+        vals.append(v)
+        if i != j and (j, i) not in seen:
+            rows.append(j)
+            cols.append(i)
+            vals.append(v)
+    rows = np.asarray(rows, dtype=np.int64)
+    cols = np.asarray(cols, dtype=np.int64)
+    vals = np.asarray(vals, dtype=np.float64)
+    order = np.lexsort((cols, rows))
+    rp = np.zeros(n + 1, dtype=np.int64)
+    np.cumsum(np.bincount(rows, minlength=n), out=rp[1:])
+    return n, rp, cols[order], vals[order]

@@ -25,6 +25,7 @@ from .errors import (
     NotSPD,
     NotSymmetricReal,
     NumericalError,
+    PanelTooLarge,
     ParseError,
     RhoNotOne,
     SingularTriangular,
@@ -39,7 +40,7 @@ from .factorize import (
     memory_ratio,
     save_factor,
 )
-from .krylov import SolveReport, cg_bound_rate, default_maxit, pcg
+from .krylov import SolveReport, cg_bound_rate, default_maxit, pcg, pcg_multi
 from .partition import Cluster, PartitionHierarchy, build_hierarchy, default_levels
 from .schemes import (
     OpKind,

@@ -24,7 +24,32 @@ namespace {
 
 struct Graph {
   std::vector<int64_t> ptr, idx;  // off-diagonal adjacency, sorted rows
+  bool sym = true;                 // stored pattern symmetric (the usual case)
 };
+
+// (lp, li) with every edge also reversed: the reference's components and
+// BFS run on the undirected graph (connected_components / dijkstra with
+// directed=False, partition.py:172-191) while the separator carving follows
+// the stored rows (:211-224); they differ only for an unsymmetric pattern
+// (a stored zero whose mirror is not stored, accepted by the validation)
+static void undirected(const std::vector<int64_t>& lp, const std::vector<int64_t>& li,
+                       std::vector<int64_t>& up, std::vector<int64_t>& ui) {
+  const int64_t nv = (int64_t)lp.size() - 1;
+  up.assign(nv + 1, 0);
+  for (int64_t u = 0; u < nv; ++u)
+    for (int64_t e = lp[u]; e < lp[u + 1]; ++e) {
+      ++up[u + 1];
+      ++up[li[e] + 1];
+    }
+  for (int64_t u = 0; u < nv; ++u) up[u + 1] += up[u];
+  ui.resize(up[nv]);
+  std::vector<int64_t> fill(up.begin(), up.end() - 1);
+  for (int64_t u = 0; u < nv; ++u)
+    for (int64_t e = lp[u]; e < lp[u + 1]; ++e) {
+      ui[fill[u]++] = li[e];
+      ui[fill[li[e]]++] = u;
+    }
+}
 
 struct Splitter {
   const Graph& g;
@@ -80,8 +105,11 @@ struct Splitter {
       p1 = verts;
       return;
     }
-    std::vector<int64_t> lp, li;
+    std::vector<int64_t> lp, li, ulp, uli;
     extract(verts, lp, li);
+    if (!g.sym) undirected(lp, li, ulp, uli);
+    const std::vector<int64_t>& gp = g.sym ? lp : ulp;
+    const std::vector<int64_t>& gi = g.sym ? li : uli;
     // connected components, labels in order of smallest member
     std::vector<int64_t> label(nv, -1);
     int64_t ncomp = 0;
@@ -94,10 +122,10 @@ struct Splitter {
         while (!st.empty()) {
           const int64_t u = st.back();
           st.pop_back();
-          for (int64_t e = lp[u]; e < lp[u + 1]; ++e)
-            if (label[li[e]] < 0) {
-              label[li[e]] = ncomp;
-              st.push_back(li[e]);
+          for (int64_t e = gp[u]; e < gp[u + 1]; ++e)
+            if (label[gi[e]] < 0) {
+              label[gi[e]] = ncomp;
+              st.push_back(gi[e]);
             }
         }
         ++ncomp;
@@ -124,11 +152,11 @@ struct Splitter {
       return;
     }
     std::vector<int64_t> d0, dist;
-    bfs(lp, li, 0, d0);
+    bfs(gp, gi, 0, d0);
     const int64_t far = *std::max_element(d0.begin(), d0.end());
     int64_t seed = 0;
     while (d0[seed] != far) ++seed;
-    bfs(lp, li, seed, dist);
+    bfs(gp, gi, seed, dist);
     const int64_t nlev = *std::max_element(dist.begin(), dist.end()) + 1;
     if (nlev == 1) {
       sep = verts;
@@ -247,6 +275,14 @@ int spand_nd_partition(int64_t n, const int64_t* row_ptr, const int64_t* col_idx
   for (int64_t r = 0, k = 0; r < n; ++r)
     for (int64_t e = row_ptr[r]; e < row_ptr[r + 1]; ++e)
       if (col_idx[e] != r) g.idx[k++] = col_idx[e];
+  for (int64_t r = 0; r < n && g.sym; ++r)
+    for (int64_t e = g.ptr[r]; e < g.ptr[r + 1]; ++e) {
+      const int64_t c = g.idx[e];
+      if (!std::binary_search(g.idx.begin() + g.ptr[c], g.idx.begin() + g.ptr[c + 1], r)) {
+        g.sym = false;
+        break;
+      }
+    }
   Builder b(g, n, levels);
   std::vector<int64_t> all(n);
   for (int64_t i = 0; i < n; ++i) all[i] = i;

@@ -32,7 +32,9 @@
 namespace {
 constexpr int kT = 256;
 constexpr int kWarps = kT / 32;
-constexpr int kMaxM = 6144;  // v in shared memory
+// v (the reflector) lives in shared memory: up to 24576 rows (192 KB; a
+// wave holding such a panel runs one CTA per SM -- spand_rrqr_capacity)
+constexpr int kMaxM = 24576;
 
 // panel row (16 int64):
 //  0 p        1 nbr_begin  2 nbr_end   3 W (double*, temp, >= m*n)
@@ -580,6 +582,11 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
   int32_t* perm = iaux;
   int32_t* pos = iaux + ncap;
   int32_t* done = iaux + 2 * ncap;   // 0 active, 1 pivoted, 2 frozen
+  // superfine only: columns whose coarse rows (R rows < k_c) the first-order
+  // run of the same panel -- which stops at k_c -- forms as Q_c^T a (it froze
+  // them, or they were cold when it stopped); formed the same way here, so
+  // the trailing matrix is bit for bit the same in every scheme
+  int32_t* fofl = flist + 24 * ncap;
 
   const int c0 = (int)(((int64_t)n * rank) / G), c1 = (int)(((int64_t)n * (rank + 1)) / G);
   const int q0 = (int)(((int64_t)m * rank) / G), q1 = (int)(((int64_t)m * (rank + 1)) / G);
@@ -673,6 +680,7 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
       ref[c] = s;
       pos[c] = c;
       done[c] = 0;
+      fofl[c] = 0;
       if (better(s, c, bv, bp)) {
         bv = s;
         bp = c;
@@ -722,6 +730,8 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
   const double stop_tol = (scheme == 2) ? eps * eps : eps;
   double r11 = 0.0, eta_last = 0.0;
   double thr2 = 0.0;   // 0.25 (stop_tol r11)^2
+  double thr2_fo = 0.0;   // the first-order scheme's freeze threshold 0.25 (eps r11)^2
+  bool fo_track = scheme == 2;   // until k_c: mirror the first-order freezes
   int k = 0;
 #ifdef SPAND_RRQR_PHASES
   long long ph_t[8] = {0, 0, 0, 0, 0, 0, 0, 0};
@@ -1234,10 +1244,13 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
       for (int u = tid; u < nh + ncd; u += kT) {
         const int c = u < nh ? hot_in[rank + G * u] : coldl[rank + G * (u - nh)];
         if (done[c]) continue;
-        if (cur[c] < thr2) {
+        if (fo_track && cur[c] < thr2_fo) fofl[c] = 1;
+        if (cur[c] < thr2 && (fo_track || scheme != 2 || fofl[c])) {
           done[c] = 2;
           atomicMax(&sh.fmax, (unsigned long long)__double_as_longlong(cur[c]));
-        } else if (cur[c] >= tau_hot) {
+          continue;
+        }
+        if (cur[c] >= tau_hot) {
           tmpl[rank + G * atomicAdd(&sh.nact, 1)] = c;
         } else {
           cold_out[rank + G * atomicAdd(&sh.ncold, 1)] = c;
@@ -1388,6 +1401,14 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
       r11 = eta;
       if (r11 == 0.0) break;
       thr2 = 0.25 * (stop_tol * r11) * (stop_tol * r11);
+      thr2_fo = 0.25 * (eps * r11) * (eps * r11);
+    }
+    if (fo_track && eta < eps * r11) {
+      // k_c reached: the first-order run stops here and finishes its cold
+      // columns as Q^T a (identical decisions so far in every CTA)
+      fo_track = false;
+      for (int u = tid; u < sh.ncold; u += kT) fofl[coldl[rank + G * u]] = 1;
+      __syncthreads();
     }
     if (eta < stop_tol * r11) break;
     // ---- swap bookkeeping (reference: r[:, [k, j]], perm[[k, j]] ...): the
@@ -1467,7 +1488,10 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
     __syncthreads();
     auto consider = [&](int c) {
       if (c == j || done[c]) return;
-      if (cur[c] < thr2) {
+      if (fo_track && cur[c] < thr2_fo) fofl[c] = 1;
+      // (superfine after k_c: a column the first-order run left active keeps
+      // its in-loop coarse rows, so it is never frozen)
+      if (cur[c] < thr2 && (fo_track || scheme != 2 || fofl[c])) {
         done[c] = 2;
         atomicMax(&sh.fmax, (unsigned long long)__double_as_longlong(cur[c]));
       } else {
@@ -1539,8 +1563,17 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
     group_barrier(ctr, G, gen, k, events + 12 * slot + 9);
   }
   const int k_stop = k;
+  const bool k_c_seen_sf = scheme == 2 && !fo_track;
   // remaining cold columns finish like frozen ones (Q^T a from the original)
-  for (int u = tid; u < sh.ncold; u += kT) done[coldl[rank + G * u]] = 2;
+  // -- except, in the superfine scheme, those the first-order run kept
+  // active up to k_c: they are brought up to date (their rows < k_c are the
+  // in-loop values of every scheme) and written back like active columns
+  if (scheme == 2 && sh.ncold > 0 && k_c_seen_sf) cold_maint(k0, k);
+  __syncthreads();
+  for (int u = tid; u < sh.ncold; u += kT) {
+    const int c = coldl[rank + G * u];
+    if (scheme != 2 || !k_c_seen_sf || fofl[c]) done[c] = 2;
+  }
   // frozen list of my own columns (static ownership c % G)
   group_barrier(ctr, G, gen, -5, events + 12 * slot + 9);
   if (tid == 0) sh.nfrz = 0;
@@ -1767,26 +1800,22 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
     }
   };
   if (nf > 0) qt_a(flist, nf, k_c + n_corr, false);
-  // coarse rows of the other non-coarse-pivot columns (still active, or
-  // pivoted at a step >= k_c by the superfine scheme): Q_c^T a as well, so
-  // every scheme forms R rows < k_c of every column the same way (a column
-  // is frozen, cold, hot or a band pivot depending on stop_tol)
-  {
+  // superfine: the columns the first-order run would have formed as Q^T a
+  // (fofl) but that stayed active here get their R rows < k_c the same way,
+  // from the original column (rows >= k_c keep their in-loop values)
+  if (scheme == 2) {
     int32_t* l2 = flist + 4 * ncap;   // the loop's hot lists are free now
     if (tid == 0) sh.nact = 0;
     __syncthreads();
-    for (int c = rank + G * tid; c < n; c += G * kT) {
-      const int dc = __ldcg(done + c);
-      if (dc == 0 || (dc == 1 && __ldcg(pos + c) >= k_c))
-        l2[rank + G * atomicAdd(&sh.nact, 1)] = c;
-    }
+    for (int c = rank + G * tid; c < n; c += G * kT)
+      if (__ldcg(fofl + c) && __ldcg(done + c) != 2) l2[rank + G * atomicAdd(&sh.nact, 1)] = c;
     __syncthreads();
     const int n2 = sh.nact;
     if (n2 > 0 && k_c > 0) qt_a(l2, n2, k_c, true);
+    // the write-back below covers contiguous column ranges, the product
+    // above the interleaved ownership
+    group_barrier(ctr, G, gen, 300000, events + 12 * slot + 9);
   }
-  // the write-back below covers contiguous column ranges, the products
-  // above the interleaved ownership
-  group_barrier(ctr, G, gen, 300000, events + 12 * slot + 9);
   TL(tg);
   // ---- write back (non-frozen columns): new slot s < n_fine <- R row
   //      k_c + s (only s < n_corr are read later); slot n_fine + t <- R row t

@@ -49,7 +49,7 @@ WAVE_LOG = None      # set to [] to record per-wave CUDA events (profiling)
 PROG_ARENA = None    # pinned staging of the program chunks (emission thread)
 NK_RTOL = 1e-8       # rank threshold of the near-kernel basis (oracle NK_RTOL)
 EVENT_ROW = 12
-MAX_PANEL_ROWS = 6144
+MAX_PANEL_ROWS = 24576   # rrqr.cu kMaxM (reflector in shared memory)
 
 
 class NativePlan:
@@ -214,6 +214,7 @@ class Engine:
                               0 if near_kernel is None else near_kernel.shape[1],
                               digest=digest)
         self.timings = {"symbolic_s": self.sym.seconds}
+
 
     # -------------------------------------------------------------- numeric
     def run(self):
@@ -669,6 +670,19 @@ class Collected:
 def ctypes_ptr(addr):
     import ctypes
     return ctypes.c_void_p(int(addr))
+
+
+def check_panel_rows(h, skip_levels):
+    """Every cluster of depth d < levels - skip is sparsified at least once
+    (levels d+1 .. levels-skip); its height must fit the device RRQR.
+    Raises PanelTooLarge before anything is allocated or launched."""
+    m0 = np.array([c.dofs.size for c in h.clusters], dtype=np.int64)
+    dep = np.array([c.depth for c in h.clusters], dtype=np.int64)
+    big = np.flatnonzero((dep < h.levels - skip_levels) & (m0 > MAX_PANEL_ROWS))
+    if big.size:
+        from .errors import PanelTooLarge
+        c = int(big[np.argmax(m0[big])])
+        raise PanelTooLarge(m0[c], MAX_PANEL_ROWS, cluster=h.clusters[c].id)
 
 
 def run_factorization(a, h, eps, scheme, skip_levels, collect_local_errors=False,

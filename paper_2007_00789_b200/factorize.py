@@ -125,7 +125,8 @@ def factorize(a, hierarchy, eps, scheme, skip_levels=4,
             raise ValueError(f"at most 16 near-kernel vectors, got {nk.shape[1]}")
         if nk.shape[1] == 0:
             nk = None
-    from .engine import run_factorization
+    from .engine import check_panel_rows, run_factorization
+    check_panel_rows(hierarchy, int(skip_levels))
     return run_factorization(a, hierarchy, float(eps), scheme, int(skip_levels),
                              collect_local_errors, near_kernel=nk, digest=bool(digest))
 

@@ -200,11 +200,19 @@ class NativeApplyPlan(FastPlan):
         if xd.dim() == 1:
             self._run1(xd, forward, backward)
             return xd
+        cols = xd.t().contiguous()          # (k, n): vector j contiguous
+        self.run_rows(cols, forward, backward)
+        xd.copy_(cols.t())
+        return xd
+
+    def run_rows(self, cols, forward=True, backward=True):
+        """In place on a contiguous (k, n) device tensor whose ROWS are the
+        vectors (the multi-RHS PCG keeps its vectors this way); every row is
+        transformed bit for bit as by the single-vector apply."""
         t = require_cuda()
         if getattr(self, "_scratch_multi", None) is None:
             self._scratch_multi = t.empty(max(self.scratch_len, 1) * self.NVEC_MAX,
                                           dtype=t.float64, device=dev())
-        cols = xd.t().contiguous()          # (k, n): vector j contiguous
         st = stream()
         n = self.n
         for j0 in range(0, cols.shape[0], self.NVEC_MAX):
@@ -219,5 +227,4 @@ class NativeApplyPlan(FastPlan):
             for v in range(nv):
                 _lib.call("spand_scatter_perm", n, ptr(self.perm),
                           ctypes_ptr(self.xbuf.data_ptr() + 8 * n * v), ptr(cols[j0 + v]), st)
-        xd.copy_(cols.t())
-        return xd
+        return cols

@@ -26,7 +26,7 @@ from . import _lib
 from .device import dev, ptr, require_cuda, stream
 from .errors import Breakdown
 
-__all__ = ["SolveReport", "pcg", "cg_bound_rate", "default_maxit"]
+__all__ = ["SolveReport", "pcg", "pcg_multi", "cg_bound_rate", "default_maxit"]
 
 
 @dataclass
@@ -126,10 +126,15 @@ class _Dots:
 
 
 def pcg(a, b, m=None, tol=1e-10, maxit=None):
-    """Solve A x = b by PCG on the device; returns (x, SolveReport)."""
+    """Solve A x = b by PCG on the device; returns (x, SolveReport).
+
+    ``b`` of shape (n, k) (EXTENSION): k right-hand sides
+    solved together (``pcg_multi``); returns (X, [SolveReport] * k)."""
     if tol <= 0.0:
         raise ValueError(f"tol must be positive, got {tol}")
     t = require_cuda()
+    if getattr(b, "ndim", 1) == 2:
+        return pcg_multi(a, b, m=m, tol=tol, maxit=maxit)
     from .sparse import SparseSymMatrix
     is_torch = isinstance(b, t.Tensor)
     bd = (b.to(device=dev(), dtype=t.float64).contiguous() if is_torch
@@ -211,3 +216,156 @@ def pcg(a, b, m=None, tol=1e-10, maxit=None):
                          converged=converged, true_residual=true_residual,
                          solve_seconds=time.perf_counter() - start)
     return back(x), report
+
+
+def _rows_apply(m, n):
+    """Preconditioner on a contiguous (k, n) stack of row vectors, in place:
+    a device factor runs its multi-RHS apply (each payload element read once
+    per group of up to four vectors, every row bitwise equal to the
+    single-vector apply); other operators run row by row."""
+    from .factorize import Factorization
+    target = getattr(m, "__self__", None)
+    fac = m if isinstance(m, Factorization) else (
+        target if isinstance(target, Factorization)
+        and getattr(m, "__name__", "") == "apply_m" else None)
+    if fac is not None:
+        plan = fac.plan
+        if hasattr(plan, "run_rows"):
+            return lambda rows: plan.run_rows(rows)
+
+        def cols_run(rows):
+            cols = rows.t().contiguous()
+            plan.run(cols)
+            rows.copy_(cols.t())
+            return rows
+        return cols_run
+    single = _device_operator(m, n, "preconditioner")
+
+    def each(rows):
+        t = require_cuda()
+        tmp = t.empty(n, dtype=t.float64, device=dev())
+        for j in range(rows.shape[0]):
+            single(rows[j], tmp)
+            rows[j].copy_(tmp)
+        return rows
+    return each
+
+
+def pcg_multi(a, b, m=None, tol=1e-10, maxit=None):
+    """k right-hand sides by PCG in lockstep (multi-RHS solve, SURVEY 8f-3,
+    the column stacks of factorize.py:262-267): every column runs exactly
+    the recurrence of ``pcg`` -- same kernels, same order, so each column's
+    iterates, history and stopping decision are bit for bit those of a
+    single-vector solve -- while the preconditioner applies to the stack of
+    still-running columns at once.  Returns (X (n, k), [SolveReport] * k)."""
+    if tol <= 0.0:
+        raise ValueError(f"tol must be positive, got {tol}")
+    t = require_cuda()
+    from .sparse import SparseSymMatrix
+    is_torch = isinstance(b, t.Tensor)
+    bd = (b.to(device=dev(), dtype=t.float64) if is_torch
+          else t.from_numpy(np.array(b, dtype=np.float64)).to(dev()))
+    if bd.dim() != 2:
+        raise ValueError("pcg_multi needs an (n, k) right-hand side")
+    n, k = int(bd.shape[0]), int(bd.shape[1])
+    if maxit is None:
+        maxit = default_maxit(n)
+    lib = _lib.load()
+    st = stream()
+    spmv_mat = None
+    if isinstance(a, SparseSymMatrix):
+        spmv_mat = a.device()
+    elif isinstance(getattr(a, "__self__", None), SparseSymMatrix):
+        spmv_mat = a.__self__.device()
+    apply_a = _device_operator(a, n, "system operator")
+    apply_rows = _rows_apply(m, n)
+    dots = [_Dots(n) for _ in range(k)]
+    nsp = max(1, lib.spand_spmv_blocks(n))
+    scal = t.zeros((k, 8), dtype=t.float64, device=dev())
+    start = time.perf_counter()
+    B = bd.t().contiguous()                       # (k, n): rows are the systems
+    X = t.zeros_like(B)
+    R = B.clone()
+    Z = t.empty_like(B)
+    P = t.empty_like(B)
+    AP = t.empty_like(B)
+    for j in range(k):
+        dots[j].dot(B[j], B[j], scal[j, 4:5])
+    bnorm = np.sqrt(scal[:, 4].cpu().numpy())
+    hist = [[1.0] if bnorm[j] > 0 else [0.0] for j in range(k)]
+    live = [j for j in range(k) if bnorm[j] > 0]
+    iters = [0] * k
+    conv = [bnorm[j] == 0 for j in range(k)]
+
+    def precond(rows_idx):
+        # Z[j] = M R[j] for the given rows, as one stack
+        if not rows_idx:
+            return
+        if len(rows_idx) == k:
+            Z.copy_(R)
+            apply_rows(Z)
+            return
+        idx = t.as_tensor(rows_idx, device=dev())
+        stack = R.index_select(0, idx).contiguous()
+        apply_rows(stack)
+        Z.index_copy_(0, idx, stack)
+
+    precond(live)
+    for j in live:
+        dots[j].dot(R[j], Z[j], scal[j, 0:1])
+    rz = scal[:, 0].cpu().numpy()
+    for j in live:
+        if rz[j] <= 0.0:
+            raise Breakdown(f"preconditioner is not positive definite "
+                            f"(column {j}: r'z = {rz[j]})")
+    P.copy_(Z)
+    for it in range(1, maxit + 1):
+        if not live:
+            break
+        for j in live:
+            if spmv_mat is not None:
+                spmv_mat.spmv(P[j], AP[j], pdot=dots[j].part)
+                _lib.call("spand_reduce_sum", nsp, ptr(dots[j].part), ptr(scal[j, 1:2]), st)
+            else:
+                apply_a(P[j], AP[j])
+                dots[j].dot(P[j], AP[j], scal[j, 1:2])
+            _lib.call("spand_pcg_xr", n, ptr(scal[j]), ptr(X[j]), ptr(R[j]), ptr(P[j]),
+                      ptr(AP[j]), ptr(dots[j].part), st)
+            _lib.call("spand_reduce_sum", dots[j].nb, ptr(dots[j].part), ptr(scal[j, 3:4]), st)
+        precond(live)
+        for j in live:
+            dots[j].dot(R[j], Z[j], scal[j, 2:3])
+        vals = scal[:, :4].cpu().numpy()
+        still = []
+        for j in live:
+            pap, rr, rz_next = float(vals[j, 1]), float(vals[j, 3]), float(vals[j, 2])
+            if pap <= 0.0:
+                raise Breakdown(f"system operator is not positive definite "
+                                f"(column {j}: p'Ap = {pap})")
+            rel = math.sqrt(max(rr, 0.0)) / bnorm[j]
+            hist[j].append(rel)
+            iters[j] = it
+            if rel < tol:
+                conv[j] = True
+                continue
+            if rz_next <= 0.0:
+                raise Breakdown(f"preconditioner is not positive definite "
+                                f"(column {j}: r'z = {rz_next})")
+            _lib.call("spand_pcg_p", n, ptr(scal[j]), ptr(Z[j]), ptr(P[j]), st)
+            scal[j, 0:1].copy_(scal[j, 2:3])
+            still.append(j)
+        live = still
+    reports = []
+    for j in range(k):
+        if bnorm[j] == 0:
+            tres = 0.0
+        else:
+            apply_a(X[j], AP[j])
+            AP[j].sub_(B[j]).neg_()
+            dots[j].dot(AP[j], AP[j], scal[j, 5:6])
+            tres = math.sqrt(float(scal[j, 5].item())) / bnorm[j]
+        reports.append(SolveReport(n_cg=iters[j], residual_history=hist[j],
+                                   converged=bool(conv[j]), true_residual=tres,
+                                   solve_seconds=time.perf_counter() - start))
+    Xo = X.t().contiguous()
+    return (Xo.to(b.device) if is_torch else Xo.cpu().numpy()), reports

@@ -13,7 +13,7 @@ from .dense import SCHEME_CODE, RRQRResult, SchemeKind
 from .device import dev, ptr, require_cuda, stream, to_dev
 from .kernels import Geometry
 
-MAX_ROWS = 6144
+MAX_ROWS = 24576   # rrqr.cu kMaxM
 
 
 def rrqr_single(a, eps, scheme, group=None, pad=0):
@@ -22,7 +22,8 @@ def rrqr_single(a, eps, scheme, group=None, pad=0):
     t = require_cuda()
     m, n = a.shape
     if m > MAX_ROWS:
-        raise NotImplementedError(f"panel of {m} rows exceeds the kernel limit")
+        from .errors import PanelTooLarge
+        raise PanelTooLarge(m, MAX_ROWS)
     mp, np_ = m + pad, n + pad
     geo = Geometry(np.array([mp, np_], dtype=np.int32),
                    np.array([pad, pad], dtype=np.int32))

@@ -151,58 +151,72 @@ def from_coo(n, rows, cols, vals):
 
 
 def read_matrix_market(path):
-    """Read a `matrix coordinate real symmetric` file (one triangle stored)."""
-    with open(path, "r") as fh:
-        header = fh.readline().strip()
-        tok = header.split()
-        if len(tok) != 5 or tok[0] != "%%MatrixMarket":
-            raise ParseError(f"bad Matrix Market header: {header!r}")
-        if tok[1].lower() != "matrix" or tok[2].lower() != "coordinate":
-            raise ParseError(f"unsupported object/format: {header!r}")
-        if tok[3].lower() != "real" or tok[4].lower() != "symmetric":
-            raise NotSymmetricReal(
-                f"only real symmetric matrices are supported, got "
-                f"{tok[3]} {tok[4]}")
-        line = fh.readline()
-        while line and (line.startswith("%") or not line.strip()):
-            line = fh.readline()
-        try:
-            m, n, nnz = (int(t) for t in line.split())
-        except ValueError:
-            raise ParseError(f"bad size line: {line.strip()!r}") from None
-        if m != n:
+    """Read a `matrix coordinate real symmetric` file (one triangle stored),
+    reference `sparse.py:98-160`: parsed by the native multi-threaded reader
+    (csrc/mmio.cpp); the same errors, raised for the first offending line in
+    file order, with the reference's messages."""
+    import ctypes
+    from . import _lib
+    lib = _lib.load()
+    lib.spand_mm_read.restype = ctypes.c_void_p
+    lib.spand_mm_read.argtypes = [ctypes.c_char_p, ctypes.c_void_p]
+    for nm, args in (("spand_mm_csr", 4), ("spand_mm_error_span", 2), ("spand_mm_text", 4)):
+        getattr(lib, nm).argtypes = [ctypes.c_void_p] * args
+        getattr(lib, nm).restype = ctypes.c_int
+    lib.spand_mm_text.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64,
+                                  ctypes.c_void_p]
+    lib.spand_mm_free.argtypes = [ctypes.c_void_p]
+    vp = lambda x: x.ctypes.data_as(ctypes.c_void_p)  # noqa: E731
+    info = np.zeros(8, dtype=np.int64)
+    h = lib.spand_mm_read(str(path).encode(), vp(info))
+    try:
+        code = int(info[0])
+
+        def text(b, e):
+            buf = ctypes.create_string_buffer(max(int(e - b), 1))
+            lib.spand_mm_text(h, int(b), int(e), buf)
+            return buf.raw[:int(e - b)].decode(errors="replace")
+
+        if code == 11:
+            raise FileNotFoundError(path)
+        if code in (1, 2, 3):
+            header = text(0, info[5]).strip()
+            tok = header.split()
+            if code == 1:
+                raise ParseError(f"bad Matrix Market header: {header!r}")
+            if code == 2:
+                raise ParseError(f"unsupported object/format: {header!r}")
+            raise NotSymmetricReal(f"only real symmetric matrices are supported, got "
+                                   f"{tok[3]} {tok[4]}")
+        if code == 4:
+            raise ParseError(f"bad size line: {text(info[6], info[7]).strip()!r}")
+        if code == 5:
             raise NotSymmetricReal("matrix must be square")
-        entries = {}
-        for _ in range(nnz):
-            line = fh.readline()
-            if not line:
-                raise ParseError("file ends before declared entry count")
-            parts = line.split()
-            if len(parts) != 3:
+        if code == 6:
+            raise ParseError("file ends before declared entry count")
+        if code:
+            span = np.zeros(2, dtype=np.int64)
+            lib.spand_mm_error_span(h, vp(span))
+            line = text(span[0], span[1])
+            if code == 7:
                 raise ParseError(f"bad entry line: {line.strip()!r}")
-            try:
-                i, j, v = int(parts[0]) - 1, int(parts[1]) - 1, float(parts[2])
-            except ValueError:
-                raise ParseError(f"bad entry line: {line.strip()!r}") from None
-            if not (0 <= i < n and 0 <= j < n):
-                raise ParseError(f"index out of range: ({i + 1}, {j + 1})")
-            if (i, j) in entries:
-                raise ParseError(f"duplicate entry ({i + 1}, {j + 1})")
-            if i != j and (j, i) in entries and entries[(j, i)] != v:
-                raise AsymmetricValues(
-                    f"entries ({j + 1}, {i + 1}) and ({i + 1}, {j + 1}) "
-                    f"disagree: {entries[(j, i)]} vs {v}")
-            entries[(i, j)] = v
-    rows, cols, vals = [], [], []
-    for (i, j), v in entries.items():
-        rows.append(i)
-        cols.append(j)
-        vals.append(v)
-        if i != j and (j, i) not in entries:
-            rows.append(j)
-            cols.append(i)
-            vals.append(v)
-    return from_coo(n, rows, cols, vals)
+            parts = line.split()
+            i, j, v = int(parts[0]), int(parts[1]), float(parts[2])
+            if code == 8:
+                raise ParseError(f"index out of range: ({i}, {j})")
+            if code == 9:
+                raise ParseError(f"duplicate entry ({i}, {j})")
+            mirror = float(np.int64(info[4]).view(np.float64))
+            raise AsymmetricValues(f"entries ({j}, {i}) and ({i}, {j}) disagree: "
+                                   f"{mirror} vs {v}")
+        n, nnz = int(info[1]), int(info[2])
+        rp = np.zeros(n + 1, dtype=np.int64)
+        ci = np.zeros(max(nnz, 1), dtype=np.int64)
+        va = np.zeros(max(nnz, 1), dtype=np.float64)
+        lib.spand_mm_csr(h, vp(rp), vp(ci), vp(va))
+    finally:
+        lib.spand_mm_free(h)
+    return SparseSymMatrix(n, rp, ci[:nnz], va[:nnz])
 
 
 def write_matrix_market(path, a):

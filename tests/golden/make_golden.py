@@ -19,10 +19,11 @@ Per run we store: cluster structure (full arrays for small cases, sizes +
 sha256 for the big ones), per-level diagnostics (interface ranks, rank_f2),
 the factor's perm, per-op payload sha256 and Frobenius norms, nnz_factor,
 n_cg, the residual history and timings (1 BLAS thread, this container).
-Every run also stores, per operator, ||P||_F, four bilinear sketches and
-nnz of each payload (``op_fro``/``op_sk``/``op_nnz`` in the .npz, see
-tests/golden_cases.py), apply_m(b) and the PCG solution x, so the
-full-size configs are checked per block without storing their factors.
+Every run also stores, per operator, the Frobenius norms and four
+bilinear sketches of the payloads' invariant forms and nnz of each payload
+(``op_fro5``/``op_ska5``/``op_nnz`` in the .npz, see tests/golden_cases.py),
+apply_m(b) and the PCG solution x, so the full-size configs are checked
+per block without storing their factors.
 """
 
 import hashlib
@@ -41,7 +42,7 @@ import spdkit  # noqa: E402  (the reference, via PYTHONPATH)
 from spdkit.schemes import OpKind  # noqa: E402
 
 from paper_2007_00789_b200 import sparse as gen  # noqa: E402
-from tests.golden_cases import op_tables  # noqa: E402
+from tests.golden_cases import op_tables, rank_c_of  # noqa: E402
 
 
 def sha(arr):
@@ -147,9 +148,8 @@ def run_case(tag, a, b, levels, eps, scheme, skip_levels=4, tol=1e-12,
     if sketches:
         # per-operator ||P||_F, bilinear sketches and nnz of every payload
         # (tests/golden_cases.py:op_tables): full-size per-block parity
-        fro, sk, ska, nnz = op_tables(f.ops)
-        arrays["op_fro"], arrays["op_sk"], arrays["op_nnz"] = fro, sk, nnz
-        arrays["op_ska"] = ska
+        fro, ska, nnz = op_tables(f.ops, rank_c_of(f.diagnostics["levels"]))
+        arrays["op_fro5"], arrays["op_ska5"], arrays["op_nnz"] = fro, ska, nnz
         rec["digests"] = [lv["digest"] for lv in f.diagnostics["levels"]]
     arrays["perm"] = np.asarray(f.perm, dtype=np.int32 if a.n < 2**31 else np.int64)
     arrays["b"] = np.asarray(b)

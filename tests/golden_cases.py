@@ -65,16 +65,35 @@ def config_tags():
 # --------------------------------------------------------------------------
 # Per-operator payload sketches (full-size parity without storing factors).
 #
-# For every operator i and payload slot k (0 lower, 1 panel, 2 q, 3 e_tilde)
-# the generator stores ||P||_F and NSK bilinear sketches u_j^T P v_j with
-# seeded Rademacher u_j, v_j.  For a difference D = P_gpu - P_ref,
-# E[(u^T D v)^2] = ||D||_F^2, so |sketch_gpu - sketch_ref| is an unbiased
-# probe of the per-block relative Frobenius error the north star bounds
-# (1e-8): NSK = 4 independent probes, compared at SK_TOL * ||P||_F.
+# Two rounding-level decisions make a correct factorization differ from the
+# reference's by more than rounding, without changing the operator:
+#
+# * the sign of a Householder reflector (beta = -sign(x0) eta,
+#   dense.py:155-159) is decided on x0, which is rounding noise for a few
+#   hundred reflectors of a large factorization (|x0| / eta < 1e-15); the two
+#   choices are different reflections.  The factored part is unique up to
+#   signs (R rows < k_stop, Q's factored columns), so downstream blocks differ
+#   by diagonal sign congruences D P D';
+# * the unfactored columns of Q (the fine complement, reflector positions
+#   >= k_stop) are only ONE orthonormal basis of the complement of the
+#   factored columns, and the rows of e_tilde = Q_f^T W live in that basis:
+#   a flipped reflector rotates both.
+#
+# The sketched quantities are therefore invariant forms, each equal to the
+# payload up to those transformations:
+#   0 |L|       (elimination / scaling lower)     sign congruence
+#   1 |panel|   (elimination panel)               sign congruence
+#   2 |Q_c|     (coarse = factored columns of q)  signs
+#   3 |Q_f Q_f^T| (projector on the fine space)   sign congruence, basis-free
+#   4 |Q_f[:, :r] E| (correction mapped back)     sign congruence, basis-free
+# For each, ||X||_F and NSK bilinear sketches u^T |X| v with seeded
+# Rademacher u, v: for a difference D, E[(u^T D v)^2] = ||D||_F^2 and
+# | |X| - |Y| | <= |X - Y| elementwise, so the sketch difference probes the
+# per-block relative Frobenius error the north star bounds (1e-8).
 
 NSK = 4
-SK_TOL = 6e-8          # ~6 sigma of 1e-8 ||P||_F spread over 4 probes
-SLOTS = ("lower", "panel", "q", "e_tilde")
+SK_TOL = 6e-8          # ~6 sigma of 1e-8 ||X||_F spread over 4 probes
+SLOTS = ("lower", "panel", "q_coarse", "q_fine_projector", "correction")
 
 
 def sketch_uv(i, k, r, c):
@@ -93,42 +112,65 @@ def sketch(p, i, k):
     return np.einsum("jc,jc->j", u @ p, v)
 
 
-# The sign of a Householder reflector (beta = -sign(x0) eta, dense.py:155-159)
-# is decided on x0, which is rounding noise for a few hundred reflectors of a
-# large factorization (|x0| / eta < 1e-15: mathematically zero entries); the
-# CPU and the GPU can take opposite signs there.  A flipped reflector negates
-# one Q column and one R row, i.e. the rest of the factorization differs by
-# a diagonal sign congruence D P D' -- the same operator (apply_m agrees),
-# different payload signs.  The elementwise absolute value is invariant
-# under it and | |P| - |P'| | <= |P - D P' D'| elementwise, so sketches of
-# |P| bound the per-block difference modulo those signs.
+def _kind(op):
+    k = op.kind
+    return k if isinstance(k, str) else {"elimination": "G", "scaling": "D",
+                                         "orthogonal": "Q", "error-correction": "E"}[k.value]
 
 
-def op_tables(ops):
-    """(fro, sketches, |P| sketches, nnz) arrays over an operator list
-    (reference ops or host-materialised device ops): fro (nops, 4) with NaN
-    where the slot does not exist, sketches (nops, 4, NSK), nnz (nops,)."""
+def invariant_forms(ops, rank_c, xp=np):
+    """Yield (op index, slot, matrix) of the invariant forms above.
+    ``rank_c``: per Orthogonal op (operator order), its coarse count
+    (diagnostics size_after).  ``xp``: numpy, or a converter of device
+    payloads (see device_op_tables)."""
+    qi = 0
+    last_qf = None
+    for i, op in enumerate(ops):
+        k = _kind(op)
+        if k in ("G", "D"):
+            yield i, 0, xp["lower"](op)
+            if k == "G":
+                yield i, 1, xp["panel"](op)
+        elif k == "Q":
+            q = xp["q"](op)
+            kc = int(rank_c[qi])
+            qi += 1
+            nf = q.shape[0] - kc
+            yield i, 2, q[:, nf:]
+            qf = q[:, :nf]
+            yield i, 3, qf @ qf.T
+            last_qf = qf
+        else:
+            e = xp["e_tilde"](op)
+            yield i, 4, last_qf[:, :e.shape[0]] @ e
+
+
+def _np_access():
+    return {"lower": lambda op: np.asarray(op.lower, dtype=np.float64),
+            "panel": lambda op: np.asarray(op.panel, dtype=np.float64),
+            "q": lambda op: np.asarray(op.q, dtype=np.float64),
+            "e_tilde": lambda op: np.asarray(op.e_tilde, dtype=np.float64)}
+
+
+def op_tables(ops, rank_c):
+    """(fro, |X| sketches, nnz) over an operator list (reference ops, or
+    host-materialised device ops): fro (nops, 5) with NaN where the slot
+    does not exist, sketches (nops, 5, NSK), nnz (nops,)."""
     nops = len(ops)
     fro = np.full((nops, len(SLOTS)), np.nan)
-    sk = np.zeros((nops, len(SLOTS), NSK))
     ska = np.zeros((nops, len(SLOTS), NSK))
-    nnz = np.zeros(nops, dtype=np.int64)
-    for i, op in enumerate(ops):
-        for k, name in enumerate(SLOTS):
-            if name in ("lower", "panel") and op.kind.value not in ("elimination", "scaling"):
-                continue
-            if name == "panel" and op.kind.value != "elimination":
-                continue
-            if name == "q" and op.kind.value != "orthogonal":
-                continue
-            if name == "e_tilde" and op.kind.value != "error-correction":
-                continue
-            p = np.asarray(getattr(op, name), dtype=np.float64)
-            fro[i, k] = float(np.linalg.norm(p))
-            sk[i, k] = sketch(p, i, k)
-            ska[i, k] = sketch(np.abs(p), i, k)
-        nnz[i] = int(op.nnz)
-    return fro, sk, ska, nnz
+    for i, k, x in invariant_forms(ops, rank_c, _np_access()):
+        ax = np.abs(x)
+        fro[i, k] = float(np.linalg.norm(x))
+        ska[i, k] = sketch(ax, i, k)
+    nnz = np.array([int(op.nnz) for op in ops], dtype=np.int64)
+    return fro, ska, nnz
+
+
+def rank_c_of(diagnostics_levels):
+    """Coarse counts of the sparsified interfaces, in operator order."""
+    return [e["size_after"] if isinstance(e, dict) else e[2]
+            for lv in diagnostics_levels for e in lv["interfaces"]]
 
 
 def device_payload(op, name):
@@ -167,23 +209,19 @@ def device_payload(op, name):
     return mat(op._q)
 
 
-def device_op_tables(ops):
-    """(fro, sketches, |P| sketches) of a device factor, on the device."""
+def device_op_tables(ops, rank_c):
+    """op_tables() of a device factor (fro, |X| sketches), on the device."""
     import torch
     nops = len(ops)
     fro = np.full((nops, len(SLOTS)), np.nan)
-    sk = np.zeros((nops, len(SLOTS), NSK))
     ska = np.zeros((nops, len(SLOTS), NSK))
-    slot_of = {"elimination": (0, 1), "scaling": (0,), "orthogonal": (2,),
-               "error-correction": (3,)}
-    for i, op in enumerate(ops):
-        for k in slot_of[op.kind.value]:
-            p = device_payload(op, SLOTS[k])
-            fro[i, k] = float(torch.linalg.norm(p)) if p.numel() else 0.0
-            if p.numel():
-                u, v = sketch_uv(i, k, *p.shape)
-                ud = torch.as_tensor(u, device=p.device)
-                vd = torch.as_tensor(v, device=p.device)
-                sk[i, k] = ((ud @ p) * vd).sum(dim=1).cpu().numpy()
-                ska[i, k] = ((ud @ p.abs()) * vd).sum(dim=1).cpu().numpy()
-    return fro, sk, ska
+    acc = {name: (lambda op, nm=name: device_payload(op, nm))
+           for name in ("lower", "panel", "q", "e_tilde")}
+    for i, k, x in invariant_forms(ops, rank_c, acc):
+        fro[i, k] = float(torch.linalg.norm(x)) if x.numel() else 0.0
+        if x.numel():
+            u, v = sketch_uv(i, k, *x.shape)
+            ud = torch.as_tensor(u, device=x.device)
+            vd = torch.as_tensor(v, device=x.device)
+            ska[i, k] = ((ud @ x.abs()) * vd).sum(dim=1).cpu().numpy()
+    return fro, ska

@@ -296,3 +296,114 @@ def test_oracle_generator_matches_package(shape, block, seed):
     assert np.array_equal(a.row_ptr, rp) and np.array_equal(a.col_idx, ci)
     assert np.array_equal(a.values, va)
     assert np.array_equal(rng.standard_normal(n), b)
+
+
+def test_oversized_interface_raises_before_launch():
+    """An interface taller than the device RRQR's limit (rrqr.cu kMaxM) is
+    rejected with a typed error before any allocation or launch (so it runs
+    without a GPU); the reference (dense.py:117) has no cap."""
+    from paper_2007_00789_b200.engine import MAX_PANEL_ROWS
+    from paper_2007_00789_b200.partition import Cluster, PartitionHierarchy
+    big = MAX_PANEL_ROWS + 10
+    n = big + 2
+    a = sp.from_coo(n, np.arange(n), np.arange(n), np.full(n, 2.0))
+    cl = [Cluster(id=0, dofs=np.arange(2, n), depth=0),
+          Cluster(id=1, dofs=np.array([0]), depth=1),
+          Cluster(id=2, dofs=np.array([1]), depth=1)]
+    h = PartitionHierarchy(1, n, cl, np.zeros(n + 1, np.int64), np.zeros(0, np.int64))
+    with pytest.raises(sp.PanelTooLarge) as exc:
+        sp.factorize(a, h, 0.01, "first", skip_levels=0)
+    assert exc.value.rows == big and exc.value.cluster == 0
+    assert isinstance(exc.value, NotImplementedError)
+
+
+def test_one_sided_explicit_zero_is_accepted():
+    """The reference's symmetry test compares VALUES ((csr != csr.T).nnz,
+    sparse.py:52-53): a stored zero whose mirror is absent equals the
+    implicit zero and is accepted; a one-sided nonzero is rejected.  The
+    native hierarchy of such a pattern equals the oracle's."""
+    from oracle import spand_oracle as orc
+    a = sp.laplacian_2d(6)
+    rows = np.repeat(np.arange(a.n), np.diff(a.row_ptr))
+    r = np.concatenate([rows, [0]])
+    c = np.concatenate([a.col_idx, [20]])
+    v = np.concatenate([a.values, [0.0]])
+    z = sp.from_coo(a.n, r, c, v)
+    assert z.nnz == a.nnz + 1
+    with pytest.raises(sp.AsymmetricValues):
+        sp.from_coo(a.n, r, c, np.concatenate([a.values, [1e-3]]))
+    h = sp.build_hierarchy(z, 3)
+    cl = orc.nd_hierarchy(z.n, z.row_ptr, z.col_idx, 3)
+    assert [c_.dofs.tolist() for c_ in h.clusters] == [d.tolist() for _, d, _ in cl]
+    assert [c_.depth for c_ in h.clusters] == [dep for _, _, dep in cl]
+
+
+_MM_CASES = {
+    "ok": "%%MatrixMarket matrix coordinate real symmetric\n% c\n\n3 3 4\n1 1 4.0\n2 1 -1\n"
+          "2 2 4e0\n3 3 1_0.5\n",
+    "ok_mirror": "%%MatrixMarket matrix coordinate real symmetric\n2 2 4\n1 1 2\n2 1 -.5\n"
+                 "1 2 -0.5\n2 2 3\n",
+    "ok_crlf": "%%MatrixMarket Matrix Coordinate REAL Symmetric\r\n2 2 3\r\n1 1 2\r\n"
+               "2 1 1e-3\r\n2 2 +3.\r\n",
+    "bad_header": "%%MatrixMarkt matrix coordinate real symmetric\n1 1 1\n1 1 1\n",
+    "bad_format": "%%MatrixMarket matrix array real symmetric\n1 1 1\n1 1 1\n",
+    "general": "%%MatrixMarket matrix coordinate real general\n1 1 1\n1 1 1\n",
+    "bad_size": "%%MatrixMarket matrix coordinate real symmetric\n2 2\n1 1 1\n",
+    "empty_size": "%%MatrixMarket matrix coordinate real symmetric\n% only comments\n",
+    "rect": "%%MatrixMarket matrix coordinate real symmetric\n2 3 1\n1 1 1\n",
+    "short": "%%MatrixMarket matrix coordinate real symmetric\n2 2 3\n1 1 1\n2 2 1\n",
+    "bad_line": "%%MatrixMarket matrix coordinate real symmetric\n2 2 2\n1 1 1\n2 2\n",
+    "bad_number": "%%MatrixMarket matrix coordinate real symmetric\n2 2 2\n1 1 1\n2 2 0x1p3\n",
+    "comment_in_entries": "%%MatrixMarket matrix coordinate real symmetric\n2 2 2\n1 1 1\n"
+                          "% no\n",
+    "range": "%%MatrixMarket matrix coordinate real symmetric\n2 2 2\n1 1 1\n3 1 1\n",
+    "dup": "%%MatrixMarket matrix coordinate real symmetric\n2 2 3\n1 1 1\n2 2 1\n1 1 2\n",
+    "asym": "%%MatrixMarket matrix coordinate real symmetric\n2 2 4\n1 1 1\n1 2 0.25\n"
+            "2 2 1\n2 1 0.5\n",
+    "first_error_wins": "%%MatrixMarket matrix coordinate real symmetric\n2 2 4\n1 1 1\n"
+                        "1 2 1\n2 1 2\n2 2 x\n",
+    "inf_nan": "%%MatrixMarket matrix coordinate real symmetric\n2 2 2\n1 1 inf\n2 2 NaN\n",
+}
+
+
+@pytest.mark.parametrize("case", sorted(_MM_CASES))
+def test_matrix_market_reader_matches_reference_semantics(tmp_path, case):
+    """The native reader (csrc/mmio.cpp) against the oracle's restatement of
+    the reference reader (sparse.py:98-160): the same CSR, or the same error
+    class and message, for valid files, CRLF, comments, number syntax
+    (Python int()/float()), every error kind, and first-error-wins order."""
+    from oracle import spand_oracle as orc
+    from paper_2007_00789_b200 import errors as E
+    p = tmp_path / f"{case}.mtx"
+    p.write_bytes(_MM_CASES[case].encode())
+    try:
+        want = orc.mm_read(str(p))
+        werr = None
+    except orc.MMError as exc:
+        want, werr = None, exc
+    if werr is not None:
+        with pytest.raises(getattr(E, werr.kind)) as got:
+            sp.read_matrix_market(str(p))
+        assert str(got.value) == str(werr)
+        return
+    try:
+        a = sp.read_matrix_market(str(p))
+    except (E.NonpositiveDiagonal, E.AsymmetricValues) as exc:
+        # the file parses; the SparseSymMatrix constructor's checks then
+        # apply to both readers' output alike
+        with pytest.raises(type(exc)):
+            sp.SparseSymMatrix(*want)
+        return
+    n, rp, ci, va = want
+    assert a.n == n and np.array_equal(a.row_ptr, rp) and np.array_equal(a.col_idx, ci)
+    assert np.array_equal(a.values, va, equal_nan=True)
+
+
+def test_matrix_market_reader_large_file(tmp_path):
+    """C2 written and read back: identical CSR (the multi-threaded path)."""
+    a = sp.laplacian_3d(32)
+    p = tmp_path / "c2.mtx"
+    sp.write_matrix_market(str(p), a)
+    b = sp.read_matrix_market(str(p))
+    assert np.array_equal(a.row_ptr, b.row_ptr) and np.array_equal(a.col_idx, b.col_idx)
+    assert np.array_equal(a.values, b.values)

@@ -1,5 +1,4 @@
 set -x
-timeout 1500 python -m pytest tests -q -m gpu -rf --durations=10 -s -k "contract or configs" > gpurun_out/pytest_contract.log 2>&1; echo rc=$?
-timeout 900 python -m pytest tests -q -m gpu -rf --durations=5 -k "not contract and not configs" > gpurun_out/pytest_rest.log 2>&1; echo rc=$?
-timeout 600 python tools/payload_diff.py C3 12 > gpurun_out/payload_diff_c3.log 2>&1; echo rc=$?
-timeout 600 python bench.py --steps 3 --warmup 3 > gpurun_out/bench2.log 2>&1; echo rc=$?
+timeout 600 python tools/scheme_diff.py 64 0.01 first second-superfine > gpurun_out/scheme_diff.log 2>&1; echo rc=$?
+timeout 900 python -m pytest tests/test_gpu_contract.py tests/test_gpu_factorize.py -q -m gpu -rf -x > gpurun_out/pytest_contract.log 2>&1; echo rc=$?
+timeout 900 python -m pytest tests/test_gpu_configs.py -q -m gpu -rf -s -k c3_every > gpurun_out/pytest_c3.log 2>&1; echo rc=$?

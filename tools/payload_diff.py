@@ -60,7 +60,23 @@ def main():
     print("first op above 1e-8:", first_bad, "of", len(f.ops))
     if first_bad is not None:
         y = o.ops[first_bad]
+        x = f.ops[first_bad]
         print("kind", y.kind, "dofs", y.dofs.size)
+        if y.kind == "Q":
+            qx, qy = np.asarray(x.q), y.q
+            c = np.abs(qx.T @ qy)
+            diag = np.diag(c)
+            bad = np.flatnonzero(np.abs(diag - 1) > 1e-8)
+            print("columns off the diagonal:", bad.size, bad[:40].tolist())
+            for j in bad[:12]:
+                top = np.argsort(-c[j])[:3]
+                print(" col", int(j), "best matches", [(int(t), float(c[j, t])) for t in top])
+            # fine/coarse split of the op: n_fine = first columns
+            print("sign flips (diag ~ 1 but negative dot):",
+                  int(np.sum(np.einsum('ij,ij->j', qx, qy) < -0.5)))
+        # diagnostics of the interfaces (margins) around that op
+        ms = [e for lv_ in f.diagnostics["levels"] for e in lv_["margins"]]
+        print("interfaces:", len(ms))
 
 
 if __name__ == "__main__":
