@@ -243,6 +243,38 @@ int spand_count_nonzero_pieces(int nview, const int64_t* views, const int64_t* p
 int spand_digest_pieces(int npiece, const int64_t* rows, const int32_t* m0,
                         const int32_t* off, void* stream);
 
+/* ---- input side on the device (sparse.py:181-308) ---------- */
+
+/* Row counts (cnt[n], device) of the nd-dimensional (2 or 3) cell-grid
+ * finite-volume matrix with dims[nd] cells per axis. */
+int spand_fv_counts(int nd, const int64_t* dims, int64_t* cnt, void* stream);
+/* Columns / values of that matrix given its row_ptr (device, n + 1):
+ * -div(a grad u), a piecewise constant with bv[] per block of `block` cells
+ * per axis (C order), harmonic-mean faces, Dirichlet faces adding the cell's
+ * coefficient; bitwise equal to the host generator diffusion_fv. */
+int spand_fv_fill(int nd, const int64_t* dims, int block, const double* bv,
+                  const int64_t* row_ptr, int64_t* col_idx, double* values,
+                  void* stream);
+/* Jacobi prescale in place on a device CSR (reference jacobi_prescale,
+ * sparse.py:290-308): diag, s = 1/sqrt(diag), b *= s (b may be null),
+ * a_ij *= s_i s_j; *bad (device int, zeroed) set on a nonpositive diagonal. */
+int spand_jacobi_prescale(int64_t n, const int64_t* row_ptr, const int64_t* col_idx,
+                          double* values, double* diag, double* s, double* b, int* bad,
+                          void* stream);
+
+/* ---- Matrix Market reader (host, multi-threaded; sparse.py:98-160) ------- */
+
+/* Parse; info[8] = {code, n, nnz, err_entry, bits(mirror value), header
+ * end, size line begin, size line end}; code 0 ok, 1 bad header, 2
+ * unsupported object/format, 3 not real symmetric, 4 bad size line, 5 not
+ * square, 6 file ends early, 7 bad entry line, 8 index out of range, 9
+ * duplicate entry, 10 mirror values disagree, 11 cannot open. */
+void* spand_mm_read(const char* path, int64_t* info);
+int spand_mm_csr(void* h, int64_t* row_ptr, int64_t* col_idx, double* values);
+int spand_mm_error_span(void* h, int64_t* span);
+int spand_mm_text(void* h, int64_t begin, int64_t end, char* out);
+void spand_mm_free(void* h);
+
 /* ---- host-side integer structure (partition.py:118-268) ------------------ */
 
 /* Nested-dissection hierarchy of the graph of a CSR matrix (host memory).

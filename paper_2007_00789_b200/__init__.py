@@ -55,6 +55,7 @@ from .sparse import (
     baseline_problem,
     c5_problem,
     diffusion_fv,
+    diffusion_fv_device,
     elasticity_q1,
     from_coo,
     jacobi_prescale,

@@ -47,6 +47,9 @@ SIGNATURES = {
     "spand_count_nonzero": [_c_int, _P, _P, _P],
     "spand_count_nonzero_pieces": [_c_int, _P, _P, _c_i64, _P, _P, _P, _P],
     "spand_digest_pieces": [_c_int, _P, _P, _P, _P],
+    "spand_fv_counts": [_c_int, _P, _P, _P],
+    "spand_fv_fill": [_c_int, _P, _c_int, _P, _P, _P, _P, _P],
+    "spand_jacobi_prescale": [_c_i64, _P, _P, _P, _P, _P, _P, _P, _P],
     "spand_nd_partition": [_c_i64, _P, _P, _c_int, _P, _P, _P, _P],
     "spand_plan_sizes": [_P, _P],
     "spand_plan_emit": [_P, _c_i64, _c_i64, _c_i64, _c_i64, _c_int],

@@ -232,13 +232,18 @@ def write_matrix_market(path, a):
             fh.write(f"{r[k] + 1} {c[k] + 1} {v[k]:.17g}\n")
 
 
-def jacobi_prescale(a, b):
+def jacobi_prescale(a, b, device=False):
     """A' = D^-1/2 A D^-1/2, b' = D^-1/2 b (reference `sparse.py:290-308`).
+
+    ``device=True``: on the B200 (csrc/input.cu), bit for bit the same
+    values; the scaled matrix keeps its device CSR cached.
 
     Input-side preprocessing (one pass over nnz(A)); the scale of entry
     (i, j) is the product s_i * s_j grouped the same way for (i, j) and
     (j, i) so the result stays exactly symmetric.
     """
+    if device:
+        return _jacobi_prescale_device(a, b)
     diag = a.diagonal()
     if np.any(diag <= 0.0):
         raise NonpositiveDiagonal("jacobi_prescale needs a positive diagonal")
@@ -247,6 +252,69 @@ def jacobi_prescale(a, b):
     vals = a.values * (s[rows] * s[a.col_idx])
     return (SparseSymMatrix(a.n, a.row_ptr, a.col_idx, vals),
             np.asarray(b, dtype=np.float64) * s, diag)
+
+
+def _device_matrix(n, rp, ci, va):
+    """SparseSymMatrix from device CSR arrays (int64 / fp64 tensors): host
+    copies for the host-side structure (validation, partition), and the
+    device CSR (int32 indices) cached so no host->device upload follows."""
+    from .device import DeviceCSR, torch
+    t = torch()
+    a = SparseSymMatrix(int(n), rp.cpu().numpy(), ci.cpu().numpy(), va.cpu().numpy())
+    a._dev[None] = (None, DeviceCSR(a.n, rp.to(t.int32), ci.to(t.int32), va))
+    return a
+
+
+def _jacobi_prescale_device(a, b):
+    from . import _lib
+    from .device import ptr, require_cuda, stream, to_dev
+    t = require_cuda()
+    n = a.n
+    rp, ci = to_dev(a.row_ptr, np.int64), to_dev(a.col_idx, np.int64)
+    va = to_dev(a.values, np.float64)
+    diag = t.empty(n, dtype=t.float64, device=va.device)
+    s = t.empty_like(diag)
+    bd = to_dev(np.asarray(b, dtype=np.float64).copy(), np.float64)
+    bad = t.zeros(1, dtype=t.int32, device=va.device)
+    _lib.call("spand_jacobi_prescale", n, ptr(rp), ptr(ci), ptr(va), ptr(diag), ptr(s),
+              ptr(bd), ptr(bad), stream())
+    if int(bad.item()):
+        raise NonpositiveDiagonal("jacobi_prescale needs a positive diagonal")
+    return _device_matrix(n, rp, ci, va), bd.cpu().numpy(), diag.cpu().numpy()
+
+
+def diffusion_fv_device(block_values, block, shape):
+    """``diffusion_fv(field)`` for a piecewise-constant field (one value per
+    block of ``block`` cells per axis, C order), generated on the B200
+    (csrc/input.cu, bitwise equal to the host generator): the CSR is built in
+    device memory and stays cached on the returned matrix."""
+    from . import _lib
+    from .device import ptr, require_cuda, stream, to_dev
+    t = require_cuda()
+    shape = tuple(int(x) for x in shape)
+    bv = np.ascontiguousarray(block_values, dtype=np.float64)
+    if len(shape) not in (2, 3) or min(shape) < 2:
+        raise DimensionMismatch("need a 2D or 3D grid with sides >= 2")
+    if bv.shape != tuple(x // block for x in shape) or any(
+            (x // block) * block != x for x in shape):
+        raise DimensionMismatch("grid must be a multiple of the block size")
+    if np.any(bv <= 0.0):
+        raise NonpositiveDiagonal("coefficients must be positive")
+    n = int(np.prod(shape))
+    dims = np.asarray(shape, dtype=np.int64)
+    dptr = dims.ctypes.data
+    import ctypes
+    cnt = t.empty(n, dtype=t.int64, device="cuda")
+    _lib.call("spand_fv_counts", len(shape), ctypes.c_void_p(dptr), ptr(cnt), stream())
+    rp = t.zeros(n + 1, dtype=t.int64, device="cuda")
+    t.cumsum(cnt, 0, out=rp[1:])
+    nnz = int(rp[-1].item())
+    ci = t.empty(nnz, dtype=t.int64, device="cuda")
+    va = t.empty(nnz, dtype=t.float64, device="cuda")
+    bvd = to_dev(bv.ravel(), np.float64)
+    _lib.call("spand_fv_fill", len(shape), ctypes.c_void_p(dptr), int(block), ptr(bvd),
+              ptr(rp), ptr(ci), ptr(va), stream())
+    return _device_matrix(n, rp, ci, va)
 
 
 # ---------------------------------------------------------------------------
@@ -458,7 +526,7 @@ BASELINE_CONFIGS = {
 }
 
 
-def baseline_problem(name, grid=None):
+def baseline_problem(name, grid=None, device=False):
     """(A, b, levels) for BASELINE.json config ``name`` (C1-C5).
 
     C5 (elasticity) levels refer to the NODE graph (``build_hierarchy(a,
@@ -466,6 +534,7 @@ def baseline_problem(name, grid=None):
 
     ``grid`` overrides the grid side (same construction, smaller size) for
     tests; the field is drawn first, then ``b = rng.standard_normal(n)``.
+    ``device=True`` builds the C2-C4 matrices on the B200 (same values).
     """
     if name == "C5":
         a, b, levels, _ = c5_problem(grid)
@@ -475,11 +544,17 @@ def baseline_problem(name, grid=None):
         shape = tuple([grid] * len(shape))
     rng = np.random.default_rng(seed)
     if block is None:
-        a = diffusion_fv(np.ones(shape))
+        a = (diffusion_fv_device(np.ones(shape), 1, shape) if device
+             else diffusion_fv(np.ones(shape)))
     else:
         if grid is not None:
             block = max(1, min(block, grid // 8 if grid >= 8 else 1))
-        a = diffusion_fv(log_uniform_block_field(shape, block, decades, rng))
+        if device:
+            nb = tuple(s_ // block for s_ in shape)
+            a = diffusion_fv_device(10.0 ** rng.uniform(-decades, decades, size=nb),
+                                    block, shape)
+        else:
+            a = diffusion_fv(log_uniform_block_field(shape, block, decades, rng))
     b = rng.standard_normal(a.n)
     return a, b, levels
 

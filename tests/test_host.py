@@ -55,6 +55,8 @@ def test_header_symbols_are_typed_or_handle_based():
                     "spand_plan_emit_begin", "spand_plan_emit_next", "spand_plan_chunk",
                     "spand_plan_pairs", "spand_plan_scatter", "spand_csr_check",
                     "spand_plan_set_group_weight", "spand_plan_set_digest",
+                    "spand_mm_read", "spand_mm_csr", "spand_mm_error_span", "spand_mm_text",
+                    "spand_mm_free",
                     "spand_collect_create", "spand_collect_destroy", "spand_collect_sizes",
                     "spand_collect_get", "spand_collect_apply", "spand_collect_apply_get",
                     "spand_collect_fine", "spand_collect_stats"}
