@@ -189,6 +189,23 @@ int spand_rrqr_cta_count(void);
 /* co-resident CTA capacity of one wave launch whose tallest panel has vmax
  * live rows (the cooperative grid must not exceed it) */
 int spand_rrqr_capacity(int vmax);
+/* The same wave launched as thread-block clusters of cs (2, 4, 8) CTAs:
+ * every panel's group is a multiple of cs CTAs starting at a multiple of cs
+ * and grid % cs == 0.  Inside the elimination loop each cluster owns the
+ * columns c = cluster index (mod clusters in the group) and splits their
+ * rows over its CTAs; column dots and the pivot norm are summed over the
+ * cluster through distributed shared memory.  Same outputs as
+ * spand_rrqr_wave (bitwise-identical decisions; rounding of the updates may
+ * differ).  vmax <= spand_rrqr_max_rows_clustered(cs). */
+int spand_rrqr_wave_clustered(int npanel, int grid, int vmax, int cs, const int64_t* panels,
+                              const int64_t* nbrs, int32_t* m0, int32_t* off, double eps,
+                              int scheme, int64_t* events, void* stream);
+/* co-resident CTA capacity of a clustered wave (whole clusters of cs) */
+int spand_rrqr_cluster_capacity(int vmax, int cs);
+int spand_rrqr_max_rows_clustered(int cs);
+/* planner: clustered RRQR waves (cs 0/1 = off) for waves whose panels all
+ * have >= min_rows live rows and that fit one cluster per panel */
+int spand_plan_set_cluster(void* h, int cs, int min_rows);
 
 /* ---- near-kernel preservation (EXTENSION, not in the reference; SURVEY.md
  *      §8a-11; CPU restatement oracle/spand_oracle.py sparsify_panel_nk).

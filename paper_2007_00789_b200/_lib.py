@@ -43,6 +43,11 @@ SIGNATURES = {
     "spand_rrqr_wave": [_c_int, _c_int, _c_int, _P, _P, _P, _P, _c_dbl, _c_int, _P, _P],
     "spand_rrqr_cta_count": [],
     "spand_rrqr_capacity": [_c_int],
+    "spand_rrqr_wave_clustered": [_c_int, _c_int, _c_int, _c_int, _P, _P, _P, _P, _c_dbl,
+                                  _c_int, _P, _P],
+    "spand_rrqr_cluster_capacity": [_c_int, _c_int],
+    "spand_rrqr_max_rows_clustered": [_c_int],
+    "spand_plan_set_cluster": [_P, _c_int, _c_int],
     "spand_assemble_final": [_c_int, _P, _c_i64, _P, _P, _P, _c_int, _P, _P],
     "spand_count_nonzero": [_c_int, _P, _P, _P],
     "spand_count_nonzero_pieces": [_c_int, _P, _P, _c_i64, _P, _P, _P, _P],

@@ -128,6 +128,17 @@ int spand_plan_set_group_weight(void* h, int w, double em, double en) {
   return 0;
 }
 
+// clustered RRQR waves: cluster size (0 or 1 = off; 2, 4, 8) and the
+// smallest panel height of a clustered wave
+int spand_plan_set_cluster(void* h, int cs, int min_rows) {
+  Plan* p = static_cast<Plan*>(h);
+  if (cs < 0 || cs > 8 || (cs > 1 && (cs & (cs - 1)))) return -1;
+  p->cluster_cs = cs;
+  p->cluster_min_rows = min_rows;
+  p->layout();   // the workspace bound depends on it
+  return 0;
+}
+
 // near-kernel extension: number of vectors (0 = reference path); resizes
 // the workspace bound, so call before spand_plan_sizes / emission
 int spand_plan_set_nk(void* h, int k) {

@@ -12,6 +12,8 @@
 #include <vector>
 
 extern "C" int spand_rrqr_capacity(int vmax);
+extern "C" int spand_rrqr_cluster_capacity(int vmax, int cs);
+extern "C" int spand_rrqr_max_rows_clustered(int cs);
 
 namespace spand {
 
@@ -138,6 +140,9 @@ struct Plan {
   // 1.105 s here) gives tall panels -- more sequential steps -- more CTAs
   int group_weight = 3;
   double gexp_m = 1.25, gexp_n = 0.5;
+  // clustered RRQR waves (rrqr.cu): cluster size (0 = off) and the smallest
+  // panel height for which a wave is launched clustered
+  int cluster_cs = 0, cluster_min_rows = 256;
   static constexpr int64_t kNkHead = 19;   // nearkernel.cu kWsHead
   int64_t nk_ws(int64_t mc) const { return nk ? kNkHead + 2 * mc * nk + mc * mc : 0; }
 
@@ -393,7 +398,8 @@ struct Plan {
       for (int p : L.active) tri2 += m0[p] * m0[p];
       need = std::max({need, resc, tri2});
       for (int wv = 0; wv < L.nwaves; ++wv) {
-        int64_t rq = 68 * (int64_t)kMaxGroupTotal;
+        int64_t rq = 68 * (int64_t)kMaxGroupTotal, lists = 4 * (int64_t)kMaxGroupTotal;
+        int64_t mn = INT64_MAX, np = 0;
         for (size_t k = 0; k < L.active.size(); ++k) {
           if (L.wave[k] != wv) continue;
           int64_t ncap = 0;
@@ -402,7 +408,14 @@ struct Plan {
           rq += mc * std::max<int64_t>(ncap, 1) + mc * mc + 32 * (ncap + mc) + 32 * mc + 1024 +
                 2 * ncap +
                 3 * mc + 8 + 1024 + (3 * ncap + 1) / 2 + 1 + 1 + 68 + nk_ws(mc);
+          lists += 2 * 8 * std::max<int64_t>(ncap, 1) + 1;
+          mn = std::min(mn, mc);
+          ++np;
         }
+        // a clustered wave's list copies (superset of the emission test)
+        if (cluster_cs > 1 && np > 0 && mn >= cluster_min_rows &&
+            np <= kMaxGroupTotal / cluster_cs)
+          rq += lists;
         need = std::max(need, rq);
       }
     }
@@ -892,6 +905,19 @@ struct Plan {
           }
         int cap = std::max(1, spand_rrqr_capacity((int)vm));
         if (cap_override > 0) cap = std::min(cap, cap_override);
+        // a wave of few large panels runs clustered: every panel gets whole
+        // clusters of cs CTAs (one at least), so cap counts clusters
+        int cs = 1;
+        if (cluster_cs > 1 && cap_override <= 0 && vm >= cluster_min_rows &&
+            vm <= spand_rrqr_max_rows_clustered(cluster_cs)) {
+          int mn = (int)vm;
+          for (size_t k : pan) mn = std::min<int>(mn, (int)m0[L.active[k]]);
+          const int capc = spand_rrqr_cluster_capacity((int)vm, cluster_cs) / cluster_cs;
+          if (mn >= cluster_min_rows && capc >= 1 && (int)pan.size() <= capc) {
+            cs = cluster_cs;
+            cap = capc;
+          }
+        }
         for (size_t c0 = 0; c0 < pan.size(); c0 += cap) {
           const size_t c1e = std::min(pan.size(), c0 + (size_t)cap);
           std::vector<int64_t> works;
@@ -912,7 +938,7 @@ struct Plan {
           for (size_t u = c0; u < c1e; ++u) {
             const size_t k = pan[u];
             const int p = L.active[k];
-            const int g = gs[u - c0];
+            const int g = gs[u - c0] * cs;
             int64_t ncap = 0;
             for (int w : L.anbrs[k]) ncap += m0[w];
             const int64_t mc = m0[p];
@@ -939,12 +965,16 @@ struct Plan {
               qbeg += mc;
               qdst = q2;
             }
+            // clustered: every CTA keeps the cluster's 4 column lists
+            const int64_t lsz =
+                cs > 1 ? (4 * (int64_t)g * (std::max<int64_t>(ncap, 1) / (g / cs) + 2) + 1) / 2 : 0;
+            const int64_t lptr = cs > 1 ? temp_base + 8 * (need + wsz + asz + isz + 1 + nk_ws(mc)) : 0;
             prow.insert(prow.end(),
                         {p, nb0, nb1, temp_base + 8 * need, qdst,
                          temp_base + 8 * (need + wsz), temp_base + 8 * (need + wsz + asz), gbeg,
-                         g, ctr_base + 8 * ctr_next, L.slot[k], ncap, mc, nkws, 0, 0});
+                         g, ctr_base + 8 * ctr_next, L.slot[k], ncap, mc, nkws, lptr, 0});
             ++ctr_next;
-            need += wsz + asz + isz + 1 + nk_ws(mc);
+            need += wsz + asz + isz + 1 + nk_ws(mc) + lsz;
             gbeg += g;
             vmax = std::max(vmax, mc);
           }
@@ -958,7 +988,7 @@ struct Plan {
             launch(8, np, kr, b);                   // basis of u_p, rank r
             launch(9, np, kr, b, 0, colbeg, vmax);  // W <- rotate(H^T W)
           }
-          launch(5, np, a, b, 0, gbeg, vmax);
+          launch(5, np, a, b, 0, gbeg, vmax, cs);
           if (nk) launch(10, np, kr, 0, 0, qbeg, vmax);   // Q = [U_perp q2_c, U, U_perp q2_f]
         }
       }

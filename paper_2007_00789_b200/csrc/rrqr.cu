@@ -24,6 +24,7 @@
 // ~1e-15 relative of a threshold (the events record the margins).
 #include <cooperative_groups.h>
 #include <cstdio>
+#include <type_traits>
 
 #include "common.cuh"
 #include "../../include/spand_b200.h"
@@ -41,7 +42,9 @@ constexpr int kMaxM = 24576;
 //  4 Q (double*, m*m, compact ld = m)  5 aux (double*)  6 iaux (int32*)
 //  7 group_begin  8 group_size  9 counters (uint32[2]: arrivals, release)  10 event slot
 //  11 ncap (column capacity of aux arrays)  12 mcap
-//  13 near-kernel workspace (nearkernel.cu; 0: none)  14-15 unused
+//  13 near-kernel workspace (nearkernel.cu; 0: none)
+//  14 clustered launches: the per-CTA list copies (int32, 4 G (ncap / (G / cs) + 2);
+//     0: inside the int-list region)  15 unused
 // nbr row (4 int64): {w, block ptr, orientation, 0}
 //  orientation 0: block (p, w) stored with rows of p (ld = m0[p])
 //  orientation 1: block (w, p) stored with rows of w (ld = m0[w])
@@ -88,6 +91,14 @@ __device__ __forceinline__ double hot_rho(int m) {
 static_assert(kMinSmem >= 64 * 65 * sizeof(double), "epilogue tile");
 static_assert(kMinSmem >= (size_t)kWarps * 16 * 33 * sizeof(double), "gather tiles");
 static_assert(kColdSmem >= kMinSmem, "cold layout covers the other phases");
+// clustered loop layout in the dynamic shared memory (doubles): exchange
+// partials [2][kXB] | sums [kXB] | pivot rows [kXS] | scratch 4096 | T, Z [32][33]
+constexpr int kXB = 1056, kXS = 512, kHC = 512;
+// partials [2][kXB] | sums [kXB] | pivot rows [kXS] | cp.async stages
+// [2][V, X][32][33] | Z, T [32][33] | hot state: cur, ref [kHC] + 4 int [kHC]
+constexpr int kClEnd = 3 * kXB + kXS + 4 * 32 * 33 + 2 * 32 * 33 + 2 * kHC + 2 * kHC;
+constexpr size_t kClSmem = (size_t)kClEnd * sizeof(double);
+static_assert(kClSmem >= kColdSmem, "clustered layout covers the post-loop phases");
 
 struct Sh {
   double red[kWarps];
@@ -110,6 +121,10 @@ struct Sh {
   unsigned long long fmax;   // bits of the max norm^2 of my frozen columns (>= 0)
   int nb_start[1025];  // column start of each neighbour (panels with <= 1024)
   int wsum[kWarps];
+  int wsum2[2 * kWarps];
+  double ccur[32], cref[32];   // clustered cold maintenance: running norms before the exchanges
+  int nhot_cl, ncold_cl;      // clustered loop: list lengths (identical in the cluster)
+  unsigned long long mcl;     // clustered reclassification: max running norm^2 (bits)
   double* cbase[64];  // frozen GEMM epilogue: column base in the pool
   int64_t cstride[64];
   int fcol[64];
@@ -128,33 +143,117 @@ __device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
 // Group barrier: ctr[0] counts arrivals, the last CTA of generation `gen`
 // publishes gen in ctr[1] (release); the others poll ctr[1] (acquire), so
 // the polled word changes once per barrier instead of once per arrival.
-__device__ __forceinline__ void group_barrier(unsigned* ctr, int G, unsigned& gen,
+// `tgt` accumulates the arrivals expected so far: every CTA arrives at a
+// group barrier (G), only cluster leaders at the clustered loop's step
+// barrier (cluster_step_barrier, G / CS), on the same two words.
+__device__ __forceinline__ void barrier_arrive_wait(unsigned* ctr, unsigned add, bool arrive,
+                                                    unsigned& gen, unsigned& tgt, int tag,
+                                                    int64_t* flag) {
+  __threadfence();
+  ++gen;
+  tgt += add;
+  bool done = false;
+  if (arrive) done = atomicAdd(ctr, 1u) + 1u == tgt;
+  if (done) {
+    st_release(ctr + 1, gen);
+  } else {
+    const long long t0 = clock64();
+    while (ld_acquire(ctr + 1) < gen) {
+      // watchdog: a group that never completes a barrier is a bug; report
+      // and fall through (~2 s) instead of hanging the device
+      if (clock64() - t0 > 4000000000ll) {
+        printf("[spand rrqr] barrier timeout block %d tag %d gen %u ctr %u tgt %u\n",
+               (int)blockIdx.x, tag, gen, ld_acquire(ctr), tgt);
+        if (flag) atomicExch(reinterpret_cast<unsigned long long*>(flag), 1ull);
+        break;
+      }
+    }
+  }
+  __threadfence();
+}
+
+__device__ __forceinline__ void group_barrier(unsigned* ctr, int G, unsigned& gen, unsigned& tgt,
                                               int tag = -1, int64_t* flag = nullptr) {
   __syncthreads();
   if (G > 1) {
-    if (threadIdx.x == 0) {
-      __threadfence();
-      ++gen;
-      const unsigned arrived = atomicAdd(ctr, 1u) + 1u;
-      if (arrived == gen * (unsigned)G) {
-        st_release(ctr + 1, gen);
-      } else {
-        const long long t0 = clock64();
-        while (ld_acquire(ctr + 1) < gen) {
-          // watchdog: a group that never completes a barrier is a bug; report
-          // and fall through (~2 s) instead of hanging the device
-          if (clock64() - t0 > 4000000000ll) {
-            printf("[spand rrqr] barrier timeout block %d tag %d gen %u ctr %u G %d\n",
-                   (int)blockIdx.x, tag, gen, ld_acquire(ctr), G);
-            if (flag) atomicExch(reinterpret_cast<unsigned long long*>(flag), 1ull);
-            break;
-          }
-        }
-      }
-      __threadfence();
-    }
+    if (threadIdx.x == 0) barrier_arrive_wait(ctr, (unsigned)G, true, gen, tgt, tag, flag);
     __syncthreads();
   }
+}
+
+// ---- thread-block clusters (the clustered elimination loop)
+__device__ __forceinline__ unsigned cluster_size_() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_nctarank;\n" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ __attribute__((unused)) unsigned cluster_rank_() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
+  return r;
+}
+// every thread of every CTA of the cluster; release/acquire at cluster scope
+__device__ __forceinline__ void cluster_sync_() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n"
+               "barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+// shared::cluster load of the word at local shared address a in CTA r; no
+// compiler memory clobber (the loads of one exchange overlap; ordering comes
+// from the cluster barrier before them and the __syncthreads after)
+__device__ __forceinline__ double ld_dsmem_nc(unsigned a, unsigned r) {
+  unsigned ra;
+  double v;
+  asm volatile(
+      "mapa.shared::cluster.u32 %1, %2, %3;\n"
+      "ld.shared::cluster.f64 %0, [%1];\n"
+      : "=d"(v), "=&r"(ra)
+      : "r"(a), "r"(r));
+  return v;
+}
+// the clustered loop's step barrier: every CTA's global writes fenced, a
+// cluster barrier, then one arrival per cluster on the group counter; all
+// CTAs poll the release word
+__device__ __forceinline__ void cluster_step_barrier(unsigned* ctr, int NC, bool leader,
+                                                     unsigned& gen, unsigned& tgt, int tag,
+                                                     int64_t* flag) {
+  if (threadIdx.x == 0) __threadfence();
+  cluster_sync_();
+  if (threadIdx.x == 0) barrier_arrive_wait(ctr, (unsigned)NC, leader, gen, tgt, tag, flag);
+  __syncthreads();
+}
+
+// block-wide stable compaction of up to kT flagged items per call: item
+// `val` of thread tid is kept in category cat (1 or 2; 0 drops it) and
+// written to out1 / out2 at base1 / base2 + its rank among the kept items of
+// the same category in thread order.  Returns both counts in c1 / c2 (every
+// thread).  `wsum` needs 2 * kWarps ints.
+__device__ __forceinline__ void stable_split(int cat, int val, int32_t* out1, int base1,
+                                             int32_t* out2, int base2, int* wsum, int& c1,
+                                             int& c2) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const unsigned b1 = __ballot_sync(0xffffffffu, cat == 1);
+  const unsigned b2 = __ballot_sync(0xffffffffu, cat == 2);
+  const unsigned lt = (1u << lane) - 1u;
+  if (lane == 0) {
+    wsum[warp] = __popc(b1);
+    wsum[kWarps + warp] = __popc(b2);
+  }
+  __syncthreads();
+  int o1 = 0, o2 = 0, t1 = 0, t2 = 0;
+#pragma unroll
+  for (int w = 0; w < kWarps; ++w) {
+    if (w < warp) {
+      o1 += wsum[w];
+      o2 += wsum[kWarps + w];
+    }
+    t1 += wsum[w];
+    t2 += wsum[kWarps + w];
+  }
+  if (cat == 1) out1[base1 + o1 + __popc(b1 & lt)] = val;
+  else if (cat == 2) out2[base2 + o2 + __popc(b2 & lt)] = val;
+  c1 = t1;
+  c2 = t2;
+  __syncthreads();
 }
 
 // better(a, b): larger value wins, ties -> smaller position
@@ -169,6 +268,7 @@ __device__ __forceinline__ void cp_async8(double* smem, const double* gmem, bool
 }
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 __device__ __forceinline__ void cp_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::); }
+__device__ __forceinline__ void cp_wait_1() { asm volatile("cp.async.wait_group 1;\n" ::); }
 
 __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
 #ifdef SPAND_DMMA_VOLATILE
@@ -483,7 +583,12 @@ __device__ void qform_batched(double* Q, const double* V, const double* taus, in
   }
 }
 
-__global__ void __launch_bounds__(kT, 2)
+#ifndef SPAND_CL_MINB1
+#define SPAND_CL_MINB1 2
+#endif
+#define SPAND_CL_MINB (kCl ? SPAND_CL_MINB1 : 2)
+template <bool kCl>
+__global__ void __launch_bounds__(kT, SPAND_CL_MINB)
 rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* __restrict__ nbrs,
                  int32_t* __restrict__ m0, int32_t* __restrict__ off, double eps, int scheme_flags,
                  int64_t* __restrict__ events) {
@@ -517,7 +622,7 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
   const int64_t slot = P[10];
   const int64_t ncap = P[11], mcap = P[12];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  unsigned gen = 0;
+  unsigned gen = 0, tgt = 0;
 
   const int offp = off[p];
   const int ldp = m0[p];
@@ -679,6 +784,7 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
       cur[c] = s;
       ref[c] = s;
       pos[c] = c;
+      perm[c] = c;   // position -> column (the clustered loop keeps it current)
       done[c] = 0;
       fofl[c] = 0;
       if (better(s, c, bv, bp)) {
@@ -715,7 +821,7 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
     __syncthreads();
   };
   publish(bv, bp, bc, 0);
-  group_barrier(ctr, G, gen, -1, events + 12 * slot + 9);
+  group_barrier(ctr, G, gen, tgt, -1, events + 12 * slot + 9);
 
   // ---- elimination (unblocked Householder steps on the ACTIVE columns).
   // Inside the loop column c belongs to CTA c % G (interleaved): the
@@ -1088,7 +1194,7 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
       const int c = rank + G * u;
       for (int i = tid; i < m; i += kT) col[i] = (i == c) ? 1.0 : 0.0;
     }
-    group_barrier(ctr, G, gen, 300000, events + 12 * slot + 9);   // every T_b published
+    group_barrier(ctr, G, gen, tgt, 300000, events + 12 * slot + 9);   // every T_b published
     const int nown = (m - rank + G - 1) / G;
     for (int u0 = 0; u0 < nown; u0 += 16) {
       const int ncl = min(16, nown - u0);
@@ -1221,6 +1327,964 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
   };
   int k0 = 0, maint = 0, cpar = 0;
   double last_wv = 0.0;
+  if constexpr (kCl) {
+    const int CS = (int)cluster_size_();
+    // ================= clustered elimination loop =================
+    // The group is NC = G / CS thread-block clusters of CS CTAs.  Column c
+    // belongs to cluster c % NC; within a cluster the ROWS are split: CTA s
+    // owns the 32-row chunks q = s (mod CS), so every CTA of the cluster
+    // works on all of the cluster's columns, over its own rows.  Per step:
+    // one candidate record and one group-counter arrival per cluster; the
+    // pivot column's norm and the hot columns' dot products are summed over
+    // the cluster through distributed shared memory (fixed rank order), so
+    // every CTA of the cluster -- and every cluster, for the pivot
+    // quantities -- computes bit-identical values.  The hot columns' state
+    // (running norms, position, first-order flag) lives in shared memory,
+    // identical copies in the cluster's CTAs; cold columns live in global
+    // memory and are brought up to date every kBlk steps by a cp.async-fed
+    // DMMA stream over the CTA's rows.  Step 0 keeps every column cold: the
+    // first maintenance (k = 1) applies reflector 0 and classifies.
+    const int NC = G / CS, cr = rank / CS, s = rank % CS;
+    const bool leader = s == 0;
+    int64_t* wflag = events + 12 * slot + 9;
+    unsigned long long* rctr = reinterpret_cast<unsigned long long*>(events + 12 * slot + 10);
+    double* xb = vsh;                    // [2][kXB] my partials (read by the peers)
+    double* Sx = xb + 2 * kXB;           // [kXB] the cluster sums
+    double* xs = Sx + kXB;               // pivot column on my rows [kXS]
+    double* stg = xs + kXS;              // [2 stages][V, X][32][33]
+    double (*ZT)[33] = reinterpret_cast<double (*)[33]>(stg + 4 * 32 * 33);
+    double (*TT)[33] = reinterpret_cast<double (*)[33]>(stg + 5 * 32 * 33);
+    double* hcur = stg + 6 * 32 * 33;    // hot state [kHC] x 6
+    double* href = hcur + kHC;
+    int* hc = reinterpret_cast<int*>(href + kHC);
+    int* hpos = hc + kHC;
+    int* hfo = hpos + kHC;
+    int* hk = hfo + kHC;
+    int xpar = 0;
+#ifdef SPAND_RRQR_PHASES
+    long long mt_[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    long long mt_last = 0;
+#define MT(x) do { long long _n = clock64(); if ((x) > 0) mt_[(x)] += _n - mt_last; mt_last = _n; } while (0)
+#else
+#define MT(x) do {} while (0)
+#endif
+    // Sx[0..L) = sum over the cluster's CTAs (rank order) of xb[xpar][0..L)
+    auto exchange = [&](int L) {
+      cluster_sync_();
+      const double* mine = xb + xpar * kXB;
+      for (int i = tid; i < L; i += kT) {
+        // all remote loads in flight at once, then summed in rank order
+        double v[8];
+        const unsigned a = (unsigned)__cvta_generic_to_shared(mine + i);
+#pragma unroll
+        for (int r = 0; r < 8; ++r) v[r] = r < CS ? ld_dsmem_nc(a, (unsigned)r) : 0.0;
+        double t = v[0];
+#pragma unroll
+        for (int r = 1; r < 8; ++r)
+          if (r < CS) t += v[r];
+        Sx[i] = t;
+      }
+      __syncthreads();
+      xpar ^= 1;
+    };
+    // per-CTA copies of the cluster's cold list (ping-pong 0 / 1)
+    const int lcap = (int)(ncap / NC) + 2;
+    int32_t* lbase = P[14] ? reinterpret_cast<int32_t*>(P[14]) : flist + 26 * ncap;
+    auto clist = [&](int which) { return lbase + ((int64_t)which * G + rank) * lcap; };
+    int csel = 0, nh = 0, ncd = 0;
+    // my 32-row chunks intersecting [kk, m): qf, qf + CS, ... (nq of them)
+    auto own_rows = [&](int kk, int& qf, int& nq) {
+      const int qlo = kk >> 5, qhi = (m - 1) >> 5;
+      qf = qlo + (s - qlo % CS + CS) % CS;
+      nq = (m > kk && qf <= qhi) ? (qhi - qf) / CS + 1 : 0;
+    };
+    // candidate of the cluster (identical in its CTAs), the leader writes it
+    auto publish_cl = [&](double v, int64_t ps, int c, int parity) {
+      if (lane == 0) {
+        sh.bval[warp] = v;
+        sh.bpos[warp] = ps;
+        sh.bcol[warp] = c;
+      }
+      __syncthreads();
+      if (tid == 0 && leader) {
+        double vv = sh.bval[0];
+        int64_t pp = sh.bpos[0];
+        int cc = sh.bcol[0];
+        for (int q = 1; q < kWarps; ++q)
+          if (better(sh.bval[q], sh.bpos[q], vv, pp)) {
+            vv = sh.bval[q];
+            pp = sh.bpos[q];
+            cc = sh.bcol[q];
+          }
+        double* rec = cand + (int64_t)(parity * G + cr) * kCR;
+        rec[0] = vv;
+        reinterpret_cast<int64_t*>(rec)[1] = (pp << 32) | (int64_t)(uint32_t)cc;
+        rec[2] = __longlong_as_double((long long)sh.fmax);
+        rec[3] = sh.coldmax;
+      }
+      __syncthreads();
+    };
+    auto warp_best = [&](double& v, int64_t& ps, int& c) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double v2 = __shfl_xor_sync(0xffffffffu, v, o);
+        const int64_t p2 = __shfl_xor_sync(0xffffffffu, ps, o);
+        const int c2 = __shfl_xor_sync(0xffffffffu, c, o);
+        if (better(v2, p2, v, ps)) {
+          v = v2;
+          ps = p2;
+          c = c2;
+        }
+      }
+    };
+    // freeze tests (the classic loop's consider()): a cold (global state)
+    // column, a hot (shared state) entry
+    auto freeze_glob = [&](int c, double cc) -> bool {
+      if (fo_track && cc < thr2_fo) fofl[c] = 1;
+      return cc < thr2 && (fo_track || scheme != 2 || __ldcg(fofl + c) != 0);
+    };
+    auto freeze_hot = [&](int u) -> bool {
+      const double cc = hcur[u];
+      if (fo_track && cc < thr2_fo && !hfo[u]) {
+        hfo[u] = 1;
+        fofl[hc[u]] = 1;
+      }
+      return cc < thr2 && (fo_track || scheme != 2 || hfo[u] != 0);
+    };
+    // ---- cold columns brought up to date with the block's reflectors
+    // ka..kb-1 over my rows: Q_b^T X = X - V T^T (V^T X), the row sums
+    // completed through the cluster; running norms replayed with the
+    // reference's downdate / refresh rule (dense.py:168-178)
+    auto cold_maint_cl = [&](int ka, int kb) {
+      const int nb = kb - ka;
+      const int nc = ncd;
+      if (nb <= 0 || nc == 0) return;
+      const int32_t* lst = clist(csel);
+      int qf, nq;
+      own_rows(ka, qf, nq);
+      const int l4 = lane & 3, l8 = lane >> 2;
+      MT(0);
+      // (1) Gram V_b^T V_b over my rows (8-row units split over the warps) -> T
+      {
+        const int U = 4 * nq;
+        const int u0 = (warp * U) / kWarps, u1 = ((warp + 1) * U) / kWarps;
+        double acc[4][4][2];
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int c = 0; c < 4; ++c) acc[a][c][0] = acc[a][c][1] = 0.0;
+        for (int u = u0; u < u1; ++u) {
+          const int rb = ((qf + CS * (u >> 2)) << 5) + ((u & 3) << 3);
+#pragma unroll
+          for (int ss = 0; ss < 2; ++ss) {
+            const int i = rb + 4 * ss + l4;
+            double f[4];
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+              const int q = t * 8 + l8;
+              f[t] = (i < m && q < nb && i >= ka + q) ? __ldcg(V + (int64_t)(ka + q) * m + i) : 0.0;
+            }
+#pragma unroll
+            for (int a = 0; a < 4; ++a)
+#pragma unroll
+              for (int c = 0; c < 4; ++c) dmma(acc[a][c][0], acc[a][c][1], f[a], f[c]);
+          }
+        }
+        double* R2 = stg;   // [4][32][32] (the stages are idle here)
+        __syncthreads();
+        if (warp < 4) {
+#pragma unroll
+          for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int c = 0; c < 4; ++c)
+#pragma unroll
+              for (int h = 0; h < 2; ++h)
+                R2[warp * 1024 + (a * 8 + l8) * 32 + c * 8 + 2 * l4 + h] = acc[a][c][h];
+        }
+        __syncthreads();
+        if (warp >= 4) {
+#pragma unroll
+          for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int c = 0; c < 4; ++c)
+#pragma unroll
+              for (int h = 0; h < 2; ++h)
+                R2[(warp - 4) * 1024 + (a * 8 + l8) * 32 + c * 8 + 2 * l4 + h] += acc[a][c][h];
+        }
+        __syncthreads();
+        double* P = xb + xpar * kXB;
+        for (int e = tid; e < 1024; e += kT) P[e] = (R2[e] + R2[1024 + e]) + (R2[2048 + e] + R2[3072 + e]);
+        MT(1);
+        exchange(1024);
+        MT(2);
+        for (int e = tid; e < 32 * 32; e += kT) {
+          const int c = e >> 5, q = e & 31;
+          ZT[c][q] = (c < q && q < nb) ? Sx[e] : 0.0;
+        }
+        __syncthreads();
+        if (warp == 0) {
+          for (int jj = 0; jj < nb; ++jj) {
+            const double tj = __ldcg(taus + ka + jj);
+            double v = 0.0;
+            if (lane < jj) {
+              for (int c = lane; c < jj; ++c) v += TT[lane][c] * ZT[c][jj];
+              v *= -tj;
+            }
+            __syncwarp();
+            if (lane < jj) TT[lane][jj] = v;
+            else if (lane == jj) TT[jj][jj] = tj;
+            else TT[lane][jj] = 0.0;
+            __syncwarp();
+          }
+        }
+        __syncthreads();
+      }
+      // (2) 32-column chunks: Y = X^T V_b, Z = Y T, X -= V_b Z^T, streamed over
+      // my 32-row chunks through two cp.async stages of (V_b rows, X rows)
+      const int mt = warp & 3, nh2 = warp >> 2;
+      auto load_stage = [&](int b, int t) {
+        double* Vs = stg + b * 2 * 32 * 33;   // [q][33]
+        double* Xs = Vs + 32 * 33;            // [c][33]
+        const int r0 = (qf + CS * t) << 5;
+#pragma unroll
+        for (int it = 0; it < 4; ++it) {
+          const int e = tid + it * kT;
+          const int q = e >> 5, r = e & 31, i = r0 + r;
+          const bool okv = q < nb && i >= ka + q && i < m;
+          cp_async8(Vs + q * 33 + r, okv ? V + (int64_t)(ka + q) * m + i : V, okv);
+          const int c = sh.fcol[q];
+          const bool okx = c >= 0 && i >= ka && i < m;
+          cp_async8(Xs + q * 33 + r, okx ? W + (int64_t)c * m + i : W, okx);
+        }
+        cp_commit();
+      };
+      for (int ct = 0; ct < nc; ct += 32) {
+        const int ncl = min(32, nc - ct);
+        __syncthreads();
+        if (tid < 32) {
+          const int c = tid < ncl ? lst[ct + tid] : -1;
+          sh.fcol[tid] = c;
+          sh.ccur[tid] = c >= 0 ? __ldcg(cur + c) : 0.0;
+          sh.cref[tid] = c >= 0 ? __ldcg(ref + c) : 0.0;
+        }
+        __syncthreads();
+        MT(1);
+        // ---- Y^T: warp (mt, nh2) -> columns mt*8.., reflectors nh2*16..
+        {
+          double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+          if (nq > 0) load_stage(0, 0);
+          for (int t = 0; t < nq; ++t) {
+            if (t + 1 < nq) {
+              load_stage((t + 1) & 1, t + 1);
+              cp_wait_1();
+            } else {
+              cp_wait_all();
+            }
+            __syncthreads();
+            const double* Vs = stg + (t & 1) * 2 * 32 * 33;
+            const double* Xs = Vs + 32 * 33;
+#pragma unroll
+            for (int kq = 0; kq < 8; ++kq) {
+              const int r = kq * 4 + l4;
+              const double af = Xs[(mt * 8 + l8) * 33 + r];
+#pragma unroll
+              for (int ni = 0; ni < 2; ++ni)
+                dmma(acc[ni][0], acc[ni][1], af, Vs[(nh2 * 16 + ni * 8 + l8) * 33 + r]);
+            }
+            __syncthreads();
+          }
+          double* P = xb + xpar * kXB;
+#pragma unroll
+          for (int ni = 0; ni < 2; ++ni)
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+              P[(mt * 8 + l8) * 32 + nh2 * 16 + ni * 8 + 2 * l4 + h] = acc[ni][h];
+        }
+        MT(3);
+        exchange(32 * 32);
+        MT(2);
+        // ---- Z^T = Y^T T
+        for (int e = tid; e < 32 * 32; e += kT) {
+          const int c = e >> 5, q = e & 31;
+          double z = 0.0;
+          if (c < ncl && q < nb)
+            for (int pp = 0; pp <= q; ++pp) z += Sx[c * 32 + pp] * TT[pp][q];
+          ZT[c][q] = z;
+        }
+        double* P2 = xb + xpar * kXB;
+        for (int e = tid; e < 32 * 33; e += kT) P2[e] = 0.0;
+        __syncthreads();
+        // ---- X -= V_b Z^T: warp -> columns mt*8.. (B = Z^T), row tiles nh2, nh2 + 2 of each chunk
+        {
+          double bz[8];
+#pragma unroll
+          for (int kq = 0; kq < 8; ++kq) bz[kq] = ZT[mt * 8 + l8][kq * 4 + l4];
+          int cc2[2];
+#pragma unroll
+          for (int h = 0; h < 2; ++h) cc2[h] = sh.fcol[mt * 8 + 2 * l4 + h];
+          double tl[2] = {0.0, 0.0};
+          if (nq > 0) load_stage(0, 0);
+          for (int t = 0; t < nq; ++t) {
+            if (t + 1 < nq) {
+              load_stage((t + 1) & 1, t + 1);
+              cp_wait_1();
+            } else {
+              cp_wait_all();
+            }
+            __syncthreads();
+            const double* Vs = stg + (t & 1) * 2 * 32 * 33;
+            const double* Xs = Vs + 32 * 33;
+            const int r0 = (qf + CS * t) << 5;
+#pragma unroll
+            for (int uu = 0; uu < 2; ++uu) {
+              const int rl = (nh2 + 2 * uu) * 8 + l8;
+              double acc2[2] = {0.0, 0.0};
+#pragma unroll
+              for (int kq = 0; kq < 8; ++kq) dmma(acc2[0], acc2[1], Vs[(kq * 4 + l4) * 33 + rl], bz[kq]);
+              const int i = r0 + rl;
+              if (i >= ka && i < m) {
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                  const int c = cc2[h];
+                  if (c < 0) continue;
+                  const int cl = mt * 8 + 2 * l4 + h;
+                  const double xv = Xs[cl * 33 + rl] - acc2[h];
+                  W[(int64_t)c * m + i] = xv;
+                  if (i < kb) P2[cl * 32 + (i - ka)] = xv;
+                  else tl[h] += xv * xv;
+                }
+              }
+            }
+            __syncthreads();
+          }
+          // lanes sharing l4 hold the same columns: reduce over l8, then the
+          // two row halves (warps w, w + 4) in fixed order
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            double t = tl[h];
+            t += __shfl_xor_sync(0xffffffffu, t, 4);
+            t += __shfl_xor_sync(0xffffffffu, t, 8);
+            t += __shfl_xor_sync(0xffffffffu, t, 16);
+            tl[h] = t;
+          }
+          if (l8 == 0) {
+#pragma unroll
+            for (int h = 0; h < 2; ++h) Sx[nh2 * 32 + mt * 8 + 2 * l4 + h] = tl[h];
+          }
+        }
+        __syncthreads();
+        MT(4);
+        if (tid < 32) P2[1024 + tid] = Sx[tid] + Sx[32 + tid];
+        exchange(32 * 33);
+        MT(2);
+        // replay the block's steps (identical in every CTA of the cluster)
+        if (tid < ncl) {
+          const int c = sh.fcol[tid];
+          double suf = Sx[1024 + tid];
+          for (int t = kb - 1; t >= ka; --t) {
+            ZT[tid][t - ka] = suf;
+            const double rk = Sx[tid * 32 + (t - ka)];
+            suf += rk * rk;
+          }
+          double cn = sh.ccur[tid], rf = sh.cref[tid];
+          for (int t = ka; t < kb; ++t) {
+            const double rk = Sx[tid * 32 + (t - ka)];
+            double d = cn - rk * rk;
+            if (d < 0.0) d = 0.0;
+            if (d < 0.01 * rf) {
+              d = ZT[tid][t - ka];
+              rf = d;
+              if (leader) atomicAdd(rctr, 1ull);
+            }
+            cn = d;
+          }
+          cur[c] = cn;
+          ref[c] = rf;
+        }
+        __syncthreads();
+        MT(5);
+      }
+    };
+#ifdef SPAND_RRQR_PHASES
+    long long cl_hotsteps = 0, cl_rounds = 0, cl_maint = 0, cl_flush = 0, cl_cold = 0;
+#endif
+    int blk_len = 1;   // step 0 keeps every column cold; the first block is one step
+    int flushes = 0;
+    while (k < kmax) {
+      PH(0);
+      if (maint) {
+        PH(6);
+#ifdef SPAND_RRQR_PHASES
+        ++cl_maint;
+        cl_flush += maint == 2;
+        cl_cold += ncd;
+#endif
+        cold_maint_cl(k0, k);
+        MT(0);
+        // ---- reclassify hot (shared) ++ cold (global) -> hot (shared) + cold (global)
+        const int32_t* cin = clist(csel);
+        int32_t* cout = clist(csel ^ 1);
+        const int tot = nh + ncd;
+        if (tid == 0) sh.mcl = 0ull;
+        __syncthreads();
+        for (int u = tid; u < tot; u += kT) {
+          double cc;
+          bool fz;
+          if (u < nh) {
+            cc = hcur[u];
+            fz = freeze_hot(u);
+          } else {
+            const int c = cin[u - nh];
+            cc = __ldcg(cur + c);
+            fz = freeze_glob(c, cc);
+          }
+          if (!fz) atomicMax(&sh.mcl, (unsigned long long)__double_as_longlong(cc));
+        }
+        __syncthreads();
+        const double mcl = __longlong_as_double((long long)sh.mcl);
+        // hot iff within rho of min(last pivot value, the cluster's max):
+        // the cluster's largest column is always hot, so no cold column can
+        // reach the next pivot value right after a classification
+        double tau_hot = hot_rho(m) * (maint == 2 ? mcl : fmin(last_wv, mcl));
+        if (tot > kHC) {
+          // the hot state holds kHC entries: raise the threshold toward the max
+          for (int it = 0; it < 60; ++it) {
+            if (tid == 0) sh.nact = 0;
+            __syncthreads();
+            int cnt = 0;
+            for (int u = tid; u < tot; u += kT) {
+              const double cc = u < nh ? hcur[u] : __ldcg(cur + cin[u - nh]);
+              const bool fz = u < nh ? freeze_hot(u) : freeze_glob(cin[u - nh], cc);
+              cnt += (!fz && cc >= tau_hot);
+            }
+            atomicAdd(&sh.nact, cnt);
+            __syncthreads();
+            const int tot_hot = sh.nact;
+            __syncthreads();
+            if (tot_hot <= kHC || tau_hot >= mcl) break;
+            tau_hot = fmin(mcl, 0.5 * (tau_hot + mcl));
+          }
+        }
+        if (tid == 0) sh.coldmax = 0.0;
+        __syncthreads();
+        int nh2 = 0, nc2 = 0;
+        for (int b0 = 0; b0 < tot; b0 += kT) {
+          const int u = b0 + tid;
+          int cat = 0, c = -1, ps = 0, fo = 0;
+          double cc = 0.0, rf = 0.0;
+          if (u < tot) {
+            if (u < nh) {
+              c = hc[u];
+              cc = hcur[u];
+              rf = href[u];
+              ps = hpos[u];
+              fo = hfo[u];
+              cat = freeze_hot(u) ? 0 : (cc >= tau_hot ? 1 : 2);
+            } else {
+              c = cin[u - nh];
+              cc = __ldcg(cur + c);
+              cat = freeze_glob(c, cc) ? 0 : (cc >= tau_hot ? 1 : 2);
+              if (cat == 1) {
+                rf = __ldcg(ref + c);
+                ps = __ldcg(pos + c);
+                fo = __ldcg(fofl + c);
+              }
+            }
+            if (cat == 0) {
+              done[c] = 2;
+              atomicMax(&sh.fmax, (unsigned long long)__double_as_longlong(cc));
+            }
+          }
+          // hot ranks first (capped at kHC; the excess stays cold), then cold
+          const unsigned b1 = __ballot_sync(0xffffffffu, cat == 1);
+          if (lane == 0) sh.wsum2[warp] = __popc(b1);
+          __syncthreads();
+          int o1 = 0, t1 = 0;
+#pragma unroll
+          for (int w = 0; w < kWarps; ++w) {
+            if (w < warp) o1 += sh.wsum2[w];
+            t1 += sh.wsum2[w];
+          }
+          const int hpos1 = nh2 + o1 + __popc(b1 & ((1u << lane) - 1u));
+          if (cat == 1 && hpos1 >= kHC) cat = 2;
+          const unsigned b2 = __ballot_sync(0xffffffffu, cat == 2);
+          __syncthreads();
+          if (lane == 0) sh.wsum2[kWarps + warp] = __popc(b2);
+          __syncthreads();
+          int o2 = 0, t2 = 0;
+#pragma unroll
+          for (int w = 0; w < kWarps; ++w) {
+            if (w < warp) o2 += sh.wsum2[kWarps + w];
+            t2 += sh.wsum2[kWarps + w];
+          }
+          if (cat == 1) {
+            hc[hpos1] = c;
+            hcur[hpos1] = cc;
+            href[hpos1] = rf;
+            hpos[hpos1] = ps;
+            hfo[hpos1] = fo;
+          } else if (cat == 2) {
+            cout[nc2 + o2 + __popc(b2 & ((1u << lane) - 1u))] = c;
+            if (u < nh) {   // hot -> cold: its state goes back to global memory
+              cur[c] = cc;
+              ref[c] = rf;
+            }
+            atomicMax(reinterpret_cast<unsigned long long*>(&sh.coldmax),
+                      (unsigned long long)__double_as_longlong(cc));
+          }
+          nh2 = min(kHC, nh2 + t1);
+          nc2 += t2;
+          __syncthreads();
+        }
+        if (nc2 == 0 && tid == 0) sh.coldmax = -1.0;
+        nh = nh2;
+        ncd = nc2;
+        csel ^= 1;
+        k0 = k;
+        blk_len = kBlk;
+        double bvm = -1.0;
+        int64_t bpm = 0x7fffffffffffLL;
+        int bcm = -1;
+        __syncthreads();
+        for (int u = tid; u < nh; u += kT) {
+          if (better(hcur[u], hpos[u], bvm, bpm)) {
+            bvm = hcur[u];
+            bpm = hpos[u];
+            bcm = hc[u];
+          }
+        }
+        warp_best(bvm, bpm, bcm);
+        __syncthreads();
+        publish_cl(bvm, bpm, bcm, cpar ^ 1);
+        MT(6);
+        cpar ^= 1;
+        maint = 0;
+        cluster_step_barrier(ctr, NC, leader, gen, tgt, -2, wflag);
+        PH(0);
+      }
+      // ---- winning column over the records (as the classic loop)
+      const int nrec = k == 0 ? G : NC;   // the prologue published one record per CTA
+      double wv = -1.0, wf = -1.0, wc = -1.0;
+      int64_t wp = 0x7fffffffffffLL, wpc = 0;
+      int wq = 0x7fffffff;
+      const int par = cpar;
+      for (int q = tid; q < nrec; q += kT) {
+        const double* rec = cand + (int64_t)(par * G + q) * kCR;
+        const double v = __ldcg(rec);
+        const int64_t pc = __ldcg(reinterpret_cast<const long long*>(rec) + 1);
+        const double fm = __ldcg(rec + 2);
+        if (fm > wf) wf = fm;
+        const double cm = __ldcg(rec + 3);
+        if (cm > wc) wc = cm;
+        const int64_t ps = pc >> 32;
+        if (better(v, ps, wv, wp) || (v == wv && ps == wp && q < wq)) {
+          wv = v;
+          wp = ps;
+          wpc = pc;
+          wq = q;
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double v2 = __shfl_xor_sync(0xffffffffu, wv, o);
+        const int64_t p2 = __shfl_xor_sync(0xffffffffu, wp, o);
+        const int64_t c2 = __shfl_xor_sync(0xffffffffu, wpc, o);
+        const int q2 = __shfl_xor_sync(0xffffffffu, wq, o);
+        const double f2 = __shfl_xor_sync(0xffffffffu, wf, o);
+        if (f2 > wf) wf = f2;
+        const double c3 = __shfl_xor_sync(0xffffffffu, wc, o);
+        if (c3 > wc) wc = c3;
+        if (better(v2, p2, wv, wp) || (v2 == wv && p2 == wp && q2 < wq)) {
+          wv = v2;
+          wp = p2;
+          wpc = c2;
+          wq = q2;
+        }
+      }
+      if (lane == 0) {
+        sh.bval[warp] = wv;
+        sh.bpos[warp] = wp;
+        sh.bpc[warp] = wpc;
+        sh.bq[warp] = wq;
+        sh.bfm[warp] = wf;
+        sh.bcm[warp] = wc;
+      }
+      __syncthreads();
+      wv = sh.bval[0];
+      wp = sh.bpos[0];
+      wpc = sh.bpc[0];
+      wq = sh.bq[0];
+      wf = sh.bfm[0];
+      wc = sh.bcm[0];
+      for (int w2 = 1; w2 < kWarps; ++w2) {
+        const double v2 = sh.bval[w2];
+        const int64_t p2 = sh.bpos[w2];
+        const int q2 = sh.bq[w2];
+        if (sh.bfm[w2] > wf) wf = sh.bfm[w2];
+        if (sh.bcm[w2] > wc) wc = sh.bcm[w2];
+        if (better(v2, p2, wv, wp) || (v2 == wv && p2 == wp && q2 < wq)) {
+          wv = v2;
+          wp = p2;
+          wpc = sh.bpc[w2];
+          wq = q2;
+        }
+      }
+      __syncthreads();
+      if (k > 0 && wc >= 0.0 && wc >= wv) {
+        // a cold column's (stale, upper-bound) norm reaches the pivot value
+        maint = 2;
+        if (++flushes > 4) __trap();   // classification cannot converge (kHC ties)
+        continue;
+      }
+      flushes = 0;
+      if (wv < 0.0) {
+        eta_last = sqrt(wf > 0.0 ? wf : 0.0);
+        break;
+      }
+      const int jpos = (int)wp;
+      const int j = (int)(uint32_t)(wpc & 0xffffffffLL);
+      PH(1);
+      // ---- my rows of the pivot column (cp.async, zero-filled), x0 owner
+      int qf, nq;
+      own_rows(k, qf, nq);
+      const bool own_k = ((k >> 5) % CS) == s;
+      {
+        const double* colj = W + (int64_t)j * m;
+        for (int e = tid; e < nq * 32; e += kT) {
+          const int i = ((qf + CS * (e >> 5)) << 5) + (e & 31);
+          const bool ok = i >= k && i < m;
+          cp_async8(xs + e, ok ? colj + i : colj, ok);
+        }
+        cp_commit();
+      }
+      // the hot entry at position k moves to jpos (reference swap order)
+      for (int u = tid; u < nh; u += kT)
+        if (hpos[u] == k) hpos[u] = jpos;
+      // ---- pivot quantities (identical everywhere): eta, beta, tau
+      double eta = 0.0, beta = 0.0, tau = 0.0, v0 = 0.0;
+      auto take_eta = [&](double s2, double x0) -> bool {
+        eta = sqrt(s2);
+        eta_last = eta;
+        if (k == 0) {
+          r11 = eta;
+          if (r11 == 0.0) return true;
+          thr2 = 0.25 * (stop_tol * r11) * (stop_tol * r11);
+          thr2_fo = 0.25 * (eps * r11) * (eps * r11);
+        }
+        if (fo_track && eta < eps * r11) {
+          // k_c reached: the first-order run stops here and finishes its
+          // cold columns as Q^T a (identical decisions in every CTA)
+          fo_track = false;
+          const int32_t* cl2 = clist(csel);
+          for (int u = tid; u < ncd; u += kT) fofl[cl2[u]] = 1;
+          __syncthreads();
+        }
+        if (eta < stop_tol * r11) return true;
+        if (eta > 0.0) {
+          beta = x0 >= 0.0 ? -eta : eta;
+          v0 = x0 - beta;
+          tau = 2.0 / (s2 - x0 * x0 + v0 * v0);
+        }
+        return false;
+      };
+      // my partial |x|^2 (CTA sum in fixed order) and x0
+      auto x_partials = [&]() {
+        cp_wait_all();
+        __syncthreads();
+        double sx = 0.0;
+        for (int e = tid; e < nq * 32; e += kT) sx += xs[e] * xs[e];
+        sx = warp_sum(sx);
+        if (lane == 0) sh.red[warp] = sx;
+        __syncthreads();
+        if (tid == 0) {
+          double t = 0.0;
+#pragma unroll
+          for (int w2 = 0; w2 < kWarps; ++w2) t += sh.red[w2];
+          double* P = xb + xpar * kXB;
+          P[0] = t;
+          P[1] = own_k ? xs[k & 31] : 0.0;
+        }
+      };
+      // V column k on my rows, position bookkeeping (rank 0 keeps pos /
+      // perm current: nobody else reads them inside the loop), pivot data
+      auto after_eta = [&]() {
+        for (int e = tid; e < nq * 32; e += kT) {
+          const int i = ((qf + CS * (e >> 5)) << 5) + (e & 31);
+          if (i >= k && i < m) V[(int64_t)k * m + i] = eta > 0.0 ? (i == k ? v0 : xs[e]) : 0.0;
+        }
+        if (rank == 0 && tid == 0) {
+          piv[k] = eta;
+          taus[k] = tau;
+          betas[k] = beta;
+          const int ck = __ldcg(perm + k);   // the column at position k
+          pos[ck] = jpos;
+          perm[jpos] = ck;
+          pos[j] = k;
+          perm[k] = j;
+          done[j] = 1;
+        }
+      };
+      if (k == 0) {
+        // ---- step 0: no hot columns; every other column starts cold (or
+        // frozen: the classic loop's consider() at k = 0)
+        x_partials();
+        exchange(2);
+        if (take_eta(Sx[0], Sx[1])) break;
+        after_eta();
+        int32_t* c0l = clist(csel);
+        const int nin = n > cr ? (n - cr + NC - 1) / NC : 0;
+        int nc2 = 0;
+        if (tid == 0) sh.coldmax = 0.0;
+        __syncthreads();
+        for (int b0 = 0; b0 < nin; b0 += kT) {
+          const int u = b0 + tid;
+          int cat = 0, c = -1;
+          if (u < nin) {
+            c = cr + NC * u;
+            if (c != j) {
+              const double cc = __ldcg(cur + c);
+              if (freeze_glob(c, cc)) {
+                done[c] = 2;
+                atomicMax(&sh.fmax, (unsigned long long)__double_as_longlong(cc));
+              } else {
+                cat = 2;
+                atomicMax(reinterpret_cast<unsigned long long*>(&sh.coldmax),
+                          (unsigned long long)__double_as_longlong(cc));
+              }
+            }
+          }
+          int a1, a2;
+          stable_split(cat, c, c0l, 0, c0l, nc2, sh.wsum2, a1, a2);
+          nc2 += a2;
+        }
+        if (nc2 == 0 && tid == 0) sh.coldmax = -1.0;
+        ncd = nc2;
+        nh = 0;
+        __syncthreads();
+        publish_cl(-1.0, 0x7fffffffffffLL, -1, cpar ^ 1);
+        cpar ^= 1;
+        last_wv = wv;
+        ++k;
+        if (k - k0 >= blk_len) maint = 1;
+        cluster_step_barrier(ctr, NC, leader, gen, tgt, k, wflag);
+        continue;
+      }
+      double bv1 = -1.0;
+      int64_t bp1 = 0x7fffffffffffLL;
+      int bc1 = -1;
+      bool stop = false, eta_done = false;
+      PH(3);
+      // one round: UW hot entries per warp, E of my 32-row chunks in registers
+      auto hot_round = [&](auto Et, auto Ut, int r0) {
+        constexpr int E = decltype(Et)::value, UW = decltype(Ut)::value;
+        int us[UW];
+        double a[UW][E];
+#pragma unroll
+        for (int t = 0; t < UW; ++t) {
+          const int u = r0 + warp + kWarps * t;
+          us[t] = u < nh ? u : -1;
+        }
+#pragma unroll
+        for (int t = 0; t < UW; ++t) {
+          const double* col = W + (int64_t)(us[t] >= 0 ? hc[us[t]] : 0) * m;
+#pragma unroll
+          for (int e = 0; e < E; ++e) {
+            const int i = ((qf + CS * e) << 5) + lane;
+            a[t][e] = (us[t] >= 0 && e < nq && i >= k && i < m) ? col[i] : 0.0;
+          }
+        }
+        if (!eta_done) x_partials();
+        double* P = xb + xpar * kXB;
+#pragma unroll
+        for (int t = 0; t < UW; ++t) {
+          double d = 0.0;
+#pragma unroll
+          for (int e = 0; e < E; ++e)
+            if (e < nq) d += xs[e * 32 + lane] * a[t][e];
+          d = warp_sum(d);
+          const double akv = __shfl_sync(0xffffffffu, a[t][0], k & 31);
+          if (lane == 0) {
+            P[2 + 2 * (warp + kWarps * t)] = d;
+            P[3 + 2 * (warp + kWarps * t)] = own_k ? akv : 0.0;
+          }
+        }
+        PH(2);
+        exchange(2 + 2 * kWarps * UW);
+        PH(3);
+        if (!eta_done) {
+          eta_done = true;
+          if (take_eta(Sx[0], Sx[1])) {
+            stop = true;
+            return;
+          }
+          after_eta();
+          // this step's filter (the classic loop's consider(), after the stop
+          // tests): keep flags for every hot entry; frozen ones marked now
+          for (int u = tid; u < nh; u += kT) {
+            const int c = hc[u];
+            bool keep = false;
+            if (c != j) {
+              if (freeze_hot(u)) {
+                done[c] = 2;
+                atomicMax(&sh.fmax, (unsigned long long)__double_as_longlong(hcur[u]));
+              } else {
+                keep = true;
+              }
+            }
+            hk[u] = keep;
+          }
+          __syncthreads();
+        }
+        double tl[UW], cn[UW];
+        bool need = false;
+#pragma unroll
+        for (int t = 0; t < UW; ++t) {
+          tl[t] = 0.0;
+          cn[t] = 0.0;
+          if (us[t] < 0 || !hk[us[t]]) continue;
+          const int i2 = 2 + 2 * (warp + kWarps * t);
+          const double ak = Sx[i2 + 1];
+          const double w = tau * (Sx[i2] - beta * ak);
+          const double rk = ak - w * v0;
+          double* col = W + (int64_t)hc[us[t]] * m;
+          double tail = 0.0;
+#pragma unroll
+          for (int e = 0; e < E; ++e) {
+            const int i = ((qf + CS * e) << 5) + lane;
+            if (e < nq && i >= k && i < m) {
+              const double y = a[t][e] - w * (i == k ? v0 : xs[e * 32 + lane]);
+              col[i] = y;
+              if (i > k) tail += y * y;
+            }
+          }
+          tl[t] = warp_sum(tail);
+          double c2 = hcur[us[t]] - rk * rk;
+          if (c2 < 0.0) c2 = 0.0;
+          cn[t] = c2;
+          need |= c2 < 0.01 * href[us[t]];
+        }
+        // (identical in every CTA of the cluster)
+        if (__syncthreads_or(need)) {
+          double* P3 = xb + xpar * kXB;
+          if (lane == 0) {
+#pragma unroll
+            for (int t = 0; t < UW; ++t) P3[warp + kWarps * t] = tl[t];
+          }
+          exchange(kWarps * UW);
+#pragma unroll
+          for (int t = 0; t < UW; ++t) tl[t] = Sx[warp + kWarps * t];
+        }
+#pragma unroll
+        for (int t = 0; t < UW; ++t) {
+          if (us[t] < 0 || !hk[us[t]]) continue;
+          const int u = us[t];
+          double c2 = cn[t];
+          if (c2 < 0.01 * href[u]) {
+            // exact tail norm of the updated column (dense.py:172-178)
+            c2 = tl[t];
+            if (lane == 0) {
+              href[u] = c2;
+              if (leader) atomicAdd(rctr, 1ull);
+            }
+          }
+          if (lane == 0) {
+            hcur[u] = c2;
+            if (better(c2, hpos[u], bv1, bp1)) {
+              bv1 = c2;
+              bp1 = hpos[u];
+              bc1 = hc[u];
+            }
+          }
+        }
+      };
+      // the round shape must be the same in every CTA of the cluster (one
+      // exchange per round): it follows the largest chunk count
+      const int nqx = m > k ? ((m - 1) / 32 - k / 32) / CS + 1 : 0;
+      for (int r0 = 0; r0 == 0 || r0 < nh;) {
+        if (nqx <= 4) {
+          hot_round(std::integral_constant<int, 4>{}, std::integral_constant<int, 4>{}, r0);
+          r0 += kWarps * 4;
+        } else if (nqx <= 8) {
+          hot_round(std::integral_constant<int, 8>{}, std::integral_constant<int, 4>{}, r0);
+          r0 += kWarps * 4;
+        } else {
+          hot_round(std::integral_constant<int, kXS / 32>{}, std::integral_constant<int, 2>{}, r0);
+          r0 += kWarps * 2;
+        }
+        if (stop) break;
+      }
+      if (stop) break;
+      PH(4);
+#ifdef SPAND_RRQR_PHASES
+      cl_hotsteps += nh;
+      cl_rounds += (nh + 15) / 16;
+#endif
+      // compact the hot state in place (stable: kept entries keep their order)
+      {
+        int nk = 0;
+        __syncthreads();
+        for (int b0 = 0; b0 < nh; b0 += kT) {
+          const int u = b0 + tid;
+          const bool keep = u < nh && hk[u];
+          int c = 0, ps = 0, fo = 0;
+          double cc = 0.0, rf = 0.0;
+          if (keep) {
+            c = hc[u];
+            ps = hpos[u];
+            fo = hfo[u];
+            cc = hcur[u];
+            rf = href[u];
+          }
+          const unsigned b1 = __ballot_sync(0xffffffffu, keep);
+          if (lane == 0) sh.wsum2[warp] = __popc(b1);
+          __syncthreads();
+          int o1 = 0, t1 = 0;
+#pragma unroll
+          for (int w = 0; w < kWarps; ++w) {
+            if (w < warp) o1 += sh.wsum2[w];
+            t1 += sh.wsum2[w];
+          }
+          if (keep) {
+            const int d = nk + o1 + __popc(b1 & ((1u << lane) - 1u));
+            hc[d] = c;
+            hpos[d] = ps;
+            hfo[d] = fo;
+            hcur[d] = cc;
+            href[d] = rf;
+          }
+          nk += t1;
+          __syncthreads();
+        }
+        nh = nk;
+      }
+      warp_best(bv1, bp1, bc1);
+      __syncthreads();
+      publish_cl(bv1, bp1, bc1, cpar ^ 1);
+      cpar ^= 1;
+      last_wv = wv;
+      ++k;
+      if (k - k0 >= blk_len) maint = 1;
+      PH(5);
+      cluster_step_barrier(ctr, NC, leader, gen, tgt, k, wflag);
+    }
+#ifdef SPAND_RRQR_PHASES
+    if (tid == 0 && m >= SPAND_PHASE_MMIN && (rank == 0 || rank == G / 2))
+      printf("[rrqr cl] p %d m %d n %d G %d rank %d k %d hot-col-steps %lld rounds(16) %lld maint %lld flush %lld cold-cols %lld | maint kcyc: gram %lld xch %lld Ypass %lld Zupd %lld replay %lld reclass %lld\n",
+             p, m, n, G, rank, k, cl_hotsteps, cl_rounds, cl_maint, cl_flush, cl_cold, mt_[1] / 1000, mt_[2] / 1000, mt_[3] / 1000, mt_[4] / 1000, mt_[5] / 1000, mt_[6] / 1000);
+#endif
+    const bool k_c_seen_cl = scheme == 2 && !fo_track;
+    if (scheme == 2 && ncd > 0 && k_c_seen_cl) cold_maint_cl(k0, k);
+    __syncthreads();
+    {
+      const int32_t* cl2 = clist(csel);
+      for (int u = tid; u < ncd; u += kT) {
+        const int c = cl2[u];
+        if (scheme != 2 || !k_c_seen_cl || __ldcg(fofl + c)) done[c] = 2;
+      }
+    }
+    if (tid == 0) sh.ncold = 0;
+    __syncthreads();
+  } else {
   while (k < kmax) {
     PH(0);
     if (maint) {
@@ -1298,7 +2362,7 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
       __syncthreads();
       publish(bv, bp, bc, cpar ^ 1);
       cpar ^= 1;
-      group_barrier(ctr, G, gen, -2, events + 12 * slot + 9);
+      group_barrier(ctr, G, gen, tgt, -2, events + 12 * slot + 9);
       PH(0);
     }
     // ---- winning column: max value, smallest current position (ties in
@@ -1560,8 +2624,9 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
     ++k;
     if (k - k0 >= kBlk) maint = 1;
     PH(5);
-    group_barrier(ctr, G, gen, k, events + 12 * slot + 9);
+    group_barrier(ctr, G, gen, tgt, k, events + 12 * slot + 9);
   }
+  }   // classic loop
   const int k_stop = k;
   const bool k_c_seen_sf = scheme == 2 && !fo_track;
   // remaining cold columns finish like frozen ones (Q^T a from the original)
@@ -1575,7 +2640,7 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
     if (scheme != 2 || !k_c_seen_sf || fofl[c]) done[c] = 2;
   }
   // frozen list of my own columns (static ownership c % G)
-  group_barrier(ctr, G, gen, -5, events + 12 * slot + 9);
+  group_barrier(ctr, G, gen, tgt, -5, events + 12 * slot + 9);
   if (tid == 0) sh.nfrz = 0;
   __syncthreads();
   for (int c = rank + G * tid; c < n; c += G * kT)
@@ -1590,7 +2655,7 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
 #endif
   // every CTA must be done reading this step's pivot column (the loop may
   // have stopped on it) before owners patch their columns
-  group_barrier(ctr, G, gen, 100000 + k, events + 12 * slot + 9);
+  group_barrier(ctr, G, gen, tgt, 100000 + k, events + 12 * slot + 9);
   // pivoted columns: R(t, t) = beta, zeros below (dense.py:161-162)
   for (int c = c0 + warp; c < c1; c += kWarps) {
     const int t = pos[c];
@@ -1698,7 +2763,7 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
       __syncwarp();
     }
   }
-  group_barrier(ctr, G, gen, 200000, events + 12 * slot + 9);   // Q and W complete
+  group_barrier(ctr, G, gen, tgt, 200000, events + 12 * slot + 9);   // Q and W complete
   TL(trs);
   // R rows t < T of Q^T a for a list of columns (a = ORIGINAL column) on
   // the tensor cores (DMMA).  to_w = false: frozen columns, a restored in W,
@@ -1814,7 +2879,7 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
     if (n2 > 0 && k_c > 0) qt_a(l2, n2, k_c, true);
     // the write-back below covers contiguous column ranges, the product
     // above the interleaved ownership
-    group_barrier(ctr, G, gen, 300000, events + 12 * slot + 9);
+    group_barrier(ctr, G, gen, tgt, 300000, events + 12 * slot + 9);
   }
   TL(tg);
   // ---- write back (non-frozen columns): new slot s < n_fine <- R row
@@ -1874,7 +2939,7 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
     ev[8] = __double_as_longlong(r11);
   }
   // every CTA of the group must finish reading off[p] before it moves
-  group_barrier(ctr, G, gen, -1, events + 12 * slot + 9);
+  group_barrier(ctr, G, gen, tgt, -1, events + 12 * slot + 9);
   if (rank == 0 && tid == 0) off[p] = offp + n_fine;
 }
 }  // namespace
@@ -1888,9 +2953,9 @@ int spand_rrqr_cta_count(void) {
   // capacity for panels up to 4224 rows (the tile staging size); taller
   // panels need more shared memory and are launched with smaller groups
   const size_t smem = kColdSmem;
-  cudaFuncSetAttribute(rrqr_wave_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  cudaFuncSetAttribute(rrqr_wave_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)(kMaxM * sizeof(double) > kColdSmem ? kMaxM * sizeof(double) : kColdSmem));
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, rrqr_wave_kernel, kT, smem) != cudaSuccess)
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, rrqr_wave_kernel<false>, kT, smem) != cudaSuccess)
     return -1;
   return per * sms;
 }
@@ -1913,9 +2978,9 @@ int spand_rrqr_capacity(int vmax) {
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   size_t smem = kColdSmem;
   if ((size_t)vmax * sizeof(double) > smem) smem = (size_t)vmax * sizeof(double);
-  cudaFuncSetAttribute(rrqr_wave_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  cudaFuncSetAttribute(rrqr_wave_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)(kMaxM * sizeof(double) > kColdSmem ? kMaxM * sizeof(double) : kColdSmem));
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, rrqr_wave_kernel, kT, smem) != cudaSuccess)
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, rrqr_wave_kernel<false>, kT, smem) != cudaSuccess)
     return -1;
   cached_dev = dev;
   cached_smem = smem;
@@ -1932,12 +2997,71 @@ int spand_rrqr_wave(int npanel, int grid, int vmax, const int64_t* panels, const
   size_t smem = (size_t)(vmax > 0 ? vmax : 1) * sizeof(double);
   if (smem < tile_bytes) smem = tile_bytes;
   cudaError_t e = cudaFuncSetAttribute(
-      rrqr_wave_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      rrqr_wave_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
       (int)(kMaxM * sizeof(double) > kColdSmem ? kMaxM * sizeof(double) : kColdSmem));
   if (e != cudaSuccess) return (int)e;
   void* args[] = {&npanel, &panels, &nbrs, &m0, &off, &eps, &scheme, &events};
-  e = cudaLaunchCooperativeKernel((void*)rrqr_wave_kernel, dim3(grid), dim3(kT), args, smem,
+  e = cudaLaunchCooperativeKernel((void*)rrqr_wave_kernel<false>, dim3(grid), dim3(kT), args, smem,
                                   (cudaStream_t)stream);
+  if (e != cudaSuccess) return (int)e;
+  return 0;
+}
+
+// Clustered variant (one launch per wave of large panels): thread-block
+// clusters of cs CTAs; every panel's group is a multiple of cs CTAs starting
+// at a multiple of cs.  The elimination loop then splits each cluster's
+// columns by rows over its CTAs (see the kernel).  Co-residency of the
+// whole grid is guaranteed by the cooperative attribute.
+static cudaLaunchConfig_t cluster_cfg(int grid, int cs, size_t smem, cudaStream_t st,
+                                      cudaLaunchAttribute* at) {
+  cudaLaunchConfig_t cfg = {};
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = (unsigned)cs;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeCooperative;
+  at[1].val.cooperative = 1;
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(kT);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cfg.attrs = at;
+  cfg.numAttrs = 2;
+  return cfg;
+}
+
+int spand_rrqr_cluster_capacity(int vmax, int cs) {
+  if (cs < 2 || cs > 8 || (cs & (cs - 1))) return -1;
+  size_t smem = kClSmem;
+  if ((size_t)vmax * sizeof(double) > smem) smem = (size_t)vmax * sizeof(double);
+  if (cudaFuncSetAttribute(rrqr_wave_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)(kMaxM * sizeof(double) > kColdSmem ? kMaxM * sizeof(double)
+                                                                    : kColdSmem)) != cudaSuccess)
+    return -1;
+  cudaLaunchAttribute at[2];
+  cudaLaunchConfig_t cfg = cluster_cfg(cs * 8, cs, smem, 0, at);
+  int ncl = 0;
+  if (cudaOccupancyMaxActiveClusters(&ncl, (void*)rrqr_wave_kernel<true>, &cfg) != cudaSuccess) return -1;
+  return ncl * cs;
+}
+
+int spand_rrqr_max_rows_clustered(int cs) { return kXS * cs; }
+
+int spand_rrqr_wave_clustered(int npanel, int grid, int vmax, int cs, const int64_t* panels,
+                              const int64_t* nbrs, int32_t* m0, int32_t* off, double eps,
+                              int scheme, int64_t* events, void* stream) {
+  if (npanel < 0 || grid < 0 || vmax < 0 || vmax > kXS * cs) return -1;
+  if (cs < 2 || cs > 8 || (cs & (cs - 1)) || grid % cs) return -1;
+  if (npanel == 0 || grid == 0) return 0;
+  size_t smem = (size_t)(vmax > 0 ? vmax : 1) * sizeof(double);
+  if (smem < kClSmem) smem = kClSmem;
+  cudaError_t e = cudaFuncSetAttribute(
+      rrqr_wave_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      (int)(kMaxM * sizeof(double) > kColdSmem ? kMaxM * sizeof(double) : kColdSmem));
+  if (e != cudaSuccess) return (int)e;
+  cudaLaunchAttribute at[2];
+  cudaLaunchConfig_t cfg = cluster_cfg(grid, cs, smem, (cudaStream_t)stream, at);
+  e = cudaLaunchKernelEx(&cfg, rrqr_wave_kernel<true>, npanel, panels, nbrs, m0, off, eps, scheme, events);
   if (e != cudaSuccess) return (int)e;
   return 0;
 }

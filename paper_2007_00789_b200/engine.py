@@ -104,6 +104,12 @@ class NativePlan:
             lib.spand_plan_set_group_weight(
                 self.h, gw, float(_os.environ.get("SPAND_GROUP_EM", "1.25")),
                 float(_os.environ.get("SPAND_GROUP_EN", "0.5")))
+        cl = _os.environ.get("SPAND_RRQR_CLUSTER")
+        if cl is not None:
+            lib.spand_plan_set_cluster.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int]
+            if lib.spand_plan_set_cluster(
+                    self.h, int(cl), int(_os.environ.get("SPAND_RRQR_CLUSTER_MIN", "256"))) != 0:
+                raise ValueError(f"SPAND_RRQR_CLUSTER={cl}: cluster size must be 0, 2, 4 or 8")
         if nk:
             if lib.spand_plan_set_nk(self.h, int(nk)) != 0:
                 raise ValueError(f"at most 16 near-kernel vectors, got {nk}")
@@ -346,10 +352,13 @@ class Engine:
                     e0 = t.cuda.Event(enable_timing=True)
                     e1 = t.cuda.Event(enable_timing=True)
                     e0.record()
-                _lib.call("spand_rrqr_wave", cnt, x0, x1, P(ao), P(bo), gm0, goff,
-                          float(self.eps),
-                          SCHEME_CODE[self.scheme] | (4 if self.local_errors else 0),
-                          ctypes.c_void_p(evb), st)
+                flags = SCHEME_CODE[self.scheme] | (4 if self.local_errors else 0)
+                if x2 > 1:
+                    _lib.call("spand_rrqr_wave_clustered", cnt, x0, x1, x2, P(ao), P(bo),
+                              gm0, goff, float(self.eps), flags, ctypes.c_void_p(evb), st)
+                else:
+                    _lib.call("spand_rrqr_wave", cnt, x0, x1, P(ao), P(bo), gm0, goff,
+                              float(self.eps), flags, ctypes.c_void_p(evb), st)
                 if WAVE_LOG is not None:
                     e1.record()
                     slots = [int(prog[ao + 16 * q + 10]) for q in range(cnt)] if prog is not None else []

@@ -16,9 +16,11 @@ from .kernels import Geometry
 MAX_ROWS = 24576   # rrqr.cu kMaxM
 
 
-def rrqr_single(a, eps, scheme, group=None, pad=0):
+def rrqr_single(a, eps, scheme, group=None, pad=0, cluster=0):
     """``pad`` > 0 stores the panel inside a larger block (live window at an
-    offset, as for an interface sparsified for the second time)."""
+    offset, as for an interface sparsified for the second time).
+    ``cluster`` = 2, 4 or 8 runs the clustered variant of the kernel
+    (``spand_rrqr_wave_clustered``) with ``group`` CTAs (a multiple of it)."""
     t = require_cuda()
     m, n = a.shape
     if m > MAX_ROWS:
@@ -32,6 +34,8 @@ def rrqr_single(a, eps, scheme, group=None, pad=0):
     blk = to_dev(np.ascontiguousarray(big.T).ravel() if big.size else np.zeros(1))
     cap = max(1, _lib.load().spand_rrqr_capacity(max(m, 1)))
     g = group or max(1, min(cap, n // 64, (m * n) // 65536 + 1))
+    if cluster > 1:
+        g = max(cluster, (g // cluster) * cluster)
     ncap, mcap = max(np_, 1), max(mp, 1)
     wsz = mcap * ncap + mcap * mcap + 32 * (ncap + mcap) + 32 * mcap + 1024   # + T blocks
     asz = 2 * ncap + 3 * mcap + 2 * g * 34 + 8 + 1024
@@ -41,15 +45,24 @@ def rrqr_single(a, eps, scheme, group=None, pad=0):
     ctr = t.zeros(2, dtype=t.int32, device=dev())
     events = t.zeros(12, dtype=t.int64, device=dev())
     wb = work.data_ptr()
+    lists = None
+    if cluster > 1:
+        lists = t.zeros(4 * g * (ncap // (g // cluster) + 2) + 2, dtype=t.int32, device=dev())
     prow = [[0, 0, 1, wb, q.data_ptr(), wb + 8 * wsz, wb + 8 * (wsz + asz), 0, g,
-             ctr.data_ptr(), 0, ncap, mcap, 0, 0, 0]]
+             ctr.data_ptr(), 0, ncap, mcap, 0,
+             lists.data_ptr() if lists is not None else 0, 0]]
     nrow = [[1, blk.data_ptr(), 0, 0]]
     pd = to_dev(np.asarray(prow, dtype=np.int64))
     nd = to_dev(np.asarray(nrow, dtype=np.int64))
     if isinstance(scheme, str):
         scheme = SchemeKind.from_string(scheme)
-    _lib.call("spand_rrqr_wave", 1, g, max(m, 1), ptr(pd), ptr(nd), ptr(geo.m0),
-              ptr(geo.off), float(eps), SCHEME_CODE[scheme], ptr(events), stream())
+    if cluster > 1:
+        _lib.call("spand_rrqr_wave_clustered", 1, g, max(m, 1), cluster, ptr(pd), ptr(nd),
+                  ptr(geo.m0), ptr(geo.off), float(eps), SCHEME_CODE[scheme], ptr(events),
+                  stream())
+    else:
+        _lib.call("spand_rrqr_wave", 1, g, max(m, 1), ptr(pd), ptr(nd), ptr(geo.m0),
+                  ptr(geo.off), float(eps), SCHEME_CODE[scheme], ptr(events), stream())
     ev = events.cpu().numpy()
     k_stop, k_c, n_fine = int(ev[3]), int(ev[4]), int(ev[6])
     qh = q[:m * m].cpu().numpy().reshape(m, m).T.copy() if m else np.zeros((0, 0))
