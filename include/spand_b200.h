@@ -118,6 +118,22 @@ int spand_apply_runs(int nchunk, const int64_t* chunks, const int64_t* contrib, 
  * nitem, chunks, nchunk, contrib, grid, 0, 0}, offsets in int64 units into
  * the device image), spand_gemv_items then spand_apply_runs on `stream`.
  * Same result as issuing the 2 nphase calls one by one. */
+/* The whole apply_m (forward + backward pass) as one persistent launch per
+ * group of <= 4 right-hand sides: units (8 int64: {phase, kind, index,
+ * first dep, ndeps, counter, counter2, 0}) run in order once their
+ * dependency counters ({counter, target} pairs) are reached; ctrs (nctr
+ * uint64) are zeroed here before every launch; phases: 8 int64 per phase
+ * {tasks, items, chunks, contributions (offsets into image), scratch base}.
+ * Schedule: spand_collect_dataflow. */
+int spand_apply_dataflow(int64_t nunit, const int64_t* units, const int64_t* deps, int64_t nctr,
+                         unsigned long long* ctrs, const int64_t* phases, const int64_t* image,
+                         double* x, int64_t ldx, double* scratch, int64_t ldscr, int nvec,
+                         void* stream);
+/* Nonzero-row bits of column-major panels (the elimination panels of the
+ * apply, reference schemes.py:102-112 stores them densely): panels rows
+ * {address, ld, rows, cols, first word}; bit i of the panel's words is set
+ * iff row i holds a nonzero.  The apply image keeps only row runs. */
+int spand_row_bits(int npanel, const int64_t* panels, uint32_t* bits, void* stream);
 int spand_apply_pass(int nphase, const int64_t* ph, const int64_t* image, double* x,
                      int64_t ldx, double* scratch, int64_t ldscr, int nvec, void* stream);
 
@@ -347,8 +363,18 @@ int spand_collect_get(void* h, int64_t* ops, int64_t* segs, int64_t* perm, int64
                       int64_t* lsum, int64_t* views, int64_t* fidx);
 int spand_collect_fine(void* h, int64_t* out);
 int spand_collect_stats(void* h, int64_t* out);
+/* bits: the nonzero-row bits of the elimination panels (spand_row_bits over
+ * spand_collect_flag_panels; null: every row kept) */
 int spand_collect_apply(void* h, int64_t pool_base, int64_t fac_base, int64_t xbuf,
-                        int64_t idx_addr, int64_t* out);
+                        int64_t idx_addr, const uint32_t* bits, int64_t* out);
+/* out[0] panels, out[1] bit words */
+int spand_collect_flag_sizes(void* h, int64_t* out);
+/* the dataflow schedule of the apply (after spand_collect_apply): out[4] =
+ * units, deps, counters, scratch doubles per right-hand side */
+int spand_collect_dataflow_sizes(void* h, int64_t* out);
+int spand_collect_dataflow(void* h, int64_t* units, int64_t* deps, int64_t* phases);
+/* 5 int64 per panel: {address, ld, rows, cols, first word} */
+int spand_collect_flag_panels(void* h, int64_t pool_base, int64_t* out);
 int spand_collect_apply_get(void* h, int64_t* image, int64_t* phases);
 
 #ifdef __cplusplus

@@ -34,6 +34,13 @@ SIGNATURES = {
                             _c_int, _P],
     "spand_apply_runs": [_c_int, _P, _P, _P, _c_i64, _P, _c_i64, _c_int, _P],
     "spand_apply_pass": [_c_int, _P, _P, _P, _c_i64, _P, _c_i64, _c_int, _P],
+    "spand_row_bits": [_c_int, _P, _P, _P],
+    "spand_run_launches": [_c_int, _P, _c_i64, _P, _P, _P, _P, _c_i64, _P, _c_dbl, _c_int, _P,
+                           _c_i64, _c_int, _c_dbl, _c_int, _P, _P],
+    "spand_launch_timer_reset": [],
+    "spand_launch_timer_read": [_P, _P],
+    "spand_apply_dataflow": [_c_i64, _P, _P, _c_i64, _P, _P, _P, _P, _c_i64, _P, _c_i64, _c_int,
+                             _P],
     "spand_potrf_batched": [_c_int, _P, _P, _P, _P, _c_int, _c_int, _P],
     "spand_trtri_batched": [_c_int, _P, _P, _P, _P],
     "spand_trtri_tiles": [_c_int, _P, _P, _P, _P],
@@ -102,7 +109,8 @@ _HOST_ONLY = {"spand_plan_sizes", "spand_plan_emit", "spand_plan_program",
               "spand_rrqr_cta_count", "spand_rrqr_capacity", "spand_spmv_blocks", "spand_dot_blocks"}
 
 # entry points issuing several kernels whose callers count them per kernel
-_COUNTED_BY_CALLER = {"spand_apply_pass"}
+_COUNTED_BY_CALLER = {"spand_apply_pass", "spand_run_launches"}
+_HOST_ONLY |= {"spand_launch_timer_reset", "spand_launch_timer_read"}
 
 
 def call(name, *args):
@@ -135,6 +143,18 @@ def launches():
     return sum(COUNTS.values())
 
 
+def profile_mask(type_names):
+    """Launch-type bit mask of the native launcher for the active profile()
+    (0: none): every type, or those whose entry point is profiled."""
+    if _PROFILE is None or _capturing():
+        return 0
+    mask = 0
+    for typ, nm in type_names.items():
+        if _PROFILE_NAMES is None or nm in _PROFILE_NAMES:
+            mask |= 1 << typ
+    return mask
+
+
 class profile:
     """Context manager: per-entry-point device time (ms) on the current
     stream, measured with CUDA events around every call() (or only around
@@ -150,6 +170,7 @@ class profile:
         _PROFILE = []
         _PROFILE_NAMES = self.names
         self.result = {}
+        load().spand_launch_timer_reset()
         return self
 
     def __exit__(self, *exc):
@@ -158,9 +179,21 @@ class profile:
         torch.cuda.synchronize()
         out = {}
         for name, e0, e1 in _PROFILE:
+            if name == "spand_run_launches":
+                continue
             ms = e0.elapsed_time(e1)
             tot, cnt = out.get(name, (0.0, 0))
             out[name] = (tot + ms, cnt + 1)
+        # launches issued by the native program launcher (timed there)
+        import numpy as np
+        from .engine import LAUNCH_NAMES
+        ms = np.zeros(32)
+        n = np.zeros(32, dtype=np.int64)
+        load().spand_launch_timer_read(ms.ctypes.data, n.ctypes.data)
+        for typ, nm in LAUNCH_NAMES.items():
+            if n[typ]:
+                tot, cnt = out.get(nm, (0.0, 0))
+                out[nm] = (tot + float(ms[typ]), cnt + int(n[typ]))
         _PROFILE = None
         self.result = {k: {"ms": round(v[0], 3), "calls": v[1]} for k, v in
                        sorted(out.items(), key=lambda kv: -kv[1][0])}

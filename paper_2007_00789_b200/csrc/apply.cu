@@ -3,6 +3,8 @@
 // schemes.py:102-112,136-140,162-166,188-192 (apply_inv / apply_inv_t).
 // HBM-bound: every payload entry is read once per pass, coalesced along the
 // column-major storage; vectors are staged in shared memory.
+#include <cstdio>
+
 #include "common.cuh"
 #include "../../include/spand_b200.h"
 
@@ -152,8 +154,13 @@ gemv_tiles_kernel(const int64_t* __restrict__ tiles, const int64_t* __restrict__
 constexpr int kItemRows = 128;   // trans 0: max rows per item
 constexpr int kItemCols = 4;     // trans 1: max columns per item
 
+template <bool kCoherent = false>
 __device__ __forceinline__ double load_in(const Task& T, const double* xv, int64_t ldx, int v,
                                           int kk) {
+  // kCoherent: x changes while the kernel runs (dataflow apply): L2 loads
+  if (kCoherent)   // plain loads: valid after the dependency acquire (L1 invalidated)
+    return T.in_kind == 0 ? xv[reinterpret_cast<const int32_t*>(T.in)[kk]]
+                          : reinterpret_cast<const double*>(T.in)[kk + v * ldx];
   return T.in_kind == 0 ? xv[reinterpret_cast<const int32_t*>(T.in)[kk]]
                         : __ldg(reinterpret_cast<const double*>(T.in) + kk + v * ldx);
 }
@@ -161,14 +168,13 @@ __device__ __forceinline__ double load_in(const Task& T, const double* xv, int64
 // NV right-hand sides per launch (x and scratch column-major with leading
 // dimensions ldx / ldscr): every payload element is loaded once and used
 // for all NV vectors (multi-RHS apply, reference factorize.py:262-267).
-template <int NV>
-__global__ void __launch_bounds__(kThreads, NV == 1 ? 4 : 2)
-gemv_items_kernel(int nitem, const int64_t* __restrict__ items, const int64_t* __restrict__ tasks,
-                  const double* __restrict__ x, int64_t ldx, double* __restrict__ scratch,
-                  int64_t ldscr, int v0) {
+// one work item by one warp (see gemv_items_kernel)
+template <int NV, bool kCoherent>
+__device__ __forceinline__ void gemv_item(int it, const int64_t* __restrict__ items,
+                                          const int64_t* __restrict__ tasks, const double* x,
+                                          int64_t ldx, double* scratch, int64_t ldscr, int v0) {
   const int lane = threadIdx.x & 31;
-  const int W = gridDim.x * kWarps;
-  for (int it = blockIdx.x * kWarps + (threadIdx.x >> 5); it < nitem; it += W) {
+  {
     // packed item (2 x int64): {task << 32 | ob << 12 | oc, out_off << 28 | kb << 11 | kc}
     const int64_t w0 = __ldg(items + 2 * (int64_t)it), w1 = __ldg(items + 2 * (int64_t)it + 1);
     const int64_t t0 = w0 >> 32;
@@ -187,8 +193,8 @@ gemv_items_kernel(int nitem, const int64_t* __restrict__ items, const int64_t* _
         double x0[NV], x1[NV];
 #pragma unroll
         for (int v = 0; v < NV; ++v) {
-          x0[v] = load_in(T, x + (v0 + v) * ldx, ldx, v0 + v, kb + c);
-          x1[v] = load_in(T, x + (v0 + v) * ldx, ldx, v0 + v, kb + c + 1);
+          x0[v] = load_in<kCoherent>(T, x + (v0 + v) * ldx, ldx, v0 + v, kb + c);
+          x1[v] = load_in<kCoherent>(T, x + (v0 + v) * ldx, ldx, v0 + v, kb + c + 1);
         }
         const double* c0 = T.M + (int64_t)phys_col(kb + c, T.rot, T.cols) * T.ld + ob;
         const double* c1 = T.M + (int64_t)phys_col(kb + c + 1, T.rot, T.cols) * T.ld + ob;
@@ -214,7 +220,7 @@ gemv_items_kernel(int nitem, const int64_t* __restrict__ items, const int64_t* _
         }
 #pragma unroll
         for (int v = 0; v < NV; ++v) {
-          const double x0 = load_in(T, x + (v0 + v) * ldx, ldx, v0 + v, kb + c);
+          const double x0 = load_in<kCoherent>(T, x + (v0 + v) * ldx, ldx, v0 + v, kb + c);
 #pragma unroll
           for (int q = 0; q < 4; ++q) acc[v][q] += m0v[q] * x0;
         }
@@ -241,7 +247,7 @@ gemv_items_kernel(int nitem, const int64_t* __restrict__ items, const int64_t* _
 #pragma unroll
         for (int v = 0; v < NV; ++v)
 #pragma unroll
-          for (int u = 0; u < 2; ++u) in2[v][u] = load_in(T, x + (v0 + v) * ldx, ldx, v0 + v, kb + r + 32 * u);
+          for (int u = 0; u < 2; ++u) in2[v][u] = load_in<kCoherent>(T, x + (v0 + v) * ldx, ldx, v0 + v, kb + r + 32 * u);
 #pragma unroll
         for (int u = 0; u < 2; ++u)
 #pragma unroll
@@ -259,7 +265,7 @@ gemv_items_kernel(int nitem, const int64_t* __restrict__ items, const int64_t* _
         for (int j = 0; j < kItemCols; ++j) p[j] = j < oc ? __ldg(col[j] + r) : 0.0;
 #pragma unroll
         for (int v = 0; v < NV; ++v) {
-          const double i0 = load_in(T, x + (v0 + v) * ldx, ldx, v0 + v, kb + r);
+          const double i0 = load_in<kCoherent>(T, x + (v0 + v) * ldx, ldx, v0 + v, kb + r);
 #pragma unroll
           for (int j = 0; j < kItemCols; ++j) acc[v][j] += p[j] * i0;
         }
@@ -278,6 +284,16 @@ gemv_items_kernel(int nitem, const int64_t* __restrict__ items, const int64_t* _
       }
     }
   }
+}
+
+template <int NV>
+__global__ void __launch_bounds__(kThreads, NV == 1 ? 4 : 2)
+gemv_items_kernel(int nitem, const int64_t* __restrict__ items, const int64_t* __restrict__ tasks,
+                  const double* __restrict__ x, int64_t ldx, double* __restrict__ scratch,
+                  int64_t ldscr, int v0) {
+  const int W = gridDim.x * kWarps;
+  for (int it = blockIdx.x * kWarps + (threadIdx.x >> 5); it < nitem; it += W)
+    gemv_item<NV, false>(it, items, tasks, x, ldx, scratch, ldscr, v0);
 }
 
 __global__ void __launch_bounds__(kThreads)
@@ -344,9 +360,223 @@ runs_kernel(const int64_t* __restrict__ chunks, const int64_t* __restrict__ cont
     }
   }
 }
+// sum of one output of a chunk (runs_kernel layout) by one thread (the
+// dataflow kernel's warp path)
+__device__ __forceinline__ double chunk_sum(const double* sv, const int64_t* __restrict__ contrib,
+                                            int64_t cb, int64_t ce) {
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+  int64_t c = cb;
+  for (; c + 3 < ce; c += 4) {
+    s0 += __ldcg(sv + __ldg(contrib + c));
+    s1 += __ldcg(sv + __ldg(contrib + c + 1));
+    s2 += __ldcg(sv + __ldg(contrib + c + 2));
+    s3 += __ldcg(sv + __ldg(contrib + c + 3));
+  }
+  for (; c < ce; ++c) s0 += __ldcg(sv + __ldg(contrib + c));
+  return (s0 + s1) + (s2 + s3);
+}
+
+// ---- dataflow apply: the whole apply_m (forward + backward) in one launch.
+// Persistent warps take units (work items, accumulation chunks) in phase
+// order from a global counter, kDisp at a time, wait for their dependency
+// counters (host schedule, collect.cpp build_dataflow) and bump their own
+// when done: no grid-wide barrier between the ~690 phases, independent
+// subtrees of the nested dissection overlap.  Sums keep a fixed order
+// (deterministic).  Dependencies only point to earlier units, so warps
+// holding earlier units always make progress (no deadlock); a warp flushes
+// its pending signals before it waits.
+__device__ __forceinline__ unsigned long long ld_acq_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];\n" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// one accumulation chunk (runs_kernel layout, <= 64 outputs) by one warp
+template <int NV>
+__device__ __forceinline__ void chunk_warp(const int64_t* __restrict__ ch,
+                                           const int64_t* __restrict__ contrib, double* x,
+                                           int64_t ldx, const double* scratch, int64_t ldscr,
+                                           int v0) {
+  const int lane = threadIdx.x & 31;
+  const int64_t dst = __ldg(ch), eoff = __ldg(ch + 5), cb = __ldg(ch + 3), ce = __ldg(ch + 4);
+  const int len = (int)__ldg(ch + 1), md = (int)__ldg(ch + 2);
+  const int32_t* idx = reinterpret_cast<const int32_t*>(__ldg(ch + 6));
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int i = lane + 32 * h;
+    if (i >= len) continue;
+    const int64_t e = eoff + i;
+    const int64_t d = idx ? (int64_t)idx[e] : dst + e;
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      const double t = chunk_sum(scratch + e + (int64_t)(v0 + v) * ldscr, contrib, cb, ce);
+      double* xd = x + d + (int64_t)(v0 + v) * ldx;
+      *xd = md == 0 ? t : __ldcg(xd) - t;
+    }
+  }
+}
+
+constexpr int kDisp = 1;   // units per dispatch
+
+template <int NV>
+__global__ void __launch_bounds__(kThreads, NV == 1 ? 4 : 2)
+dataflow_kernel(int64_t nunit, const int64_t* __restrict__ units, const int64_t* __restrict__ deps,
+                unsigned long long* ctrs, const int64_t* __restrict__ ph,
+                const int64_t* __restrict__ image, double* x, int64_t ldx, double* scratch,
+                int64_t ldscr, int v0) {
+  const int lane = threadIdx.x & 31;
+  // pending signals (lane 0): consecutive units bumping the same counters
+  int64_t pc0 = -1, pc1 = -1;
+  unsigned long long pn0 = 0, pn1 = 0;
+  auto flush = [&]() {
+    __syncwarp();
+    if (lane == 0 && (pn0 || pn1)) {
+      __threadfence();
+      if (pn0) atomicAdd(ctrs + pc0, pn0);
+      if (pn1) atomicAdd(ctrs + pc1, pn1);
+    }
+    pn0 = pn1 = 0;
+    pc0 = pc1 = -1;
+  };
+#ifdef SPAND_DF_STATS
+  long long st_wait = 0, st_item = 0, st_chunk = 0, st_disp = 0, st_flush = 0, n_item = 0, n_chunk = 0;
+  long long t_ = clock64();
+#define DFT(var) do { long long _n = clock64(); var += _n - t_; t_ = _n; } while (0)
+#else
+#define DFT(var) do {} while (0)
+#endif
+  for (;;) {
+    long long u0 = 0;
+    DFT(st_flush);
+    if (lane == 0) u0 = (long long)atomicAdd(ctrs, (unsigned long long)kDisp);
+    u0 = __shfl_sync(0xffffffffu, u0, 0);
+    DFT(st_disp);
+    if (u0 >= nunit) break;
+    const long long u1 = min((long long)nunit, u0 + kDisp);
+    for (long long u = u0; u < u1; ++u) {
+      const int64_t* U = units + 8 * u;
+      const int64_t g = __ldg(U), kind = __ldg(U + 1), li = __ldg(U + 2);
+      const int64_t doff = __ldg(U + 3), dn = __ldg(U + 4), inc0 = __ldg(U + 5), inc1 = __ldg(U + 6);
+      if (dn > 0) {
+        flush();
+        // every lane acquires (the loads of one address coalesce)
+        for (int64_t d = 0; d < dn; ++d) {
+          const int64_t c = __ldg(deps + 2 * (doff + d));
+          const unsigned long long tg = (unsigned long long)__ldg(deps + 2 * (doff + d) + 1);
+          unsigned ns = 32;
+          while (ld_acq_u64(ctrs + c) < tg) {
+            __nanosleep(ns);
+            if (ns < 1024) ns <<= 1;
+          }
+        }
+      }
+      DFT(st_wait);
+      const int64_t* P = ph + 8 * g;
+      double* scr = scratch + __ldg(P + 4);
+      if (kind == 0) {
+        gemv_item<NV, true>((int)li, image + __ldg(P + 1), image + __ldg(P), x, ldx, scr, ldscr, v0);
+        DFT(st_item);
+#ifdef SPAND_DF_STATS
+        ++n_item;
+#endif
+      } else {
+        chunk_warp<NV>(image + __ldg(P + 2) + 8 * li, image + __ldg(P + 3), x, ldx, scr, ldscr, v0);
+        DFT(st_chunk);
+#ifdef SPAND_DF_STATS
+        ++n_chunk;
+#endif
+      }
+      // signal at once: dependents are on the critical path
+      pc0 = inc0;
+      pn0 = 1;
+      if (inc1 >= 0) {
+        pc1 = inc1;
+        pn1 = 1;
+      }
+      flush();
+    }
+  }
+  flush();
+#ifdef SPAND_DF_STATS
+  if (lane == 0) {
+    unsigned long long* S = ctrs + 1;   // debug: stats after the counters (caller sizes)
+    (void)S;
+    printf("[df] blk %d warp %d wait %lld item %lld chunk %lld disp %lld flush %lld items %lld chunks %lld\n",
+           (int)blockIdx.x, (int)(threadIdx.x >> 5), st_wait / 1000, st_item / 1000, st_chunk / 1000,
+           st_disp / 1000, st_flush / 1000, n_item, n_chunk);
+  }
+#endif
+}
+
+// Nonzero-row bits of column-major panels (rows {address, ld, rows, cols,
+// first word}): bit i of the panel's words is set iff row i has a nonzero.
+// One CTA per panel, a warp per 32-row word (coalesced down each column).
+__global__ void __launch_bounds__(kThreads)
+row_bits_kernel(const int64_t* __restrict__ panels, uint32_t* __restrict__ bits) {
+  const int64_t* r = panels + 5 * (int64_t)blockIdx.x;
+  const double* M = reinterpret_cast<const double*>(r[0]);
+  const int64_t ld = r[1];
+  const int rows = (int)r[2], cols = (int)r[3];
+  const int64_t w0 = r[4];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int wd = warp; wd * 32 < rows; wd += kWarps) {
+    const int i = wd * 32 + lane;
+    bool nz = false;
+    if (i < rows)
+      for (int j = 0; j < cols && !nz; ++j) nz = __ldg(M + i + (int64_t)j * ld) != 0.0;
+    const unsigned b = __ballot_sync(0xffffffffu, nz);
+    if (lane == 0) bits[w0 + wd] = b;
+  }
+}
 }  // namespace
 
 extern "C" {
+
+int spand_apply_dataflow(int64_t nunit, const int64_t* units, const int64_t* deps, int64_t nctr,
+                         unsigned long long* ctrs, const int64_t* phases, const int64_t* image,
+                         double* x, int64_t ldx, double* scratch, int64_t ldscr, int nvec,
+                         void* stream) {
+  if (nunit < 0 || nctr < 1 || nvec < 1) return -1;
+  if (nunit == 0) return 0;
+  static int sms = 0, occ1 = 0, occ2 = 0, occ4 = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ1, dataflow_kernel<1>, kThreads, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, dataflow_kernel<2>, kThreads, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ4, dataflow_kernel<4>, kThreads, 0);
+  }
+  cudaStream_t st = as_stream(stream);
+  for (int v0 = 0; v0 < nvec;) {
+    const int left = nvec - v0;
+    cudaError_t e = cudaMemsetAsync(ctrs, 0, (size_t)nctr * sizeof(unsigned long long), st);
+    if (e != cudaSuccess) return (int)e;
+    if (left >= 4) {
+      dataflow_kernel<4><<<sms * occ4, kThreads, 0, st>>>(nunit, units, deps, ctrs, phases, image,
+                                                         x, ldx, scratch, ldscr, v0);
+      v0 += 4;
+    } else if (left >= 2) {
+      dataflow_kernel<2><<<sms * occ2, kThreads, 0, st>>>(nunit, units, deps, ctrs, phases, image,
+                                                         x, ldx, scratch, ldscr, v0);
+      v0 += 2;
+    } else {
+      dataflow_kernel<1><<<sms * occ1, kThreads, 0, st>>>(nunit, units, deps, ctrs, phases, image,
+                                                         x, ldx, scratch, ldscr, v0);
+      v0 += 1;
+    }
+    SPAND_CHECK_LAUNCH();
+  }
+  return 0;
+}
+
+int spand_row_bits(int npanel, const int64_t* panels, uint32_t* bits, void* stream) {
+  if (npanel < 0) return -1;
+  if (npanel == 0) return 0;
+  row_bits_kernel<<<npanel, kThreads, 0, as_stream(stream)>>>(panels, bits);
+  SPAND_CHECK_LAUNCH();
+  return 0;
+}
 
 int spand_apply_runs(int nchunk, const int64_t* chunks, const int64_t* contrib, double* x,
                      int64_t ldx, const double* scratch, int64_t ldscr, int nvec, void* stream) {

@@ -32,10 +32,16 @@ struct Task {
   int64_t out_start;   // permuted start of the outputs, or -1: index list
   int64_t out_idx;     // offset into the index store when out_start < 0
   int64_t mode;
+  int64_t flag_off = -1;   // elimination panels: first word of the nonzero-row bits
+  int lower = 0;           // explicit lower-triangular inverses: zero tiles skipped
 };
 
 struct PhaseImage {
   std::vector<int64_t> rows, tiles, chunks, contrib;
+  // dataflow schedule inputs: per item its input and output cluster, per
+  // chunk its output cluster (cluster-contiguous numbering; ncl = the final
+  // block's index list)
+  std::vector<int32_t> item_src, item_dst, chunk_dst;
   int64_t pos = 0;
   bool overflow = false;
 };
@@ -59,6 +65,15 @@ struct Collected {
   int64_t img_len = 0;
   std::vector<int64_t> phases; // 10 per phase (see spand_collect_apply_get)
   int64_t scratch_len = 0;
+  // elimination panels scanned for nonzero rows before the image compiles:
+  // {pool offset, ld, rows, cols, first bit word}
+  std::vector<int64_t> flag_panels;
+  int64_t flag_words = 0;
+  // dataflow schedule (spand_collect_dataflow)
+  std::vector<int64_t> cstart;             // ncl + 1
+  std::vector<int32_t> fin;                // clusters of the final block
+  std::vector<int64_t> df_units, df_deps, df_phase;
+  int64_t df_nctr = 0, df_scratch = 0;
 };
 
 }  // namespace
@@ -71,6 +86,8 @@ void* spand_collect_create(void* plan, const int64_t* events, int scheme) {
   const int ncl = pv.ncl;
   std::vector<int64_t> off(ncl, 0), cstart(ncl + 1, 0);
   for (int c = 0; c < ncl; ++c) cstart[c + 1] = cstart[c] + pv.m0[c];
+  C->cstart = cstart;
+  C->fin.assign(pv.fin.begin(), pv.fin.end());
   auto live = [&](int c) { return pv.m0[c] - off[c]; };
   auto pst = [&](int c) { return cstart[c] + off[c]; };
   // apply phase numbering (forward per level: [G-T][G-A]([D]([Q-T][E-A])*waves))
@@ -152,12 +169,18 @@ void* spand_collect_create(void* plan, const int64_t* events, int scheme) {
         C->views.insert(C->views.end(), {a, pv.m0[w], lw, ns});
         add(C->fph[gfA], a, pv.m0[w], lw, ns, 0, 0, 0, pst(s), pst(w), 1);
         add(C->bph[gbA], a, pv.m0[w], lw, ns, 0, 1, 0, pst(w), pst(s), 1);
+        // the panel's rows of w not coupled to s are zero (the reference
+        // stores them densely): their nonzero-row bits select row runs
+        C->fph[gfA].back().flag_off = C->bph[gbA].back().flag_off = C->flag_words;
+        C->flag_panels.insert(C->flag_panels.end(), {a, pv.m0[w], lw, ns, C->flag_words});
+        C->flag_words += (lw + 31) / 32;
       }
       const int64_t se = (int64_t)C->segs.size() / 8;
       C->ops.insert(C->ops.end(), {0, s, li, 0, off[s], ns, 0, lower, m0s, linv, -1, 0, sb, se, 0, 0});
       C->views.insert(C->views.end(), {lower, m0s, ns, ns});
       add(C->fph[gfT], linv | (int64_t(1) << 62), m0s, ns, ns, 0, 0, 0, pst(s), pst(s), 0);
       add(C->bph[gbT], linv | (int64_t(1) << 62), m0s, ns, ns, 0, 1, 0, pst(s), pst(s), 0);
+      C->fph[gfT].back().lower = C->bph[gbT].back().lower = 1;
       for (int64_t i = 0; i < ns; ++i) C->perm.push_back(pv.dofs[pv.dptr[s] + off[s] + i]);
     }
     C->lsum.insert(C->lsum.end(), {L.level, nint, ndofs, L.skipped});
@@ -176,6 +199,7 @@ void* spand_collect_create(void* plan, const int64_t* events, int scheme) {
       C->views.insert(C->views.end(), {lo | (int64_t(1) << 62), m0p, mp, mp});
       add(C->fph[fb + 2], li2 | (int64_t(1) << 62), m0p, mp, mp, 0, 0, 0, pst(p), pst(p), 0);
       add(C->bph[bb + 2 * nw], li2 | (int64_t(1) << 62), m0p, mp, mp, 0, 1, 0, pst(p), pst(p), 0);
+      C->fph[fb + 2].back().lower = C->bph[bb + 2 * nw].back().lower = 1;
     }
     // RRQR critical path: waves run one after the other, panels of a wave
     // concurrently
@@ -282,6 +306,7 @@ void* spand_collect_create(void* plan, const int64_t* events, int scheme) {
     tf.out_start = -1;
     tf.out_idx = 0;
     tf.mode = 0;
+    tf.lower = 1;
     C->fph[nph - 1].push_back(tf);
     tf.trans = 1;
     C->bph[0].push_back(tf);
@@ -345,8 +370,14 @@ int spand_collect_get(void* h, int64_t* ops, int64_t* segs, int64_t* perm, int64
 // selects the factor buffer), inputs xbuf + 8 * permuted index.
 
 static void compile_phase(PhaseImage& P, const std::vector<Task>& ph, int64_t pool_base,
-                          int64_t fac_base, int64_t xbuf, int64_t idx_addr) {
+                          int64_t fac_base, int64_t xbuf, int64_t idx_addr, const uint32_t* bits,
+                          const std::vector<int64_t>& cstart) {
+  const int ncl = (int)cstart.size() - 1;
+  auto cluster_of = [&](int64_t x) {
+    return (int32_t)(std::upper_bound(cstart.begin(), cstart.end(), x) - cstart.begin() - 1);
+  };
   constexpr int64_t RUN = 64;
+  constexpr int64_t GAP = 8;   // zero-row gaps shorter than this stay inside a row run
   // warp work items of ~32 KB of payload (apply.cu gemv_items_kernel):
   //   trans 0: kc <= 64 columns x oc <= 128 rows (64 rows for wide tasks)
   //   trans 1: oc <= 4 columns x kc <= 1024 rows
@@ -354,26 +385,71 @@ static void compile_phase(PhaseImage& P, const std::vector<Task>& ph, int64_t po
   std::vector<int64_t>& tiles = P.tiles;
   std::vector<int64_t>& chunks = P.chunks;
   std::vector<int64_t>& contrib = P.contrib;
-  struct Run { int64_t dst, len, mode; bool idx; std::vector<int64_t> parts; };
-  std::vector<Run> runs;
-  std::unordered_map<int64_t, int> run_of;   // destination start -> run
-  int64_t pos = 0;
+  // A piece is the scratch block one k-tile of one (sub)task produces for a
+  // destination range [start, start + len): absolute x positions (key 0) or
+  // positions in the final block's index list (key 1).  Pieces of one phase
+  // may overlap (many operators update one interface); the destination is
+  // cut into segments covered by a fixed set of pieces, summed in task order.
+  struct Piece { int64_t key, start, len, part, mode, order; };
+  std::vector<Piece> pieces;
+  int64_t pos = 0, order = 0;
+  // first row >= i (< n) whose bit equals `want` (word-level scans)
+  auto next_bit = [&](int64_t off, int64_t i, int64_t n, bool want) -> int64_t {
+    while (i < n) {
+      uint32_t w = bits[off + (i >> 5)];
+      if (!want) w = ~w;
+      w &= ~0u << (i & 31);
+      if (w) {
+        const int64_t r = (i & ~int64_t(31)) + __builtin_ctz(w);
+        return r < n ? r : n;
+      }
+      i = (i & ~int64_t(31)) + 32;
+    }
+    return n;
+  };
+  // sub-tasks: elimination panels split into runs of nonzero rows
+  struct Sub { const Task* t; int64_t ra, rb; };
+  std::vector<Sub> subs;
+  int64_t payload = 0;
+  for (const Task& t : ph) {
+    if ((t.trans ? t.cols : t.rows) == 0) continue;
+    if (t.flag_off >= 0 && bits) {
+      const int64_t nr = t.rows;
+      int64_t i = next_bit(t.flag_off, 0, nr, true);
+      while (i < nr) {
+        // extend over runs of nonzero rows and zero gaps of <= GAP rows
+        int64_t last = next_bit(t.flag_off, i, nr, false) - 1;
+        for (;;) {
+          const int64_t nx = next_bit(t.flag_off, last + 1, nr, true);
+          if (nx >= nr || nx - last > GAP) break;
+          last = next_bit(t.flag_off, nx, nr, false) - 1;
+        }
+        subs.push_back({&t, i, last + 1});
+        payload += (last + 1 - i) * t.cols * 8;
+        i = next_bit(t.flag_off, last + 1, nr, true);
+      }
+    } else {
+      subs.push_back({&t, 0, t.rows});
+      payload += t.rows * t.cols * 8 / (t.lower ? 2 : 1);
+    }
+  }
   // item size: ~32 KB, smaller when the phase is small, so that every phase
   // offers about one item per resident warp (148 SMs x 32 warps)
-  int64_t payload = 0;
-  for (const Task& t : ph) payload += t.rows * t.cols * 8;
   const int64_t isz = std::max<int64_t>(4096, std::min<int64_t>(32768, payload / (148 * 32)));
-  for (const Task& t : ph) {
-    const int64_t nout = t.trans ? t.cols : t.rows;
-    const int64_t nk = t.trans ? t.rows : t.cols;
-    if (nout == 0) continue;
+  for (const Sub& sb : subs) {
+    const Task& t = *sb.t;
+    const int64_t srows = sb.rb - sb.ra;
+    const int64_t nout = t.trans ? t.cols : srows;
+    const int64_t nk = t.trans ? srows : t.cols;
+    if (nout == 0 || nk == 0) continue;
     if (nout >= (int64_t(1) << 20) || nk >= (int64_t(1) << 17)) P.overflow = true;
     const bool in_fac = (t.M >> 62) & 1;
-    const int64_t moff = t.M & ((int64_t(1) << 62) - 1);
+    const int64_t moff = (t.M & ((int64_t(1) << 62) - 1)) + sb.ra;
     const int64_t maddr = (in_fac ? fac_base : pool_base) + 8 * moff;
-    const int64_t inp = t.in_kind == 1 ? xbuf + 8 * t.in_ptr : idx_addr;
+    const int64_t in_ptr = t.in_ptr + (t.trans ? sb.ra : 0);
+    const int64_t inp = t.in_kind == 1 ? xbuf + 8 * in_ptr : idx_addr;
     const int64_t tid = (int64_t)rows.size() / 8;
-    rows.insert(rows.end(), {maddr, t.ld, t.rows, t.cols, t.trans, t.rot, t.in_kind, inp});
+    rows.insert(rows.end(), {maddr, t.ld, srows, t.cols, t.trans, t.rot, t.in_kind, inp});
     int64_t TO, TK;
     if (t.trans) {
       TO = 4;
@@ -382,39 +458,90 @@ static void compile_phase(PhaseImage& P, const std::vector<Task>& ph, int64_t po
       TO = nk <= 32 ? 128 : 64;
       TK = std::max<int64_t>(8, std::min<int64_t>(64, isz / (8 * TO)));
     }
+    const int64_t out0 = t.out_start >= 0 ? t.out_start + (t.trans ? 0 : sb.ra) : 0;
+    const int64_t key = t.out_start >= 0 ? 0 : 1;
+    const int32_t src = t.in_kind == 1 ? cluster_of(in_ptr) : ncl;
+    const int32_t dst = key ? ncl : cluster_of(out0);
     const int64_t nkt = std::max<int64_t>(1, (nk + TK - 1) / TK);
-    for (int64_t kb = 0; kb < nkt; ++kb)
-      for (int64_t ob = 0; ob < nout; ob += TO) {
-        const int64_t oc = std::min(TO, nout - ob);
-        const int64_t kc = std::max<int64_t>(0, std::min(TK, nk - kb * TK));
+    for (int64_t kb = 0; kb < nkt; ++kb) {
+      const int64_t k0 = kb * TK;
+      const int64_t kc = std::max<int64_t>(0, std::min(TK, nk - k0));
+      // the outputs this k-tile touches: all, or the lower-triangular part
+      int64_t lo = 0, hi = nout;
+      if (t.lower) {
+        if (!t.trans) lo = std::min(nout, k0);          // rows >= the tile's first column
+        else hi = std::min(nout, k0 + kc);              // columns <= the tile's last row
+      }
+      if (lo >= hi) continue;
+      const int64_t part = pos;
+      for (int64_t ob = lo; ob < hi; ob += TO) {
+        const int64_t oc = std::min(TO, hi - ob);
         // packed item (apply.cu): task | ob | oc, out_off | kb | kc
         tiles.insert(tiles.end(), {(tid << 32) | (ob << 12) | oc,
-                                   ((pos + kb * nout + ob) << 28) | ((kb * TK) << 11) | kc});
+                                   ((part + ob - lo) << 28) | (k0 << 11) | kc});
+        P.item_src.push_back(src);
+        P.item_dst.push_back(dst);
       }
-    const int64_t key = t.out_start >= 0 ? t.out_start : -1;
-    auto it = run_of.find(key);
-    int r;
-    if (it == run_of.end()) {
-      r = (int)runs.size();
-      run_of.emplace(key, r);
-      runs.push_back({t.out_start >= 0 ? t.out_start : 0, nout, t.mode, t.out_start < 0, {}});
-    } else {
-      r = it->second;
+      pieces.push_back({key, out0 + lo, hi - lo, part, t.mode, order++});
+      pos += hi - lo;
     }
-    for (int64_t kb = 0; kb < nkt; ++kb) runs[r].parts.push_back(pos + kb * nout);
-    pos += nout * nkt;
   }
   if (rows.empty()) return;
   // packed-item field limits (apply.cu): ob < 2^20, inner offset < 2^17,
   // scratch offset < 2^35
   if (pos >= (int64_t(1) << 35)) P.overflow = true;
-  for (const Run& R : runs) {
-    const int64_t cb = (int64_t)contrib.size();
-    contrib.insert(contrib.end(), R.parts.begin(), R.parts.end());
-    const int64_t ce = (int64_t)contrib.size();
-    for (int64_t e = 0; e < R.len; e += RUN)
-      chunks.insert(chunks.end(), {R.dst, std::min(RUN, R.len - e), R.mode, cb, ce, e,
-                                   R.idx ? idx_addr : 0, 0});
+  // segments: the destination (per key) is cut where pieces begin or end;
+  // every segment has a fixed set of covering pieces, summed in task order
+  // (contribution = part - start: output e of the segment reads
+  // scratch[contrib + e]); chunks of <= RUN outputs of one segment
+  std::sort(pieces.begin(), pieces.end(), [](const Piece& x, const Piece& y) {
+    return x.key != y.key ? x.key < y.key : (x.start != y.start ? x.start < y.start : x.order < y.order);
+  });
+  size_t i0 = 0;
+  std::vector<int64_t> cuts;
+  std::vector<size_t> active;
+  while (i0 < pieces.size()) {
+    size_t i1 = i0;
+    while (i1 < pieces.size() && pieces[i1].key == pieces[i0].key) ++i1;
+    const int64_t key = pieces[i0].key;
+    cuts.clear();
+    for (size_t q = i0; q < i1; ++q) {
+      cuts.push_back(pieces[q].start);
+      cuts.push_back(pieces[q].start + pieces[q].len);
+    }
+    std::sort(cuts.begin(), cuts.end());
+    cuts.erase(std::unique(cuts.begin(), cuts.end()), cuts.end());
+    active.clear();
+    size_t nxt = i0;
+    int64_t cb = -1, ce = -1;   // the current covering list (reused while unchanged)
+    for (size_t c = 0; c + 1 < cuts.size(); ++c) {
+      const int64_t a = cuts[c], b = cuts[c + 1];
+      size_t w = 0;
+      bool changed = false;
+      for (size_t q : active) {
+        if (pieces[q].start + pieces[q].len > a) active[w++] = q;
+        else changed = true;
+      }
+      active.resize(w);
+      while (nxt < i1 && pieces[nxt].start == a) {
+        active.push_back(nxt++);
+        changed = true;
+      }
+      if (active.empty()) continue;
+      if (changed || cb < 0) {
+        std::sort(active.begin(), active.end(),
+                  [&](size_t x, size_t y) { return pieces[x].order < pieces[y].order; });
+        cb = (int64_t)contrib.size();
+        for (size_t q : active) contrib.push_back(pieces[q].part - pieces[q].start);
+        ce = (int64_t)contrib.size();
+      }
+      const int64_t md = pieces[active[0]].mode;
+      for (int64_t e = a; e < b; e += RUN) {
+        chunks.insert(chunks.end(), {0, std::min(RUN, b - e), md, cb, ce, e, key ? idx_addr : 0, 0});
+        P.chunk_dst.push_back(key ? ncl : cluster_of(e));
+      }
+    }
+    i0 = i1;
   }
   P.pos = pos;
 }
@@ -433,11 +560,107 @@ static void append_phase(Collected* C, const PhaseImage& P) {
   C->scratch_len = std::max(C->scratch_len, P.pos);
 }
 
+// Dataflow schedule of the whole apply (forward then backward phases): one
+// unit per work item and per accumulation chunk, in phase order (items
+// before chunks).  Counters (uint64, zeroed per launch; 0 = the dispatch
+// counter): per phase and output cluster, the items done; per phase and
+// input cluster, the items done (readers); per phase and output cluster,
+// the chunks done.  An item waits for the chunks of the last phase that
+// wrote its input cluster; a chunk waits for the items of its own phase
+// that produce its cluster, for the last writer of its cluster and for
+// every reader of the cluster since then (write-after-read).  Every
+// dependency points to an earlier unit, so persistent warps taking units in
+// order never deadlock.  Unit rows (8 int64): {phase, kind (0 item,
+// 1 chunk), index in the phase, first dep, ndeps, counter to bump, second
+// counter (-1: none), 0}; deps: {counter, target}; phase rows (8 int64):
+// {tasks, items, chunks, contributions (image offsets), scratch base, 0...}.
+static void build_dataflow(Collected* C) {
+  const int ncl = (int)C->cstart.size() - 1;
+  const int32_t FIN = ncl;
+  std::vector<int64_t>& U = C->df_units;
+  std::vector<int64_t>& D = C->df_deps;
+  std::vector<int64_t>& PH = C->df_phase;
+  U.clear();
+  D.clear();
+  PH.clear();
+  int64_t nctr = 1;
+  std::vector<int64_t> lw_ctr(ncl, -1), lw_tgt(ncl, 0);
+  std::vector<std::vector<std::pair<int64_t, int64_t>>> readers(ncl);
+  std::vector<std::pair<int64_t, int64_t>> dep;
+  auto each = [&](int32_t c, auto&& f) {
+    if (c == FIN) {
+      for (int32_t q : C->fin) f(q);
+    } else {
+      f(c);
+    }
+  };
+  auto flush_deps = [&]() -> std::pair<int64_t, int64_t> {
+    std::sort(dep.begin(), dep.end());
+    dep.erase(std::unique(dep.begin(), dep.end()), dep.end());
+    const int64_t at = (int64_t)D.size() / 2;
+    for (auto& d : dep) D.insert(D.end(), {d.first, d.second});
+    return {at, (int64_t)dep.size()};
+  };
+  int64_t sb = 0;
+  int64_t g = 0;
+  for (size_t k = 0; k < C->imgs.size(); ++k) {
+    if (C->img_at[k] < 0) continue;
+    const PhaseImage& P = C->imgs[k];
+    const int64_t* row = C->phases.data() + 10 * g;
+    PH.insert(PH.end(), {row[0], row[2], row[4], row[6], sb, 0, 0, 0});
+    const int64_t nitem = row[3], nchunk = row[5];
+    std::unordered_map<int32_t, std::pair<int64_t, int64_t>> ictr, sctr, cctr;
+    for (int64_t i = 0; i < nitem; ++i) {
+      auto& a = ictr[P.item_dst[i]];
+      if (a.second++ == 0) a.first = nctr++;
+      auto& b = sctr[P.item_src[i]];
+      if (b.second++ == 0) b.first = nctr++;
+    }
+    for (int64_t i = 0; i < nchunk; ++i) {
+      auto& a = cctr[P.chunk_dst[i]];
+      if (a.second++ == 0) a.first = nctr++;
+    }
+    for (int64_t i = 0; i < nitem; ++i) {
+      dep.clear();
+      each(P.item_src[i], [&](int32_t c) {
+        if (lw_ctr[c] >= 0) dep.push_back({lw_ctr[c], lw_tgt[c]});
+      });
+      const auto at = flush_deps();
+      U.insert(U.end(), {g, 0, i, at.first, at.second, ictr[P.item_dst[i]].first,
+                         sctr[P.item_src[i]].first, 0});
+    }
+    for (auto& kv : sctr)
+      each(kv.first, [&](int32_t c) { readers[c].push_back(kv.second); });
+    for (int64_t i = 0; i < nchunk; ++i) {
+      const int32_t d = P.chunk_dst[i];
+      dep.clear();
+      auto ic = ictr.find(d);
+      if (ic != ictr.end()) dep.push_back(ic->second);
+      each(d, [&](int32_t c) {
+        if (lw_ctr[c] >= 0) dep.push_back({lw_ctr[c], lw_tgt[c]});
+        for (auto& r : readers[c]) dep.push_back(r);
+      });
+      const auto at = flush_deps();
+      U.insert(U.end(), {g, 1, i, at.first, at.second, cctr[d].first, -1, 0});
+    }
+    for (auto& kv : cctr)
+      each(kv.first, [&](int32_t c) {
+        lw_ctr[c] = kv.second.first;
+        lw_tgt[c] = kv.second.second;
+        readers[c].clear();
+      });
+    sb += row[9];
+    ++g;
+  }
+  C->df_nctr = nctr;
+  C->df_scratch = std::max<int64_t>(sb, 1);
+}
+
 // Build the apply image.  idx_addr: device address of the final block's
 // permuted index list (int32, spand_collect_get's fidx).  out[4]: image
 // length, number of forward phases, number of backward phases, scratch.
 int spand_collect_apply(void* h, int64_t pool_base, int64_t fac_base, int64_t xbuf,
-                        int64_t idx_addr, int64_t* out) {
+                        int64_t idx_addr, const uint32_t* bits, int64_t* out) {
   Collected* C = static_cast<Collected*>(h);
   C->phases.clear();
   C->img_len = 0;
@@ -455,7 +678,8 @@ int spand_collect_apply(void* h, int64_t pool_base, int64_t fac_base, int64_t xb
   std::atomic<size_t> next{0};
   auto work = [&]() {
     for (size_t q = next++; q < nt; q = next++)
-      compile_phase(imgs[order[q]], phase(order[q]), pool_base, fac_base, xbuf, idx_addr);
+      compile_phase(imgs[order[q]], phase(order[q]), pool_base, fac_base, xbuf, idx_addr, bits,
+                    C->cstart);
   };
   const unsigned nth = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
   std::vector<std::thread> pool;
@@ -477,6 +701,50 @@ int spand_collect_apply(void* h, int64_t pool_base, int64_t fac_base, int64_t xb
   out[1] = nfw;
   out[2] = nbw;
   out[3] = C->scratch_len;
+  if (getenv("SPAND_APPLY_DATAFLOW") && getenv("SPAND_APPLY_DATAFLOW")[0] == '1') build_dataflow(C);
+  return 0;
+}
+
+// the dataflow schedule (after spand_collect_apply): out[4] = units, deps,
+// counters, scratch doubles per right-hand side
+int spand_collect_dataflow_sizes(void* h, int64_t* out) {
+  Collected* C = static_cast<Collected*>(h);
+  out[0] = (int64_t)C->df_units.size() / 8;
+  out[1] = (int64_t)C->df_deps.size() / 2;
+  out[2] = C->df_nctr;
+  out[3] = C->df_scratch;
+  return 0;
+}
+
+int spand_collect_dataflow(void* h, int64_t* units, int64_t* deps, int64_t* phases) {
+  Collected* C = static_cast<Collected*>(h);
+  auto cp = [](int64_t* dst, const std::vector<int64_t>& v) {
+    if (dst && !v.empty()) std::memcpy(dst, v.data(), v.size() * sizeof(int64_t));
+  };
+  cp(units, C->df_units);
+  cp(deps, C->df_deps);
+  cp(phases, C->df_phase);
+  return 0;
+}
+
+// elimination panels to scan for nonzero rows: out[0] = panel count,
+// out[1] = bit words (spand_collect_flag_panels fills 5 int64 per panel:
+// {address, ld, rows, cols, first word})
+int spand_collect_flag_sizes(void* h, int64_t* out) {
+  Collected* C = static_cast<Collected*>(h);
+  out[0] = (int64_t)C->flag_panels.size() / 5;
+  out[1] = C->flag_words;
+  return 0;
+}
+
+int spand_collect_flag_panels(void* h, int64_t pool_base, int64_t* out) {
+  Collected* C = static_cast<Collected*>(h);
+  const size_t np = C->flag_panels.size() / 5;
+  for (size_t k = 0; k < np; ++k) {
+    const int64_t* r = C->flag_panels.data() + 5 * k;
+    out[5 * k] = pool_base + 8 * r[0];
+    for (int q = 1; q < 5; ++q) out[5 * k + q] = r[q];
+  }
   return 0;
 }
 

@@ -45,6 +45,11 @@ from .schemes import (Elimination, ErrorCorrection, MatView, Orthogonal,
 import os as _os
 from collections.abc import Sequence
 
+# launch record type -> entry point (csrc/launcher.cu spand_run_launches)
+LAUNCH_NAMES = {1: "spand_potrf_batched", 2: "spand_trtri_tiles", 3: "spand_gemm_grouped",
+                4: "spand_copy_batched", 5: "spand_rrqr_wave", 6: "spand_assemble_final",
+                7: "spand_nk_rescale", 8: "spand_nk_basis", 9: "spand_nk_deflate",
+                10: "spand_nk_qform", 11: "spand_digest_pieces"}
 WAVE_LOG = None      # set to [] to record per-wave CUDA events (profiling)
 PROG_ARENA = None    # pinned staging of the program chunks (emission thread)
 NK_RTOL = 1e-8       # rank threshold of the near-kernel basis (oracle NK_RTOL)
@@ -330,6 +335,9 @@ class Engine:
         self.timings["device_s"] = time.perf_counter() - tstart
 
     def _launch(self, launches, base, gm0, goff, ib, evb, fb, st, prog=None):
+        if WAVE_LOG is None and _os.environ.get("SPAND_NATIVE_LAUNCH", "1") != "0":
+            self._launch_native(launches, base, gm0, goff, ib, evb, fb, st)
+            return
         import ctypes
         t = self.t
         P = lambda off: ctypes.c_void_p(base + 8 * int(off))  # noqa: E731
@@ -382,6 +390,26 @@ class Engine:
                           x1, ctypes.c_void_p(fb + 8 * x2), st)
             else:
                 raise RuntimeError(f"unknown launch type {typ}")
+
+    def _launch_native(self, launches, base, gm0, goff, ib, evb, fb, st):
+        """All records of a program chunk issued by one native call
+        (csrc/launcher.cu): no per-launch ctypes overhead on the host."""
+        import ctypes
+        recs = np.ascontiguousarray(launches, dtype=np.int64)
+        if recs.size == 0:
+            return
+        counts = np.zeros(16, dtype=np.int64)
+        U, ldu, nkv = None, 0, 0
+        if self.nk is not None and hasattr(self, "nkbuf"):
+            U, ldu, nkv = ptr(self.nkbuf), int(self.nkbuf.shape[1]), int(self.nkbuf.shape[0])
+        mask = _lib.profile_mask(LAUNCH_NAMES)
+        _lib.call("spand_run_launches", int(recs.shape[0]), recs.ctypes.data, int(base), gm0, goff,
+                  ctypes.c_void_p(ib), ctypes.c_void_p(evb), int(fb), self._btab_p,
+                  float(self.eps), SCHEME_CODE[self.scheme] | (4 if self.local_errors else 0),
+                  U, ldu, nkv, float(NK_RTOL), mask, counts.ctypes.data, st)
+        for typ, nm in LAUNCH_NAMES.items():
+            if counts[typ]:
+                _lib.COUNTS[nm] = _lib.COUNTS.get(nm, 0) + int(counts[typ])
 
     def _scatter_a(self):
         """Initial blocks from the entries of A (factorize.py:61-96).

@@ -10,6 +10,7 @@ contiguous slices of a plan-owned permuted vector, permuted in/out once per
 call.
 """
 
+import os as _os
 import time
 from concurrent.futures import ThreadPoolExecutor
 
@@ -29,11 +30,27 @@ class FastPlan:
 
     @property
     def launches(self):
+        if getattr(self, "flow", None) is not None:
+            return 3   # gather, one dataflow kernel (after a counter memset), scatter
         return 2 * (len(self.fwd) + len(self.bwd)) + 2
+
+    def _run_flow(self, nvec, scratch=None, ldscr=None):
+        fl = self.flow
+        _lib.call("spand_apply_dataflow", fl["nunit"], ptr(fl["units"]), ptr(fl["deps"]),
+                  fl["nctr"], ptr(fl["ctrs"]), ptr(fl["phases"]), ptr(self.image),
+                  ptr(self.xbuf), self.n, ptr(scratch if scratch is not None else fl["scratch"]),
+                  ldscr or fl["scratch_len"], nvec, stream())
+        _lib.COUNTS["spand_apply_dataflow"] = (_lib.COUNTS.get("spand_apply_dataflow", 0)
+                                               + (nvec + 3) // 4 + (1 if nvec % 4 == 3 else 0))
 
     def _run1(self, xd, forward, backward):
         st = stream()
         _lib.call("spand_gather", self.n, ptr(self.perm), ptr(xd), ptr(self.xbuf), st)
+        if forward and backward and getattr(self, "flow", None) is not None:
+            self._run_flow(1)
+            _lib.call("spand_scatter_perm", self.n, ptr(self.perm), ptr(self.xbuf),
+                      ptr(xd), st)
+            return
         if forward:
             self._run_pass(self.fwd)
         if backward:
@@ -109,19 +126,52 @@ class NativeApplyPlan(FastPlan):
                                        dtype=np.int32), np.int32)
         self._graph = None
         self._collected = collected
+        # nonzero-row bits of the elimination panels (device scan, one pass
+        # over those payloads), downloaded for the image compiler
+        bits, ready = self._row_bits(collected, pool)
         self._future = _COMPILER.submit(self._compile_image, collected, pool.data_ptr(),
                                         fac.data_ptr(), self.xbuf.data_ptr(),
-                                        self._fidx.data_ptr())
+                                        self._fidx.data_ptr(), bits, ready)
 
     @staticmethod
-    def _compile_image(collected, pool_base, fac_base, xbuf, fidx):
+    def _row_bits(collected, pool):
+        import ctypes
+        t = require_cuda()
+        lib, vp = collected.lib, collected.vp
+        sz = np.zeros(2, dtype=np.int64)
+        lib.spand_collect_flag_sizes.argtypes = [ctypes.c_void_p] * 2
+        lib.spand_collect_flag_sizes(collected.h, vp(sz))
+        npan, nwords = int(sz[0]), int(sz[1])
+        if npan == 0:
+            return None, None
+        rows = np.zeros(5 * npan, dtype=np.int64)
+        lib.spand_collect_flag_panels.argtypes = [ctypes.c_void_p, ctypes.c_int64,
+                                                  ctypes.c_void_p]
+        lib.spand_collect_flag_panels(collected.h, pool.data_ptr(), vp(rows))
+        rd = to_dev(rows, np.int64)
+        bd = t.empty(max(nwords, 1), dtype=t.int32, device=dev())
+        _lib.call("spand_row_bits", npan, ptr(rd), ptr(bd), stream())
+        host = t.empty(bd.shape, dtype=t.int32, pin_memory=True)
+        host.copy_(bd, non_blocking=True)
+        ev = t.cuda.Event()
+        ev.record()
+        return (host, rd, bd), ev
+
+    @staticmethod
+    def _compile_image(collected, pool_base, fac_base, xbuf, fidx, bits=None, ready=None):
         import ctypes
         lib, vp = collected.lib, collected.vp
         t0 = time.perf_counter()
+        bptr = None
+        if bits is not None:
+            ready.synchronize()
+            bptr = ctypes.c_void_p(bits[0].data_ptr())
+        t_bits = time.perf_counter() - t0
         out = np.zeros(4, dtype=np.int64)
         lib.spand_collect_apply.argtypes = [ctypes.c_void_p] + [ctypes.c_int64] * 4 + \
-            [ctypes.c_void_p]
-        rc = lib.spand_collect_apply(collected.h, pool_base, fac_base, xbuf, fidx, vp(out))
+            [ctypes.c_void_p, ctypes.c_void_p]
+        rc = lib.spand_collect_apply(collected.h, pool_base, fac_base, xbuf, fidx, bptr,
+                                     vp(out))
         if rc != 0:
             raise RuntimeError(f"apply image build failed ({rc}): an operator exceeds "
                                "the packed work-item limits")
@@ -133,7 +183,18 @@ class NativeApplyPlan(FastPlan):
         ph = np.zeros((nfw + nbw, 10), dtype=np.int64)
         lib.spand_collect_apply_get.argtypes = [ctypes.c_void_p] * 3
         lib.spand_collect_apply_get(collected.h, vp(image), vp(ph))
-        return pinned, ph, nfw, scratch_len, (t1 - t0, time.perf_counter() - t1)
+        # the dataflow schedule of apply_m (one launch for both passes)
+        dsz = np.zeros(4, dtype=np.int64)
+        lib.spand_collect_dataflow_sizes.argtypes = [ctypes.c_void_p] * 2
+        lib.spand_collect_dataflow_sizes(collected.h, vp(dsz))
+        nunit, ndep, nctr, dscr = (int(v) for v in dsz)
+        units = np.zeros(8 * max(nunit, 1), dtype=np.int64)
+        deps = np.zeros(2 * max(ndep, 1), dtype=np.int64)
+        dph = np.zeros(8 * max(nfw + nbw, 1), dtype=np.int64)
+        lib.spand_collect_dataflow.argtypes = [ctypes.c_void_p] * 4
+        lib.spand_collect_dataflow(collected.h, vp(units), vp(deps), vp(dph))
+        flow = (nunit, units, deps, nctr, dscr, dph)
+        return pinned, ph, nfw, scratch_len, (t1 - t0, time.perf_counter() - t1, t_bits), flow
 
     def __getattr__(self, name):
         if name in NativeApplyPlan._LAZY:
@@ -146,7 +207,7 @@ class NativeApplyPlan(FastPlan):
         if "fwd" in self.__dict__:
             return
         t = require_cuda()
-        pinned, ph, nfw, scratch_len, (t_setup, t_image) = self._future.result()
+        pinned, ph, nfw, scratch_len, (t_setup, t_image, t_bits), flow = self._future.result()
         t0 = time.perf_counter()
         self.scratch_len = scratch_len
         self.image = t.empty(pinned.shape, dtype=t.int64, device=dev())
@@ -164,11 +225,22 @@ class NativeApplyPlan(FastPlan):
         self.phase_table = ph
         # host phase tables of the two passes (spand_apply_pass)
         self._ph = (np.ascontiguousarray(ph[:nfw]), np.ascontiguousarray(ph[nfw:]))
-        self.build_times = {"setup_s": t_setup, "image_s": t_image,
+        self.build_times = {"setup_s": t_setup, "image_s": t_image, "bits_wait_s": t_bits,
                             "upload_s": time.perf_counter() - t0, "image_mb": image.nbytes / 1e6,
                             "since_factor_s": time.perf_counter() - self._t0}
         self.bwd = rows[nfw:]
         self.fwd = rows[:nfw]
+        nunit, units, deps, nctr, dscr, dph = flow
+        self.flow = None
+        if nunit > 0 and _os.environ.get("SPAND_APPLY_DATAFLOW", "0") == "1":
+            self.flow = {"nunit": nunit, "units": to_dev(units, np.int64),
+                         "deps": to_dev(deps, np.int64), "nctr": nctr,
+                         "ctrs": t.zeros(nctr, dtype=t.int64, device=dev()),
+                         "phases": to_dev(dph, np.int64), "scratch_len": dscr,
+                         "scratch": t.empty(dscr, dtype=t.float64, device=dev())}
+            self.build_times["dataflow_units"] = nunit
+            self.build_times["dataflow_deps"] = int(deps.size // 2)
+            self.build_times["dataflow_scratch_mb"] = 8 * dscr / 1e6
 
     NVEC_MAX = 8   # right-hand sides per multi-vector pass
 
@@ -220,10 +292,17 @@ class NativeApplyPlan(FastPlan):
             for v in range(nv):
                 _lib.call("spand_gather", n, ptr(self.perm), ptr(cols[j0 + v]),
                           ctypes_ptr(self.xbuf.data_ptr() + 8 * n * v), st)
-            if forward:
-                self._run_pass(self.fwd, nv)
-            if backward:
-                self._run_pass(self.bwd, nv)
+            if forward and backward and getattr(self, "flow", None) is not None:
+                fl = self.flow
+                if fl.get("scratch_multi") is None:
+                    fl["scratch_multi"] = t.empty(fl["scratch_len"] * 4, dtype=t.float64,
+                                                  device=dev())
+                self._run_flow(nv, fl["scratch_multi"], fl["scratch_len"])
+            else:
+                if forward:
+                    self._run_pass(self.fwd, nv)
+                if backward:
+                    self._run_pass(self.bwd, nv)
             for v in range(nv):
                 _lib.call("spand_scatter_perm", n, ptr(self.perm),
                           ctypes_ptr(self.xbuf.data_ptr() + 8 * n * v), ptr(cols[j0 + v]), st)

@@ -59,7 +59,9 @@ def test_header_symbols_are_typed_or_handle_based():
                     "spand_mm_free",
                     "spand_collect_create", "spand_collect_destroy", "spand_collect_sizes",
                     "spand_collect_get", "spand_collect_apply", "spand_collect_apply_get",
-                    "spand_collect_fine", "spand_collect_stats"}
+                    "spand_collect_fine", "spand_collect_stats", "spand_collect_flag_sizes",
+                    "spand_collect_flag_panels", "spand_collect_dataflow_sizes",
+                    "spand_collect_dataflow", "spand_launch_timer_reset"}
     for nm in _declared():
         assert nm in _lib.SIGNATURES or nm in handle_based, nm
 

@@ -51,7 +51,7 @@ for rep in range(4):
     ch = lib.spand_collect_create(sym.h, vp(ev), E.SCHEME_CODE[sp.SchemeKind.from_string("second-full")])
     t1 = time.perf_counter()
     out = np.zeros(4, dtype=np.int64)
-    rc = lib.spand_collect_apply(ch, 1 << 40, 2 << 40, 3 << 40, 4 << 40, vp(out))
+    rc = lib.spand_collect_apply(ch, 1 << 40, 2 << 40, 3 << 40, 4 << 40, None, vp(out))
     t2 = time.perf_counter()
     img = np.empty(int(out[0]), dtype=np.int64)
     ph = np.zeros((int(out[1] + out[2]), 10), dtype=np.int64)
