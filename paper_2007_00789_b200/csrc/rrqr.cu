@@ -71,6 +71,9 @@ constexpr int kRowUnroll = SPAND_ROW_UNROLL;   // row loops of the DMMA block up
 #define SPAND_BLK 32
 #endif
 constexpr int kBlk = SPAND_BLK;  // reflectors per cold-column block update (<= 32)
+#ifndef SPAND_BLK0
+#define SPAND_BLK0 8
+#endif
 // hot iff running norm^2 >= rho * pivot norm^2; rho grows with the panel
 // height (cheaper blocked cold updates vs. per-step column work; measured on
 // C4-L15 with rho in {0.1 .. 0.9}: best 0.35 below 700 rows, 0.5 below 1200,
@@ -2622,7 +2625,9 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
     cpar ^= 1;
     last_wv = wv;
     ++k;
-    if (k - k0 >= kBlk) maint = 1;
+    // the first block is SPAND_BLK0 steps (every active column is hot until
+    // the first classification; C4-L15 swept over 1 / 4 / 8 / 32: 8 best, -2 %)
+    if (k - k0 >= (k0 == 0 ? SPAND_BLK0 : kBlk)) maint = 1;
     PH(5);
     group_barrier(ctr, G, gen, tgt, k, events + 12 * slot + 9);
   }

@@ -180,3 +180,25 @@ class DeviceCSR:
                           ptr(ys[j]), None, stream())
             out.copy_(ys.t())
         return out
+
+
+class nvtx:
+    """NVTX range around a host phase (ncu --nvtx / Nsight filters): the
+    factorization's symbolic analysis, device program and collection, the
+    PCG solve and the apply image build."""
+
+    def __init__(self, name):
+        self.name = name
+
+    def __enter__(self):
+        try:
+            torch().cuda.nvtx.range_push(self.name)
+            self.ok = True
+        except Exception:
+            self.ok = False
+        return self
+
+    def __exit__(self, *exc):
+        if self.ok:
+            torch().cuda.nvtx.range_pop()
+        return False

@@ -725,11 +725,15 @@ def check_panel_rows(h, skip_levels):
 def run_factorization(a, h, eps, scheme, skip_levels, collect_local_errors=False,
                       near_kernel=None, digest=False):
     from .factorize import Factorization
+    from .device import nvtx
     t0 = time.perf_counter()
-    eng = Engine(a, h, eps, scheme, skip_levels, near_kernel, collect_local_errors,
-                 digest=digest)
-    eng.run()
-    ops, perm, diag, nnz = eng.collect()
+    with nvtx("spand.symbolic"):
+        eng = Engine(a, h, eps, scheme, skip_levels, near_kernel, collect_local_errors,
+                     digest=digest)
+    with nvtx("spand.factor_program"):
+        eng.run()
+    with nvtx("spand.collect"):
+        ops, perm, diag, nnz = eng.collect()
     eng.timings["total_s"] = time.perf_counter() - t0
     f = Factorization(ops=ops, perm=perm, n=a.n, eps=float(eps), scheme=scheme,
                       skip_levels=int(skip_levels), nnz_factor=int(nnz),

@@ -130,6 +130,16 @@ def pcg(a, b, m=None, tol=1e-10, maxit=None):
 
     ``b`` of shape (n, k) (EXTENSION): k right-hand sides
     solved together (``pcg_multi``); returns (X, [SolveReport] * k)."""
+    from .device import nvtx
+    with nvtx("spand.pcg"):
+        return _pcg_impl(a, b, m, tol, maxit)
+
+
+def _pcg_impl(a, b, m=None, tol=1e-10, maxit=None):
+    """Solve A x = b by PCG on the device; returns (x, SolveReport).
+
+    ``b`` of shape (n, k) (EXTENSION): k right-hand sides
+    solved together (``pcg_multi``); returns (X, [SolveReport] * k)."""
     if tol <= 0.0:
         raise ValueError(f"tol must be positive, got {tol}")
     t = require_cuda()
