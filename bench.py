@@ -460,12 +460,27 @@ def main():
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
+    # eager (the launches a short solve issues: ~690 per apply_m) ...
     e0.record(st)
     for _ in range(10):
         f.apply_m_device(xa)
     e1.record(st)
     torch.cuda.synchronize()
-    apply_ms = e0.elapsed_time(e1) / 10
+    apply_eager_ms = e0.elapsed_time(e1) / 10
+    # ... and one CUDA graph per apply_m (a factor reused for many solves:
+    # captured after fastplan.GRAPH_AFTER applies), L2 flushed before each
+    for _ in range(40):
+        f.apply_m_device(xa)
+    g_ms = []
+    for _ in range(10):
+        flush.zero_()
+        torch.cuda.synchronize()
+        e0.record(st)
+        f.apply_m_device(xa)
+        e1.record(st)
+        torch.cuda.synchronize()
+        g_ms.append(e0.elapsed_time(e1))
+    apply_ms = float(np.median(g_ms))
     apply_gbs = counts["B_apply"] / (apply_ms / 1000.0) / 1e9
     # multi-RHS apply (8 right-hand sides per pass, payload read once per 4)
     xm = torch.randn(a.n, 8, dtype=torch.float64, device=bd.device)
@@ -511,7 +526,11 @@ def main():
         "true_residual": rep.true_residual, "hierarchy_s": t_hier,
         "nnz_factor": f.nnz_factor, "mu": f.nnz_factor / a.nnz,
         "apply": {"ms": apply_ms, "gbs": apply_gbs, "frac_hbm": apply_gbs / pk["hbm_gbs"],
-                  "bytes": counts["B_apply"], "basis": "B_apply = 16 nnz_factor + 32 n per apply_m (one CUDA graph)"},
+                  "bytes": counts["B_apply"], "eager_ms": apply_eager_ms,
+                  "eager_gbs": counts["B_apply"] / (apply_eager_ms / 1000.0) / 1e9,
+                  "basis": "B_apply = 16 nnz_factor + 32 n per apply_m; ms: one CUDA graph "
+                           "replay (L2 flushed before, median of 10); eager_ms: the ~690 "
+                           "launches of a short solve, back to back"},
         "apply_multi_rhs": {"rhs": 8, "ms": multi_ms, "ms_per_rhs": multi_ms / 8,
                             "gbs_per_rhs_equiv": 8 * counts["B_apply"] / (multi_ms / 1000.0) / 1e9,
                             "basis": "apply_m of an n x 8 stack (eager launches, two passes of "

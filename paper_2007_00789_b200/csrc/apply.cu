@@ -316,64 +316,75 @@ scatter_kernel(int nout, const int64_t* __restrict__ dst, const int64_t* __restr
 }
 
 // Run-structured ordered accumulation: chunk row (8 int64)
-// {dst, len, mode, cb, ce, eoff, idx, 0}; element i < len of the chunk is
+// {dst, len, mode, cb, ce, eoff, idx, splits}; element i < len of the chunk is
 // x[d] with d = dst + eoff + i (idx == 0) or ((int32*)idx)[eoff + i]; the value is
-// sum_{c in [cb, ce)} scratch[contrib[c] + eoff + i], summed in order.
+// the sum of scratch[contrib[c] + eoff + i] over c in [cb, ce).  The
+// contributions come in four summation groups (splits: 16-bit offsets of
+// groups 1-3 from cb), each summed strictly in order by its own thread group,
+// the group sums combined in a fixed order: an image that drops exact-zero
+// parts gives the same bits (collect.cpp compile_phase).
+__device__ __forceinline__ void group_range(int64_t cb, int64_t ce, int64_t splits, int g,
+                                            int64_t& gb, int64_t& ge) {
+  const int64_t s1 = cb + (splits & 0xffff), s2 = cb + ((splits >> 16) & 0xffff),
+                s3 = cb + ((splits >> 32) & 0xffff);
+  gb = g == 0 ? cb : (g == 1 ? s1 : (g == 2 ? s2 : s3));
+  ge = g == 0 ? s1 : (g == 1 ? s2 : (g == 2 ? s3 : ce));
+}
+
 __global__ void __launch_bounds__(kThreads)
 runs_kernel(const int64_t* __restrict__ chunks, const int64_t* __restrict__ contrib,
             double* __restrict__ x, int64_t ldx, const double* __restrict__ scratch,
             int64_t ldscr, int nvec) {
-  // chunk of <= 64 outputs; 4 thread groups split the contributions, the
-  // group partials are added in group order (deterministic)
   __shared__ double part[kThreads];
   const int64_t* ch = chunks + 8 * (int64_t)blockIdx.x;
   const int len = (int)ch[1];
   const int i = threadIdx.x & 63, g = threadIdx.x >> 6;
   const int64_t dst = ch[0], cb = ch[3], ce = ch[4], eoff = ch[5], idx = ch[6];
   const int md = (int)ch[2];
+  int64_t gb, ge;
+  group_range(cb, ce, ch[7], g, gb, ge);
   for (int v = 0; v < nvec; ++v) {
-    // four independent partial sums per thread (fixed combination order)
-    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    double s = 0.0;
     if (i < len) {
-      const double* sv = scratch + eoff + i + v * ldscr;
-      int64_t c = cb + g;
-      for (; c + 12 < ce; c += 16) {
-        const int64_t a0 = __ldg(contrib + c), a1 = __ldg(contrib + c + 4),
-                      a2 = __ldg(contrib + c + 8), a3 = __ldg(contrib + c + 12);
-        s0 += sv[a0];
-        s1 += sv[a1];
-        s2 += sv[a2];
-        s3 += sv[a3];
+      const double* sv = scratch + eoff + i + (int64_t)v * ldscr;
+      int64_t c = gb;
+      for (; c + 3 < ge; c += 4) {
+        const double v0 = sv[__ldg(contrib + c)], v1 = sv[__ldg(contrib + c + 1)],
+                     v2 = sv[__ldg(contrib + c + 2)], v3 = sv[__ldg(contrib + c + 3)];
+        s += v0;
+        s += v1;
+        s += v2;
+        s += v3;
       }
-      for (; c < ce; c += 4) s0 += sv[__ldg(contrib + c)];
+      for (; c < ge; ++c) s += sv[__ldg(contrib + c)];
     }
-    const double s = (s0 + s1) + (s2 + s3);
     __syncthreads();
     part[threadIdx.x] = s;
     __syncthreads();
     if (threadIdx.x < len) {
-      const double t = part[i] + part[i + 64] + part[i + 128] + part[i + 192];
+      const double t = (part[i] + part[i + 64]) + (part[i + 128] + part[i + 192]);
       const int64_t d = idx ? (int64_t)reinterpret_cast<const int32_t*>(idx)[eoff + i] : dst + eoff + i;
-      double* xd = x + d + v * ldx;
+      double* xd = x + d + (int64_t)v * ldx;
       if (md == 0) *xd = t;
       else *xd -= t;
     }
   }
 }
+
 // sum of one output of a chunk (runs_kernel layout) by one thread (the
 // dataflow kernel's warp path)
 __device__ __forceinline__ double chunk_sum(const double* sv, const int64_t* __restrict__ contrib,
-                                            int64_t cb, int64_t ce) {
-  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-  int64_t c = cb;
-  for (; c + 3 < ce; c += 4) {
-    s0 += __ldcg(sv + __ldg(contrib + c));
-    s1 += __ldcg(sv + __ldg(contrib + c + 1));
-    s2 += __ldcg(sv + __ldg(contrib + c + 2));
-    s3 += __ldcg(sv + __ldg(contrib + c + 3));
+                                            int64_t cb, int64_t ce, int64_t splits) {
+  double p[4];   // the four summation groups, as runs_kernel
+#pragma unroll
+  for (int g = 0; g < 4; ++g) {
+    int64_t gb, ge;
+    group_range(cb, ce, splits, g, gb, ge);
+    double s = 0.0;
+    for (int64_t c = gb; c < ge; ++c) s += __ldcg(sv + __ldg(contrib + c));
+    p[g] = s;
   }
-  for (; c < ce; ++c) s0 += __ldcg(sv + __ldg(contrib + c));
-  return (s0 + s1) + (s2 + s3);
+  return (p[0] + p[1]) + (p[2] + p[3]);
 }
 
 // ---- dataflow apply: the whole apply_m (forward + backward) in one launch.
@@ -399,6 +410,7 @@ __device__ __forceinline__ void chunk_warp(const int64_t* __restrict__ ch,
                                            int v0) {
   const int lane = threadIdx.x & 31;
   const int64_t dst = __ldg(ch), eoff = __ldg(ch + 5), cb = __ldg(ch + 3), ce = __ldg(ch + 4);
+  const int64_t sp = __ldg(ch + 7);
   const int len = (int)__ldg(ch + 1), md = (int)__ldg(ch + 2);
   const int32_t* idx = reinterpret_cast<const int32_t*>(__ldg(ch + 6));
 #pragma unroll
@@ -409,7 +421,7 @@ __device__ __forceinline__ void chunk_warp(const int64_t* __restrict__ ch,
     const int64_t d = idx ? (int64_t)idx[e] : dst + e;
 #pragma unroll
     for (int v = 0; v < NV; ++v) {
-      const double t = chunk_sum(scratch + e + (int64_t)(v0 + v) * ldscr, contrib, cb, ce);
+      const double t = chunk_sum(scratch + e + (int64_t)(v0 + v) * ldscr, contrib, cb, ce, sp);
       double* xd = x + d + (int64_t)(v0 + v) * ldx;
       *xd = md == 0 ? t : __ldcg(xd) - t;
     }

@@ -390,7 +390,7 @@ static void compile_phase(PhaseImage& P, const std::vector<Task>& ph, int64_t po
   // positions in the final block's index list (key 1).  Pieces of one phase
   // may overlap (many operators update one interface); the destination is
   // cut into segments covered by a fixed set of pieces, summed in task order.
-  struct Piece { int64_t key, start, len, part, mode, order; };
+  struct Piece { int64_t key, start, len, part, mode, order, grp; };
   std::vector<Piece> pieces;
   int64_t pos = 0, order = 0;
   // first row >= i (< n) whose bit equals `want` (word-level scans)
@@ -408,12 +408,18 @@ static void compile_phase(PhaseImage& P, const std::vector<Task>& ph, int64_t po
     return n;
   };
   // sub-tasks: elimination panels split into runs of nonzero rows
+  // Results must not depend on the bits (the first image of a factor has
+  // none, the compressed one replaces it later): items and k-tiles keep the
+  // uncompressed shapes, transposed tasks only drop all-zero k-tiles, and the
+  // accumulation sums each output's parts in order (apply.cu runs_kernel),
+  // so a dropped part -- an exact zero -- changes nothing.
   struct Sub { const Task* t; int64_t ra, rb; };
   std::vector<Sub> subs;
   int64_t payload = 0;
   for (const Task& t : ph) {
     if ((t.trans ? t.cols : t.rows) == 0) continue;
-    if (t.flag_off >= 0 && bits) {
+    payload += t.rows * t.cols * 8 / (t.lower ? 2 : 1);
+    if (t.flag_off >= 0 && bits && !t.trans) {
       const int64_t nr = t.rows;
       int64_t i = next_bit(t.flag_off, 0, nr, true);
       while (i < nr) {
@@ -425,12 +431,10 @@ static void compile_phase(PhaseImage& P, const std::vector<Task>& ph, int64_t po
           last = next_bit(t.flag_off, nx, nr, false) - 1;
         }
         subs.push_back({&t, i, last + 1});
-        payload += (last + 1 - i) * t.cols * 8;
         i = next_bit(t.flag_off, last + 1, nr, true);
       }
     } else {
       subs.push_back({&t, 0, t.rows});
-      payload += t.rows * t.cols * 8 / (t.lower ? 2 : 1);
     }
   }
   // item size: ~32 KB, smaller when the phase is small, so that every phase
@@ -466,6 +470,10 @@ static void compile_phase(PhaseImage& P, const std::vector<Task>& ph, int64_t po
     for (int64_t kb = 0; kb < nkt; ++kb) {
       const int64_t k0 = kb * TK;
       const int64_t kc = std::max<int64_t>(0, std::min(TK, nk - k0));
+      // transposed elimination panel: a k-tile of all-zero rows adds nothing
+      if (t.trans && t.flag_off >= 0 && bits && kc > 0 &&
+          next_bit(t.flag_off, sb.ra + k0, sb.ra + k0 + kc, true) >= sb.ra + k0 + kc)
+        continue;
       // the outputs this k-tile touches: all, or the lower-triangular part
       int64_t lo = 0, hi = nout;
       if (t.lower) {
@@ -482,7 +490,10 @@ static void compile_phase(PhaseImage& P, const std::vector<Task>& ph, int64_t po
         P.item_src.push_back(src);
         P.item_dst.push_back(dst);
       }
-      pieces.push_back({key, out0 + lo, hi - lo, part, t.mode, order++});
+      // summation group of the part: fixed by (task, k-tile), the same in
+      // the compressed and uncompressed images
+      pieces.push_back({key, out0 + lo, hi - lo, part, t.mode, order++,
+                        ((int64_t)(&t - ph.data()) + kb) & 3});
       pos += hi - lo;
     }
   }
@@ -513,7 +524,7 @@ static void compile_phase(PhaseImage& P, const std::vector<Task>& ph, int64_t po
     cuts.erase(std::unique(cuts.begin(), cuts.end()), cuts.end());
     active.clear();
     size_t nxt = i0;
-    int64_t cb = -1, ce = -1;   // the current covering list (reused while unchanged)
+    int64_t cb = -1, ce = -1, splits = 0;   // the current covering list (reused while unchanged)
     for (size_t c = 0; c + 1 < cuts.size(); ++c) {
       const int64_t a = cuts[c], b = cuts[c + 1];
       size_t w = 0;
@@ -529,15 +540,26 @@ static void compile_phase(PhaseImage& P, const std::vector<Task>& ph, int64_t po
       }
       if (active.empty()) continue;
       if (changed || cb < 0) {
-        std::sort(active.begin(), active.end(),
-                  [&](size_t x, size_t y) { return pieces[x].order < pieces[y].order; });
+        // by summation group, task order within a group; split points of
+        // groups 1-3 packed (16 bits each, relative to cb) in the chunk row
+        std::sort(active.begin(), active.end(), [&](size_t x, size_t y) {
+          return pieces[x].grp != pieces[y].grp ? pieces[x].grp < pieces[y].grp
+                                                : pieces[x].order < pieces[y].order;
+        });
         cb = (int64_t)contrib.size();
-        for (size_t q : active) contrib.push_back(pieces[q].part - pieces[q].start);
+        int64_t cnt[4] = {0, 0, 0, 0};
+        for (size_t q : active) {
+          contrib.push_back(pieces[q].part - pieces[q].start);
+          ++cnt[pieces[q].grp];
+        }
         ce = (int64_t)contrib.size();
+        if (ce - cb >= 65536) P.overflow = true;
+        splits = cnt[0] | ((cnt[0] + cnt[1]) << 16) | ((cnt[0] + cnt[1] + cnt[2]) << 32);
       }
       const int64_t md = pieces[active[0]].mode;
       for (int64_t e = a; e < b; e += RUN) {
-        chunks.insert(chunks.end(), {0, std::min(RUN, b - e), md, cb, ce, e, key ? idx_addr : 0, 0});
+        chunks.insert(chunks.end(), {0, std::min(RUN, b - e), md, cb, ce, e, key ? idx_addr : 0,
+                                     splits});
         P.chunk_dst.push_back(key ? ncl : cluster_of(e));
       }
     }

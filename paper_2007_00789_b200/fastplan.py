@@ -65,6 +65,7 @@ class FastPlan:
         first GRAPH_AFTER applies launch eagerly (capturing and instantiating
         a graph of ~350 kernels costs more than a short PCG solve); a factor
         reused for many solves switches to one CUDA graph replay."""
+        self._maybe_swap()
         t = require_cuda()
         self._napply = getattr(self, "_napply", 0) + 1
         if self._graph is None and self._napply <= self.GRAPH_AFTER:
@@ -126,12 +127,15 @@ class NativeApplyPlan(FastPlan):
                                        dtype=np.int32), np.int32)
         self._graph = None
         self._collected = collected
-        # nonzero-row bits of the elimination panels (device scan, one pass
-        # over those payloads), downloaded for the image compiler
-        bits, ready = self._row_bits(collected, pool)
+        # the first image keeps every panel row (fast to compile: the first
+        # applies wait for it); the row-compressed image (nonzero-row bits of
+        # the elimination panels, a device scan) compiles in the background
+        # after the first apply and replaces it once ready
+        self._pool, self._fac = pool, fac
         self._future = _COMPILER.submit(self._compile_image, collected, pool.data_ptr(),
                                         fac.data_ptr(), self.xbuf.data_ptr(),
-                                        self._fidx.data_ptr(), bits, ready)
+                                        self._fidx.data_ptr())
+        self._future2 = None
 
     @staticmethod
     def _row_bits(collected, pool):
@@ -202,12 +206,35 @@ class NativeApplyPlan(FastPlan):
             return object.__getattribute__(self, name)
         raise AttributeError(name)
 
+    ROW_COMPRESS = _os.environ.get("SPAND_APPLY_ROWBITS", "1") != "0"
+
     def _ensure(self):
-        import ctypes
         if "fwd" in self.__dict__:
             return
+        self._install(self._future.result(), compressed=False)
+        if self.ROW_COMPRESS:
+            bits, ready = self._row_bits(self._collected, self._pool)
+            if bits is not None:
+                self._future2 = _COMPILER.submit(
+                    self._compile_image, self._collected, self._pool.data_ptr(),
+                    self._fac.data_ptr(), self.xbuf.data_ptr(), self._fidx.data_ptr(), bits,
+                    ready)
+
+    def _maybe_swap(self):
+        """Install the row-compressed image once its background compile is
+        done (between applies; both images give the same bits, collect.cpp
+        compile_phase); a captured graph is dropped."""
+        f2 = getattr(self, "_future2", None)
+        if f2 is not None and f2.done():
+            self._future2 = None
+            self._install(f2.result(), compressed=True)
+            self._graph = None
+            self._scratch_multi = None
+
+    def _install(self, result, compressed):
+        import ctypes
         t = require_cuda()
-        pinned, ph, nfw, scratch_len, (t_setup, t_image, t_bits), flow = self._future.result()
+        pinned, ph, nfw, scratch_len, (t_setup, t_image, t_bits), flow = result
         t0 = time.perf_counter()
         self.scratch_len = scratch_len
         self.image = t.empty(pinned.shape, dtype=t.int64, device=dev())
@@ -225,9 +252,13 @@ class NativeApplyPlan(FastPlan):
         self.phase_table = ph
         # host phase tables of the two passes (spand_apply_pass)
         self._ph = (np.ascontiguousarray(ph[:nfw]), np.ascontiguousarray(ph[nfw:]))
-        self.build_times = {"setup_s": t_setup, "image_s": t_image, "bits_wait_s": t_bits,
-                            "upload_s": time.perf_counter() - t0, "image_mb": image.nbytes / 1e6,
-                            "since_factor_s": time.perf_counter() - self._t0}
+        bt = {"setup_s": t_setup, "image_s": t_image, "bits_wait_s": t_bits,
+              "upload_s": time.perf_counter() - t0, "image_mb": image.nbytes / 1e6,
+              "since_factor_s": time.perf_counter() - self._t0, "row_compressed": compressed}
+        if compressed:
+            self.build_times["compressed"] = bt
+        else:
+            self.build_times = bt
         self.bwd = rows[nfw:]
         self.fwd = rows[:nfw]
         nunit, units, deps, nctr, dscr, dph = flow
@@ -269,6 +300,7 @@ class NativeApplyPlan(FastPlan):
         """In place on a device tensor of shape (n,) or (n, k); column stacks
         go through the factor NVEC_MAX vectors at a time (each payload
         element is read once per group of up to 4: GEMM-like reuse)."""
+        self._maybe_swap()
         if xd.dim() == 1:
             self._run1(xd, forward, backward)
             return xd
@@ -281,6 +313,7 @@ class NativeApplyPlan(FastPlan):
         """In place on a contiguous (k, n) device tensor whose ROWS are the
         vectors (the multi-RHS PCG keeps its vectors this way); every row is
         transformed bit for bit as by the single-vector apply."""
+        self._maybe_swap()
         t = require_cuda()
         if getattr(self, "_scratch_multi", None) is None:
             self._scratch_multi = t.empty(max(self.scratch_len, 1) * self.NVEC_MAX,

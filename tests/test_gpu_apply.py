@@ -43,3 +43,35 @@ def test_loaded_reference_factor_applies(tag):
     zz = f.apply_m(stack)
     assert np.allclose(zz[:, 0], z, rtol=0, atol=1e-13 * np.abs(z).max())
     assert np.allclose(zz[:, 1], 2 * z, rtol=0, atol=1e-13 * np.abs(z).max())
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", [("lap3d", 16, 6), ("hc3d", 16, 7)])
+def test_row_compressed_image_is_bitwise_identical(case, monkeypatch):
+    """The first apply image keeps every elimination-panel row; the
+    row-compressed image (device nonzero-row bits, compiled in the
+    background) replaces it later.  Both must give the same bits for
+    apply_m, apply_inv, apply_inv_t and column stacks (fastplan.py,
+    collect.cpp compile_phase: fixed summation groups)."""
+    import paper_2007_00789_b200 as sp
+    from paper_2007_00789_b200.fastplan import NativeApplyPlan
+    kind, d, lv = case
+    a = sp.laplacian_3d(d) if kind == "lap3d" else sp.baseline_problem("C4", grid=d)[0]
+    h = sp.build_hierarchy(a, lv)
+    b = np.random.default_rng(1).standard_normal((a.n, 3))
+
+    def results(f):
+        return [f.apply_m(b[:, 0]), f.apply_inv(b[:, 1]), f.apply_inv_t(b[:, 2]), f.apply_m(b)]
+    monkeypatch.setattr(NativeApplyPlan, "ROW_COMPRESS", False)
+    f1 = sp.factorize(a, h, 0.01, "second-full", skip_levels=2)
+    plain = results(f1)
+    assert "compressed" not in f1.plan.build_times
+    monkeypatch.setattr(NativeApplyPlan, "ROW_COMPRESS", True)
+    f2 = sp.factorize(a, h, 0.01, "second-full", skip_levels=2)
+    f2.apply_m(b[:, 0])
+    if f2.plan._future2 is not None:
+        f2.plan._future2.result()
+    comp = results(f2)
+    assert f2.plan.build_times.get("compressed") is not None
+    for x, y in zip(plain, comp):
+        assert np.array_equal(x, y)
