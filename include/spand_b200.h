@@ -118,6 +118,14 @@ int spand_apply_runs(int nchunk, const int64_t* chunks, const int64_t* contrib, 
  * nitem, chunks, nchunk, contrib, grid, 0, 0}, offsets in int64 units into
  * the device image), spand_gemv_items then spand_apply_runs on `stream`.
  * Same result as issuing the 2 nphase calls one by one. */
+/* One forward or backward pass of the apply as one cooperative launch per
+ * group of <= 4 right-hand sides: every phase's work items, a grid barrier,
+ * its accumulation chunks, a grid barrier (spand_apply_pass does the same
+ * with two launches per phase).  ph: the phase table (10 int64 per phase)
+ * in DEVICE memory; bar: 2 uint32 of device scratch (zeroed here). */
+int spand_apply_pass_persistent(int nphase, const int64_t* ph, const int64_t* image, double* x,
+                                int64_t ldx, double* scratch, int64_t ldscr, int nvec,
+                                unsigned* bar, void* stream);
 /* The whole apply_m (forward + backward pass) as one persistent launch per
  * group of <= 4 right-hand sides: units (8 int64: {phase, kind, index,
  * first dep, ndeps, counter, counter2, 0}) run in order once their

@@ -35,6 +35,7 @@ SIGNATURES = {
     "spand_apply_runs": [_c_int, _P, _P, _P, _c_i64, _P, _c_i64, _c_int, _P],
     "spand_apply_pass": [_c_int, _P, _P, _P, _c_i64, _P, _c_i64, _c_int, _P],
     "spand_row_bits": [_c_int, _P, _P, _P],
+    "spand_apply_pass_persistent": [_c_int, _P, _P, _P, _c_i64, _P, _c_i64, _c_int, _P, _P],
     "spand_run_launches": [_c_int, _P, _c_i64, _P, _P, _P, _P, _c_i64, _P, _c_dbl, _c_int, _P,
                            _c_i64, _c_int, _c_dbl, _c_int, _P, _P],
     "spand_launch_timer_reset": [],
@@ -109,7 +110,7 @@ _HOST_ONLY = {"spand_plan_sizes", "spand_plan_emit", "spand_plan_program",
               "spand_rrqr_cta_count", "spand_rrqr_capacity", "spand_spmv_blocks", "spand_dot_blocks"}
 
 # entry points issuing several kernels whose callers count them per kernel
-_COUNTED_BY_CALLER = {"spand_apply_pass", "spand_run_launches"}
+_COUNTED_BY_CALLER = {"spand_apply_pass", "spand_run_launches", "spand_apply_pass_persistent"}
 _HOST_ONLY |= {"spand_launch_timer_reset", "spand_launch_timer_read"}
 
 

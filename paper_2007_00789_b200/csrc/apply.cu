@@ -331,19 +331,31 @@ __device__ __forceinline__ void group_range(int64_t cb, int64_t ce, int64_t spli
   ge = g == 0 ? s1 : (g == 1 ? s2 : (g == 2 ? s3 : ce));
 }
 
+__device__ __forceinline__ void runs_chunk(const int64_t* __restrict__ ch,
+                                           const int64_t* __restrict__ contrib, double* x,
+                                           int64_t ldx, const double* scratch, int64_t ldscr,
+                                           int nvec, int v0, double* part);
+
 __global__ void __launch_bounds__(kThreads)
 runs_kernel(const int64_t* __restrict__ chunks, const int64_t* __restrict__ contrib,
             double* __restrict__ x, int64_t ldx, const double* __restrict__ scratch,
             int64_t ldscr, int nvec) {
   __shared__ double part[kThreads];
-  const int64_t* ch = chunks + 8 * (int64_t)blockIdx.x;
+  runs_chunk(chunks + 8 * (int64_t)blockIdx.x, contrib, x, ldx, scratch, ldscr, nvec, 0, part);
+}
+
+// one chunk by one CTA (vectors v0 .. v0 + nvec - 1)
+__device__ __forceinline__ void runs_chunk(const int64_t* __restrict__ ch,
+                                           const int64_t* __restrict__ contrib, double* x,
+                                           int64_t ldx, const double* scratch, int64_t ldscr,
+                                           int nvec, int v0, double* part) {
   const int len = (int)ch[1];
   const int i = threadIdx.x & 63, g = threadIdx.x >> 6;
   const int64_t dst = ch[0], cb = ch[3], ce = ch[4], eoff = ch[5], idx = ch[6];
   const int md = (int)ch[2];
   int64_t gb, ge;
   group_range(cb, ce, ch[7], g, gb, ge);
-  for (int v = 0; v < nvec; ++v) {
+  for (int v = v0; v < v0 + nvec; ++v) {
     double s = 0.0;
     if (i < len) {
       const double* sv = scratch + eoff + i + (int64_t)v * ldscr;
@@ -385,6 +397,53 @@ __device__ __forceinline__ double chunk_sum(const double* sv, const int64_t* __r
     p[g] = s;
   }
   return (p[0] + p[1]) + (p[2] + p[3]);
+}
+
+// ---- persistent pass: one cooperative launch runs every phase of a pass
+// (items, grid barrier, accumulation chunks, grid barrier) instead of two
+// launches per phase (~690 per apply_m).  Grid barrier: arrival counter +
+// release word, as the RRQR group barrier.
+__device__ __forceinline__ void pass_barrier(unsigned* bar, unsigned& gen) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    ++gen;
+    if (atomicAdd(bar, 1u) + 1u == gen * gridDim.x) {
+      asm volatile("st.release.gpu.global.u32 [%0], %1;\n" ::"l"(bar + 1), "r"(gen) : "memory");
+    } else {
+      unsigned v;
+      do {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(bar + 1) : "memory");
+      } while (v < gen);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+template <int NV>
+__global__ void __launch_bounds__(kThreads, NV == 1 ? 4 : 2)
+pass_kernel(int nphase, const int64_t* __restrict__ ph, const int64_t* __restrict__ image,
+            double* x, int64_t ldx, double* scratch, int64_t ldscr, unsigned* bar, int v0) {
+  __shared__ double part[kThreads];
+  unsigned gen = 0;
+  const int warp = threadIdx.x >> 5;
+  const int W = gridDim.x * kWarps;
+  for (int q = 0; q < nphase; ++q) {
+    const int64_t* r = ph + 10 * (int64_t)q;
+    const int64_t* tasks = image + r[0];
+    const int64_t* items = image + r[2];
+    const int nitem = (int)r[3];
+    for (int it = blockIdx.x * kWarps + warp; it < nitem; it += W)
+      gemv_item<NV, true>(it, items, tasks, x, ldx, scratch, ldscr, v0);
+    pass_barrier(bar, gen);
+    const int64_t* chunks = image + r[4];
+    const int64_t* contrib = image + r[6];
+    const int nch = (int)r[5];
+    for (int c = blockIdx.x; c < nch; c += gridDim.x)
+      runs_chunk(chunks + 8 * (int64_t)c, contrib, x, ldx, scratch, ldscr, NV, v0, part);
+    pass_barrier(bar, gen);
+  }
 }
 
 // ---- dataflow apply: the whole apply_m (forward + backward) in one launch.
@@ -543,6 +602,40 @@ row_bits_kernel(const int64_t* __restrict__ panels, uint32_t* __restrict__ bits)
 }  // namespace
 
 extern "C" {
+
+// a whole forward or backward pass as one cooperative launch per group of
+// <= 4 vectors; ph: the phase table on the DEVICE (10 int64 per phase, image
+// offsets); bar: 2 uint32 of zeroed scratch (reset here)
+int spand_apply_pass_persistent(int nphase, const int64_t* ph, const int64_t* image, double* x,
+                                int64_t ldx, double* scratch, int64_t ldscr, int nvec,
+                                unsigned* bar, void* stream) {
+  if (nphase < 0 || nvec < 1) return -1;
+  if (nphase == 0) return 0;
+  static int sms = 0, occ1 = 0, occ2 = 0, occ4 = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ1, pass_kernel<1>, kThreads, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, pass_kernel<2>, kThreads, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ4, pass_kernel<4>, kThreads, 0);
+  }
+  cudaStream_t st = as_stream(stream);
+  for (int v0 = 0; v0 < nvec;) {
+    const int left = nvec - v0;
+    cudaError_t e = cudaMemsetAsync(bar, 0, 2 * sizeof(unsigned), st);
+    if (e != cudaSuccess) return (int)e;
+    int nv = left >= 4 ? 4 : (left >= 2 ? 2 : 1);
+    int grid = sms * (nv == 4 ? occ4 : (nv == 2 ? occ2 : occ1));
+    void* args[] = {&nphase, (void*)&ph, (void*)&image, &x, &ldx, &scratch, &ldscr, &bar, &v0};
+    if (nv == 4) e = cudaLaunchCooperativeKernel((void*)pass_kernel<4>, grid, kThreads, args, 0, st);
+    else if (nv == 2) e = cudaLaunchCooperativeKernel((void*)pass_kernel<2>, grid, kThreads, args, 0, st);
+    else e = cudaLaunchCooperativeKernel((void*)pass_kernel<1>, grid, kThreads, args, 0, st);
+    if (e != cudaSuccess) return (int)e;
+    v0 += nv;
+  }
+  return 0;
+}
 
 int spand_apply_dataflow(int64_t nunit, const int64_t* units, const int64_t* deps, int64_t nctr,
                          unsigned long long* ctrs, const int64_t* phases, const int64_t* image,

@@ -32,6 +32,8 @@ class FastPlan:
     def launches(self):
         if getattr(self, "flow", None) is not None:
             return 3   # gather, one dataflow kernel (after a counter memset), scatter
+        if getattr(self, "PERSISTENT", False) and getattr(self, "_ph", None) is not None:
+            return 4   # gather, one cooperative kernel per pass, scatter
         return 2 * (len(self.fwd) + len(self.bwd)) + 2
 
     def _run_flow(self, nvec, scratch=None, ldscr=None):
@@ -207,6 +209,7 @@ class NativeApplyPlan(FastPlan):
         raise AttributeError(name)
 
     ROW_COMPRESS = _os.environ.get("SPAND_APPLY_ROWBITS", "1") != "0"
+    PERSISTENT = _os.environ.get("SPAND_APPLY_PERSISTENT", "0") == "1"
 
     def _ensure(self):
         if "fwd" in self.__dict__:
@@ -250,8 +253,14 @@ class NativeApplyPlan(FastPlan):
                          nitem, ctypes.c_void_p(base + 8 * co), nch,
                          ctypes.c_void_p(base + 8 * cbo), grid))
         self.phase_table = ph
-        # host phase tables of the two passes (spand_apply_pass)
+        # host phase tables of the two passes (spand_apply_pass) and their
+        # device copies (spand_apply_pass_persistent)
         self._ph = (np.ascontiguousarray(ph[:nfw]), np.ascontiguousarray(ph[nfw:]))
+        self._phd = (to_dev(self._ph[0].ravel() if nfw else np.zeros(1, np.int64), np.int64),
+                     to_dev(self._ph[1].ravel() if len(ph) > nfw else np.zeros(1, np.int64),
+                            np.int64))
+        if getattr(self, "_bar", None) is None:
+            self._bar = t.zeros(2, dtype=t.int32, device=dev())
         bt = {"setup_s": t_setup, "image_s": t_image, "bits_wait_s": t_bits,
               "upload_s": time.perf_counter() - t0, "image_mb": image.nbytes / 1e6,
               "since_factor_s": time.perf_counter() - self._t0, "row_compressed": compressed}
@@ -280,6 +289,18 @@ class NativeApplyPlan(FastPlan):
         x = self.xbuf
         scr = self.scratch if nvec == 1 else self._scratch_multi
         tab = getattr(self, "_ph", None)
+        if tab is not None and self.PERSISTENT:
+            # the whole pass in ONE cooperative launch (grid barriers between
+            # the phases' item and accumulation stages)
+            fw = phases is self.fwd
+            ph = tab[0] if fw else tab[1]
+            _lib.call("spand_apply_pass_persistent", len(ph), ptr(self._phd[0 if fw else 1]),
+                      ptr(self.image), ptr(x), self.n, ptr(scr), self.scratch_len, nvec,
+                      ptr(self._bar), st)
+            _lib.COUNTS["spand_apply_pass_persistent"] = (
+                _lib.COUNTS.get("spand_apply_pass_persistent", 0) + (nvec + 3) // 4
+                + (1 if nvec % 4 == 3 else 0))
+            return
         if tab is not None:
             # the whole pass in one native call (launch cost ~2 us per kernel
             # instead of ~5 us through ctypes per call)
