@@ -590,7 +590,7 @@ __device__ void qform_batched(double* Q, const double* V, const double* taus, in
 #define SPAND_CL_MINB1 2
 #endif
 #define SPAND_CL_MINB (kCl ? SPAND_CL_MINB1 : 2)
-template <bool kCl>
+template <bool kCl, int kSch>
 __global__ void __launch_bounds__(kT, SPAND_CL_MINB)
 rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* __restrict__ nbrs,
                  int32_t* __restrict__ m0, int32_t* __restrict__ off, double eps, int scheme_flags,
@@ -598,7 +598,9 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
   // scheme_flags: scheme (0 first, 1 second-full, 2 superfine) | 4: keep every
   // fine row of Q^T W in the dead slots (local-error diagnostics,
   // schemes.py:297-306), not only the correction rows
-  const int scheme = scheme_flags & 3;
+  // the scheme is a template parameter (superfine-only code is compiled out
+  // of the other schemes' kernels: fewer registers); scheme_flags & 3 == kSch
+  constexpr int scheme = kSch;
   const bool keep_fine = (scheme_flags & 4) != 0;
   extern __shared__ double vsh[];
   __shared__ Sh sh;
@@ -2958,9 +2960,9 @@ int spand_rrqr_cta_count(void) {
   // capacity for panels up to 4224 rows (the tile staging size); taller
   // panels need more shared memory and are launched with smaller groups
   const size_t smem = kColdSmem;
-  cudaFuncSetAttribute(rrqr_wave_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  cudaFuncSetAttribute(rrqr_wave_kernel<false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)(kMaxM * sizeof(double) > kColdSmem ? kMaxM * sizeof(double) : kColdSmem));
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, rrqr_wave_kernel<false>, kT, smem) != cudaSuccess)
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, rrqr_wave_kernel<false, 1>, kT, smem) != cudaSuccess)
     return -1;
   return per * sms;
 }
@@ -2983,9 +2985,9 @@ int spand_rrqr_capacity(int vmax) {
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   size_t smem = kColdSmem;
   if ((size_t)vmax * sizeof(double) > smem) smem = (size_t)vmax * sizeof(double);
-  cudaFuncSetAttribute(rrqr_wave_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  cudaFuncSetAttribute(rrqr_wave_kernel<false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)(kMaxM * sizeof(double) > kColdSmem ? kMaxM * sizeof(double) : kColdSmem));
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, rrqr_wave_kernel<false>, kT, smem) != cudaSuccess)
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, rrqr_wave_kernel<false, 1>, kT, smem) != cudaSuccess)
     return -1;
   cached_dev = dev;
   cached_smem = smem;
@@ -3002,12 +3004,17 @@ int spand_rrqr_wave(int npanel, int grid, int vmax, const int64_t* panels, const
   size_t smem = (size_t)(vmax > 0 ? vmax : 1) * sizeof(double);
   if (smem < tile_bytes) smem = tile_bytes;
   cudaError_t e = cudaFuncSetAttribute(
-      rrqr_wave_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      rrqr_wave_kernel<false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
       (int)(kMaxM * sizeof(double) > kColdSmem ? kMaxM * sizeof(double) : kColdSmem));
   if (e != cudaSuccess) return (int)e;
   void* args[] = {&npanel, &panels, &nbrs, &m0, &off, &eps, &scheme, &events};
-  e = cudaLaunchCooperativeKernel((void*)rrqr_wave_kernel<false>, dim3(grid), dim3(kT), args, smem,
-                                  (cudaStream_t)stream);
+  const int sch = scheme & 3;
+  void* fn = sch == 0 ? (void*)rrqr_wave_kernel<false, 0>
+                      : (sch == 1 ? (void*)rrqr_wave_kernel<false, 1> : (void*)rrqr_wave_kernel<false, 2>);
+  e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)(kMaxM * sizeof(double) > kColdSmem ? kMaxM * sizeof(double) : kColdSmem));
+  if (e != cudaSuccess) return (int)e;
+  e = cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kT), args, smem, (cudaStream_t)stream);
   if (e != cudaSuccess) return (int)e;
   return 0;
 }
@@ -3039,14 +3046,14 @@ int spand_rrqr_cluster_capacity(int vmax, int cs) {
   if (cs < 2 || cs > 8 || (cs & (cs - 1))) return -1;
   size_t smem = kClSmem;
   if ((size_t)vmax * sizeof(double) > smem) smem = (size_t)vmax * sizeof(double);
-  if (cudaFuncSetAttribute(rrqr_wave_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  if (cudaFuncSetAttribute(rrqr_wave_kernel<true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)(kMaxM * sizeof(double) > kColdSmem ? kMaxM * sizeof(double)
                                                                     : kColdSmem)) != cudaSuccess)
     return -1;
   cudaLaunchAttribute at[2];
   cudaLaunchConfig_t cfg = cluster_cfg(cs * 8, cs, smem, 0, at);
   int ncl = 0;
-  if (cudaOccupancyMaxActiveClusters(&ncl, (void*)rrqr_wave_kernel<true>, &cfg) != cudaSuccess) return -1;
+  if (cudaOccupancyMaxActiveClusters(&ncl, (void*)rrqr_wave_kernel<true, 1>, &cfg) != cudaSuccess) return -1;
   return ncl * cs;
 }
 
@@ -3061,12 +3068,17 @@ int spand_rrqr_wave_clustered(int npanel, int grid, int vmax, int cs, const int6
   size_t smem = (size_t)(vmax > 0 ? vmax : 1) * sizeof(double);
   if (smem < kClSmem) smem = kClSmem;
   cudaError_t e = cudaFuncSetAttribute(
-      rrqr_wave_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      rrqr_wave_kernel<true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
       (int)(kMaxM * sizeof(double) > kColdSmem ? kMaxM * sizeof(double) : kColdSmem));
   if (e != cudaSuccess) return (int)e;
   cudaLaunchAttribute at[2];
   cudaLaunchConfig_t cfg = cluster_cfg(grid, cs, smem, (cudaStream_t)stream, at);
-  e = cudaLaunchKernelEx(&cfg, rrqr_wave_kernel<true>, npanel, panels, nbrs, m0, off, eps, scheme, events);
+  const int sch = scheme & 3;
+  auto fn = sch == 0 ? rrqr_wave_kernel<true, 0> : (sch == 1 ? rrqr_wave_kernel<true, 1> : rrqr_wave_kernel<true, 2>);
+  e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)(kMaxM * sizeof(double) > kColdSmem ? kMaxM * sizeof(double) : kColdSmem));
+  if (e != cudaSuccess) return (int)e;
+  e = cudaLaunchKernelEx(&cfg, fn, npanel, panels, nbrs, m0, off, eps, scheme, events);
   if (e != cudaSuccess) return (int)e;
   return 0;
 }
