@@ -589,7 +589,10 @@ __device__ void qform_batched(double* Q, const double* V, const double* taus, in
 #ifndef SPAND_CL_MINB1
 #define SPAND_CL_MINB1 2
 #endif
-#define SPAND_CL_MINB (kCl ? SPAND_CL_MINB1 : 2)
+#ifndef SPAND_MINB_CLASSIC
+#define SPAND_MINB_CLASSIC 1
+#endif
+#define SPAND_CL_MINB (kCl ? SPAND_CL_MINB1 : SPAND_MINB_CLASSIC)
 template <bool kCl, int kSch>
 __global__ void __launch_bounds__(kT, SPAND_CL_MINB)
 rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* __restrict__ nbrs,

@@ -1,0 +1,10 @@
+timeout 1500 python -m pytest tests -q -m gpu -x > gpurun_out/pytest_gpu_r02z.log 2>&1; echo pytest_rc=$?
+tail -2 gpurun_out/pytest_gpu_r02z.log
+timeout 900 python bench.py --no-cpu-baseline > gpurun_out/bench_r02z.json 2> gpurun_out/bench_r02z.err; echo bench_rc=$?
+python - <<'P'
+import json
+d=json.loads(open('gpurun_out/bench_r02z.json').read().strip().splitlines()[-1])
+for k in ['value','ms_per_step','factorize_s','solve_s','n_cg','e2e']: print(k, d.get(k))
+print(d['kernels_ms_per_step'])
+print(d['apply'])
+P
