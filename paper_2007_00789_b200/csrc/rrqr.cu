@@ -91,7 +91,14 @@ __device__ __forceinline__ double hot_rho(int m) {
   return m < 700 ? SPAND_RHO_A : (m < 1200 ? SPAND_RHO_B : (m < 2000 ? SPAND_RHO_C : SPAND_RHO_D));
 #endif
 }
-static_assert(kMinSmem >= 64 * 65 * sizeof(double), "epilogue tile");
+static_assert(kColdSmem >= 128 * 65 * sizeof(double), "epilogue tile");
+// frozen-column GEMM (qt_a): kFS cp.async stages of kFK rows of A (64 + 4
+// padded) and B (128 + 4 padded); the classic kernel runs one CTA per SM, so
+// its launches ask for kLaunchSmem of dynamic shared memory
+constexpr int kFK = 32, kFS = 3;
+constexpr size_t kFrozenSmem = (size_t)kFS * kFK * (68 + 132) * sizeof(double);
+constexpr size_t kLaunchSmem = kFrozenSmem > kColdSmem ? kFrozenSmem : kColdSmem;
+static_assert(kLaunchSmem >= 128 * 65 * sizeof(double), "frozen GEMM epilogue");
 static_assert(kMinSmem >= (size_t)kWarps * 16 * 33 * sizeof(double), "gather tiles");
 static_assert(kColdSmem >= kMinSmem, "cold layout covers the other phases");
 // clustered loop layout in the dynamic shared memory (doubles): exchange
@@ -128,9 +135,9 @@ struct Sh {
   double ccur[32], cref[32];   // clustered cold maintenance: running norms before the exchanges
   int nhot_cl, ncold_cl;      // clustered loop: list lengths (identical in the cluster)
   unsigned long long mcl;     // clustered reclassification: max running norm^2 (bits)
-  double* cbase[64];  // frozen GEMM epilogue: column base in the pool
-  int64_t cstride[64];
-  int fcol[64];
+  double* cbase[128];  // frozen GEMM epilogue: column base in the pool
+  int64_t cstride[128];
+  int fcol[128];
 };
 
 __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
@@ -2783,14 +2790,18 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
   // Element (t, c) accumulates over the rows in the same order in both
   // modes, whatever T and the column's tile.
   auto qt_a = [&](const int32_t* lst, const int cnt, const int T, const bool to_w) {
-    // two cp.async stages of A (Q^T rows) and B (original columns) tiles
-    double (*As)[16][kLDS] = reinterpret_cast<double (*)[16][kLDS]>(vsh);               // [2][16][kLDS]
-    double (*Bs)[16][kLDS] = reinterpret_cast<double (*)[16][kLDS]>(vsh + 2 * 16 * kLDS);  // [2][16][kLDS]
-    double (*Cs)[65] = reinterpret_cast<double (*)[65]>(vsh);                 // [64][65] (epilogue)
+    // CTA tile 64 rows (of Q^T) x 128 columns, warp tile 32 x 32 (16 DMMAs
+    // per k-step: one CTA per SM, 255 registers); two cp.async stages of A
+    // (Q^T rows) and B (original columns).  The K order per element is that
+    // of the previous 64 x 64 tiling (bit-identical results).
+    constexpr int kLB = 132;
+    double (*As)[kFK][kLDS] = reinterpret_cast<double (*)[kFK][kLDS]>(vsh);                 // [kFS][kFK][kLDS]
+    double (*Bs)[kFK][kLB] = reinterpret_cast<double (*)[kFK][kLB]>(vsh + kFS * kFK * kLDS);  // [kFS][kFK][kLB]
+    double (*Cs)[65] = reinterpret_cast<double (*)[65]>(vsh);                  // [128][65] (epilogue)
     const int wm = warp >> 2, wn = warp & 3;
-    for (int ct = 0; ct < cnt; ct += 64) {
+    for (int ct = 0; ct < cnt; ct += 128) {
       __syncthreads();
-      if (tid < 64) {
+      if (tid < 128) {
         if (ct + tid < cnt) {
           double* base;
           int64_t stride;
@@ -2805,19 +2816,25 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
       }
       __syncthreads();
       for (int rt = 0; rt < T; rt += 64) {
-        double acc[4][2][2];
+        double acc[4][4][2];
 #pragma unroll
         for (int a = 0; a < 4; ++a)
 #pragma unroll
-          for (int b = 0; b < 2; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+          for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
         auto load_stage = [&](int st, int i0) {
 #pragma unroll
-          for (int r = 0; r < 4; ++r) {
+          for (int r = 0; r < (kFK * 64) / kT; ++r) {
             const int e = tid + r * kT;
-            const int kk = e & 15, cl = e >> 4;
+            const int kk = e % kFK, cl = e / kFK;
             const int i = i0 + kk;
             const bool oka = i < m && rt + cl < T;
             cp_async8(&As[st][kk][cl], oka ? Q + (int64_t)i + (int64_t)(rt + cl) * m : Q, oka);
+          }
+#pragma unroll
+          for (int r = 0; r < (kFK * 128) / kT; ++r) {
+            const int e = tid + r * kT;
+            const int kk = e % kFK, cl = e / kFK;
+            const int i = i0 + kk;
             const int fc = sh.fcol[cl];
             const bool okb = i < m && fc >= 0;
             const double* bsrc =
@@ -2828,38 +2845,46 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
           cp_commit();
         };
         __syncthreads();
-        load_stage(0, 0);
-        int st = 0;
-        for (int i0 = 0; i0 < m; i0 += 16) {
-          cp_wait_all();
-          __syncthreads();
-          if (i0 + 16 < m) load_stage(st ^ 1, i0 + 16);
+        // kFS-stage pipeline: stages s + 1 .. s + kFS - 1 in flight while s computes
+        const int nstep = (m + kFK - 1) / kFK;
 #pragma unroll
-          for (int kq = 0; kq < 4; ++kq) {
+        for (int q = 0; q < kFS - 1; ++q) {
+          if (q < nstep) load_stage(q, q * kFK);
+          else cp_commit();
+        }
+        for (int s2 = 0; s2 < nstep; ++s2) {
+          asm volatile("cp.async.wait_group %0;\n" ::"n"(kFS - 2));
+          __syncthreads();
+          const int nx = s2 + kFS - 1;
+          if (nx < nstep) load_stage(nx % kFS, nx * kFK);
+          else cp_commit();
+          const int st = s2 % kFS;
+#pragma unroll
+          for (int kq = 0; kq < kFK / 4; ++kq) {
             const int kr = kq * 4 + (lane & 3);
-            double af[4], bf[2];
+            double af[4], bf[4];
 #pragma unroll
             for (int mi = 0; mi < 4; ++mi) af[mi] = As[st][kr][wm * 32 + mi * 8 + (lane >> 2)];
 #pragma unroll
-            for (int ni = 0; ni < 2; ++ni) bf[ni] = Bs[st][kr][wn * 16 + ni * 8 + (lane >> 2)];
+            for (int ni = 0; ni < 4; ++ni) bf[ni] = Bs[st][kr][wn * 32 + ni * 8 + (lane >> 2)];
 #pragma unroll
             for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
-              for (int ni = 0; ni < 2; ++ni) dmma(acc[mi][ni][0], acc[mi][ni][1], af[mi], bf[ni]);
+              for (int ni = 0; ni < 4; ++ni) dmma(acc[mi][ni][0], acc[mi][ni][1], af[mi], bf[ni]);
           }
-          st ^= 1;
         }
+        cp_wait_all();
         __syncthreads();
 #pragma unroll
         for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
-          for (int ni = 0; ni < 2; ++ni)
+          for (int ni = 0; ni < 4; ++ni)
 #pragma unroll
             for (int h = 0; h < 2; ++h)
-              Cs[wn * 16 + ni * 8 + (lane & 3) * 2 + h][wm * 32 + mi * 8 + (lane >> 2)] =
+              Cs[wn * 32 + ni * 8 + (lane & 3) * 2 + h][wm * 32 + mi * 8 + (lane >> 2)] =
                   acc[mi][ni][h];
         __syncthreads();
-        for (int e = tid; e < 64 * 64; e += kT) {
+        for (int e = tid; e < 64 * 128; e += kT) {
           const int r = e & 63, cl = e >> 6;
           const int t = rt + r;
           if (t < T && ct + cl < cnt) {
@@ -2962,7 +2987,7 @@ int spand_rrqr_cta_count(void) {
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   // capacity for panels up to 4224 rows (the tile staging size); taller
   // panels need more shared memory and are launched with smaller groups
-  const size_t smem = kColdSmem;
+  const size_t smem = kLaunchSmem;
   cudaFuncSetAttribute(rrqr_wave_kernel<false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)(kMaxM * sizeof(double) > kColdSmem ? kMaxM * sizeof(double) : kColdSmem));
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, rrqr_wave_kernel<false, 1>, kT, smem) != cudaSuccess)
@@ -2978,7 +3003,7 @@ int spand_rrqr_capacity(int vmax) {
   int dev = 0, sms = 0, per = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return -1;
   {
-    size_t smem0 = kColdSmem;
+    size_t smem0 = kLaunchSmem;
     if ((size_t)vmax * sizeof(double) > smem0) smem0 = (size_t)vmax * sizeof(double);
     if (dev == cached_dev && smem0 == cached_smem && cached_per > 0) {
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -2986,7 +3011,7 @@ int spand_rrqr_capacity(int vmax) {
     }
   }
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  size_t smem = kColdSmem;
+  size_t smem = kLaunchSmem;
   if ((size_t)vmax * sizeof(double) > smem) smem = (size_t)vmax * sizeof(double);
   cudaFuncSetAttribute(rrqr_wave_kernel<false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)(kMaxM * sizeof(double) > kColdSmem ? kMaxM * sizeof(double) : kColdSmem));
@@ -3003,7 +3028,7 @@ int spand_rrqr_wave(int npanel, int grid, int vmax, const int64_t* panels, const
                     void* stream) {
   if (npanel < 0 || grid < 0 || vmax < 0 || vmax > kMaxM) return -1;
   if (npanel == 0 || grid == 0) return 0;
-  const size_t tile_bytes = kColdSmem;
+  const size_t tile_bytes = kLaunchSmem;
   size_t smem = (size_t)(vmax > 0 ? vmax : 1) * sizeof(double);
   if (smem < tile_bytes) smem = tile_bytes;
   cudaError_t e = cudaFuncSetAttribute(
