@@ -437,7 +437,9 @@ def main():
                          "read (profiles/rrqr_step_probe_r01.jsonl)"}
         except Exception:
             pass
-    prof_path = os.path.join(HERE, "profiles", "ncu_r01_summary.json")
+    prof_path = os.path.join(HERE, "profiles", "ncu_r02_summary.json")
+    if not os.path.exists(prof_path):
+        prof_path = os.path.join(HERE, "profiles", "ncu_r01_summary.json")
     if os.path.exists(prof_path):
         try:
             with open(prof_path) as fh:
