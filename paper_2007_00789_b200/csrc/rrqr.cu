@@ -109,6 +109,9 @@ constexpr int kXB = 1056, kXS = 512, kHC = 512;
 constexpr int kClEnd = 3 * kXB + kXS + 4 * 32 * 33 + 2 * 32 * 33 + 2 * kHC + 2 * kHC;
 constexpr size_t kClSmem = (size_t)kClEnd * sizeof(double);
 static_assert(kClSmem >= kColdSmem, "clustered layout covers the post-loop phases");
+// the clustered kernel shares the post-loop phases, so its launches must also
+// cover the frozen-column GEMM's staging buffers
+constexpr size_t kClLaunchSmem = kClSmem > kFrozenSmem ? kClSmem : kFrozenSmem;
 
 struct Sh {
   double red[kWarps];
@@ -3072,7 +3075,7 @@ static cudaLaunchConfig_t cluster_cfg(int grid, int cs, size_t smem, cudaStream_
 
 int spand_rrqr_cluster_capacity(int vmax, int cs) {
   if (cs < 2 || cs > 8 || (cs & (cs - 1))) return -1;
-  size_t smem = kClSmem;
+  size_t smem = kClLaunchSmem;
   if ((size_t)vmax * sizeof(double) > smem) smem = (size_t)vmax * sizeof(double);
   if (cudaFuncSetAttribute(rrqr_wave_kernel<true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)(kMaxM * sizeof(double) > kColdSmem ? kMaxM * sizeof(double)
@@ -3094,7 +3097,7 @@ int spand_rrqr_wave_clustered(int npanel, int grid, int vmax, int cs, const int6
   if (cs < 2 || cs > 8 || (cs & (cs - 1)) || grid % cs) return -1;
   if (npanel == 0 || grid == 0) return 0;
   size_t smem = (size_t)(vmax > 0 ? vmax : 1) * sizeof(double);
-  if (smem < kClSmem) smem = kClSmem;
+  if (smem < kClLaunchSmem) smem = kClLaunchSmem;
   cudaError_t e = cudaFuncSetAttribute(
       rrqr_wave_kernel<true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
       (int)(kMaxM * sizeof(double) > kColdSmem ? kMaxM * sizeof(double) : kColdSmem));

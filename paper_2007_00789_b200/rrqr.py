@@ -35,6 +35,10 @@ def rrqr_single(a, eps, scheme, group=None, pad=0, cluster=0):
     cap = max(1, _lib.load().spand_rrqr_capacity(max(m, 1)))
     g = group or max(1, min(cap, n // 64, (m * n) // 65536 + 1))
     if cluster > 1:
+        # co-resident clusters bound the group (cooperative launch)
+        ccap = _lib.load().spand_rrqr_cluster_capacity(max(m, 1), cluster)
+        if ccap >= cluster:
+            g = min(g, ccap)
         g = max(cluster, (g // cluster) * cluster)
     ncap, mcap = max(np_, 1), max(mp, 1)
     wsz = mcap * ncap + mcap * mcap + 32 * (ncap + mcap) + 32 * mcap + 1024   # + T blocks

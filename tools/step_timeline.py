@@ -36,5 +36,5 @@ for rep in range(3):
     torch.cuda.synchronize()
     T["pcg"] = time.perf_counter() - t4
     T["total"] = time.perf_counter() - t0
-    print({k: round(v, 4) for k, v in T.items()}, "n_cg", rep_.n_cg, {k: round(v, 4) for k, v in f._plan.build_times.items()},
+    print({k: round(v, 4) for k, v in T.items()}, "n_cg", rep_.n_cg, {k: (round(v, 4) if isinstance(v, float) else v) for k, v in f._plan.build_times.items()},
           {k: round(v, 4) for k, v in TC.items() if k.startswith("collect")}, flush=True)
