@@ -113,6 +113,9 @@ static_assert(kClSmem >= kColdSmem, "clustered layout covers the post-loop phase
 // cover the frozen-column GEMM's staging buffers
 constexpr size_t kClLaunchSmem = kClSmem > kFrozenSmem ? kClSmem : kFrozenSmem;
 
+// largest group whose frozen-column product is dealt tile by tile over the
+// whole group (larger groups keep the per-CTA lists)
+constexpr int kMaxG = 320;
 struct Sh {
   double red[kWarps];
   double bval[kWarps];
@@ -141,6 +144,7 @@ struct Sh {
   double* cbase[128];  // frozen GEMM epilogue: column base in the pool
   int64_t cstride[128];
   int fcol[128];
+  int fpre[kMaxG + 1];  // frozen GEMM: prefix sums of the group's frozen-column counts
 };
 
 __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
@@ -2783,7 +2787,21 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
       __syncwarp();
     }
   }
+  // frozen-column counts of every CTA (the candidate records are free now:
+  // nobody reads them after the loop's last barrier)
+  int32_t* fcnt_g = reinterpret_cast<int32_t*>(cand);
+  if (tid == 0) fcnt_g[rank] = nf;
   group_barrier(ctr, G, gen, tgt, 200000, events + 12 * slot + 9);   // Q and W complete
+  const bool deal = G <= kMaxG;
+  if (deal) {
+    for (int r = tid; r < G; r += kT) sh.fpre[r + 1] = __ldcg(fcnt_g + r);
+    __syncthreads();
+    if (tid == 0) {
+      sh.fpre[0] = 0;
+      for (int r = 0; r < G; ++r) sh.fpre[r + 1] += sh.fpre[r];
+    }
+    __syncthreads();
+  }
   TL(trs);
   // R rows t < T of Q^T a for a list of columns (a = ORIGINAL column) on
   // the tensor cores (DMMA).  to_w = false: frozen columns, a restored in W,
@@ -2792,7 +2810,16 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
   // yet written back), rows written into W (replacing the in-loop values).
   // Element (t, c) accumulates over the rows in the same order in both
   // modes, whatever T and the column's tile.
-  auto qt_a = [&](const int32_t* lst, const int cnt, const int T, const bool to_w) {
+  //
+  // dealt = true (frozen columns): the group's frozen lists are taken as one
+  // list (rank-major) cut into 128-column tiles, and the (column tile, row
+  // tile) items are dealt round-robin over the whole group.  Every CTA gets
+  // the same number of items (+-1) whatever its own frozen count, and the
+  // group works on ~G / (T / 64) column tiles at a time, so their columns
+  // (3 MB each for the root panel) stay in L2 while Q is swept: with per-CTA
+  // lists the G column tiles in flight (470 MB) missed L2 on every sweep.
+  auto qt_a = [&](const int32_t* lst, const int cnt, const int T, const bool to_w,
+                  const bool dealt) {
     // CTA tile 64 rows (of Q^T) x 128 columns, warp tile 32 x 32 (16 DMMAs
     // per k-step: one CTA per SM, 255 registers); two cp.async stages of A
     // (Q^T rows) and B (original columns).  The K order per element is that
@@ -2802,39 +2829,66 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
     double (*Bs)[kFK][kLB] = reinterpret_cast<double (*)[kFK][kLB]>(vsh + kFS * kFK * kLDS);  // [kFS][kFK][kLB]
     double (*Cs)[65] = reinterpret_cast<double (*)[65]>(vsh);                  // [128][65] (epilogue)
     const int wm = warp >> 2, wn = warp & 3;
-    for (int ct = 0; ct < cnt; ct += 128) {
-      __syncthreads();
-      if (tid < 128) {
-        if (ct + tid < cnt) {
-          double* base;
-          int64_t stride;
-          const int c = lst[rank + G * (ct + tid)];
-          pool_col(c, base, stride);
-          sh.cbase[tid] = base;
-          sh.cstride[tid] = stride;
-          sh.fcol[tid] = c;
-        } else {
-          sh.fcol[tid] = -1;
+    const int total = dealt ? sh.fpre[G] : cnt;
+    const int nrt = (T + 63) / 64;
+    const int64_t nitem = (int64_t)((total + 127) / 128) * nrt;
+    int loaded = -1;
+    for (int64_t it = dealt ? rank : 0; it < nitem; it += dealt ? G : 1) {
+      const int cti = (int)(it / nrt);
+      const int ct = cti * 128, rt = (int)(it % nrt) * 64;
+      if (cti != loaded) {
+        loaded = cti;
+        __syncthreads();
+        if (tid < 128) {
+          if (ct + tid < total) {
+            double* base;
+            int64_t stride;
+            int c;
+            if (dealt) {
+              // owner of the tile's column: last r with fpre[r] <= index
+              const int g = ct + tid;
+              int lo2 = 0, hi2 = G - 1;
+              while (lo2 < hi2) {
+                const int mid = (lo2 + hi2 + 1) >> 1;
+                if (sh.fpre[mid] <= g) lo2 = mid;
+                else hi2 = mid - 1;
+              }
+              c = __ldcg(lst + lo2 + (int64_t)G * (g - sh.fpre[lo2]));
+            } else {
+              c = lst[rank + G * (ct + tid)];
+            }
+            pool_col(c, base, stride);
+            sh.cbase[tid] = base;
+            sh.cstride[tid] = stride;
+            sh.fcol[tid] = c;
+          } else {
+            sh.fcol[tid] = -1;
+          }
         }
+        __syncthreads();
       }
-      __syncthreads();
-      for (int rt = 0; rt < T; rt += 64) {
+      {
         double acc[4][4][2];
 #pragma unroll
         for (int a = 0; a < 4; ++a)
 #pragma unroll
           for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
-        auto load_stage = [&](int st, int i0) {
-#pragma unroll
-          for (int r = 0; r < (kFK * 64) / kT; ++r) {
-            const int e = tid + r * kT;
+        // one eighth of a stage's copies (1 of the 8 A and 2 of the 16 B copies
+        // of each thread): the next stage is issued in pieces between the
+        // k-steps of the current one, so the tensor pipe does not idle behind
+        // a block of address arithmetic at every stage boundary
+        static_assert((kFK * 64) / kT == 8 && (kFK * 128) / kT == 16 && kFK / 4 == 8,
+                      "stage copies split over the 8 k-steps");
+        auto load_part = [&](int st, int i0, int part) {
+          {
+            const int e = tid + part * kT;
             const int kk = e % kFK, cl = e / kFK;
             const int i = i0 + kk;
             const bool oka = i < m && rt + cl < T;
             cp_async8(&As[st][kk][cl], oka ? Q + (int64_t)i + (int64_t)(rt + cl) * m : Q, oka);
           }
 #pragma unroll
-          for (int r = 0; r < (kFK * 128) / kT; ++r) {
+          for (int r = 2 * part; r < 2 * part + 2; ++r) {
             const int e = tid + r * kT;
             const int kk = e % kFK, cl = e / kFK;
             const int i = i0 + kk;
@@ -2845,6 +2899,10 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
                                  : W + (int64_t)i + (int64_t)fc * m);
             cp_async8(&Bs[st][kk][cl], bsrc, okb);
           }
+        };
+        auto load_stage = [&](int st, int i0) {
+#pragma unroll
+          for (int part = 0; part < 8; ++part) load_part(st, i0, part);
           cp_commit();
         };
         __syncthreads();
@@ -2859,11 +2917,12 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
           asm volatile("cp.async.wait_group %0;\n" ::"n"(kFS - 2));
           __syncthreads();
           const int nx = s2 + kFS - 1;
-          if (nx < nstep) load_stage(nx % kFS, nx * kFK);
-          else cp_commit();
+          const bool more = nx < nstep;
           const int st = s2 % kFS;
 #pragma unroll
           for (int kq = 0; kq < kFK / 4; ++kq) {
+            if (more) load_part(nx % kFS, nx * kFK, kq);
+            if (kq == kFK / 4 - 1) cp_commit();
             const int kr = kq * 4 + (lane & 3);
             double af[4], bf[4];
 #pragma unroll
@@ -2890,7 +2949,7 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
         for (int e = tid; e < 64 * 128; e += kT) {
           const int r = e & 63, cl = e >> 6;
           const int t = rt + r;
-          if (t < T && ct + cl < cnt) {
+          if (t < T && ct + cl < total) {
             if (to_w) {
               W[(int64_t)t + (int64_t)sh.fcol[cl] * m] = Cs[cl][r];
             } else {
@@ -2902,7 +2961,11 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
       }
     }
   };
-  if (nf > 0) qt_a(flist, nf, k_c + n_corr, false);
+  if (deal) {
+    if (sh.fpre[G] > 0) qt_a(flist, 0, k_c + n_corr, false, true);
+  } else if (nf > 0) {
+    qt_a(flist, nf, k_c + n_corr, false, false);
+  }
   // superfine: the columns the first-order run would have formed as Q^T a
   // (fofl) but that stayed active here get their R rows < k_c the same way,
   // from the original column (rows >= k_c keep their in-loop values)
@@ -2914,7 +2977,7 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
       if (__ldcg(fofl + c) && __ldcg(done + c) != 2) l2[rank + G * atomicAdd(&sh.nact, 1)] = c;
     __syncthreads();
     const int n2 = sh.nact;
-    if (n2 > 0 && k_c > 0) qt_a(l2, n2, k_c, true);
+    if (n2 > 0 && k_c > 0) qt_a(l2, n2, k_c, true, false);
     // the write-back below covers contiguous column ranges, the product
     // above the interleaved ownership
     group_barrier(ctr, G, gen, tgt, 300000, events + 12 * slot + 9);
