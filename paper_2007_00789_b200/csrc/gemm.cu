@@ -13,6 +13,8 @@
 // 5 64x32, 6 32x64 --
 // the leaf levels' targets are a few rows or columns wide, and a 64x64 tile
 // on a 6-column target spends 90 % of its tensor work on padding.
+#include <type_traits>
+
 #include "common.cuh"
 #include "../../include/spand_b200.h"
 
@@ -141,6 +143,7 @@ gemm_grouped_kernel(const int64_t* __restrict__ tiles, const int64_t* __restrict
 
   if (seg < se) {
     int st = 0;
+    int dense_run = 0, unchecked = 0;   // zero-slice test policy (warp-uniform)
     load_stage(0, A, B, k0, K);
     while (true) {
       // advance iterator to the next chunk and prefetch it
@@ -160,19 +163,62 @@ gemm_grouped_kernel(const int64_t* __restrict__ tiles, const int64_t* __restrict
       cp_wait_all();
       __syncthreads();
       if (have_next) load_stage(st ^ 1, An, Bn, kn, Kn);
+      // The operands are block-sparse by rows: an eliminated interior
+      // touches a few dofs of each separator, so most 4-deep k-slices of a
+      // panel's rows (Schur update) or of an unscaled interface block
+      // (Z^-1 B) are exact zeros over a warp's 32 rows / columns.  A slice
+      // whose A or B fragments are all zero adds +-0 to every accumulator
+      // (they start at +0, so the bits do not change): its DMMAs are skipped.
+      // The test splits the unrolled k-loop (no fragment prefetch across
+      // slices), which costs ~15 % on dense operands, so a warp that skipped
+      // nothing in two consecutive stages runs the next 8 stages unchecked.
+      auto stage = [&](auto checked) {
+        constexpr bool kCheck = decltype(checked)::value;
+        bool skipped = false;
 #pragma unroll
-      for (int kk = 0; kk < BK / 4; ++kk) {
-        double af[FM], bf[FN];
-        const int kr = kk * 4 + (lane & 3);
+        for (int kk = 0; kk < BK / 4; ++kk) {
+          double af[FM], bf[FN];
+          const int kr = kk * 4 + (lane & 3);
+          bool nzb = false;
 #pragma unroll
-        for (int mi = 0; mi < FM; ++mi) af[mi] = As[st][kr][wm * WM + mi * 8 + (lane >> 2)];
+          for (int ni = 0; ni < FN; ++ni) {
+            bf[ni] = Bs[st][kr][wn * WN + ni * 8 + (lane >> 2)];
+            if (kCheck) nzb |= bf[ni] != 0.0;
+          }
+          if (kCheck && !__any_sync(0xffffffffu, nzb)) {
+            skipped = true;
+            continue;
+          }
+          bool nza = false;
 #pragma unroll
-        for (int ni = 0; ni < FN; ++ni) bf[ni] = Bs[st][kr][wn * WN + ni * 8 + (lane >> 2)];
+          for (int mi = 0; mi < FM; ++mi) {
+            af[mi] = As[st][kr][wm * WM + mi * 8 + (lane >> 2)];
+            if (kCheck) nza |= af[mi] != 0.0;
+          }
+          if (kCheck && !__any_sync(0xffffffffu, nza)) {
+            skipped = true;
+            continue;
+          }
 #pragma unroll
-        for (int mi = 0; mi < FM; ++mi)
+          for (int mi = 0; mi < FM; ++mi)
 #pragma unroll
-          for (int ni = 0; ni < FN; ++ni) dmma(acc[mi][ni][0], acc[mi][ni][1], af[mi], bf[ni]);
+            for (int ni = 0; ni < FN; ++ni) dmma(acc[mi][ni][0], acc[mi][ni][1], af[mi], bf[ni]);
+        }
+        return skipped;
+      };
+#ifdef SPAND_GEMM_NOSKIP
+      stage(std::false_type{});
+#else
+      if (unchecked > 0) {
+        --unchecked;
+        stage(std::false_type{});
+      } else if (stage(std::true_type{})) {
+        dense_run = 0;
+      } else if (++dense_run >= 2) {
+        dense_run = 0;
+        unchecked = 8;
       }
+#endif
       __syncthreads();
       if (!have_next) break;
       st ^= 1;

@@ -714,6 +714,9 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
   // them, or they were cold when it stopped); formed the same way here, so
   // the trailing matrix is bit for bit the same in every scheme
   int32_t* fofl = flist + 24 * ncap;
+  // 1: frozen at step 0 of the classic loop, before any reflector touched
+  // the column: W still holds the original data (no restore needed)
+  int32_t* untouched = flist + 28 * ncap;
 
   const int c0 = (int)(((int64_t)n * rank) / G), c1 = (int)(((int64_t)n * (rank + 1)) / G);
   const int q0 = (int)(((int64_t)m * rank) / G), q1 = (int)(((int64_t)m * (rank + 1)) / G);
@@ -809,6 +812,7 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
       perm[c] = c;   // position -> column (the clustered loop keeps it current)
       done[c] = 0;
       fofl[c] = 0;
+      if (!kCl) untouched[c] = 0;   // (the clustered loop's lists may use that region)
       if (better(s, c, bv, bp)) {
         bv = s;
         bp = c;
@@ -2579,6 +2583,7 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
       // its in-loop coarse rows, so it is never frozen)
       if (cur[c] < thr2 && (fo_track || scheme != 2 || fofl[c])) {
         done[c] = 2;
+        if (k == 0) untouched[c] = 1;
         atomicMax(&sh.fmax, (unsigned long long)__double_as_longlong(cur[c]));
       } else {
         list_out[rank + G * atomicAdd(&sh.nact, 1)] = c;
@@ -2760,12 +2765,13 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
     for (int tix = warp; tix < ntc * ntr; tix += kWarps) {
       const int tc = c0 + (tix / ntr) * 16, tr = (tix % ntr) * 32;
       bool any = false;
-      for (int q = 0; q < 16; ++q) any |= (tc + q < c1) && done[tc + q] == 2;
+      for (int q = 0; q < 16; ++q)
+        any |= (tc + q < c1) && done[tc + q] == 2 && (kCl || !__ldcg(untouched + tc + q));
       if (!any) continue;
       for (int q = 0; q < 16; ++q) {
         const int c = tc + q;
         double val = 0.0;
-        if (c < c1 && done[c] == 2) {
+        if (c < c1 && done[c] == 2 && (kCl || !__ldcg(untouched + c))) {
           int j, cc;
           nbr_of(c, j, cc);
           const int64_t* nr = nbrs + 4 * (int64_t)(nb0 + j);
@@ -2782,7 +2788,8 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
       __syncwarp();
       for (int q = 0; q < 16; ++q) {
         const int c = tc + q, i = tr + lane;
-        if (c < c1 && i < m && done[c] == 2) W[(int64_t)i + (int64_t)c * m] = tile[warp][q][lane];
+        if (c < c1 && i < m && done[c] == 2 && (kCl || !__ldcg(untouched + c)))
+          W[(int64_t)i + (int64_t)c * m] = tile[warp][q][lane];
       }
       __syncwarp();
     }
