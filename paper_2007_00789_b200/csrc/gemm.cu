@@ -40,8 +40,13 @@ struct SegIter {
   int seg, seg_end, k0;
 };
 
+// four CTAs per SM (<= 128 registers, no spills: 124 for the 64x64 tile,
+// which takes 154 unconstrained = three CTAs per SM; GEMM 171 -> 163 ms)
+#ifndef SPAND_GEMM_MINB
+#define SPAND_GEMM_MINB 4
+#endif
 template <int BM, int BN, int WM, int WN>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, SPAND_GEMM_MINB)
 gemm_grouped_kernel(const int64_t* __restrict__ tiles, const int64_t* __restrict__ targets,
                     const int64_t* __restrict__ segs, const int32_t* __restrict__ m0,
                     const int32_t* __restrict__ off, double alpha, double beta, int bT,

@@ -6,8 +6,12 @@ config, so only size-independent properties are compared here):
 - integer structure bit-exact: per-level interior counts, per-interface
   (cluster, size_before, size_after, rank_f2), the final block, the
   permutation (sha256) and the operator-kind string;
-- nnz_factor within 2e-3 (exact-zero counting of rounding noise, see
-  test_gpu_factorize.py);
+- nnz_factor within 5e-4 (measured: 2e-5 .. 2e-4).  Eliminations, scalings
+  and corrections count exactly; a few entries per orthogonal operator that
+  are mathematically zero come out as exact 0.0 in the reference's
+  operation order (a cancellation such as 1 - 1 in its forward accumulation
+  of Q) and as 1e-16 .. 1e-50 residue in any other order (tools/
+  q_zero_pattern.py lists them: 1-3 entries of 3 % of the Q's);
 - PCG: n_cg within +-1, same convergence flag, true residual within 10x of
   the reference's, and
   the first residual-history entries within 1e-6 relative of the
@@ -58,7 +62,7 @@ def test_config_matches_reference(tag):
     kinds = "".join("GDQE"[["elimination", "scaling", "orthogonal",
                             "error-correction"].index(op.kind.value)] for op in f.ops)
     assert kinds == rec["op_kinds"]
-    assert abs(f.nnz_factor - rec["nnz_factor"]) <= 2e-3 * rec["nnz_factor"] + 16
+    assert abs(f.nnz_factor - rec["nnz_factor"]) <= 5e-4 * rec["nnz_factor"] + 16
     b = arr["b"]
     x, rep = sp.pcg(a, b, m=f.apply_m, tol=rec["tol"])
     assert abs(rep.n_cg - rec["n_cg"]) <= 1

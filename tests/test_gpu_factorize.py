@@ -73,12 +73,16 @@ def test_factorize_matches_reference(tag):
     kinds = "".join("GDQE"[["elimination", "scaling", "orthogonal",
                             "error-correction"].index(op.kind.value)] for op in f.ops)
     assert kinds == rec["op_kinds"]
-    # nnz counts EXACT zeros.  Q is accumulated backwards on the device
-    # (dorg2r order) while the reference accumulates forwards
-    # (dense.py:165-166); entries that are mathematically zero come out as
-    # exact 0.0 in one order and as 1e-17..1e-27 rounding noise in the other,
-    # so the count agrees to ~1% (payloads themselves are checked below)
-    assert abs(f.nnz_factor - rec["nnz_factor"]) <= 2e-3 * rec["nnz_factor"] + 16
+    # nnz counts EXACT zeros.  Eliminations, scalings and corrections count
+    # exactly like the reference's; in 2-3 % of the orthogonal operators one
+    # to three entries that are mathematically zero are an exact 0.0 in the
+    # reference (a cancellation such as 1 - 1 in ITS operation order, the
+    # forward accumulation of dense.py:165-166) and 1e-16 .. 1e-50 residue in
+    # any other order (tools/q_zero_pattern.py prints them), so the count
+    # agrees to a few entries per Q
+    n_q = sum(1 for op in f.ops if op.kind.value == "orthogonal")
+    # (measured over the 20 fixtures: 0 .. 8 entries, tools/nnz_small.py)
+    assert abs(f.nnz_factor - rec["nnz_factor"]) <= n_q
     # payloads vs the oracle factor, per block
     cl = [(c.id, c.dofs, c.depth) for c in h.clusters]
     of = orc.factorize(a.n, a.row_ptr, a.col_idx, a.values, cl, rec["levels"],
