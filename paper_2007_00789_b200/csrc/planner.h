@@ -795,12 +795,17 @@ struct Plan {
           for (size_t u = 0; u < L.inbrs[k].size(); ++u) {
             const int w = L.inbrs[k][u];
             const int64_t pws = pool_base + 8 * boff[L.inb_blk[L.inb_ptr[k] + u]];
-            const int64_t tmp = temp_base + 8 * acc;
+            // a panel one column tile wide is updated in place: each tile
+            // reads its own rows of the block over the whole K range before
+            // its epilogue writes them (no other tile touches those rows)
+            const bool inplace = m0[s] <= kShapeN[tile_shape(m0[w], m0[s])];
+            const int64_t tmp = inplace ? pws : temp_base + 8 * acc;
             tg.target(m0[w], m0[s], dry, tmp, (int64_t)w, (int64_t)s, (int64_t)0, (int64_t)0,
                       (int64_t)-1, (int64_t)-1);
             const int64_t oa[7] = {pws, w, s, 0, 0, -1, -1};
             const int64_t ob[7] = {linv_s, s, s, 0, 0, -1, -1};
             tg.seg_opnds(oa, ob);
+            if (inplace) continue;
             cps.insert(cps.end(), {tmp, w, s, 0, 0, -1, -1, pws, w, s, 0, 0, -1, -1, 0});
             acc += m0[w] * m0[s];
           }
