@@ -437,9 +437,8 @@ def main():
                          "read (profiles/rrqr_step_probe_r01.jsonl)"}
         except Exception:
             pass
-    prof_path = os.path.join(HERE, "profiles", "ncu_r02_summary.json")
-    if not os.path.exists(prof_path):
-        prof_path = os.path.join(HERE, "profiles", "ncu_r01_summary.json")
+    prof_path = next((q for q in (os.path.join(HERE, "profiles", f"ncu_r0{k}_summary.json")
+                                  for k in (3, 2, 1)) if os.path.exists(q)), "")
     if os.path.exists(prof_path):
         try:
             with open(prof_path) as fh:
@@ -558,6 +557,19 @@ def main():
         "roofline": roof, "gpu_launches": int(launches),
         "clocks": clk.summary(),
     }
+    # the Schur / TRSM / rescale products (north_star d): algorithmic flops
+    # F_elim + F_scale over the grouped-GEMM launches of a step (with the
+    # K-chunk mask pass that feeds them)
+    gemm_ms = sum(v["ms"] for k, v in kern.items()
+                  if k in ("spand_gemm_grouped", "spand_gemm_kmask"))
+    if gemm_ms > 0:
+        gtf = (ff["F_elim"] + ff["F_scale"]) / (gemm_ms / 1000.0) / 1e12
+        line["gemm"] = {"ms": gemm_ms, "tflops": gtf,
+                        "frac_cublas_dgemm": gtf / FP64_DGEMM_TFLOPS,
+                        "frac_dmma_peak": gtf / 33.1,
+                        "basis": "(F_elim + F_scale) / (spand_gemm_grouped + spand_gemm_kmask "
+                                 "time of the profiled step); peaks: cuBLAS DGEMM 35.5, DMMA "
+                                 "loop 33.1 TFLOP/s (profiles/fp64_peak_r01.jsonl)"}
     if rank == 0 and not args.no_near_kernel:
         # near-kernel extension (not in the reference, so not the headline):
         # BASELINE C4 asks for the constant vector preserved in each coarse

@@ -197,6 +197,25 @@ int spand_gemm_grouped(int ntile, const int64_t* tiles, const int64_t* targets,
                        const int32_t* off, double alpha, double beta, int bT,
                        int lower_only, int tri, const int64_t* btab, int compact,
                        void* stream);
+/* The same product with K-chunk masks (bT = 0, compact = 0, one segment per
+ * target): kmask[kmoff[t] + c] != 0 when rows 16 c .. 16 c + 15 of target t's
+ * B operand hold a nonzero; chunks of zero rows are neither loaded nor
+ * multiplied (their products are exact zeros, so the result is bit for bit
+ * that of spand_gemm_grouped).  Serves the interface rescale Z_i^-1 B
+ * (factorize.py:165-173, schemes.py:235): before its first sparsification a
+ * separator is coupled to a neighbour through a few of its rows only.
+ * kmask = NULL: no masks. */
+int spand_gemm_grouped_masked(int ntile, const int64_t* tiles, const int64_t* targets,
+                              const int64_t* segs, const int32_t* m0,
+                              const int32_t* off, double alpha, double beta, int bT,
+                              int lower_only, int tri, const int64_t* btab, int compact,
+                              const unsigned char* kmask, const int64_t* kmoff,
+                              void* stream);
+/* Writes the K-chunk masks of a masked launch: one CTA per target, B = the B
+ * operand of the target's first segment (14-int64 segment rows). */
+int spand_gemm_kmask(int ntarget, const int64_t* targets, const int64_t* segs,
+                     const int32_t* m0, const int32_t* off, unsigned char* kmask,
+                     const int64_t* kmoff, void* stream);
 
 /* One wave of the batched early-stopping column-pivoted Householder QR of
  * interface panels (restates dense.py:117-222, schemes.py:272-318,

@@ -50,7 +50,8 @@ __global__ void __launch_bounds__(kThreads, SPAND_GEMM_MINB)
 gemm_grouped_kernel(const int64_t* __restrict__ tiles, const int64_t* __restrict__ targets,
                     const int64_t* __restrict__ segs, const int32_t* __restrict__ m0,
                     const int32_t* __restrict__ off, double alpha, double beta, int bT,
-                    int lower_only, int tri, const int64_t* __restrict__ btab, int compact) {
+                    int lower_only, int tri, const int64_t* __restrict__ btab, int compact,
+                    const unsigned char* __restrict__ kmask, const int64_t* __restrict__ kmoff) {
   static_assert((BM / WM) * (BN / WN) == kThreads / 32, "4 warps per tile");
   constexpr int FM = WM / 8, FN = WN / 8;              // 8x8 fragments per warp
   constexpr int LDA = BM + 4, LDB = BN + 4;            // padding: conflict-free frags
@@ -102,12 +103,23 @@ gemm_grouped_kernel(const int64_t* __restrict__ tiles, const int64_t* __restrict
     if ((tri & 2) && j0 + BN < khi) khi = j0 + BN;
     klo = (tri & 4) ? j0 : 0;
   };
+  // K-chunk mask of the target's (single) segment: byte c is nonzero when
+  // rows 16 c .. 16 c + 15 of B hold a nonzero (kmask_kernel below).  Chunks
+  // of zero rows are not even loaded: an unscaled interface block couples a
+  // separator to a neighbour through a few of its rows only.
+  const unsigned char* mk = kmask ? kmask + kmoff[t] : nullptr;
+  auto next_k = [&](int k, int kend) {
+    if (mk)
+      while (k < kend && !mk[k >> 4]) k += BK;
+    return k;
+  };
   int seg = sb, k0 = 0;
   Opnd A, B;
   int K = 0;
   auto open_seg = [&](int s) {
     seg_opnds(s, A, B);
     krange(A, B, k0, K);
+    k0 = next_k(k0, K);
   };
   // skip empty segments
   while (seg < se) {
@@ -153,13 +165,14 @@ gemm_grouped_kernel(const int64_t* __restrict__ tiles, const int64_t* __restrict
     while (true) {
       // advance iterator to the next chunk and prefetch it
       Opnd An = A, Bn = B;
-      int Kn = K, segn = seg, kn = k0 + BK;
+      int Kn = K, segn = seg, kn = next_k(k0 + BK, K);
       bool have_next = true;
       if (kn >= Kn) {
         ++segn;
         while (segn < se) {
           seg_opnds(segn, An, Bn);
           krange(An, Bn, kn, Kn);
+          kn = next_k(kn, Kn);
           if (Kn > kn) break;
           ++segn;
         }
@@ -176,7 +189,7 @@ gemm_grouped_kernel(const int64_t* __restrict__ tiles, const int64_t* __restrict
       // (they start at +0, so the bits do not change): its DMMAs are skipped.
       // The test splits the unrolled k-loop (no fragment prefetch across
       // slices), which costs ~15 % on dense operands, so a warp that skipped
-      // nothing in two consecutive stages runs the next 8 stages unchecked.
+      // nothing in two consecutive stages runs the next 16 stages unchecked.
       auto stage = [&](auto checked) {
         constexpr bool kCheck = decltype(checked)::value;
         bool skipped = false;
@@ -221,7 +234,7 @@ gemm_grouped_kernel(const int64_t* __restrict__ tiles, const int64_t* __restrict
         dense_run = 0;
       } else if (++dense_run >= 2) {
         dense_run = 0;
-        unchecked = 8;
+        unchecked = 16;
       }
 #endif
       __syncthreads();
@@ -252,20 +265,83 @@ gemm_grouped_kernel(const int64_t* __restrict__ tiles, const int64_t* __restrict
     }
   }
 }
+// K-chunk masks of a masked GEMM launch: B = the B operand of the target's
+// first segment (14-int64 segment rows); kmask[kmoff[t] + c] = any nonzero
+// in rows 16 c .. 16 c + 15 of B.  Work unit = (target, 128-row slab): one
+// row per thread (coalesced column reads, 8 independent loads in flight), a
+// chunk is 16 consecutive lanes.  Slabs of a target are dealt over
+// gridDim.y CTAs (the blocks between two top separators have ~10^7 entries).
+constexpr int kMaskY = 8;
+__global__ void __launch_bounds__(kThreads)
+kmask_kernel(const int64_t* __restrict__ targets, const int64_t* __restrict__ segs,
+             const int32_t* __restrict__ m0, const int32_t* __restrict__ off,
+             unsigned char* __restrict__ kmask, const int64_t* __restrict__ kmoff) {
+  const int64_t t = blockIdx.x;
+  const int64_t s = targets[8 * t + 7];
+  const Opnd B = load_opnd(segs + 14 * s + 7, m0, off);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nch = (B.rows + 15) >> 4;
+  unsigned char* out = kmask + kmoff[t];
+  for (int r0 = kThreads * blockIdx.y; r0 < B.rows; r0 += kThreads * gridDim.y) {
+    const int r = r0 + tid;
+    bool nz = false;
+    if (r < B.rows) {
+      const double* rp = B.p + r;
+      int col = 0;
+      for (; col + 8 <= B.cols; col += 8) {
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = __ldg(rp + (int64_t)(col + u) * B.ld);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) nz |= v[u] != 0.0;
+      }
+      for (; col < B.cols; ++col) nz |= __ldg(rp + (int64_t)col * B.ld) != 0.0;
+    }
+    const unsigned bal = __ballot_sync(0xffffffffu, nz);
+    if (lane == 0) {
+      const int c = (r0 >> 4) + 2 * warp;
+      if (c < nch) out[c] = (bal & 0xffffu) ? 1 : 0;
+      if (c + 1 < nch) out[c + 1] = (bal >> 16) ? 1 : 0;
+    }
+  }
+}
 }  // namespace
+
+extern "C" int spand_gemm_kmask(int ntarget, const int64_t* targets, const int64_t* segs,
+                                const int32_t* m0, const int32_t* off, unsigned char* kmask,
+                                const int64_t* kmoff, void* stream) {
+  if (ntarget < 0) return -1;
+  if (ntarget == 0) return 0;
+  kmask_kernel<<<dim3(ntarget, kMaskY), kThreads, 0, as_stream(stream)>>>(targets, segs, m0, off,
+                                                                          kmask, kmoff);
+  SPAND_CHECK_LAUNCH();
+  return 0;
+}
 
 extern "C" int spand_gemm_grouped(int ntile, const int64_t* tiles, const int64_t* targets,
                                   const int64_t* segs, const int32_t* m0, const int32_t* off,
                                   double alpha, double beta, int bT, int lower_only,
                                   int tri, const int64_t* btab, int compact, void* stream) {
+  return spand_gemm_grouped_masked(ntile, tiles, targets, segs, m0, off, alpha, beta, bT,
+                                   lower_only, tri, btab, compact, nullptr, nullptr, stream);
+}
+
+extern "C" int spand_gemm_grouped_masked(int ntile, const int64_t* tiles, const int64_t* targets,
+                                  const int64_t* segs, const int32_t* m0, const int32_t* off,
+                                  double alpha, double beta, int bT, int lower_only,
+                                  int tri, const int64_t* btab, int compact,
+                                  const unsigned char* kmask, const int64_t* kmoff,
+                                  void* stream) {
   if (ntile < 0) return -1;
+  // masks describe 16-row chunks of B: C = A B with 14-int64 segment rows
+  if (kmask && (bT || compact || !kmoff)) return -1;
   if (ntile == 0) return 0;
   const int shape = (tri >> 4) & 7;
   tri &= 7;
   cudaStream_t st = as_stream(stream);
 #define SPAND_GEMM_LAUNCH(BM_, BN_, WM_, WN_)                                             \
   gemm_grouped_kernel<BM_, BN_, WM_, WN_><<<ntile, kThreads, 0, st>>>(                    \
-      tiles, targets, segs, m0, off, alpha, beta, bT, lower_only, tri, btab, compact)
+      tiles, targets, segs, m0, off, alpha, beta, bT, lower_only, tri, btab, compact, kmask, kmoff)
   switch (shape) {
     case 0: SPAND_GEMM_LAUNCH(64, 64, 32, 32); break;
     case 1: SPAND_GEMM_LAUNCH(64, 16, 16, 16); break;

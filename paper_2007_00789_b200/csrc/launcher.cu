@@ -60,10 +60,18 @@ int spand_run_launches(int nl, const int64_t* recs, int64_t base, int32_t* m0, i
         double alpha, beta;
         std::memcpy(&alpha, r + 8, 8);
         std::memcpy(&beta, r + 9, 8);
-        st = spand_gemm_grouped(cnt, P(ao), P(bo), P(co), m0, off, alpha, beta, (int)x0, (int)x1,
-                                (int)x2, btab, (int)r[10], stream);
+        // fields 11 / 12: K-chunk masks (device address; offsets row relative
+        // to the targets row), written by the type-12 record just before
+        st = spand_gemm_grouped_masked(cnt, P(ao), P(bo), P(co), m0, off, alpha, beta, (int)x0,
+                                       (int)x1, (int)x2, btab, (int)r[10],
+                                       reinterpret_cast<const unsigned char*>(r[11]),
+                                       r[11] ? P(bo + r[12]) : nullptr, stream);
         break;
       }
+      case 12:
+        st = spand_gemm_kmask(cnt, P(ao), P(bo), m0, off, reinterpret_cast<unsigned char*>(x0),
+                              P(co), stream);
+        break;
       case 4:
         st = spand_copy_batched(cnt, P(ao), m0, off, stream);
         break;

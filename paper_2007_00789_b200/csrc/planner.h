@@ -393,8 +393,12 @@ struct Plan {
       }
       need = std::max({need, trsm, tri});
       if (L.skipped) continue;
-      int64_t resc = 0, tri2 = 0;
-      for (int b : L.resc_blocks) resc += m0[bi[b]] * m0[bj[b]];
+      int64_t resc = 0, tri2 = 0, kmask_bytes = 0;
+      for (int b : L.resc_blocks) {
+        resc += m0[bi[b]] * m0[bj[b]];
+        kmask_bytes += (m0[bi[b]] + 15) / 16;   // K-chunk masks behind the products
+      }
+      resc += (kmask_bytes + 7) / 8 + 1;
       for (int p : L.active) tri2 += m0[p] * m0[p];
       need = std::max({need, resc, tri2});
       for (int wv = 0; wv < L.nwaves; ++wv) {
@@ -487,14 +491,21 @@ struct Plan {
   };
   // tri: triangular-operand K bounds (gemm.cu): 1 A lower, 2 B lower with
   // C = A B^T, 4 B lower with C = A B
+  // mask_addr != 0: K-chunk masks (gemm.cu kmask_kernel) of the targets' B
+  // operands at that device address, one byte per 16 rows of B, target t at
+  // the running sum of ceil(mm / 16) (mm = the static row count of C and B)
   void gemm(const std::vector<Target>& ts, double alpha, double beta, int bT, int lower,
-            int tri = 0, int compact = 0) {
+            int tri = 0, int compact = 0, int64_t mask_addr = 0) {
     if (ts.empty()) return;
     const int64_t sw = compact ? 1 : 14;
-    std::vector<int64_t> trow, srow, tiles[kNShape];
-    int64_t nseg = 0;
+    std::vector<int64_t> trow, srow, tiles[kNShape], kmoff;
+    int64_t nseg = 0, moff = 0;
     trow.reserve(8 * ts.size() + 8);
     for (size_t t = 0; t < ts.size(); ++t) {
+      if (mask_addr) {
+        kmoff.push_back(moff);
+        moff += (ts[t].mm + 15) / 16;
+      }
       trow.insert(trow.end(), ts[t].c.data(), ts[t].c.data() + ts[t].c.size());
       trow.push_back(nseg);
       srow.insert(srow.end(), ts[t].segs.data(), ts[t].segs.data() + ts[t].segs.size());
@@ -505,22 +516,34 @@ struct Plan {
     }
     trow.insert(trow.end(), {0, 0, 0, 0, 0, 0, 0, nseg});
     if (dry) return;
-    emit_gemm(tiles, trow, srow, alpha, beta, bT, lower, tri, compact);
+    emit_gemm(tiles, trow, srow, alpha, beta, bT, lower, tri, compact, mask_addr,
+              mask_addr ? &kmoff : nullptr);
   }
   void emit_gemm(std::vector<int64_t> (&tiles)[kNShape], std::vector<int64_t>& trow,
                  std::vector<int64_t>& srow, double alpha, double beta, int bT, int lower,
-                 int tri, int compact) {
-    int64_t b = -1, c = -1;
+                 int tri, int compact, int64_t mask_addr = 0,
+                 const std::vector<int64_t>* kmoff = nullptr) {
+    int64_t b = -1, c = -1, ko = 0;
     for (int s = 0; s < kNShape; ++s) {
       if (tiles[s].empty()) continue;
       if (b < 0) {
         if (srow.empty()) srow.assign(14, 0);
         b = push(trow);
         c = push(srow);
+        if (mask_addr) {
+          ko = push(*kmoff);
+          launch(12, (int64_t)kmoff->size(), b, c, ko, mask_addr);
+        }
       }
       const int64_t a = push(tiles[s]);
       launch(3, (int64_t)tiles[s].size(), a, b, c, bT, lower, tri | (s << 4), alpha, beta);
       launches[launches.size() - 6] = compact;   // field 10
+      if (mask_addr) {
+        launches[launches.size() - 5] = mask_addr;   // field 11
+        // field 12: the offsets row relative to the targets row (only the
+        // fields a, b, c are rebased when a program chunk is exported)
+        launches[launches.size() - 4] = ko - b;
+      }
     }
   }
 
@@ -876,7 +899,7 @@ struct Plan {
       for (size_t k = 0; k < na; ++k) linv_of[L.active[k]] = L.linv_off[k];
       if (!L.resc_blocks.empty()) {
         std::vector<Target> g1, g2;
-        int64_t acc = 0;
+        int64_t acc = 0, mask_bytes = 0;
         for (int b : L.resc_blocks) {
           const int i = bi[b], j = bj[b];
           Target t1;
@@ -894,9 +917,12 @@ struct Plan {
           t2.nn = m0[j];
           g2.push_back(std::move(t2));
           acc += m0[i] * m0[j];
+          mask_bytes += (m0[i] + 15) / 16;
         }
-        temp_size = std::max(temp_size, acc);
-        gemm(g1, 1.0, 0.0, 0, 0, 1);   // T = Z_i^-1 B
+        // K-chunk masks of the unscaled blocks behind the products' temp
+        const int64_t mask_addr = temp_base + 8 * acc;
+        temp_size = std::max(temp_size, acc + (mask_bytes + 7) / 8 + 1);
+        gemm(g1, 1.0, 0.0, 0, 0, 1, 0, mask_addr);   // T = Z_i^-1 B
         gemm(g2, 1.0, 0.0, 1, 0, 2);   // B = T Z_j^-T
       }
       // sparsify, wave by wave (factorize.py:323-340)

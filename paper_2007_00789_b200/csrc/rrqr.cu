@@ -67,6 +67,10 @@ constexpr size_t kColdSmem = (size_t)kColdEnd * sizeof(double);
 #define SPAND_ROW_UNROLL 1
 #endif
 constexpr int kRowUnroll = SPAND_ROW_UNROLL;   // row loops of the DMMA block updates
+#ifndef SPAND_ROW_BATCH
+#define SPAND_ROW_BATCH 1
+#endif
+constexpr int kRowBatch = SPAND_ROW_BATCH;     // 8-row slabs loaded ahead per iteration
 #ifndef SPAND_BLK
 #define SPAND_BLK 32
 #endif
@@ -871,8 +875,14 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
   if (tid == 0) sh.nhot = sh.nhot3 = 0;
   int ph_cur = 7;
 #define PH(x) do { long long _n = clock64(); ph_t[ph_cur] += _n - ph_last; ph_last = _n; ph_cur = (x); } while (0)
+  // cold maintenance sub-phases: 0 T build, 1 Y, 2 reduce + Z, 3 X, 4 tails + replay, 5 reclassify, 6 maintenance barrier
+  long long cm_t[8] = {0, 0, 0, 0, 0, 0, 0, 0}, cm_last = 0, cm_calls = 0, cm_cols = 0;
+#define CM0() do { cm_last = clock64(); } while (0)
+#define CM(x) do { long long _n = clock64(); cm_t[(x)] += _n - cm_last; cm_last = _n; } while (0)
 #else
 #define PH(x) do {} while (0)
+#define CM0() do {} while (0)
+#define CM(x) do {} while (0)
 #endif
   // ---- hot / cold columns.  Only columns whose running norm^2 is within
   // kHotRho of the current pivot value are updated every step (HOT); the
@@ -898,6 +908,11 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
     double (*ZT)[33] = reinterpret_cast<double (*)[33]>(vsh + kCZ);
     double (*RK)[33] = reinterpret_cast<double (*)[33]>(vsh + kCR2);
     double* TAIL = vsh + kCTail;
+    CM0();
+#ifdef SPAND_RRQR_PHASES
+    ++cm_calls;
+    cm_cols += nc;
+#endif
     // per-warp partials (fixed-order reductions): [warp][16][32] for Y^T,
     // [warp][16] for the tails
     double (*RED)[16][32] = reinterpret_cast<double (*)[16][32]>(vsh + kCScr);
@@ -926,6 +941,7 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
       }
     }
     __syncthreads();
+    CM(0);
     // rows ka..m-1 split over the 8 warps (4-row aligned chunks): every warp
     // streams its own rows of the cold columns and of V through DMMA
     // fragments straight from L2 -- no block barriers inside the row loops
@@ -953,11 +969,16 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
           oka[mi] = c >= 0;
           xa[mi] = W + (int64_t)(c >= 0 ? c : 0) * m;
         }
+        // kRowBatch 8-row slabs per iteration, all their loads issued before
+        // the first DMMA (same accumulation order).  Measured on C4-L15:
+        // 1 slab 871 ms, 2 slabs 872 ms, 4 slabs 944 ms (spills) -- the loop is
+        // bound by the 8-sector fragment loads and the DMMA issue rate, not
+        // by the latency of one load round trip
         #pragma unroll kRowUnroll
-        for (int r = rb; r < re; r += 8) {
-          double af[2][2], bf[2][4];
+        for (int r = rb; r < re; r += 8 * kRowBatch) {
+          double af[2 * kRowBatch][2], bf[2 * kRowBatch][4];
 #pragma unroll
-          for (int s = 0; s < 2; ++s) {
+          for (int s = 0; s < 2 * kRowBatch; ++s) {
             const int i = r + 4 * s + l4;
             const bool okr = i < re;
 #pragma unroll
@@ -970,7 +991,7 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
             }
           }
 #pragma unroll
-          for (int s = 0; s < 2; ++s)
+          for (int s = 0; s < 2 * kRowBatch; ++s)
 #pragma unroll
             for (int mi = 0; mi < 2; ++mi)
 #pragma unroll
@@ -986,6 +1007,7 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
             for (int h = 0; h < 2; ++h) RED[warp][mi * 8 + l8][ni * 8 + 2 * l4 + h] = acc[mi][ni][h];
       }
       __syncthreads();
+      CM(1);
       for (int e = tid; e < 16 * 32; e += kT) {
         const int c = e >> 5, q = e & 31;
         double s = 0.0;
@@ -1012,6 +1034,7 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
         ZT[e >> 5][e & 31] = zv[u];
       }
       __syncthreads();
+      CM(2);
       // ---- X -= V Z: M = rows (8-row tiles of the warp's chunk), N = columns
       // (2 x 8), K = reflectors; rows ka..kb-1 captured, squares below summed
       {
@@ -1033,38 +1056,45 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
           }
         const int nkq = (nb + 3) >> 2;
         #pragma unroll kRowUnroll
-        for (int r0 = rb; r0 < re; r0 += 8) {
-          const int i = r0 + l8;   // this lane's A row and C row
-          double af[8];
+        for (int r0 = rb; r0 < re; r0 += 8 * kRowBatch) {
+          // kRowBatch 8-row slabs: every load first (see the Y loop)
+          double af[kRowBatch][8], xo[kRowBatch][2][2];
 #pragma unroll
-          for (int kq = 0; kq < 8; ++kq) {
-            const int q = kq * 4 + l4;
-            af[kq] = (kq < nkq && i < re && q < nb && i >= ka + q)
-                         ? __ldcg(V + (int64_t)(ka + q) * m + i)
-                         : 0.0;
-          }
-          double xo[2][2];
+          for (int u = 0; u < kRowBatch; ++u) {
+            const int i = r0 + 8 * u + l8;   // this lane's A row and C row
 #pragma unroll
-          for (int ni = 0; ni < 2; ++ni)
-#pragma unroll
-            for (int h = 0; h < 2; ++h)
-              xo[ni][h] = (i < re && okc[ni][h]) ? xc[ni][h][i] : 0.0;
-          double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
-#pragma unroll
-          for (int kq = 0; kq < 8; ++kq)
-#pragma unroll
-            for (int ni = 0; ni < 2; ++ni) dmma(acc[ni][0], acc[ni][1], af[kq], bz[kq][ni]);
-          if (i < re) {
+            for (int kq = 0; kq < 8; ++kq) {
+              const int q = kq * 4 + l4;
+              af[u][kq] = (kq < nkq && i < re && q < nb && i >= ka + q)
+                              ? __ldcg(V + (int64_t)(ka + q) * m + i)
+                              : 0.0;
+            }
 #pragma unroll
             for (int ni = 0; ni < 2; ++ni)
 #pragma unroll
-              for (int h = 0; h < 2; ++h) {
-                if (!okc[ni][h]) continue;
-                const double xv = xo[ni][h] - acc[ni][h];
-                xc[ni][h][i] = xv;
-                if (i < kb) RK[ni * 8 + 2 * l4 + h][i - ka] = xv;
-                else tail[ni][h] += xv * xv;
-              }
+              for (int h = 0; h < 2; ++h)
+                xo[u][ni][h] = (i < re && okc[ni][h]) ? xc[ni][h][i] : 0.0;
+          }
+#pragma unroll
+          for (int u = 0; u < kRowBatch; ++u) {
+            const int i = r0 + 8 * u + l8;
+            double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+#pragma unroll
+            for (int kq = 0; kq < 8; ++kq)
+#pragma unroll
+              for (int ni = 0; ni < 2; ++ni) dmma(acc[ni][0], acc[ni][1], af[u][kq], bz[kq][ni]);
+            if (i < re) {
+#pragma unroll
+              for (int ni = 0; ni < 2; ++ni)
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                  if (!okc[ni][h]) continue;
+                  const double xv = xo[u][ni][h] - acc[ni][h];
+                  xc[ni][h][i] = xv;
+                  if (i < kb) RK[ni * 8 + 2 * l4 + h][i - ka] = xv;
+                  else tail[ni][h] += xv * xv;
+                }
+            }
           }
         }
         // lanes sharing l4 hold the same columns: reduce over l8
@@ -1079,6 +1109,7 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
             tail[ni][h] = t;
           }
         __syncthreads();   // RED (aliased by RED2) fully consumed
+        CM(3);
         if (l8 == 0) {
 #pragma unroll
           for (int ni = 0; ni < 2; ++ni)
@@ -1119,6 +1150,7 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
         ref[c] = rf;
       }
       __syncthreads();
+      CM(4);
     }
   };
   // ---- blocked Q formation (large panels): Q = Q_0 Q_1 ... with
@@ -1250,10 +1282,10 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
             xa[mi] = Q + (int64_t)(c >= 0 ? c : 0) * m;
           }
           #pragma unroll kRowUnroll
-          for (int r = rb; r < re; r += 8) {
-            double af[2][2], bf[2][4];
+          for (int r = rb; r < re; r += 8 * kRowBatch) {
+            double af[2 * kRowBatch][2], bf[2 * kRowBatch][4];
 #pragma unroll
-            for (int s = 0; s < 2; ++s) {
+            for (int s = 0; s < 2 * kRowBatch; ++s) {
               const int i = r + 4 * s + l4;
               const bool okr = i < re;
 #pragma unroll
@@ -1266,7 +1298,7 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
               }
             }
 #pragma unroll
-            for (int s = 0; s < 2; ++s)
+            for (int s = 0; s < 2 * kRowBatch; ++s)
 #pragma unroll
               for (int mi = 0; mi < 2; ++mi)
 #pragma unroll
@@ -1323,27 +1355,39 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
             }
           const int nkq = (nb + 3) >> 2;
           #pragma unroll kRowUnroll
-          for (int r0 = rb; r0 < re; r0 += 8) {
-            const int i = r0 + l8;
-            double af[8];
+          for (int r0 = rb; r0 < re; r0 += 8 * kRowBatch) {
+            double af[kRowBatch][8], xo[kRowBatch][2][2];
 #pragma unroll
-            for (int kq = 0; kq < 8; ++kq) {
-              const int q = kq * 4 + l4;
-              af[kq] = (kq < nkq && i < re && q < nb && i >= ka + q)
-                           ? __ldcg(V + (int64_t)(ka + q) * m + i)
-                           : 0.0;
-            }
-            double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+            for (int u = 0; u < kRowBatch; ++u) {
+              const int i = r0 + 8 * u + l8;
 #pragma unroll
-            for (int kq = 0; kq < 8; ++kq)
-#pragma unroll
-              for (int ni = 0; ni < 2; ++ni) dmma(acc[ni][0], acc[ni][1], af[kq], bz[kq][ni]);
-            if (i < re) {
+              for (int kq = 0; kq < 8; ++kq) {
+                const int q = kq * 4 + l4;
+                af[u][kq] = (kq < nkq && i < re && q < nb && i >= ka + q)
+                                ? __ldcg(V + (int64_t)(ka + q) * m + i)
+                                : 0.0;
+              }
 #pragma unroll
               for (int ni = 0; ni < 2; ++ni)
 #pragma unroll
                 for (int h = 0; h < 2; ++h)
-                  if (okc[ni][h]) xc[ni][h][i] -= acc[ni][h];
+                  xo[u][ni][h] = (i < re && okc[ni][h]) ? xc[ni][h][i] : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < kRowBatch; ++u) {
+              const int i = r0 + 8 * u + l8;
+              double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+#pragma unroll
+              for (int kq = 0; kq < 8; ++kq)
+#pragma unroll
+                for (int ni = 0; ni < 2; ++ni) dmma(acc[ni][0], acc[ni][1], af[u][kq], bz[kq][ni]);
+              if (i < re) {
+#pragma unroll
+                for (int ni = 0; ni < 2; ++ni)
+#pragma unroll
+                  for (int h = 0; h < 2; ++h)
+                    if (okc[ni][h]) xc[ni][h][i] = xo[u][ni][h] - acc[ni][h];
+              }
             }
           }
         }
@@ -2321,6 +2365,7 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
       int32_t* hot_in = (k & 1) ? hotA : hotB;
       int32_t* tmpl = flist + 20 * ncap;
       cold_maint(k0, k);
+      CM0();
       const int nh = sh.nact, ncd = sh.ncold;
       __syncthreads();
       if (tid == 0) {
@@ -2388,7 +2433,9 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
       __syncthreads();
       publish(bv, bp, bc, cpar ^ 1);
       cpar ^= 1;
+      CM(5);
       group_barrier(ctr, G, gen, tgt, -2, events + 12 * slot + 9);
+      CM(6);
       PH(0);
     }
     // ---- winning column: max value, smallest current position (ties in
@@ -3028,6 +3075,10 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
     atomicAdd(reinterpret_cast<unsigned long long*>(events + 12 * slot + 11), (unsigned long long)nf);
   TL(twb);
 #ifdef SPAND_RRQR_PHASES
+  if (lane == 0 && warp == 0 && m >= SPAND_PHASE_MMIN && (rank == 0 || rank == G / 2))
+    printf("[rrqr maint] p %d m %d rank %d calls %lld cols %lld | kcycles: T %lld Y %lld Z %lld X %lld replay %lld reclass %lld barrier %lld\n",
+           p, m, rank, cm_calls, cm_cols, cm_t[0] / 1000, cm_t[1] / 1000, cm_t[2] / 1000, cm_t[3] / 1000,
+           cm_t[4] / 1000, cm_t[5] / 1000, cm_t[6] / 1000);
   if (lane == 0 && warp == 0 && m >= SPAND_PHASE_MMIN && (rank == 0 || rank == G / 2))
     printf("[rrqr phases] p %d m %d n %d G %d rank %d k %d nf %d act-steps %lld hot %lld hot3 %lld | kcycles: cand %lld maint %lld pivcol %lld refl %lld colpass %lld publish %lld barrier %lld | Q %lld restore %lld frozen-gemm %lld writeback %lld\n",
            p, m, n, G, rank, k_stop, nf, nact_sum, hot_sum, hot3_sum, ph_t[0] / 1000, ph_t[6] / 1000, ph_t[1] / 1000, ph_t[2] / 1000,

@@ -49,7 +49,7 @@ from collections.abc import Sequence
 LAUNCH_NAMES = {1: "spand_potrf_batched", 2: "spand_trtri_tiles", 3: "spand_gemm_grouped",
                 4: "spand_copy_batched", 5: "spand_rrqr_wave", 6: "spand_assemble_final",
                 7: "spand_nk_rescale", 8: "spand_nk_basis", 9: "spand_nk_deflate",
-                10: "spand_nk_qform", 11: "spand_digest_pieces"}
+                10: "spand_nk_qform", 11: "spand_digest_pieces", 12: "spand_gemm_kmask"}
 WAVE_LOG = None      # set to [] to record per-wave CUDA events (profiling)
 PROG_ARENA = None    # pinned staging of the program chunks (emission thread)
 NK_RTOL = 1e-8       # rank threshold of the near-kernel basis (oracle NK_RTOL)
@@ -351,8 +351,17 @@ class Engine:
             elif typ == 3:
                 alpha = float(np.int64(rec[8]).view(np.float64))
                 beta = float(np.int64(rec[9]).view(np.float64))
-                _lib.call("spand_gemm_grouped", cnt, P(ao), P(bo), P(co), gm0, goff,
-                          alpha, beta, x0, x1, x2, self._btab_p, int(rec[10]), st)
+                if int(rec[11]):
+                    # K-chunk masks (written by a type-12 record just before)
+                    _lib.call("spand_gemm_grouped_masked", cnt, P(ao), P(bo), P(co), gm0, goff,
+                              alpha, beta, x0, x1, x2, self._btab_p, int(rec[10]),
+                              ctypes.c_void_p(int(rec[11])), P(bo + int(rec[12])), st)
+                else:
+                    _lib.call("spand_gemm_grouped", cnt, P(ao), P(bo), P(co), gm0, goff,
+                              alpha, beta, x0, x1, x2, self._btab_p, int(rec[10]), st)
+            elif typ == 12:
+                _lib.call("spand_gemm_kmask", cnt, P(ao), P(bo), gm0, goff,
+                          ctypes.c_void_p(x0), P(co), st)
             elif typ == 4:
                 _lib.call("spand_copy_batched", cnt, P(ao), gm0, goff, st)
             elif typ == 5:

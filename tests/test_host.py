@@ -129,7 +129,7 @@ def test_scheduler_program_is_self_consistent(tag):
     plan.emit(1 << 40, 2 << 40, 3 << 40, 4 << 40, dry=False)
     prog, lau = plan.program()
     assert lau.shape[0] == plan.n_launch > 0
-    assert set(np.unique(lau[:, 0])) <= {1, 2, 3, 4, 5, 6}
+    assert set(np.unique(lau[:, 0])) <= {1, 2, 3, 4, 5, 6, 12}
     for rec in lau:
         for off in rec[2:5]:
             assert 0 <= off <= prog.size
