@@ -204,18 +204,26 @@ int spand_gemm_grouped(int ntile, const int64_t* tiles, const int64_t* targets,
  * that of spand_gemm_grouped).  Serves the interface rescale Z_i^-1 B
  * (factorize.py:165-173, schemes.py:235): before its first sparsification a
  * separator is coupled to a neighbour through a few of its rows only.
- * kmask = NULL: no masks. */
+ * With bT = 1 (the panel TRSM A_ws L_s^-T of eliminate_interior,
+ * factorize.py:131-149 / schemes.py:217) the bytes flag 16-row chunks of the
+ * A operand instead: a tile whose rows of A are all zero writes its zeros
+ * without loading anything.  With compact = 1 (the Schur update) kmoff has
+ * one entry per SEGMENT, {A panel's flag offset << 32 | B panel's}: a tile
+ * opens only the segments whose A rows (its i range) and B rows (its j
+ * range) both hold a nonzero, in their original order.  kmask = NULL: no
+ * masks. */
 int spand_gemm_grouped_masked(int ntile, const int64_t* tiles, const int64_t* targets,
                               const int64_t* segs, const int32_t* m0,
                               const int32_t* off, double alpha, double beta, int bT,
                               int lower_only, int tri, const int64_t* btab, int compact,
                               const unsigned char* kmask, const int64_t* kmoff,
                               void* stream);
-/* Writes the K-chunk masks of a masked launch: one CTA per target, B = the B
- * operand of the target's first segment (14-int64 segment rows). */
+/* Writes the row-chunk masks of a masked launch: the A (which = 0) or B
+ * (which = 1) operand of every target's first segment (14-int64 segment
+ * rows), one byte per 16 rows. */
 int spand_gemm_kmask(int ntarget, const int64_t* targets, const int64_t* segs,
                      const int32_t* m0, const int32_t* off, unsigned char* kmask,
-                     const int64_t* kmoff, void* stream);
+                     const int64_t* kmoff, int which, void* stream);
 
 /* One wave of the batched early-stopping column-pivoted Householder QR of
  * interface panels (restates dense.py:117-222, schemes.py:272-318,

@@ -50,7 +50,7 @@ SIGNATURES = {
                            _c_int, _c_int, _P, _c_int, _P],
     "spand_gemm_grouped_masked": [_c_int, _P, _P, _P, _P, _P, _c_dbl, _c_dbl, _c_int,
                                   _c_int, _c_int, _P, _c_int, _P, _P, _P],
-    "spand_gemm_kmask": [_c_int, _P, _P, _P, _P, _P, _P, _P],
+    "spand_gemm_kmask": [_c_int, _P, _P, _P, _P, _P, _P, _c_int, _P],
     "spand_rrqr_wave": [_c_int, _c_int, _c_int, _P, _P, _P, _P, _c_dbl, _c_int, _P, _P],
     "spand_rrqr_cta_count": [],
     "spand_rrqr_capacity": [_c_int],

@@ -107,13 +107,73 @@ gemm_grouped_kernel(const int64_t* __restrict__ tiles, const int64_t* __restrict
   // rows 16 c .. 16 c + 15 of B hold a nonzero (kmask_kernel below).  Chunks
   // of zero rows are not even loaded: an unscaled interface block couples a
   // separator to a neighbour through a few of its rows only.
-  const unsigned char* mk = kmask ? kmask + kmoff[t] : nullptr;
+  const unsigned char* mk = (kmask && !compact) ? kmask + kmoff[t] : nullptr;
+  // bT = 1 (panel TRSM C = A L^-T, A = the panel (w, s) of an eliminated
+  // interior): the bytes flag 16-row chunks of A instead.  A tile whose rows
+  // of A are all zero has nothing to load: it writes its zeros and leaves
+  // (on the leaf levels most 64-row tiles of a panel are such).
+  bool a_rows_zero = false;
+  if (mk && bT) {
+    const int c1 = ((i0 + BM < C.rows ? i0 + BM : C.rows) + 15) >> 4;
+    bool any = false;
+    for (int c = i0 >> 4; c < c1; ++c) any |= mk[c] != 0;
+    a_rows_zero = !any;
+    mk = nullptr;
+  }
   auto next_k = [&](int k, int kend) {
     if (mk)
       while (k < kend && !mk[k >> 4]) k += BK;
     return k;
   };
-  int seg = sb, k0 = 0;
+  // Compact (Schur) segments with flags: kmoff[s] = {A panel's flag offset <<
+  // 32 | B panel's} into the row-chunk flags of the level's panels.  A tile of
+  // a separator block is touched by few of the interiors whose segments its
+  // target lists (root x root: ~2000 segments, a few dozen per tile), so the
+  // segments are tested 128 at a time, one per thread, and only those whose A
+  // rows (the tile's i range) and B rows (its j range) both hold a nonzero
+  // are opened, in their original order (same sums, bit for bit).
+  const bool seglist = compact && kmask != nullptr;
+  __shared__ int slist[kThreads];
+  __shared__ int wcnt[kThreads / 32];
+  int sbase = sb, scount = 0, spos = 0;
+  const int ca0 = i0 >> 4, ca1 = ((i0 + BM < C.rows ? i0 + BM : C.rows) + 15) >> 4;
+  const int cb0 = j0 >> 4, cb1 = ((j0 + BN < C.cols ? j0 + BN : C.cols) + 15) >> 4;
+  auto seg_pass = [&](int s) {
+    const int64_t fo = kmoff[s];
+    const unsigned char* fa = kmask + (fo >> 32);
+    const unsigned char* fb = kmask + (fo & 0xffffffffLL);
+    bool a = false, b = false;
+    for (int c = ca0; c < ca1; ++c) a |= fa[c] != 0;
+    if (!a) return false;
+    for (int c = cb0; c < cb1; ++c) b |= fb[c] != 0;
+    return b;
+  };
+  // the segment after `cur` (block-uniform calls only: the list refill
+  // synchronises the CTA)
+  auto following = [&](int cur) -> int {
+    if (!seglist) return cur + 1;
+    while (true) {
+      if (spos < scount) return slist[spos++];
+      if (sbase >= se) return se;
+      const int s = sbase + tid;
+      const bool pass = s < se && seg_pass(s);
+      const unsigned bal = __ballot_sync(0xffffffffu, pass);
+      if (lane == 0) wcnt[warp] = __popc(bal);
+      __syncthreads();
+      int before = 0, total = 0;
+#pragma unroll
+      for (int w = 0; w < kThreads / 32; ++w) {
+        if (w < warp) before += wcnt[w];
+        total += wcnt[w];
+      }
+      if (pass) slist[before + __popc(bal & ((1u << lane) - 1u))] = s;
+      __syncthreads();
+      sbase += kThreads;
+      scount = total;
+      spos = 0;
+    }
+  };
+  int seg = seglist ? following(sb) : sb, k0 = 0;
   Opnd A, B;
   int K = 0;
   auto open_seg = [&](int s) {
@@ -121,11 +181,12 @@ gemm_grouped_kernel(const int64_t* __restrict__ tiles, const int64_t* __restrict
     krange(A, B, k0, K);
     k0 = next_k(k0, K);
   };
+  if (a_rows_zero) seg = se;
   // skip empty segments
   while (seg < se) {
     open_seg(seg);
     if (K > k0) break;
-    ++seg;
+    seg = following(seg);
   }
   auto load_stage = [&](int st, const Opnd& a, const Opnd& b, int kbase, int kmax) {
 #pragma unroll
@@ -168,13 +229,13 @@ gemm_grouped_kernel(const int64_t* __restrict__ tiles, const int64_t* __restrict
       int Kn = K, segn = seg, kn = next_k(k0 + BK, K);
       bool have_next = true;
       if (kn >= Kn) {
-        ++segn;
+        segn = following(segn);
         while (segn < se) {
           seg_opnds(segn, An, Bn);
           krange(An, Bn, kn, Kn);
           kn = next_k(kn, Kn);
           if (Kn > kn) break;
-          ++segn;
+          segn = following(segn);
         }
         have_next = segn < se;
       }
@@ -265,9 +326,9 @@ gemm_grouped_kernel(const int64_t* __restrict__ tiles, const int64_t* __restrict
     }
   }
 }
-// K-chunk masks of a masked GEMM launch: B = the B operand of the target's
-// first segment (14-int64 segment rows); kmask[kmoff[t] + c] = any nonzero
-// in rows 16 c .. 16 c + 15 of B.  Work unit = (target, 128-row slab): one
+// Row-chunk masks of a masked GEMM launch: B = the A (which = 0) or B
+// (which = 1) operand of the target's first segment (14-int64 segment
+// rows); kmask[kmoff[t] + c] = any nonzero in rows 16 c .. 16 c + 15 of it.  Work unit = (target, 128-row slab): one
 // row per thread (coalesced column reads, 8 independent loads in flight), a
 // chunk is 16 consecutive lanes.  Slabs of a target are dealt over
 // gridDim.y CTAs (the blocks between two top separators have ~10^7 entries).
@@ -275,10 +336,10 @@ constexpr int kMaskY = 8;
 __global__ void __launch_bounds__(kThreads)
 kmask_kernel(const int64_t* __restrict__ targets, const int64_t* __restrict__ segs,
              const int32_t* __restrict__ m0, const int32_t* __restrict__ off,
-             unsigned char* __restrict__ kmask, const int64_t* __restrict__ kmoff) {
+             unsigned char* __restrict__ kmask, const int64_t* __restrict__ kmoff, int which) {
   const int64_t t = blockIdx.x;
   const int64_t s = targets[8 * t + 7];
-  const Opnd B = load_opnd(segs + 14 * s + 7, m0, off);
+  const Opnd B = load_opnd(segs + 14 * s + (which ? 7 : 0), m0, off);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nch = (B.rows + 15) >> 4;
   unsigned char* out = kmask + kmoff[t];
@@ -309,11 +370,11 @@ kmask_kernel(const int64_t* __restrict__ targets, const int64_t* __restrict__ se
 
 extern "C" int spand_gemm_kmask(int ntarget, const int64_t* targets, const int64_t* segs,
                                 const int32_t* m0, const int32_t* off, unsigned char* kmask,
-                                const int64_t* kmoff, void* stream) {
+                                const int64_t* kmoff, int which, void* stream) {
   if (ntarget < 0) return -1;
   if (ntarget == 0) return 0;
   kmask_kernel<<<dim3(ntarget, kMaskY), kThreads, 0, as_stream(stream)>>>(targets, segs, m0, off,
-                                                                          kmask, kmoff);
+                                                                          kmask, kmoff, which);
   SPAND_CHECK_LAUNCH();
   return 0;
 }
@@ -333,8 +394,10 @@ extern "C" int spand_gemm_grouped_masked(int ntile, const int64_t* tiles, const 
                                   const unsigned char* kmask, const int64_t* kmoff,
                                   void* stream) {
   if (ntile < 0) return -1;
-  // masks describe 16-row chunks of B: C = A B with 14-int64 segment rows
-  if (kmask && (bT || compact || !kmoff)) return -1;
+  // masks describe 16-row chunks of B (bT = 0: K chunks) or of A (bT = 1: a
+  // tile's own rows), with 14-int64 segment rows
+  // (compact = 1: per-segment flag offsets of the A and B panels)
+  if (kmask && !kmoff) return -1;
   if (ntile == 0) return 0;
   const int shape = (tri >> 4) & 7;
   tri &= 7;

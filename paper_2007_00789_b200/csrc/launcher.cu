@@ -70,7 +70,7 @@ int spand_run_launches(int nl, const int64_t* recs, int64_t base, int32_t* m0, i
       }
       case 12:
         st = spand_gemm_kmask(cnt, P(ao), P(bo), m0, off, reinterpret_cast<unsigned char*>(x0),
-                              P(co), stream);
+                              P(co), (int)x1, stream);
         break;
       case 4:
         st = spand_copy_batched(cnt, P(ao), m0, off, stream);

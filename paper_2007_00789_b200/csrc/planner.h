@@ -385,12 +385,16 @@ struct Plan {
     // program can be emitted in one pass after a single allocation
     int64_t need = fcap * fcap;
     for (auto& L : lv) {
-      int64_t trsm = 0, tri = 0;
+      int64_t trsm = 0, tri = 0, pflag_bytes = 0;
       for (size_t k = 0; k < L.interiors.size(); ++k) {
         const int s = L.interiors[k];
         tri += m0[s] * m0[s];
-        for (int w : L.inbrs[k]) trsm += m0[w] * m0[s];
+        for (int w : L.inbrs[k]) {
+          trsm += m0[w] * m0[s];
+          pflag_bytes += (m0[w] + 15) / 16;   // row-chunk flags behind the products
+        }
       }
+      trsm += (pflag_bytes + 7) / 8 + 1;
       need = std::max({need, trsm, tri});
       if (L.skipped) continue;
       int64_t resc = 0, tri2 = 0, kmask_bytes = 0;
@@ -468,6 +472,7 @@ struct Plan {
     for (int64_t x : e) v.push_back(x);
   }
   bool dry = false;   // sizing pass: compute temp_size only, emit nothing
+  std::vector<int64_t> blkflag;   // block -> row-chunk flag offset (panels of the level being emitted)
   int64_t push(const std::vector<int64_t>& rows) {
     if (dry) return 0;
     const int64_t at = (int64_t)prog.size();
@@ -522,7 +527,7 @@ struct Plan {
   void emit_gemm(std::vector<int64_t> (&tiles)[kNShape], std::vector<int64_t>& trow,
                  std::vector<int64_t>& srow, double alpha, double beta, int bT, int lower,
                  int tri, int compact, int64_t mask_addr = 0,
-                 const std::vector<int64_t>* kmoff = nullptr) {
+                 const std::vector<int64_t>* kmoff = nullptr, bool mask_pass = true) {
     int64_t b = -1, c = -1, ko = 0;
     for (int s = 0; s < kNShape; ++s) {
       if (tiles[s].empty()) continue;
@@ -532,7 +537,9 @@ struct Plan {
         c = push(srow);
         if (mask_addr) {
           ko = push(*kmoff);
-          launch(12, (int64_t)kmoff->size(), b, c, ko, mask_addr);
+          // which operand the bytes describe: B's K chunks (C = A B) or A's rows
+          // (mask_pass = false: the flags were written by an earlier launch)
+          if (mask_pass) launch(12, (int64_t)kmoff->size(), b, c, ko, mask_addr, bT ? 0 : 1);
         }
       }
       const int64_t a = push(tiles[s]);
@@ -581,11 +588,14 @@ struct Plan {
       ++nseg;
     }
   };
-  void gemm_flat(FlatGemm& g, double alpha, double beta, int bT, int tri = 0) {
+  void gemm_flat(FlatGemm& g, double alpha, double beta, int bT, int tri = 0,
+                 int64_t mask_addr = 0, const std::vector<int64_t>* kmoff = nullptr,
+                 bool mask_pass = true) {
     if (g.ntarget == 0) return;
     g.trow.insert(g.trow.end(), {0, 0, 0, 0, 0, 0, 0, g.nseg});
     if (dry) return;
-    emit_gemm(g.tiles, g.trow, g.srow, alpha, beta, bT, g.lower ? 1 : 0, tri, g.sw == 1 ? 1 : 0);
+    emit_gemm(g.tiles, g.trow, g.srow, alpha, beta, bT, g.lower ? 1 : 0, tri, g.sw == 1 ? 1 : 0,
+              mask_addr, kmoff, mask_pass);
   }
 
   // batched triangular inverses: 64-tiles + recursive doubling GEMMs
@@ -808,8 +818,8 @@ struct Plan {
         trtri(Ls, Xs, sz, 0);
         // panel TRSM as a product with the explicit inverse, into temp, copied back
         FlatGemm tg;
-        std::vector<int64_t> cps;
-        int64_t acc = 0;
+        std::vector<int64_t> cps, pflag;   // pflag: row-chunk flag offset of every panel
+        int64_t acc = 0, flag_bytes = 0;
         tg.reserve(L.inb_blk.size(), L.inb_blk.size());
         cps.reserve(15 * L.inb_blk.size());
         for (size_t k = 0; k < L.interiors.size(); ++k) {
@@ -828,30 +838,49 @@ struct Plan {
             const int64_t oa[7] = {pws, w, s, 0, 0, -1, -1};
             const int64_t ob[7] = {linv_s, s, s, 0, 0, -1, -1};
             tg.seg_opnds(oa, ob);
+            pflag.push_back(flag_bytes);
+            {
+              const int blk = L.inb_blk[L.inb_ptr[k] + u];
+              if ((int)blkflag.size() <= blk) blkflag.resize(bi.size() + 1024, 0);
+              blkflag[blk] = flag_bytes;
+            }
+            flag_bytes += (m0[w] + 15) / 16;
             if (inplace) continue;
             cps.insert(cps.end(), {tmp, w, s, 0, 0, -1, -1, pws, w, s, 0, 0, -1, -1, 0});
             acc += m0[w] * m0[s];
           }
         }
-        temp_size = std::max(temp_size, acc);
-        gemm_flat(tg, 1.0, 0.0, 1, 2);    // panel L_s^-T
+        // row-chunk flags of the panels behind the products' temp: an
+        // interior touches a few dofs of each separator, so most 64-row tiles
+        // of a panel hold only zeros and are skipped (gemm.cu)
+        const int64_t flag_addr = temp_base + 8 * acc;
+        temp_size = std::max(temp_size, acc + (flag_bytes + 7) / 8 + 1);
+        gemm_flat(tg, 1.0, 0.0, 1, 2, flag_addr, &pflag);    // panel L_s^-T
         if (!cps.empty()) launch(4, (int64_t)cps.size() / 15, push(cps));
         // grouped Schur / fill update: off-diagonal targets, then diagonal
         // ones (lower tiles only: potrf reads the lower triangle)
         for (int diag = 0; diag < 2; ++diag) {
           FlatGemm st;
+          std::vector<int64_t> sflag;   // per segment: {A panel flags << 32 | B panel flags}
           st.sw = 1;
           st.lower = diag == 1;
           st.reserve(L.targets.size(), L.tseg_idx.size());
+          sflag.reserve(L.tseg_idx.size());
           for (size_t t = 0; t < L.targets.size(); ++t) {
             const int b = L.targets[t];
             const int wa = bi[b], wb = bj[b];
             if ((wa == wb) != (diag == 1)) continue;
             st.target(m0[wa], m0[wb], dry, pool_base + 8 * boff[b], (int64_t)wa, (int64_t)wb,
                       (int64_t)0, (int64_t)0, (int64_t)-1, (int64_t)-1);
-            for (int q = L.tseg_ptr[t]; q < L.tseg_ptr[t + 1]; ++q) st.seg(L.tseg_blk[q]);
+            for (int q = L.tseg_ptr[t]; q < L.tseg_ptr[t + 1]; ++q) {
+              st.seg(L.tseg_blk[q]);
+              sflag.push_back((blkflag[L.tseg_blk[q] >> 32] << 32) |
+                              blkflag[L.tseg_blk[q] & 0xffffffffLL]);
+            }
           }
-          gemm_flat(st, -1.0, 1.0, 1);
+          // the panels' row-chunk flags (written before the panel TRSM) pick
+          // the segments each tile opens
+          gemm_flat(st, -1.0, 1.0, 1, 0, flag_addr, &sflag, false);
         }
       }
       if (L.skipped) return;

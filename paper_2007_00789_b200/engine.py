@@ -361,7 +361,7 @@ class Engine:
                               alpha, beta, x0, x1, x2, self._btab_p, int(rec[10]), st)
             elif typ == 12:
                 _lib.call("spand_gemm_kmask", cnt, P(ao), P(bo), gm0, goff,
-                          ctypes.c_void_p(x0), P(co), st)
+                          ctypes.c_void_p(x0), P(co), x1, st)
             elif typ == 4:
                 _lib.call("spand_copy_batched", cnt, P(ao), gm0, goff, st)
             elif typ == 5:
