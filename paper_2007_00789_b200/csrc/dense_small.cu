@@ -16,8 +16,10 @@ __global__ void __launch_bounds__(kT)
 potrf_kernel(const int64_t* __restrict__ ops, const int32_t* __restrict__ m0,
              const int32_t* __restrict__ off, int32_t* __restrict__ info, int piv_off,
              int first_only) {
-  __shared__ double Bk[NB][65];     // rows jb..jb+NB of columns kb..kb+64
-  __shared__ double D[NB][NB + 1];  // diagonal tile
+  // one buffer: the general path's Bk / D tiles, or a whole block of <= 64
+  __shared__ double raw[64 * 65];
+  double (*Bk)[65] = reinterpret_cast<double (*)[65]>(raw);                // [NB][65]: rows jb..jb+NB of columns kb..kb+64
+  double (*D)[NB + 1] = reinterpret_cast<double (*)[NB + 1]>(raw + NB * 65);  // [NB][NB + 1]: diagonal tile
   __shared__ int bad;
   const int64_t* row = ops + 8 * (int64_t)blockIdx.x;
   const Opnd A = load_opnd(row, m0, off);
@@ -26,6 +28,52 @@ potrf_kernel(const int64_t* __restrict__ ops, const int32_t* __restrict__ m0,
   double* a = A.p;
   if (threadIdx.x == 0) bad = 0;
   __syncthreads();
+  if (n <= 64) {
+    // Blocks of <= 64 (leaf interiors, the diagonal steps of the blocked
+    // factorization): the lower triangle is staged in shared memory and
+    // factored right-looking by the whole CTA -- per column: sqrt, scale,
+    // rank-1 update of the trailing triangle (element (i, c) accumulates its
+    // updates in column order).  One coalesced read and one write of the
+    // block instead of the left-looking passes over global memory.
+    double (*S)[65] = reinterpret_cast<double (*)[65]>(raw);
+    for (int e = threadIdx.x; e < n * n; e += kT) {
+      const int r = e % n, c = e / n;
+      S[r][c] = (c <= r) ? a[r + (int64_t)c * ld] : 0.0;
+    }
+    __syncthreads();
+    for (int j = 0; j < n; ++j) {
+      const double d = S[j][j];
+      if (!(d > 0.0)) {  // also catches NaN (uniform: every thread reads the same d)
+        if (threadIdx.x == 0) bad = j + 1;
+        break;
+      }
+      const double rd = sqrt(d);
+      __syncthreads();
+      if (threadIdx.x == 0) S[j][j] = rd;
+      for (int i = j + 1 + threadIdx.x; i < n; i += kT) S[i][j] /= rd;
+      __syncthreads();
+      // trailing lower triangle: rows i > j, columns j < c <= i
+      const int tl = n - j - 1;
+      for (int e = threadIdx.x; e < tl * tl; e += kT) {
+        const int i = j + 1 + e % tl, c = j + 1 + e / tl;
+        if (c <= i) S[i][c] -= S[i][j] * S[c][j];
+      }
+      __syncthreads();
+    }
+    __syncthreads();
+    if (!bad) {
+      for (int e = threadIdx.x; e < n * n; e += kT) {
+        const int r = e % n, c = e / n;
+        a[r + (int64_t)c * ld] = S[r][c];   // zeros above the diagonal (dense.py:53)
+      }
+    }
+    if (threadIdx.x == 0) {
+      int32_t* slot = info + row[7];
+      if (!first_only) *slot = bad ? bad + piv_off : 0;
+      else if (bad && *slot == 0) *slot = bad + piv_off;
+    }
+    return;
+  }
   for (int jb = 0; jb < n; jb += NB) {
     const int nbk = min(NB, n - jb);
     // ---- panel update A[jb:, jb:jb+nbk] -= A[jb:, :jb] * A[jb:jb+nbk, :jb]^T
@@ -357,14 +405,22 @@ trtri_tile_kernel(const int64_t* __restrict__ ops, const int32_t* __restrict__ m
     Xs[r][c] = 0.0;
   }
   __syncthreads();
-  // column j of X solves L x = e_j; one thread per column, forward order
-  if (threadIdx.x < n) {
-    const int j = threadIdx.x;
-    Xs[j][j] = 1.0 / Ls[j][j];
-    for (int i = j + 1; i < n; ++i) {
-      double s = 0.0;
-      for (int k = j; k < i; ++k) s += Ls[i][k] * Xs[k][j];
-      Xs[i][j] = -s / Ls[i][i];
+  // column j of X solves L x = e_j by forward substitution; four lanes per
+  // column split each row's dot product (terms k = j + p, j + p + 4, ...) and
+  // add their partials in a fixed order.  The row loop is warp-uniform (a
+  // warp holds 8 columns): rows above a column's diagonal are predicated off.
+  {
+    const int j = threadIdx.x >> 2, p = threadIdx.x & 3;
+    if (p == 0 && j < n) Xs[j][j] = 1.0 / Ls[j][j];
+    __syncwarp();
+    for (int i = 1; i < n; ++i) {
+      double sum = 0.0;
+      if (j < i)
+        for (int k = j + p; k < i; k += 4) sum += Ls[i][k] * Xs[k][j];
+      const double s1 = sum + __shfl_xor_sync(0xffffffffu, sum, 1);
+      const double s2 = s1 + __shfl_xor_sync(0xffffffffu, s1, 2);
+      if (p == 0 && j < i) Xs[i][j] = -s2 / Ls[i][i];
+      __syncwarp();
     }
   }
   __syncthreads();
