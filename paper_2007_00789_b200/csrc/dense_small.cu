@@ -236,7 +236,11 @@ int spand_copy_batched(int ntask, const int64_t* ops, const int32_t* m0, const i
                        void* stream) {
   if (ntask < 0) return -1;
   if (ntask == 0) return 0;
-  dim3 grid(ntask, 16);
+  // few tasks = the large blocks of the top levels (up to 3104^2 entries):
+  // enough CTAs per task to fill the device (16 each left a 77 MB copy on 16 SMs)
+  int gy = 16;
+  if (ntask < 74) gy = (1184 + ntask - 1) / ntask;
+  dim3 grid(ntask, gy);
   copy_kernel<<<grid, kT, 0, as_stream(stream)>>>(ops, m0, off);
   SPAND_CHECK_LAUNCH();
   return 0;
