@@ -433,8 +433,9 @@ def main():
                 "critical_steps": steps, "step_floor_us": step_us, "floor_ms": floor_ms,
                 "frac": floor_ms / roof["ms_per_step"],
                 "basis": "critical path = sum over waves of the largest k_stop; each step "
-                         "needs one 296-CTA group barrier + candidate scan + pivot-column "
-                         "read (profiles/rrqr_step_probe_r01.jsonl)"}
+                         "needs one group barrier + candidate scan + pivot-column read "
+                         "(profiles/rrqr_step_probe_r01.jsonl: probed with 296 CTAs; the "
+                         "waves now run 148, one per SM)"}
         except Exception:
             pass
     prof_path = next((q for q in (os.path.join(HERE, "profiles", f"ncu_r0{k}_summary.json")

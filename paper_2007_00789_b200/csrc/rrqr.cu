@@ -60,8 +60,17 @@ constexpr size_t kMinSmem = (size_t)4 * 16 * kLDS * sizeof(double);   // 2 stage
 // scratch (2 stages x kPBK rows of the A (64) and V (32) operands, and the
 // 64 x 65 update tile) | T [32][33] | Y/Z [64][33] | R rows [64][33] | tails [64]
 constexpr int kPBK = 32;         // rows per stage of the cold-column product
-constexpr int kCScr = 0, kCT = 2 * kPBK * (kLDS + 36), kCZ = kCT + 32 * 33, kCR2 = kCZ + 64 * 33,
-              kCTail = kCR2 + 64 * 33, kColdEnd = kCTail + 64;
+// columns per sweep of the blocked reflector updates (cold maintenance, Q
+// formation): kMT DMMA m-tiles of 8.  The reflector block V_b is streamed once
+// per sweep, so wider sweeps halve its traffic for CTAs with > 16 columns.
+#ifndef SPAND_COLD_MT
+#define SPAND_COLD_MT 2
+#endif
+constexpr int kMT = SPAND_COLD_MT, kSweep = 8 * kMT;
+static_assert(kMT == 2 || kMT == 4, "sweep width 16 or 32 columns");
+constexpr int kScr0 = 2 * kPBK * (kLDS + 36), kScr1 = 8 * kSweep * 32;   // stages | per-warp partials
+constexpr int kCScr = 0, kCT = kScr0 > kScr1 ? kScr0 : kScr1, kCZ = kCT + 32 * 33,
+              kCR2 = kCZ + 64 * 33, kCTail = kCR2 + 64 * 33, kColdEnd = kCTail + 64;
 constexpr size_t kColdSmem = (size_t)kColdEnd * sizeof(double);
 #ifndef SPAND_ROW_UNROLL
 #define SPAND_ROW_UNROLL 1
@@ -112,7 +121,8 @@ constexpr int kXB = 1056, kXS = 512, kHC = 512;
 // [2][V, X][32][33] | Z, T [32][33] | hot state: cur, ref [kHC] + 4 int [kHC]
 constexpr int kClEnd = 3 * kXB + kXS + 4 * 32 * 33 + 2 * 32 * 33 + 2 * kHC + 2 * kHC;
 constexpr size_t kClSmem = (size_t)kClEnd * sizeof(double);
-static_assert(kClSmem >= kColdSmem, "clustered layout covers the post-loop phases");
+static_assert((kClSmem > kFrozenSmem ? kClSmem : kFrozenSmem) >= kColdSmem,
+              "clustered launches cover the post-loop phases");
 // the clustered kernel shares the post-loop phases, so its launches must also
 // cover the frozen-column GEMM's staging buffers
 constexpr size_t kClLaunchSmem = kClSmem > kFrozenSmem ? kClSmem : kFrozenSmem;
@@ -915,8 +925,8 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
 #endif
     // per-warp partials (fixed-order reductions): [warp][16][32] for Y^T,
     // [warp][16] for the tails
-    double (*RED)[16][32] = reinterpret_cast<double (*)[16][32]>(vsh + kCScr);
-    double (*RED2)[16] = reinterpret_cast<double (*)[16]>(vsh + kCScr);
+    double (*RED)[kSweep][32] = reinterpret_cast<double (*)[kSweep][32]>(vsh + kCScr);
+    double (*RED2)[kSweep] = reinterpret_cast<double (*)[kSweep]>(vsh + kCScr);
     // T of Q_b = H_ka ... H_{kb-1} = I - V T V^T (dlarft, forward columnwise)
     // from the Gram columns gathered during the block's steps
     __syncthreads();
@@ -949,22 +959,22 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
     const int chunk = ((L + 4 * kWarps - 1) / (4 * kWarps)) * 4;
     const int rb = ka + warp * chunk, re = min(m, rb + chunk);
     const int l4 = lane & 3, l8 = lane >> 2;
-    for (int ct = 0; ct < nc; ct += 16) {
-      const int ncl = min(16, nc - ct);
-      if (tid < 16) sh.fcol[tid] = tid < ncl ? coldl[rank + G * (ct + tid)] : -1;
+    for (int ct = 0; ct < nc; ct += kSweep) {
+      const int ncl = min(kSweep, nc - ct);
+      if (tid < kSweep) sh.fcol[tid] = tid < ncl ? coldl[rank + G * (ct + tid)] : -1;
       __syncthreads();
       // ---- Y^T[c][q] = sum_{i >= ka} X_c[i] V[i, ka + q]: M = columns (2 x 8),
       // N = reflectors (4 x 8), K = rows
       {
-        double acc[2][4][2];
+        double acc[kMT][4][2];
 #pragma unroll
-        for (int a = 0; a < 2; ++a)
+        for (int a = 0; a < kMT; ++a)
 #pragma unroll
           for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
-        const double* xa[2];
-        bool oka[2];
+        const double* xa[kMT];
+        bool oka[kMT];
 #pragma unroll
-        for (int mi = 0; mi < 2; ++mi) {
+        for (int mi = 0; mi < kMT; ++mi) {
           const int c = sh.fcol[mi * 8 + l8];
           oka[mi] = c >= 0;
           xa[mi] = W + (int64_t)(c >= 0 ? c : 0) * m;
@@ -976,13 +986,13 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
         // by the latency of one load round trip
         #pragma unroll kRowUnroll
         for (int r = rb; r < re; r += 8 * kRowBatch) {
-          double af[2 * kRowBatch][2], bf[2 * kRowBatch][4];
+          double af[2 * kRowBatch][kMT], bf[2 * kRowBatch][4];
 #pragma unroll
           for (int s = 0; s < 2 * kRowBatch; ++s) {
             const int i = r + 4 * s + l4;
             const bool okr = i < re;
 #pragma unroll
-            for (int mi = 0; mi < 2; ++mi) af[s][mi] = (okr && oka[mi]) ? __ldcg(xa[mi] + i) : 0.0;
+            for (int mi = 0; mi < kMT; ++mi) af[s][mi] = (okr && oka[mi]) ? __ldcg(xa[mi] + i) : 0.0;
 #pragma unroll
             for (int ni = 0; ni < 4; ++ni) {
               const int q = ni * 8 + l8;
@@ -993,14 +1003,14 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
 #pragma unroll
           for (int s = 0; s < 2 * kRowBatch; ++s)
 #pragma unroll
-            for (int mi = 0; mi < 2; ++mi)
+            for (int mi = 0; mi < kMT; ++mi)
 #pragma unroll
               for (int ni = 0; ni < 4; ++ni)
                 dmma(acc[mi][ni][0], acc[mi][ni][1], af[s][mi], bf[s][ni]);
         }
         // C[row = column l8 (+8 mi)][col = reflector 2 l4 + h (+8 ni)]
 #pragma unroll
-        for (int mi = 0; mi < 2; ++mi)
+        for (int mi = 0; mi < kMT; ++mi)
 #pragma unroll
           for (int ni = 0; ni < 4; ++ni)
 #pragma unroll
@@ -1008,7 +1018,7 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
       }
       __syncthreads();
       CM(1);
-      for (int e = tid; e < 16 * 32; e += kT) {
+      for (int e = tid; e < kSweep * 32; e += kT) {
         const int c = e >> 5, q = e & 31;
         double s = 0.0;
 #pragma unroll
@@ -1017,9 +1027,9 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
       }
       __syncthreads();
       // ---- Z^T = Y^T T
-      double zv[2];
+      double zv[kMT];
 #pragma unroll
-      for (int u = 0; u < 2; ++u) {
+      for (int u = 0; u < kMT; ++u) {
         const int e = tid + kT * u;
         const int c = e >> 5, q = e & 31;
         double z = 0.0;
@@ -1029,7 +1039,7 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
       }
       __syncthreads();
 #pragma unroll
-      for (int u = 0; u < 2; ++u) {
+      for (int u = 0; u < kMT; ++u) {
         const int e = tid + kT * u;
         ZT[e >> 5][e & 31] = zv[u];
       }
@@ -1038,16 +1048,16 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
       // ---- X -= V Z: M = rows (8-row tiles of the warp's chunk), N = columns
       // (2 x 8), K = reflectors; rows ka..kb-1 captured, squares below summed
       {
-        double tail[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
-        double bz[8][2];
+        double tail[kMT][2] = {};
+        double bz[8][kMT];
 #pragma unroll
         for (int kq = 0; kq < 8; ++kq)
 #pragma unroll
-          for (int ni = 0; ni < 2; ++ni) bz[kq][ni] = ZT[ni * 8 + l8][kq * 4 + l4];
-        double* xc[2][2];
-        bool okc[2][2];
+          for (int ni = 0; ni < kMT; ++ni) bz[kq][ni] = ZT[ni * 8 + l8][kq * 4 + l4];
+        double* xc[kMT][2];
+        bool okc[kMT][2];
 #pragma unroll
-        for (int ni = 0; ni < 2; ++ni)
+        for (int ni = 0; ni < kMT; ++ni)
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
             const int c = sh.fcol[ni * 8 + 2 * l4 + h];
@@ -1058,7 +1068,7 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
         #pragma unroll kRowUnroll
         for (int r0 = rb; r0 < re; r0 += 8 * kRowBatch) {
           // kRowBatch 8-row slabs: every load first (see the Y loop)
-          double af[kRowBatch][8], xo[kRowBatch][2][2];
+          double af[kRowBatch][8], xo[kRowBatch][kMT][2];
 #pragma unroll
           for (int u = 0; u < kRowBatch; ++u) {
             const int i = r0 + 8 * u + l8;   // this lane's A row and C row
@@ -1070,7 +1080,7 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
                               : 0.0;
             }
 #pragma unroll
-            for (int ni = 0; ni < 2; ++ni)
+            for (int ni = 0; ni < kMT; ++ni)
 #pragma unroll
               for (int h = 0; h < 2; ++h)
                 xo[u][ni][h] = (i < re && okc[ni][h]) ? xc[ni][h][i] : 0.0;
@@ -1078,14 +1088,14 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
 #pragma unroll
           for (int u = 0; u < kRowBatch; ++u) {
             const int i = r0 + 8 * u + l8;
-            double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+            double acc[kMT][2] = {};
 #pragma unroll
             for (int kq = 0; kq < 8; ++kq)
 #pragma unroll
-              for (int ni = 0; ni < 2; ++ni) dmma(acc[ni][0], acc[ni][1], af[u][kq], bz[kq][ni]);
+              for (int ni = 0; ni < kMT; ++ni) dmma(acc[ni][0], acc[ni][1], af[u][kq], bz[kq][ni]);
             if (i < re) {
 #pragma unroll
-              for (int ni = 0; ni < 2; ++ni)
+              for (int ni = 0; ni < kMT; ++ni)
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
                   if (!okc[ni][h]) continue;
@@ -1099,7 +1109,7 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
         }
         // lanes sharing l4 hold the same columns: reduce over l8
 #pragma unroll
-        for (int ni = 0; ni < 2; ++ni)
+        for (int ni = 0; ni < kMT; ++ni)
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
             double t = tail[ni][h];
@@ -1112,13 +1122,13 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
         CM(3);
         if (l8 == 0) {
 #pragma unroll
-          for (int ni = 0; ni < 2; ++ni)
+          for (int ni = 0; ni < kMT; ++ni)
 #pragma unroll
             for (int h = 0; h < 2; ++h) RED2[warp][ni * 8 + 2 * l4 + h] = tail[ni][h];
         }
       }
       __syncthreads();
-      if (tid < 16) {
+      if (tid < kSweep) {
         double s = 0.0;
 #pragma unroll
         for (int w2 = 0; w2 < kWarps; ++w2) s += RED2[w2][tid];
@@ -1165,7 +1175,7 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
     double* Tbuf = V + (int64_t)mcap * mcap + 32 * (ncap + mcap);
     double (*TT)[33] = reinterpret_cast<double (*)[33]>(vsh + kCT);
     double (*ZT)[33] = reinterpret_cast<double (*)[33]>(vsh + kCZ);
-    double (*RED)[16][32] = reinterpret_cast<double (*)[16][32]>(vsh + kCScr);
+    double (*RED)[kSweep][32] = reinterpret_cast<double (*)[kSweep][32]>(vsh + kCScr);
     const int nblk = (kst + 31) / 32;
     const int l4 = lane & 3, l8 = lane >> 2;
     // (1) T of my blocks
@@ -1254,11 +1264,11 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
     }
     group_barrier(ctr, G, gen, tgt, 300000, events + 12 * slot + 9);   // every T_b published
     const int nown = (m - rank + G - 1) / G;
-    for (int u0 = 0; u0 < nown; u0 += 16) {
-      const int ncl = min(16, nown - u0);
+    for (int u0 = 0; u0 < nown; u0 += kSweep) {
+      const int ncl = min(kSweep, nown - u0);
       const int cmax = rank + G * (u0 + ncl - 1);
       __syncthreads();
-      if (tid < 16) sh.fcol[tid] = tid < ncl ? rank + G * (u0 + tid) : -1;
+      if (tid < kSweep) sh.fcol[tid] = tid < ncl ? rank + G * (u0 + tid) : -1;
       __syncthreads();
       for (int b = min(nblk - 1, cmax / 32); b >= 0; --b) {
         const int ka = 32 * b, nb = min(32, kst - ka);
@@ -1268,28 +1278,28 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
         const int rb = ka + warp * chunk, re = min(m, rb + chunk);
         // Y^T = X^T V_b
         {
-          double acc[2][4][2];
+          double acc[kMT][4][2];
 #pragma unroll
-          for (int a = 0; a < 2; ++a)
+          for (int a = 0; a < kMT; ++a)
 #pragma unroll
             for (int c = 0; c < 4; ++c) acc[a][c][0] = acc[a][c][1] = 0.0;
-          const double* xa[2];
-          bool oka[2];
+          const double* xa[kMT];
+          bool oka[kMT];
 #pragma unroll
-          for (int mi = 0; mi < 2; ++mi) {
+          for (int mi = 0; mi < kMT; ++mi) {
             const int c = sh.fcol[mi * 8 + l8];
             oka[mi] = c >= 0;
             xa[mi] = Q + (int64_t)(c >= 0 ? c : 0) * m;
           }
           #pragma unroll kRowUnroll
           for (int r = rb; r < re; r += 8 * kRowBatch) {
-            double af[2 * kRowBatch][2], bf[2 * kRowBatch][4];
+            double af[2 * kRowBatch][kMT], bf[2 * kRowBatch][4];
 #pragma unroll
             for (int s = 0; s < 2 * kRowBatch; ++s) {
               const int i = r + 4 * s + l4;
               const bool okr = i < re;
 #pragma unroll
-              for (int mi = 0; mi < 2; ++mi) af[s][mi] = (okr && oka[mi]) ? __ldcg(xa[mi] + i) : 0.0;
+              for (int mi = 0; mi < kMT; ++mi) af[s][mi] = (okr && oka[mi]) ? __ldcg(xa[mi] + i) : 0.0;
 #pragma unroll
               for (int ni = 0; ni < 4; ++ni) {
                 const int q = ni * 8 + l8;
@@ -1300,13 +1310,13 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
 #pragma unroll
             for (int s = 0; s < 2 * kRowBatch; ++s)
 #pragma unroll
-              for (int mi = 0; mi < 2; ++mi)
+              for (int mi = 0; mi < kMT; ++mi)
 #pragma unroll
                 for (int ni = 0; ni < 4; ++ni)
                   dmma(acc[mi][ni][0], acc[mi][ni][1], af[s][mi], bf[s][ni]);
           }
 #pragma unroll
-          for (int mi = 0; mi < 2; ++mi)
+          for (int mi = 0; mi < kMT; ++mi)
 #pragma unroll
             for (int ni = 0; ni < 4; ++ni)
 #pragma unroll
@@ -1314,9 +1324,9 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
         }
         __syncthreads();
         // Z^T[c][q] = sum_{p >= q} Y^T[c][p] T[q][p]  (Z = T Y)
-        double zv[2];
+        double zv[kMT];
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
+        for (int u = 0; u < kMT; ++u) {
           const int e = tid + kT * u;
           const int c = e >> 5, q = e & 31;
           double z = 0.0;
@@ -1331,22 +1341,22 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
         }
         __syncthreads();
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
+        for (int u = 0; u < kMT; ++u) {
           const int e = tid + kT * u;
           ZT[e >> 5][e & 31] = zv[u];
         }
         __syncthreads();
         // X -= V_b Z
         {
-          double bz[8][2];
+          double bz[8][kMT];
 #pragma unroll
           for (int kq = 0; kq < 8; ++kq)
 #pragma unroll
-            for (int ni = 0; ni < 2; ++ni) bz[kq][ni] = ZT[ni * 8 + l8][kq * 4 + l4];
-          double* xc[2][2];
-          bool okc[2][2];
+            for (int ni = 0; ni < kMT; ++ni) bz[kq][ni] = ZT[ni * 8 + l8][kq * 4 + l4];
+          double* xc[kMT][2];
+          bool okc[kMT][2];
 #pragma unroll
-          for (int ni = 0; ni < 2; ++ni)
+          for (int ni = 0; ni < kMT; ++ni)
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
               const int c = sh.fcol[ni * 8 + 2 * l4 + h];
@@ -1356,7 +1366,7 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
           const int nkq = (nb + 3) >> 2;
           #pragma unroll kRowUnroll
           for (int r0 = rb; r0 < re; r0 += 8 * kRowBatch) {
-            double af[kRowBatch][8], xo[kRowBatch][2][2];
+            double af[kRowBatch][8], xo[kRowBatch][kMT][2];
 #pragma unroll
             for (int u = 0; u < kRowBatch; ++u) {
               const int i = r0 + 8 * u + l8;
@@ -1368,7 +1378,7 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
                                 : 0.0;
               }
 #pragma unroll
-              for (int ni = 0; ni < 2; ++ni)
+              for (int ni = 0; ni < kMT; ++ni)
 #pragma unroll
                 for (int h = 0; h < 2; ++h)
                   xo[u][ni][h] = (i < re && okc[ni][h]) ? xc[ni][h][i] : 0.0;
@@ -1376,14 +1386,14 @@ rrqr_wave_kernel(int npanel, const int64_t* __restrict__ panels, const int64_t* 
 #pragma unroll
             for (int u = 0; u < kRowBatch; ++u) {
               const int i = r0 + 8 * u + l8;
-              double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+              double acc[kMT][2] = {};
 #pragma unroll
               for (int kq = 0; kq < 8; ++kq)
 #pragma unroll
-                for (int ni = 0; ni < 2; ++ni) dmma(acc[ni][0], acc[ni][1], af[u][kq], bz[kq][ni]);
+                for (int ni = 0; ni < kMT; ++ni) dmma(acc[ni][0], acc[ni][1], af[u][kq], bz[kq][ni]);
               if (i < re) {
 #pragma unroll
-                for (int ni = 0; ni < 2; ++ni)
+                for (int ni = 0; ni < kMT; ++ni)
 #pragma unroll
                   for (int h = 0; h < 2; ++h)
                     if (okc[ni][h]) xc[ni][h][i] = xo[u][ni][h] - acc[ni][h];
