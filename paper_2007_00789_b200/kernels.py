@@ -142,11 +142,17 @@ def _tile_grid(mm, nn, lower_only=False, shape=0):
 
 
 def gemm_grouped(geo, targets, alpha, beta, bT, lower_only=False,
-                 max_rows=None, max_cols=None, tri=0, shape=0):
+                 max_rows=None, max_cols=None, tri=0, shape=0, mask_rows=None):
     """targets: [(C operand, [(A operand, B operand), ...], (max_m, max_n))].
 
     Tiles are laid out for the maximal (m0-geometry) sizes; tiles beyond a
-    target's live size exit immediately on the device."""
+    target's live size exit immediately on the device.
+
+    ``mask_rows`` (one segment per target): the row counts of the masked
+    operand -- B for bT = 0 (its zero 16-row K chunks are skipped), A for
+    bT = 1 (tiles over zero rows of A write zeros at once).  The masks are
+    written by ``spand_gemm_kmask`` and the product runs through
+    ``spand_gemm_grouped_masked`` (bit-identical to the unmasked call)."""
     if not targets:
         return
     trow, srow = [], []
@@ -164,6 +170,19 @@ def gemm_grouped(geo, targets, alpha, beta, bT, lower_only=False,
     if not srow:
         srow.append([0] * 14)
     td, sd, tl = _rows(trow, 8), _rows(srow, 14), _rows(tiles, 1)
+    if mask_rows is not None:
+        t = require_cuda()
+        chunks = (np.asarray(mask_rows, dtype=np.int64) + 15) // 16
+        kmoff = np.concatenate([[0], np.cumsum(chunks)[:-1]]).astype(np.int64)
+        kd = _rows(kmoff, 1)
+        mask = t.full((int(chunks.sum()) + 1,), 255, dtype=t.uint8, device=dev())
+        _lib.call("spand_gemm_kmask", len(targets), ptr(td), ptr(sd), ptr(geo.m0),
+                  ptr(geo.off), ptr(mask), ptr(kd), 0 if bT else 1, stream())
+        _lib.call("spand_gemm_grouped_masked", int(tiles.shape[0]), ptr(tl), ptr(td), ptr(sd),
+                  ptr(geo.m0), ptr(geo.off), float(alpha), float(beta), int(bT),
+                  int(bool(lower_only)), int(tri) | (int(shape) << 4), None, 0,
+                  ptr(mask), ptr(kd), stream())
+        return mask
     _lib.call("spand_gemm_grouped", int(tiles.shape[0]), ptr(tl), ptr(td), ptr(sd),
               ptr(geo.m0), ptr(geo.off), float(alpha), float(beta), int(bT),
               int(bool(lower_only)), int(tri) | (int(shape) << 4), None, 0, stream())
