@@ -14,7 +14,7 @@ def test_spmv_matches_csr():
     assert np.linalg.norm(y - ref) <= 1e-14 * np.linalg.norm(ref)
 
 
-@pytest.mark.parametrize("n", [1, 5, 31, 32, 33, 100, 257])
+@pytest.mark.parametrize("n", [1, 5, 31, 32, 33, 63, 64, 65, 100, 257])
 def test_cholesky_reconstruction(n):
     from paper_2007_00789_b200 import cholesky
     rng = np.random.default_rng(n)
@@ -37,6 +37,13 @@ def test_cholesky_hand_and_pivot():
     with pytest.raises(NotSPD) as exc:
         cholesky(np.array([[-1.0]]))
     assert exc.value.pivot == 0
+    # a failing pivot inside a block of <= 64 (the shared-memory path)
+    g = np.random.default_rng(5).standard_normal((40, 40))
+    m = g @ g.T + 40 * np.eye(40)
+    m[23, 23] = -1e6
+    with pytest.raises(NotSPD) as exc:
+        cholesky(m)
+    assert exc.value.pivot == 23
     rng = np.random.default_rng(3)
     g = rng.standard_normal((70, 70))
     m = g @ g.T + 70 * np.eye(70)
@@ -49,7 +56,7 @@ def test_cholesky_hand_and_pivot():
     assert exc.value.pivot == ref.value.pivot
 
 
-@pytest.mark.parametrize("n", [1, 8, 40, 130])
+@pytest.mark.parametrize("n", [1, 8, 40, 63, 64, 130])
 def test_tri_inverse(n):
     from paper_2007_00789_b200 import tri_inverse
     rng = np.random.default_rng(2)
