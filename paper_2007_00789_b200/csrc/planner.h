@@ -873,6 +873,11 @@ struct Plan {
             st.target(m0[wa], m0[wb], dry, pool_base + 8 * boff[b], (int64_t)wa, (int64_t)wb,
                       (int64_t)0, (int64_t)0, (int64_t)-1, (int64_t)-1);
             for (int q = L.tseg_ptr[t]; q < L.tseg_ptr[t + 1]; ++q) {
+              // (the two table reads are random over ~10^5 blocks: prefetch ahead)
+              if ((size_t)q + 16 < L.tseg_blk.size()) {
+                __builtin_prefetch(&blkflag[L.tseg_blk[q + 16] >> 32]);
+                __builtin_prefetch(&blkflag[L.tseg_blk[q + 16] & 0xffffffffLL]);
+              }
               st.seg(L.tseg_blk[q]);
               sflag.push_back((blkflag[L.tseg_blk[q] >> 32] << 32) |
                               blkflag[L.tseg_blk[q] & 0xffffffffLL]);
