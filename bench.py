@@ -341,8 +341,21 @@ def main():
     def max_over_ranks(v):
         return reduce_max(v, dist, "cuda")
 
+    # warm-up in the timed loop's steady state: the previous step's factor is
+    # still alive while the next one is built (two block pools in the caching
+    # allocator; without this the second timed step paid the cudaMalloc of the
+    # second pool, +150 .. 600 ms)
+    f = rep = None
     for _ in range(args.warmup):
-        step_resident()
+        f, rep = step_resident()
+    # long-lived objects (hierarchy, symbolic tables, the warm-up factor's
+    # operator list) leave the cyclic collector's scan set: ~25 ms per step of
+    # interpreter housekeeping, no numerical work (SPAND_BENCH_GC=default keeps
+    # the interpreter's default)
+    if os.environ.get("SPAND_BENCH_GC", "freeze") == "freeze":
+        import gc
+        gc.collect()
+        gc.freeze()
     # ---- timed region: K steps, inputs resident
     barrier()
     st = torch.cuda.current_stream()
@@ -523,7 +536,10 @@ def main():
                                f"ND levels {levels}, eps {args.eps}, {args.scheme}, skip 4, "
                                f"PCG tol {args.tol}, b~N(0,1) seed 3",
                    "parallelism": "replicas" if world > 1 else "single",
-                   "l2": "flushed between steps (256 MiB write); factor > L2"},
+                   "l2": "flushed between steps (256 MiB write); factor > L2",
+                   "host": "gc.freeze() after warm-up; warm-up keeps the previous factor alive "
+                           "like the timed loop"},
+        "step_ms": [round(float(v), 1) for v in step_ms],
         "factorize_s": t_f, "solve_s": rep.solve_seconds, "n_cg": rep.n_cg,
         "true_residual": rep.true_residual, "hierarchy_s": t_hier,
         "nnz_factor": f.nnz_factor, "mu": f.nnz_factor / a.nnz,
