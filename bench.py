@@ -599,8 +599,9 @@ def main():
             fnk_ = sp.factorize(a, h, args.eps, args.scheme, near_kernel=ones)
             _, rnk_ = sp.pcg(a, bd, m=fnk_.apply_m, tol=args.tol)
             return fnk_, rnk_
+        fnk = rnk = None
         for _ in range(max(1, args.warmup)):
-            step_nk()
+            fnk, rnk = step_nk()   # previous factor alive, as in the timed loop
         nk_ms = []
         for _ in range(args.steps):
             flush.zero_()
